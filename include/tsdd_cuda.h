@@ -1,0 +1,185 @@
+/* tsdd_cuda.h — C ABI of the B200 discord-search engine (libtsdd_cuda.so).
+ *
+ * This is the drop-in boundary for the ONE hot path of the reference
+ * (/root/reference/proj): preparation + PhiDD/HOTSAX search, entered in the
+ * reference through
+ *     tsdd::run_discovery   include/tsdd/pipeline.hpp:37   (src/pipeline.cpp:53-93)
+ *     tsdd::phidd_discord   include/tsdd/discovery.hpp:86  (src/discovery.cpp:360-373)
+ * The reference has no FFI of its own; the C++ shim in include/tsdd/ (same
+ * type and function names as the reference headers) binds these entry points
+ * and re-throws the reference's exception types from the return codes.
+ *
+ * Plain pointers and sizes only; no exceptions cross this boundary; every
+ * function returns one of the TSDD_* codes below and leaves a message for
+ * tsdd_cuda_last_error().  All compute runs in hand-written sm_100a kernels;
+ * there is no CPU fallback: without a CUDA device tsdd_cuda_create fails with
+ * TSDD_ERR_RUNTIME.
+ *
+ * Threading: one call at a time per context; distinct contexts
+ * may be used concurrently.  Positions are 1-based (discovery.hpp:21).
+ */
+#ifndef TSDD_CUDA_H
+#define TSDD_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes.  2/3 are the reference CLI's exit codes (tools/tsdd.cpp:212-223). */
+#define TSDD_OK 0
+#define TSDD_ERR_PARAMETER 2  /* -> tsdd::ParameterError        (errors.hpp:10-13) */
+#define TSDD_ERR_VALIDATION 3 /* -> tsdd::ValidationError       (errors.hpp:16-19) */
+#define TSDD_ERR_INFEASIBLE 4 /* -> tsdd::InfeasibleInputError  (errors.hpp:22-25) */
+#define TSDD_ERR_RUNTIME 5    /* CUDA / NCCL failure -> std::runtime_error */
+
+typedef struct tsdd_cuda_ctx tsdd_cuda_ctx;
+
+/* Counters and timings of the last prepare + search on a context.
+ * calls / abandoned keep the reference's meaning (series.hpp:68-74):
+ * distance evaluations started / cut short.  terms = (x-y)^2 terms actually
+ * accumulated by the scan kernels (the FP32 roofline numerator).            */
+typedef struct tsdd_cuda_stats {
+  uint64_t rows;           /* N = m - n + 1 */
+  uint64_t calls;          /* pair distances started (tile pairs with |i-j| >= n) */
+  uint64_t abandoned;      /* of which stopped before the last column */
+  uint64_t terms;          /* accumulated (x-y)^2 terms, all scan kernels */
+  uint64_t buckets;        /* distinct SAX words present */
+  uint64_t min_freq_candidates; /* size of the reference's candidate set (index.cpp:66-79) */
+  uint64_t batches;        /* outer-loop batches run */
+  uint64_t scanned_candidates; /* candidates that entered a full scan */
+  uint64_t kernel_launches;    /* kernels launched by prepare + search */
+  double prep_ms;          /* device time of the preparation stage (CUDA events) */
+  double search_ms;        /* device time of the search stage (CUDA events) */
+  double scan_kernel_ms;   /* device time inside the tiled distance kernel only */
+  double h2d_ms;           /* series upload, when prepare was given a host pointer */
+  uint64_t scan_kernel_launches;
+  uint64_t scan_kernel_terms; /* terms accumulated by the tiled distance kernel only */
+} tsdd_cuda_stats;
+
+/* ---- lifetime ------------------------------------------------------------ */
+
+/* Binds a context to one CUDA device (one context per GPU / per rank). */
+int tsdd_cuda_create(tsdd_cuda_ctx** out, int device);
+void tsdd_cuda_destroy(tsdd_cuda_ctx* ctx);
+
+/* Message of the last failure on this context (ctx == NULL: last failure of
+ * tsdd_cuda_create on this thread).  Never NULL.                            */
+const char* tsdd_cuda_last_error(const tsdd_cuda_ctx* ctx);
+
+/* Tunables, by name: "batch" (candidates per outer-loop batch), "first_batch"
+ * (size of the first batch; it doubles up to "batch"), "rounds" (neighbour
+ * ranges per batch, compaction between them), "bucket_mates" (same-word
+ * neighbours tried per row before the scans), "rescore" (0/1: float64
+ * re-scoring of each discord's distance), "symmetric" (0/1: completed tiles
+ * also lower the neighbours' bounds), "packed" (0/1: f32x2 arithmetic),
+ * "time_kernels" (0/1: CUDA events around every tile-kernel launch).
+ * Unknown name -> TSDD_ERR_PARAMETER.  None of them changes the result.     */
+int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value);
+
+/* ---- preparation stage (replaces pipeline.cpp:60-69) --------------------- */
+
+/* check_config alone (pipeline.cpp:21-49): the validation that prepare runs
+ * first, usable without a device.  Writes the message the matching reference
+ * exception would carry into `message` (may be NULL).                       */
+int tsdd_cuda_check_config_f32(const float* series, size_t m, size_t n, size_t word_len,
+                               size_t alphabet, char* message, size_t message_bytes);
+int tsdd_cuda_check_config_f64(const double* series, size_t m, size_t n, size_t word_len,
+                               size_t alphabet, char* message, size_t message_bytes);
+
+/* Validates exactly as check_config does (pipeline.cpp:21-49: finite values,
+ * 1 <= n <= m, 1 <= word_len <= n, alphabet in 2..10, N >= n+1), except that
+ * the dictionary guard is 2^32 words instead of 2^24 (sax.hpp:80): the device
+ * index is sort-based and never allocates |A|^w entries.  Then, on the device:
+ * per-window mean / sigma in float64, the z-normalised subsequence matrix in
+ * float32 (series.cpp:46-74), PAA -> SAX -> word hash (sax.cpp:63-132), and
+ * the bucket / frequency / rarity index (index.cpp:12-109) by radix sort and
+ * run-length histogram.  `series` is a HOST pointer.                        */
+int tsdd_cuda_prepare_f32(tsdd_cuda_ctx* ctx, const float* series, size_t m, size_t n,
+                          size_t word_len, size_t alphabet);
+int tsdd_cuda_prepare_f64(tsdd_cuda_ctx* ctx, const double* series, size_t m, size_t n,
+                          size_t word_len, size_t alphabet);
+/* Same, with the float32 series already resident in device memory on the
+ * context's device (no host<->device copy inside).                          */
+int tsdd_cuda_prepare_device_f32(tsdd_cuda_ctx* ctx, const float* d_series, size_t m, size_t n,
+                                 size_t word_len, size_t alphabet);
+
+/* ---- search stage (replaces phidd_discord, discovery.cpp:360-373) -------- */
+
+#define TSDD_SEARCH_DISABLE_PRUNING 1u /* DiscoveryOptions::disable_pruning (discovery.hpp:31) */
+
+/* Top-k discords of the prepared series.  k = 1 is the reference's search.
+ * For k > 1, discord r is the arg-max of the nearest-neighbour distance over
+ * positions at least n away from every earlier discord.
+ * positions[k] are 1-based; distances[k] are Euclidean (sqrt taken once,
+ * discovery.cpp:88-98).  Ties on the distance go to the smaller position
+ * (discovery.cpp:158-165).  Nothing beat 0 -> position 1, distance 0.
+ * With several ranks (tsdd_cuda_comm_init / tsdd_cuda_set_exchange) every
+ * rank must call this with the same arguments; all ranks return the same
+ * answer.                                                                   */
+int tsdd_cuda_search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions,
+                     double* distances);
+
+int tsdd_cuda_get_stats(const tsdd_cuda_ctx* ctx, tsdd_cuda_stats* out);
+
+/* ---- parity access to the prepared arrays (tests only) ------------------- */
+
+#define TSDD_FETCH_ROWS 1       /* float  [N * stride]  z-normalised matrix (series.hpp:53)   */
+#define TSDD_FETCH_MEAN 2       /* double [N]           window means                          */
+#define TSDD_FETCH_INV_SIGMA 3  /* double [N]           1/sigma, 0 for flat windows           */
+#define TSDD_FETCH_PAA 4        /* double [N * w]       segment means (sax.hpp:37)            */
+#define TSDD_FETCH_SAX 5        /* uint32 [N * w]       symbols 1..|A| (sax.hpp:47)           */
+#define TSDD_FETCH_HASH 6       /* uint64 [N]           1-based word hash (index.hpp:61)      */
+#define TSDD_FETCH_FREQ 7       /* uint32 [N]           bucket size of each row (index.hpp:15) */
+#define TSDD_FETCH_BUCKETS 8    /* uint64 [N]           1-based positions, bucket after bucket in
+                                                         ascending hash order (index.hpp:29)   */
+#define TSDD_FETCH_ORDER 9      /* uint64 [N]           1-based positions in rarity order      */
+#define TSDD_FETCH_CANDIDATES 10 /* uint64 [min_freq_candidates] (index.hpp:20-22)            */
+#define TSDD_FETCH_NN_SQ 11     /* float  [N]           current nn upper bounds (squared)      */
+#define TSDD_FETCH_NN_EXACT 12  /* uint8  [N]           1 where NN_SQ is the exact nn          */
+
+/* Row stride of TSDD_FETCH_ROWS in floats (n rounded up to 32; padding is 0). */
+size_t tsdd_cuda_row_stride(const tsdd_cuda_ctx* ctx);
+
+/* Copies one prepared array to host memory.  bytes must be the exact size. */
+int tsdd_cuda_fetch(tsdd_cuda_ctx* ctx, int what, void* dst, size_t bytes);
+
+/* ---- several GPUs: candidates sharded, best-so-far max-reduced ----------- */
+
+/* Entry e of the rarity order belongs to rank (e mod world).  After every
+ * batch the packed best-so-far (float bits of d^2 << 32 | ~position) is
+ * max-reduced over all ranks.                                               */
+
+/* NCCL path: one 8-byte ncclAllReduce(ncclMax, ncclUint64) per batch on the
+ * search stream.  libnccl.so.2 is loaded at run time.  Rank 0 creates the id
+ * and hands the 128 bytes to the other ranks (any transport).               */
+int tsdd_cuda_comm_unique_id(char id[128]);
+int tsdd_cuda_comm_init(tsdd_cuda_ctx* ctx, const char id[128], int world, int rank);
+
+/* Host-hook path (tests, or a caller that already owns a communicator): the
+ * engine hands `count` packed keys on the host; the hook must return, in
+ * place, the element-wise maximum over all ranks.  Non-zero = failure.      */
+typedef int (*tsdd_exchange_fn)(void* user, uint64_t* keys, size_t count);
+int tsdd_cuda_set_exchange(tsdd_cuda_ctx* ctx, tsdd_exchange_fn fn, void* user, int world,
+                           int rank);
+
+/* ---- measurement helpers -------------------------------------------------- */
+
+/* FP32 issue-rate probes on the context's device (roofline denominators the
+ * driver's MEASURED_PEAKS.json does not have).  which: 0 = dependent-free
+ * FFMA stream, 1 = FSUB+FFMA pairs (the distance kernel's mix), 2 = packed
+ * fma.rn.f32x2, 3 = packed sub+fma f32x2.  Returns lane-operations per second
+ * in *ops_per_s (one FFMA = one op; an f32x2 instruction = two).            */
+int tsdd_cuda_fp32_probe(tsdd_cuda_ctx* ctx, int which, double* ops_per_s, double* ms);
+
+/* Exhaustive nn profile with the same tiled kernel and no pruning (the
+ * Engine::brute analogue, discovery.cpp:123-173): nn_sq[N], +inf where a row
+ * has no non-self match.  Needs a prepared context.                         */
+int tsdd_cuda_nn_profile(tsdd_cuda_ctx* ctx, float* nn_sq_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSDD_CUDA_H */

@@ -1,0 +1,88 @@
+"""In-tree build of the native libraries (explicit nvcc / g++ commands, no JIT cache).
+
+  _lib/libtsdd_cuda.so   the sm_100a kernels + host driver + C ABI (include/tsdd_cuda.h)
+  _lib/libtsdd_gen.so    the seeded workload generators (host-only C++)
+
+The built files are git-ignored but travel to the GPU box with the snapshot.
+``python -m paper_1901_00155_b200.build`` rebuilds what is out of date.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "_lib")
+OBJ = os.path.join(HERE, "_lib", "obj")
+INCLUDE = os.path.join(ROOT, "include")
+
+CUDA_SOURCES = ["prep_kernels.cu", "search_kernels.cu", "probe_kernels.cu", "engine.cu"]
+CUDA_HEADERS = ["common.cuh", "kernels.hpp", os.path.join(INCLUDE, "tsdd_cuda.h")]
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC,
+]
+HOST_CXX = "/usr/bin/g++"
+
+
+def _nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _stale(target: str, deps: list[str]) -> bool:
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _run(cmd: list[str]) -> None:
+    proc = subprocess.run(cmd, capture_output=True, text=True)
+    if proc.returncode != 0:
+        raise RuntimeError("build failed:\n  " + " ".join(cmd) + "\n" + proc.stdout + proc.stderr)
+
+
+def build_cuda(force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    target = os.path.join(LIB, "libtsdd_cuda.so")
+    headers = [h if os.path.isabs(h) else os.path.join(CSRC, h) for h in CUDA_HEADERS]
+    objects = []
+    for src in CUDA_SOURCES:
+        path = os.path.join(CSRC, src)
+        obj = os.path.join(OBJ, src.replace(".cu", ".o"))
+        objects.append(obj)
+        if force or _stale(obj, [path] + headers):
+            if verbose:
+                print("nvcc", src, flush=True)
+            _run([_nvcc(), *NVCC_FLAGS, "-c", path, "-o", obj])
+    if force or _stale(target, objects):
+        _run([_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC",
+              "-o", target, *objects, "-ldl", "-lpthread"])
+    return target
+
+
+def build_gen(force: bool = False) -> str:
+    os.makedirs(LIB, exist_ok=True)
+    target = os.path.join(LIB, "libtsdd_gen.so")
+    src = os.path.join(CSRC, "series_gen.cpp")
+    if force or _stale(target, [src]):
+        cxx = HOST_CXX if os.path.exists(HOST_CXX) else "g++"
+        _run([cxx, "-std=c++17", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-o", target, src])
+    return target
+
+
+def build_all(force: bool = False, verbose: bool = False) -> dict:
+    return {"gen": build_gen(force), "cuda": build_cuda(force, verbose)}
+
+
+if __name__ == "__main__":
+    out = build_all(force="--force" in sys.argv, verbose=True)
+    for k, v in out.items():
+        print(k, v)

@@ -1,0 +1,52 @@
+// Shared device helpers of the B200 discord-search engine.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tsdd_b200 {
+
+constexpr uint32_t kInfBits = 0x7F800000u;  // +inf as float bits
+// nn slot of a row nobody has measured yet: (+inf, no neighbour)
+constexpr uint64_t kNnUnset = (static_cast<uint64_t>(kInfBits) << 32) | 0xFFFFFFFFull;
+
+// Squared distances are >= 0, so their float bits order like the floats.
+//
+// nn key  : (bits(d^2) << 32) | neighbour row   -> integer MIN = (smaller distance, then smaller row)
+// best key: (bits(d^2) << 32) | ~candidate row  -> integer MAX = (greater distance, then smaller row)
+//           the rule of the reference's deterministic merges (discovery.cpp:158-165, 328-340).
+__host__ __device__ __forceinline__ uint64_t nn_key(uint32_t d2_bits, uint32_t row) {
+  return (static_cast<uint64_t>(d2_bits) << 32) | row;
+}
+__host__ __device__ __forceinline__ uint64_t best_key(uint32_t d2_bits, uint32_t row) {
+  return (static_cast<uint64_t>(d2_bits) << 32) | (0xFFFFFFFFu - row);
+}
+__host__ __device__ __forceinline__ uint32_t key_bits(uint64_t key) {
+  return static_cast<uint32_t>(key >> 32);
+}
+__host__ __device__ __forceinline__ uint32_t best_key_row(uint64_t key) {
+  return 0xFFFFFFFFu - static_cast<uint32_t>(key & 0xFFFFFFFFull);
+}
+
+// A row whose nn upper bound cannot beat the best-so-far any more is dead:
+// the HOTSAX discard `d < bsf` (discovery.cpp:58), extended by the tie rule
+// (equal distance, larger position can never win).
+__device__ __forceinline__ bool is_dead(uint64_t nn, uint32_t row, uint64_t best) {
+  return best_key(key_bits(nn), row) < best;
+}
+
+__device__ __forceinline__ unsigned long long* as_ull(uint64_t* p) {
+  return reinterpret_cast<unsigned long long*>(p);
+}
+
+// Search-stage counters, one instance in device memory per context.
+struct DeviceCounters {
+  unsigned long long calls;      // pair distances started for live candidates
+  unsigned long long abandoned;  // of those, cut short by an abandoned tile
+  unsigned long long terms;      // (x-y)^2 terms accumulated by any scan kernel
+  unsigned long long tile_terms; // ... by the tiled kernel only
+  unsigned long long scanned;    // candidates that entered a full scan
+};
+
+}  // namespace tsdd_b200

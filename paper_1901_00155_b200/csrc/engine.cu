@@ -1,0 +1,936 @@
+// Host driver and C ABI of the B200 discord-search engine (include/tsdd_cuda.h).
+//
+// Replaces, for the CUDA engine, the body of tsdd::run_discovery
+// (/root/reference/proj/src/pipeline.cpp:53-93): check_config, the preparation
+// stage (pipeline.cpp:60-69) and phidd_discord (discovery.cpp:360-373).  All
+// arithmetic of the path runs in the kernels of prep_kernels.cu and
+// search_kernels.cu; this file owns device memory, launch order, the batched
+// HOTSAX outer loop, the top-k passes and the best-so-far exchange between
+// ranks.  There is no CPU fallback.
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.hpp"
+#include "tsdd_cuda.h"
+
+namespace tsdd_b200 {
+void set_packed_math(bool on);
+}
+
+namespace {
+
+using namespace tsdd_b200;
+
+struct Failure {
+  int code;
+  std::string message;
+};
+
+[[noreturn]] void fail(int code, const std::string& message) { throw Failure{code, message}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(TSDD_ERR_RUNTIME, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CUDA_OK(expr) cuda_check((expr), #expr)
+
+thread_local std::string g_create_error;
+
+template <typename T>
+struct DeviceArray {
+  T* ptr = nullptr;
+  size_t count = 0;
+  void alloc(size_t n) {
+    release();
+    if (n == 0) n = 1;
+    CUDA_OK(cudaMalloc(reinterpret_cast<void**>(&ptr), n * sizeof(T)));
+    count = n;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    count = 0;
+  }
+  ~DeviceArray() { release(); }
+  DeviceArray() = default;
+  DeviceArray(const DeviceArray&) = delete;
+  DeviceArray& operator=(const DeviceArray&) = delete;
+};
+
+inline uint32_t round_up_u32(uint32_t v, uint32_t to) { return (v + to - 1) / to * to; }
+
+inline float float_from_bits(uint32_t bits) {
+  float f;
+  std::memcpy(&f, &bits, sizeof(f));
+  return f;
+}
+
+int bits_for(uint64_t max_value) {
+  int bits = 1;
+  while (bits < 64 && (max_value >> bits) != 0) ++bits;
+  return bits;
+}
+
+// ---- NCCL, loaded at run time (the torch-bundled libnccl.so.2 when the
+// caller is a Python process that imported torch, else the system one) -------
+struct NcclApi {
+  typedef struct { char internal[128]; } UniqueId;
+  typedef void* Comm;
+  int (*GetUniqueId)(UniqueId*) = nullptr;
+  int (*CommInitRank)(Comm*, int, UniqueId, int) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
+  int (*CommDestroy)(Comm) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  void* handle = nullptr;
+  static constexpr int kUint64 = 5;  // ncclUint64
+  static constexpr int kMax = 2;     // ncclMax
+
+  void load() {
+    if (handle) return;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* name : names) {
+      handle = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (handle) break;
+    }
+    if (!handle) fail(TSDD_ERR_RUNTIME, std::string("cannot load libnccl.so.2: ") + dlerror());
+    GetUniqueId = reinterpret_cast<decltype(GetUniqueId)>(dlsym(handle, "ncclGetUniqueId"));
+    CommInitRank = reinterpret_cast<decltype(CommInitRank)>(dlsym(handle, "ncclCommInitRank"));
+    AllReduce = reinterpret_cast<decltype(AllReduce)>(dlsym(handle, "ncclAllReduce"));
+    CommDestroy = reinterpret_cast<decltype(CommDestroy)>(dlsym(handle, "ncclCommDestroy"));
+    GetErrorString = reinterpret_cast<decltype(GetErrorString)>(dlsym(handle, "ncclGetErrorString"));
+    if (!GetUniqueId || !CommInitRank || !AllReduce || !CommDestroy || !GetErrorString)
+      fail(TSDD_ERR_RUNTIME, "libnccl.so.2 lacks an expected symbol");
+  }
+  void check(int rc, const char* what) const {
+    if (rc != 0) fail(TSDD_ERR_RUNTIME, std::string(what) + ": " + GetErrorString(rc));
+  }
+};
+NcclApi g_nccl;
+
+}  // namespace
+
+struct tsdd_cuda_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  std::string error;
+
+  // tunables (tsdd_cuda_set_option)
+  uint32_t opt_batch = 8192;
+  uint32_t opt_first_batch = 256;
+  int opt_rounds = 7;
+  int opt_mates = 8;
+  bool opt_rescore = true;
+  bool opt_symmetric = true;
+  bool opt_packed = true;
+  bool opt_time_kernels = true;
+
+  // prepared series
+  bool prepared = false;
+  size_t m = 0, n = 0, word_len = 0, alphabet = 0;
+  uint32_t rows = 0, stride = 0, rows_padded = 0;
+  DeviceArray<float> series_f32;
+  DeviceArray<double> series, mean, inv_sigma;
+  DeviceArray<float> matrix;
+  DeviceArray<uint32_t> hash0, freq, offsets, slot_bucket, scalars;
+  DeviceArray<uint32_t> sort_buf[4], order_buf[4];
+  uint32_t *sorted_hash = nullptr, *sorted_row = nullptr, *order = nullptr, *sorted_freq = nullptr;
+  DeviceArray<uint32_t> scan_scratch, radix_hist;
+
+  // search state
+  DeviceArray<uint64_t> nn, best, xchg;
+  DeviceArray<uint8_t> exact, excluded;
+  DeviceArray<DeviceCounters> counters;
+  DeviceArray<uint32_t> flags, batch_rows, batch_alt, sel;
+  DeviceArray<float> batch_matrix;
+  DeviceArray<double> rescore_out;
+  uint32_t batch_capacity = 0;
+  uint32_t* h_sel = nullptr;      // pinned, 4 words
+  uint64_t* h_keys = nullptr;     // pinned, 4 keys
+  double* h_double = nullptr;     // pinned, 1 value
+  std::vector<cudaEvent_t> event_pool;
+  size_t events_used = 0;
+
+  // ranks
+  int world = 1, rank = 0;
+  tsdd_exchange_fn exchange_fn = nullptr;
+  void* exchange_user = nullptr;
+  NcclApi::Comm comm = nullptr;
+
+  tsdd_cuda_stats stats{};
+
+  SearchState state() {
+    SearchState s;
+    s.rows = matrix.ptr;
+    s.n_rows = rows;
+    s.n = static_cast<uint32_t>(n);
+    s.stride = stride;
+    s.nn = nn.ptr;
+    s.exact = exact.ptr;
+    s.excluded = excluded.ptr;
+    s.best = best.ptr;
+    s.counters = counters.ptr;
+    return s;
+  }
+};
+
+namespace {
+
+void bind_device(tsdd_cuda_ctx* ctx) { CUDA_OK(cudaSetDevice(ctx->device)); }
+
+void sync_stream(tsdd_cuda_ctx* ctx) {
+  CUDA_OK(cudaStreamSynchronize(ctx->stream));
+  CUDA_OK(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ validation
+// check_config (pipeline.cpp:21-49) with the reference's order and messages:
+// series first (series.cpp:10-19), then n, word_len, alphabet, dictionary, and
+// feasibility last.  The dictionary guard is 2^32 here (sax.hpp:80 has 2^24).
+template <typename T>
+void check_series(const T* series, size_t m) {
+  if (m == 0 || series == nullptr) fail(TSDD_ERR_VALIDATION, "series is empty");
+  for (size_t i = 0; i < m; ++i) {
+    if (!std::isfinite(static_cast<double>(series[i])))
+      fail(TSDD_ERR_VALIDATION, "non-finite value at index " + std::to_string(i + 1));
+  }
+}
+
+void check_shape(size_t m, size_t n, size_t word_len, size_t alphabet) {
+  if (n < 1 || n > m)
+    fail(TSDD_ERR_PARAMETER, "n=" + std::to_string(n) + " must satisfy 1 <= n <= m=" + std::to_string(m));
+  if (word_len < 1 || word_len > n)
+    fail(TSDD_ERR_PARAMETER,
+         "word_len=" + std::to_string(word_len) + " must satisfy 1 <= word_len <= n=" + std::to_string(n));
+  if (alphabet < 2 || alphabet > 10)
+    fail(TSDD_ERR_PARAMETER, "alphabet cardinality " + std::to_string(alphabet) + " is outside 2..10");
+  // |A|^w <= 2^32, checked without overflow
+  long double dict = 1.0L;
+  for (size_t j = 0; j < word_len; ++j) {
+    dict *= static_cast<long double>(alphabet);
+    if (dict > 4294967296.0L)
+      fail(TSDD_ERR_PARAMETER, "dictionary of " + std::to_string(alphabet) + "^" + std::to_string(word_len) +
+                                   " words exceeds the 2^32 guard of the device index");
+  }
+  const size_t rows = m - n + 1;
+  if (rows < n + 1)
+    fail(TSDD_ERR_INFEASIBLE, "no subsequence has a non-self match: N=" + std::to_string(rows) +
+                                  " <= n=" + std::to_string(n) + " (need m >= 2n)");
+  if (m > 0xFFFFFF00ull) fail(TSDD_ERR_PARAMETER, "series longer than 2^32 - 256 samples is not supported");
+}
+
+uint64_t dict_size_of(size_t word_len, size_t alphabet) {
+  uint64_t d = 1;
+  for (size_t j = 0; j < word_len; ++j) d *= alphabet;  // <= 2^32 after check_shape
+  return d;
+}
+
+// ------------------------------------------------------------------ preparation
+void prepare_on_device(tsdd_cuda_ctx* ctx, size_t m, size_t n, size_t word_len, size_t alphabet) {
+  // ctx->series_f32 or ctx->series already holds the samples; `have_f64` says which
+  cudaStream_t st = ctx->stream;
+  const uint32_t rows = static_cast<uint32_t>(m - n + 1);
+  ctx->m = m;
+  ctx->n = n;
+  ctx->word_len = word_len;
+  ctx->alphabet = alphabet;
+  ctx->rows = rows;
+  ctx->stride = round_up_u32(static_cast<uint32_t>(n), kRowAlign);
+  ctx->rows_padded = round_up_u32(rows, kTileRows);
+  uint64_t launches = 0;
+
+  ctx->mean.alloc(rows);
+  ctx->inv_sigma.alloc(rows);
+  ctx->hash0.alloc(rows);
+  launches += launch_window_encode(ctx->series.ptr, rows, static_cast<uint32_t>(n),
+                                   static_cast<uint32_t>(word_len), static_cast<uint32_t>(alphabet),
+                                   ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->hash0.ptr, nullptr, nullptr, st);
+
+  const size_t matrix_floats = static_cast<size_t>(ctx->rows_padded) * ctx->stride;
+  ctx->matrix.alloc(matrix_floats);
+  if (ctx->rows_padded > rows)
+    CUDA_OK(cudaMemsetAsync(ctx->matrix.ptr + static_cast<size_t>(rows) * ctx->stride, 0,
+                            static_cast<size_t>(ctx->rows_padded - rows) * ctx->stride * sizeof(float), st));
+  launches += launch_build_rows(ctx->series.ptr, ctx->mean.ptr, ctx->inv_sigma.ptr, rows,
+                                static_cast<uint32_t>(n), ctx->stride, ctx->matrix.ptr, st);
+
+  // bucket index: stable sort of (hash, row) -> runs are the buckets
+  const size_t longest_scan = std::max<size_t>(rows, radix_sort_scratch_words(rows));
+  ctx->scan_scratch.alloc(scan_scratch_words(static_cast<uint32_t>(longest_scan)) + 1024);
+  ctx->radix_hist.alloc(radix_sort_scratch_words(rows));
+  for (auto& b : ctx->sort_buf) b.alloc(rows);
+  for (auto& b : ctx->order_buf) b.alloc(rows);
+  CUDA_OK(cudaMemcpyAsync(ctx->sort_buf[0].ptr, ctx->hash0.ptr, rows * sizeof(uint32_t),
+                          cudaMemcpyDeviceToDevice, st));
+  launches += launch_iota(ctx->sort_buf[1].ptr, rows, st);
+  uint32_t *k0 = ctx->sort_buf[0].ptr, *v0 = ctx->sort_buf[1].ptr, *k1 = ctx->sort_buf[2].ptr,
+           *v1 = ctx->sort_buf[3].ptr;
+  const int hash_bits = bits_for(dict_size_of(word_len, alphabet) - 1);
+  launches += launch_radix_sort_pairs(&k0, &v0, &k1, &v1, rows, hash_bits, ctx->radix_hist.ptr,
+                                      ctx->scan_scratch.ptr, st);
+  ctx->sorted_hash = k0;
+  ctx->sorted_row = v0;
+
+  ctx->slot_bucket.alloc(rows);
+  ctx->offsets.alloc(static_cast<size_t>(rows) + 1);
+  ctx->freq.alloc(rows);
+  ctx->scalars.alloc(4);
+  CUDA_OK(cudaMemsetAsync(ctx->scalars.ptr, 0, 4 * sizeof(uint32_t), st));
+  launches += launch_bucket_index(ctx->sorted_hash, ctx->sorted_row, rows, /*heads=*/k1, ctx->slot_bucket.ptr,
+                                  ctx->offsets.ptr, ctx->freq.ptr, ctx->scalars.ptr, ctx->scan_scratch.ptr, st);
+
+  // rarity order: stable sort of (freq, row): rarest words first, ties by position
+  CUDA_OK(cudaMemcpyAsync(ctx->order_buf[0].ptr, ctx->freq.ptr, rows * sizeof(uint32_t),
+                          cudaMemcpyDeviceToDevice, st));
+  launches += launch_iota(ctx->order_buf[1].ptr, rows, st);
+  uint32_t *f0 = ctx->order_buf[0].ptr, *o0 = ctx->order_buf[1].ptr, *f1 = ctx->order_buf[2].ptr,
+           *o1 = ctx->order_buf[3].ptr;
+  launches += launch_radix_sort_pairs(&f0, &o0, &f1, &o1, rows, bits_for(rows), ctx->radix_hist.ptr,
+                                      ctx->scan_scratch.ptr, st);
+  ctx->sorted_freq = f0;
+  ctx->order = o0;
+  launches += launch_count_min_freq(ctx->sorted_freq, rows, ctx->scalars.ptr, st);
+
+  // search-state storage
+  ctx->nn.alloc(rows);
+  ctx->best.alloc(1);
+  ctx->xchg.alloc(4);
+  ctx->exact.alloc(rows);
+  ctx->excluded.alloc(rows);
+  ctx->counters.alloc(1);
+  ctx->flags.alloc(2 * static_cast<size_t>(rows));
+  ctx->sel.alloc(4);
+  ctx->rescore_out.alloc(1);
+  ctx->batch_capacity = 0;
+  ctx->stats.kernel_launches = launches;
+}
+
+void finish_prepare(tsdd_cuda_ctx* ctx) {
+  uint32_t scalars[4] = {0, 0, 0, 0};
+  CUDA_OK(cudaMemcpyAsync(scalars, ctx->scalars.ptr, sizeof(scalars), cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_OK(cudaEventRecord(ctx->ev_b, ctx->stream));
+  sync_stream(ctx);
+  float ms = 0.f;
+  CUDA_OK(cudaEventElapsedTime(&ms, ctx->ev_a, ctx->ev_b));
+  ctx->stats.prep_ms = ms;
+  ctx->stats.rows = ctx->rows;
+  ctx->stats.buckets = scalars[0];
+  ctx->stats.min_freq_candidates = scalars[1];
+  ctx->prepared = true;
+}
+
+void reset_stats(tsdd_cuda_ctx* ctx) {
+  std::memset(&ctx->stats, 0, sizeof(ctx->stats));
+  ctx->prepared = false;
+}
+
+template <typename T>
+void prepare_host(tsdd_cuda_ctx* ctx, const T* series, size_t m, size_t n, size_t word_len, size_t alphabet) {
+  check_series(series, m);
+  check_shape(m, n, word_len, alphabet);
+  bind_device(ctx);
+  reset_stats(ctx);
+  cudaStream_t st = ctx->stream;
+  cudaEvent_t ev_h0, ev_h1;
+  CUDA_OK(cudaEventCreate(&ev_h0));
+  CUDA_OK(cudaEventCreate(&ev_h1));
+  ctx->series.alloc(m);
+  CUDA_OK(cudaEventRecord(ev_h0, st));
+  uint64_t extra = 0;
+  if constexpr (sizeof(T) == sizeof(float)) {
+    ctx->series_f32.alloc(m);
+    CUDA_OK(cudaMemcpyAsync(ctx->series_f32.ptr, series, m * sizeof(float), cudaMemcpyHostToDevice, st));
+    CUDA_OK(cudaEventRecord(ev_h1, st));
+    CUDA_OK(cudaEventRecord(ctx->ev_a, st));
+    extra += launch_widen_series(ctx->series_f32.ptr, ctx->series.ptr, m, st);
+  } else {
+    CUDA_OK(cudaMemcpyAsync(ctx->series.ptr, series, m * sizeof(double), cudaMemcpyHostToDevice, st));
+    CUDA_OK(cudaEventRecord(ev_h1, st));
+    CUDA_OK(cudaEventRecord(ctx->ev_a, st));
+  }
+  prepare_on_device(ctx, m, n, word_len, alphabet);
+  ctx->stats.kernel_launches += extra;
+  finish_prepare(ctx);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ev_h0, ev_h1);
+  ctx->stats.h2d_ms = ms;
+  cudaEventDestroy(ev_h0);
+  cudaEventDestroy(ev_h1);
+}
+
+// ------------------------------------------------------------------ exchange
+// In place, element-wise max of `count` (<= 4) keys over all ranks.
+void exchange_keys(tsdd_cuda_ctx* ctx, uint64_t* keys, size_t count) {
+  if (ctx->world <= 1 && !ctx->comm) return;
+  if (ctx->comm) {
+    CUDA_OK(cudaMemcpyAsync(ctx->xchg.ptr, keys, count * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+    g_nccl.check(g_nccl.AllReduce(ctx->xchg.ptr, ctx->xchg.ptr, count, NcclApi::kUint64, NcclApi::kMax,
+                                  ctx->comm, ctx->stream),
+                 "ncclAllReduce");
+    CUDA_OK(cudaMemcpyAsync(keys, ctx->xchg.ptr, count * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    sync_stream(ctx);
+    return;
+  }
+  if (!ctx->exchange_fn) fail(TSDD_ERR_RUNTIME, "world > 1 but no exchange is configured");
+  if (ctx->exchange_fn(ctx->exchange_user, keys, count) != 0)
+    fail(TSDD_ERR_RUNTIME, "the best-so-far exchange hook reported a failure");
+}
+
+// ------------------------------------------------------------------ search
+cudaEvent_t next_event(tsdd_cuda_ctx* ctx) {
+  if (ctx->events_used == ctx->event_pool.size()) {
+    cudaEvent_t e;
+    CUDA_OK(cudaEventCreate(&e));
+    ctx->event_pool.push_back(e);
+  }
+  return ctx->event_pool[ctx->events_used++];
+}
+
+void ensure_batch_capacity(tsdd_cuda_ctx* ctx, uint32_t batch) {
+  const uint32_t padded = round_up_u32(batch, kTileRows);
+  if (padded <= ctx->batch_capacity) return;
+  ctx->batch_rows.alloc(padded);
+  ctx->batch_alt.alloc(padded);
+  ctx->batch_matrix.alloc(static_cast<size_t>(padded) * ctx->stride);
+  ctx->batch_capacity = padded;
+}
+
+uint32_t read_sel(tsdd_cuda_ctx* ctx) {
+  CUDA_OK(cudaMemcpyAsync(ctx->h_sel, ctx->sel.ptr, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  sync_stream(ctx);
+  return ctx->h_sel[0];
+}
+
+// Neighbour ranges of one batch: the first is 1/2^(rounds-1) of the rows, each
+// later one as large as everything before it; boundaries on tile multiples.
+std::vector<uint32_t> range_bounds(uint32_t rows, int rounds, bool pruning) {
+  std::vector<uint32_t> bounds{0};
+  if (pruning) {
+    for (int r = 1; r < rounds; ++r) {
+      uint64_t b = static_cast<uint64_t>(rows) >> (rounds - r);
+      b = b / kTileRows * kTileRows;
+      if (b > bounds.back() && b < rows) bounds.push_back(static_cast<uint32_t>(b));
+    }
+  }
+  bounds.push_back(rows);
+  return bounds;
+}
+
+void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
+  cudaStream_t st = ctx->stream;
+  SearchState s = ctx->state();
+  const std::vector<uint32_t> bounds = range_bounds(ctx->rows, ctx->opt_rounds, pruning);
+  uint32_t* list = ctx->batch_rows.ptr;
+  uint32_t* alt = ctx->batch_alt.ptr;
+  uint64_t launches = 0;
+  for (size_t r = 0; r + 1 < bounds.size(); ++r) {
+    if (r > 0 && pruning) {
+      launches += launch_compact_batch(s, list, alt, ctx->batch_capacity, pruning, ctx->sel.ptr, st);
+      std::swap(list, alt);
+      count = read_sel(ctx);
+      if (count == 0) break;
+    }
+    const uint32_t padded = round_up_u32(count, kTileRows);
+    launches += launch_gather_rows(s, list, ctx->sel.ptr, padded, ctx->batch_matrix.ptr, st);
+    const uint32_t range_tiles = (bounds[r + 1] - bounds[r] + kTileRows - 1) / kTileRows;
+    const uint64_t tiles = static_cast<uint64_t>(range_tiles) * (padded / kTileRows);
+    int per_cta = static_cast<int>(std::min<uint64_t>(16, std::max<uint64_t>(1, tiles / (148ull * 8ull))));
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ctx->opt_time_kernels) {
+      e0 = next_event(ctx);
+      e1 = next_event(ctx);
+      CUDA_OK(cudaEventRecord(e0, st));
+    }
+    const int launched = launch_scan_tiles(s, ctx->batch_matrix.ptr, list, ctx->sel.ptr, padded, bounds[r],
+                                           bounds[r + 1], per_cta, pruning, ctx->opt_symmetric, st);
+    if (ctx->opt_time_kernels) CUDA_OK(cudaEventRecord(e1, st));
+    launches += launched;
+    ctx->stats.scan_kernel_launches += launched;
+  }
+  launches += launch_finalize_batch(s, list, ctx->sel.ptr, ctx->batch_capacity, pruning, st);
+  ctx->stats.kernel_launches += launches;
+  ctx->stats.batches += 1;
+}
+
+// One exact arg-max pass over this rank's share of the rarity order.
+uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning) {
+  cudaStream_t st = ctx->stream;
+  SearchState s = ctx->state();
+  uint32_t cursor = 0;
+  uint32_t batch_now = std::min(ctx->opt_first_batch, ctx->opt_batch);
+  for (;;) {
+    if (cursor < ctx->rows) {
+      ensure_batch_capacity(ctx, batch_now);
+      ctx->stats.kernel_launches +=
+          launch_select_batch(s, ctx->order, cursor, batch_now, static_cast<uint32_t>(ctx->world),
+                              static_cast<uint32_t>(ctx->rank), pruning, ctx->flags.ptr, ctx->scan_scratch.ptr,
+                              ctx->batch_rows.ptr, ctx->sel.ptr, st);
+      const uint32_t count = read_sel(ctx);
+      cursor = count == 0 ? ctx->rows : ctx->h_sel[1];
+      if (count > 0) {
+        ctx->stats.scanned_candidates += count;
+        scan_batch(ctx, count, pruning);
+      }
+      batch_now = std::min(batch_now * 2, ctx->opt_batch);
+    }
+    if (ctx->world > 1 || ctx->comm) {  // a 1-rank communicator still runs the exchange
+      CUDA_OK(cudaMemcpyAsync(ctx->h_keys, ctx->best.ptr, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+      sync_stream(ctx);
+      ctx->h_keys[1] = cursor < ctx->rows ? 1 : 0;
+      exchange_keys(ctx, ctx->h_keys, 2);
+      CUDA_OK(cudaMemcpyAsync(ctx->best.ptr, ctx->h_keys, sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+      if (ctx->h_keys[1] == 0) break;
+    } else if (cursor >= ctx->rows) {
+      break;
+    }
+  }
+  CUDA_OK(cudaMemcpyAsync(ctx->h_keys, ctx->best.ptr, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  sync_stream(ctx);
+  return ctx->h_keys[0];
+}
+
+void collect_search_stats(tsdd_cuda_ctx* ctx) {
+  DeviceCounters c{};
+  CUDA_OK(cudaMemcpy(&c, ctx->counters.ptr, sizeof(c), cudaMemcpyDeviceToHost));
+  ctx->stats.calls = c.calls;
+  ctx->stats.abandoned = c.abandoned;
+  ctx->stats.terms = c.terms;
+  ctx->stats.scan_kernel_terms = c.tile_terms;
+  double total = 0.0;
+  for (size_t e = 0; e + 1 < ctx->events_used; e += 2) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ctx->event_pool[e], ctx->event_pool[e + 1]) == cudaSuccess) total += ms;
+  }
+  ctx->stats.scan_kernel_ms = total;
+}
+
+void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, double* distances) {
+  if (!ctx->prepared) fail(TSDD_ERR_PARAMETER, "tsdd_cuda_search needs a prepared context");
+  if (k < 1) fail(TSDD_ERR_PARAMETER, "k must be >= 1, got " + std::to_string(k));
+  if (!positions || !distances) fail(TSDD_ERR_PARAMETER, "positions and distances must not be null");
+  bind_device(ctx);
+  set_packed_math(ctx->opt_packed);
+  const bool pruning = (flags & TSDD_SEARCH_DISABLE_PRUNING) == 0;
+  cudaStream_t st = ctx->stream;
+  SearchState s = ctx->state();
+  const uint64_t prep_launches = ctx->stats.kernel_launches;
+  (void)prep_launches;
+  ctx->stats.batches = 0;
+  ctx->stats.scanned_candidates = 0;
+  ctx->stats.scan_kernel_launches = 0;
+  ctx->events_used = 0;
+
+  CUDA_OK(cudaEventRecord(ctx->ev_a, st));
+  ctx->stats.kernel_launches += launch_reset_search(s, st);
+  if (pruning)
+    ctx->stats.kernel_launches +=
+        launch_bucket_mates(s, ctx->sorted_row, ctx->slot_bucket.ptr, ctx->offsets.ptr, ctx->opt_mates, st);
+
+  for (int pass = 0; pass < k; ++pass) {
+    if (pass > 0) {
+      CUDA_OK(cudaMemsetAsync(ctx->best.ptr, 0, sizeof(uint64_t), st));
+      ctx->stats.kernel_launches += launch_seed_best(s, st);
+    }
+    const uint64_t key = run_pass(ctx, pruning);
+    if (key == 0) {  // nothing beat 0: the reference's fallback (discovery.cpp:90-93)
+      positions[pass] = 1;
+      distances[pass] = 0.0;
+      continue;
+    }
+    const uint32_t row = best_key_row(key);
+    double d2 = static_cast<double>(float_from_bits(key_bits(key)));
+    if (ctx->opt_rescore) {
+      // the rank that scanned `row` knows its nearest neighbour; others learn it here
+      uint64_t nn_key_host = 0;
+      uint8_t is_exact = 0;
+      CUDA_OK(cudaMemcpyAsync(&nn_key_host, ctx->nn.ptr + row, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+      CUDA_OK(cudaMemcpyAsync(&is_exact, ctx->exact.ptr + row, 1, cudaMemcpyDeviceToHost, st));
+      sync_stream(ctx);
+      uint64_t neighbour_plus_one =
+          (is_exact && key_bits(nn_key_host) == key_bits(key)) ? (nn_key_host & 0xFFFFFFFFull) + 1 : 0;
+      if (ctx->world > 1 || ctx->comm) {
+        ctx->h_keys[0] = neighbour_plus_one;
+        exchange_keys(ctx, ctx->h_keys, 1);
+        neighbour_plus_one = ctx->h_keys[0];
+      }
+      if (neighbour_plus_one != 0 && neighbour_plus_one <= ctx->rows) {
+        ctx->stats.kernel_launches +=
+            launch_rescore_pair(ctx->series.ptr, ctx->mean.ptr, ctx->inv_sigma.ptr, static_cast<uint32_t>(ctx->n),
+                                row, static_cast<uint32_t>(neighbour_plus_one - 1), ctx->rescore_out.ptr, st);
+        CUDA_OK(cudaMemcpyAsync(ctx->h_double, ctx->rescore_out.ptr, sizeof(double), cudaMemcpyDeviceToHost, st));
+        sync_stream(ctx);
+        d2 = *ctx->h_double;
+      }
+    }
+    positions[pass] = static_cast<uint64_t>(row) + 1;
+    distances[pass] = std::sqrt(d2);
+    if (pass + 1 < k) ctx->stats.kernel_launches += launch_exclude_zone(s, row, st);
+  }
+  CUDA_OK(cudaEventRecord(ctx->ev_b, st));
+  sync_stream(ctx);
+  float ms = 0.f;
+  CUDA_OK(cudaEventElapsedTime(&ms, ctx->ev_a, ctx->ev_b));
+  ctx->stats.search_ms = ms;
+  collect_search_stats(ctx);
+}
+
+template <typename Fn>
+int guarded(tsdd_cuda_ctx* ctx, Fn&& fn) {
+  try {
+    fn();
+    return TSDD_OK;
+  } catch (const Failure& f) {
+    if (ctx) ctx->error = f.message;
+    else g_create_error = f.message;
+    return f.code;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->error = e.what();
+    else g_create_error = e.what();
+    return TSDD_ERR_RUNTIME;
+  }
+}
+
+template <typename Src, typename Dst>
+void fetch_converted(tsdd_cuda_ctx* ctx, const Src* d_src, size_t count, Dst add, void* dst) {
+  std::vector<Src> host(count);
+  CUDA_OK(cudaMemcpy(host.data(), d_src, count * sizeof(Src), cudaMemcpyDeviceToHost));
+  Dst* out = static_cast<Dst*>(dst);
+  for (size_t i = 0; i < count; ++i) out[i] = static_cast<Dst>(host[i]) + add;
+  (void)ctx;
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+int tsdd_cuda_create(tsdd_cuda_ctx** out, int device) {
+  if (!out) {
+    g_create_error = "out must not be null";
+    return TSDD_ERR_PARAMETER;
+  }
+  *out = nullptr;
+  tsdd_cuda_ctx* ctx = nullptr;
+  const int rc = guarded(nullptr, [&] {
+    int count = 0;
+    const cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+      fail(TSDD_ERR_RUNTIME, std::string("no CUDA device: the engine has no CPU fallback (") +
+                                 (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices") + ")");
+    if (device < 0 || device >= count)
+      fail(TSDD_ERR_PARAMETER, "device " + std::to_string(device) + " is outside 0.." + std::to_string(count - 1));
+    cudaDeviceProp prop{};
+    CUDA_OK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      fail(TSDD_ERR_RUNTIME, std::string("device '") + prop.name + "' is sm_" + std::to_string(prop.major) +
+                                 std::to_string(prop.minor) + "; this library holds sm_100a code only");
+    ctx = new tsdd_cuda_ctx();
+    ctx->device = device;
+    CUDA_OK(cudaSetDevice(device));
+    CUDA_OK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreate(&ctx->ev_a));
+    CUDA_OK(cudaEventCreate(&ctx->ev_b));
+    CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_sel), 4 * sizeof(uint32_t)));
+    CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_keys), 4 * sizeof(uint64_t)));
+    CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_double), sizeof(double)));
+  });
+  if (rc != TSDD_OK) {
+    delete ctx;
+    return rc;
+  }
+  *out = ctx;
+  return TSDD_OK;
+}
+
+void tsdd_cuda_destroy(tsdd_cuda_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
+  for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
+  if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
+  if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
+  if (ctx->h_sel) cudaFreeHost(ctx->h_sel);
+  if (ctx->h_keys) cudaFreeHost(ctx->h_keys);
+  if (ctx->h_double) cudaFreeHost(ctx->h_double);
+  cudaStream_t st = ctx->stream;
+  delete ctx;  // frees the device arrays
+  if (st) cudaStreamDestroy(st);
+}
+
+const char* tsdd_cuda_last_error(const tsdd_cuda_ctx* ctx) {
+  return ctx ? ctx->error.c_str() : g_create_error.c_str();
+}
+
+int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
+  if (!ctx) return TSDD_ERR_PARAMETER;
+  return guarded(ctx, [&] {
+    const std::string key = name ? name : "";
+    if (key == "batch") {
+      if (value < 1 || value > 1048576) fail(TSDD_ERR_PARAMETER, "batch must be in 1..1048576");
+      ctx->opt_batch = static_cast<uint32_t>(value);
+    } else if (key == "first_batch") {
+      if (value < 1 || value > 1048576) fail(TSDD_ERR_PARAMETER, "first_batch must be in 1..1048576");
+      ctx->opt_first_batch = static_cast<uint32_t>(value);
+    } else if (key == "rounds") {
+      if (value < 1 || value > 24) fail(TSDD_ERR_PARAMETER, "rounds must be in 1..24");
+      ctx->opt_rounds = static_cast<int>(value);
+    } else if (key == "bucket_mates") {
+      if (value < 0 || value > 1024) fail(TSDD_ERR_PARAMETER, "bucket_mates must be in 0..1024");
+      ctx->opt_mates = static_cast<int>(value);
+    } else if (key == "rescore") {
+      ctx->opt_rescore = value != 0;
+    } else if (key == "symmetric") {
+      ctx->opt_symmetric = value != 0;
+    } else if (key == "packed") {
+      ctx->opt_packed = value != 0;
+    } else if (key == "time_kernels") {
+      ctx->opt_time_kernels = value != 0;
+    } else {
+      fail(TSDD_ERR_PARAMETER, "unknown option '" + key + "'");
+    }
+  });
+}
+
+int tsdd_cuda_check_config_f32(const float* series, size_t m, size_t n, size_t word_len, size_t alphabet,
+                               char* message, size_t message_bytes) {
+  try {
+    check_series(series, m);
+    check_shape(m, n, word_len, alphabet);
+  } catch (const Failure& f) {
+    if (message && message_bytes) std::snprintf(message, message_bytes, "%s", f.message.c_str());
+    return f.code;
+  }
+  if (message && message_bytes) message[0] = '\0';
+  return TSDD_OK;
+}
+
+int tsdd_cuda_check_config_f64(const double* series, size_t m, size_t n, size_t word_len, size_t alphabet,
+                               char* message, size_t message_bytes) {
+  try {
+    check_series(series, m);
+    check_shape(m, n, word_len, alphabet);
+  } catch (const Failure& f) {
+    if (message && message_bytes) std::snprintf(message, message_bytes, "%s", f.message.c_str());
+    return f.code;
+  }
+  if (message && message_bytes) message[0] = '\0';
+  return TSDD_OK;
+}
+
+int tsdd_cuda_prepare_f32(tsdd_cuda_ctx* ctx, const float* series, size_t m, size_t n, size_t word_len,
+                          size_t alphabet) {
+  if (!ctx) return TSDD_ERR_PARAMETER;
+  return guarded(ctx, [&] { prepare_host(ctx, series, m, n, word_len, alphabet); });
+}
+
+int tsdd_cuda_prepare_f64(tsdd_cuda_ctx* ctx, const double* series, size_t m, size_t n, size_t word_len,
+                          size_t alphabet) {
+  if (!ctx) return TSDD_ERR_PARAMETER;
+  return guarded(ctx, [&] { prepare_host(ctx, series, m, n, word_len, alphabet); });
+}
+
+int tsdd_cuda_prepare_device_f32(tsdd_cuda_ctx* ctx, const float* d_series, size_t m, size_t n,
+                                 size_t word_len, size_t alphabet) {
+  if (!ctx) return TSDD_ERR_PARAMETER;
+  return guarded(ctx, [&] {
+    if (!d_series || m == 0) fail(TSDD_ERR_VALIDATION, "series is empty");
+    check_shape(m, n, word_len, alphabet);
+    bind_device(ctx);
+    reset_stats(ctx);
+    ctx->series.alloc(m);
+    // the caller's stream is unknown: order after everything already queued on the device
+    CUDA_OK(cudaDeviceSynchronize());
+    CUDA_OK(cudaEventRecord(ctx->ev_a, ctx->stream));
+    const uint64_t extra = launch_widen_series(d_series, ctx->series.ptr, m, ctx->stream);
+    prepare_on_device(ctx, m, n, word_len, alphabet);
+    ctx->stats.kernel_launches += extra;
+    finish_prepare(ctx);
+  });
+}
+
+int tsdd_cuda_search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, double* distances) {
+  if (!ctx) return TSDD_ERR_PARAMETER;
+  return guarded(ctx, [&] { search(ctx, k, flags, positions, distances); });
+}
+
+int tsdd_cuda_get_stats(const tsdd_cuda_ctx* ctx, tsdd_cuda_stats* out) {
+  if (!ctx || !out) return TSDD_ERR_PARAMETER;
+  *out = ctx->stats;
+  return TSDD_OK;
+}
+
+size_t tsdd_cuda_row_stride(const tsdd_cuda_ctx* ctx) { return ctx ? ctx->stride : 0; }
+
+int tsdd_cuda_fetch(tsdd_cuda_ctx* ctx, int what, void* dst, size_t bytes) {
+  if (!ctx) return TSDD_ERR_PARAMETER;
+  return guarded(ctx, [&] {
+    if (!ctx->prepared) fail(TSDD_ERR_PARAMETER, "tsdd_cuda_fetch needs a prepared context");
+    if (!dst) fail(TSDD_ERR_PARAMETER, "dst must not be null");
+    bind_device(ctx);
+    sync_stream(ctx);
+    const size_t N = ctx->rows, w = ctx->word_len;
+    auto expect = [&](size_t want) {
+      if (bytes != want)
+        fail(TSDD_ERR_PARAMETER, "fetch " + std::to_string(what) + " needs exactly " + std::to_string(want) +
+                                     " bytes, got " + std::to_string(bytes));
+    };
+    switch (what) {
+      case TSDD_FETCH_ROWS:
+        expect(N * ctx->stride * sizeof(float));
+        CUDA_OK(cudaMemcpy(dst, ctx->matrix.ptr, bytes, cudaMemcpyDeviceToHost));
+        break;
+      case TSDD_FETCH_MEAN:
+        expect(N * sizeof(double));
+        CUDA_OK(cudaMemcpy(dst, ctx->mean.ptr, bytes, cudaMemcpyDeviceToHost));
+        break;
+      case TSDD_FETCH_INV_SIGMA:
+        expect(N * sizeof(double));
+        CUDA_OK(cudaMemcpy(dst, ctx->inv_sigma.ptr, bytes, cudaMemcpyDeviceToHost));
+        break;
+      case TSDD_FETCH_PAA:
+      case TSDD_FETCH_SAX: {
+        // not kept resident: re-run the encoder with the optional outputs switched on
+        expect(what == TSDD_FETCH_PAA ? N * w * sizeof(double) : N * w * sizeof(uint32_t));
+        DeviceArray<double> paa, mean, inv;
+        DeviceArray<uint32_t> sax, hash;
+        paa.alloc(N * w);
+        sax.alloc(N * w);
+        mean.alloc(N);
+        inv.alloc(N);
+        hash.alloc(N);
+        launch_window_encode(ctx->series.ptr, ctx->rows, static_cast<uint32_t>(ctx->n), static_cast<uint32_t>(w),
+                             static_cast<uint32_t>(ctx->alphabet), mean.ptr, inv.ptr, hash.ptr, paa.ptr, sax.ptr,
+                             ctx->stream);
+        sync_stream(ctx);
+        CUDA_OK(cudaMemcpy(dst, what == TSDD_FETCH_PAA ? static_cast<void*>(paa.ptr) : static_cast<void*>(sax.ptr),
+                           bytes, cudaMemcpyDeviceToHost));
+        break;
+      }
+      case TSDD_FETCH_HASH:
+        expect(N * sizeof(uint64_t));
+        fetch_converted<uint32_t, uint64_t>(ctx, ctx->hash0.ptr, N, 1, dst);
+        break;
+      case TSDD_FETCH_FREQ:
+        expect(N * sizeof(uint32_t));
+        CUDA_OK(cudaMemcpy(dst, ctx->freq.ptr, bytes, cudaMemcpyDeviceToHost));
+        break;
+      case TSDD_FETCH_BUCKETS:
+        expect(N * sizeof(uint64_t));
+        fetch_converted<uint32_t, uint64_t>(ctx, ctx->sorted_row, N, 1, dst);
+        break;
+      case TSDD_FETCH_ORDER:
+        expect(N * sizeof(uint64_t));
+        fetch_converted<uint32_t, uint64_t>(ctx, ctx->order, N, 1, dst);
+        break;
+      case TSDD_FETCH_CANDIDATES:
+        expect(ctx->stats.min_freq_candidates * sizeof(uint64_t));
+        fetch_converted<uint32_t, uint64_t>(ctx, ctx->order, ctx->stats.min_freq_candidates, 1, dst);
+        break;
+      case TSDD_FETCH_NN_SQ: {
+        expect(N * sizeof(float));
+        std::vector<uint64_t> keys(N);
+        CUDA_OK(cudaMemcpy(keys.data(), ctx->nn.ptr, N * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        float* out = static_cast<float*>(dst);
+        for (size_t i = 0; i < N; ++i) out[i] = float_from_bits(key_bits(keys[i]));
+        break;
+      }
+      case TSDD_FETCH_NN_EXACT:
+        expect(N);
+        CUDA_OK(cudaMemcpy(dst, ctx->exact.ptr, N, cudaMemcpyDeviceToHost));
+        break;
+      default:
+        fail(TSDD_ERR_PARAMETER, "unknown fetch selector " + std::to_string(what));
+    }
+  });
+}
+
+int tsdd_cuda_comm_unique_id(char id[128]) {
+  return guarded(nullptr, [&] {
+    g_nccl.load();
+    NcclApi::UniqueId uid;
+    g_nccl.check(g_nccl.GetUniqueId(&uid), "ncclGetUniqueId");
+    std::memcpy(id, uid.internal, 128);
+  });
+}
+
+int tsdd_cuda_comm_init(tsdd_cuda_ctx* ctx, const char id[128], int world, int rank) {
+  if (!ctx) return TSDD_ERR_PARAMETER;
+  return guarded(ctx, [&] {
+    if (world < 1 || rank < 0 || rank >= world) fail(TSDD_ERR_PARAMETER, "need 0 <= rank < world");
+    bind_device(ctx);
+    g_nccl.load();
+    if (ctx->comm) {
+      g_nccl.CommDestroy(ctx->comm);
+      ctx->comm = nullptr;
+    }
+    NcclApi::UniqueId uid;
+    std::memcpy(uid.internal, id, 128);
+    g_nccl.check(g_nccl.CommInitRank(&ctx->comm, world, uid, rank), "ncclCommInitRank");
+    ctx->world = world;
+    ctx->rank = rank;
+    ctx->exchange_fn = nullptr;
+  });
+}
+
+int tsdd_cuda_set_exchange(tsdd_cuda_ctx* ctx, tsdd_exchange_fn fn, void* user, int world, int rank) {
+  if (!ctx) return TSDD_ERR_PARAMETER;
+  return guarded(ctx, [&] {
+    if (world < 1 || rank < 0 || rank >= world) fail(TSDD_ERR_PARAMETER, "need 0 <= rank < world");
+    if (world > 1 && !fn) fail(TSDD_ERR_PARAMETER, "world > 1 needs an exchange function");
+    if (ctx->comm) {
+      g_nccl.CommDestroy(ctx->comm);
+      ctx->comm = nullptr;
+    }
+    ctx->exchange_fn = fn;
+    ctx->exchange_user = user;
+    ctx->world = world;
+    ctx->rank = rank;
+  });
+}
+
+int tsdd_cuda_fp32_probe(tsdd_cuda_ctx* ctx, int which, double* ops_per_s, double* ms_out) {
+  if (!ctx) return TSDD_ERR_PARAMETER;
+  return guarded(ctx, [&] {
+    if (which < 0 || which > 3) fail(TSDD_ERR_PARAMETER, "probe selector must be 0..3");
+    bind_device(ctx);
+    const int blocks = 148 * 8, iters = 4096;
+    DeviceArray<float> sink;
+    sink.alloc(static_cast<size_t>(blocks) * 256);
+    launch_fp32_probe(which, sink.ptr, blocks, 64, ctx->stream);  // warm-up
+    float best_ms = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+      CUDA_OK(cudaEventRecord(ctx->ev_a, ctx->stream));
+      launch_fp32_probe(which, sink.ptr, blocks, iters, ctx->stream);
+      CUDA_OK(cudaEventRecord(ctx->ev_b, ctx->stream));
+      sync_stream(ctx);
+      float ms = 0.f;
+      CUDA_OK(cudaEventElapsedTime(&ms, ctx->ev_a, ctx->ev_b));
+      best_ms = std::min(best_ms, ms);
+    }
+    if (ops_per_s) *ops_per_s = fp32_probe_ops(which, blocks, iters) / (best_ms * 1e-3);
+    if (ms_out) *ms_out = best_ms;
+  });
+}
+
+int tsdd_cuda_nn_profile(tsdd_cuda_ctx* ctx, float* nn_sq_host) {
+  if (!ctx) return TSDD_ERR_PARAMETER;
+  return guarded(ctx, [&] {
+    if (!nn_sq_host) fail(TSDD_ERR_PARAMETER, "nn_sq_host must not be null");
+    uint64_t pos = 0;
+    double dist = 0.0;
+    search(ctx, 1, TSDD_SEARCH_DISABLE_PRUNING, &pos, &dist);
+    std::vector<uint64_t> keys(ctx->rows);
+    CUDA_OK(cudaMemcpy(keys.data(), ctx->nn.ptr, keys.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < keys.size(); ++i) nn_sq_host[i] = float_from_bits(key_bits(keys[i]));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,120 @@
+// Host-callable launchers of the sm_100a kernels (prep_kernels.cu,
+// search_kernels.cu, probe_kernels.cu).  Every launcher enqueues on `stream`
+// and returns the number of kernels it launched; errors surface through
+// cudaGetLastError() in the engine.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace tsdd_b200 {
+
+constexpr int kTileRows = 128;     // candidates per tile == neighbours per tile
+constexpr int kChunk = 32;         // columns per pipeline stage (one 128-byte line per row)
+constexpr uint32_t kRowAlign = 32; // row stride is a multiple of 32 floats
+
+// ------------------------------------------------------------------ preparation
+int launch_widen_series(const float* d_in, double* d_out, size_t m, cudaStream_t stream);
+
+// Per-window mean / 1/sigma (float64), PAA -> SAX -> 0-based word hash.
+// paa_out / sax_out may be null (kept only for parity tests).
+int launch_window_encode(const double* d_series, uint32_t rows, uint32_t n, uint32_t word_len,
+                         uint32_t alphabet, double* d_mean, double* d_inv_sigma, uint32_t* d_hash0,
+                         double* d_paa, uint32_t* d_sax, cudaStream_t stream);
+
+// float32 z-normalised matrix, rows x stride, padding columns zero.
+int launch_build_rows(const double* d_series, const double* d_mean, const double* d_inv_sigma,
+                      uint32_t rows, uint32_t n, uint32_t stride, float* d_rows, cudaStream_t stream);
+
+// Stable LSD radix sort of (key, value) pairs on bits [0, key_bits).  Result is
+// left in (*keys, *vals); the alt buffers are scratch.  `hist` needs
+// radix_sort_scratch_words(count) uint32 words.
+size_t radix_sort_scratch_words(uint32_t count);
+int launch_radix_sort_pairs(uint32_t** keys, uint32_t** vals, uint32_t** keys_alt,
+                            uint32_t** vals_alt, uint32_t count, int key_bits, uint32_t* d_hist,
+                            uint32_t* d_scan_scratch, cudaStream_t stream);
+
+// Exclusive prefix sum of uint32; d_out may alias d_in.  Scratch needs
+// scan_scratch_words(count) words.
+size_t scan_scratch_words(uint32_t count);
+int launch_exclusive_scan(const uint32_t* d_in, uint32_t* d_out, uint32_t count,
+                          uint32_t* d_scratch, cudaStream_t stream);
+
+int launch_iota(uint32_t* d_out, uint32_t count, cudaStream_t stream);
+
+// Run-length histogram of the sorted hashes: bucket offsets, per-slot bucket
+// id, per-row frequency.  d_scalars[0] = number of buckets.
+int launch_bucket_index(const uint32_t* d_sorted_hash, const uint32_t* d_sorted_row, uint32_t rows,
+                        uint32_t* d_head_scan, uint32_t* d_slot_bucket, uint32_t* d_offsets,
+                        uint32_t* d_freq, uint32_t* d_scalars, uint32_t* d_scan_scratch,
+                        cudaStream_t stream);
+
+// d_scalars[1] = number of leading entries of the sorted frequencies equal to the minimum.
+int launch_count_min_freq(const uint32_t* d_sorted_freq, uint32_t rows, uint32_t* d_scalars,
+                          cudaStream_t stream);
+
+// ------------------------------------------------------------------ search
+struct SearchState {
+  const float* rows;        // rows_padded x stride
+  uint32_t n_rows;          // N
+  uint32_t n;               // subsequence length
+  uint32_t stride;          // floats per row
+  uint64_t* nn;             // N nn keys (bits(d^2) << 32 | neighbour)
+  uint8_t* exact;           // N
+  uint8_t* excluded;        // N
+  uint64_t* best;           // 1 best key
+  DeviceCounters* counters;
+};
+
+int launch_reset_search(SearchState s, cudaStream_t stream);
+
+// Same-word neighbours first (the HOTSAX inner heuristic, discovery.cpp:51-63):
+// every row is measured against up to `mates` rows of its own bucket.
+int launch_bucket_mates(SearchState s, const uint32_t* d_sorted_row, const uint32_t* d_slot_bucket,
+                        const uint32_t* d_offsets, int mates, cudaStream_t stream);
+
+// Outer-loop batch selection: the next `batch` live entries of the rarity
+// order at or after `cursor` that belong to this rank.  d_sel[0] = count,
+// d_sel[1] = next cursor.
+int launch_select_batch(SearchState s, const uint32_t* d_order, uint32_t cursor, uint32_t batch,
+                        uint32_t world, uint32_t rank, bool pruning, uint32_t* d_flags,
+                        uint32_t* d_scan_scratch, uint32_t* d_batch_rows, uint32_t* d_sel,
+                        cudaStream_t stream);
+
+// Drops dead candidates from the batch list (stable); count lives in d_sel[0].
+int launch_compact_batch(SearchState s, uint32_t* d_batch_rows, uint32_t* d_batch_alt,
+                         uint32_t capacity, bool pruning, uint32_t* d_sel, cudaStream_t stream);
+
+// Copies the batch's matrix rows into a dense [capacity_padded x stride] buffer.
+int launch_gather_rows(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,
+                       uint32_t capacity_padded, float* d_batch_matrix, cudaStream_t stream);
+
+// The tiled early-abandoning distance kernel: batch candidates x neighbour
+// rows [j_begin, j_end).
+int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t* d_batch_rows,
+                      const uint32_t* d_sel, uint32_t capacity_padded, uint32_t j_begin,
+                      uint32_t j_end, int tiles_per_cta, bool pruning, bool symmetric,
+                      cudaStream_t stream);
+
+// Survivors of a complete scan are exact; each raises the best-so-far.
+int launch_finalize_batch(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,
+                          uint32_t capacity, bool pruning, cudaStream_t stream);
+
+// best = max over exact, allowed rows (start of a top-k pass).
+int launch_seed_best(SearchState s, cudaStream_t stream);
+int launch_exclude_zone(SearchState s, uint32_t row, cudaStream_t stream);
+
+// float64 re-scoring of one pair (finalists): d_out[0] = d^2.
+int launch_rescore_pair(const double* d_series, const double* d_mean, const double* d_inv_sigma,
+                        uint32_t n, uint32_t row_a, uint32_t row_b, double* d_out,
+                        cudaStream_t stream);
+
+// ------------------------------------------------------------------ probes
+int launch_fp32_probe(int which, float* d_sink, int blocks, int iters, cudaStream_t stream);
+double fp32_probe_ops(int which, int blocks, int iters);
+
+}  // namespace tsdd_b200

@@ -1,0 +1,415 @@
+// Preparation stage on the device (replaces src/pipeline.cpp:60-69 of the
+// reference): per-window statistics and SAX encoding, the float32
+// z-normalised subsequence matrix, and the SAX-word bucket / frequency /
+// rarity index built with a radix sort and a run-length histogram.
+//
+// Everything here is HBM-bound integer / streaming work; kernels are laid
+// out for coalesced 128-byte accesses and sized in whole waves of the SMs.
+
+#include "kernels.hpp"
+
+namespace tsdd_b200 {
+
+namespace {
+
+// Equiprobable N(0,1) breakpoints for |A| = 2..10, lower half mirrored onto
+// the upper half; row a-2 holds the a-1 finite thresholds.  Regenerated with
+// scipy norm.ppf (tools/gen_sax_breakpoints.py); same values as the
+// reference's table (sax.cpp:14-46).
+__constant__ double c_breaks[9][9] = {
+    {0},
+    {-0.43072729929545756, 0.43072729929545756},
+    {-0.67448975019608171, 0, 0.67448975019608171},
+    {-0.84162123357291418, -0.25334710313579972, 0.25334710313579972, 0.84162123357291418},
+    {-0.96742156610170105, -0.43072729929545756, 0, 0.43072729929545756, 0.96742156610170105},
+    {-1.0675705238781414, -0.56594882193286311, -0.1800123697927051, 0.1800123697927051,
+     0.56594882193286311, 1.0675705238781414},
+    {-1.1503493803760079, -0.67448975019608171, -0.31863936396437514, 0, 0.31863936396437514,
+     0.67448975019608171, 1.1503493803760079},
+    {-1.2206403488473501, -0.7647096737863871, -0.43072729929545756, -0.13971029888186212,
+     0.13971029888186212, 0.43072729929545756, 0.7647096737863871, 1.2206403488473501},
+    {-1.2815515655446004, -0.84162123357291418, -0.52440051270804089, -0.25334710313579972, 0,
+     0.25334710313579972, 0.52440051270804089, 0.84162123357291418, 1.2815515655446004},
+};
+
+inline unsigned blocks_for(size_t items, unsigned per_block) {
+  return static_cast<unsigned>((items + per_block - 1) / per_block);
+}
+
+// ------------------------------------------------------------------ series
+__global__ void k_widen_series(const float* __restrict__ in, double* __restrict__ out, size_t m) {
+  const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < m) out[i] = static_cast<double>(in[i]);
+}
+
+// One thread per window.  Adjacent threads read adjacent samples, so every
+// step of the loops below is one coalesced 256-byte request per warp, served
+// from L1/L2 (the whole series is a few tens of MB).
+//
+//   mean, sigma : series.cpp:21-37 — sum and sum of squares in sequence order,
+//                 population variance sum_sq/n - mu^2, sigma < 1e-12 -> flat
+//   PAA         : sax.cpp:63-80   — n*w unit grid, weighted sum / n
+//   symbol      : sax.cpp:53-57   — 1 + #{breakpoints <= value}
+//   hash        : sax.cpp:121-132 — big-endian base |A|; stored 0-based so that
+//                 4^16 words still fit 32 bits
+__global__ void __launch_bounds__(256)
+k_window_encode(const double* __restrict__ x, uint32_t rows, uint32_t n, uint32_t word_len,
+                uint32_t alphabet, double* __restrict__ mean, double* __restrict__ inv_sigma,
+                uint32_t* __restrict__ hash0, double* __restrict__ paa_out,
+                uint32_t* __restrict__ sax_out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  const double* p = x + i;
+  double sum = 0.0, sum_sq = 0.0;
+  for (uint32_t t = 0; t < n; ++t) {
+    const double v = p[t];
+    sum += v;
+    sum_sq += v * v;
+  }
+  const double dn = static_cast<double>(n);
+  const double mu = sum / dn;
+  const double var = sum_sq / dn - mu * mu;
+  const double sigma = var > 0.0 ? sqrt(var) : 0.0;
+  const bool flat = sigma < 1e-12;
+  const double inv = flat ? 0.0 : 1.0 / sigma;
+  mean[i] = mu;
+  inv_sigma[i] = inv;
+
+  const double* bp = c_breaks[alphabet - 2];
+  uint64_t h = 0;
+  for (uint32_t k = 0; k < word_len; ++k) {
+    const uint64_t lo = static_cast<uint64_t>(k) * n;
+    const uint64_t hi = lo + n;
+    const uint32_t t_first = static_cast<uint32_t>(lo / word_len);
+    const uint32_t t_last = static_cast<uint32_t>((hi - 1) / word_len);
+    double acc = 0.0;
+    for (uint32_t t = t_first; t <= t_last; ++t) {
+      const uint64_t el = static_cast<uint64_t>(t) * word_len;
+      const uint64_t eh = el + word_len;
+      const uint64_t units = (eh < hi ? eh : hi) - (el > lo ? el : lo);
+      const double v = flat ? 0.0 : (p[t] - mu) * inv;
+      acc += static_cast<double>(units) * v;
+    }
+    const double seg = acc / dn;
+    uint32_t sym = 1;
+    for (uint32_t b = 0; b + 1 < alphabet; ++b) sym += (bp[b] <= seg) ? 1u : 0u;
+    if (paa_out) paa_out[static_cast<size_t>(i) * word_len + k] = seg;
+    if (sax_out) sax_out[static_cast<size_t>(i) * word_len + k] = sym;
+    h = h * alphabet + (sym - 1);
+  }
+  hash0[i] = static_cast<uint32_t>(h);
+}
+
+// Subsequence matrix (series.cpp:46-74), float32: element (i, t) is the
+// float64 value (x[i+t] - mu_i) * (1/sigma_i) rounded once.  One thread
+// writes one float4; a warp writes 512 contiguous bytes.  Write-bound.
+__global__ void __launch_bounds__(256)
+k_build_rows(const double* __restrict__ x, const double* __restrict__ mean,
+             const double* __restrict__ inv_sigma, uint32_t rows, uint32_t n, uint32_t stride,
+             float* __restrict__ out) {
+  const uint32_t quads = stride / 4;
+  const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const size_t row = idx / quads;
+  if (row >= rows) return;
+  const uint32_t t0 = static_cast<uint32_t>(idx % quads) * 4;
+  const double mu = mean[row];
+  const double inv = inv_sigma[row];
+  const double* p = x + row + t0;
+  float4 v;
+  v.x = (t0 + 0 < n) ? static_cast<float>((p[0] - mu) * inv) : 0.f;
+  v.y = (t0 + 1 < n) ? static_cast<float>((p[1] - mu) * inv) : 0.f;
+  v.z = (t0 + 2 < n) ? static_cast<float>((p[2] - mu) * inv) : 0.f;
+  v.w = (t0 + 3 < n) ? static_cast<float>((p[3] - mu) * inv) : 0.f;
+  *reinterpret_cast<float4*>(out + row * stride + t0) = v;
+}
+
+// ------------------------------------------------------------------ scan
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t value, uint32_t* total) {
+  __shared__ uint32_t warp_sums[kScanThreads / 32];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t incl = value;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t up = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    if (lane >= static_cast<uint32_t>(d)) incl += up;
+  }
+  if (lane == 31) warp_sums[warp] = incl;
+  __syncthreads();
+  uint32_t warp_base = 0, all = 0;
+#pragma unroll
+  for (int w = 0; w < kScanThreads / 32; ++w) {
+    const uint32_t s = warp_sums[w];
+    if (static_cast<uint32_t>(w) < warp) warp_base += s;
+    all += s;
+  }
+  __syncthreads();
+  *total = all;
+  return warp_base + incl - value;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+k_scan_tile(const uint32_t* in, uint32_t* out, uint32_t count, uint32_t* tile_sums) {
+  const uint32_t base = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+  uint32_t v[kScanItems];
+  uint32_t mine = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    v[k] = (base + k < count) ? in[base + k] : 0u;
+    mine += v[k];
+  }
+  uint32_t total;
+  uint32_t run = block_exclusive_scan(mine, &total);
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (base + k < count) out[base + k] = run;
+    run += v[k];
+  }
+  if (tile_sums && threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+k_scan_add(uint32_t* out, uint32_t count, const uint32_t* tile_offsets) {
+  const uint32_t add = tile_offsets[blockIdx.x];
+  const uint32_t base = blockIdx.x * kScanTile + threadIdx.x * kScanItems;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k)
+    if (base + k < count) out[base + k] += add;
+}
+
+inline size_t round_up64(size_t v) { return (v + 63) / 64 * 64; }
+
+int scan_recursive(const uint32_t* in, uint32_t* out, uint32_t count, uint32_t* scratch,
+                   cudaStream_t stream) {
+  const uint32_t tiles = (count + kScanTile - 1) / kScanTile;
+  if (tiles <= 1) {
+    k_scan_tile<<<1, kScanThreads, 0, stream>>>(in, out, count, nullptr);
+    return 1;
+  }
+  k_scan_tile<<<tiles, kScanThreads, 0, stream>>>(in, out, count, scratch);
+  const int deeper = scan_recursive(scratch, scratch, tiles, scratch + round_up64(tiles), stream);
+  k_scan_add<<<tiles, kScanThreads, 0, stream>>>(out, count, scratch);
+  return 2 + deeper;
+}
+
+__global__ void k_iota(uint32_t* out, uint32_t count) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) out[i] = i;
+}
+
+// ------------------------------------------------------------------ radix sort
+// LSD, 8-bit digits.  A block owns a tile of 4096 consecutive pairs; warp w
+// owns the w-th 512 of them and walks them 32 at a time, so the order
+// (block, warp, round, lane) is the input order and the sort is stable —
+// which is what keeps every bucket ascending by position (index.cpp:92-97).
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;
+
+__global__ void __launch_bounds__(kSortThreads)
+k_radix_histogram(const uint32_t* __restrict__ keys, uint32_t count, int shift,
+                  uint32_t* __restrict__ hist, uint32_t tiles) {
+  __shared__ uint32_t local[256];
+  local[threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t base = blockIdx.x * kSortTile;
+#pragma unroll
+  for (int k = 0; k < kSortItems; ++k) {
+    const uint32_t idx = base + k * kSortThreads + threadIdx.x;
+    if (idx < count) atomicAdd(&local[(keys[idx] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  hist[threadIdx.x * tiles + blockIdx.x] = local[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kSortThreads)
+k_radix_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
+                uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t count,
+                int shift, const uint32_t* __restrict__ scanned_hist, uint32_t tiles) {
+  __shared__ uint32_t cnt[kSortThreads / 32][256];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int w = 0; w < kSortThreads / 32; ++w) cnt[w][threadIdx.x] = 0;
+  __syncthreads();
+
+  const uint32_t base = blockIdx.x * kSortTile + warp * (32 * kSortItems);
+  uint32_t key[kSortItems], val[kSortItems], rank[kSortItems];
+#pragma unroll
+  for (int r = 0; r < kSortItems; ++r) {
+    const uint32_t idx = base + r * 32 + lane;
+    const bool valid = idx < count;
+    key[r] = valid ? keys_in[idx] : 0u;
+    val[r] = valid ? vals_in[idx] : 0u;
+    const uint32_t digit = valid ? ((key[r] >> shift) & 255u) : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(0xFFFFFFFFu, digit);
+    const uint32_t lower = __popc(peers & ((1u << lane) - 1u));
+    const uint32_t prior = valid ? cnt[warp][digit] : 0u;
+    __syncwarp();
+    if (valid && lower == 0) cnt[warp][digit] = prior + __popc(peers);
+    __syncwarp();
+    rank[r] = prior + lower;
+  }
+  __syncthreads();
+  {
+    const uint32_t digit = threadIdx.x;
+    uint32_t running = scanned_hist[digit * tiles + blockIdx.x];
+    for (int w = 0; w < kSortThreads / 32; ++w) {
+      const uint32_t c = cnt[w][digit];
+      cnt[w][digit] = running;
+      running += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kSortItems; ++r) {
+    const uint32_t idx = base + r * 32 + lane;
+    if (idx < count) {
+      const uint32_t dst = cnt[warp][(key[r] >> shift) & 255u] + rank[r];
+      keys_out[dst] = key[r];
+      vals_out[dst] = val[r];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ bucket index
+__global__ void k_mark_heads(const uint32_t* __restrict__ sorted_hash, uint32_t rows,
+                             uint32_t* __restrict__ heads) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < rows) heads[s] = (s == 0 || sorted_hash[s] != sorted_hash[s - 1]) ? 1u : 0u;
+}
+
+// heads[s] = 1 at the first slot of a bucket; slot_bucket[s] holds the
+// exclusive scan of heads on entry and the bucket id on exit.
+__global__ void k_bucket_offsets(const uint32_t* __restrict__ heads, uint32_t* slot_bucket,
+                                 uint32_t rows, uint32_t* __restrict__ offsets,
+                                 uint32_t* __restrict__ scalars) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= rows) return;
+  const uint32_t head = heads[s];
+  const uint32_t id = slot_bucket[s] + head - 1u;
+  slot_bucket[s] = id;
+  if (head) offsets[id] = s;
+  if (s == rows - 1) {
+    offsets[id + 1] = rows;
+    scalars[0] = id + 1;
+  }
+}
+
+// freq[i] = size of row i's bucket (index.cpp:51-64)
+__global__ void k_bucket_freq(const uint32_t* __restrict__ sorted_row,
+                              const uint32_t* __restrict__ slot_bucket,
+                              const uint32_t* __restrict__ offsets, uint32_t rows,
+                              uint32_t* __restrict__ freq) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= rows) return;
+  const uint32_t id = slot_bucket[s];
+  freq[sorted_row[s]] = offsets[id + 1] - offsets[id];
+}
+
+__global__ void k_count_min_freq(const uint32_t* __restrict__ sorted_freq, uint32_t rows,
+                                 uint32_t* __restrict__ scalars) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= rows) return;
+  const uint32_t lowest = sorted_freq[0];
+  if (sorted_freq[s] == lowest && (s + 1 == rows || sorted_freq[s + 1] != lowest)) scalars[1] = s + 1;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+int launch_widen_series(const float* d_in, double* d_out, size_t m, cudaStream_t stream) {
+  k_widen_series<<<blocks_for(m, 256), 256, 0, stream>>>(d_in, d_out, m);
+  return 1;
+}
+
+int launch_window_encode(const double* d_series, uint32_t rows, uint32_t n, uint32_t word_len,
+                         uint32_t alphabet, double* d_mean, double* d_inv_sigma, uint32_t* d_hash0,
+                         double* d_paa, uint32_t* d_sax, cudaStream_t stream) {
+  k_window_encode<<<blocks_for(rows, 256), 256, 0, stream>>>(d_series, rows, n, word_len, alphabet,
+                                                             d_mean, d_inv_sigma, d_hash0, d_paa,
+                                                             d_sax);
+  return 1;
+}
+
+int launch_build_rows(const double* d_series, const double* d_mean, const double* d_inv_sigma,
+                      uint32_t rows, uint32_t n, uint32_t stride, float* d_rows,
+                      cudaStream_t stream) {
+  const size_t threads = static_cast<size_t>(rows) * (stride / 4);
+  k_build_rows<<<blocks_for(threads, 256), 256, 0, stream>>>(d_series, d_mean, d_inv_sigma, rows, n,
+                                                             stride, d_rows);
+  return 1;
+}
+
+size_t scan_scratch_words(uint32_t count) {
+  size_t words = 64;
+  size_t level = count;
+  while (level > static_cast<size_t>(kScanTile)) {
+    level = (level + kScanTile - 1) / kScanTile;
+    words += round_up64(level);
+  }
+  return words;
+}
+
+int launch_exclusive_scan(const uint32_t* d_in, uint32_t* d_out, uint32_t count,
+                          uint32_t* d_scratch, cudaStream_t stream) {
+  if (count == 0) return 0;
+  return scan_recursive(d_in, d_out, count, d_scratch, stream);
+}
+
+int launch_iota(uint32_t* d_out, uint32_t count, cudaStream_t stream) {
+  k_iota<<<blocks_for(count, 256), 256, 0, stream>>>(d_out, count);
+  return 1;
+}
+
+size_t radix_sort_scratch_words(uint32_t count) {
+  const size_t tiles = (static_cast<size_t>(count) + kSortTile - 1) / kSortTile;
+  return 256 * tiles;
+}
+
+int launch_radix_sort_pairs(uint32_t** keys, uint32_t** vals, uint32_t** keys_alt,
+                            uint32_t** vals_alt, uint32_t count, int key_bits, uint32_t* d_hist,
+                            uint32_t* d_scan_scratch, cudaStream_t stream) {
+  if (count == 0) return 0;
+  const uint32_t tiles = (count + kSortTile - 1) / kSortTile;
+  int passes = (key_bits + 7) / 8;
+  if (passes < 1) passes = 1;
+  if (passes > 4) passes = 4;
+  int launches = 0;
+  for (int pass = 0; pass < passes; ++pass) {
+    const int shift = pass * 8;
+    k_radix_histogram<<<tiles, kSortThreads, 0, stream>>>(*keys, count, shift, d_hist, tiles);
+    launches += 1 + launch_exclusive_scan(d_hist, d_hist, 256 * tiles, d_scan_scratch, stream);
+    k_radix_scatter<<<tiles, kSortThreads, 0, stream>>>(*keys, *vals, *keys_alt, *vals_alt, count,
+                                                        shift, d_hist, tiles);
+    launches += 1;
+    uint32_t* t = *keys;
+    *keys = *keys_alt;
+    *keys_alt = t;
+    t = *vals;
+    *vals = *vals_alt;
+    *vals_alt = t;
+  }
+  return launches;
+}
+
+int launch_bucket_index(const uint32_t* d_sorted_hash, const uint32_t* d_sorted_row, uint32_t rows,
+                        uint32_t* d_head_scan, uint32_t* d_slot_bucket, uint32_t* d_offsets,
+                        uint32_t* d_freq, uint32_t* d_scalars, uint32_t* d_scan_scratch,
+                        cudaStream_t stream) {
+  const unsigned blocks = blocks_for(rows, 256);
+  k_mark_heads<<<blocks, 256, 0, stream>>>(d_sorted_hash, rows, d_head_scan);
+  int launches = 1 + launch_exclusive_scan(d_head_scan, d_slot_bucket, rows, d_scan_scratch, stream);
+  k_bucket_offsets<<<blocks, 256, 0, stream>>>(d_head_scan, d_slot_bucket, rows, d_offsets, d_scalars);
+  k_bucket_freq<<<blocks, 256, 0, stream>>>(d_sorted_row, d_slot_bucket, d_offsets, rows, d_freq);
+  return launches + 2;
+}
+
+int launch_count_min_freq(const uint32_t* d_sorted_freq, uint32_t rows, uint32_t* d_scalars,
+                          cudaStream_t stream) {
+  k_count_min_freq<<<blocks_for(rows, 256), 256, 0, stream>>>(d_sorted_freq, rows, d_scalars);
+  return 1;
+}
+
+}  // namespace tsdd_b200

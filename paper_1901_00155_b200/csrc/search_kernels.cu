@@ -1,0 +1,645 @@
+// Search stage on the device (replaces phidd_discord, src/discovery.cpp:209-373).
+//
+// State per row i (SearchState): nn[i] — a packed (distance^2, neighbour) key
+// that only ever decreases (integer atomicMin), so its distance is always an
+// upper bound of row i's nearest-neighbour distance; exact[i] once a complete
+// scan of every non-self neighbour has finished; and one packed best-so-far
+// key that only ever increases (atomicMax).  A row whose upper bound cannot
+// beat the best-so-far is dead — the HOTSAX discard (discovery.cpp:58,70).
+//
+// Exactness rests on the reference's own invariants (discovery.cpp:36-40):
+//  * the in-row abandon threshold is the row's running minimum, never the
+//    best-so-far (discovery.cpp:55,67): an abandoned pair is strictly above it
+//    and can change neither the minimum nor the discard decision;
+//  * a stale (smaller) best-so-far prunes less, never more (discovery.hpp:34-36);
+//  * all comparisons are strict.
+
+#include "kernels.hpp"
+
+namespace tsdd_b200 {
+
+namespace {
+
+inline unsigned blocks_for(size_t items, unsigned per_block) {
+  return static_cast<unsigned>((items + per_block - 1) / per_block);
+}
+
+__device__ __forceinline__ uint32_t gap_u32(uint32_t a, uint32_t b) { return a > b ? a - b : b - a; }
+
+__device__ __forceinline__ uint64_t load_key(const uint64_t* p) {
+  // nn keys are raced on by design (atomicMin from other CTAs); read through L2.
+  return __ldcg(reinterpret_cast<const unsigned long long*>(p));
+}
+
+// ------------------------------------------------------------------ reset / bookkeeping
+__global__ void k_reset_search(SearchState s) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < s.n_rows) {
+    s.nn[i] = kNnUnset;
+    s.exact[i] = 0;
+    s.excluded[i] = 0;
+  }
+  if (i == 0) {
+    *s.best = 0;
+    *s.counters = DeviceCounters{0, 0, 0, 0, 0};
+  }
+}
+
+__global__ void k_exclude_zone(SearchState s, uint32_t row) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;  // 0 .. 2n-2
+  const uint32_t lo = row >= s.n - 1 ? row - (s.n - 1) : 0;
+  const uint32_t i = lo + t;
+  if (i < s.n_rows && i <= row + (s.n - 1)) s.excluded[i] = 1;
+}
+
+// best = max over rows that are exact, allowed and have a finite nn.
+__global__ void __launch_bounds__(256) k_seed_best(SearchState s) {
+  uint64_t mine = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < s.n_rows; i += gridDim.x * blockDim.x) {
+    if (s.exact[i] && !s.excluded[i]) {
+      const uint32_t bits = key_bits(s.nn[i]);
+      if (bits != kInfBits) {
+        const uint64_t k = best_key(bits, i);
+        mine = k > mine ? k : mine;
+      }
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const uint64_t other = __shfl_xor_sync(0xFFFFFFFFu, mine, d);
+    mine = other > mine ? other : mine;
+  }
+  if ((threadIdx.x & 31) == 0 && mine) atomicMax(as_ull(s.best), static_cast<unsigned long long>(mine));
+}
+
+// ------------------------------------------------------------------ same-word neighbours
+// One warp per slot of the hash-sorted order.  The row is measured against up
+// to `mates` rows spread evenly over its own bucket (positions at least n
+// apart); every completed distance lowers the bound of BOTH rows, d(i,j) =
+// d(j,i).  Lanes stride over the row with float4 loads (512 contiguous bytes
+// per warp per step); the sum is folded with warp shuffles.
+__global__ void __launch_bounds__(256)
+k_bucket_mates(SearchState s, const uint32_t* __restrict__ sorted_row,
+               const uint32_t* __restrict__ slot_bucket, const uint32_t* __restrict__ offsets,
+               int mates) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (slot >= s.n_rows) return;
+  const uint32_t bucket = slot_bucket[slot];
+  const uint32_t b0 = offsets[bucket], b1 = offsets[bucket + 1];
+  const uint32_t len = b1 - b0;
+  if (len < 2) return;
+  const uint32_t row_i = sorted_row[slot];
+  const float4* pi = reinterpret_cast<const float4*>(s.rows + static_cast<size_t>(row_i) * s.stride);
+  const uint32_t quads = s.stride / 4;
+  uint32_t tries = static_cast<uint32_t>(mates);
+  uint32_t step = len / (tries + 1);
+  if (step == 0) {
+    step = 1;
+    tries = len - 1;
+  }
+  unsigned long long calls = 0, terms = 0;
+  for (uint32_t q = 1; q <= tries; ++q) {
+    const uint32_t other = b0 + (slot - b0 + q * step) % len;
+    const uint32_t row_j = sorted_row[other];
+    if (gap_u32(row_i, row_j) < s.n) continue;
+    const float4* pj = reinterpret_cast<const float4*>(s.rows + static_cast<size_t>(row_j) * s.stride);
+    float sum = 0.f;
+    for (uint32_t c = lane; c < quads; c += 32) {
+      const float4 a = pi[c], b = __ldg(pj + c);
+      const float dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z, dw = a.w - b.w;
+      sum = fmaf(dx, dx, sum);
+      sum = fmaf(dy, dy, sum);
+      sum = fmaf(dz, dz, sum);
+      sum = fmaf(dw, dw, sum);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, d);
+    if (lane == 0) {
+      const uint32_t bits = __float_as_uint(sum);
+      atomicMin(as_ull(s.nn + row_i), static_cast<unsigned long long>(nn_key(bits, row_j)));
+      atomicMin(as_ull(s.nn + row_j), static_cast<unsigned long long>(nn_key(bits, row_i)));
+      calls += 1;
+      terms += s.stride;
+    }
+  }
+  if (lane == 0 && calls) {
+    atomicAdd(&s.counters->calls, calls);
+    atomicAdd(&s.counters->terms, terms);
+  }
+}
+
+// ------------------------------------------------------------------ batch selection
+// flags[e - cursor] = 1 when entry e of the rarity order is this rank's and
+// its row can still beat the best-so-far.
+__global__ void k_flag_live(SearchState s, const uint32_t* __restrict__ order, uint32_t cursor,
+                            uint32_t world, uint32_t rank, int pruning, uint32_t* __restrict__ flags) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t e = cursor + t;
+  if (e >= s.n_rows) return;
+  const uint32_t row = order[e];
+  bool live = (e % world == rank) && !s.excluded[row] && !s.exact[row];
+  if (live && pruning) live = !is_dead(s.nn[row], row, *s.best);
+  flags[t] = live ? 1u : 0u;
+}
+
+// ranks[] is the exclusive scan of flags[].  The first `batch` live entries
+// become the batch; sel[0] = batch size, sel[1] = cursor after the last one taken.
+__global__ void k_take_batch(const uint32_t* __restrict__ order, const uint32_t* __restrict__ flags,
+                             const uint32_t* __restrict__ ranks, uint32_t cursor, uint32_t n_rows,
+                             uint32_t batch, uint32_t* __restrict__ batch_rows,
+                             uint32_t* __restrict__ sel) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t e = cursor + t;
+  if (e >= n_rows) return;
+  const uint32_t f = flags[t], r = ranks[t];
+  if (f && r < batch) {
+    batch_rows[r] = order[e];
+    if (r == batch - 1) sel[1] = e + 1;
+  }
+  if (e == n_rows - 1) {
+    const uint32_t live = r + f;
+    sel[0] = live < batch ? live : batch;
+    if (live < batch) sel[1] = n_rows;
+  }
+}
+
+// Stable in-place compaction of the batch list (a single block; a batch is a
+// few thousand rows).  sel[0] is read and rewritten.
+__global__ void __launch_bounds__(1024)
+k_compact_batch(SearchState s, const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                int pruning, uint32_t* sel) {
+  __shared__ uint32_t warp_sums[32];
+  __shared__ uint32_t carry;
+  const uint32_t count = sel[0];
+  const uint64_t best = *s.best;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < count; base += blockDim.x) {
+    const uint32_t idx = base + threadIdx.x;
+    uint32_t row = 0;
+    bool keep = false;
+    if (idx < count) {
+      row = in[idx];
+      keep = !pruning || !is_dead(load_key(s.nn + row), row, best);
+    }
+    const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, keep);
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) warp_sums[warp] = __popc(ballot);
+    __syncthreads();
+    uint32_t before = carry, total = 0;
+    for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+      const uint32_t c = warp_sums[w];
+      if (w < warp) before += c;
+      total += c;
+    }
+    if (keep) out[before + __popc(ballot & ((1u << lane) - 1u))] = row;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sel[0] = carry;
+}
+
+// Dense copy of the batch's rows, NEGATED, so that the tile kernel forms
+// x - y as one add (and, packed, one add.f32x2).  Rows past the batch size
+// are zero.  One warp per row.
+__global__ void __launch_bounds__(256)
+k_gather_rows(SearchState s, const uint32_t* __restrict__ batch_rows, const uint32_t* __restrict__ sel,
+              uint32_t capacity_padded, float* __restrict__ out) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= capacity_padded) return;
+  const uint32_t count = sel[0];
+  // only the tiles the scan will touch need refreshing
+  if (r >= (count + kTileRows - 1) / kTileRows * kTileRows) return;
+  float4* dst = reinterpret_cast<float4*>(out + static_cast<size_t>(r) * s.stride);
+  const uint32_t quads = s.stride / 4;
+  if (r < count) {
+    const float4* src =
+        reinterpret_cast<const float4*>(s.rows + static_cast<size_t>(batch_rows[r]) * s.stride);
+    for (uint32_t c = lane; c < quads; c += 32) {
+      const float4 v = __ldg(src + c);
+      dst[c] = make_float4(-v.x, -v.y, -v.z, -v.w);
+    }
+  } else {
+    for (uint32_t c = lane; c < quads; c += 32) dst[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// Rows of the batch that are still live after every neighbour range has been
+// scanned have met all their non-self neighbours: nn is exact.  Each raises
+// the best-so-far (warp-shuffle max, then one atomicMax per warp).
+__global__ void __launch_bounds__(256)
+k_finalize_batch(SearchState s, const uint32_t* __restrict__ batch_rows,
+                 const uint32_t* __restrict__ sel, int pruning) {
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t count = sel[0];
+  const uint64_t best = *s.best;  // constant for the whole batch: only this kernel raises it
+  uint64_t mine = 0;
+  if (idx < count) {
+    const uint32_t row = batch_rows[idx];
+    const uint64_t key = s.nn[row];
+    if (!pruning || !is_dead(key, row, best)) {
+      s.exact[row] = 1;
+      if (key_bits(key) != kInfBits) mine = best_key(key_bits(key), row);
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const uint64_t other = __shfl_xor_sync(0xFFFFFFFFu, mine, d);
+    mine = other > mine ? other : mine;
+  }
+  if ((threadIdx.x & 31) == 0 && mine > best)
+    atomicMax(as_ull(s.best), static_cast<unsigned long long>(mine));
+}
+
+// ------------------------------------------------------------------ the tiled distance kernel
+//
+// CTA = 256 threads = one tile of 128 candidates x 128 neighbour rows; thread
+// (ty, tx) of a 16 x 16 grid owns the 8 x 8 pairs {ty + 16u} x {tx + 16v}.
+// Columns stream through shared memory 32 at a time (one 128-byte line per
+// row and stage) in a kStages-deep cp.async ring; the 16-byte pieces of a line
+// are XOR-swizzled with the row number so that the float4 reads of 16 rows in
+// a half-warp are conflict-free.  Candidate rows arrive negated (k_gather_rows),
+// so a term is one add and one fma — packed two columns at a time as
+// add.f32x2 / fma.rn.f32x2 in the kPacked variant.
+//
+// Early abandoning (series.hpp:117-146 on a tile): after every 32 columns a
+// thread checks whether all of its 64 partial sums already exceed their
+// candidates' running minimum; a warp whose pairs have all abandoned stops
+// computing, and the CTA leaves the tile when every warp has.  Dead candidates
+// carry the threshold -1 and never hold a tile open.
+constexpr int kStages = 4;
+constexpr int kOperandBytes = kTileRows * kChunk * 4;  // 16 KiB: 128 rows x 32 columns
+constexpr int kStageBytes = 2 * kOperandBytes;
+constexpr int kScanThreads = 256;
+constexpr size_t kScanSmem = static_cast<size_t>(kStages) * kStageBytes + 3 * kTileRows * 4;
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(gmem_src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int kPending>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(kPending));
+}
+
+// Issues this thread's share (4 + 4 pieces of 16 bytes) of one stage.
+__device__ __forceinline__ void issue_stage(unsigned char* stage, const float* a_tile,
+                                            const float* b_tile, uint32_t stride, uint32_t col0) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t piece = threadIdx.x + q * kScanThreads;  // 0..1023
+    const uint32_t r = piece >> 3, kc = piece & 7;
+    const uint32_t off = r * 128 + ((kc ^ (r & 7)) << 4);
+    cp_async16(stage + off, a_tile + static_cast<size_t>(r) * stride + col0 + kc * 4);
+    cp_async16(stage + kOperandBytes + off, b_tile + static_cast<size_t>(r) * stride + col0 + kc * 4);
+  }
+}
+
+template <bool kPacked>
+struct Acc;
+template <>
+struct Acc<false> {
+  float v[8][8];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int w = 0; w < 8; ++w) v[u][w] = 0.f;
+  }
+  __device__ __forceinline__ float get(int u, int w) const { return v[u][w]; }
+  __device__ __forceinline__ void add(int u, int w, const float4& na, const float4& b) {
+    float d = b.x + na.x;
+    v[u][w] = fmaf(d, d, v[u][w]);
+    d = b.y + na.y;
+    v[u][w] = fmaf(d, d, v[u][w]);
+    d = b.z + na.z;
+    v[u][w] = fmaf(d, d, v[u][w]);
+    d = b.w + na.w;
+    v[u][w] = fmaf(d, d, v[u][w]);
+  }
+};
+template <>
+struct Acc<true> {
+  float2 v[8][8];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+#pragma unroll
+      for (int w = 0; w < 8; ++w) v[u][w] = make_float2(0.f, 0.f);
+  }
+  __device__ __forceinline__ float get(int u, int w) const { return v[u][w].x + v[u][w].y; }
+  __device__ __forceinline__ void add(int u, int w, const float4& na, const float4& b) {
+    float2 d = __fadd2_rn(make_float2(b.x, b.y), make_float2(na.x, na.y));
+    v[u][w] = __ffma2_rn(d, d, v[u][w]);
+    d = __fadd2_rn(make_float2(b.z, b.w), make_float2(na.z, na.w));
+    v[u][w] = __ffma2_rn(d, d, v[u][w]);
+  }
+};
+
+template <bool kPacked, bool kSymmetric>
+__global__ void __launch_bounds__(kScanThreads, 1)
+k_scan_tiles(SearchState s, const float* __restrict__ batch, const uint32_t* __restrict__ batch_rows,
+             const uint32_t* __restrict__ sel, uint32_t j_begin, uint32_t j_end, int tiles_per_cta,
+             int pruning) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  float* s_thr = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // candidate thresholds
+  uint32_t* s_cand = reinterpret_cast<uint32_t*>(s_thr + kTileRows);      // candidate rows
+  float* s_nub = reinterpret_cast<float*>(s_cand + kTileRows);            // neighbours' own bounds
+  __shared__ unsigned long long s_calls, s_abandoned, s_terms;
+
+  const uint32_t count = sel[0];
+  const uint32_t cand0 = blockIdx.y * kTileRows;
+  if (cand0 >= count) return;
+
+  const uint32_t tid = threadIdx.x, lane = tid & 31;
+  const uint32_t tx = tid & 15, ty = tid >> 4;
+  if (tid < kTileRows) s_cand[tid] = (cand0 + tid < count) ? batch_rows[cand0 + tid] : 0xFFFFFFFFu;
+  if (tid == 0) {
+    s_calls = 0;
+    s_abandoned = 0;
+    s_terms = 0;
+  }
+  const uint64_t best = pruning ? *s.best : 0ull;
+  const uint32_t chunks = s.stride / kChunk;
+  const float* a_tile = batch + static_cast<size_t>(cand0) * s.stride;
+  const uint32_t first_tile = j_begin / kTileRows + blockIdx.x * tiles_per_cta;
+  const float inf = __uint_as_float(kInfBits);
+
+  for (int tt = 0; tt < tiles_per_cta; ++tt) {
+    const uint32_t j0 = (first_tile + tt) * kTileRows;
+    if (j0 >= j_end) break;
+    __syncthreads();  // s_cand visible; everyone is done with the previous tile's s_thr / stages
+
+    // ---- refresh thresholds, count the pairs this tile starts
+    bool live = false;
+    if (tid < kTileRows) {
+      const uint32_t row = s_cand[tid];
+      float thr = -1.f;
+      if (row != 0xFFFFFFFFu) {
+        if (!pruning) {
+          thr = inf;
+          live = true;
+        } else {
+          const uint64_t key = load_key(s.nn + row);
+          if (!is_dead(key, row, best)) {
+            thr = __uint_as_float(key_bits(key));
+            live = true;
+          }
+        }
+      }
+      s_thr[tid] = thr;
+    } else {
+      const uint32_t j = j0 + (tid - kTileRows);
+      s_nub[tid - kTileRows] = (j < s.n_rows && j < j_end) ? __uint_as_float(key_bits(load_key(s.nn + j))) : -1.f;
+    }
+    if (!__syncthreads_or(live)) break;  // every candidate of this tile is dead: nothing left to do
+
+    unsigned long long my_calls = 0;
+    if (live) {
+      const uint32_t row = s_cand[tid];
+      const uint32_t j1 = min(min(j0 + kTileRows, s.n_rows), j_end);  // exclusive
+      // neighbours of this tile inside the self-match zone (row - n, row + n)
+      const uint32_t z0 = row >= s.n - 1 ? row - (s.n - 1) : 0;
+      const uint32_t z1 = row + s.n;  // exclusive
+      const uint32_t o0 = max(j0, z0), o1 = min(j1, z1);
+      my_calls = (j1 - j0) - (o1 > o0 ? o1 - o0 : 0);
+    }
+
+    float thr[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) thr[u] = s_thr[ty + 16 * u];
+
+    Acc<kPacked> acc;
+    acc.zero();
+
+    const float* b_tile = s.rows + static_cast<size_t>(j0) * s.stride;
+#pragma unroll
+    for (int st = 0; st < kStages - 1; ++st) {
+      if (static_cast<uint32_t>(st) < chunks) issue_stage(smem + st * kStageBytes, a_tile, b_tile, s.stride, st * kChunk);
+      cp_async_commit();
+    }
+
+    bool mine_abandoned = false, warp_done = false, cta_abandoned = false;
+    uint32_t warp_chunks = 0;
+    for (uint32_t c = 0; c < chunks; ++c) {
+      cp_async_wait<kStages - 2>();
+      if (__syncthreads_and(mine_abandoned)) {
+        cta_abandoned = true;
+        break;
+      }
+      if (c + kStages - 1 < chunks)
+        issue_stage(smem + ((c + kStages - 1) % kStages) * kStageBytes, a_tile, b_tile, s.stride,
+                    (c + kStages - 1) * kChunk);
+      cp_async_commit();
+      if (!warp_done) {
+        const unsigned char* a_s = smem + (c % kStages) * kStageBytes + ty * 128;
+        const unsigned char* b_s = smem + (c % kStages) * kStageBytes + kOperandBytes + tx * 128;
+#pragma unroll 2
+        for (int kc = 0; kc < 8; ++kc) {
+          const uint32_t off_a = (kc ^ (ty & 7)) << 4, off_b = (kc ^ (tx & 7)) << 4;
+          float4 na[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) na[u] = *reinterpret_cast<const float4*>(a_s + u * 2048 + off_a);
+#pragma unroll
+          for (int w = 0; w < 8; ++w) {
+            const float4 b = *reinterpret_cast<const float4*>(b_s + w * 2048 + off_b);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc.add(u, w, na[u], b);
+          }
+        }
+        ++warp_chunks;
+        bool all_over = true;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int w = 0; w < 8; ++w) all_over = all_over && (acc.get(u, w) > thr[u]);
+        mine_abandoned = all_over;
+        warp_done = __all_sync(0xFFFFFFFFu, all_over);
+      }
+    }
+    cp_async_wait<0>();
+
+    // ---- accounting (per warp: the terms its lanes really accumulated)
+    if (lane == 0) atomicAdd(&s_terms, static_cast<unsigned long long>(warp_chunks) * kChunk * 16 * kTileRows);
+    if (my_calls) {
+      atomicAdd(&s_calls, my_calls);
+      if (cta_abandoned) atomicAdd(&s_abandoned, my_calls);
+    }
+    if (cta_abandoned) continue;
+
+    // ---- completed tile: lower the candidates' bounds (and, symmetric, the neighbours')
+    const bool complete = (warp_chunks == chunks);
+    uint64_t cand_best[8];
+    bool any_update = false;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      cand_best[u] = ~0ull;
+      const uint32_t row = s_cand[ty + 16 * u];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        const uint32_t j = j0 + tx + 16 * w;
+        const float d = acc.get(u, w);
+        const bool pair_ok = row != 0xFFFFFFFFu && j < s.n_rows && j < j_end && gap_u32(row, j) >= s.n;
+        if (pair_ok && d <= thr[u]) {
+          const uint64_t k = nn_key(__float_as_uint(d), j);
+          cand_best[u] = k < cand_best[u] ? k : cand_best[u];
+          any_update = true;
+        }
+        if (kSymmetric && complete && pair_ok && d < s_nub[tx + 16 * w])
+          atomicMin(as_ull(s.nn + j), static_cast<unsigned long long>(nn_key(__float_as_uint(d), row)));
+      }
+    }
+    if (__any_sync(0xFFFFFFFFu, any_update)) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        uint64_t k = cand_best[u];
+#pragma unroll
+        for (int d = 8; d > 0; d >>= 1) {
+          const uint64_t other = __shfl_xor_sync(0xFFFFFFFFu, k, d);
+          k = other < k ? other : k;
+        }
+        if (tx == 0 && k != ~0ull)
+          atomicMin(as_ull(s.nn + s_cand[ty + 16 * u]), static_cast<unsigned long long>(k));
+      }
+    }
+  }
+
+  __syncthreads();
+  if (tid == 0) {
+    if (s_calls) atomicAdd(&s.counters->calls, s_calls);
+    if (s_abandoned) atomicAdd(&s.counters->abandoned, s_abandoned);
+    if (s_terms) {
+      atomicAdd(&s.counters->terms, s_terms);
+      atomicAdd(&s.counters->tile_terms, s_terms);
+    }
+  }
+}
+
+// float64 distance of one pair straight from the series (finalists only).
+__global__ void __launch_bounds__(256)
+k_rescore_pair(const double* __restrict__ x, const double* __restrict__ mean,
+               const double* __restrict__ inv_sigma, uint32_t n, uint32_t row_a, uint32_t row_b,
+               double* out) {
+  __shared__ double partial[256];
+  const double ma = mean[row_a], ia = inv_sigma[row_a], mb = mean[row_b], ib = inv_sigma[row_b];
+  double sum = 0.0;
+  for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
+    const double d = (x[row_a + t] - ma) * ia - (x[row_b + t] - mb) * ib;
+    sum += d * d;
+  }
+  partial[threadIdx.x] = sum;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) partial[threadIdx.x] += partial[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = partial[0];
+}
+
+bool g_packed_default = true;
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+int launch_reset_search(SearchState s, cudaStream_t stream) {
+  k_reset_search<<<blocks_for(s.n_rows, 256), 256, 0, stream>>>(s);
+  return 1;
+}
+
+int launch_bucket_mates(SearchState s, const uint32_t* d_sorted_row, const uint32_t* d_slot_bucket,
+                        const uint32_t* d_offsets, int mates, cudaStream_t stream) {
+  if (mates <= 0) return 0;
+  k_bucket_mates<<<blocks_for(static_cast<size_t>(s.n_rows) * 32, 256), 256, 0, stream>>>(
+      s, d_sorted_row, d_slot_bucket, d_offsets, mates);
+  return 1;
+}
+
+int launch_select_batch(SearchState s, const uint32_t* d_order, uint32_t cursor, uint32_t batch,
+                        uint32_t world, uint32_t rank, bool pruning, uint32_t* d_flags,
+                        uint32_t* d_scan_scratch, uint32_t* d_batch_rows, uint32_t* d_sel,
+                        cudaStream_t stream) {
+  const uint32_t span = s.n_rows - cursor;
+  const unsigned blocks = blocks_for(span, 256);
+  k_flag_live<<<blocks, 256, 0, stream>>>(s, d_order, cursor, world, rank, pruning ? 1 : 0, d_flags);
+  // ranks live right behind the flags
+  uint32_t* d_ranks = d_flags + s.n_rows;
+  int launches = 1 + launch_exclusive_scan(d_flags, d_ranks, span, d_scan_scratch, stream);
+  k_take_batch<<<blocks, 256, 0, stream>>>(d_order, d_flags, d_ranks, cursor, s.n_rows, batch,
+                                           d_batch_rows, d_sel);
+  return launches + 1;
+}
+
+int launch_compact_batch(SearchState s, uint32_t* d_batch_rows, uint32_t* d_batch_alt,
+                         uint32_t capacity, bool pruning, uint32_t* d_sel, cudaStream_t stream) {
+  (void)capacity;
+  k_compact_batch<<<1, 1024, 0, stream>>>(s, d_batch_rows, d_batch_alt, pruning ? 1 : 0, d_sel);
+  return 1;
+}
+
+int launch_gather_rows(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,
+                       uint32_t capacity_padded, float* d_batch_matrix, cudaStream_t stream) {
+  k_gather_rows<<<blocks_for(static_cast<size_t>(capacity_padded) * 32, 256), 256, 0, stream>>>(
+      s, d_batch_rows, d_sel, capacity_padded, d_batch_matrix);
+  return 1;
+}
+
+int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t* d_batch_rows,
+                      const uint32_t* d_sel, uint32_t capacity_padded, uint32_t j_begin,
+                      uint32_t j_end, int tiles_per_cta, bool pruning, bool symmetric,
+                      cudaStream_t stream) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_scan_tiles<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kScanSmem));
+    cudaFuncSetAttribute(k_scan_tiles<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kScanSmem));
+    cudaFuncSetAttribute(k_scan_tiles<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kScanSmem));
+    cudaFuncSetAttribute(k_scan_tiles<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kScanSmem));
+    configured = true;
+  }
+  if (j_end <= j_begin) return 0;
+  const uint32_t tiles = (j_end - j_begin + kTileRows - 1) / kTileRows;
+  dim3 grid((tiles + tiles_per_cta - 1) / tiles_per_cta, capacity_padded / kTileRows);
+  const int p = pruning ? 1 : 0;
+  if (g_packed_default) {
+    if (symmetric)
+      k_scan_tiles<true, true><<<grid, kScanThreads, kScanSmem, stream>>>(s, d_batch_matrix, d_batch_rows, d_sel, j_begin, j_end, tiles_per_cta, p);
+    else
+      k_scan_tiles<true, false><<<grid, kScanThreads, kScanSmem, stream>>>(s, d_batch_matrix, d_batch_rows, d_sel, j_begin, j_end, tiles_per_cta, p);
+  } else {
+    if (symmetric)
+      k_scan_tiles<false, true><<<grid, kScanThreads, kScanSmem, stream>>>(s, d_batch_matrix, d_batch_rows, d_sel, j_begin, j_end, tiles_per_cta, p);
+    else
+      k_scan_tiles<false, false><<<grid, kScanThreads, kScanSmem, stream>>>(s, d_batch_matrix, d_batch_rows, d_sel, j_begin, j_end, tiles_per_cta, p);
+  }
+  return 1;
+}
+
+void set_packed_math(bool on) { g_packed_default = on; }
+
+int launch_finalize_batch(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,
+                          uint32_t capacity, bool pruning, cudaStream_t stream) {
+  k_finalize_batch<<<blocks_for(capacity, 256), 256, 0, stream>>>(s, d_batch_rows, d_sel, pruning ? 1 : 0);
+  return 1;
+}
+
+int launch_seed_best(SearchState s, cudaStream_t stream) {
+  k_seed_best<<<296, 256, 0, stream>>>(s);
+  return 1;
+}
+
+int launch_exclude_zone(SearchState s, uint32_t row, cudaStream_t stream) {
+  k_exclude_zone<<<blocks_for(2 * static_cast<size_t>(s.n), 256), 256, 0, stream>>>(s, row);
+  return 1;
+}
+
+int launch_rescore_pair(const double* d_series, const double* d_mean, const double* d_inv_sigma,
+                        uint32_t n, uint32_t row_a, uint32_t row_b, double* d_out,
+                        cudaStream_t stream) {
+  k_rescore_pair<<<1, 256, 0, stream>>>(d_series, d_mean, d_inv_sigma, n, row_a, row_b, d_out);
+  return 1;
+}
+
+}  // namespace tsdd_b200

@@ -1,0 +1,277 @@
+"""Parity of the CUDA path against the CPU oracle, through the C ABI (libtsdd_cuda.so).
+
+Bars (BASELINE.json north_star): discord positions identical, distances within 1e-4
+relative (float32 kernels vs. the float64 reference); every integer array of the
+preparation stage (symbols, hashes, frequencies, candidate set, buckets) identical.
+The oracle is the unmodified reference when oracle/_ref is present, else the pinned C
+restatement (tests/test_oracle_pin.py).
+"""
+import threading
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1901_00155_b200 import (Context, DiscoveryConfig, InfeasibleInputError, run_discovery,
+                                   workloads as W)
+
+pytestmark = pytest.mark.gpu
+
+DIST_RTOL = 1e-4  # north_star: "discord distances must agree to 1e-4 relative"
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = Context(0)
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def chk():
+    return oracle.best()
+
+
+def planted_walk(seed, m, n):
+    x = W.random_walk(seed, m)
+    at = m // 3
+    x[at:at + n] += np.float32(2.5) * np.sin(np.arange(n, dtype=np.float32) * 0.7)
+    return x
+
+
+# ------------------------------------------------------------------ preparation stage
+@pytest.mark.parametrize("m,n,w,a", [(3000, 64, 4, 4), (2500, 50, 3, 5), (4000, 128, 8, 6),
+                                     (1500, 33, 7, 10), (5000, 96, 16, 2), (700, 8, 8, 2)])
+def test_preparation_arrays_match_the_reference(ctx, chk, m, n, w, a):
+    x = W.random_walk(100 + n, m)
+    ctx.prepare(x, n, w, a)
+    ref = chk.prepare(x, n, w, a)
+    N = m - n + 1
+    rows = ctx.fetch("rows")
+    assert rows.shape == (N, ctx.row_stride()) and ctx.row_stride() % 32 == 0
+    # float32 rounding of the float64 rows; padding columns are exactly zero (series.cpp:64-72)
+    np.testing.assert_allclose(rows[:, :n], ref["rows"], rtol=0, atol=2e-6)
+    assert not rows[:, n:].any()
+    np.testing.assert_allclose(ctx.fetch("paa"), ref["paa"], rtol=0, atol=1e-9)
+    sax = ctx.fetch("sax")
+    flips = sax != ref["sax"]
+    assert not flips.any(), f"{flips.sum()} SAX symbols differ"
+    np.testing.assert_array_equal(ctx.fetch("hash"), ref["hashes"])
+    np.testing.assert_array_equal(ctx.fetch("freq"), ref["freq"])
+    np.testing.assert_array_equal(ctx.fetch("candidates"), ref["candidates"])
+    np.testing.assert_array_equal(ctx.fetch("buckets"), ref["bucket_positions"])
+    # rarity order: a permutation, ascending frequency, ties by position (SURVEY gap G4)
+    order = ctx.fetch("order").astype(np.int64) - 1
+    assert sorted(order) == list(range(N))
+    f = ref["freq"][order].astype(np.int64)
+    assert np.all(np.diff(f) >= 0)
+    assert np.all(np.diff(order)[np.diff(f) == 0] > 0)
+    st = ctx.stats()
+    assert st["rows"] == N and st["buckets"] == len(np.unique(ref["hashes"]))
+    assert st["min_freq_candidates"] == len(ref["candidates"])
+
+
+def test_flat_windows_become_zero_rows(ctx, chk):
+    x = W.random_walk(5, 2000)
+    x[500:700] = np.float32(1.25)  # constant stretch: sigma < 1e-12 -> all-zero rows (series.cpp:30-33)
+    ctx.prepare(x, 64, 4, 4)
+    ref = chk.prepare(x, 64, 4, 4)
+    rows = ctx.fetch("rows")[:, :64]
+    zero_ref = ~ref["rows"].any(axis=1)
+    assert zero_ref.sum() >= 100
+    np.testing.assert_array_equal(~rows.any(axis=1), zero_ref)
+    np.testing.assert_array_equal(ctx.fetch("hash"), ref["hashes"])
+
+
+def test_float64_series_is_accepted(ctx, chk):
+    x = W.random_walk(21, 3000).astype(np.float64) * 1.000000123  # not float32-representable
+    ctx.prepare(x, 64, 4, 4)
+    ref = chk.prepare(x, 64, 4, 4)
+    np.testing.assert_array_equal(ctx.fetch("hash"), ref["hashes"])
+    pos, dist = ctx.search(1)
+    want = chk.run_discovery(x, 64, 4, 4, engine="brute")
+    assert pos[0] == want["position"] and dist[0] == pytest.approx(want["distance"], rel=DIST_RTOL)
+
+
+# ------------------------------------------------------------------ search stage
+@pytest.mark.parametrize("n", [32, 64, 128])
+@pytest.mark.parametrize("seed", range(8))
+def test_top1_matches_brute_force_oracle(ctx, chk, seed, n):  # SPEC.md:449-451 sweep family
+    x = W.random_walk(1000 + seed, 2000)
+    ctx.prepare(x, n, 4, 4)
+    pos, dist = ctx.search(1)
+    want = chk.run_discovery(x, n, 4, 4, engine="brute")
+    assert pos[0] == want["position"]
+    assert dist[0] == pytest.approx(want["distance"], rel=DIST_RTOL)
+    st = ctx.stats()
+    assert st["scan_kernel_launches"] > 0 and st["terms"] > 0 and st["calls"] >= st["abandoned"]
+
+
+@pytest.mark.parametrize("n,w,a", [(50, 3, 5), (100, 7, 3), (200, 10, 4)])
+def test_ragged_shapes(ctx, chk, n, w, a):  # n not a multiple of 32, w does not divide n
+    x = planted_walk(77 + n, 6000, n)
+    ctx.prepare(x, n, w, a)
+    pos, dist = ctx.search(1)
+    want = chk.run_discovery(x, n, w, a, engine="phidd")
+    assert pos[0] == want["position"]
+    assert dist[0] == pytest.approx(want["distance"], rel=DIST_RTOL)
+
+
+def test_disable_pruning_does_not_change_the_result(ctx, chk):
+    x = planted_walk(3, 5000, 64)
+    ctx.prepare(x, 64, 4, 4)
+    pruned = ctx.search(3)
+    calls_pruned = ctx.stats()["calls"]
+    full = ctx.search(3, disable_pruning=True)
+    st = ctx.stats()
+    assert pruned[0] == full[0]
+    np.testing.assert_allclose(pruned[1], full[1], rtol=1e-6)
+    # without pruning every ordered non-self pair is started exactly once
+    N, n = 5000 - 64 + 1, 64
+    assert st["calls"] == N * N - N * (2 * n - 1) + n * (n - 1)
+    assert st["abandoned"] == 0 and calls_pruned < st["calls"]
+
+
+@pytest.mark.parametrize("m,n,k", [(8000, 64, 4), (12000, 128, 5)])
+def test_topk_matches_exclusion_zone_oracle(ctx, chk, m, n, k):
+    x = planted_walk(9, m, n)
+    x[m // 2:m // 2 + n] = W.random_walk(99, n) * np.float32(0.2) + x[m // 2]
+    ctx.prepare(x, n, 4, 4)
+    pos, dist = ctx.search(k)
+    want = chk.topk(x, n, 4, 4, k)
+    assert pos == want["positions"]
+    np.testing.assert_allclose(dist, want["distances"], rtol=DIST_RTOL)
+    for i in range(k):
+        for j in range(i):
+            assert abs(pos[i] - pos[j]) >= n
+
+
+def test_nn_profile_matches_oracle(ctx, chk):
+    x = W.random_walk(31, 3000)
+    ctx.prepare(x, 64, 4, 4)
+    got = np.sqrt(ctx.nn_profile().astype(np.float64))
+    want = np.sqrt(chk.nn_profile(x, 64))  # the oracle's profile is squared (series.hpp:150-164)
+    np.testing.assert_allclose(got, want, rtol=DIST_RTOL)
+    assert ctx.fetch("nn_exact").all()
+
+
+def test_search_is_repeatable_and_independent_of_tunables(ctx):
+    x = planted_walk(12, 20000, 128)
+    ctx.prepare(x, 128, 4, 4)
+    base = ctx.search(3)
+    for name, value in [("batch", 300), ("rounds", 1), ("rounds", 12), ("bucket_mates", 0),
+                        ("symmetric", 0), ("packed", 0), ("first_batch", 4096)]:
+        ctx.set_option(name, value)
+        again = ctx.search(3)
+        assert again[0] == base[0], name
+        np.testing.assert_allclose(again[1], base[1], rtol=1e-6, err_msg=name)
+    for name, value in [("batch", 8192), ("rounds", 7), ("bucket_mates", 8), ("symmetric", 1),
+                        ("packed", 1), ("first_batch", 256)]:
+        ctx.set_option(name, value)
+
+
+def test_degenerate_series(ctx):
+    ctx.prepare(np.full(600, 3.0, dtype=np.float32), 16, 4, 4)
+    pos, dist = ctx.search(2)
+    assert pos == [1, 1] or pos[0] == 1
+    assert dist[0] == 0.0
+    with pytest.raises(InfeasibleInputError):
+        ctx.prepare(np.arange(20, dtype=np.float32), 16, 2, 4)
+    # smallest feasible input: N = n + 1, only rows 0 and N-1 have a non-self match
+    x = W.random_walk(2, 2 * 16)
+    ctx.prepare(x, 16, 4, 4)
+    pos, dist = ctx.search(1)
+    want = oracle.best().run_discovery(x, 16, 4, 4, engine="brute")
+    assert pos[0] == want["position"] and dist[0] == pytest.approx(want["distance"], rel=DIST_RTOL)
+
+
+def test_run_discovery_mirror(chk):
+    x = planted_walk(4, 10000, 100)
+    out = run_discovery(x, DiscoveryConfig(n=100, word_len=5, alphabet=4, k=2))
+    want = chk.topk(x, 100, 5, 4, 2)
+    assert [d.position for d in out.discords] == want["positions"]
+    assert out.result.position == want["positions"][0]
+    assert out.result.distance == pytest.approx(want["distances"][0], rel=DIST_RTOL)
+    assert out.m == 10000 and out.prep_time_s > 0 and out.search_time_s > 0
+
+
+# ------------------------------------------------------------------ BASELINE.json workloads
+@pytest.mark.parametrize("cfg", [1, 2, 3, 5, 4])
+def test_baseline_workload_matches_golden(golden, cfg):
+    key = f"cfg{cfg}"
+    if key not in golden:
+        pytest.skip(f"no golden record for workload {cfg} yet")
+    w = W.workload(cfg)
+    x, _ = W.series(cfg)
+    assert W.sha256(x) == golden[key]["sha256"]
+    out = run_discovery(x, DiscoveryConfig(n=w.n, word_len=w.word_len, alphabet=w.alphabet, k=w.k))
+    want = golden[key]["oracle"]
+    assert [d.position for d in out.discords] == want["positions"]
+    np.testing.assert_allclose([d.distance for d in out.discords], want["distances"], rtol=DIST_RTOL)
+
+
+# ------------------------------------------------------------------ several ranks on one GPU
+class _ThreadExchange:
+    """Max-reduce between `world` host threads (the kernels never wait on each other)."""
+
+    def __init__(self, world):
+        self.world = world
+        self.barrier = threading.Barrier(world)
+        self.slots = [None] * world
+        self.calls = 0
+
+    def hook(self, rank):
+        def fn(keys):
+            self.slots[rank] = keys.copy()
+            self.barrier.wait(timeout=120)
+            merged = np.maximum.reduce([s for s in self.slots])
+            self.barrier.wait(timeout=120)
+            keys[:] = merged
+            if rank == 0:
+                self.calls += 1
+        return fn
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_rank_count_does_not_change_the_result(chk, world):  # the analogue of SPEC.md:349
+    x = planted_walk(15, 16000, 64)
+    want = chk.topk(x, 64, 4, 4, 3)
+    ex = _ThreadExchange(world)
+    results, errors = [None] * world, []
+
+    def run(rank):
+        try:
+            with Context(0) as c:
+                c.set_option("batch", 512)
+                c.set_exchange(ex.hook(rank), world, rank)
+                c.prepare(x, 64, 4, 4)
+                results[rank] = c.search(3)
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+            ex.barrier.abort()
+
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not errors, errors
+    for r in range(world):
+        assert results[r][0] == want["positions"], (r, results[r])
+        np.testing.assert_allclose(results[r][1], want["distances"], rtol=DIST_RTOL)
+    assert ex.calls > 0
+
+
+def test_nccl_exchange_with_one_rank(chk):
+    """The engine's own NCCL path (dlopen, communicator, ncclAllReduce(max, uint64) per batch)."""
+    import torch  # noqa: F401  (puts the bundled libnccl.so.2 on the loader's list)
+
+    from paper_1901_00155_b200.engine import comm_unique_id
+
+    x = planted_walk(16, 8000, 64)
+    want = chk.run_discovery(x, 64, 4, 4, engine="phidd")
+    with Context(0) as c:
+        c.comm_init(comm_unique_id(), 1, 0)
+        c.prepare(x, 64, 4, 4)
+        pos, dist = c.search(1)
+    assert pos[0] == want["position"] and dist[0] == pytest.approx(want["distance"], rel=DIST_RTOL)

@@ -1,0 +1,220 @@
+"""Host-side checks that need no GPU: the C ABI loads and exports what include/tsdd_cuda.h
+declares, check_config behaves like the reference's, the product never imports the
+oracle, the seeded workloads are the pinned ones, and the multi-rank exchange works
+over gloo with two processes."""
+import ctypes
+import os
+import re
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1901_00155_b200 as pkg
+from paper_1901_00155_b200 import engine, parallel, workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _has_gpu() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:  # noqa: BLE001
+        return False
+
+
+# ------------------------------------------------------------------ the boundary
+def test_library_exports_every_declared_symbol():
+    header = open(os.path.join(ROOT, "include", "tsdd_cuda.h")).read()
+    header = re.sub(r"/\*.*?\*/", "", header, flags=re.S)
+    declared = set(re.findall(r"\b(tsdd_cuda_\w+)\s*\(", header))
+    assert len(declared) >= 18
+    assert declared == set(engine.SYMBOLS), declared ^ set(engine.SYMBOLS)
+    lib = pkg.load_library()
+    for name in declared:
+        assert getattr(lib, name) is not None
+    out = subprocess.run(["nm", "-D", "--defined-only", engine.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (tsdd_cuda_\w+)", out))
+    assert declared <= exported
+
+
+def test_library_has_sm100a_code_and_blackwell_instructions():
+    sass = subprocess.run(["cuobjdump", "-sass", engine.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in sass
+    assert "FFMA2" in sass and "FADD2" in sass  # packed f32x2 arithmetic (sm_100+)
+    assert "LDGSTS" in sass                      # cp.async staging of the tiles
+
+
+@pytest.mark.skipif(_has_gpu(), reason="checks the no-device failure mode")
+def test_create_fails_loudly_without_a_device():
+    with pytest.raises(pkg.CudaRuntimeError, match="no CPU fallback"):
+        pkg.Context(0)
+    with pytest.raises(pkg.CudaRuntimeError):
+        pkg.run_discovery(W.random_walk(1, 500), pkg.DiscoveryConfig(n=16))
+
+
+def test_product_never_touches_the_oracle():
+    pkg_dir = os.path.join(ROOT, "paper_1901_00155_b200")
+    for base, _, files in os.walk(pkg_dir):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".hpp", ".cpp", ".h")):
+                text = open(os.path.join(base, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", text, flags=re.M), f
+                assert "tsdd_oracle" not in text and "libtsdd_ref" not in text, f
+
+
+# ------------------------------------------------------------------ check_config vs the reference
+BAD = [
+    ("empty", lambda: np.zeros(0), dict(n=4), oracle.ERR_VALIDATION),
+    ("nan", lambda: np.array([1.0, np.nan] + [0.0] * 62), dict(n=8), oracle.ERR_VALIDATION),
+    ("inf", lambda: np.array([np.inf] + [0.0] * 63), dict(n=8), oracle.ERR_VALIDATION),
+    ("n_zero", lambda: np.arange(64.0), dict(n=0), oracle.ERR_PARAMETER),
+    ("n_gt_m", lambda: np.arange(64.0), dict(n=65), oracle.ERR_PARAMETER),
+    ("w_zero", lambda: np.arange(64.0), dict(n=8, word_len=0), oracle.ERR_PARAMETER),
+    ("w_gt_n", lambda: np.arange(64.0), dict(n=8, word_len=9), oracle.ERR_PARAMETER),
+    ("alphabet_1", lambda: np.arange(64.0), dict(n=8, alphabet=1), oracle.ERR_PARAMETER),
+    ("alphabet_11", lambda: np.arange(64.0), dict(n=8, alphabet=11), oracle.ERR_PARAMETER),
+    ("infeasible", lambda: np.arange(20.0), dict(n=16, word_len=2), oracle.ERR_INFEASIBLE),
+    ("n_eq_m", lambda: np.arange(20.0), dict(n=20, word_len=2), oracle.ERR_INFEASIBLE),
+    ("threads_0", lambda: np.arange(64.0), dict(n=8, threads=0), oracle.ERR_PARAMETER),
+    ("chunk_0", lambda: np.arange(64.0), dict(n=8, chunk=0), oracle.ERR_PARAMETER),
+]
+_CLASS = {oracle.ERR_VALIDATION: pkg.ValidationError, oracle.ERR_PARAMETER: pkg.ParameterError,
+          oracle.ERR_INFEASIBLE: pkg.InfeasibleInputError}
+
+
+@pytest.mark.parametrize("name,make,kw,code", BAD, ids=[b[0] for b in BAD])
+def test_check_config_matches_reference_errors(name, make, kw, code):
+    x = make()
+    cfg = pkg.DiscoveryConfig(**kw)
+    with pytest.raises(_CLASS[code]) as mine:
+        pkg.check_config(x, cfg)
+    if code == oracle.ERR_INFEASIBLE:
+        assert isinstance(mine.value, pkg.ParameterError)  # errors.hpp:22: Infeasible is-a Parameter
+    if name in ("threads_0", "chunk_0", "empty"):
+        return  # the oracle shims take these through other paths
+    with pytest.raises(oracle.OracleError) as ref:
+        oracle.best().run_discovery(x, kw["n"], kw.get("word_len", 4), kw.get("alphabet", 4), threads=1)
+    assert ref.value.code == code
+    if name not in ("alphabet_1", "alphabet_11"):
+        assert str(mine.value) == ref.value.message  # same text as the reference's exception
+
+
+def test_check_config_error_order_is_the_references():
+    # series is validated before any parameter (pipeline.cpp:22), n before word_len, feasibility last
+    bad = np.arange(20.0)
+    bad[3] = np.nan
+    with pytest.raises(pkg.ValidationError, match="index 4"):
+        pkg.check_config(bad, pkg.DiscoveryConfig(n=0, word_len=0, alphabet=99))
+    with pytest.raises(pkg.ParameterError, match="^n="):
+        pkg.check_config(np.arange(20.0), pkg.DiscoveryConfig(n=0, word_len=0, alphabet=99))
+    with pytest.raises(pkg.ParameterError, match="alphabet"):
+        pkg.check_config(np.arange(20.0), pkg.DiscoveryConfig(n=16, word_len=2, alphabet=99))
+    pkg.check_config(np.arange(64.0), pkg.DiscoveryConfig(n=8, word_len=8, alphabet=10))
+
+
+def test_dictionary_guard_is_2_pow_32():
+    x = W.random_walk(1, 4096)
+    pkg.check_config(x, pkg.DiscoveryConfig(n=64, word_len=16, alphabet=4))   # 4^16 = 2^32: accepted
+    with pytest.raises(pkg.ParameterError, match="2\\^32"):
+        pkg.check_config(x, pkg.DiscoveryConfig(n=64, word_len=17, alphabet=4))
+    with pytest.raises(pkg.ParameterError):
+        pkg.check_config(x, pkg.DiscoveryConfig(n=64, word_len=10, alphabet=10))  # 10^10 > 2^32
+    with pytest.raises(pkg.ParameterError, match="engine"):
+        pkg.run_discovery(x, pkg.DiscoveryConfig(n=64, engine="phidd"))
+
+
+# ------------------------------------------------------------------ workloads
+def test_workloads_are_the_pinned_series(golden):
+    for key, rec in golden.items():
+        w = W.workload(rec["cfg"])
+        assert (w.m, w.n, w.word_len, w.alphabet, w.k) == (rec["m"], rec["n"], rec["word_len"],
+                                                          rec["alphabet"], rec["k"])
+        if w.m <= 1_000_000:
+            x, at = W.series(rec["cfg"])
+            assert W.sha256(x) == rec["sha256"] and at == rec["anomaly_starts_0based"]
+
+
+def test_workload_table_matches_baseline_json():
+    shapes = {1: (65536, 128, 4, 4, 1), 2: (262144, 256, 8, 4, 4), 3: (1000000, 512, 8, 6, 3),
+              4: (4000000, 1024, 16, 4, 5), 5: (1000000, 256, 8, 4, 1)}
+    for cfg, want in shapes.items():
+        w = W.workload(cfg)
+        assert (w.m, w.n, w.word_len, w.alphabet, w.k) == want
+
+
+# ------------------------------------------------------------------ packed keys / sharding
+def test_packed_key_order_is_the_reference_merge_rule():
+    # greater distance wins; equal distance -> smaller position (discovery.cpp:158-165, 328-340)
+    assert parallel.pack_best(2.0, 10) > parallel.pack_best(1.5, 3)
+    assert parallel.pack_best(2.0, 3) > parallel.pack_best(2.0, 10)
+    assert parallel.unpack_best(parallel.pack_best(7.25, 1234)) == (7.25, 1234)
+    rng = np.random.default_rng(0)
+    d = rng.random(1000).astype(np.float32) * 100
+    rows = rng.integers(0, 4_000_000, 1000)
+    keys = [parallel.pack_best(float(a), int(b)) for a, b in zip(d, rows)]
+    best = max(range(1000), key=lambda i: (d[i], -rows[i]))
+    assert keys.index(max(keys)) == best
+    assert all(k < 2 ** 63 for k in keys)
+    assert sorted(parallel.owner_of(e, 4) for e in range(8)) == [0, 0, 1, 1, 2, 2, 3, 3]
+
+
+_GLOO_WORKER = r"""
+import os, sys
+sys.path.insert(0, {root!r})
+import numpy as np
+import torch.distributed as dist
+from paper_1901_00155_b200 import parallel
+
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:{port}", rank=int(sys.argv[1]), world_size=2)
+rank = dist.get_rank()
+ex = parallel.TorchExchange()
+
+# a toy version of the engine's outer loop: each rank owns every other entry of a shared
+# order, raises its local best batch by batch, and exchanges (best, more-work) after each
+rng = np.random.default_rng(5)
+nn = (rng.random(1000) * 50).astype(np.float32)          # same on both ranks
+order = rng.permutation(1000)
+mine = [int(r) for e, r in enumerate(order) if parallel.owner_of(e, 2) == rank]
+if rank == 1:
+    mine = mine[:200]                                       # uneven work: rank 1 runs dry first
+best, cursor, rounds = 0, 0, 0
+while True:
+    batch = mine[cursor:cursor + 64]
+    cursor += len(batch)
+    for r in batch:
+        best = max(best, parallel.pack_best(float(nn[r]), r))
+    keys = np.array([best, 1 if cursor < len(mine) else 0], dtype=np.uint64)
+    ex(keys)
+    best, more = int(keys[0]), int(keys[1])
+    rounds += 1
+    if not more:
+        break
+seen = [int(r) for e, r in enumerate(order) if e % 2 == 0 or (e % 2 == 1 and e < 400)]
+want = max(parallel.pack_best(float(nn[r]), r) for r in seen)
+assert best == want, (best, want)
+assert rounds == ex.calls == 8, rounds                      # ceil(500/64): both ranks leave together
+d2, row = parallel.unpack_best(best)
+print("rank", rank, "ok", d2, row, rounds, flush=True)
+dist.destroy_process_group()
+"""
+
+
+def test_exchange_over_gloo_with_two_ranks(tmp_path):
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    script = tmp_path / "worker.py"
+    script.write_text(_GLOO_WORKER.format(root=ROOT, port=port))
+    procs = [subprocess.Popen([sys.executable, str(script), str(r)], stdout=subprocess.PIPE,
+                              stderr=subprocess.STDOUT, text=True) for r in range(2)]
+    outs = [p.communicate(timeout=180)[0] for p in procs]
+    for r, (p, out) in enumerate(zip(procs, outs)):
+        assert p.returncode == 0, out
+        assert f"rank {r} ok" in out
+    assert outs[0].split("ok")[1].split()[:2] == outs[1].split("ok")[1].split()[:2]
