@@ -1,0 +1,333 @@
+"""Benchmark of the discord-search hot path (prepare + search) on B200.
+
+    python bench.py --gpus N --steps K --warmup W            # this repo's CUDA engine
+    python bench.py --impl reference --gpus N --steps K ...  # the reference's CPU path
+
+One "step" is one complete discord search (preparation stage + top-k search) of one
+BASELINE.json workload.  Default workload: cfg5 (i.i.d. noise, m = 1,000,000, n = 256,
+the "pruning worst case" that BASELINE.json uses for raw distance throughput).
+
+Metric (BASELINE.json): subsequence-pair distances per second = distance evaluations
+started (the reference's own counter, series.hpp:68-74,120) / step time; the end-to-end
+top-k time of a step is reported beside it (`topk_time_s`).
+  value : series already resident in HBM, prepare_device + search, CUDA events on the
+          stream the kernels run on, max over ranks.
+  e2e   : the reference-facing call (run_discovery with a HOST series in pinned memory):
+          H2D copy + prepare + search + D2H of the result inside the timed region.
+  roofline : the tiled distance kernel against the FP32 CUDA-core peak.  One term
+          (x-y)^2 accumulated = 3 FLOP; `peak` is measured live with an
+          FFMA-only probe kernel (MEASURED_PEAKS.json has no FP32 entry) and
+          `peak_nominal` = 148 SMs x 128 lanes x 2 x 1.965 GHz.
+  cpu_baseline : the unmodified reference (oracle/_ref; else the C restatement) on the
+          box's host cores, on a bounded sample (a prefix of the same series).
+
+The oracle is used here only as the timed CPU baseline, never on the product path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "subsequence_pair_distances_per_s"
+UNIT = "distances/s"
+CPU_SAMPLE = {1: 65536, 2: 262144, 3: 300000, 4: 400000, 5: 200000}  # prefix lengths for the CPU arm
+ORACLE_SHAPE = {4: (8, 4)}  # the reference rejects 4^16 words (sax.hpp:80); results are shape-independent
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.samples, self._stop, self._thread = index, [], threading.Event(), None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([c.strip() for c in out.splitlines()[0].split(",")])
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._thread = threading.Thread(target=self._run, daemon=True)
+        self._thread.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._thread.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = [n for i, n in enumerate(names) if any(s[3 + i].lower().startswith("active") for s in self.samples)]
+        power = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(self.samples[0][1]),
+                "power_w_max": max(power) if power else None, "reasons": reasons, "samples": len(self.samples)}
+
+
+def workload_inputs(cfg: int):
+    from paper_1901_00155_b200 import workloads as W
+
+    w = W.workload(cfg)
+    x, _ = W.series(cfg)
+    return w, x
+
+
+def cpu_reference_run(cfg: int, x: np.ndarray, w, threads: int | None = None) -> dict:
+    """The reference's own CPU path (prepare + phidd search, exclusion-zone wrapper for k > 1)
+    on a prefix of the workload's series.  The one place bench.py executes oracle/."""
+    import oracle
+
+    chk = oracle.best()
+    sample_m = min(CPU_SAMPLE[cfg], len(x))
+    word_len, alphabet = ORACLE_SHAPE.get(cfg, (w.word_len, w.alphabet))
+    threads = threads or os.cpu_count() or 1
+    t0 = time.perf_counter()
+    if w.k == 1:
+        out = chk.run_discovery(x[:sample_m], w.n, word_len, alphabet, engine="phidd", threads=threads, chunk=64)
+        calls, prep_s, search_s = out["calls"], out["prep_s"], out["search_s"]
+    else:
+        out = chk.topk(x[:sample_m], w.n, word_len, alphabet, w.k, threads=threads, chunk=64)
+        calls, prep_s, search_s = out["calls"], out["prep_s"], out["search_s"]
+    wall = time.perf_counter() - t0
+    step_s = prep_s + search_s
+    return {"value": calls / step_s, "unit": UNIT, "cores": threads, "kind": chk.kind,
+            "sample": f"prefix of {sample_m} samples of cfg{cfg} (n={w.n}, k={w.k}, SAX {word_len}x{alphabet}), "
+                      f"engine=phidd chunk=64",
+            "calls": calls, "prep_s": prep_s, "search_s": search_s, "wall_s": wall, "topk_time_s": step_s}
+
+
+def run_reference_arm(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w, x = workload_inputs(args.workload)
+    for _ in range(args.warmup):
+        pass  # a CPU run has no warm-up state worth paying 10+ s for; the count is still reported
+    runs = [cpu_reference_run(args.workload, x, w) for _ in range(max(1, args.steps))]
+    step_s = [r["topk_time_s"] for r in runs]
+    calls = runs[0]["calls"]
+    value = sum(r["calls"] for r in runs) / sum(step_s)
+    base = dict(runs[0])
+    base["value"] = value
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": len(runs), "warmup": args.warmup, "ms_per_step": 1e3 * sum(step_s) / len(runs),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cfg{args.workload}", "m": w.m, "n": w.n, "k": w.k, "sample": base["sample"]},
+        "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "topk_time_s": sum(step_s) / len(runs), "calls_per_step": calls, "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_cuda_arm(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_1901_00155_b200 import Context, DiscoveryConfig, parallel, run_discovery
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device; the engine has no CPU fallback")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    w, x = workload_inputs(args.workload)
+    k = w.k
+    host = torch.from_numpy(x).pin_memory()          # e2e arm: pinned host buffer
+    x_pinned = host.numpy()
+    dev = host.to(f"cuda:{local}", non_blocking=False)  # value arm: resident in HBM
+    stream = torch.cuda.current_stream()
+
+    ctx = Context(local)
+    ctx.set_stream(stream.cuda_stream)
+    for opt in args.opt:
+        name, val = opt.split("=")
+        ctx.set_option(name, float(val))
+    if world > 1:
+        parallel.attach_nccl(ctx)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def device_step():
+        ctx.prepare_device(dev.data_ptr(), w.m, w.n, w.word_len, w.alphabet)
+        pos, dd = ctx.search(k)
+        return pos, dd, ctx.stats()
+
+    def host_step():
+        out = run_discovery(x_pinned, DiscoveryConfig(n=w.n, word_len=w.word_len, alphabet=w.alphabet, k=k,
+                                                      device=local), context=ctx)
+        return [d.position for d in out.discords], [d.distance for d in out.discords], out.stats
+
+    # FP32 peak, measured on this device now (FFMA-only stream; one FFMA = 2 FLOP)
+    ffma_ops, _ = ctx.fp32_probe(0)
+    mix_ops, _ = ctx.fp32_probe(3)
+
+    for _ in range(args.warmup):
+        device_step()
+    barrier()
+    sampler = ClockSampler(local)
+    totals = {"calls": 0, "terms": 0, "scan_terms": 0, "scan_ms": 0.0, "scan_launches": 0, "launches": 0,
+              "prep_ms": 0.0, "search_ms": 0.0, "build_rows_ms": 0.0, "encode_ms": 0.0, "index_ms": 0.0}
+    with sampler:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            pos, dd, st = device_step()
+            totals["calls"] += st["calls"]
+            totals["terms"] += st["terms"]
+            totals["scan_terms"] += st["scan_kernel_terms"]
+            totals["scan_ms"] += st["scan_kernel_ms"]
+            totals["scan_launches"] += st["scan_kernel_launches"]
+            totals["launches"] += st["kernel_launches"]
+            for key in ("prep_ms", "search_ms", "build_rows_ms", "encode_ms", "index_ms"):
+                totals[key] += st[key]
+        ev1.record(stream)
+        barrier()
+        elapsed_ms = ev0.elapsed_time(ev1)
+
+        # end to end through the reference-facing call, host buffers
+        host_step()
+        barrier()
+        t0 = time.perf_counter()
+        e2e_calls = 0
+        for _ in range(args.steps):
+            pos_h, dd_h, st_h = host_step()
+            e2e_calls += st_h["calls"]
+        barrier()
+        e2e_s = time.perf_counter() - t0
+    assert pos_h == pos, (pos_h, pos)
+
+    t = torch.tensor([elapsed_ms, e2e_s], dtype=torch.float64, device=f"cuda:{local}")
+    c = torch.tensor([totals["calls"], e2e_calls], dtype=torch.float64, device=f"cuda:{local}")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+    elapsed_ms, e2e_s = float(t[0]), float(t[1])
+    all_calls, all_e2e_calls = float(c[0]), float(c[1])
+
+    if rank == 0:
+        golden_ok = None
+        try:
+            golden = json.load(open(os.path.join(ROOT, "tests", "golden", "workloads.json")))
+            rec = golden.get(f"cfg{args.workload}")
+            if rec:
+                golden_ok = pos == rec["oracle"]["positions"]
+        except OSError:
+            pass
+        scan_s = totals["scan_ms"] * 1e-3
+        achieved = 3.0 * totals["scan_terms"] / scan_s / 1e12 if scan_s > 0 else 0.0
+        peak = 2.0 * ffma_ops / 1e12
+        nominal = 148 * 128 * 2 * 1.965e9 / 1e12
+        traffic = None
+        try:
+            prof = json.load(open(os.path.join(ROOT, "profiles", "scan_tiles_summary.json")))
+            traffic = prof.get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            prof = {}
+        N = w.m - w.n + 1
+        matrix_bytes = 4.0 * N * ((w.n + 31) // 32 * 32)
+        line = {
+            "metric": METRIC, "value": all_calls / (elapsed_ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": f"cfg{args.workload}", "m": w.m, "n": w.n, "word_len": w.word_len,
+                       "alphabet": w.alphabet, "k": k, "rows": N,
+                       "parallelism": f"candidates sharded over {world} rank(s), per-batch NCCL max-allreduce"
+                       if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2" if matrix_bytes > 126e6 else
+                       "matrix fits L2; every step rebuilds it from the series"},
+            "topk_time_s": elapsed_ms * 1e-3 / args.steps,
+            "discords": {"positions": pos, "distances": dd, "matches_golden": golden_ok},
+            "e2e": {"value": all_e2e_calls / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(x.nbytes),
+                    "d2h_bytes_per_step": int(k * 16 + 160), "topk_time_s": e2e_s / args.steps},
+            "gpu_launches": int(totals["launches"]),
+            "roofline": {"bound": "fp32", "kernel": "k_scan_tiles", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
+                         "peak_source": "live FFMA-only probe kernel x 2 FLOP (MEASURED_PEAKS.json has no FP32 "
+                                        "entry; B200_PROFILING.md states no FP32 fallback)",
+                         "peak_nominal": nominal, "frac_nominal": achieved / nominal,
+                         "terms_per_s": totals["scan_terms"] / scan_s if scan_s else 0.0,
+                         "fma_pipe_util": 2.0 * totals["scan_terms"] / scan_s / ffma_ops if scan_s else 0.0,
+                         "sub_fma_mix_probe_lane_ops_per_s": mix_ops, "ffma_probe_lane_ops_per_s": ffma_ops,
+                         "launches": int(totals["scan_launches"]),
+                         "avg_launch_ms": totals["scan_ms"] / max(1, totals["scan_launches"]),
+                         "kernel_share_of_step": totals["scan_ms"] / elapsed_ms, "traffic": traffic},
+            "roofline_prep": {"bound": "hbm", "kernel": "k_build_rows", "unit": "GB/s",
+                              "achieved": matrix_bytes * args.steps / (totals["build_rows_ms"] * 1e-3) / 1e9
+                              if totals["build_rows_ms"] else None,
+                              "peak": _measured_peak("hbm_gbs", 6650.0)[0],
+                              "peak_source": _measured_peak("hbm_gbs", 6650.0)[1]},
+            "stage_ms_per_step": {key: totals[key] / args.steps for key in
+                                  ("prep_ms", "encode_ms", "build_rows_ms", "index_ms", "search_ms")},
+            "calls_per_step": all_calls / args.steps, "terms_per_step": totals["terms"] / args.steps,
+            "clocks": sampler.summary(),
+        }
+        rp = line["roofline_prep"]
+        rp["frac"] = rp["achieved"] / rp["peak"] if rp["achieved"] else None
+        if world == 1 and not args.no_cpu_baseline:
+            cb = cpu_reference_run(args.workload, x, w)
+            line["cpu_baseline"] = {key: cb[key] for key in ("value", "unit", "cores", "kind", "sample",
+                                                             "calls", "topk_time_s")}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _measured_peak(key: str, fallback: float):
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))[key]), "MEASURED_PEAKS.json"
+    except (OSError, KeyError, ValueError):
+        return fallback, "fallback (B200_PROFILING.md)"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", type=int, default=5, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--opt", action="append", default=[], help="engine tunable name=value")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_cuda_arm(args)
+
+
+if __name__ == "__main__":
+    main()

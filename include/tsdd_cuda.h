@@ -57,6 +57,9 @@ typedef struct tsdd_cuda_stats {
   double h2d_ms;           /* series upload, when prepare was given a host pointer */
   uint64_t scan_kernel_launches;
   uint64_t scan_kernel_terms; /* terms accumulated by the tiled distance kernel only */
+  double encode_ms;        /* preparation: window statistics + PAA/SAX/hash kernel */
+  double build_rows_ms;    /* preparation: float32 matrix build (HBM write-bound) */
+  double index_ms;         /* preparation: radix sorts, run-length histogram, rarity order */
 } tsdd_cuda_stats;
 
 /* ---- lifetime ------------------------------------------------------------ */
@@ -68,6 +71,11 @@ void tsdd_cuda_destroy(tsdd_cuda_ctx* ctx);
 /* Message of the last failure on this context (ctx == NULL: last failure of
  * tsdd_cuda_create on this thread).  Never NULL.                            */
 const char* tsdd_cuda_last_error(const tsdd_cuda_ctx* ctx);
+
+/* Runs all further work of the context on the caller's CUDA stream (a
+ * cudaStream_t, e.g. torch.cuda.current_stream().cuda_stream) so that the
+ * caller's events bracket it; NULL restores the context's own stream.      */
+int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream);
 
 /* Tunables, by name: "batch" (candidates per outer-loop batch), "first_batch"
  * (size of the first batch; it doubles up to "batch"), "rounds" (neighbour

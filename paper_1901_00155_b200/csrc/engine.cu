@@ -47,9 +47,11 @@ template <typename T>
 struct DeviceArray {
   T* ptr = nullptr;
   size_t count = 0;
+  // grow-only: a context that is prepared again with the same shape allocates nothing
   void alloc(size_t n) {
-    release();
     if (n == 0) n = 1;
+    if (ptr && count >= n) return;
+    release();
     CUDA_OK(cudaMalloc(reinterpret_cast<void**>(&ptr), n * sizeof(T)));
     count = n;
   }
@@ -119,7 +121,9 @@ NcclApi g_nccl;
 struct tsdd_cuda_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  cudaEvent_t ev_prep[4] = {nullptr, nullptr, nullptr, nullptr};  // encode | build rows | index | end
   std::string error;
 
   // tunables (tsdd_cuda_set_option)
@@ -249,18 +253,21 @@ void prepare_on_device(tsdd_cuda_ctx* ctx, size_t m, size_t n, size_t word_len, 
   ctx->mean.alloc(rows);
   ctx->inv_sigma.alloc(rows);
   ctx->hash0.alloc(rows);
+  const size_t matrix_floats = static_cast<size_t>(ctx->rows_padded) * ctx->stride;
+  ctx->matrix.alloc(matrix_floats);
+  CUDA_OK(cudaEventRecord(ctx->ev_prep[0], st));
   launches += launch_window_encode(ctx->series.ptr, rows, static_cast<uint32_t>(n),
                                    static_cast<uint32_t>(word_len), static_cast<uint32_t>(alphabet),
                                    ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->hash0.ptr, nullptr, nullptr, st);
 
-  const size_t matrix_floats = static_cast<size_t>(ctx->rows_padded) * ctx->stride;
-  ctx->matrix.alloc(matrix_floats);
+  CUDA_OK(cudaEventRecord(ctx->ev_prep[1], st));
   if (ctx->rows_padded > rows)
     CUDA_OK(cudaMemsetAsync(ctx->matrix.ptr + static_cast<size_t>(rows) * ctx->stride, 0,
                             static_cast<size_t>(ctx->rows_padded - rows) * ctx->stride * sizeof(float), st));
   launches += launch_build_rows(ctx->series.ptr, ctx->mean.ptr, ctx->inv_sigma.ptr, rows,
                                 static_cast<uint32_t>(n), ctx->stride, ctx->matrix.ptr, st);
 
+  CUDA_OK(cudaEventRecord(ctx->ev_prep[2], st));
   // bucket index: stable sort of (hash, row) -> runs are the buckets
   const size_t longest_scan = std::max<size_t>(rows, radix_sort_scratch_words(rows));
   ctx->scan_scratch.alloc(scan_scratch_words(static_cast<uint32_t>(longest_scan)) + 1024);
@@ -297,6 +304,7 @@ void prepare_on_device(tsdd_cuda_ctx* ctx, size_t m, size_t n, size_t word_len, 
   ctx->sorted_freq = f0;
   ctx->order = o0;
   launches += launch_count_min_freq(ctx->sorted_freq, rows, ctx->scalars.ptr, st);
+  CUDA_OK(cudaEventRecord(ctx->ev_prep[3], st));
 
   // search-state storage
   ctx->nn.alloc(rows);
@@ -320,6 +328,12 @@ void finish_prepare(tsdd_cuda_ctx* ctx) {
   float ms = 0.f;
   CUDA_OK(cudaEventElapsedTime(&ms, ctx->ev_a, ctx->ev_b));
   ctx->stats.prep_ms = ms;
+  CUDA_OK(cudaEventElapsedTime(&ms, ctx->ev_prep[0], ctx->ev_prep[1]));
+  ctx->stats.encode_ms = ms;
+  CUDA_OK(cudaEventElapsedTime(&ms, ctx->ev_prep[1], ctx->ev_prep[2]));
+  ctx->stats.build_rows_ms = ms;
+  CUDA_OK(cudaEventElapsedTime(&ms, ctx->ev_prep[2], ctx->ev_prep[3]));
+  ctx->stats.index_ms = ms;
   ctx->stats.rows = ctx->rows;
   ctx->stats.buckets = scalars[0];
   ctx->stats.min_freq_candidates = scalars[1];
@@ -634,7 +648,9 @@ int tsdd_cuda_create(tsdd_cuda_ctx** out, int device) {
     ctx = new tsdd_cuda_ctx();
     ctx->device = device;
     CUDA_OK(cudaSetDevice(device));
-    CUDA_OK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+    ctx->stream = ctx->own_stream;
+    for (auto& e : ctx->ev_prep) CUDA_OK(cudaEventCreate(&e));
     CUDA_OK(cudaEventCreate(&ctx->ev_a));
     CUDA_OK(cudaEventCreate(&ctx->ev_b));
     CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_sel), 4 * sizeof(uint32_t)));
@@ -655,18 +671,29 @@ void tsdd_cuda_destroy(tsdd_cuda_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
   for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->ev_prep)
+    if (e) cudaEventDestroy(e);
   if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
   if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
   if (ctx->h_sel) cudaFreeHost(ctx->h_sel);
   if (ctx->h_keys) cudaFreeHost(ctx->h_keys);
   if (ctx->h_double) cudaFreeHost(ctx->h_double);
-  cudaStream_t st = ctx->stream;
+  cudaStream_t st = ctx->own_stream;
   delete ctx;  // frees the device arrays
   if (st) cudaStreamDestroy(st);
 }
 
 const char* tsdd_cuda_last_error(const tsdd_cuda_ctx* ctx) {
   return ctx ? ctx->error.c_str() : g_create_error.c_str();
+}
+
+int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream) {
+  if (!ctx) return TSDD_ERR_PARAMETER;
+  return guarded(ctx, [&] {
+    bind_device(ctx);
+    sync_stream(ctx);
+    ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
+  });
 }
 
 int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
@@ -746,8 +773,9 @@ int tsdd_cuda_prepare_device_f32(tsdd_cuda_ctx* ctx, const float* d_series, size
     bind_device(ctx);
     reset_stats(ctx);
     ctx->series.alloc(m);
-    // the caller's stream is unknown: order after everything already queued on the device
-    CUDA_OK(cudaDeviceSynchronize());
+    // unless the caller handed over its stream (tsdd_cuda_set_stream), its work is
+    // unordered with ours: wait for everything already queued on the device
+    if (ctx->stream == ctx->own_stream) CUDA_OK(cudaDeviceSynchronize());
     CUDA_OK(cudaEventRecord(ctx->ev_a, ctx->stream));
     const uint64_t extra = launch_widen_series(d_series, ctx->series.ptr, m, ctx->stream);
     prepare_on_device(ctx, m, n, word_len, alphabet);

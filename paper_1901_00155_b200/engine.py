@@ -57,7 +57,9 @@ class Stats(ctypes.Structure):
                 ("scanned_candidates", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
                 ("prep_ms", ctypes.c_double), ("search_ms", ctypes.c_double),
                 ("scan_kernel_ms", ctypes.c_double), ("h2d_ms", ctypes.c_double),
-                ("scan_kernel_launches", ctypes.c_uint64), ("scan_kernel_terms", ctypes.c_uint64)]
+                ("scan_kernel_launches", ctypes.c_uint64), ("scan_kernel_terms", ctypes.c_uint64),
+                ("encode_ms", ctypes.c_double), ("build_rows_ms", ctypes.c_double),
+                ("index_ms", ctypes.c_double)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -71,6 +73,7 @@ SYMBOLS = {
     "tsdd_cuda_create": (_int, [ctypes.POINTER(_vp), _int]),
     "tsdd_cuda_destroy": (None, [_vp]),
     "tsdd_cuda_last_error": (ctypes.c_char_p, [_vp]),
+    "tsdd_cuda_set_stream": (_int, [_vp, _vp]),
     "tsdd_cuda_set_option": (_int, [_vp, ctypes.c_char_p, _dbl]),
     "tsdd_cuda_check_config_f32": (_int, [_vp, _sz, _sz, _sz, _sz, ctypes.c_char_p, _sz]),
     "tsdd_cuda_check_config_f64": (_int, [_vp, _sz, _sz, _sz, _sz, ctypes.c_char_p, _sz]),
@@ -216,6 +219,10 @@ class Context:
     def _check(self, rc: int):
         if rc != OK:
             _raise(rc, self._lib.tsdd_cuda_last_error(self._h).decode())
+
+    def set_stream(self, cuda_stream: int | None):
+        """Run on the caller's stream (``torch.cuda.current_stream().cuda_stream``); None = own."""
+        self._check(self._lib.tsdd_cuda_set_stream(self._h, cuda_stream))
 
     def set_option(self, name: str, value: float):
         self._check(self._lib.tsdd_cuda_set_option(self._h, name.encode(), float(value)))
