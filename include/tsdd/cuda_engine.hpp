@@ -1,0 +1,193 @@
+// tsdd/cuda_engine.hpp — C++ host side of the B200 discord-search engine.
+//
+// Header-only binding of the C ABI (tsdd_cuda.h) to the reference's own
+// interface for this path: the same type names, fields, 1-based positions and
+// exception contract as /root/reference/proj/include/tsdd/
+//     pipeline.hpp:15-37   DiscoveryConfig, RunOutcome, run_discovery
+//     discovery.hpp:16-32  Engine, DiscordResult, DiscoveryOptions
+//     series.hpp:14-19     TimeSeries
+//     errors.hpp:10-25     ParameterError, ValidationError, InfeasibleInputError
+//
+// Two ways to use it:
+//   * inside the reference tree: define TSDD_CUDA_WITH_REFERENCE_HEADERS, the
+//     reference's headers supply the types and tsdd::cuda::run_discovery is the
+//     body of one more case of the engine switch (pipeline.cpp:78-88); see
+//     INTEGRATION.md;
+//   * standalone (default): the small mirror types below are defined here.
+//
+// No exception crosses the C ABI: return codes are turned back into the
+// reference's exception types here.
+#ifndef TSDD_CUDA_ENGINE_HPP
+#define TSDD_CUDA_ENGINE_HPP
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tsdd_cuda.h"
+
+#ifdef TSDD_CUDA_WITH_REFERENCE_HEADERS
+#include "tsdd/errors.hpp"
+#include "tsdd/pipeline.hpp"
+#else
+namespace tsdd {
+
+struct ParameterError : std::invalid_argument {  // CLI exit code 2
+  using std::invalid_argument::invalid_argument;
+};
+struct ValidationError : std::runtime_error {  // CLI exit code 3
+  using std::runtime_error::runtime_error;
+};
+struct InfeasibleInputError : ParameterError {  // no non-self match at this n
+  using ParameterError::ParameterError;
+};
+
+struct TimeSeries {
+  std::vector<double> values;
+  std::size_t length() const { return values.size(); }
+};
+
+enum class Engine { brute, hotsax, phidd, cuda };
+
+struct DiscordResult {
+  std::size_t position = 0;     // 1-based start of the discord
+  double distance = 0.0;        // Euclidean, square root taken once
+  std::uint64_t calls = 0;      // distance evaluations started
+  std::uint64_t abandoned = 0;  // of which cut short
+  Engine engine = Engine::cuda;
+};
+
+struct DiscoveryConfig {
+  std::size_t n = 0;
+  std::size_t word_len = 4;
+  std::size_t alphabet = 4;
+  std::size_t vec_width = 8;  // validated (>= 1); the device row stride is fixed at 32 floats
+  Engine engine = Engine::cuda;
+  int threads = 1;  // validated (>= 1); no meaning on the device
+  int chunk = 1;    // validated (>= 1); no meaning on the device
+  bool disable_pruning = false;
+};
+
+struct RunOutcome {
+  DiscordResult result;
+  std::size_t m = 0;
+  double prep_time_s = 0.0;
+  double search_time_s = 0.0;
+};
+
+}  // namespace tsdd
+#endif  // TSDD_CUDA_WITH_REFERENCE_HEADERS
+
+namespace tsdd::cuda {
+
+// Thrown for TSDD_ERR_RUNTIME: CUDA / NCCL failure or no usable device.
+struct DeviceError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void raise_for(int code, const std::string& message) {
+  switch (code) {
+    case TSDD_OK: return;
+    case TSDD_ERR_PARAMETER: throw ParameterError(message);
+    case TSDD_ERR_VALIDATION: throw ValidationError(message);
+    case TSDD_ERR_INFEASIBLE: throw InfeasibleInputError(message);
+    default: throw DeviceError(message);
+  }
+}
+
+// One engine instance on one GPU.  Externally synchronised, like every
+// instance in the reference.
+class Session {
+ public:
+  explicit Session(int device = 0) {
+    const int rc = tsdd_cuda_create(&ctx_, device);
+    if (rc != TSDD_OK) raise_for(rc, tsdd_cuda_last_error(nullptr));
+  }
+  ~Session() { tsdd_cuda_destroy(ctx_); }
+  Session(const Session&) = delete;
+  Session& operator=(const Session&) = delete;
+
+  tsdd_cuda_ctx* handle() const { return ctx_; }
+
+  void set_option(const char* name, double value) { check(tsdd_cuda_set_option(ctx_, name, value)); }
+
+  // Preparation stage (pipeline.cpp:60-69) on the device.
+  void prepare(const TimeSeries& series, std::size_t n, std::size_t word_len, std::size_t alphabet) {
+    check(tsdd_cuda_prepare_f64(ctx_, series.values.data(), series.values.size(), n, word_len, alphabet));
+  }
+  void prepare(const std::vector<float>& series, std::size_t n, std::size_t word_len, std::size_t alphabet) {
+    check(tsdd_cuda_prepare_f32(ctx_, series.data(), series.size(), n, word_len, alphabet));
+  }
+
+  // Search stage (phidd_discord, discovery.cpp:360-373); k > 1 adds the
+  // exclusion-zone top-k of tsdd_cuda.h.
+  std::vector<DiscordResult> search(int k = 1, bool disable_pruning = false) {
+    std::vector<std::uint64_t> pos(static_cast<std::size_t>(k > 0 ? k : 1));
+    std::vector<double> dist(pos.size());
+    check(tsdd_cuda_search(ctx_, k, disable_pruning ? TSDD_SEARCH_DISABLE_PRUNING : 0u, pos.data(), dist.data()));
+    const tsdd_cuda_stats st = stats();
+    std::vector<DiscordResult> out(pos.size());
+    for (std::size_t r = 0; r < out.size(); ++r) {
+      out[r].position = static_cast<std::size_t>(pos[r]);
+      out[r].distance = dist[r];
+      out[r].calls = st.calls;
+      out[r].abandoned = st.abandoned;
+      out[r].engine = Engine::cuda;
+    }
+    return out;
+  }
+
+  tsdd_cuda_stats stats() const {
+    tsdd_cuda_stats st{};
+    tsdd_cuda_get_stats(ctx_, &st);
+    return st;
+  }
+
+ private:
+  void check(int rc) const {
+    if (rc != TSDD_OK) raise_for(rc, tsdd_cuda_last_error(ctx_));
+  }
+  tsdd_cuda_ctx* ctx_ = nullptr;
+};
+
+// The host-only part of check_config that the C ABI does not see
+// (pipeline.cpp:33-41), placed where the reference places it: after the
+// series / n / word_len checks and before alphabet, dictionary, feasibility.
+inline void check_host_fields(const TimeSeries& series, const DiscoveryConfig& config) {
+  char message[512];
+  const int rc = tsdd_cuda_check_config_f64(series.values.data(), series.values.size(), config.n,
+                                            config.word_len, config.alphabet, message, sizeof(message));
+  const std::string text = message;
+  const bool early = rc == TSDD_ERR_VALIDATION ||
+                     (rc == TSDD_ERR_PARAMETER && (text.rfind("n=", 0) == 0 || text.rfind("word_len=", 0) == 0));
+  if (early) raise_for(rc, text);
+  if (config.vec_width < 1) throw ParameterError("vec_width must be >= 1");
+  if (config.threads < 1) throw ParameterError("threads must be >= 1, got " + std::to_string(config.threads));
+  if (config.chunk < 1) throw ParameterError("chunk must be >= 1, got " + std::to_string(config.chunk));
+  raise_for(rc, text);
+}
+
+// tsdd::run_discovery for Engine::cuda: validate everything, then the two
+// timed stages.  `all`, when given, receives the k discords (best first).
+inline RunOutcome run_discovery(const TimeSeries& series, const DiscoveryConfig& config, int k = 1,
+                                std::vector<DiscordResult>* all = nullptr, int device = 0) {
+  check_host_fields(series, config);
+  if (k < 1) throw ParameterError("k must be >= 1, got " + std::to_string(k));
+  Session session(device);
+  session.prepare(series, config.n, config.word_len, config.alphabet);
+  std::vector<DiscordResult> found = session.search(k, config.disable_pruning);
+  const tsdd_cuda_stats st = session.stats();
+  RunOutcome outcome;
+  outcome.result = found.front();
+  outcome.m = series.length();
+  outcome.prep_time_s = (st.prep_ms + st.h2d_ms) * 1e-3;
+  outcome.search_time_s = st.search_ms * 1e-3;
+  if (all) *all = std::move(found);
+  return outcome;
+}
+
+}  // namespace tsdd::cuda
+
+#endif  // TSDD_CUDA_ENGINE_HPP

@@ -275,3 +275,22 @@ def test_nccl_exchange_with_one_rank(chk):
         c.prepare(x, 64, 4, 4)
         pos, dist = c.search(1)
     assert pos[0] == want["position"] and dist[0] == pytest.approx(want["distance"], rel=DIST_RTOL)
+
+
+def test_cpp_host_layer_end_to_end(chk, tmp_path):
+    """include/tsdd/cuda_engine.hpp through tools/tsdd_cuda_find (the `tsdd find` analogue)."""
+    import json
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    x = planted_walk(8, 9000, 96)
+    path = tmp_path / "series.f32le"
+    x.tofile(path)
+    p = subprocess.run([os.path.join(root, "paper_1901_00155_b200", "_lib", "tsdd_cuda_find"), str(path),
+                        "96", "6", "5", "3"], capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr
+    got = json.loads(p.stdout)
+    want = chk.topk(x, 96, 6, 5, 3)
+    assert [d["pos"] for d in got["discords"]] == want["positions"] and got["pos"] == want["positions"][0]
+    np.testing.assert_allclose([d["dist"] for d in got["discords"]], want["distances"], rtol=DIST_RTOL)

@@ -218,3 +218,26 @@ def test_exchange_over_gloo_with_two_ranks(tmp_path):
         assert p.returncode == 0, out
         assert f"rank {r} ok" in out
     assert outs[0].split("ok")[1].split()[:2] == outs[1].split("ok")[1].split()[:2]
+
+
+# ------------------------------------------------------------------ C++ host layer (include/tsdd/cuda_engine.hpp)
+FIND = os.path.join(ROOT, "paper_1901_00155_b200", "_lib", "tsdd_cuda_find")
+
+
+@pytest.mark.parametrize("args,code,text", [
+    (["16", "2", "4"], 2, "no subsequence has a non-self match: N=5 <= n=16 (need m >= 2n)"),
+    (["0", "2", "4"], 2, "n=0 must satisfy 1 <= n <= m=20"),
+    (["4", "9", "4"], 2, "word_len=9 must satisfy 1 <= word_len <= n=4"),
+    (["4", "2", "11"], 2, "alphabet"),
+])
+def test_cpp_layer_maps_errors_to_reference_exit_codes(tmp_path, args, code, text):  # tools/tsdd.cpp:212-223
+    path = tmp_path / "a.f64le"
+    np.arange(20.0).tofile(path)
+    p = subprocess.run([FIND, str(path), *args], capture_output=True, text=True)
+    assert p.returncode == code and text in p.stderr
+    bad = tmp_path / "b.f64le"
+    x = np.arange(20.0)
+    x[6] = np.inf
+    x.tofile(bad)
+    p = subprocess.run([FIND, str(bad), "4", "2", "4"], capture_output=True, text=True)
+    assert p.returncode == 3 and "non-finite value at index 7" in p.stderr
