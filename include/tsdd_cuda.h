@@ -78,8 +78,12 @@ const char* tsdd_cuda_last_error(const tsdd_cuda_ctx* ctx);
 int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream);
 
 /* Tunables, by name: "batch" (candidates per outer-loop batch), "first_batch"
- * (size of the first batch; it doubles up to "batch"), "rounds" (neighbour
- * ranges per batch, compaction between them), "bucket_mates" (same-word
+ * (size of the first batch; it doubles up to "batch"), "first_range" / "growth"
+ * / "rounds" (neighbour rows are visited in ranges: first_range rows, then each
+ * range growth times larger, at most rounds of them; dead candidates are
+ * dropped between ranges), "window_rounds" / "window_first" / "window_growth"
+ * (before that covering scan, each candidate tile visits its own SAX word's
+ * neighbourhood in the hash-sorted order: window_first slots, growing), "bucket_mates" (same-word
  * neighbours tried per row before the scans), "rescore" (0/1: float64
  * re-scoring of each discord's distance), "symmetric" (0/1: completed tiles
  * also lower the neighbours' bounds), "packed" (0/1: f32x2 arithmetic),

@@ -127,9 +127,15 @@ struct tsdd_cuda_ctx {
   std::string error;
 
   // tunables (tsdd_cuda_set_option)
-  uint32_t opt_batch = 8192;
+  uint32_t opt_batch = 16384;
   uint32_t opt_first_batch = 256;
-  int opt_rounds = 7;
+  int opt_rounds = 64;            // upper limit on neighbour ranges per batch
+  uint32_t opt_first_range = 2048;  // rows in the first range
+  double opt_growth = 1.5;          // each range is this much larger than the one before
+  int opt_window_rounds = 4;        // same-word-neighbourhood rounds before the covering scan
+  uint32_t opt_window_first = 2048; // slots in the first of them
+  double opt_window_growth = 3.0;
+  bool opt_rotate = true;           // each batch starts its covering scan at a different row
   int opt_mates = 8;
   bool opt_rescore = true;
   bool opt_symmetric = true;
@@ -143,7 +149,7 @@ struct tsdd_cuda_ctx {
   DeviceArray<float> series_f32;
   DeviceArray<double> series, mean, inv_sigma;
   DeviceArray<float> matrix;
-  DeviceArray<uint32_t> hash0, freq, offsets, slot_bucket, scalars;
+  DeviceArray<uint32_t> hash0, freq, offsets, slot_bucket, scalars, slot_of_row;
   DeviceArray<uint32_t> sort_buf[4], order_buf[4];
   uint32_t *sorted_hash = nullptr, *sorted_row = nullptr, *order = nullptr, *sorted_freq = nullptr;
   DeviceArray<uint32_t> scan_scratch, radix_hist;
@@ -152,7 +158,7 @@ struct tsdd_cuda_ctx {
   DeviceArray<uint64_t> nn, best, xchg;
   DeviceArray<uint8_t> exact, excluded;
   DeviceArray<DeviceCounters> counters;
-  DeviceArray<uint32_t> flags, batch_rows, batch_alt, sel;
+  DeviceArray<uint32_t> flags, batch_rows, batch_alt, batch_slots, batch_slots_alt, sel;
   DeviceArray<float> batch_matrix;
   DeviceArray<double> rescore_out;
   uint32_t batch_capacity = 0;
@@ -247,7 +253,7 @@ void prepare_on_device(tsdd_cuda_ctx* ctx, size_t m, size_t n, size_t word_len, 
   ctx->alphabet = alphabet;
   ctx->rows = rows;
   ctx->stride = round_up_u32(static_cast<uint32_t>(n), kRowAlign);
-  ctx->rows_padded = round_up_u32(rows, kTileRows);
+  ctx->rows_padded = round_up_u32(rows + 1, kTileRows);  // at least one all-zero row after the last
   uint64_t launches = 0;
 
   ctx->mean.alloc(rows);
@@ -284,6 +290,8 @@ void prepare_on_device(tsdd_cuda_ctx* ctx, size_t m, size_t n, size_t word_len, 
                                       ctx->scan_scratch.ptr, st);
   ctx->sorted_hash = k0;
   ctx->sorted_row = v0;
+  ctx->slot_of_row.alloc(rows);
+  launches += launch_invert_order(ctx->sorted_row, rows, ctx->slot_of_row.ptr, st);
 
   ctx->slot_bucket.alloc(rows);
   ctx->offsets.alloc(static_cast<size_t>(rows) + 1);
@@ -412,6 +420,8 @@ void ensure_batch_capacity(tsdd_cuda_ctx* ctx, uint32_t batch) {
   if (padded <= ctx->batch_capacity) return;
   ctx->batch_rows.alloc(padded);
   ctx->batch_alt.alloc(padded);
+  ctx->batch_slots.alloc(padded);
+  ctx->batch_slots_alt.alloc(padded);
   ctx->batch_matrix.alloc(static_cast<size_t>(padded) * ctx->stride);
   ctx->batch_capacity = padded;
 }
@@ -422,48 +432,103 @@ uint32_t read_sel(tsdd_cuda_ctx* ctx) {
   return ctx->h_sel[0];
 }
 
-// Neighbour ranges of one batch: the first is 1/2^(rounds-1) of the rows, each
-// later one as large as everything before it; boundaries on tile multiples.
-std::vector<uint32_t> range_bounds(uint32_t rows, int rounds, bool pruning) {
+// Neighbour ranges of one batch: `first` rows, then each range `growth` times the one
+// before it, at most `rounds` of them (the last takes the rest); boundaries on tile
+// multiples.  Dead candidates are dropped between ranges, so a candidate costs at most
+// `growth` times the rows it needed to meet a neighbour closer than the best-so-far.
+std::vector<uint32_t> range_bounds(uint32_t rows, int rounds, uint32_t first, double growth, bool pruning) {
   std::vector<uint32_t> bounds{0};
   if (pruning) {
+    double size = std::max<double>(first, kTileRows);
+    uint64_t at = 0;
     for (int r = 1; r < rounds; ++r) {
-      uint64_t b = static_cast<uint64_t>(rows) >> (rounds - r);
-      b = b / kTileRows * kTileRows;
-      if (b > bounds.back() && b < rows) bounds.push_back(static_cast<uint32_t>(b));
+      at += static_cast<uint64_t>(size) / kTileRows * kTileRows;
+      if (at >= rows) break;
+      bounds.push_back(static_cast<uint32_t>(at));
+      size *= growth;
     }
   }
   bounds.push_back(rows);
   return bounds;
 }
 
+struct Segment {
+  bool window;              // same-word neighbourhood (bounds only) or covering scan
+  uint32_t k_begin, k_end;  // neighbour tile numbers
+};
+
+// The neighbour tiles one batch visits, in order; dead candidates are dropped between
+// segments.  First the window rounds around each candidate tile's own SAX word (the
+// HOTSAX inner heuristic), then the covering scan of all rows in growing ranges.
+std::vector<Segment> plan_segments(const tsdd_cuda_ctx* ctx, bool pruning) {
+  std::vector<Segment> plan;
+  const uint32_t slot_tiles = (ctx->rows + kTileRows - 1) / kTileRows;
+  if (pruning) {
+    // the windows only lower bounds (their rows are met again by the covering scan):
+    // keep them to an eighth of the rows
+    const uint32_t window_limit = slot_tiles / 8;
+    double size = std::max<double>(ctx->opt_window_first, kTileRows);
+    uint32_t at = 0;
+    for (int r = 0; r < ctx->opt_window_rounds && at < window_limit; ++r) {
+      const uint32_t upto = std::min<uint64_t>(window_limit, at + static_cast<uint64_t>(size) / kTileRows);
+      plan.push_back({true, at, upto});
+      at = upto;
+      size *= ctx->opt_window_growth;
+    }
+  }
+  const std::vector<uint32_t> bounds =
+      range_bounds(ctx->rows, ctx->opt_rounds, ctx->opt_first_range, ctx->opt_growth, pruning);
+  for (size_t r = 0; r + 1 < bounds.size(); ++r)
+    plan.push_back({false, bounds[r] / kTileRows, (bounds[r + 1] + kTileRows - 1) / kTileRows});
+  return plan;
+}
+
 void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
   cudaStream_t st = ctx->stream;
   SearchState s = ctx->state();
-  const std::vector<uint32_t> bounds = range_bounds(ctx->rows, ctx->opt_rounds, pruning);
-  uint32_t* list = ctx->batch_rows.ptr;
-  uint32_t* alt = ctx->batch_alt.ptr;
   uint64_t launches = 0;
-  for (size_t r = 0; r + 1 < bounds.size(); ++r) {
+
+  // word-coherent candidate tiles: sort the batch by slot in the hash-sorted order
+  uint32_t *list = ctx->batch_rows.ptr, *list_alt = ctx->batch_alt.ptr;
+  uint32_t *slots = ctx->batch_slots.ptr, *slots_alt = ctx->batch_slots_alt.ptr;
+  const bool use_windows = pruning && ctx->opt_window_rounds > 0;
+  if (use_windows) {
+    launches += launch_batch_slots(list, ctx->sel.ptr, ctx->slot_of_row.ptr, count, slots, st);
+    launches += launch_radix_sort_pairs(&slots, &list, &slots_alt, &list_alt, count, bits_for(ctx->rows),
+                                        ctx->radix_hist.ptr, ctx->scan_scratch.ptr, st);
+  }
+
+  // Every batch starts its covering scan somewhere else (golden-ratio steps around the
+  // ring of tiles), so that the rows whose bounds drop as a by-product (d(i,j) = d(j,i))
+  // are spread over the whole series instead of always being the first ones.
+  const uint32_t slot_tiles = (ctx->rows + kTileRows - 1) / kTileRows;
+  const uint32_t rotation =
+      (pruning && ctx->opt_rotate)
+          ? static_cast<uint32_t>((ctx->stats.batches * 0.6180339887498949 - std::floor(ctx->stats.batches * 0.6180339887498949)) * slot_tiles) % slot_tiles
+          : 0u;
+  const std::vector<Segment> plan = plan_segments(ctx, pruning);
+  for (size_t r = 0; r < plan.size(); ++r) {
     if (r > 0 && pruning) {
-      launches += launch_compact_batch(s, list, alt, ctx->batch_capacity, pruning, ctx->sel.ptr, st);
-      std::swap(list, alt);
+      launches += launch_compact_batch(s, list, slots, list_alt, slots_alt, pruning, ctx->sel.ptr, st);
+      std::swap(list, list_alt);
+      std::swap(slots, slots_alt);
       count = read_sel(ctx);
       if (count == 0) break;
     }
     const uint32_t padded = round_up_u32(count, kTileRows);
     launches += launch_gather_rows(s, list, ctx->sel.ptr, padded, ctx->batch_matrix.ptr, st);
-    const uint32_t range_tiles = (bounds[r + 1] - bounds[r] + kTileRows - 1) / kTileRows;
-    const uint64_t tiles = static_cast<uint64_t>(range_tiles) * (padded / kTileRows);
-    int per_cta = static_cast<int>(std::min<uint64_t>(16, std::max<uint64_t>(1, tiles / (148ull * 8ull))));
+    const uint64_t tiles = static_cast<uint64_t>(plan[r].k_end - plan[r].k_begin) * (padded / kTileRows);
+    const int per_cta = static_cast<int>(std::min<uint64_t>(16, std::max<uint64_t>(1, tiles / (148ull * 8ull))));
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->opt_time_kernels) {
       e0 = next_event(ctx);
       e1 = next_event(ctx);
       CUDA_OK(cudaEventRecord(e0, st));
     }
-    const int launched = launch_scan_tiles(s, ctx->batch_matrix.ptr, list, ctx->sel.ptr, padded, bounds[r],
-                                           bounds[r + 1], per_cta, pruning, ctx->opt_symmetric, st);
+    const int launched =
+        launch_scan_tiles(s, ctx->batch_matrix.ptr, list, slots, ctx->sel.ptr, padded,
+                          plan[r].window ? ctx->sorted_row : nullptr, plan[r].k_begin, plan[r].k_end, rotation,
+                          per_cta, pruning, ctx->opt_symmetric, st);
     if (ctx->opt_time_kernels) CUDA_OK(cudaEventRecord(e1, st));
     launches += launched;
     ctx->stats.scan_kernel_launches += launched;
@@ -707,8 +772,25 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
       if (value < 1 || value > 1048576) fail(TSDD_ERR_PARAMETER, "first_batch must be in 1..1048576");
       ctx->opt_first_batch = static_cast<uint32_t>(value);
     } else if (key == "rounds") {
-      if (value < 1 || value > 24) fail(TSDD_ERR_PARAMETER, "rounds must be in 1..24");
+      if (value < 1 || value > 4096) fail(TSDD_ERR_PARAMETER, "rounds must be in 1..4096");
       ctx->opt_rounds = static_cast<int>(value);
+    } else if (key == "first_range") {
+      if (value < 128 || value > 1e9) fail(TSDD_ERR_PARAMETER, "first_range must be in 128..1e9");
+      ctx->opt_first_range = static_cast<uint32_t>(value);
+    } else if (key == "window_rounds") {
+      if (value < 0 || value > 64) fail(TSDD_ERR_PARAMETER, "window_rounds must be in 0..64");
+      ctx->opt_window_rounds = static_cast<int>(value);
+    } else if (key == "window_first") {
+      if (value < 128 || value > 1e9) fail(TSDD_ERR_PARAMETER, "window_first must be in 128..1e9");
+      ctx->opt_window_first = static_cast<uint32_t>(value);
+    } else if (key == "window_growth") {
+      if (value < 1.0 || value > 16.0) fail(TSDD_ERR_PARAMETER, "window_growth must be in 1..16");
+      ctx->opt_window_growth = value;
+    } else if (key == "rotate") {
+      ctx->opt_rotate = value != 0;
+    } else if (key == "growth") {
+      if (value < 1.0 || value > 16.0) fail(TSDD_ERR_PARAMETER, "growth must be in 1..16");
+      ctx->opt_growth = value;
     } else if (key == "bucket_mates") {
       if (value < 0 || value > 1024) fail(TSDD_ERR_PARAMETER, "bucket_mates must be in 0..1024");
       ctx->opt_mates = static_cast<int>(value);

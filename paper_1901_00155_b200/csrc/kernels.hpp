@@ -85,20 +85,30 @@ int launch_select_batch(SearchState s, const uint32_t* d_order, uint32_t cursor,
                         uint32_t* d_scan_scratch, uint32_t* d_batch_rows, uint32_t* d_sel,
                         cudaStream_t stream);
 
-// Drops dead candidates from the batch list (stable); count lives in d_sel[0].
-int launch_compact_batch(SearchState s, uint32_t* d_batch_rows, uint32_t* d_batch_alt,
-                         uint32_t capacity, bool pruning, uint32_t* d_sel, cudaStream_t stream);
+// Drops dead candidates from the batch list (stable); rows and hash-order slots move
+// together; count lives in d_sel[0].
+int launch_compact_batch(SearchState s, uint32_t* d_batch_rows, uint32_t* d_batch_slots, uint32_t* d_rows_alt,
+                         uint32_t* d_slots_alt, bool pruning, uint32_t* d_sel, cudaStream_t stream);
+
+// slot_of_row = inverse permutation of the hash-sorted row list.
+int launch_invert_order(const uint32_t* d_sorted_row, uint32_t rows, uint32_t* d_slot_of_row,
+                        cudaStream_t stream);
+// keys[i] = slot_of_row[batch_rows[i]] for i < sel[0].
+int launch_batch_slots(const uint32_t* d_batch_rows, const uint32_t* d_sel, const uint32_t* d_slot_of_row,
+                       uint32_t capacity, uint32_t* d_keys, cudaStream_t stream);
 
 // Copies the batch's matrix rows into a dense [capacity_padded x stride] buffer.
 int launch_gather_rows(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,
                        uint32_t capacity_padded, float* d_batch_matrix, cudaStream_t stream);
 
-// The tiled early-abandoning distance kernel: batch candidates x neighbour
-// rows [j_begin, j_end).
+// The tiled early-abandoning distance kernel: batch candidates x neighbour tiles
+// [k_begin, k_end).  d_nbr_index == nullptr: tile k holds the 128 rows of tile
+// (k + rotation) mod T (the covering scan).  Otherwise (window mode) tile k holds 128 slots of d_nbr_index (the
+// hash-sorted row list) around the candidate tile's own slot, alternating outwards.
 int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t* d_batch_rows,
-                      const uint32_t* d_sel, uint32_t capacity_padded, uint32_t j_begin,
-                      uint32_t j_end, int tiles_per_cta, bool pruning, bool symmetric,
-                      cudaStream_t stream);
+                      const uint32_t* d_batch_slots, const uint32_t* d_sel, uint32_t capacity_padded,
+                      const uint32_t* d_nbr_index, uint32_t k_begin, uint32_t k_end, uint32_t rotation,
+                      int tiles_per_cta, bool pruning, bool symmetric, cudaStream_t stream);
 
 // Survivors of a complete scan are exact; each raises the best-so-far.
 int launch_finalize_batch(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,

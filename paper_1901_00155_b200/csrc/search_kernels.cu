@@ -164,11 +164,12 @@ __global__ void k_take_batch(const uint32_t* __restrict__ order, const uint32_t*
   }
 }
 
-// Stable in-place compaction of the batch list (a single block; a batch is a
-// few thousand rows).  sel[0] is read and rewritten.
+// Stable compaction of the batch list (a single block; a batch is a few
+// thousand rows): rows and their hash-order slots move together.  sel[0] is
+// read and rewritten.
 __global__ void __launch_bounds__(1024)
-k_compact_batch(SearchState s, const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
-                int pruning, uint32_t* sel) {
+k_compact_batch(SearchState s, const uint32_t* __restrict__ in, const uint32_t* __restrict__ in_slots,
+                uint32_t* __restrict__ out, uint32_t* __restrict__ out_slots, int pruning, uint32_t* sel) {
   __shared__ uint32_t warp_sums[32];
   __shared__ uint32_t carry;
   const uint32_t count = sel[0];
@@ -177,10 +178,11 @@ k_compact_batch(SearchState s, const uint32_t* __restrict__ in, uint32_t* __rest
   __syncthreads();
   for (uint32_t base = 0; base < count; base += blockDim.x) {
     const uint32_t idx = base + threadIdx.x;
-    uint32_t row = 0;
+    uint32_t row = 0, slot = 0;
     bool keep = false;
     if (idx < count) {
       row = in[idx];
+      slot = in_slots[idx];
       keep = !pruning || !is_dead(load_key(s.nn + row), row, best);
     }
     const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, keep);
@@ -193,12 +195,30 @@ k_compact_batch(SearchState s, const uint32_t* __restrict__ in, uint32_t* __rest
       if (w < warp) before += c;
       total += c;
     }
-    if (keep) out[before + __popc(ballot & ((1u << lane) - 1u))] = row;
+    if (keep) {
+      const uint32_t at = before + __popc(ballot & ((1u << lane) - 1u));
+      out[at] = row;
+      out_slots[at] = slot;
+    }
     __syncthreads();
     if (threadIdx.x == 0) carry += total;
     __syncthreads();
   }
   if (threadIdx.x == 0) sel[0] = carry;
+}
+
+// slot_of_row[sorted_row[s]] = s: where each row sits in the hash-sorted order.
+__global__ void k_invert_order(const uint32_t* __restrict__ sorted_row, uint32_t rows,
+                               uint32_t* __restrict__ slot_of_row) {
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < rows) slot_of_row[sorted_row[s]] = s;
+}
+
+// keys[i] = hash-order slot of batch row i (the sort key that makes tiles word-coherent)
+__global__ void k_batch_slots(const uint32_t* __restrict__ batch_rows, const uint32_t* __restrict__ sel,
+                              const uint32_t* __restrict__ slot_of_row, uint32_t* __restrict__ keys) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < sel[0]) keys[i] = slot_of_row[batch_rows[i]];
 }
 
 // Dense copy of the batch's rows, NEGATED, so that the tile kernel forms
@@ -274,7 +294,7 @@ constexpr int kStages = 4;
 constexpr int kOperandBytes = kTileRows * kChunk * 4;  // 16 KiB: 128 rows x 32 columns
 constexpr int kStageBytes = 2 * kOperandBytes;
 constexpr int kScanThreads = 256;
-constexpr size_t kScanSmem = static_cast<size_t>(kStages) * kStageBytes + 3 * kTileRows * 4;
+constexpr size_t kScanSmem = static_cast<size_t>(kStages) * kStageBytes + 5 * kTileRows * 4;
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
   const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
@@ -286,16 +306,20 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(kPending));
 }
 
-// Issues this thread's share (4 + 4 pieces of 16 bytes) of one stage.
+// Issues this thread's share (4 + 4 pieces of 16 bytes) of one stage.  The
+// neighbour rows are addressed through s_brow (row numbers in shared memory),
+// so a tile may hold any 128 rows: every piece is still one 16-byte part of a
+// full 128-byte line.
 __device__ __forceinline__ void issue_stage(unsigned char* stage, const float* a_tile,
-                                            const float* b_tile, uint32_t stride, uint32_t col0) {
+                                            const float* rows, const uint32_t* s_brow,
+                                            uint32_t stride, uint32_t col0) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const uint32_t piece = threadIdx.x + q * kScanThreads;  // 0..1023
     const uint32_t r = piece >> 3, kc = piece & 7;
     const uint32_t off = r * 128 + ((kc ^ (r & 7)) << 4);
     cp_async16(stage + off, a_tile + static_cast<size_t>(r) * stride + col0 + kc * 4);
-    cp_async16(stage + kOperandBytes + off, b_tile + static_cast<size_t>(r) * stride + col0 + kc * 4);
+    cp_async16(stage + kOperandBytes + off, rows + static_cast<size_t>(s_brow[r]) * stride + col0 + kc * 4);
   }
 }
 
@@ -340,47 +364,76 @@ struct Acc<true> {
   }
 };
 
+// Which 128 neighbour rows tile number k of a scan holds.
+//   global mode (nbr_index == nullptr): rows [128t, 128t + 128), t = (k + rotation)
+//     mod T — every row exactly once over k = 0 .. T-1 whatever the rotation; this
+//     is the scan that makes a survivor exact.
+//   window mode: slots of the hash-sorted order around the candidate tile's own
+//     bucket, alternating outwards (own tile, +1, -1, +2, ...), wrapping at the
+//     ends — the HOTSAX "same word first" heuristic (discovery.cpp:51-63)
+//     widened to neighbouring words.  It only lowers bounds; coverage is not
+//     counted, so re-centring after a compaction is harmless.
+struct ScanArgs {
+  const float* batch;          // dense, negated candidate rows
+  const uint32_t* batch_rows;  // candidate row numbers
+  const uint32_t* batch_slots; // their slots in the hash-sorted order (window mode)
+  const uint32_t* sel;         // sel[0] = live batch size
+  const uint32_t* nbr_index;   // hash-sorted row list (window mode) or nullptr
+  uint32_t k_begin, k_end;     // tile numbers of this launch
+  uint32_t rotation;           // global mode: tile k holds rows of tile (k + rotation) mod T
+  int tiles_per_cta;
+  int pruning;
+};
+
 template <bool kPacked, bool kSymmetric>
 __global__ void __launch_bounds__(kScanThreads, 1)
-k_scan_tiles(SearchState s, const float* __restrict__ batch, const uint32_t* __restrict__ batch_rows,
-             const uint32_t* __restrict__ sel, uint32_t j_begin, uint32_t j_end, int tiles_per_cta,
-             int pruning) {
+k_scan_tiles(SearchState s, ScanArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   float* s_thr = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // candidate thresholds
   uint32_t* s_cand = reinterpret_cast<uint32_t*>(s_thr + kTileRows);      // candidate rows
   float* s_nub = reinterpret_cast<float*>(s_cand + kTileRows);            // neighbours' own bounds
+  uint32_t* s_jrow = reinterpret_cast<uint32_t*>(s_nub + kTileRows);      // neighbour rows, ~0 = none
+  uint32_t* s_brow = s_jrow + kTileRows;                                  // rows to load (none -> zero row)
   __shared__ unsigned long long s_calls, s_abandoned, s_terms;
 
-  const uint32_t count = sel[0];
+  const uint32_t count = a.sel[0];
   const uint32_t cand0 = blockIdx.y * kTileRows;
   if (cand0 >= count) return;
 
   const uint32_t tid = threadIdx.x, lane = tid & 31;
   const uint32_t tx = tid & 15, ty = tid >> 4;
-  if (tid < kTileRows) s_cand[tid] = (cand0 + tid < count) ? batch_rows[cand0 + tid] : 0xFFFFFFFFu;
+  if (tid < kTileRows) s_cand[tid] = (cand0 + tid < count) ? a.batch_rows[cand0 + tid] : 0xFFFFFFFFu;
   if (tid == 0) {
     s_calls = 0;
     s_abandoned = 0;
     s_terms = 0;
   }
-  const uint64_t best = pruning ? *s.best : 0ull;
+  const bool window = a.nbr_index != nullptr;
+  const uint32_t slot_tiles = (s.n_rows + kTileRows - 1) / kTileRows;
+  const uint32_t centre = window ? a.batch_slots[min(cand0 + kTileRows / 2, count - 1)] / kTileRows : 0u;
+  const uint64_t best = a.pruning ? *s.best : 0ull;
   const uint32_t chunks = s.stride / kChunk;
-  const float* a_tile = batch + static_cast<size_t>(cand0) * s.stride;
-  const uint32_t first_tile = j_begin / kTileRows + blockIdx.x * tiles_per_cta;
+  const float* a_tile = a.batch + static_cast<size_t>(cand0) * s.stride;
   const float inf = __uint_as_float(kInfBits);
 
-  for (int tt = 0; tt < tiles_per_cta; ++tt) {
-    const uint32_t j0 = (first_tile + tt) * kTileRows;
-    if (j0 >= j_end) break;
-    __syncthreads();  // s_cand visible; everyone is done with the previous tile's s_thr / stages
+  for (int tt = 0; tt < a.tiles_per_cta; ++tt) {
+    const uint32_t k = a.k_begin + blockIdx.x * a.tiles_per_cta + tt;
+    if (k >= a.k_end) break;
+    uint32_t slot_tile = (k + a.rotation) % slot_tiles;
+    if (window) {
+      const uint32_t step = (k + 1) >> 1;  // 0, 1, 1, 2, 2, ...
+      slot_tile = (k & 1) ? (centre + step) % slot_tiles : (centre + slot_tiles - step % slot_tiles) % slot_tiles;
+    }
+    const uint32_t slot0 = slot_tile * kTileRows;
+    __syncthreads();  // s_cand visible; everyone is done with the previous tile's shared arrays
 
-    // ---- refresh thresholds, count the pairs this tile starts
+    // ---- refresh thresholds, fetch the neighbour rows of this tile
     bool live = false;
     if (tid < kTileRows) {
       const uint32_t row = s_cand[tid];
       float thr = -1.f;
       if (row != 0xFFFFFFFFu) {
-        if (!pruning) {
+        if (!a.pruning) {
           thr = inf;
           live = true;
         } else {
@@ -393,20 +446,31 @@ k_scan_tiles(SearchState s, const float* __restrict__ batch, const uint32_t* __r
       }
       s_thr[tid] = thr;
     } else {
-      const uint32_t j = j0 + (tid - kTileRows);
-      s_nub[tid - kTileRows] = (j < s.n_rows && j < j_end) ? __uint_as_float(key_bits(load_key(s.nn + j))) : -1.f;
+      const uint32_t t = tid - kTileRows;
+      const uint32_t slot = slot0 + t;
+      uint32_t j = 0xFFFFFFFFu;
+      if (slot < s.n_rows) j = window ? a.nbr_index[slot] : slot;
+      s_jrow[t] = j;
+      s_brow[t] = j != 0xFFFFFFFFu ? j : s.n_rows;  // row n_rows is zero padding
+      s_nub[t] = j != 0xFFFFFFFFu ? __uint_as_float(key_bits(load_key(s.nn + j))) : -1.f;
     }
     if (!__syncthreads_or(live)) break;  // every candidate of this tile is dead: nothing left to do
 
     unsigned long long my_calls = 0;
     if (live) {
       const uint32_t row = s_cand[tid];
-      const uint32_t j1 = min(min(j0 + kTileRows, s.n_rows), j_end);  // exclusive
-      // neighbours of this tile inside the self-match zone (row - n, row + n)
-      const uint32_t z0 = row >= s.n - 1 ? row - (s.n - 1) : 0;
-      const uint32_t z1 = row + s.n;  // exclusive
-      const uint32_t o0 = max(j0, z0), o1 = min(j1, z1);
-      my_calls = (j1 - j0) - (o1 > o0 ? o1 - o0 : 0);
+      const uint32_t valid = min(kTileRows, s.n_rows - slot0);
+      uint32_t overlap = 0;
+      if (!window) {
+        // contiguous rows [slot0, slot0 + valid): the self-match zone is an interval
+        const uint32_t z0 = row >= s.n - 1 ? row - (s.n - 1) : 0;
+        const uint32_t z1 = row + s.n;  // exclusive
+        const uint32_t o0 = max(slot0, z0), o1 = min(slot0 + valid, z1);
+        overlap = o1 > o0 ? o1 - o0 : 0;
+      } else {
+        for (uint32_t q = 0; q < valid; ++q) overlap += gap_u32(row, s_jrow[q]) < s.n ? 1u : 0u;
+      }
+      my_calls = valid - overlap;
     }
 
     float thr[8];
@@ -416,10 +480,10 @@ k_scan_tiles(SearchState s, const float* __restrict__ batch, const uint32_t* __r
     Acc<kPacked> acc;
     acc.zero();
 
-    const float* b_tile = s.rows + static_cast<size_t>(j0) * s.stride;
 #pragma unroll
     for (int st = 0; st < kStages - 1; ++st) {
-      if (static_cast<uint32_t>(st) < chunks) issue_stage(smem + st * kStageBytes, a_tile, b_tile, s.stride, st * kChunk);
+      if (static_cast<uint32_t>(st) < chunks)
+        issue_stage(smem + st * kStageBytes, a_tile, s.rows, s_brow, s.stride, st * kChunk);
       cp_async_commit();
     }
 
@@ -432,7 +496,7 @@ k_scan_tiles(SearchState s, const float* __restrict__ batch, const uint32_t* __r
         break;
       }
       if (c + kStages - 1 < chunks)
-        issue_stage(smem + ((c + kStages - 1) % kStages) * kStageBytes, a_tile, b_tile, s.stride,
+        issue_stage(smem + ((c + kStages - 1) % kStages) * kStageBytes, a_tile, s.rows, s_brow, s.stride,
                     (c + kStages - 1) * kChunk);
       cp_async_commit();
       if (!warp_done) {
@@ -481,12 +545,12 @@ k_scan_tiles(SearchState s, const float* __restrict__ batch, const uint32_t* __r
       const uint32_t row = s_cand[ty + 16 * u];
 #pragma unroll
       for (int w = 0; w < 8; ++w) {
-        const uint32_t j = j0 + tx + 16 * w;
+        const uint32_t j = s_jrow[tx + 16 * w];
         const float d = acc.get(u, w);
-        const bool pair_ok = row != 0xFFFFFFFFu && j < s.n_rows && j < j_end && gap_u32(row, j) >= s.n;
+        const bool pair_ok = row != 0xFFFFFFFFu && j != 0xFFFFFFFFu && gap_u32(row, j) >= s.n;
         if (pair_ok && d <= thr[u]) {
-          const uint64_t k = nn_key(__float_as_uint(d), j);
-          cand_best[u] = k < cand_best[u] ? k : cand_best[u];
+          const uint64_t key = nn_key(__float_as_uint(d), j);
+          cand_best[u] = key < cand_best[u] ? key : cand_best[u];
           any_update = true;
         }
         if (kSymmetric && complete && pair_ok && d < s_nub[tx + 16 * w])
@@ -496,14 +560,14 @@ k_scan_tiles(SearchState s, const float* __restrict__ batch, const uint32_t* __r
     if (__any_sync(0xFFFFFFFFu, any_update)) {
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        uint64_t k = cand_best[u];
+        uint64_t key = cand_best[u];
 #pragma unroll
         for (int d = 8; d > 0; d >>= 1) {
-          const uint64_t other = __shfl_xor_sync(0xFFFFFFFFu, k, d);
-          k = other < k ? other : k;
+          const uint64_t other = __shfl_xor_sync(0xFFFFFFFFu, key, d);
+          key = other < key ? other : key;
         }
-        if (tx == 0 && k != ~0ull)
-          atomicMin(as_ull(s.nn + s_cand[ty + 16 * u]), static_cast<unsigned long long>(k));
+        if (tx == 0 && key != ~0ull)
+          atomicMin(as_ull(s.nn + s_cand[ty + 16 * u]), static_cast<unsigned long long>(key));
       }
     }
   }
@@ -573,10 +637,22 @@ int launch_select_batch(SearchState s, const uint32_t* d_order, uint32_t cursor,
   return launches + 1;
 }
 
-int launch_compact_batch(SearchState s, uint32_t* d_batch_rows, uint32_t* d_batch_alt,
-                         uint32_t capacity, bool pruning, uint32_t* d_sel, cudaStream_t stream) {
-  (void)capacity;
-  k_compact_batch<<<1, 1024, 0, stream>>>(s, d_batch_rows, d_batch_alt, pruning ? 1 : 0, d_sel);
+int launch_compact_batch(SearchState s, uint32_t* d_batch_rows, uint32_t* d_batch_slots, uint32_t* d_rows_alt,
+                         uint32_t* d_slots_alt, bool pruning, uint32_t* d_sel, cudaStream_t stream) {
+  k_compact_batch<<<1, 1024, 0, stream>>>(s, d_batch_rows, d_batch_slots, d_rows_alt, d_slots_alt,
+                                          pruning ? 1 : 0, d_sel);
+  return 1;
+}
+
+int launch_invert_order(const uint32_t* d_sorted_row, uint32_t rows, uint32_t* d_slot_of_row,
+                        cudaStream_t stream) {
+  k_invert_order<<<blocks_for(rows, 256), 256, 0, stream>>>(d_sorted_row, rows, d_slot_of_row);
+  return 1;
+}
+
+int launch_batch_slots(const uint32_t* d_batch_rows, const uint32_t* d_sel, const uint32_t* d_slot_of_row,
+                       uint32_t capacity, uint32_t* d_keys, cudaStream_t stream) {
+  k_batch_slots<<<blocks_for(capacity, 256), 256, 0, stream>>>(d_batch_rows, d_sel, d_slot_of_row, d_keys);
   return 1;
 }
 
@@ -588,9 +664,9 @@ int launch_gather_rows(SearchState s, const uint32_t* d_batch_rows, const uint32
 }
 
 int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t* d_batch_rows,
-                      const uint32_t* d_sel, uint32_t capacity_padded, uint32_t j_begin,
-                      uint32_t j_end, int tiles_per_cta, bool pruning, bool symmetric,
-                      cudaStream_t stream) {
+                      const uint32_t* d_batch_slots, const uint32_t* d_sel, uint32_t capacity_padded,
+                      const uint32_t* d_nbr_index, uint32_t k_begin, uint32_t k_end, uint32_t rotation,
+                      int tiles_per_cta, bool pruning, bool symmetric, cudaStream_t stream) {
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(k_scan_tiles<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kScanSmem));
@@ -599,20 +675,21 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
     cudaFuncSetAttribute(k_scan_tiles<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kScanSmem));
     configured = true;
   }
-  if (j_end <= j_begin) return 0;
-  const uint32_t tiles = (j_end - j_begin + kTileRows - 1) / kTileRows;
+  if (k_end <= k_begin) return 0;
+  const uint32_t tiles = k_end - k_begin;
   dim3 grid((tiles + tiles_per_cta - 1) / tiles_per_cta, capacity_padded / kTileRows);
-  const int p = pruning ? 1 : 0;
+  ScanArgs a{d_batch_matrix, d_batch_rows, d_batch_slots, d_sel, d_nbr_index, k_begin, k_end, rotation,
+             tiles_per_cta, pruning ? 1 : 0};
   if (g_packed_default) {
     if (symmetric)
-      k_scan_tiles<true, true><<<grid, kScanThreads, kScanSmem, stream>>>(s, d_batch_matrix, d_batch_rows, d_sel, j_begin, j_end, tiles_per_cta, p);
+      k_scan_tiles<true, true><<<grid, kScanThreads, kScanSmem, stream>>>(s, a);
     else
-      k_scan_tiles<true, false><<<grid, kScanThreads, kScanSmem, stream>>>(s, d_batch_matrix, d_batch_rows, d_sel, j_begin, j_end, tiles_per_cta, p);
+      k_scan_tiles<true, false><<<grid, kScanThreads, kScanSmem, stream>>>(s, a);
   } else {
     if (symmetric)
-      k_scan_tiles<false, true><<<grid, kScanThreads, kScanSmem, stream>>>(s, d_batch_matrix, d_batch_rows, d_sel, j_begin, j_end, tiles_per_cta, p);
+      k_scan_tiles<false, true><<<grid, kScanThreads, kScanSmem, stream>>>(s, a);
     else
-      k_scan_tiles<false, false><<<grid, kScanThreads, kScanSmem, stream>>>(s, d_batch_matrix, d_batch_rows, d_sel, j_begin, j_end, tiles_per_cta, p);
+      k_scan_tiles<false, false><<<grid, kScanThreads, kScanSmem, stream>>>(s, a);
   }
   return 1;
 }

@@ -165,7 +165,7 @@ def test_search_is_repeatable_and_independent_of_tunables(ctx):
         again = ctx.search(3)
         assert again[0] == base[0], name
         np.testing.assert_allclose(again[1], base[1], rtol=1e-6, err_msg=name)
-    for name, value in [("batch", 8192), ("rounds", 7), ("bucket_mates", 8), ("symmetric", 1),
+    for name, value in [("batch", 8192), ("rounds", 64), ("bucket_mates", 8), ("symmetric", 1),
                         ("packed", 1), ("first_batch", 256)]:
         ctx.set_option(name, value)
 

@@ -1,0 +1,16 @@
+#!/bin/bash
+# usage: tools/sweep.sh "<cfgs>" "opts1" "opts2" ...   (each opts: "name=value name=value")
+cfgs="$1"; shift
+for o in "$@"; do
+  args=""
+  for kv in $o; do args="$args --opt $kv"; done
+  echo "### $o"
+  python tools/run_workload.py $cfgs $args 2>&1 | python -c "
+import sys, json
+for line in sys.stdin:
+    try: r = json.loads(line)
+    except Exception: print(line.strip()); continue
+    s = r['stats']
+    print('cfg%d pos=%s ok=%s prep=%.1fms search=%.1fms scan=%.1fms calls=%.3g terms=%.3g batches=%d scanned=%d launches=%d terms/s=%.3g' % (r['cfg'], r['positions'][:2], r['golden_match'], s['prep_ms'], s['search_ms'], s['scan_kernel_ms'], s['calls'], s['terms'], s['batches'], s['scanned_candidates'], s['kernel_launches'], r['terms_per_s']))
+"
+done
