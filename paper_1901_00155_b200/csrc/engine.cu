@@ -23,6 +23,7 @@
 
 namespace tsdd_b200 {
 void set_packed_math(bool on);
+void set_wide_tile(bool on);
 }
 
 namespace {
@@ -140,6 +141,7 @@ struct tsdd_cuda_ctx {
   bool opt_rescore = true;
   bool opt_symmetric = true;
   bool opt_packed = true;
+  bool opt_wide_tile = false;
   bool opt_time_kernels = true;
 
   // prepared series
@@ -462,7 +464,8 @@ struct Segment {
 // HOTSAX inner heuristic), then the covering scan of all rows in growing ranges.
 std::vector<Segment> plan_segments(const tsdd_cuda_ctx* ctx, bool pruning) {
   std::vector<Segment> plan;
-  const uint32_t slot_tiles = (ctx->rows + kTileRows - 1) / kTileRows;
+  const uint32_t tile = scan_neighbour_tile_rows();
+  const uint32_t slot_tiles = (ctx->rows + tile - 1) / tile;
   if (pruning) {
     // the windows only lower bounds (their rows are met again by the covering scan):
     // keep them to an eighth of the rows
@@ -470,7 +473,7 @@ std::vector<Segment> plan_segments(const tsdd_cuda_ctx* ctx, bool pruning) {
     double size = std::max<double>(ctx->opt_window_first, kTileRows);
     uint32_t at = 0;
     for (int r = 0; r < ctx->opt_window_rounds && at < window_limit; ++r) {
-      const uint32_t upto = std::min<uint64_t>(window_limit, at + static_cast<uint64_t>(size) / kTileRows);
+      const uint32_t upto = std::min<uint64_t>(window_limit, at + static_cast<uint64_t>(size) / tile);
       plan.push_back({true, at, upto});
       at = upto;
       size *= ctx->opt_window_growth;
@@ -479,7 +482,7 @@ std::vector<Segment> plan_segments(const tsdd_cuda_ctx* ctx, bool pruning) {
   const std::vector<uint32_t> bounds =
       range_bounds(ctx->rows, ctx->opt_rounds, ctx->opt_first_range, ctx->opt_growth, pruning);
   for (size_t r = 0; r + 1 < bounds.size(); ++r)
-    plan.push_back({false, bounds[r] / kTileRows, (bounds[r + 1] + kTileRows - 1) / kTileRows});
+    plan.push_back({false, bounds[r] / tile, (bounds[r + 1] + tile - 1) / tile});
   return plan;
 }
 
@@ -501,7 +504,8 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
   // Every batch starts its covering scan somewhere else (golden-ratio steps around the
   // ring of tiles), so that the rows whose bounds drop as a by-product (d(i,j) = d(j,i))
   // are spread over the whole series instead of always being the first ones.
-  const uint32_t slot_tiles = (ctx->rows + kTileRows - 1) / kTileRows;
+  const uint32_t tile = scan_neighbour_tile_rows();
+  const uint32_t slot_tiles = (ctx->rows + tile - 1) / tile;
   const uint32_t rotation =
       (pruning && ctx->opt_rotate)
           ? static_cast<uint32_t>((ctx->stats.batches * 0.6180339887498949 - std::floor(ctx->stats.batches * 0.6180339887498949)) * slot_tiles) % slot_tiles
@@ -518,7 +522,8 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
     const uint32_t padded = round_up_u32(count, kTileRows);
     launches += launch_gather_rows(s, list, ctx->sel.ptr, padded, ctx->batch_matrix.ptr, st);
     const uint64_t tiles = static_cast<uint64_t>(plan[r].k_end - plan[r].k_begin) * (padded / kTileRows);
-    const int per_cta = static_cast<int>(std::min<uint64_t>(16, std::max<uint64_t>(1, tiles / (148ull * 8ull))));
+    const uint64_t resident = 148ull * (tile == 64 ? 2 : 1);
+    const int per_cta = static_cast<int>(std::min<uint64_t>(16, std::max<uint64_t>(1, tiles / (resident * 8ull))));
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->opt_time_kernels) {
       e0 = next_event(ctx);
@@ -596,6 +601,7 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   if (!positions || !distances) fail(TSDD_ERR_PARAMETER, "positions and distances must not be null");
   bind_device(ctx);
   set_packed_math(ctx->opt_packed);
+  set_wide_tile(ctx->opt_wide_tile);
   const bool pruning = (flags & TSDD_SEARCH_DISABLE_PRUNING) == 0;
   cudaStream_t st = ctx->stream;
   SearchState s = ctx->state();
@@ -800,6 +806,8 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
       ctx->opt_symmetric = value != 0;
     } else if (key == "packed") {
       ctx->opt_packed = value != 0;
+    } else if (key == "wide_tile") {
+      ctx->opt_wide_tile = value != 0;
     } else if (key == "time_kernels") {
       ctx->opt_time_kernels = value != 0;
     } else {

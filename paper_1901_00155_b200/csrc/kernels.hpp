@@ -110,6 +110,10 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
                       const uint32_t* d_nbr_index, uint32_t k_begin, uint32_t k_end, uint32_t rotation,
                       int tiles_per_cta, bool pruning, bool symmetric, cudaStream_t stream);
 
+// Neighbour rows per tile of the variant launch_scan_tiles currently uses (64 or 128):
+// the unit of k_begin / k_end / rotation.
+uint32_t scan_neighbour_tile_rows();
+
 // Survivors of a complete scan are exact; each raises the best-so-far.
 int launch_finalize_batch(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,
                           uint32_t capacity, bool pruning, cudaStream_t stream);

@@ -291,10 +291,11 @@ k_finalize_batch(SearchState s, const uint32_t* __restrict__ batch_rows,
 // computing, and the CTA leaves the tile when every warp has.  Dead candidates
 // carry the threshold -1 and never hold a tile open.
 constexpr int kStages = 4;
-constexpr int kOperandBytes = kTileRows * kChunk * 4;  // 16 KiB: 128 rows x 32 columns
-constexpr int kStageBytes = 2 * kOperandBytes;
+constexpr int kOperandBytes = kTileRows * kChunk * 4;  // 16 KiB: 128 candidate rows x 32 columns
 constexpr int kScanThreads = 256;
-constexpr size_t kScanSmem = static_cast<size_t>(kStages) * kStageBytes + 5 * kTileRows * 4;
+constexpr size_t scan_smem_bytes(int nbr_rows) {
+  return static_cast<size_t>(kStages) * (kOperandBytes + nbr_rows * kChunk * 4) + 5 * kTileRows * 4;
+}
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
   const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
@@ -306,33 +307,42 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(kPending));
 }
 
-// Issues this thread's share (4 + 4 pieces of 16 bytes) of one stage.  The
-// neighbour rows are addressed through s_brow (row numbers in shared memory),
-// so a tile may hold any 128 rows: every piece is still one 16-byte part of a
-// full 128-byte line.
+// Issues this thread's share of one stage (1024 + 1024 pieces of 16 bytes per
+// CTA).  The neighbour rows are addressed through s_brow (row numbers in shared
+// memory), so a tile may hold any 128 rows: every piece is still one 16-byte
+// part of a full 128-byte line.
+template <int kNbr>
 __device__ __forceinline__ void issue_stage(unsigned char* stage, const float* a_tile,
                                             const float* rows, const uint32_t* s_brow,
                                             uint32_t stride, uint32_t col0) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const uint32_t piece = threadIdx.x + q * kScanThreads;  // 0..1023
+  for (int q = 0; q < kTileRows * 8 / kScanThreads; ++q) {  // candidate rows: 1024 pieces
+    const uint32_t piece = threadIdx.x + q * kScanThreads;
     const uint32_t r = piece >> 3, kc = piece & 7;
-    const uint32_t off = r * 128 + ((kc ^ (r & 7)) << 4);
-    cp_async16(stage + off, a_tile + static_cast<size_t>(r) * stride + col0 + kc * 4);
-    cp_async16(stage + kOperandBytes + off, rows + static_cast<size_t>(s_brow[r]) * stride + col0 + kc * 4);
+    cp_async16(stage + r * 128 + ((kc ^ (r & 7)) << 4), a_tile + static_cast<size_t>(r) * stride + col0 + kc * 4);
+  }
+#pragma unroll
+  for (int q = 0; q < kNbr * 8 / kScanThreads; ++q) {  // neighbour rows: 512 or 1024 pieces
+    const uint32_t piece = threadIdx.x + q * kScanThreads;
+    const uint32_t r = piece >> 3, kc = piece & 7;
+    cp_async16(stage + kOperandBytes + r * 128 + ((kc ^ (r & 7)) << 4),
+               rows + static_cast<size_t>(s_brow[r]) * stride + col0 + kc * 4);
   }
 }
 
-template <bool kPacked>
+// Per-thread accumulators of a kU x kW block of pairs.  Packed: two partial
+// sums per pair (even / odd columns) in one 64-bit register pair, updated with
+// add.f32x2 / fma.rn.f32x2.
+template <bool kPacked, int kU, int kW>
 struct Acc;
-template <>
-struct Acc<false> {
-  float v[8][8];
+template <int kU, int kW>
+struct Acc<false, kU, kW> {
+  float v[kU][kW];
   __device__ __forceinline__ void zero() {
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < kU; ++u)
 #pragma unroll
-      for (int w = 0; w < 8; ++w) v[u][w] = 0.f;
+      for (int w = 0; w < kW; ++w) v[u][w] = 0.f;
   }
   __device__ __forceinline__ float get(int u, int w) const { return v[u][w]; }
   __device__ __forceinline__ void add(int u, int w, const float4& na, const float4& b) {
@@ -346,14 +356,14 @@ struct Acc<false> {
     v[u][w] = fmaf(d, d, v[u][w]);
   }
 };
-template <>
-struct Acc<true> {
-  float2 v[8][8];
+template <int kU, int kW>
+struct Acc<true, kU, kW> {
+  float2 v[kU][kW];
   __device__ __forceinline__ void zero() {
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < kU; ++u)
 #pragma unroll
-      for (int w = 0; w < 8; ++w) v[u][w] = make_float2(0.f, 0.f);
+      for (int w = 0; w < kW; ++w) v[u][w] = make_float2(0.f, 0.f);
   }
   __device__ __forceinline__ float get(int u, int w) const { return v[u][w].x + v[u][w].y; }
   __device__ __forceinline__ void add(int u, int w, const float4& na, const float4& b) {
@@ -364,8 +374,8 @@ struct Acc<true> {
   }
 };
 
-// Which 128 neighbour rows tile number k of a scan holds.
-//   global mode (nbr_index == nullptr): rows [128t, 128t + 128), t = (k + rotation)
+// Which neighbour rows (kNbr = 64 or 128 of them) tile number k of a scan holds.
+//   global mode (nbr_index == nullptr): rows [kNbr t, kNbr t + kNbr), t = (k + rotation)
 //     mod T — every row exactly once over k = 0 .. T-1 whatever the rotation; this
 //     is the scan that makes a survivor exact.
 //   window mode: slots of the hash-sorted order around the candidate tile's own
@@ -385,9 +395,18 @@ struct ScanArgs {
   int pruning;
 };
 
-template <bool kPacked, bool kSymmetric>
-__global__ void __launch_bounds__(kScanThreads, 1)
+// CTA = 256 threads = 16 x 16; thread (ty, tx) owns the pairs {ty + 16u} x {tx + 16w},
+// u < 8, w < kW.  kW = 8: a 128 x 128 tile, 255 registers, one CTA per SM.  kW = 4: a
+// 128 x 64 tile, <= 128 registers and 98 KB of shared memory, so TWO CTAs share an SM
+// and one computes while the other sits in its per-chunk barrier, threshold refresh or
+// pipeline refill (with one CTA per SM all warps leave the FMA pipe idle together).
+template <bool kPacked, bool kSymmetric, int kW>
+__global__ void __launch_bounds__(kScanThreads, kW == 4 ? 2 : 1)
 k_scan_tiles(SearchState s, ScanArgs a) {
+  constexpr int kU = 8;
+  constexpr int kTx = 16;
+  constexpr int kNbr = kTx * kW;                              // neighbour rows per tile
+  constexpr int kStageBytes = kOperandBytes + kNbr * kChunk * 4;
   extern __shared__ __align__(1024) unsigned char smem[];
   float* s_thr = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // candidate thresholds
   uint32_t* s_cand = reinterpret_cast<uint32_t*>(s_thr + kTileRows);      // candidate rows
@@ -401,7 +420,8 @@ k_scan_tiles(SearchState s, ScanArgs a) {
   if (cand0 >= count) return;
 
   const uint32_t tid = threadIdx.x, lane = tid & 31;
-  const uint32_t tx = tid & 15, ty = tid >> 4;
+  const uint32_t tx = tid % kTx, ty = tid / kTx;
+  static_assert(kScanThreads == 16 * kTx, "thread grid is 16 x 16");
   if (tid < kTileRows) s_cand[tid] = (cand0 + tid < count) ? a.batch_rows[cand0 + tid] : 0xFFFFFFFFu;
   if (tid == 0) {
     s_calls = 0;
@@ -409,8 +429,8 @@ k_scan_tiles(SearchState s, ScanArgs a) {
     s_terms = 0;
   }
   const bool window = a.nbr_index != nullptr;
-  const uint32_t slot_tiles = (s.n_rows + kTileRows - 1) / kTileRows;
-  const uint32_t centre = window ? a.batch_slots[min(cand0 + kTileRows / 2, count - 1)] / kTileRows : 0u;
+  const uint32_t slot_tiles = (s.n_rows + kNbr - 1) / kNbr;
+  const uint32_t centre = window ? a.batch_slots[min(cand0 + kTileRows / 2, count - 1)] / kNbr : 0u;
   const uint64_t best = a.pruning ? *s.best : 0ull;
   const uint32_t chunks = s.stride / kChunk;
   const float* a_tile = a.batch + static_cast<size_t>(cand0) * s.stride;
@@ -424,7 +444,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
       const uint32_t step = (k + 1) >> 1;  // 0, 1, 1, 2, 2, ...
       slot_tile = (k & 1) ? (centre + step) % slot_tiles : (centre + slot_tiles - step % slot_tiles) % slot_tiles;
     }
-    const uint32_t slot0 = slot_tile * kTileRows;
+    const uint32_t slot0 = slot_tile * kNbr;
     __syncthreads();  // s_cand visible; everyone is done with the previous tile's shared arrays
 
     // ---- refresh thresholds, fetch the neighbour rows of this tile
@@ -445,7 +465,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
         }
       }
       s_thr[tid] = thr;
-    } else {
+    } else if (tid < kTileRows + kNbr) {
       const uint32_t t = tid - kTileRows;
       const uint32_t slot = slot0 + t;
       uint32_t j = 0xFFFFFFFFu;
@@ -459,7 +479,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
     unsigned long long my_calls = 0;
     if (live) {
       const uint32_t row = s_cand[tid];
-      const uint32_t valid = min(kTileRows, s.n_rows - slot0);
+      const uint32_t valid = min(static_cast<uint32_t>(kNbr), s.n_rows - slot0);
       uint32_t overlap = 0;
       if (!window) {
         // contiguous rows [slot0, slot0 + valid): the self-match zone is an interval
@@ -473,17 +493,17 @@ k_scan_tiles(SearchState s, ScanArgs a) {
       my_calls = valid - overlap;
     }
 
-    float thr[8];
+    float thr[kU];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) thr[u] = s_thr[ty + 16 * u];
+    for (int u = 0; u < kU; ++u) thr[u] = s_thr[ty + 16 * u];
 
-    Acc<kPacked> acc;
+    Acc<kPacked, kU, kW> acc;
     acc.zero();
 
 #pragma unroll
     for (int st = 0; st < kStages - 1; ++st) {
       if (static_cast<uint32_t>(st) < chunks)
-        issue_stage(smem + st * kStageBytes, a_tile, s.rows, s_brow, s.stride, st * kChunk);
+        issue_stage<kNbr>(smem + st * kStageBytes, a_tile, s.rows, s_brow, s.stride, st * kChunk);
       cp_async_commit();
     }
 
@@ -496,31 +516,45 @@ k_scan_tiles(SearchState s, ScanArgs a) {
         break;
       }
       if (c + kStages - 1 < chunks)
-        issue_stage(smem + ((c + kStages - 1) % kStages) * kStageBytes, a_tile, s.rows, s_brow, s.stride,
-                    (c + kStages - 1) * kChunk);
+        issue_stage<kNbr>(smem + ((c + kStages - 1) % kStages) * kStageBytes, a_tile, s.rows, s_brow,
+                          s.stride, (c + kStages - 1) * kChunk);
       cp_async_commit();
       if (!warp_done) {
         const unsigned char* a_s = smem + (c % kStages) * kStageBytes + ty * 128;
-        const unsigned char* b_s = smem + (c % kStages) * kStageBytes + kOperandBytes + tx * 128;
+        const unsigned char* b_s = smem + (c % kStages) * kStageBytes + kOperandBytes + tx * 128;  // rows tx + kTx*w
 #pragma unroll 2
         for (int kc = 0; kc < 8; ++kc) {
           const uint32_t off_a = (kc ^ (ty & 7)) << 4, off_b = (kc ^ (tx & 7)) << 4;
-          float4 na[8];
+          if constexpr (kW == 8) {
+            float4 na[kU];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) na[u] = *reinterpret_cast<const float4*>(a_s + u * 2048 + off_a);
+            for (int u = 0; u < kU; ++u) na[u] = *reinterpret_cast<const float4*>(a_s + u * 2048 + off_a);
 #pragma unroll
-          for (int w = 0; w < 8; ++w) {
-            const float4 b = *reinterpret_cast<const float4*>(b_s + w * 2048 + off_b);
+            for (int w = 0; w < kW; ++w) {
+              const float4 b = *reinterpret_cast<const float4*>(b_s + w * (kTx * 128) + off_b);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) acc.add(u, w, na[u], b);
+              for (int u = 0; u < kU; ++u) acc.add(u, w, na[u], b);
+            }
+          } else {
+            // hold the neighbours, stream the candidates (a warp shares one candidate
+            // row per u: its LDS.128 is a broadcast)
+            float4 b[kW];
+#pragma unroll
+            for (int w = 0; w < kW; ++w) b[w] = *reinterpret_cast<const float4*>(b_s + w * (kTx * 128) + off_b);
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+              const float4 na = *reinterpret_cast<const float4*>(a_s + u * 2048 + off_a);
+#pragma unroll
+              for (int w = 0; w < kW; ++w) acc.add(u, w, na, b[w]);
+            }
           }
         }
         ++warp_chunks;
         bool all_over = true;
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < kU; ++u)
 #pragma unroll
-          for (int w = 0; w < 8; ++w) all_over = all_over && (acc.get(u, w) > thr[u]);
+          for (int w = 0; w < kW; ++w) all_over = all_over && (acc.get(u, w) > thr[u]);
         mine_abandoned = all_over;
         warp_done = __all_sync(0xFFFFFFFFu, all_over);
       }
@@ -528,7 +562,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
     cp_async_wait<0>();
 
     // ---- accounting (per warp: the terms its lanes really accumulated)
-    if (lane == 0) atomicAdd(&s_terms, static_cast<unsigned long long>(warp_chunks) * kChunk * 16 * kTileRows);
+    if (lane == 0) atomicAdd(&s_terms, static_cast<unsigned long long>(warp_chunks) * kChunk * 32 * kU * kW);
     if (my_calls) {
       atomicAdd(&s_calls, my_calls);
       if (cta_abandoned) atomicAdd(&s_abandoned, my_calls);
@@ -537,15 +571,15 @@ k_scan_tiles(SearchState s, ScanArgs a) {
 
     // ---- completed tile: lower the candidates' bounds (and, symmetric, the neighbours')
     const bool complete = (warp_chunks == chunks);
-    uint64_t cand_best[8];
+    uint64_t cand_best[kU];
     bool any_update = false;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < kU; ++u) {
       cand_best[u] = ~0ull;
       const uint32_t row = s_cand[ty + 16 * u];
 #pragma unroll
-      for (int w = 0; w < 8; ++w) {
-        const uint32_t j = s_jrow[tx + 16 * w];
+      for (int w = 0; w < kW; ++w) {
+        const uint32_t j = s_jrow[tx + kTx * w];
         const float d = acc.get(u, w);
         const bool pair_ok = row != 0xFFFFFFFFu && j != 0xFFFFFFFFu && gap_u32(row, j) >= s.n;
         if (pair_ok && d <= thr[u]) {
@@ -553,16 +587,16 @@ k_scan_tiles(SearchState s, ScanArgs a) {
           cand_best[u] = key < cand_best[u] ? key : cand_best[u];
           any_update = true;
         }
-        if (kSymmetric && complete && pair_ok && d < s_nub[tx + 16 * w])
+        if (kSymmetric && complete && pair_ok && d < s_nub[tx + kTx * w])
           atomicMin(as_ull(s.nn + j), static_cast<unsigned long long>(nn_key(__float_as_uint(d), row)));
       }
     }
     if (__any_sync(0xFFFFFFFFu, any_update)) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < kU; ++u) {
         uint64_t key = cand_best[u];
 #pragma unroll
-        for (int d = 8; d > 0; d >>= 1) {
+        for (int d = kTx / 2; d > 0; d >>= 1) {  // the kTx lanes that share candidate u
           const uint64_t other = __shfl_xor_sync(0xFFFFFFFFu, key, d);
           key = other < key ? other : key;
         }
@@ -605,6 +639,7 @@ k_rescore_pair(const double* __restrict__ x, const double* __restrict__ mean,
 }
 
 bool g_packed_default = true;
+bool g_wide_tile = false;  // true: 128 x 128 tile, one CTA per SM; false: 128 x 64 tile, two CTAs per SM
 
 }  // namespace
 
@@ -667,34 +702,34 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
                       const uint32_t* d_batch_slots, const uint32_t* d_sel, uint32_t capacity_padded,
                       const uint32_t* d_nbr_index, uint32_t k_begin, uint32_t k_end, uint32_t rotation,
                       int tiles_per_cta, bool pruning, bool symmetric, cudaStream_t stream) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_scan_tiles<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kScanSmem));
-    cudaFuncSetAttribute(k_scan_tiles<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kScanSmem));
-    cudaFuncSetAttribute(k_scan_tiles<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kScanSmem));
-    cudaFuncSetAttribute(k_scan_tiles<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kScanSmem));
-    configured = true;
-  }
   if (k_end <= k_begin) return 0;
   const uint32_t tiles = k_end - k_begin;
   dim3 grid((tiles + tiles_per_cta - 1) / tiles_per_cta, capacity_padded / kTileRows);
   ScanArgs a{d_batch_matrix, d_batch_rows, d_batch_slots, d_sel, d_nbr_index, k_begin, k_end, rotation,
              tiles_per_cta, pruning ? 1 : 0};
-  if (g_packed_default) {
-    if (symmetric)
-      k_scan_tiles<true, true><<<grid, kScanThreads, kScanSmem, stream>>>(s, a);
-    else
-      k_scan_tiles<true, false><<<grid, kScanThreads, kScanSmem, stream>>>(s, a);
-  } else {
-    if (symmetric)
-      k_scan_tiles<false, true><<<grid, kScanThreads, kScanSmem, stream>>>(s, a);
-    else
-      k_scan_tiles<false, false><<<grid, kScanThreads, kScanSmem, stream>>>(s, a);
+  auto launch = [&](auto kernel, int nbr_rows) {
+    const int smem = static_cast<int>(scan_smem_bytes(nbr_rows));
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    kernel<<<grid, kScanThreads, smem, stream>>>(s, a);
+  };
+  const int shape = (g_packed_default ? 4 : 0) | (symmetric ? 2 : 0) | (g_wide_tile ? 1 : 0);
+  switch (shape) {
+    case 7: launch(k_scan_tiles<true, true, 8>, 128); break;
+    case 6: launch(k_scan_tiles<true, true, 4>, 64); break;
+    case 5: launch(k_scan_tiles<true, false, 8>, 128); break;
+    case 4: launch(k_scan_tiles<true, false, 4>, 64); break;
+    case 3: launch(k_scan_tiles<false, true, 8>, 128); break;
+    case 2: launch(k_scan_tiles<false, true, 4>, 64); break;
+    case 1: launch(k_scan_tiles<false, false, 8>, 128); break;
+    default: launch(k_scan_tiles<false, false, 4>, 64); break;
   }
   return 1;
 }
 
+uint32_t scan_neighbour_tile_rows() { return g_wide_tile ? 128u : 64u; }
+
 void set_packed_math(bool on) { g_packed_default = on; }
+void set_wide_tile(bool on) { g_wide_tile = on; }
 
 int launch_finalize_batch(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,
                           uint32_t capacity, bool pruning, cudaStream_t stream) {
