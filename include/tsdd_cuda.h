@@ -152,7 +152,7 @@ int tsdd_cuda_get_stats(const tsdd_cuda_ctx* ctx, tsdd_cuda_stats* out);
 #define TSDD_FETCH_NN_SQ 11     /* float  [N]           current nn upper bounds (squared)      */
 #define TSDD_FETCH_NN_EXACT 12  /* uint8  [N]           1 where NN_SQ is the exact nn          */
 
-/* Row stride of TSDD_FETCH_ROWS in floats (n rounded up to 32; padding is 0). */
+/* Row stride of TSDD_FETCH_ROWS in floats (n rounded up to a multiple of 64; padding is 0). */
 size_t tsdd_cuda_row_stride(const tsdd_cuda_ctx* ctx);
 
 /* Copies one prepared array to host memory.  bytes must be the exact size. */
@@ -182,7 +182,8 @@ int tsdd_cuda_set_exchange(tsdd_cuda_ctx* ctx, tsdd_exchange_fn fn, void* user, 
 /* FP32 issue-rate probes on the context's device (roofline denominators the
  * driver's MEASURED_PEAKS.json does not have).  which: 0 = dependent-free
  * FFMA stream, 1 = FSUB+FFMA pairs (the distance kernel's mix), 2 = packed
- * fma.rn.f32x2, 3 = packed sub+fma f32x2.  Returns lane-operations per second
+ * fma.rn.f32x2, 3 = packed sub+fma f32x2; +4 = the same at 8 warps per SM, +8 = at
+ * 16 warps per SM (the tile kernels' occupancies).  Returns lane-operations per second
  * in *ops_per_s (one FFMA = one op; an f32x2 instruction = two).            */
 int tsdd_cuda_fp32_probe(tsdd_cuda_ctx* ctx, int which, double* ops_per_s, double* ms);
 

@@ -25,7 +25,7 @@ CUDA_HEADERS = ["common.cuh", "kernels.hpp", os.path.join(INCLUDE, "tsdd_cuda.h"
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
     "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC,
-]
+] + os.environ.get("TSDD_NVCC_EXTRA", "").split()  # e.g. "-DTSDD_SCAN_CHUNK=32 -DTSDD_SCAN_STAGES=4"
 HOST_CXX = "/usr/bin/g++"
 
 

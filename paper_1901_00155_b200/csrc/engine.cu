@@ -1017,9 +1017,33 @@ int tsdd_cuda_set_exchange(tsdd_cuda_ctx* ctx, tsdd_exchange_fn fn, void* user, 
 int tsdd_cuda_fp32_probe(tsdd_cuda_ctx* ctx, int which, double* ops_per_s, double* ms_out) {
   if (!ctx) return TSDD_ERR_PARAMETER;
   return guarded(ctx, [&] {
-    if (which < 0 || which > 3) fail(TSDD_ERR_PARAMETER, "probe selector must be 0..3");
+    if (which >= 16 && which <= 19) {  // packed + scalar mixes (see probe_kernels.cu)
+      bind_device(ctx);
+      const int blocks = 148 * 8, iters = 4096;
+      DeviceArray<float> sink;
+      sink.alloc(static_cast<size_t>(blocks) * 256);
+      launch_fp32_probe(which, sink.ptr, blocks, 64, ctx->stream);
+      float best_ms = 1e30f;
+      for (int rep = 0; rep < 5; ++rep) {
+        CUDA_OK(cudaEventRecord(ctx->ev_a, ctx->stream));
+        launch_fp32_probe(which, sink.ptr, blocks, iters, ctx->stream);
+        CUDA_OK(cudaEventRecord(ctx->ev_b, ctx->stream));
+        sync_stream(ctx);
+        float ms = 0.f;
+        CUDA_OK(cudaEventElapsedTime(&ms, ctx->ev_a, ctx->ev_b));
+        best_ms = std::min(best_ms, ms);
+      }
+      if (ops_per_s) *ops_per_s = fp32_probe_ops(which, blocks, iters) / (best_ms * 1e-3);
+      if (ms_out) *ms_out = best_ms;
+      return;
+    }
+    if (which < 0 || which > 11) fail(TSDD_ERR_PARAMETER, "probe selector must be 0..11 or 16..19");
     bind_device(ctx);
-    const int blocks = 148 * 8, iters = 4096;
+    // 0..3: 64 warps per SM; 4..7: the same mixes at 8 warps per SM (the 128 x 128 tile
+    // kernel's occupancy); 8..11: at 16 warps per SM (the 128 x 64 tile kernel's)
+    const int blocks = which < 4 ? 148 * 8 : which < 8 ? 148 : 148 * 2;
+    const int iters = 4096;
+    which &= 3;
     DeviceArray<float> sink;
     sink.alloc(static_cast<size_t>(blocks) * 256);
     launch_fp32_probe(which, sink.ptr, blocks, 64, ctx->stream);  // warm-up

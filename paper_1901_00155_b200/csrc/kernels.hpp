@@ -14,8 +14,14 @@
 namespace tsdd_b200 {
 
 constexpr int kTileRows = 128;     // candidates per tile == neighbours per tile
-constexpr int kChunk = 32;         // columns per pipeline stage (one 128-byte line per row)
-constexpr uint32_t kRowAlign = 32; // row stride is a multiple of 32 floats
+#ifndef TSDD_SCAN_CHUNK
+#define TSDD_SCAN_CHUNK 64
+#endif
+#ifndef TSDD_SCAN_STAGES
+#define TSDD_SCAN_STAGES 2
+#endif
+constexpr int kChunk = TSDD_SCAN_CHUNK;  // columns per pipeline stage (kChunk*4 bytes of every row)
+constexpr uint32_t kRowAlign = kChunk;   // row stride is a multiple of this many floats
 
 // ------------------------------------------------------------------ preparation
 int launch_widen_series(const float* d_in, double* d_out, size_t m, cudaStream_t stream);

@@ -16,6 +16,7 @@
 
 #include "kernels.hpp"
 
+
 namespace tsdd_b200 {
 
 namespace {
@@ -276,25 +277,29 @@ k_finalize_batch(SearchState s, const uint32_t* __restrict__ batch_rows,
 
 // ------------------------------------------------------------------ the tiled distance kernel
 //
-// CTA = 256 threads = one tile of 128 candidates x 128 neighbour rows; thread
-// (ty, tx) of a 16 x 16 grid owns the 8 x 8 pairs {ty + 16u} x {tx + 16v}.
-// Columns stream through shared memory 32 at a time (one 128-byte line per
-// row and stage) in a kStages-deep cp.async ring; the 16-byte pieces of a line
-// are XOR-swizzled with the row number so that the float4 reads of 16 rows in
-// a half-warp are conflict-free.  Candidate rows arrive negated (k_gather_rows),
-// so a term is one add and one fma — packed two columns at a time as
-// add.f32x2 / fma.rn.f32x2 in the kPacked variant.
+// CTA = 256 threads = a tile of 128 candidates x kNbr neighbour rows (64 by
+// default, two CTAs per SM; 128 with "wide_tile"); thread (ty, tx) of a 16 x 16
+// grid owns the pairs {ty + 16u} x {tx + 16w}.  Columns stream through shared
+// memory kChunk (64) at a time in a kStages-deep cp.async ring — a 64-column
+// stage is ~16k cycles of arithmetic per CTA, many times the L2/HBM latency,
+// so two stages suffice and leave room for the second CTA.  The 16-byte
+// pieces of a row are XOR-swizzled with the row number so that the LDS.128 of
+// the rows of a quarter-warp are conflict-free.  Candidate rows arrive negated
+// (k_gather_rows), so a term is one add and one fma — packed two columns at a
+// time as add.f32x2 / fma.rn.f32x2 (FADD2 / FFMA2) in the kPacked variant.
 //
-// Early abandoning (series.hpp:117-146 on a tile): after every 32 columns a
-// thread checks whether all of its 64 partial sums already exceed their
-// candidates' running minimum; a warp whose pairs have all abandoned stops
-// computing, and the CTA leaves the tile when every warp has.  Dead candidates
-// carry the threshold -1 and never hold a tile open.
-constexpr int kStages = 4;
-constexpr int kOperandBytes = kTileRows * kChunk * 4;  // 16 KiB: 128 candidate rows x 32 columns
+// Early abandoning (series.hpp:117-146 on a tile): after every chunk a thread
+// checks whether all of its partial sums already exceed their candidates'
+// running minimum; a warp whose pairs have all abandoned stops computing, and
+// the CTA leaves the tile when every warp has.  Dead candidates carry the
+// threshold -1 and never hold a tile open.
+constexpr int kStages = TSDD_SCAN_STAGES;
+constexpr int kRowBytes = kChunk * 4;   // bytes of one row inside a stage
+constexpr int kPieces = kChunk / 4;     // 16-byte pieces per row and stage
+constexpr int kOperandBytes = kTileRows * kChunk * 4;  // the 128 candidate rows of a stage
 constexpr int kScanThreads = 256;
 constexpr size_t scan_smem_bytes(int nbr_rows) {
-  return static_cast<size_t>(kStages) * (kOperandBytes + nbr_rows * kChunk * 4) + 5 * kTileRows * 4;
+  return static_cast<size_t>(kStages) * (kOperandBytes + nbr_rows * kChunk * 4) + 6 * kTileRows * 4;
 }
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
@@ -316,16 +321,16 @@ __device__ __forceinline__ void issue_stage(unsigned char* stage, const float* a
                                             const float* rows, const uint32_t* s_brow,
                                             uint32_t stride, uint32_t col0) {
 #pragma unroll
-  for (int q = 0; q < kTileRows * 8 / kScanThreads; ++q) {  // candidate rows: 1024 pieces
+  for (int q = 0; q < kTileRows * kPieces / kScanThreads; ++q) {  // candidate rows
     const uint32_t piece = threadIdx.x + q * kScanThreads;
-    const uint32_t r = piece >> 3, kc = piece & 7;
-    cp_async16(stage + r * 128 + ((kc ^ (r & 7)) << 4), a_tile + static_cast<size_t>(r) * stride + col0 + kc * 4);
+    const uint32_t r = piece / kPieces, kc = piece % kPieces;
+    cp_async16(stage + r * kRowBytes + ((kc ^ (r & 7)) << 4), a_tile + static_cast<size_t>(r) * stride + col0 + kc * 4);
   }
 #pragma unroll
-  for (int q = 0; q < kNbr * 8 / kScanThreads; ++q) {  // neighbour rows: 512 or 1024 pieces
+  for (int q = 0; q < kNbr * kPieces / kScanThreads; ++q) {  // neighbour rows
     const uint32_t piece = threadIdx.x + q * kScanThreads;
-    const uint32_t r = piece >> 3, kc = piece & 7;
-    cp_async16(stage + kOperandBytes + r * 128 + ((kc ^ (r & 7)) << 4),
+    const uint32_t r = piece / kPieces, kc = piece % kPieces;
+    cp_async16(stage + kOperandBytes + r * kRowBytes + ((kc ^ (r & 7)) << 4),
                rows + static_cast<size_t>(s_brow[r]) * stride + col0 + kc * 4);
   }
 }
@@ -413,6 +418,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
   float* s_nub = reinterpret_cast<float*>(s_cand + kTileRows);            // neighbours' own bounds
   uint32_t* s_jrow = reinterpret_cast<uint32_t*>(s_nub + kTileRows);      // neighbour rows, ~0 = none
   uint32_t* s_brow = s_jrow + kTileRows;                                  // rows to load (none -> zero row)
+  float* s_loc = reinterpret_cast<float*>(s_brow + kTileRows);            // bounds this CTA found itself
   __shared__ unsigned long long s_calls, s_abandoned, s_terms;
 
   const uint32_t count = a.sel[0];
@@ -436,18 +442,40 @@ k_scan_tiles(SearchState s, ScanArgs a) {
   const float* a_tile = a.batch + static_cast<size_t>(cand0) * s.stride;
   const float inf = __uint_as_float(kInfBits);
 
-  for (int tt = 0; tt < a.tiles_per_cta; ++tt) {
-    const uint32_t k = a.k_begin + blockIdx.x * a.tiles_per_cta + tt;
-    if (k >= a.k_end) break;
-    uint32_t slot_tile = (k + a.rotation) % slot_tiles;
-    if (window) {
-      const uint32_t step = (k + 1) >> 1;  // 0, 1, 1, 2, 2, ...
-      slot_tile = (k & 1) ? (centre + step) % slot_tiles : (centre + slot_tiles - step % slot_tiles) % slot_tiles;
+  auto slot_tile_of = [&](uint32_t k) -> uint32_t {
+    if (!window) return (k + a.rotation) % slot_tiles;
+    const uint32_t step = (k + 1) >> 1;  // 0, 1, 1, 2, 2, ...
+    return (k & 1) ? (centre + step) % slot_tiles : (centre + slot_tiles - step % slot_tiles) % slot_tiles;
+  };
+  // The bounds a tile starts from are fetched one tile ahead (two dependent global
+  // loads in window mode), so their latency hides behind the previous tile's
+  // arithmetic.  A bound that is one tile stale is larger, never smaller: it
+  // abandons less, and s_loc folds in what this CTA itself has found meanwhile.
+  uint64_t pf_key = 0;
+  uint32_t pf_j = 0xFFFFFFFFu;
+  auto prefetch = [&](uint32_t k) {
+    if (tid < kTileRows) {
+      const uint32_t row = s_cand[tid];
+      pf_key = (row != 0xFFFFFFFFu && a.pruning) ? load_key(s.nn + row) : 0ull;
+    } else if (tid < kTileRows + kNbr) {
+      const uint32_t slot = slot_tile_of(k) * kNbr + (tid - kTileRows);
+      pf_j = 0xFFFFFFFFu;
+      if (slot < s.n_rows) pf_j = window ? a.nbr_index[slot] : slot;
+      pf_key = pf_j != 0xFFFFFFFFu ? load_key(s.nn + pf_j) : 0ull;
     }
-    const uint32_t slot0 = slot_tile * kNbr;
-    __syncthreads();  // s_cand visible; everyone is done with the previous tile's shared arrays
+  };
+  if (tid < kTileRows) s_loc[tid] = inf;
+  __syncthreads();  // s_cand visible
+  const uint32_t k_first = a.k_begin + blockIdx.x * a.tiles_per_cta;
+  if (k_first < a.k_end) prefetch(k_first);
 
-    // ---- refresh thresholds, fetch the neighbour rows of this tile
+  for (int tt = 0; tt < a.tiles_per_cta; ++tt) {
+    const uint32_t k = k_first + tt;
+    if (k >= a.k_end) break;
+    const uint32_t slot0 = slot_tile_of(k) * kNbr;
+    __syncthreads();  // everyone is done with the previous tile's shared arrays
+
+    // ---- thresholds and neighbour rows of this tile, from the prefetched registers
     bool live = false;
     if (tid < kTileRows) {
       const uint32_t row = s_cand[tid];
@@ -457,9 +485,9 @@ k_scan_tiles(SearchState s, ScanArgs a) {
           thr = inf;
           live = true;
         } else {
-          const uint64_t key = load_key(s.nn + row);
-          if (!is_dead(key, row, best)) {
-            thr = __uint_as_float(key_bits(key));
+          const float bound = fminf(__uint_as_float(key_bits(pf_key)), s_loc[tid]);
+          if (!(best_key(__float_as_uint(bound), row) < best)) {
+            thr = bound;
             live = true;
           }
         }
@@ -467,14 +495,12 @@ k_scan_tiles(SearchState s, ScanArgs a) {
       s_thr[tid] = thr;
     } else if (tid < kTileRows + kNbr) {
       const uint32_t t = tid - kTileRows;
-      const uint32_t slot = slot0 + t;
-      uint32_t j = 0xFFFFFFFFu;
-      if (slot < s.n_rows) j = window ? a.nbr_index[slot] : slot;
-      s_jrow[t] = j;
-      s_brow[t] = j != 0xFFFFFFFFu ? j : s.n_rows;  // row n_rows is zero padding
-      s_nub[t] = j != 0xFFFFFFFFu ? __uint_as_float(key_bits(load_key(s.nn + j))) : -1.f;
+      s_jrow[t] = pf_j;
+      s_brow[t] = pf_j != 0xFFFFFFFFu ? pf_j : s.n_rows;  // row n_rows is zero padding
+      s_nub[t] = pf_j != 0xFFFFFFFFu ? __uint_as_float(key_bits(pf_key)) : -1.f;
     }
     if (!__syncthreads_or(live)) break;  // every candidate of this tile is dead: nothing left to do
+    if (tt + 1 < a.tiles_per_cta && k + 1 < a.k_end) prefetch(k + 1);
 
     unsigned long long my_calls = 0;
     if (live) {
@@ -488,7 +514,13 @@ k_scan_tiles(SearchState s, ScanArgs a) {
         const uint32_t o0 = max(slot0, z0), o1 = min(slot0 + valid, z1);
         overlap = o1 > o0 ? o1 - o0 : 0;
       } else {
-        for (uint32_t q = 0; q < valid; ++q) overlap += gap_u32(row, s_jrow[q]) < s.n ? 1u : 0u;
+        const uint4* jr = reinterpret_cast<const uint4*>(s_jrow);  // empty entries are ~0: far away
+#pragma unroll 4
+        for (int q = 0; q < kNbr / 4; ++q) {
+          const uint4 v = jr[q];
+          overlap += (gap_u32(row, v.x) < s.n ? 1u : 0u) + (gap_u32(row, v.y) < s.n ? 1u : 0u) +
+                     (gap_u32(row, v.z) < s.n ? 1u : 0u) + (gap_u32(row, v.w) < s.n ? 1u : 0u);
+        }
       }
       my_calls = valid - overlap;
     }
@@ -520,18 +552,18 @@ k_scan_tiles(SearchState s, ScanArgs a) {
                           s.stride, (c + kStages - 1) * kChunk);
       cp_async_commit();
       if (!warp_done) {
-        const unsigned char* a_s = smem + (c % kStages) * kStageBytes + ty * 128;
-        const unsigned char* b_s = smem + (c % kStages) * kStageBytes + kOperandBytes + tx * 128;  // rows tx + kTx*w
+        const unsigned char* a_s = smem + (c % kStages) * kStageBytes + ty * kRowBytes;
+        const unsigned char* b_s = smem + (c % kStages) * kStageBytes + kOperandBytes + tx * kRowBytes;  // rows tx + kTx*w
 #pragma unroll 2
-        for (int kc = 0; kc < 8; ++kc) {
+        for (int kc = 0; kc < kPieces; ++kc) {
           const uint32_t off_a = (kc ^ (ty & 7)) << 4, off_b = (kc ^ (tx & 7)) << 4;
           if constexpr (kW == 8) {
             float4 na[kU];
 #pragma unroll
-            for (int u = 0; u < kU; ++u) na[u] = *reinterpret_cast<const float4*>(a_s + u * 2048 + off_a);
+            for (int u = 0; u < kU; ++u) na[u] = *reinterpret_cast<const float4*>(a_s + u * (16 * kRowBytes) + off_a);
 #pragma unroll
             for (int w = 0; w < kW; ++w) {
-              const float4 b = *reinterpret_cast<const float4*>(b_s + w * (kTx * 128) + off_b);
+              const float4 b = *reinterpret_cast<const float4*>(b_s + w * (kTx * kRowBytes) + off_b);
 #pragma unroll
               for (int u = 0; u < kU; ++u) acc.add(u, w, na[u], b);
             }
@@ -540,10 +572,10 @@ k_scan_tiles(SearchState s, ScanArgs a) {
             // row per u: its LDS.128 is a broadcast)
             float4 b[kW];
 #pragma unroll
-            for (int w = 0; w < kW; ++w) b[w] = *reinterpret_cast<const float4*>(b_s + w * (kTx * 128) + off_b);
+            for (int w = 0; w < kW; ++w) b[w] = *reinterpret_cast<const float4*>(b_s + w * (kTx * kRowBytes) + off_b);
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
-              const float4 na = *reinterpret_cast<const float4*>(a_s + u * 2048 + off_a);
+              const float4 na = *reinterpret_cast<const float4*>(a_s + u * (16 * kRowBytes) + off_a);
 #pragma unroll
               for (int w = 0; w < kW; ++w) acc.add(u, w, na, b[w]);
             }
@@ -568,40 +600,55 @@ k_scan_tiles(SearchState s, ScanArgs a) {
       if (cta_abandoned) atomicAdd(&s_abandoned, my_calls);
     }
     if (cta_abandoned) continue;
-
     // ---- completed tile: lower the candidates' bounds (and, symmetric, the neighbours')
+    // Fast test first: in a pruned scan almost no pair of a tile ends below its
+    // candidate's (or its neighbour's) bound, and then nothing else is looked at.
     const bool complete = (warp_chunks == chunks);
-    uint64_t cand_best[kU];
-    bool any_update = false;
+    float nub[kW];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      cand_best[u] = ~0ull;
-      const uint32_t row = s_cand[ty + 16 * u];
+    for (int w = 0; w < kW; ++w) nub[w] = (kSymmetric && complete) ? s_nub[tx + kTx * w] : -1.f;
+    bool hit = false;
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
 #pragma unroll
       for (int w = 0; w < kW; ++w) {
-        const uint32_t j = s_jrow[tx + kTx * w];
+        const float d = acc.get(u, w);
+        hit = hit || d <= thr[u] || d < nub[w];
+      }
+    if (!__any_sync(0xFFFFFFFFu, hit)) continue;
+
+    uint32_t jrow[kW];
+#pragma unroll
+    for (int w = 0; w < kW; ++w) jrow[w] = s_jrow[tx + kTx * w];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t row = s_cand[ty + 16 * u];
+      uint32_t d_min = 0xFFFFFFFFu, j_min = 0xFFFFFFFFu;  // this thread's best (distance bits, neighbour)
+#pragma unroll
+      for (int w = 0; w < kW; ++w) {
+        const uint32_t j = jrow[w];
         const float d = acc.get(u, w);
         const bool pair_ok = row != 0xFFFFFFFFu && j != 0xFFFFFFFFu && gap_u32(row, j) >= s.n;
         if (pair_ok && d <= thr[u]) {
-          const uint64_t key = nn_key(__float_as_uint(d), j);
-          cand_best[u] = key < cand_best[u] ? key : cand_best[u];
-          any_update = true;
+          const uint32_t bits = __float_as_uint(d);
+          if (bits < d_min || (bits == d_min && j < j_min)) {
+            d_min = bits;
+            j_min = j;
+          }
         }
-        if (kSymmetric && complete && pair_ok && d < s_nub[tx + kTx * w])
+        if (pair_ok && d < nub[w])
           atomicMin(as_ull(s.nn + j), static_cast<unsigned long long>(nn_key(__float_as_uint(d), row)));
       }
-    }
-    if (__any_sync(0xFFFFFFFFu, any_update)) {
+      // min over the kTx lanes that share candidate u: distance first, then neighbour
+      uint32_t g_min = d_min;
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        uint64_t key = cand_best[u];
+      for (int d = kTx / 2; d > 0; d >>= 1) g_min = min(g_min, __shfl_xor_sync(0xFFFFFFFFu, g_min, d));
+      uint32_t g_j = d_min == g_min ? j_min : 0xFFFFFFFFu;
 #pragma unroll
-        for (int d = kTx / 2; d > 0; d >>= 1) {  // the kTx lanes that share candidate u
-          const uint64_t other = __shfl_xor_sync(0xFFFFFFFFu, key, d);
-          key = other < key ? other : key;
-        }
-        if (tx == 0 && key != ~0ull)
-          atomicMin(as_ull(s.nn + s_cand[ty + 16 * u]), static_cast<unsigned long long>(key));
+      for (int d = kTx / 2; d > 0; d >>= 1) g_j = min(g_j, __shfl_xor_sync(0xFFFFFFFFu, g_j, d));
+      if (tx == 0 && g_j != 0xFFFFFFFFu) {
+        atomicMin(as_ull(s.nn + row), static_cast<unsigned long long>(nn_key(g_min, g_j)));
+        s_loc[ty + 16 * u] = fminf(s_loc[ty + 16 * u], __uint_as_float(g_min));
       }
     }
   }

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--repeat", type=int, default=1)
     ap.add_argument("--k", type=int, default=0)
     ap.add_argument("--prefix", type=int, default=0, help="use only the first PREFIX samples")
+    ap.add_argument("--no-pruning", action="store_true", help="exhaustive scan (DiscoveryOptions::disable_pruning)")
     args = ap.parse_args()
     golden = json.load(open(os.path.join(os.path.dirname(__file__), "..", "tests", "golden", "workloads.json")))
     with Context(0) as ctx:
@@ -38,7 +39,7 @@ def main():
                 t0 = time.time()
                 ctx.prepare(x, w.n, w.word_len, w.alphabet)
                 t1 = time.time()
-                pos, dist = ctx.search(k)
+                pos, dist = ctx.search(k, args.no_pruning)
                 t2 = time.time()
                 st = ctx.stats()
                 want = golden.get(f"cfg{cfg}", {}).get("oracle") if not args.prefix else None
