@@ -24,6 +24,7 @@
 namespace tsdd_b200 {
 void set_packed_math(bool on);
 void set_wide_tile(bool on);
+void set_scan_variant(int variant);
 }
 
 namespace {
@@ -142,6 +143,7 @@ struct tsdd_cuda_ctx {
   bool opt_symmetric = true;
   bool opt_packed = true;
   bool opt_wide_tile = false;
+  int opt_kernel = 1;
   bool opt_time_kernels = true;
 
   // prepared series
@@ -602,6 +604,7 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   bind_device(ctx);
   set_packed_math(ctx->opt_packed);
   set_wide_tile(ctx->opt_wide_tile);
+  set_scan_variant(ctx->opt_packed ? ctx->opt_kernel : 1);
   const bool pruning = (flags & TSDD_SEARCH_DISABLE_PRUNING) == 0;
   cudaStream_t st = ctx->stream;
   SearchState s = ctx->state();
@@ -806,6 +809,9 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
       ctx->opt_symmetric = value != 0;
     } else if (key == "packed") {
       ctx->opt_packed = value != 0;
+    } else if (key == "kernel") {
+      if (value != 1 && value != 2) fail(TSDD_ERR_PARAMETER, "kernel must be 1 or 2");
+      ctx->opt_kernel = static_cast<int>(value);
     } else if (key == "wide_tile") {
       ctx->opt_wide_tile = value != 0;
     } else if (key == "time_kernels") {

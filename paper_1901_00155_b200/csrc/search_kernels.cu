@@ -664,6 +664,389 @@ k_scan_tiles(SearchState s, ScanArgs a) {
   }
 }
 
+// ------------------------------------------------------------------ warp-specialised tile kernel
+//
+// Same tiles, same arithmetic, different plumbing.  CTA = 8 consumer warps (the
+// 16 x 16 thread grid above, 8 x 4 pairs per thread) + 1 producer warp; two CTAs
+// per SM.  The producer streams 64-column stages — one 256-byte cp.async.bulk per
+// row (UBLKCP), completing on an mbarrier — through a 2-stage ring that runs
+// ACROSS tile boundaries, so the first stage of the next tile lands while the
+// consumers are still in the last chunk and epilogue of the current one.  It also
+// prepares each tile's thresholds / neighbour rows one tile ahead (two metadata
+// slots).  Consumers never meet in a CTA-wide barrier: each warp waits for a stage
+// (full mbarrier), reads the stage's tag (tile, chunk), computes, and releases the
+// stage (empty mbarrier).  A tile is abandoned when all 8 warps have voted
+// (shared counter); the producer then stops feeding it and moves on.  Rows sit in
+// shared memory at a 272-byte pitch (256 + 16), which makes the LDS.128 of the
+// 8 rows of a quarter-warp conflict-free without a swizzle.
+namespace ws {
+
+constexpr int kStagesWs = 2;
+constexpr int kNbrWs = 64;
+constexpr int kPitch = kChunk * 4 + 16;
+constexpr int kRowsPerStage = kTileRows + kNbrWs;
+constexpr int kStageBytesWs = kRowsPerStage * kPitch;
+constexpr int kConsumerWarps = 8;
+constexpr int kThreadsWs = (kConsumerWarps + 1) * 32;
+constexpr uint32_t kTagDone = 0xFFFFFFFFu;
+
+struct TileMeta {
+  float thr[kTileRows];      // candidate thresholds, -1 = dead / none
+  float nub[kNbrWs];         // neighbours' own bounds, -1 = none
+  uint32_t jrow[kNbrWs];     // neighbour rows, ~0 = none
+  uint32_t brow[kNbrWs];     // rows to load (none -> the zero row)
+  unsigned long long calls;  // pair distances this tile starts
+  uint32_t done;             // consumer warps that have abandoned the tile
+  uint32_t pad;
+};
+
+struct SharedWs {
+  unsigned char stages[kStagesWs][kStageBytesWs];
+  TileMeta meta[2];
+  uint32_t cand[kTileRows];
+  float loc[kTileRows];
+  uint32_t tag_tile[kStagesWs];
+  uint32_t tag_chunk[kStagesWs];
+  unsigned long long full[kStagesWs], empty[kStagesWs], meta_full[2], meta_empty[2];  // mbarriers
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @p bra DONE_%=;\n"
+      " bra WAIT_%=;\n DONE_%=:\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_copy_row(void* smem_dst, const void* gmem_src, uint32_t bytes,
+                                              unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(smem_dst)),
+               "l"(gmem_src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+
+// 288 threads x 112 registers: two CTAs fit the 64 K registers of an SM.
+template <bool kSymmetric>
+__global__ void __maxnreg__(112)
+k_scan_tiles_ws(SearchState s, ScanArgs a) {
+  constexpr int kU = 8, kW = 4, kTx = 16;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  SharedWs& sh = *reinterpret_cast<SharedWs*>(smem_raw);
+
+  const uint32_t count = a.sel[0];
+  const uint32_t cand0 = blockIdx.y * kTileRows;
+  if (cand0 >= count) return;
+
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float inf = __uint_as_float(kInfBits);
+  if (tid < kTileRows) {
+    sh.cand[tid] = (cand0 + tid < count) ? a.batch_rows[cand0 + tid] : 0xFFFFFFFFu;
+    sh.loc[tid] = inf;
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kStagesWs; ++i) {
+      mbar_init(&sh.full[i], 1);
+      mbar_init(&sh.empty[i], kConsumerWarps);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sh.meta_full[i], 1);
+      mbar_init(&sh.meta_empty[i], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();  // the only CTA-wide barrier
+
+  const bool window = a.nbr_index != nullptr;
+  const uint32_t slot_tiles = (s.n_rows + kNbrWs - 1) / kNbrWs;
+  const uint32_t chunks = s.stride / kChunk;
+  const uint32_t k_first = a.k_begin + blockIdx.x * a.tiles_per_cta;
+  const uint32_t n_tiles = k_first < a.k_end ? min(static_cast<uint32_t>(a.tiles_per_cta), a.k_end - k_first) : 0u;
+
+  if (warp == kConsumerWarps) {
+    // ================================================================ producer warp
+    const uint32_t centre = window ? a.batch_slots[min(cand0 + kTileRows / 2, count - 1)] / kNbrWs : 0u;
+    const uint64_t best = a.pruning ? *s.best : 0ull;
+    const float* a_tile = a.batch + static_cast<size_t>(cand0) * s.stride;
+    auto slot_tile_of = [&](uint32_t k) -> uint32_t {
+      if (!window) return (k + a.rotation) % slot_tiles;
+      const uint32_t step = (k + 1) >> 1;
+      return (k & 1) ? (centre + step) % slot_tiles : (centre + slot_tiles - step % slot_tiles) % slot_tiles;
+    };
+    // bounds of the next tile, fetched while the current one streams
+    uint64_t cand_key[4], nbr_key[2];
+    uint32_t nbr_j[2];
+    auto fetch_bounds = [&](uint32_t k) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t row = sh.cand[lane + 32 * q];
+        cand_key[q] = (row != 0xFFFFFFFFu && a.pruning) ? load_key(s.nn + row) : 0ull;
+      }
+      const uint32_t slot0 = slot_tile_of(k) * kNbrWs;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t slot = slot0 + lane + 32 * q;
+        nbr_j[q] = 0xFFFFFFFFu;
+        if (slot < s.n_rows) nbr_j[q] = window ? a.nbr_index[slot] : slot;
+        nbr_key[q] = nbr_j[q] != 0xFFFFFFFFu ? load_key(s.nn + nbr_j[q]) : 0ull;
+      }
+    };
+    if (n_tiles) fetch_bounds(k_first);
+
+    uint32_t seq = 0;
+    unsigned long long calls_total = 0;
+#pragma unroll 1
+    for (uint32_t ti = 0; ti < n_tiles; ++ti) {
+      const uint32_t k = k_first + ti, m = ti & 1, use = ti >> 1;
+      TileMeta& meta = sh.meta[m];
+      if (use >= 1) mbar_wait(&sh.meta_empty[m], (use - 1) & 1);  // every consumer has left tile ti - 2
+
+      // ---- metadata of tile ti from the prefetched bounds
+      bool live[4];
+      bool any_live = false;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t r = lane + 32 * q, row = sh.cand[r];
+        float thr = -1.f;
+        live[q] = false;
+        if (row != 0xFFFFFFFFu) {
+          if (!a.pruning) {
+            thr = inf;
+            live[q] = true;
+          } else {
+            const float bound = fminf(__uint_as_float(key_bits(cand_key[q])), sh.loc[r]);
+            if (!(best_key(__float_as_uint(bound), row) < best)) {
+              thr = bound;
+              live[q] = true;
+            }
+          }
+        }
+        meta.thr[r] = thr;
+        any_live = any_live || live[q];
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t t = lane + 32 * q, j = nbr_j[q];
+        meta.jrow[t] = j;
+        meta.brow[t] = j != 0xFFFFFFFFu ? j : s.n_rows;  // row n_rows is zero padding
+        meta.nub[t] = j != 0xFFFFFFFFu ? __uint_as_float(key_bits(nbr_key[q])) : -1.f;
+      }
+      any_live = __any_sync(0xFFFFFFFFu, any_live);
+      __syncwarp();
+      // pair distances this tile starts (series.hpp:120): live candidates x neighbours at least n away
+      const uint32_t slot0 = slot_tile_of(k) * kNbrWs;
+      const uint32_t valid = min(static_cast<uint32_t>(kNbrWs), s.n_rows - slot0);
+      unsigned long long calls = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (!live[q]) continue;
+        const uint32_t row = sh.cand[lane + 32 * q];
+        uint32_t overlap = 0;
+        if (!window) {
+          const uint32_t z0 = row >= s.n - 1 ? row - (s.n - 1) : 0, z1 = row + s.n;
+          const uint32_t o0 = max(slot0, z0), o1 = min(slot0 + valid, z1);
+          overlap = o1 > o0 ? o1 - o0 : 0;
+        } else {
+          const uint4* jr = reinterpret_cast<const uint4*>(meta.jrow);
+#pragma unroll 4
+          for (int e = 0; e < kNbrWs / 4; ++e) {
+            const uint4 v = jr[e];
+            overlap += (gap_u32(row, v.x) < s.n ? 1u : 0u) + (gap_u32(row, v.y) < s.n ? 1u : 0u) +
+                       (gap_u32(row, v.z) < s.n ? 1u : 0u) + (gap_u32(row, v.w) < s.n ? 1u : 0u);
+          }
+        }
+        calls += valid - overlap;
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) calls += __shfl_xor_sync(0xFFFFFFFFu, calls, d);
+      if (lane == 0) {
+        meta.calls = calls;
+        meta.done = 0;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.meta_full[m]);
+      if (!any_live) break;  // candidates only ever die: nothing is left for this CTA
+      calls_total += calls;
+
+      const float* src[6];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) src[q] = a_tile + static_cast<size_t>(lane + 32 * q) * s.stride;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) src[4 + q] = s.rows + static_cast<size_t>(meta.brow[lane + 32 * q]) * s.stride;
+      if (ti + 1 < n_tiles) fetch_bounds(k + 1);
+
+      // ---- stream the tile's chunks; stop as soon as every consumer warp has abandoned it
+#pragma unroll 1
+      for (uint32_t c = 0; c < chunks; ++c) {
+        if (a.pruning && *reinterpret_cast<volatile uint32_t*>(&meta.done) == kConsumerWarps) break;
+        const uint32_t st = seq % kStagesWs, round = seq / kStagesWs;
+        if (round >= 1) mbar_wait(&sh.empty[st], (round - 1) & 1);
+        if (lane == 0) {
+          sh.tag_tile[st] = ti;
+          sh.tag_chunk[st] = c;
+          mbar_arrive_expect_tx(&sh.full[st], kRowsPerStage * kChunk * 4);
+        }
+        __syncwarp();
+        unsigned char* dst = sh.stages[st];
+#pragma unroll
+        for (int q = 0; q < 6; ++q)
+          bulk_copy_row(dst + (lane + 32 * q) * kPitch, src[q] + c * kChunk, kChunk * 4, &sh.full[st]);
+        ++seq;
+      }
+    }
+    {  // the end-of-work tag
+      const uint32_t st = seq % kStagesWs, round = seq / kStagesWs;
+      if (round >= 1) mbar_wait(&sh.empty[st], (round - 1) & 1);
+      if (lane == 0) {
+        sh.tag_tile[st] = kTagDone;
+        mbar_arrive(&sh.full[st]);
+      }
+    }
+    if (lane == 0 && calls_total) atomicAdd(&s.counters->calls, calls_total);
+    return;
+  }
+
+  // ================================================================== consumer warps
+  const uint32_t tx = tid % kTx, ty = tid / kTx;
+  Acc<true, kU, kW> acc;
+  float thr[kU];
+  uint32_t seq = 0, cur = kTagDone, m = 0, chunks_done = 0;
+  bool released = true, warp_done = false;
+  unsigned long long chunks_total = 0, abandoned_total = 0;
+#pragma unroll 1
+  for (;;) {
+    const uint32_t st = seq % kStagesWs, round = seq / kStagesWs;
+    mbar_wait(&sh.full[st], round & 1);
+    const uint32_t tile = *reinterpret_cast<volatile uint32_t*>(&sh.tag_tile[st]);
+    if (tile == kTagDone) break;
+    const uint32_t c = *reinterpret_cast<volatile uint32_t*>(&sh.tag_chunk[st]);
+    if (tile != cur) {
+      if (!released) {  // the previous tile was cut short by the producer
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sh.meta_empty[m]);
+      }
+      cur = tile;
+      m = tile & 1;
+      mbar_wait(&sh.meta_full[m], (tile >> 1) & 1);
+#pragma unroll
+      for (int u = 0; u < kU; ++u) thr[u] = sh.meta[m].thr[ty + 16 * u];
+      acc.zero();
+      warp_done = false;
+      released = false;
+      chunks_done = 0;
+    }
+    TileMeta& meta = sh.meta[m];
+    if (!warp_done) {
+      const unsigned char* a_s = sh.stages[st] + ty * kPitch;
+      const unsigned char* b_s = sh.stages[st] + kTileRows * kPitch + tx * kPitch;
+#pragma unroll 2
+      for (int kc = 0; kc < kPieces; ++kc) {
+        float4 b[kW];
+#pragma unroll
+        for (int w = 0; w < kW; ++w) b[w] = *reinterpret_cast<const float4*>(b_s + w * (kTx * kPitch) + kc * 16);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const float4 na = *reinterpret_cast<const float4*>(a_s + u * (16 * kPitch) + kc * 16);
+#pragma unroll
+          for (int w = 0; w < kW; ++w) acc.add(u, w, na, b[w]);
+        }
+      }
+      ++chunks_done;
+      ++chunks_total;
+      bool all_over = true;
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+#pragma unroll
+        for (int w = 0; w < kW; ++w) all_over = all_over && (acc.get(u, w) > thr[u]);
+      warp_done = __all_sync(0xFFFFFFFFu, all_over);
+      if (warp_done && c + 1 < chunks && lane == 0) {
+        if (atomicAdd(&meta.done, 1u) == kConsumerWarps - 1) abandoned_total += meta.calls;  // the last vote
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sh.empty[st]);  // this warp is done reading the stage
+
+    if (c + 1 == chunks) {
+      if (chunks_done == chunks) {
+        // ---- completed tile: same epilogue as k_scan_tiles
+        float nub[kW];
+#pragma unroll
+        for (int w = 0; w < kW; ++w) nub[w] = kSymmetric ? meta.nub[tx + kTx * w] : -1.f;
+        bool hit = false;
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+#pragma unroll
+          for (int w = 0; w < kW; ++w) {
+            const float d = acc.get(u, w);
+            hit = hit || d <= thr[u] || d < nub[w];
+          }
+        if (__any_sync(0xFFFFFFFFu, hit)) {
+          uint32_t jrow[kW];
+#pragma unroll
+          for (int w = 0; w < kW; ++w) jrow[w] = meta.jrow[tx + kTx * w];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const uint32_t row = sh.cand[ty + 16 * u];
+            uint32_t d_min = 0xFFFFFFFFu, j_min = 0xFFFFFFFFu;
+#pragma unroll
+            for (int w = 0; w < kW; ++w) {
+              const uint32_t j = jrow[w];
+              const float d = acc.get(u, w);
+              const bool pair_ok = row != 0xFFFFFFFFu && j != 0xFFFFFFFFu && gap_u32(row, j) >= s.n;
+              if (pair_ok && d <= thr[u]) {
+                const uint32_t bits = __float_as_uint(d);
+                if (bits < d_min || (bits == d_min && j < j_min)) {
+                  d_min = bits;
+                  j_min = j;
+                }
+              }
+              if (pair_ok && d < nub[w])
+                atomicMin(as_ull(s.nn + j), static_cast<unsigned long long>(nn_key(__float_as_uint(d), row)));
+            }
+            uint32_t g_min = d_min;
+#pragma unroll
+            for (int d = kTx / 2; d > 0; d >>= 1) g_min = min(g_min, __shfl_xor_sync(0xFFFFFFFFu, g_min, d));
+            uint32_t g_j = d_min == g_min ? j_min : 0xFFFFFFFFu;
+#pragma unroll
+            for (int d = kTx / 2; d > 0; d >>= 1) g_j = min(g_j, __shfl_xor_sync(0xFFFFFFFFu, g_j, d));
+            if (tx == 0 && g_j != 0xFFFFFFFFu) {
+              atomicMin(as_ull(s.nn + row), static_cast<unsigned long long>(nn_key(g_min, g_j)));
+              sh.loc[ty + 16 * u] = fminf(sh.loc[ty + 16 * u], __uint_as_float(g_min));
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.meta_empty[m]);  // this warp is done with the tile's metadata
+      released = true;
+    }
+    ++seq;
+  }
+  if (lane == 0) {
+    const unsigned long long terms = chunks_total * kChunk * 32ull * kU * kW;
+    if (terms) {
+      atomicAdd(&s.counters->terms, terms);
+      atomicAdd(&s.counters->tile_terms, terms);
+    }
+    if (abandoned_total) atomicAdd(&s.counters->abandoned, abandoned_total);
+  }
+}
+
+}  // namespace ws
+
 // float64 distance of one pair straight from the series (finalists only).
 __global__ void __launch_bounds__(256)
 k_rescore_pair(const double* __restrict__ x, const double* __restrict__ mean,
@@ -686,6 +1069,7 @@ k_rescore_pair(const double* __restrict__ x, const double* __restrict__ mean,
 }
 
 bool g_packed_default = true;
+int g_scan_variant = 1;  // 1: cp.async + CTA barriers (k_scan_tiles), 2: warp-specialised (k_scan_tiles_ws)
 bool g_wide_tile = false;  // true: 128 x 128 tile, one CTA per SM; false: 128 x 64 tile, two CTAs per SM
 
 }  // namespace
@@ -754,6 +1138,17 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
   dim3 grid((tiles + tiles_per_cta - 1) / tiles_per_cta, capacity_padded / kTileRows);
   ScanArgs a{d_batch_matrix, d_batch_rows, d_batch_slots, d_sel, d_nbr_index, k_begin, k_end, rotation,
              tiles_per_cta, pruning ? 1 : 0};
+  if (g_scan_variant == 2) {
+    const int smem = static_cast<int>(sizeof(ws::SharedWs));
+    if (symmetric) {
+      cudaFuncSetAttribute(ws::k_scan_tiles_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      ws::k_scan_tiles_ws<true><<<grid, ws::kThreadsWs, smem, stream>>>(s, a);
+    } else {
+      cudaFuncSetAttribute(ws::k_scan_tiles_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      ws::k_scan_tiles_ws<false><<<grid, ws::kThreadsWs, smem, stream>>>(s, a);
+    }
+    return 1;
+  }
   auto launch = [&](auto kernel, int nbr_rows) {
     const int smem = static_cast<int>(scan_smem_bytes(nbr_rows));
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -773,7 +1168,8 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
   return 1;
 }
 
-uint32_t scan_neighbour_tile_rows() { return g_wide_tile ? 128u : 64u; }
+uint32_t scan_neighbour_tile_rows() { return (g_scan_variant != 2 && g_wide_tile) ? 128u : 64u; }
+void set_scan_variant(int variant) { g_scan_variant = variant; }
 
 void set_packed_math(bool on) { g_packed_default = on; }
 void set_wide_tile(bool on) { g_wide_tile = on; }
