@@ -87,6 +87,9 @@ int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream);
  * neighbours tried per row before the scans), "rescore" (0/1: float64
  * re-scoring of each discord's distance), "symmetric" (0/1: completed tiles
  * also lower the neighbours' bounds), "packed" (0/1: f32x2 arithmetic),
+ * "wide_tile" (0/1: 128 x 128 tiles, one CTA per SM, instead of 128 x 64, two),
+ * "kernel" (1: cp.async tile kernel; 2: the warp-specialised cp.async.bulk +
+ * mbarrier variant, experimental and currently slower), "rotate" (0/1),
  * "time_kernels" (0/1: CUDA events around every tile-kernel launch).
  * Unknown name -> TSDD_ERR_PARAMETER.  None of them changes the result.     */
 int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value);

@@ -679,6 +679,15 @@ k_scan_tiles(SearchState s, ScanArgs a) {
 // (shared counter); the producer then stops feeding it and moves on.  Rows sit in
 // shared memory at a 272-byte pitch (256 + 16), which makes the LDS.128 of the
 // 8 rows of a quarter-warp conflict-free without a swizzle.
+//
+// Status (round 1): results identical to k_scan_tiles on every test, but SLOWER
+// (cfg 5: 1.01e13 vs 1.33e13 terms/s).  ncu shows why: registers are allocated per
+// 4 warps, so the 9-warp CTA is charged for 12 and only ONE CTA fits an SM
+// (launch__occupancy_limit_registers = 1); with 2 consumer warps per scheduler the
+// LDS latency at the top of every 4-column step is exposed.  The copies themselves
+// keep up (consumers wait on a full barrier for ~5 % of their time).  Kept behind
+// the "kernel"=2 option as the starting point for a variant whose producer duty
+// fits an 8-warp CTA.
 namespace ws {
 
 constexpr int kStagesWs = 2;
