@@ -60,6 +60,8 @@ typedef struct tsdd_cuda_stats {
   double encode_ms;        /* preparation: window statistics + PAA/SAX/hash kernel */
   double build_rows_ms;    /* preparation: float32 matrix build (HBM write-bound) */
   double index_ms;         /* preparation: radix sorts, run-length histogram, rarity order */
+  uint64_t tiles;          /* candidate-tile x neighbour-tile pairs the tile kernel started */
+  uint64_t tile_live_candidates; /* live candidates summed over them (128 per tile = dense tiles) */
 } tsdd_cuda_stats;
 
 /* ---- lifetime ------------------------------------------------------------ */
@@ -78,7 +80,8 @@ const char* tsdd_cuda_last_error(const tsdd_cuda_ctx* ctx);
 int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream);
 
 /* Tunables, by name: "batch" (candidates per outer-loop batch), "first_batch"
- * (size of the first batch; it doubles up to "batch"), "first_range" / "growth"
+ * / "batch_growth" (size of the first batch of the first pass and the factor by
+ * which batches grow up to "batch"), "first_range" / "growth"
  * / "rounds" (neighbour rows are visited in ranges: first_range rows, then each
  * range growth times larger, at most rounds of them; dead candidates are
  * dropped between ranges), "window_rounds" / "window_first" / "window_growth"

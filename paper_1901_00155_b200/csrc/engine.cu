@@ -129,8 +129,9 @@ struct tsdd_cuda_ctx {
   std::string error;
 
   // tunables (tsdd_cuda_set_option)
-  uint32_t opt_batch = 16384;
+  uint32_t opt_batch = 65536;
   uint32_t opt_first_batch = 256;
+  uint32_t opt_batch_growth = 8;
   int opt_rounds = 64;            // upper limit on neighbour ranges per batch
   uint32_t opt_first_range = 2048;  // rows in the first range
   double opt_growth = 1.5;          // each range is this much larger than the one before
@@ -166,7 +167,8 @@ struct tsdd_cuda_ctx {
   DeviceArray<float> batch_matrix;
   DeviceArray<double> rescore_out;
   uint32_t batch_capacity = 0;
-  uint32_t* h_sel = nullptr;      // pinned, 4 words
+  uint32_t* h_sel = nullptr;      // pinned, 4 words + a ring of 4 x 4 words for lagged counts
+  cudaEvent_t ev_ring[4] = {nullptr, nullptr, nullptr, nullptr};
   uint64_t* h_keys = nullptr;     // pinned, 4 keys
   double* h_double = nullptr;     // pinned, 1 value
   std::vector<cudaEvent_t> event_pool;
@@ -512,14 +514,24 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
       (pruning && ctx->opt_rotate)
           ? static_cast<uint32_t>((ctx->stats.batches * 0.6180339887498949 - std::floor(ctx->stats.batches * 0.6180339887498949)) * slot_tiles) % slot_tiles
           : 0u;
+  // The live count after each compaction is read back ONE segment late: segment r's grid is
+  // sized with the count after compaction r - 1 (an upper bound, candidates only die; surplus
+  // CTAs exit at once), so the host never waits for the segment the GPU is working on and
+  // the GPU never waits for the host.
   const std::vector<Segment> plan = plan_segments(ctx, pruning);
   for (size_t r = 0; r < plan.size(); ++r) {
     if (r > 0 && pruning) {
       launches += launch_compact_batch(s, list, slots, list_alt, slots_alt, pruning, ctx->sel.ptr, st);
       std::swap(list, list_alt);
       std::swap(slots, slots_alt);
-      count = read_sel(ctx);
-      if (count == 0) break;
+      uint32_t* slot_now = ctx->h_sel + 4 + 4 * (r & 3);
+      CUDA_OK(cudaMemcpyAsync(slot_now, ctx->sel.ptr, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      CUDA_OK(cudaEventRecord(ctx->ev_ring[r & 3], st));
+      if (r >= 2) {
+        CUDA_OK(cudaEventSynchronize(ctx->ev_ring[(r - 1) & 3]));
+        count = ctx->h_sel[4 + 4 * ((r - 1) & 3)];
+        if (count == 0) break;
+      }
     }
     const uint32_t padded = round_up_u32(count, kTileRows);
     launches += launch_gather_rows(s, list, ctx->sel.ptr, padded, ctx->batch_matrix.ptr, st);
@@ -546,11 +558,16 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
 }
 
 // One exact arg-max pass over this rank's share of the rarity order.
-uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning) {
+uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
   cudaStream_t st = ctx->stream;
   SearchState s = ctx->state();
   uint32_t cursor = 0;
-  uint32_t batch_now = std::min(ctx->opt_first_batch, ctx->opt_batch);
+  // Small batches first: the best-so-far rises fastest over the rarest words, and every
+  // later candidate is cheaper for it.  Later top-k passes start from a best-so-far that is
+  // already seeded with exact rows, so they use full batches at once — every batch leaves a
+  // few long-lived survivors that scan the whole series in a part-filled tile, and fewer
+  // batches mean fewer such tiles.
+  uint32_t batch_now = pass == 0 ? std::min(ctx->opt_first_batch, ctx->opt_batch) : ctx->opt_batch;
   for (;;) {
     if (cursor < ctx->rows) {
       ensure_batch_capacity(ctx, batch_now);
@@ -564,7 +581,7 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning) {
         ctx->stats.scanned_candidates += count;
         scan_batch(ctx, count, pruning);
       }
-      batch_now = std::min(batch_now * 2, ctx->opt_batch);
+      batch_now = static_cast<uint32_t>(std::min<uint64_t>(static_cast<uint64_t>(batch_now) * ctx->opt_batch_growth, ctx->opt_batch));
     }
     if (ctx->world > 1 || ctx->comm) {  // a 1-rank communicator still runs the exchange
       CUDA_OK(cudaMemcpyAsync(ctx->h_keys, ctx->best.ptr, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
@@ -589,6 +606,8 @@ void collect_search_stats(tsdd_cuda_ctx* ctx) {
   ctx->stats.abandoned = c.abandoned;
   ctx->stats.terms = c.terms;
   ctx->stats.scan_kernel_terms = c.tile_terms;
+  ctx->stats.tiles = c.tiles;
+  ctx->stats.tile_live_candidates = c.tile_live;
   double total = 0.0;
   for (size_t e = 0; e + 1 < ctx->events_used; e += 2) {
     float ms = 0.f;
@@ -626,7 +645,7 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
       CUDA_OK(cudaMemsetAsync(ctx->best.ptr, 0, sizeof(uint64_t), st));
       ctx->stats.kernel_launches += launch_seed_best(s, st);
     }
-    const uint64_t key = run_pass(ctx, pruning);
+    const uint64_t key = run_pass(ctx, pruning, pass);
     if (key == 0) {  // nothing beat 0: the reference's fallback (discovery.cpp:90-93)
       positions[pass] = 1;
       distances[pass] = 0.0;
@@ -727,7 +746,8 @@ int tsdd_cuda_create(tsdd_cuda_ctx** out, int device) {
     for (auto& e : ctx->ev_prep) CUDA_OK(cudaEventCreate(&e));
     CUDA_OK(cudaEventCreate(&ctx->ev_a));
     CUDA_OK(cudaEventCreate(&ctx->ev_b));
-    CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_sel), 4 * sizeof(uint32_t)));
+    CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_sel), 20 * sizeof(uint32_t)));
+    for (auto& e : ctx->ev_ring) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_keys), 4 * sizeof(uint64_t)));
     CUDA_OK(cudaMallocHost(reinterpret_cast<void**>(&ctx->h_double), sizeof(double)));
   });
@@ -746,6 +766,8 @@ void tsdd_cuda_destroy(tsdd_cuda_ctx* ctx) {
   if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
   for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->ev_prep)
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->ev_ring)
     if (e) cudaEventDestroy(e);
   if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
   if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
@@ -780,6 +802,9 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
     } else if (key == "first_batch") {
       if (value < 1 || value > 1048576) fail(TSDD_ERR_PARAMETER, "first_batch must be in 1..1048576");
       ctx->opt_first_batch = static_cast<uint32_t>(value);
+    } else if (key == "batch_growth") {
+      if (value < 1 || value > 1024) fail(TSDD_ERR_PARAMETER, "batch_growth must be in 1..1024");
+      ctx->opt_batch_growth = static_cast<uint32_t>(value);
     } else if (key == "rounds") {
       if (value < 1 || value > 4096) fail(TSDD_ERR_PARAMETER, "rounds must be in 1..4096");
       ctx->opt_rounds = static_cast<int>(value);

@@ -42,7 +42,7 @@ __global__ void k_reset_search(SearchState s) {
   }
   if (i == 0) {
     *s.best = 0;
-    *s.counters = DeviceCounters{0, 0, 0, 0, 0};
+    *s.counters = DeviceCounters{0, 0, 0, 0, 0, 0, 0};
   }
 }
 
@@ -419,7 +419,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
   uint32_t* s_jrow = reinterpret_cast<uint32_t*>(s_nub + kTileRows);      // neighbour rows, ~0 = none
   uint32_t* s_brow = s_jrow + kTileRows;                                  // rows to load (none -> zero row)
   float* s_loc = reinterpret_cast<float*>(s_brow + kTileRows);            // bounds this CTA found itself
-  __shared__ unsigned long long s_calls, s_abandoned, s_terms;
+  __shared__ unsigned long long s_calls, s_abandoned, s_terms, s_tiles, s_tile_live;
 
   const uint32_t count = a.sel[0];
   const uint32_t cand0 = blockIdx.y * kTileRows;
@@ -433,6 +433,8 @@ k_scan_tiles(SearchState s, ScanArgs a) {
     s_calls = 0;
     s_abandoned = 0;
     s_terms = 0;
+    s_tiles = 0;
+    s_tile_live = 0;
   }
   const bool window = a.nbr_index != nullptr;
   const uint32_t slot_tiles = (s.n_rows + kNbr - 1) / kNbr;
@@ -499,7 +501,12 @@ k_scan_tiles(SearchState s, ScanArgs a) {
       s_brow[t] = pf_j != 0xFFFFFFFFu ? pf_j : s.n_rows;  // row n_rows is zero padding
       s_nub[t] = pf_j != 0xFFFFFFFFu ? __uint_as_float(key_bits(pf_key)) : -1.f;
     }
-    if (!__syncthreads_or(live)) break;  // every candidate of this tile is dead: nothing left to do
+    const int n_live = __syncthreads_count(live);
+    if (n_live == 0) break;  // every candidate of this tile is dead: nothing left to do
+    if (tid == 0) {
+      s_tiles += 1;
+      s_tile_live += n_live;
+    }
     if (tt + 1 < a.tiles_per_cta && k + 1 < a.k_end) prefetch(k + 1);
 
     unsigned long long my_calls = 0;
@@ -660,6 +667,10 @@ k_scan_tiles(SearchState s, ScanArgs a) {
     if (s_terms) {
       atomicAdd(&s.counters->terms, s_terms);
       atomicAdd(&s.counters->tile_terms, s_terms);
+    }
+    if (s_tiles) {
+      atomicAdd(&s.counters->tiles, s_tiles);
+      atomicAdd(&s.counters->tile_live, s_tile_live);
     }
   }
 }

@@ -166,7 +166,7 @@ def test_search_is_repeatable_and_independent_of_tunables(ctx):
         again = ctx.search(3)
         assert again[0] == base[0], name
         np.testing.assert_allclose(again[1], base[1], rtol=1e-6, err_msg=name)
-    for name, value in [("batch", 16384), ("rounds", 64), ("bucket_mates", 8), ("symmetric", 1),
+    for name, value in [("batch", 65536), ("rounds", 64), ("bucket_mates", 8), ("symmetric", 1),
                         ("packed", 1), ("first_batch", 256), ("wide_tile", 0), ("kernel", 1),
                         ("window_rounds", 4), ("rotate", 1), ("growth", 1.5), ("first_range", 2048)]:
         ctx.set_option(name, value)
