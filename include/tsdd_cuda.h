@@ -87,8 +87,9 @@ int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream);
  * dropped between ranges), "window_rounds" / "window_first" / "window_growth"
  * (before that covering scan, each candidate tile visits its own SAX word's
  * neighbourhood in the hash-sorted order: window_first slots, growing), "bucket_mates" (same-word
- * neighbours tried per row before the scans), "rescore" (0/1: float64
- * re-scoring of each discord's distance), "symmetric" (0/1: completed tiles
+ * neighbours tried per row before the scans), "rescore" (0/1: decide each pass
+ * among the near-tied finalists by their exact float64 nn distance),
+ * "margin_delta" (safety band of the float32 discard test; negative = from n), "symmetric" (0/1: completed tiles
  * also lower the neighbours' bounds), "packed" (0/1: f32x2 arithmetic),
  * "wide_tile" (0/1: 128 x 128 tiles, one CTA per SM, instead of 128 x 64, two),
  * "kernel" (1: cp.async tile kernel; 2: the warp-specialised cp.async.bulk +

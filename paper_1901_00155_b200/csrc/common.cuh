@@ -29,11 +29,20 @@ __host__ __device__ __forceinline__ uint32_t best_key_row(uint64_t key) {
   return 0xFFFFFFFFu - static_cast<uint32_t>(key & 0xFFFFFFFFull);
 }
 
-// A row whose nn upper bound cannot beat the best-so-far any more is dead:
-// the HOTSAX discard `d < bsf` (discovery.cpp:58), extended by the tie rule
-// (equal distance, larger position can never win).
-__device__ __forceinline__ bool is_dead(uint64_t nn, uint32_t row, uint64_t best) {
-  return best_key(key_bits(nn), row) < best;
+// A row whose nn upper bound cannot beat the best-so-far any more is dead: the
+// HOTSAX discard `d < bsf` (discovery.cpp:58,70).  The kernels compute in
+// float32 and the reference in float64, so the test keeps a safety factor
+// (`margin` = 1 + delta, delta a bound of the float32 rounding of a distance):
+// a row is discarded only if its bound is below the best-so-far even after the
+// factor.  Rows inside the band stay alive, finish their scan, and the winner
+// among them is decided in float64 (k_exact_nn): float32 noise can then cost
+// work, never the answer.  A bound of exactly 0 is dead at once: nothing beats
+// the initial best-so-far 0 with it (discovery.cpp:90-93, hpp:45 `sq > best`).
+__device__ __forceinline__ bool dead_bound(float d2, uint64_t best, float margin) {
+  return d2 == 0.f || d2 * margin < __uint_as_float(key_bits(best));
+}
+__device__ __forceinline__ bool is_dead(uint64_t nn, uint64_t best, float margin) {
+  return dead_bound(__uint_as_float(key_bits(nn)), best, margin);
 }
 
 __device__ __forceinline__ unsigned long long* as_ull(uint64_t* p) {

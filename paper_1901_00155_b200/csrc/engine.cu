@@ -31,6 +31,8 @@ namespace {
 
 using namespace tsdd_b200;
 
+constexpr uint32_t kFinalistCap = 64;
+
 struct Failure {
   int code;
   std::string message;
@@ -141,6 +143,7 @@ struct tsdd_cuda_ctx {
   bool opt_rotate = true;           // each batch starts its covering scan at a different row
   int opt_mates = 8;
   bool opt_rescore = true;
+  double opt_margin_delta = -1.0;  // < 0: derive from n (see discard_margin)
   bool opt_symmetric = true;
   bool opt_packed = true;
   bool opt_wide_tile = false;
@@ -165,7 +168,9 @@ struct tsdd_cuda_ctx {
   DeviceArray<DeviceCounters> counters;
   DeviceArray<uint32_t> flags, batch_rows, batch_alt, batch_slots, batch_slots_alt, sel;
   DeviceArray<float> batch_matrix;
-  DeviceArray<double> rescore_out;
+  DeviceArray<double> zrow;
+  DeviceArray<uint32_t> finalists;
+  DeviceArray<unsigned long long> nn_bits;
   uint32_t batch_capacity = 0;
   uint32_t* h_sel = nullptr;      // pinned, 4 words + a ring of 4 x 4 words for lagged counts
   cudaEvent_t ev_ring[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -182,6 +187,15 @@ struct tsdd_cuda_ctx {
 
   tsdd_cuda_stats stats{};
 
+  // Safety factor of the discard test (common.cuh: dead_bound): a float32 distance of n
+  // terms is within about n * 2^-24 (relative) of its float64 value; twice that, and at
+  // least 4e-6, keeps every row that float32 noise could mis-rank alive until the float64
+  // decision.
+  float discard_margin() const {
+    const double delta = opt_margin_delta >= 0.0 ? opt_margin_delta : std::max(4e-6, 1.2e-7 * static_cast<double>(n));
+    return static_cast<float>(1.0 + delta);
+  }
+
   SearchState state() {
     SearchState s;
     s.rows = matrix.ptr;
@@ -193,6 +207,7 @@ struct tsdd_cuda_ctx {
     s.excluded = excluded.ptr;
     s.best = best.ptr;
     s.counters = counters.ptr;
+    s.margin = discard_margin();
     return s;
   }
 };
@@ -329,7 +344,9 @@ void prepare_on_device(tsdd_cuda_ctx* ctx, size_t m, size_t n, size_t word_len, 
   ctx->counters.alloc(1);
   ctx->flags.alloc(2 * static_cast<size_t>(rows));
   ctx->sel.alloc(4);
-  ctx->rescore_out.alloc(1);
+  ctx->zrow.alloc(n);
+  ctx->finalists.alloc(kFinalistCap + 1);
+  ctx->nn_bits.alloc(1);
   ctx->batch_capacity = 0;
   ctx->stats.kernel_launches = launches;
 }
@@ -646,34 +663,73 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
       ctx->stats.kernel_launches += launch_seed_best(s, st);
     }
     const uint64_t key = run_pass(ctx, pruning, pass);
-    if (key == 0) {  // nothing beat 0: the reference's fallback (discovery.cpp:90-93)
+    if (key == 0 || key_bits(key) == 0) {  // nothing beat 0: the reference's fallback (discovery.cpp:90-93)
       positions[pass] = 1;
       distances[pass] = 0.0;
       continue;
     }
-    const uint32_t row = best_key_row(key);
+    uint32_t row = best_key_row(key);
     double d2 = static_cast<double>(float_from_bits(key_bits(key)));
     if (ctx->opt_rescore) {
-      // the rank that scanned `row` knows its nearest neighbour; others learn it here
-      uint64_t nn_key_host = 0;
-      uint8_t is_exact = 0;
-      CUDA_OK(cudaMemcpyAsync(&nn_key_host, ctx->nn.ptr + row, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-      CUDA_OK(cudaMemcpyAsync(&is_exact, ctx->exact.ptr + row, 1, cudaMemcpyDeviceToHost, st));
+      // Decide the pass in float64: every exact row whose float32 nn lies within the safety
+      // band of the best-so-far gets its exact nn over all non-self rows, straight from the
+      // series; greatest distance wins, ties go to the smaller position.
+      uint32_t* d_count = ctx->finalists.ptr + kFinalistCap;
+      ctx->stats.kernel_launches += launch_collect_finalists(s, ctx->finalists.ptr, kFinalistCap, d_count, st);
+      std::vector<uint32_t> mine(kFinalistCap + 1);
+      CUDA_OK(cudaMemcpyAsync(mine.data(), ctx->finalists.ptr, (kFinalistCap + 1) * sizeof(uint32_t),
+                              cudaMemcpyDeviceToHost, st));
       sync_stream(ctx);
-      uint64_t neighbour_plus_one =
-          (is_exact && key_bits(nn_key_host) == key_bits(key)) ? (nn_key_host & 0xFFFFFFFFull) + 1 : 0;
-      if (ctx->world > 1 || ctx->comm) {
-        ctx->h_keys[0] = neighbour_plus_one;
-        exchange_keys(ctx, ctx->h_keys, 1);
-        neighbour_plus_one = ctx->h_keys[0];
+      uint32_t n_final = mine[kFinalistCap];
+      mine.resize(std::min(n_final, kFinalistCap));
+      if (n_final > kFinalistCap) {
+        // more near-ties than are worth settling: keep the float32 winner, make only its distance exact
+        mine.clear();
+        uint8_t is_exact = 0;
+        CUDA_OK(cudaMemcpy(&is_exact, ctx->exact.ptr + row, 1, cudaMemcpyDeviceToHost));
+        if (is_exact) mine.push_back(row);
       }
-      if (neighbour_plus_one != 0 && neighbour_plus_one <= ctx->rows) {
-        ctx->stats.kernel_launches +=
-            launch_rescore_pair(ctx->series.ptr, ctx->mean.ptr, ctx->inv_sigma.ptr, static_cast<uint32_t>(ctx->n),
-                                row, static_cast<uint32_t>(neighbour_plus_one - 1), ctx->rescore_out.ptr, st);
-        CUDA_OK(cudaMemcpyAsync(ctx->h_double, ctx->rescore_out.ptr, sizeof(double), cudaMemcpyDeviceToHost, st));
+      double best64 = -1.0;
+      uint32_t best_row = 0xFFFFFFFFu;
+      for (const uint32_t cand : mine) {
+        uint64_t nn_key_host = 0;
+        CUDA_OK(cudaMemcpyAsync(&nn_key_host, ctx->nn.ptr + cand, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
         sync_stream(ctx);
-        d2 = *ctx->h_double;
+        // start from an upper bound just above the float32 value so that most rows abandon early
+        const double start = static_cast<double>(float_from_bits(key_bits(nn_key_host))) *
+                             static_cast<double>(s.margin) * static_cast<double>(s.margin);
+        unsigned long long bits;
+        std::memcpy(&bits, &start, sizeof(bits));
+        CUDA_OK(cudaMemcpyAsync(ctx->nn_bits.ptr, &bits, sizeof(bits), cudaMemcpyHostToDevice, st));
+        ctx->stats.kernel_launches +=
+            launch_exact_nn(ctx->series.ptr, ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->rows, static_cast<uint32_t>(ctx->n),
+                            cand, ctx->zrow.ptr, ctx->nn_bits.ptr, st);
+        CUDA_OK(cudaMemcpyAsync(&bits, ctx->nn_bits.ptr, sizeof(bits), cudaMemcpyDeviceToHost, st));
+        sync_stream(ctx);
+        double exact;
+        std::memcpy(&exact, &bits, sizeof(exact));
+        if (exact > best64 || (exact == best64 && cand < best_row)) {
+          best64 = exact;
+          best_row = cand;
+        }
+      }
+      if (ctx->world > 1 || ctx->comm) {
+        // the finalists are spread over the ranks: greatest float64 distance, then smallest row
+        uint64_t value_bits = 0;
+        if (best_row != 0xFFFFFFFFu) std::memcpy(&value_bits, &best64, sizeof(value_bits));
+        ctx->h_keys[0] = value_bits;
+        exchange_keys(ctx, ctx->h_keys, 1);
+        const uint64_t global_bits = ctx->h_keys[0];
+        ctx->h_keys[0] = (best_row != 0xFFFFFFFFu && value_bits == global_bits) ? 0xFFFFFFFFull - best_row : 0ull;
+        exchange_keys(ctx, ctx->h_keys, 1);
+        if (global_bits != 0 || ctx->h_keys[0] != 0) {
+          std::memcpy(&best64, &global_bits, sizeof(best64));
+          best_row = static_cast<uint32_t>(0xFFFFFFFFull - ctx->h_keys[0]);
+        }
+      }
+      if (best_row != 0xFFFFFFFFu) {
+        row = best_row;
+        d2 = best64;
       }
     }
     positions[pass] = static_cast<uint64_t>(row) + 1;
@@ -830,6 +886,9 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
       ctx->opt_mates = static_cast<int>(value);
     } else if (key == "rescore") {
       ctx->opt_rescore = value != 0;
+    } else if (key == "margin_delta") {
+      if (value > 0.5) fail(TSDD_ERR_PARAMETER, "margin_delta must be below 0.5 (negative = derive from n)");
+      ctx->opt_margin_delta = value;
     } else if (key == "symmetric") {
       ctx->opt_symmetric = value != 0;
     } else if (key == "packed") {

@@ -74,6 +74,7 @@ struct SearchState {
   uint8_t* excluded;        // N
   uint64_t* best;           // 1 best key
   DeviceCounters* counters;
+  float margin;             // 1 + delta of the discard test (common.cuh: dead_bound)
 };
 
 int launch_reset_search(SearchState s, cudaStream_t stream);
@@ -128,10 +129,17 @@ int launch_finalize_batch(SearchState s, const uint32_t* d_batch_rows, const uin
 int launch_seed_best(SearchState s, cudaStream_t stream);
 int launch_exclude_zone(SearchState s, uint32_t row, cudaStream_t stream);
 
-// float64 re-scoring of one pair (finalists): d_out[0] = d^2.
-int launch_rescore_pair(const double* d_series, const double* d_mean, const double* d_inv_sigma,
-                        uint32_t n, uint32_t row_a, uint32_t row_b, double* d_out,
-                        cudaStream_t stream);
+// Finalists of a pass: exact, allowed rows whose float32 nn is within the safety band of
+// the best-so-far.  d_list[0 .. min(count, cap)) = rows; d_count[0] = how many qualify.
+int launch_collect_finalists(SearchState s, uint32_t* d_list, uint32_t cap, uint32_t* d_count,
+                             cudaStream_t stream);
+
+// Exact float64 nearest-neighbour distance (squared) of one row over ALL non-self rows,
+// straight from the series: d_out_bits[0] = bits of the minimum (must be preset to the
+// bits of an upper bound, e.g. +inf), with early abandoning against it.
+int launch_exact_nn(const double* d_series, const double* d_mean, const double* d_inv_sigma,
+                    uint32_t n_rows, uint32_t n, uint32_t row, double* d_zrow,
+                    unsigned long long* d_out_bits, cudaStream_t stream);
 
 // ------------------------------------------------------------------ probes
 int launch_fp32_probe(int which, float* d_sink, int blocks, int iters, cudaStream_t stream);

@@ -140,7 +140,7 @@ __global__ void k_flag_live(SearchState s, const uint32_t* __restrict__ order, u
   if (e >= s.n_rows) return;
   const uint32_t row = order[e];
   bool live = (e % world == rank) && !s.excluded[row] && !s.exact[row];
-  if (live && pruning) live = !is_dead(s.nn[row], row, *s.best);
+  if (live && pruning) live = !is_dead(s.nn[row], *s.best, s.margin);
   flags[t] = live ? 1u : 0u;
 }
 
@@ -184,7 +184,7 @@ k_compact_batch(SearchState s, const uint32_t* __restrict__ in, const uint32_t* 
     if (idx < count) {
       row = in[idx];
       slot = in_slots[idx];
-      keep = !pruning || !is_dead(load_key(s.nn + row), row, best);
+      keep = !pruning || !is_dead(load_key(s.nn + row), best, s.margin);
     }
     const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, keep);
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -261,7 +261,7 @@ k_finalize_batch(SearchState s, const uint32_t* __restrict__ batch_rows,
   if (idx < count) {
     const uint32_t row = batch_rows[idx];
     const uint64_t key = s.nn[row];
-    if (!pruning || !is_dead(key, row, best)) {
+    if (!pruning || !is_dead(key, best, s.margin)) {
       s.exact[row] = 1;
       if (key_bits(key) != kInfBits) mine = best_key(key_bits(key), row);
     }
@@ -488,7 +488,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
           live = true;
         } else {
           const float bound = fminf(__uint_as_float(key_bits(pf_key)), s_loc[tid]);
-          if (!(best_key(__float_as_uint(bound), row) < best)) {
+          if (!dead_bound(bound, best, s.margin)) {
             thr = bound;
             live = true;
           }
@@ -848,7 +848,7 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
             live[q] = true;
           } else {
             const float bound = fminf(__uint_as_float(key_bits(cand_key[q])), sh.loc[r]);
-            if (!(best_key(__float_as_uint(bound), row) < best)) {
+            if (!dead_bound(bound, best, s.margin)) {
               thr = bound;
               live[q] = true;
             }
@@ -1067,25 +1067,55 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
 
 }  // namespace ws
 
-// float64 distance of one pair straight from the series (finalists only).
+// ------------------------------------------------------------------ finalists, decided in float64
 __global__ void __launch_bounds__(256)
-k_rescore_pair(const double* __restrict__ x, const double* __restrict__ mean,
-               const double* __restrict__ inv_sigma, uint32_t n, uint32_t row_a, uint32_t row_b,
-               double* out) {
-  __shared__ double partial[256];
-  const double ma = mean[row_a], ia = inv_sigma[row_a], mb = mean[row_b], ib = inv_sigma[row_b];
-  double sum = 0.0;
-  for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) {
-    const double d = (x[row_a + t] - ma) * ia - (x[row_b + t] - mb) * ib;
-    sum += d * d;
+k_collect_finalists(SearchState s, uint32_t* __restrict__ list, uint32_t cap, uint32_t* __restrict__ count) {
+  const uint64_t best = *s.best;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < s.n_rows; i += gridDim.x * blockDim.x) {
+    if (!s.exact[i] || s.excluded[i]) continue;
+    const uint64_t key = s.nn[i];
+    if (key_bits(key) == kInfBits || is_dead(key, best, s.margin)) continue;
+    const uint32_t at = atomicAdd(count, 1u);
+    if (at < cap) list[at] = i;
   }
-  partial[threadIdx.x] = sum;
-  __syncthreads();
-  for (int w = 128; w > 0; w >>= 1) {
-    if (threadIdx.x < w) partial[threadIdx.x] += partial[threadIdx.x + w];
-    __syncthreads();
+}
+
+// z-normalised float64 values of one row (series.cpp:21-37), kept in global memory
+// so that every thread of k_exact_nn reads them as a broadcast.
+__global__ void k_zrow(const double* __restrict__ x, const double* __restrict__ mean,
+                       const double* __restrict__ inv_sigma, uint32_t n, uint32_t row, double* __restrict__ z) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < n) z[t] = __dmul_rn(x[row + t] - mean[row], inv_sigma[row]);  // same rounding as in k_exact_nn
+}
+
+// One thread per neighbour j (adjacent threads read adjacent samples: coalesced),
+// float64 throughout, early abandoning against the running minimum.
+__global__ void __launch_bounds__(256)
+k_exact_nn(const double* __restrict__ x, const double* __restrict__ mean, const double* __restrict__ inv_sigma,
+           uint32_t n_rows, uint32_t n, uint32_t row, const double* __restrict__ z,
+           unsigned long long* out_bits) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  double mine = __longlong_as_double(0x7FF0000000000000ll);  // +inf
+  if (j < n_rows && gap_u32(row, j) >= n) {
+    const double bound = __longlong_as_double(static_cast<long long>(
+        __ldcg(reinterpret_cast<const unsigned long long*>(out_bits))));
+    const double mu = mean[j], inv = inv_sigma[j];
+    const double* p = x + j;
+    double sum = 0.0;
+    uint32_t t = 0;
+    for (; t < n; ++t) {
+      // both rows rounded the same way (no fma contraction), so that d(i, j) == d(j, i) to the
+      // last bit and mutual nearest neighbours tie exactly, as they do in the reference
+      const double d = z[t] - __dmul_rn(p[t] - mu, inv);
+      sum = fma(d, d, sum);
+      if ((t & 31) == 31 && sum > bound) break;
+    }
+    if (t >= n) mine = sum;
   }
-  if (threadIdx.x == 0) out[0] = partial[0];
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) mine = fmin(mine, __shfl_xor_sync(0xFFFFFFFFu, mine, d));
+  if ((threadIdx.x & 31) == 0 && mine < __longlong_as_double(0x7FF0000000000000ll))
+    atomicMin(out_bits, static_cast<unsigned long long>(__double_as_longlong(mine)));  // doubles >= 0 order like their bits
 }
 
 bool g_packed_default = true;
@@ -1210,11 +1240,20 @@ int launch_exclude_zone(SearchState s, uint32_t row, cudaStream_t stream) {
   return 1;
 }
 
-int launch_rescore_pair(const double* d_series, const double* d_mean, const double* d_inv_sigma,
-                        uint32_t n, uint32_t row_a, uint32_t row_b, double* d_out,
-                        cudaStream_t stream) {
-  k_rescore_pair<<<1, 256, 0, stream>>>(d_series, d_mean, d_inv_sigma, n, row_a, row_b, d_out);
+int launch_collect_finalists(SearchState s, uint32_t* d_list, uint32_t cap, uint32_t* d_count,
+                             cudaStream_t stream) {
+  cudaMemsetAsync(d_count, 0, sizeof(uint32_t), stream);
+  k_collect_finalists<<<296, 256, 0, stream>>>(s, d_list, cap, d_count);
   return 1;
+}
+
+int launch_exact_nn(const double* d_series, const double* d_mean, const double* d_inv_sigma,
+                    uint32_t n_rows, uint32_t n, uint32_t row, double* d_zrow,
+                    unsigned long long* d_out_bits, cudaStream_t stream) {
+  k_zrow<<<blocks_for(n, 256), 256, 0, stream>>>(d_series, d_mean, d_inv_sigma, n, row, d_zrow);
+  k_exact_nn<<<blocks_for(n_rows, 256), 256, 0, stream>>>(d_series, d_mean, d_inv_sigma, n_rows, n, row,
+                                                         d_zrow, d_out_bits);
+  return 2;
 }
 
 }  // namespace tsdd_b200
