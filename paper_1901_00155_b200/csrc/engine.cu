@@ -485,7 +485,7 @@ struct Segment {
 // HOTSAX inner heuristic), then the covering scan of all rows in growing ranges.
 std::vector<Segment> plan_segments(const tsdd_cuda_ctx* ctx, bool pruning) {
   std::vector<Segment> plan;
-  const uint32_t tile = scan_neighbour_tile_rows();
+  const uint32_t tile = kTileRows;  // planning unit: 128 neighbour rows
   const uint32_t slot_tiles = (ctx->rows + tile - 1) / tile;
   if (pruning) {
     // the windows only lower bounds (their rows are met again by the covering scan):
@@ -525,8 +525,7 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
   // Every batch starts its covering scan somewhere else (golden-ratio steps around the
   // ring of tiles), so that the rows whose bounds drop as a by-product (d(i,j) = d(j,i))
   // are spread over the whole series instead of always being the first ones.
-  const uint32_t tile = scan_neighbour_tile_rows();
-  const uint32_t slot_tiles = (ctx->rows + tile - 1) / tile;
+  const uint32_t slot_tiles = (ctx->rows + kTileRows - 1) / kTileRows;
   const uint32_t rotation =
       (pruning && ctx->opt_rotate)
           ? static_cast<uint32_t>((ctx->stats.batches * 0.6180339887498949 - std::floor(ctx->stats.batches * 0.6180339887498949)) * slot_tiles) % slot_tiles
@@ -552,9 +551,6 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
     }
     const uint32_t padded = round_up_u32(count, kTileRows);
     launches += launch_gather_rows(s, list, ctx->sel.ptr, padded, ctx->batch_matrix.ptr, st);
-    const uint64_t tiles = static_cast<uint64_t>(plan[r].k_end - plan[r].k_begin) * (padded / kTileRows);
-    const uint64_t resident = 148ull * (tile == 64 ? 2 : 1);
-    const int per_cta = static_cast<int>(std::min<uint64_t>(16, std::max<uint64_t>(1, tiles / (resident * 8ull))));
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->opt_time_kernels) {
       e0 = next_event(ctx);
@@ -562,9 +558,9 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
       CUDA_OK(cudaEventRecord(e0, st));
     }
     const int launched =
-        launch_scan_tiles(s, ctx->batch_matrix.ptr, list, slots, ctx->sel.ptr, padded,
+        launch_scan_tiles(s, ctx->batch_matrix.ptr, list, slots, ctx->sel.ptr, count,
                           plan[r].window ? ctx->sorted_row : nullptr, plan[r].k_begin, plan[r].k_end, rotation,
-                          per_cta, pruning, ctx->opt_symmetric, st);
+                          pruning, ctx->opt_symmetric, st);
     if (ctx->opt_time_kernels) CUDA_OK(cudaEventRecord(e1, st));
     launches += launched;
     ctx->stats.scan_kernel_launches += launched;

@@ -108,18 +108,16 @@ int launch_batch_slots(const uint32_t* d_batch_rows, const uint32_t* d_sel, cons
 int launch_gather_rows(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,
                        uint32_t capacity_padded, float* d_batch_matrix, cudaStream_t stream);
 
-// The tiled early-abandoning distance kernel: batch candidates x neighbour tiles
-// [k_begin, k_end).  d_nbr_index == nullptr: tile k holds the 128 rows of tile
-// (k + rotation) mod T (the covering scan).  Otherwise (window mode) tile k holds 128 slots of d_nbr_index (the
-// hash-sorted row list) around the candidate tile's own slot, alternating outwards.
+// The tiled early-abandoning distance kernel: batch candidates x neighbour units
+// [k_begin, k_end), one unit = 128 rows.  d_nbr_index == nullptr: unit k holds the rows of
+// unit (k + rotation) mod T of the matrix (the covering scan).  Otherwise (window mode)
+// unit k holds 128 slots of d_nbr_index (the hash-sorted row list) around the candidate
+// tile's own slot, alternating outwards.  live_upper_bound >= the live batch size in
+// d_sel[0]; it sizes the grid and picks the tile shape.
 int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t* d_batch_rows,
-                      const uint32_t* d_batch_slots, const uint32_t* d_sel, uint32_t capacity_padded,
+                      const uint32_t* d_batch_slots, const uint32_t* d_sel, uint32_t live_upper_bound,
                       const uint32_t* d_nbr_index, uint32_t k_begin, uint32_t k_end, uint32_t rotation,
-                      int tiles_per_cta, bool pruning, bool symmetric, cudaStream_t stream);
-
-// Neighbour rows per tile of the variant launch_scan_tiles currently uses (64 or 128):
-// the unit of k_begin / k_end / rotation.
-uint32_t scan_neighbour_tile_rows();
+                      bool pruning, bool symmetric, cudaStream_t stream);
 
 // Survivors of a complete scan are exact; each raises the best-so-far.
 int launch_finalize_batch(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,

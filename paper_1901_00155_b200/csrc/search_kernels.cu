@@ -296,10 +296,9 @@ k_finalize_batch(SearchState s, const uint32_t* __restrict__ batch_rows,
 constexpr int kStages = TSDD_SCAN_STAGES;
 constexpr int kRowBytes = kChunk * 4;   // bytes of one row inside a stage
 constexpr int kPieces = kChunk / 4;     // 16-byte pieces per row and stage
-constexpr int kOperandBytes = kTileRows * kChunk * 4;  // the 128 candidate rows of a stage
 constexpr int kScanThreads = 256;
-constexpr size_t scan_smem_bytes(int nbr_rows) {
-  return static_cast<size_t>(kStages) * (kOperandBytes + nbr_rows * kChunk * 4) + 6 * kTileRows * 4;
+constexpr size_t scan_smem_bytes(int cand_rows, int nbr_rows) {
+  return static_cast<size_t>(kStages) * (cand_rows + nbr_rows) * kChunk * 4 + 6 * kTileRows * 4;
 }
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
@@ -316,12 +315,12 @@ __device__ __forceinline__ void cp_async_wait() {
 // CTA).  The neighbour rows are addressed through s_brow (row numbers in shared
 // memory), so a tile may hold any 128 rows: every piece is still one 16-byte
 // part of a full 128-byte line.
-template <int kNbr>
+template <int kCand, int kNbr>
 __device__ __forceinline__ void issue_stage(unsigned char* stage, const float* a_tile,
                                             const float* rows, const uint32_t* s_brow,
                                             uint32_t stride, uint32_t col0) {
 #pragma unroll
-  for (int q = 0; q < kTileRows * kPieces / kScanThreads; ++q) {  // candidate rows
+  for (int q = 0; q < kCand * kPieces / kScanThreads; ++q) {  // candidate rows
     const uint32_t piece = threadIdx.x + q * kScanThreads;
     const uint32_t r = piece / kPieces, kc = piece % kPieces;
     cp_async16(stage + r * kRowBytes + ((kc ^ (r & 7)) << 4), a_tile + static_cast<size_t>(r) * stride + col0 + kc * 4);
@@ -330,7 +329,7 @@ __device__ __forceinline__ void issue_stage(unsigned char* stage, const float* a
   for (int q = 0; q < kNbr * kPieces / kScanThreads; ++q) {  // neighbour rows
     const uint32_t piece = threadIdx.x + q * kScanThreads;
     const uint32_t r = piece / kPieces, kc = piece % kPieces;
-    cp_async16(stage + kOperandBytes + r * kRowBytes + ((kc ^ (r & 7)) << 4),
+    cp_async16(stage + kCand * kRowBytes + r * kRowBytes + ((kc ^ (r & 7)) << 4),
                rows + static_cast<size_t>(s_brow[r]) * stride + col0 + kc * 4);
   }
 }
@@ -400,18 +399,28 @@ struct ScanArgs {
   int pruning;
 };
 
-// CTA = 256 threads = 16 x 16; thread (ty, tx) owns the pairs {ty + 16u} x {tx + 16w},
-// u < 8, w < kW.  kW = 8: a 128 x 128 tile, 255 registers, one CTA per SM.  kW = 4: a
-// 128 x 64 tile, <= 128 registers and 98 KB of shared memory, so TWO CTAs share an SM
-// and one computes while the other sits in its per-chunk barrier, threshold refresh or
-// pipeline refill (with one CTA per SM all warps leave the FMA pipe idle together).
-template <bool kPacked, bool kSymmetric, int kW>
+// CTA = 256 threads = kTy x kTx; thread (ty, tx) owns the pairs {ty + kTy u} x {tx + kTx w},
+// u < 8, w < kW.  Three shapes (candidates x neighbours per tile):
+//   kTy 16, kW 4: 128 x 64   <= 128 registers, 98 KB: TWO CTAs share an SM and one computes
+//                            while the other sits in a barrier, threshold refresh or refill
+//                            (with one CTA per SM all warps leave the FMA pipe idle together);
+//   kTy  8, kW 4:  64 x 128  same resources; for batches that have shrunk to <= 64 live
+//                            candidates (the long-lived survivors that scan the whole series):
+//                            half the padding rows of a 128-row candidate tile;
+//   kTy 16, kW 8: 128 x 128  255 registers, one CTA per SM ("wide_tile", measured 7 % slower).
+// Tile numbers k (ScanArgs) always count 128 neighbour rows; a shape with 64-row
+// neighbour tiles walks the two halves of each.
+template <bool kPacked, bool kSymmetric, int kTy, int kW>
 __global__ void __launch_bounds__(kScanThreads, kW == 4 ? 2 : 1)
 k_scan_tiles(SearchState s, ScanArgs a) {
   constexpr int kU = 8;
-  constexpr int kTx = 16;
+  constexpr int kTx = kScanThreads / kTy;
+  constexpr int kCand = kTy * kU;                             // candidate rows per tile
   constexpr int kNbr = kTx * kW;                              // neighbour rows per tile
-  constexpr int kStageBytes = kOperandBytes + kNbr * kChunk * 4;
+  constexpr int kSub = kTileRows / kNbr;                      // neighbour tiles per 128-row unit
+  constexpr int kCandBytes = kCand * kRowBytes;
+  constexpr int kStageBytes = (kCand + kNbr) * kRowBytes;
+  static_assert(kCand <= kTileRows && kNbr <= kTileRows && kTileRows % kNbr == 0, "tile shape");
   extern __shared__ __align__(1024) unsigned char smem[];
   float* s_thr = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // candidate thresholds
   uint32_t* s_cand = reinterpret_cast<uint32_t*>(s_thr + kTileRows);      // candidate rows
@@ -422,13 +431,12 @@ k_scan_tiles(SearchState s, ScanArgs a) {
   __shared__ unsigned long long s_calls, s_abandoned, s_terms, s_tiles, s_tile_live;
 
   const uint32_t count = a.sel[0];
-  const uint32_t cand0 = blockIdx.y * kTileRows;
+  const uint32_t cand0 = blockIdx.y * kCand;
   if (cand0 >= count) return;
 
   const uint32_t tid = threadIdx.x, lane = tid & 31;
   const uint32_t tx = tid % kTx, ty = tid / kTx;
-  static_assert(kScanThreads == 16 * kTx, "thread grid is 16 x 16");
-  if (tid < kTileRows) s_cand[tid] = (cand0 + tid < count) ? a.batch_rows[cand0 + tid] : 0xFFFFFFFFu;
+  if (tid < kCand) s_cand[tid] = (cand0 + tid < count) ? a.batch_rows[cand0 + tid] : 0xFFFFFFFFu;
   if (tid == 0) {
     s_calls = 0;
     s_abandoned = 0;
@@ -437,17 +445,24 @@ k_scan_tiles(SearchState s, ScanArgs a) {
     s_tile_live = 0;
   }
   const bool window = a.nbr_index != nullptr;
-  const uint32_t slot_tiles = (s.n_rows + kNbr - 1) / kNbr;
-  const uint32_t centre = window ? a.batch_slots[min(cand0 + kTileRows / 2, count - 1)] / kNbr : 0u;
+  const uint32_t slot_tiles = (s.n_rows + kTileRows - 1) / kTileRows;
+  const uint32_t centre = window ? a.batch_slots[min(cand0 + kCand / 2, count - 1)] / kTileRows : 0u;
   const uint64_t best = a.pruning ? *s.best : 0ull;
   const uint32_t chunks = s.stride / kChunk;
   const float* a_tile = a.batch + static_cast<size_t>(cand0) * s.stride;
   const float inf = __uint_as_float(kInfBits);
 
-  auto slot_tile_of = [&](uint32_t k) -> uint32_t {
-    if (!window) return (k + a.rotation) % slot_tiles;
-    const uint32_t step = (k + 1) >> 1;  // 0, 1, 1, 2, 2, ...
-    return (k & 1) ? (centre + step) % slot_tiles : (centre + slot_tiles - step % slot_tiles) % slot_tiles;
+  // first slot of sub-tile h: unit h / kSub of the launch, half h % kSub of it
+  auto slot0_of = [&](uint32_t h) -> uint32_t {
+    const uint32_t k = h / kSub;
+    uint32_t unit;
+    if (!window) {
+      unit = (k + a.rotation) % slot_tiles;
+    } else {
+      const uint32_t step = (k + 1) >> 1;  // 0, 1, 1, 2, 2, ...
+      unit = (k & 1) ? (centre + step) % slot_tiles : (centre + slot_tiles - step % slot_tiles) % slot_tiles;
+    }
+    return unit * kTileRows + (h % kSub) * kNbr;
   };
   // The bounds a tile starts from are fetched one tile ahead (two dependent global
   // loads in window mode), so their latency hides behind the previous tile's
@@ -455,31 +470,31 @@ k_scan_tiles(SearchState s, ScanArgs a) {
   // abandons less, and s_loc folds in what this CTA itself has found meanwhile.
   uint64_t pf_key = 0;
   uint32_t pf_j = 0xFFFFFFFFu;
-  auto prefetch = [&](uint32_t k) {
-    if (tid < kTileRows) {
+  auto prefetch = [&](uint32_t h) {
+    if (tid < kCand) {
       const uint32_t row = s_cand[tid];
       pf_key = (row != 0xFFFFFFFFu && a.pruning) ? load_key(s.nn + row) : 0ull;
-    } else if (tid < kTileRows + kNbr) {
-      const uint32_t slot = slot_tile_of(k) * kNbr + (tid - kTileRows);
+    } else if (tid < kCand + kNbr) {
+      const uint32_t slot = slot0_of(h) + (tid - kCand);
       pf_j = 0xFFFFFFFFu;
       if (slot < s.n_rows) pf_j = window ? a.nbr_index[slot] : slot;
       pf_key = pf_j != 0xFFFFFFFFu ? load_key(s.nn + pf_j) : 0ull;
     }
   };
-  if (tid < kTileRows) s_loc[tid] = inf;
+  if (tid < kCand) s_loc[tid] = inf;
   __syncthreads();  // s_cand visible
-  const uint32_t k_first = a.k_begin + blockIdx.x * a.tiles_per_cta;
-  if (k_first < a.k_end) prefetch(k_first);
+  const uint32_t h_first = a.k_begin * kSub + blockIdx.x * a.tiles_per_cta, h_end = a.k_end * kSub;
+  if (h_first < h_end) prefetch(h_first);
 
   for (int tt = 0; tt < a.tiles_per_cta; ++tt) {
-    const uint32_t k = k_first + tt;
-    if (k >= a.k_end) break;
-    const uint32_t slot0 = slot_tile_of(k) * kNbr;
+    const uint32_t k = h_first + tt;  // sub-tile number
+    if (k >= h_end) break;
+    const uint32_t slot0 = slot0_of(k);
     __syncthreads();  // everyone is done with the previous tile's shared arrays
 
     // ---- thresholds and neighbour rows of this tile, from the prefetched registers
     bool live = false;
-    if (tid < kTileRows) {
+    if (tid < kCand) {
       const uint32_t row = s_cand[tid];
       float thr = -1.f;
       if (row != 0xFFFFFFFFu) {
@@ -495,8 +510,8 @@ k_scan_tiles(SearchState s, ScanArgs a) {
         }
       }
       s_thr[tid] = thr;
-    } else if (tid < kTileRows + kNbr) {
-      const uint32_t t = tid - kTileRows;
+    } else if (tid < kCand + kNbr) {
+      const uint32_t t = tid - kCand;
       s_jrow[t] = pf_j;
       s_brow[t] = pf_j != 0xFFFFFFFFu ? pf_j : s.n_rows;  // row n_rows is zero padding
       s_nub[t] = pf_j != 0xFFFFFFFFu ? __uint_as_float(key_bits(pf_key)) : -1.f;
@@ -507,12 +522,12 @@ k_scan_tiles(SearchState s, ScanArgs a) {
       s_tiles += 1;
       s_tile_live += n_live;
     }
-    if (tt + 1 < a.tiles_per_cta && k + 1 < a.k_end) prefetch(k + 1);
+    if (tt + 1 < a.tiles_per_cta && k + 1 < h_end) prefetch(k + 1);
 
     unsigned long long my_calls = 0;
     if (live) {
       const uint32_t row = s_cand[tid];
-      const uint32_t valid = min(static_cast<uint32_t>(kNbr), s.n_rows - slot0);
+      const uint32_t valid = slot0 < s.n_rows ? min(static_cast<uint32_t>(kNbr), s.n_rows - slot0) : 0u;
       uint32_t overlap = 0;
       if (!window) {
         // contiguous rows [slot0, slot0 + valid): the self-match zone is an interval
@@ -534,7 +549,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
 
     float thr[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) thr[u] = s_thr[ty + 16 * u];
+    for (int u = 0; u < kU; ++u) thr[u] = s_thr[ty + kTy * u];
 
     Acc<kPacked, kU, kW> acc;
     acc.zero();
@@ -542,7 +557,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
 #pragma unroll
     for (int st = 0; st < kStages - 1; ++st) {
       if (static_cast<uint32_t>(st) < chunks)
-        issue_stage<kNbr>(smem + st * kStageBytes, a_tile, s.rows, s_brow, s.stride, st * kChunk);
+        issue_stage<kCand, kNbr>(smem + st * kStageBytes, a_tile, s.rows, s_brow, s.stride, st * kChunk);
       cp_async_commit();
     }
 
@@ -555,19 +570,19 @@ k_scan_tiles(SearchState s, ScanArgs a) {
         break;
       }
       if (c + kStages - 1 < chunks)
-        issue_stage<kNbr>(smem + ((c + kStages - 1) % kStages) * kStageBytes, a_tile, s.rows, s_brow,
+        issue_stage<kCand, kNbr>(smem + ((c + kStages - 1) % kStages) * kStageBytes, a_tile, s.rows, s_brow,
                           s.stride, (c + kStages - 1) * kChunk);
       cp_async_commit();
       if (!warp_done) {
         const unsigned char* a_s = smem + (c % kStages) * kStageBytes + ty * kRowBytes;
-        const unsigned char* b_s = smem + (c % kStages) * kStageBytes + kOperandBytes + tx * kRowBytes;  // rows tx + kTx*w
+        const unsigned char* b_s = smem + (c % kStages) * kStageBytes + kCandBytes + tx * kRowBytes;  // rows tx + kTx*w
 #pragma unroll 2
         for (int kc = 0; kc < kPieces; ++kc) {
           const uint32_t off_a = (kc ^ (ty & 7)) << 4, off_b = (kc ^ (tx & 7)) << 4;
           if constexpr (kW == 8) {
             float4 na[kU];
 #pragma unroll
-            for (int u = 0; u < kU; ++u) na[u] = *reinterpret_cast<const float4*>(a_s + u * (16 * kRowBytes) + off_a);
+            for (int u = 0; u < kU; ++u) na[u] = *reinterpret_cast<const float4*>(a_s + u * (kTy * kRowBytes) + off_a);
 #pragma unroll
             for (int w = 0; w < kW; ++w) {
               const float4 b = *reinterpret_cast<const float4*>(b_s + w * (kTx * kRowBytes) + off_b);
@@ -582,7 +597,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
             for (int w = 0; w < kW; ++w) b[w] = *reinterpret_cast<const float4*>(b_s + w * (kTx * kRowBytes) + off_b);
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
-              const float4 na = *reinterpret_cast<const float4*>(a_s + u * (16 * kRowBytes) + off_a);
+              const float4 na = *reinterpret_cast<const float4*>(a_s + u * (kTy * kRowBytes) + off_a);
 #pragma unroll
               for (int w = 0; w < kW; ++w) acc.add(u, w, na, b[w]);
             }
@@ -629,7 +644,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
     for (int w = 0; w < kW; ++w) jrow[w] = s_jrow[tx + kTx * w];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const uint32_t row = s_cand[ty + 16 * u];
+      const uint32_t row = s_cand[ty + kTy * u];
       uint32_t d_min = 0xFFFFFFFFu, j_min = 0xFFFFFFFFu;  // this thread's best (distance bits, neighbour)
 #pragma unroll
       for (int w = 0; w < kW; ++w) {
@@ -655,7 +670,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
       for (int d = kTx / 2; d > 0; d >>= 1) g_j = min(g_j, __shfl_xor_sync(0xFFFFFFFFu, g_j, d));
       if (tx == 0 && g_j != 0xFFFFFFFFu) {
         atomicMin(as_ull(s.nn + row), static_cast<unsigned long long>(nn_key(g_min, g_j)));
-        s_loc[ty + 16 * u] = fminf(s_loc[ty + 16 * u], __uint_as_float(g_min));
+        s_loc[ty + kTy * u] = fminf(s_loc[ty + kTy * u], __uint_as_float(g_min));
       }
     }
   }
@@ -791,20 +806,27 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
   __syncthreads();  // the only CTA-wide barrier
 
   const bool window = a.nbr_index != nullptr;
-  const uint32_t slot_tiles = (s.n_rows + kNbrWs - 1) / kNbrWs;
+  constexpr uint32_t kSub = kTileRows / kNbrWs;  // ScanArgs counts 128-row units; this kernel walks their halves
+  const uint32_t slot_tiles = (s.n_rows + kTileRows - 1) / kTileRows;
   const uint32_t chunks = s.stride / kChunk;
-  const uint32_t k_first = a.k_begin + blockIdx.x * a.tiles_per_cta;
-  const uint32_t n_tiles = k_first < a.k_end ? min(static_cast<uint32_t>(a.tiles_per_cta), a.k_end - k_first) : 0u;
+  const uint32_t k_first = a.k_begin * kSub + blockIdx.x * a.tiles_per_cta, k_end = a.k_end * kSub;
+  const uint32_t n_tiles = k_first < k_end ? min(static_cast<uint32_t>(a.tiles_per_cta), k_end - k_first) : 0u;
 
   if (warp == kConsumerWarps) {
     // ================================================================ producer warp
-    const uint32_t centre = window ? a.batch_slots[min(cand0 + kTileRows / 2, count - 1)] / kNbrWs : 0u;
+    const uint32_t centre = window ? a.batch_slots[min(cand0 + kTileRows / 2, count - 1)] / kTileRows : 0u;
     const uint64_t best = a.pruning ? *s.best : 0ull;
     const float* a_tile = a.batch + static_cast<size_t>(cand0) * s.stride;
-    auto slot_tile_of = [&](uint32_t k) -> uint32_t {
-      if (!window) return (k + a.rotation) % slot_tiles;
-      const uint32_t step = (k + 1) >> 1;
-      return (k & 1) ? (centre + step) % slot_tiles : (centre + slot_tiles - step % slot_tiles) % slot_tiles;
+    auto slot0_of = [&](uint32_t h) -> uint32_t {
+      const uint32_t k = h / kSub;
+      uint32_t unit;
+      if (!window) {
+        unit = (k + a.rotation) % slot_tiles;
+      } else {
+        const uint32_t step = (k + 1) >> 1;
+        unit = (k & 1) ? (centre + step) % slot_tiles : (centre + slot_tiles - step % slot_tiles) % slot_tiles;
+      }
+      return unit * kTileRows + (h % kSub) * kNbrWs;
     };
     // bounds of the next tile, fetched while the current one streams
     uint64_t cand_key[4], nbr_key[2];
@@ -815,7 +837,7 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
         const uint32_t row = sh.cand[lane + 32 * q];
         cand_key[q] = (row != 0xFFFFFFFFu && a.pruning) ? load_key(s.nn + row) : 0ull;
       }
-      const uint32_t slot0 = slot_tile_of(k) * kNbrWs;
+      const uint32_t slot0 = slot0_of(k);
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const uint32_t slot = slot0 + lane + 32 * q;
@@ -867,8 +889,8 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
       any_live = __any_sync(0xFFFFFFFFu, any_live);
       __syncwarp();
       // pair distances this tile starts (series.hpp:120): live candidates x neighbours at least n away
-      const uint32_t slot0 = slot_tile_of(k) * kNbrWs;
-      const uint32_t valid = min(static_cast<uint32_t>(kNbrWs), s.n_rows - slot0);
+      const uint32_t slot0 = slot0_of(k);
+      const uint32_t valid = slot0 < s.n_rows ? min(static_cast<uint32_t>(kNbrWs), s.n_rows - slot0) : 0u;
       unsigned long long calls = 0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -1180,12 +1202,21 @@ int launch_gather_rows(SearchState s, const uint32_t* d_batch_rows, const uint32
 }
 
 int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t* d_batch_rows,
-                      const uint32_t* d_batch_slots, const uint32_t* d_sel, uint32_t capacity_padded,
+                      const uint32_t* d_batch_slots, const uint32_t* d_sel, uint32_t live_upper_bound,
                       const uint32_t* d_nbr_index, uint32_t k_begin, uint32_t k_end, uint32_t rotation,
-                      int tiles_per_cta, bool pruning, bool symmetric, cudaStream_t stream) {
-  if (k_end <= k_begin) return 0;
-  const uint32_t tiles = k_end - k_begin;
-  dim3 grid((tiles + tiles_per_cta - 1) / tiles_per_cta, capacity_padded / kTileRows);
+                      bool pruning, bool symmetric, cudaStream_t stream) {
+  if (k_end <= k_begin || live_upper_bound == 0) return 0;
+  // tile shape: 64-candidate tiles once the batch has shrunk to that, else 128
+  const bool narrow = !g_wide_tile && g_scan_variant != 2 && live_upper_bound <= 64;
+  const uint32_t cand_rows = narrow ? 64 : 128;
+  const uint32_t nbr_rows = (g_scan_variant == 2) ? 64 : g_wide_tile ? 128 : narrow ? 128 : 64;
+  const uint32_t cand_tiles = (live_upper_bound + cand_rows - 1) / cand_rows;
+  const uint64_t sub_tiles = static_cast<uint64_t>(k_end - k_begin) * (kTileRows / nbr_rows);
+  // a few tiles per CTA (thresholds are refreshed per tile), several waves of CTAs per launch
+  const uint64_t resident = 148ull * ((g_wide_tile || g_scan_variant == 2) ? 1 : 2);
+  const uint64_t want = sub_tiles * cand_tiles / (resident * 8ull);
+  const int tiles_per_cta = static_cast<int>(want < 1 ? 1 : want > 16 ? 16 : want);
+  dim3 grid(static_cast<unsigned>((sub_tiles + tiles_per_cta - 1) / tiles_per_cta), cand_tiles);
   ScanArgs a{d_batch_matrix, d_batch_rows, d_batch_slots, d_sel, d_nbr_index, k_begin, k_end, rotation,
              tiles_per_cta, pruning ? 1 : 0};
   if (g_scan_variant == 2) {
@@ -1199,30 +1230,32 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
     }
     return 1;
   }
-  auto launch = [&](auto kernel, int nbr_rows) {
-    const int smem = static_cast<int>(scan_smem_bytes(nbr_rows));
+  auto launch = [&](auto kernel) {
+    const int smem = static_cast<int>(scan_smem_bytes(cand_rows, nbr_rows));
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     kernel<<<grid, kScanThreads, smem, stream>>>(s, a);
   };
-  const int shape = (g_packed_default ? 4 : 0) | (symmetric ? 2 : 0) | (g_wide_tile ? 1 : 0);
+  const int shape = (g_packed_default ? 8 : 0) | (symmetric ? 4 : 0) | (g_wide_tile ? 2 : narrow ? 1 : 0);
   switch (shape) {
-    case 7: launch(k_scan_tiles<true, true, 8>, 128); break;
-    case 6: launch(k_scan_tiles<true, true, 4>, 64); break;
-    case 5: launch(k_scan_tiles<true, false, 8>, 128); break;
-    case 4: launch(k_scan_tiles<true, false, 4>, 64); break;
-    case 3: launch(k_scan_tiles<false, true, 8>, 128); break;
-    case 2: launch(k_scan_tiles<false, true, 4>, 64); break;
-    case 1: launch(k_scan_tiles<false, false, 8>, 128); break;
-    default: launch(k_scan_tiles<false, false, 4>, 64); break;
+    case 14: launch(k_scan_tiles<true, true, 16, 8>); break;
+    case 13: launch(k_scan_tiles<true, true, 8, 4>); break;
+    case 12: launch(k_scan_tiles<true, true, 16, 4>); break;
+    case 10: launch(k_scan_tiles<true, false, 16, 8>); break;
+    case 9: launch(k_scan_tiles<true, false, 8, 4>); break;
+    case 8: launch(k_scan_tiles<true, false, 16, 4>); break;
+    case 6: launch(k_scan_tiles<false, true, 16, 8>); break;
+    case 5: launch(k_scan_tiles<false, true, 8, 4>); break;
+    case 4: launch(k_scan_tiles<false, true, 16, 4>); break;
+    case 2: launch(k_scan_tiles<false, false, 16, 8>); break;
+    case 1: launch(k_scan_tiles<false, false, 8, 4>); break;
+    default: launch(k_scan_tiles<false, false, 16, 4>); break;
   }
   return 1;
 }
 
-uint32_t scan_neighbour_tile_rows() { return (g_scan_variant != 2 && g_wide_tile) ? 128u : 64u; }
-void set_scan_variant(int variant) { g_scan_variant = variant; }
-
 void set_packed_math(bool on) { g_packed_default = on; }
 void set_wide_tile(bool on) { g_wide_tile = on; }
+void set_scan_variant(int variant) { g_scan_variant = variant; }
 
 int launch_finalize_batch(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,
                           uint32_t capacity, bool pruning, cudaStream_t stream) {
