@@ -101,26 +101,47 @@ k_window_encode(const double* __restrict__ x, uint32_t rows, uint32_t n, uint32_
 }
 
 // Subsequence matrix (series.cpp:46-74), float32: element (i, t) is the
-// float64 value (x[i+t] - mu_i) * (1/sigma_i) rounded once.  One thread
-// writes one float4; a warp writes 512 contiguous bytes.  Write-bound.
-__global__ void __launch_bounds__(256)
+// float64 value (x[i+t] - mu_i) * (1/sigma_i) rounded once.  HBM write-bound:
+// a block owns kBuildRows consecutive rows x kBuildCols columns, whose samples
+// x[i0 + t0 .. i0 + t0 + kBuildRows + kBuildCols) it stages in shared memory
+// ONCE (each sample is needed by up to kBuildRows rows).  Thread j produces
+// columns j, j + 256, ... of every row: consecutive lanes read consecutive
+// doubles (conflict-free) and write consecutive floats (one full 128-byte line
+// per warp and store).
+constexpr int kBuildRows = 32;
+constexpr int kBuildCols = 1024;
+constexpr int kBuildThreads = 256;
+
+__global__ void __launch_bounds__(kBuildThreads)
 k_build_rows(const double* __restrict__ x, const double* __restrict__ mean,
              const double* __restrict__ inv_sigma, uint32_t rows, uint32_t n, uint32_t stride,
              float* __restrict__ out) {
-  const uint32_t quads = stride / 4;
-  const size_t idx = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const size_t row = idx / quads;
-  if (row >= rows) return;
-  const uint32_t t0 = static_cast<uint32_t>(idx % quads) * 4;
-  const double mu = mean[row];
-  const double inv = inv_sigma[row];
-  const double* p = x + row + t0;
-  float4 v;
-  v.x = (t0 + 0 < n) ? static_cast<float>((p[0] - mu) * inv) : 0.f;
-  v.y = (t0 + 1 < n) ? static_cast<float>((p[1] - mu) * inv) : 0.f;
-  v.z = (t0 + 2 < n) ? static_cast<float>((p[2] - mu) * inv) : 0.f;
-  v.w = (t0 + 3 < n) ? static_cast<float>((p[3] - mu) * inv) : 0.f;
-  *reinterpret_cast<float4*>(out + row * stride + t0) = v;
+  __shared__ double s_x[kBuildRows + kBuildCols];
+  __shared__ double s_mu[kBuildRows], s_inv[kBuildRows];
+  const uint32_t i0 = blockIdx.x * kBuildRows;
+  const uint32_t t0 = blockIdx.y * kBuildCols;
+  const uint32_t n_rows = min(static_cast<uint32_t>(kBuildRows), rows - i0);
+  const uint32_t n_cols = min(static_cast<uint32_t>(kBuildCols), stride - t0);
+  // samples x[i0 + t0 + e], e < n_rows + n_cols - 1, clipped to the window columns that exist (t < n)
+  const uint32_t last_sample = i0 + n_rows - 1 + n;  // exclusive end of what these rows may touch
+  for (uint32_t e = threadIdx.x; e < n_rows + n_cols; e += kBuildThreads) {
+    const uint32_t at = i0 + t0 + e;
+    s_x[e] = at < last_sample ? x[at] : 0.0;
+  }
+  if (threadIdx.x < n_rows) {
+    s_mu[threadIdx.x] = mean[i0 + threadIdx.x];
+    s_inv[threadIdx.x] = inv_sigma[i0 + threadIdx.x];
+  }
+  __syncthreads();
+  for (uint32_t r = 0; r < n_rows; ++r) {
+    const double mu = s_mu[r], inv = s_inv[r];
+    float* dst = out + static_cast<size_t>(i0 + r) * stride + t0;
+#pragma unroll
+    for (int q = 0; q < kBuildCols / kBuildThreads; ++q) {
+      const uint32_t c = threadIdx.x + q * kBuildThreads;
+      if (c < n_cols) dst[c] = (t0 + c < n) ? static_cast<float>((s_x[r + c] - mu) * inv) : 0.f;
+    }
+  }
 }
 
 // ------------------------------------------------------------------ scan
@@ -336,9 +357,8 @@ int launch_window_encode(const double* d_series, uint32_t rows, uint32_t n, uint
 int launch_build_rows(const double* d_series, const double* d_mean, const double* d_inv_sigma,
                       uint32_t rows, uint32_t n, uint32_t stride, float* d_rows,
                       cudaStream_t stream) {
-  const size_t threads = static_cast<size_t>(rows) * (stride / 4);
-  k_build_rows<<<blocks_for(threads, 256), 256, 0, stream>>>(d_series, d_mean, d_inv_sigma, rows, n,
-                                                             stride, d_rows);
+  dim3 grid(blocks_for(rows, kBuildRows), blocks_for(stride, kBuildCols));
+  k_build_rows<<<grid, kBuildThreads, 0, stream>>>(d_series, d_mean, d_inv_sigma, rows, n, stride, d_rows);
   return 1;
 }
 
