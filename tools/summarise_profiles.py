@@ -63,15 +63,15 @@ def full(src, dst):
                 rec[f"{h} [{U[j]}]"] = r[j]
         out.append(rec)
     json.dump(out, open(dst + "_raw.json", "w"), indent=1)
-    per_launch = []
-    for rec in out:
-        rd = float(rec["dram__bytes_read.sum [Gbyte]"]) * 1e9 if "dram__bytes_read.sum [Gbyte]" in rec else None
-        wr_key = next((k for k in rec if k.startswith("dram__bytes_write.sum [")), None)
-        wr = None
-        if wr_key:
-            unit = wr_key.split("[")[1].rstrip("]")
-            wr = float(rec[wr_key]) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}[unit]
-        per_launch.append((rd or 0) + (wr or 0))
+    scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}
+
+    def in_bytes(rec, name):
+        key = next((k for k in rec if k.startswith(name + " [")), None)
+        if key is None:
+            return 0.0
+        return float(rec[key]) * scale[key.split("[")[1].rstrip("]")]
+
+    per_launch = [in_bytes(rec, "dram__bytes_read.sum") + in_bytes(rec, "dram__bytes_write.sum") for rec in out]
     summary = {"source": src, "launches_captured": len(out),
                "dram_bytes_per_launch": sum(per_launch) / max(1, len(per_launch)),
                "dram_bytes_each": per_launch}
