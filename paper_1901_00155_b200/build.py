@@ -79,21 +79,21 @@ def build_gen(force: bool = False) -> str:
 
 
 def build_tools(force: bool = False) -> str:
-    """tools/tsdd_cuda_find: the C++ host layer (include/tsdd/cuda_engine.hpp) end to end."""
-    target = os.path.join(LIB, "tsdd_cuda_find")
-    src = os.path.join(ROOT, "tools", "tsdd_cuda_find.cpp")
+    """tools/tsdd_cuda (find | bench | generate): the C++ host layer (include/tsdd/cuda_engine.hpp) end to end."""
+    target = os.path.join(LIB, "tsdd_cuda")
+    src = os.path.join(ROOT, "tools", "tsdd_cuda.cpp")
     deps = [src, os.path.join(INCLUDE, "tsdd", "cuda_engine.hpp"), os.path.join(INCLUDE, "tsdd_cuda.h"),
             os.path.join(LIB, "libtsdd_cuda.so")]
     if force or _stale(target, deps):
         cxx = HOST_CXX if os.path.exists(HOST_CXX) else "g++"
         _run([cxx, "-std=c++17", "-O2", "-Wall", "-Wextra", "-I", INCLUDE, "-o", target, src, "-L", LIB,
-              "-ltsdd_cuda", "-Wl,-rpath,$ORIGIN"])
+              "-ltsdd_cuda", "-ldl", "-lpthread", "-Wl,-rpath,$ORIGIN"])
     return target
 
 
 def build_all(force: bool = False, verbose: bool = False) -> dict:
     out = {"gen": build_gen(force), "cuda": build_cuda(force, verbose)}
-    out["find"] = build_tools(force)
+    out["cli"] = build_tools(force)
     return out
 
 

@@ -298,23 +298,76 @@ def test_nccl_exchange_with_one_rank(chk):
     assert pos[0] == want["position"] and dist[0] == pytest.approx(want["distance"], rel=DIST_RTOL)
 
 
-def test_cpp_host_layer_end_to_end(chk, tmp_path):
-    """include/tsdd/cuda_engine.hpp through tools/tsdd_cuda_find (the `tsdd find` analogue)."""
-    import json
+def _cli(*args, env=None):
     import os
     import subprocess
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "paper_1901_00155_b200", "_lib", "tsdd_cuda")
+    full_env = dict(os.environ, **(env or {}))
+    return subprocess.run([exe, *[str(a) for a in args]], capture_output=True, text=True, env=full_env)
+
+
+def test_cli_find_end_to_end(chk, tmp_path):
+    """include/tsdd/cuda_engine.hpp through tools/tsdd_cuda.cpp (the `tsdd find` analogue)."""
+    import json
+
     x = planted_walk(8, 9000, 96)
+    want = chk.topk(x, 96, 6, 5, 3)
     path = tmp_path / "series.f32le"
     x.tofile(path)
-    p = subprocess.run([os.path.join(root, "paper_1901_00155_b200", "_lib", "tsdd_cuda_find"), str(path),
-                        "96", "6", "5", "3"], capture_output=True, text=True)
+    p = _cli("find", "--input", path, "--format", "f32le", "--n", 96, "--word-len", 6, "--alphabet", 5, "--k", 3)
     assert p.returncode == 0, p.stderr
     got = json.loads(p.stdout)
-    want = chk.topk(x, 96, 6, 5, 3)
     assert [d["pos"] for d in got["discords"]] == want["positions"] and got["pos"] == want["positions"][0]
     np.testing.assert_allclose([d["dist"] for d in got["discords"]], want["distances"], rtol=DIST_RTOL)
+    assert got["engine"] == "cuda" and got["m"] == 9000 and got["calls"] > 0
+    # csv series and csv result (tools/tsdd.cpp:96-108: same columns)
+    csv = tmp_path / "series.csv"
+    csv.write_text("t\n" + "\n".join(repr(float(v)) for v in x) + "\n")
+    p = _cli("find", "--input", csv, "--n", 96, "--word-len", 6, "--alphabet", 5, "--output", "csv")
+    assert p.returncode == 0, p.stderr
+    header, row = p.stdout.strip().splitlines()
+    assert header == "engine,m,n,word_len,alphabet,threads,pos,dist,calls,prep_time_s,search_time_s"
+    cells = row.split(",")
+    assert cells[0] == "cuda" and int(cells[6]) == want["positions"][0]
+    assert float(cells[7]) == pytest.approx(want["distances"][0], rel=DIST_RTOL)
+
+
+def test_cli_several_ranks_in_one_process(chk, tmp_path):
+    """--gpus: one host thread and one context per rank, in-process max-exchange
+    (here every rank on device 0; the kernels never wait on one another)."""
+    import json
+
+    x = planted_walk(15, 16000, 64)
+    want = chk.topk(x, 64, 4, 4, 3)
+    path = tmp_path / "series.f32le"
+    x.tofile(path)
+    p = _cli("find", "--input", path, "--format", "f32le", "--n", 64, "--k", 3, "--gpus", "0,0,0")
+    assert p.returncode == 0, p.stderr
+    got = json.loads(p.stdout)
+    assert got["gpus"] == 3 and [d["pos"] for d in got["discords"]] == want["positions"]
+    np.testing.assert_allclose([d["dist"] for d in got["discords"]], want["distances"], rtol=DIST_RTOL)
+
+
+def test_cli_bench_sweep(chk, tmp_path):  # run_bench / write_bench_csv, src/bench.cpp:21-87
+    x = planted_walk(21, 12000, 64)
+    path = tmp_path / "series.f32le"
+    x.tofile(path)
+    p = _cli("bench", "--input", path, "--format", "f32le", "--n", "32,64", "--gpus", "1,2", "--repeats", 2,
+             env={"TSDD_CUDA_SAME_DEVICE": "1"})
+    assert p.returncode == 0, p.stderr
+    lines = p.stdout.strip().splitlines()
+    assert lines[0] == ("engine,m,n,threads,wall_time_s,calls,pos,dist,speedup,efficiency,"
+                        "gpus,prep_time_s,search_time_s")
+    rows = [dict(zip(lines[0].split(","), ln.split(","))) for ln in lines[1:]]
+    assert [(int(r["n"]), int(r["gpus"])) for r in rows] == [(32, 1), (32, 2), (64, 1), (64, 2)]
+    for r in rows:
+        want = chk.run_discovery(x, int(r["n"]), 4, 4, engine="phidd")
+        assert int(r["pos"]) == want["position"] and float(r["dist"]) == pytest.approx(want["distance"], rel=DIST_RTOL)
+        if int(r["gpus"]) == 1:
+            assert float(r["speedup"]) == 1.0 and float(r["efficiency"]) == 1.0
+        assert float(r["efficiency"]) == pytest.approx(float(r["speedup"]) / int(r["gpus"]), rel=1e-5)
 
 
 # ------------------------------------------------------------------ randomised small cases (edge shapes)

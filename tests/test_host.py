@@ -220,24 +220,69 @@ def test_exchange_over_gloo_with_two_ranks(tmp_path):
     assert outs[0].split("ok")[1].split()[:2] == outs[1].split("ok")[1].split()[:2]
 
 
-# ------------------------------------------------------------------ C++ host layer (include/tsdd/cuda_engine.hpp)
-FIND = os.path.join(ROOT, "paper_1901_00155_b200", "_lib", "tsdd_cuda_find")
+# ------------------------------------------------------------------ C++ host layer and CLI (tools/tsdd_cuda.cpp)
+CLI = os.path.join(ROOT, "paper_1901_00155_b200", "_lib", "tsdd_cuda")
+
+
+def _cli(*args):
+    return subprocess.run([CLI, *[str(a) for a in args]], capture_output=True, text=True)
 
 
 @pytest.mark.parametrize("args,code,text", [
-    (["16", "2", "4"], 2, "no subsequence has a non-self match: N=5 <= n=16 (need m >= 2n)"),
-    (["0", "2", "4"], 2, "n=0 must satisfy 1 <= n <= m=20"),
-    (["4", "9", "4"], 2, "word_len=9 must satisfy 1 <= word_len <= n=4"),
-    (["4", "2", "11"], 2, "alphabet"),
+    (["--n", "16", "--word-len", "2"], 2, "no subsequence has a non-self match: N=5 <= n=16 (need m >= 2n)"),
+    (["--n", "0", "--word-len", "2"], 2, "n=0 must satisfy 1 <= n <= m=20"),
+    (["--n", "4", "--word-len", "9"], 2, "word_len=9 must satisfy 1 <= word_len <= n=4"),
+    (["--n", "4", "--word-len", "2", "--alphabet", "11"], 2, "alphabet"),
+    (["--n", "4", "--threads", "0"], 2, "threads must be >= 1, got 0"),
+    (["--n", "4", "--engine", "phidd"], 2, "unknown engine"),
+    (["--n", "4", "--bogus", "1"], 2, "unknown option '--bogus'"),
+    (["--word-len", "2"], 2, "--n is required"),
 ])
-def test_cpp_layer_maps_errors_to_reference_exit_codes(tmp_path, args, code, text):  # tools/tsdd.cpp:212-223
+def test_cli_maps_errors_to_reference_exit_codes(tmp_path, args, code, text):  # tools/tsdd.cpp:212-223
     path = tmp_path / "a.f64le"
     np.arange(20.0).tofile(path)
-    p = subprocess.run([FIND, str(path), *args], capture_output=True, text=True)
-    assert p.returncode == code and text in p.stderr
-    bad = tmp_path / "b.f64le"
+    p = _cli("find", "--input", path, "--format", "f64le", *args)
+    assert p.returncode == code and text in p.stderr, p.stderr
+
+
+def test_cli_series_readers_follow_the_reference(tmp_path):  # src/io.cpp:23-91
+    csv = tmp_path / "s.csv"
+    csv.write_text("value\n 1.5\n\n2.5\t\r\n3\n")
+    p = _cli("find", "--input", csv, "--n", "2", "--word-len", "2")  # header and blanks skipped; m = 3 < 2n
+    assert p.returncode == 2 and "N=2 <= n=2" in p.stderr and "series: 3 values, min 1.5, max 3" in p.stderr
+    csv.write_text("1\n2\nabc\n")
+    p = _cli("find", "--input", csv, "--n", "1")
+    assert p.returncode == 3 and f"cannot parse 'abc' at {csv}:3" in p.stderr
+    csv.write_text("1\ninf\n")
+    p = _cli("find", "--input", csv, "--n", "1")
+    assert p.returncode == 3 and f"non-finite value at {csv}:2" in p.stderr
+    csv.write_text("header only\n")
+    p = _cli("find", "--input", csv, "--n", "1")
+    assert p.returncode == 3 and "no values found" in p.stderr
+    raw = tmp_path / "s.f64le"
+    raw.write_bytes(b"\0" * 20)
+    p = _cli("find", "--input", raw, "--format", "f64le", "--n", "1")
+    assert p.returncode == 3 and "is not a multiple of 8 (truncated at byte offset 16)" in p.stderr
     x = np.arange(20.0)
     x[6] = np.inf
-    x.tofile(bad)
-    p = subprocess.run([FIND, str(bad), "4", "2", "4"], capture_output=True, text=True)
+    x.tofile(raw)
+    p = _cli("find", "--input", raw, "--format", "f64le", "--n", "4")
     assert p.returncode == 3 and "non-finite value at index 7" in p.stderr
+    p = _cli("find", "--input", tmp_path / "nope", "--n", "4")
+    assert p.returncode == 3 and "cannot open" in p.stderr
+    p = _cli("find", "--input", raw, "--format", "parquet", "--n", "4")
+    assert p.returncode == 2 and "unknown series format 'parquet'" in p.stderr
+    p = _cli("bench", "--input", raw, "--format", "f64le", "--n", "4", "--gpus", "2,4")
+    assert p.returncode == 2 and "must include 1" in p.stderr
+
+
+def test_cli_generate_writes_the_pinned_workloads(tmp_path, golden):
+    out = tmp_path / "cfg1.f32le"
+    p = _cli("generate", "--workload", 1, "--output", out)
+    assert p.returncode == 0, p.stderr
+    x = np.fromfile(out, dtype=np.float32)
+    assert W.sha256(x) == golden["cfg1"]["sha256"]
+    out64 = tmp_path / "cfg1.f64le"
+    assert _cli("generate", "--workload", 1, "--output", out64, "--format", "f64le").returncode == 0
+    np.testing.assert_array_equal(np.fromfile(out64, dtype=np.float64), x.astype(np.float64))
+    assert _cli("generate", "--workload", 9, "--output", out).returncode == 2
