@@ -93,7 +93,7 @@ int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream);
  * also lower the neighbours' bounds), "packed" (0/1: f32x2 arithmetic),
  * "wide_tile" (0/1: 128 x 128 tiles, one CTA per SM, instead of 128 x 64, two),
  * "kernel" (1: cp.async tile kernel; 2: the warp-specialised cp.async.bulk +
- * mbarrier variant, experimental and currently slower), "rotate" (0/1),
+ * mbarrier variant, experimental and currently slower), "rotate" (0/1), "share_bounds" (0/1),
  * "time_kernels" (0/1: CUDA events around every tile-kernel launch).
  * Unknown name -> TSDD_ERR_PARAMETER.  None of them changes the result.     */
 int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value);
@@ -169,10 +169,12 @@ int tsdd_cuda_fetch(tsdd_cuda_ctx* ctx, int what, void* dst, size_t bytes);
 
 /* Entry e of the rarity order belongs to rank (e mod world).  After every
  * batch the packed best-so-far (float bits of d^2 << 32 | ~position) is
- * max-reduced over all ranks.                                               */
+ * max-reduced over all ranks, and (option "share_bounds", default on) the N
+ * nn bounds are min-reduced, so that what one rank's scans learn about a row
+ * prunes it on every rank.                                                  */
 
-/* NCCL path: one 8-byte ncclAllReduce(ncclMax, ncclUint64) per batch on the
- * search stream.  libnccl.so.2 is loaded at run time.  Rank 0 creates the id
+/* NCCL path: one 16-byte ncclAllReduce(ncclMax, ncclUint64) and one N-element
+ * ncclAllReduce(ncclMin, ncclUint64) per batch on the search stream.  libnccl.so.2 is loaded at run time.  Rank 0 creates the id
  * and hands the 128 bytes to the other ranks (any transport).               */
 int tsdd_cuda_comm_unique_id(char id[128]);
 int tsdd_cuda_comm_init(tsdd_cuda_ctx* ctx, const char id[128], int world, int rank);

@@ -6,8 +6,10 @@ to rank ``e mod world``.  After every outer-loop batch the ranks max-reduce two 
 64-bit keys: the best-so-far ``(float bits of d^2) << 32 | ~row`` — integer max is
 "greater distance, then smaller position", the reference's deterministic merge rule
 (discovery.cpp:328-340) — and a "some rank still has candidates" flag that ends the loop
-on all ranks together.  This is the only exchange of the path: one 16-byte
-``ncclAllReduce(ncclMax, ncclUint64)`` per batch on NVLink.
+on all ranks together (one 16-byte ``ncclAllReduce(ncclMax, ncclUint64)`` per batch) —
+and, unless the engine option ``share_bounds`` is off, min-reduce the N packed nn bounds
+(``ncclAllReduce(ncclMin, ncclUint64, N)``), so that what one rank's scans learn about a
+row prunes it on every rank.
 
 Two transports:
   * ``attach_nccl``   the engine's own NCCL communicator (libnccl loaded by the C library);

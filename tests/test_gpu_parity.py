@@ -253,8 +253,9 @@ class _ThreadExchange:
         return fn
 
 
+@pytest.mark.parametrize("share", [1, 0])
 @pytest.mark.parametrize("world", [2, 3])
-def test_rank_count_does_not_change_the_result(chk, world):  # the analogue of SPEC.md:349
+def test_rank_count_does_not_change_the_result(chk, world, share):  # the analogue of SPEC.md:349
     x = planted_walk(15, 16000, 64)
     want = chk.topk(x, 64, 4, 4, 3)
     ex = _ThreadExchange(world)
@@ -264,6 +265,7 @@ def test_rank_count_does_not_change_the_result(chk, world):  # the analogue of S
         try:
             with Context(0) as c:
                 c.set_option("batch", 512)
+                c.set_option("share_bounds", share)
                 c.set_exchange(ex.hook(rank), world, rank)
                 c.prepare(x, 64, 4, 4)
                 results[rank] = c.search(3)
@@ -281,6 +283,34 @@ def test_rank_count_does_not_change_the_result(chk, world):  # the analogue of S
         assert results[r][0] == want["positions"], (r, results[r])
         np.testing.assert_allclose(results[r][1], want["distances"], rtol=DIST_RTOL)
     assert ex.calls > 0
+
+
+def test_sharing_bounds_between_ranks_saves_work():
+    """With "share_bounds" every rank sees what the others' scans learnt about a row; the ranks
+    together then scan fewer candidates than when each keeps its bounds to itself."""
+    x = W.series(1)[0][:40000]
+    scanned = {}
+    for share in (0, 1):
+        world, ex, out = 2, _ThreadExchange(2), [None, None]
+
+        def run(rank, share=share, ex=ex, out=out):
+            with Context(0) as c:
+                c.set_option("batch", 1024)
+                c.set_option("share_bounds", share)
+                c.set_exchange(ex.hook(rank), world, rank)
+                c.prepare(x, 128, 4, 4)
+                res = c.search(1)
+                out[rank] = (res, c.stats()["scanned_candidates"], c.stats()["calls"])
+
+        threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join(timeout=300)
+        assert out[0] is not None and out[1] is not None and out[0][0] == out[1][0]
+        scanned[share] = (out[0][0], out[0][1] + out[1][1], out[0][2] + out[1][2])
+    assert scanned[0][0] == scanned[1][0]              # same discord either way
+    assert scanned[1][2] <= scanned[0][2]              # and fewer pair distances with sharing
 
 
 def test_nccl_exchange_with_one_rank(chk):
