@@ -58,6 +58,7 @@ struct DeviceCounters {
   unsigned long long scanned;    // candidates that entered a full scan
   unsigned long long tiles;      // candidate-tile x neighbour-tile pairs started by the tiled kernel
   unsigned long long tile_live;  // live candidates summed over those tiles (128 per tile = dense)
+  unsigned long long lb_skipped; // (candidate, neighbour tile) pairs the lower-bound filter ruled out
 };
 
 }  // namespace tsdd_b200

@@ -150,7 +150,8 @@ struct tsdd_cuda_ctx {
   bool opt_wide_tile = false;
   int opt_kernel = 1;
   bool opt_time_kernels = true;
-  bool opt_share_bounds = true;     // several ranks: min-reduce the nn bounds after every batch
+  bool opt_share_bounds = true;
+  bool opt_lower_bound = true;      // tile filter by segment-mean lower bounds in the covering scan     // several ranks: min-reduce the nn bounds after every batch
 
   // prepared series
   bool prepared = false;
@@ -158,7 +159,7 @@ struct tsdd_cuda_ctx {
   uint32_t rows = 0, stride = 0, rows_padded = 0;
   DeviceArray<float> series_f32;
   DeviceArray<double> series, mean, inv_sigma;
-  DeviceArray<float> matrix;
+  DeviceArray<float> matrix, lb_means, lb_boxes;
   DeviceArray<uint32_t> hash0, freq, offsets, slot_bucket, scalars, slot_of_row;
   DeviceArray<uint32_t> sort_buf[4], order_buf[4];
   uint32_t *sorted_hash = nullptr, *sorted_row = nullptr, *order = nullptr, *sorted_freq = nullptr;
@@ -174,6 +175,8 @@ struct tsdd_cuda_ctx {
   DeviceArray<uint32_t> finalists;
   DeviceArray<unsigned long long> nn_bits;
   uint32_t batch_capacity = 0;
+  bool lb_active = true;    // the lower-bound filter is still worth its (small) cost in this search
+  bool lb_decided = false;
   uint32_t* h_sel = nullptr;      // pinned, 4 words + a ring of 4 x 4 words for lagged counts
   cudaEvent_t ev_ring[4] = {nullptr, nullptr, nullptr, nullptr};
   uint64_t* h_keys = nullptr;     // pinned, 4 keys
@@ -210,6 +213,9 @@ struct tsdd_cuda_ctx {
     s.best = best.ptr;
     s.counters = counters.ptr;
     s.margin = discard_margin();
+    s.lb_means = (opt_lower_bound && lb_active) ? lb_means.ptr : nullptr;
+    s.lb_boxes = lb_boxes.ptr;
+    s.lb_scale = static_cast<float>(stride / kLbSegments);
     return s;
   }
 };
@@ -296,6 +302,10 @@ void prepare_on_device(tsdd_cuda_ctx* ctx, size_t m, size_t n, size_t word_len, 
   launches += launch_build_rows(ctx->series.ptr, ctx->mean.ptr, ctx->inv_sigma.ptr, rows,
                                 static_cast<uint32_t>(n), ctx->stride, ctx->matrix.ptr, st);
 
+  ctx->lb_means.alloc(static_cast<size_t>(rows) * kLbSegments);
+  ctx->lb_boxes.alloc(static_cast<size_t>((rows + kLbBoxRows - 1) / kLbBoxRows) * 2 * kLbSegments);
+  launches += launch_lower_bound_summaries(ctx->matrix.ptr, rows, ctx->stride, ctx->lb_means.ptr,
+                                           ctx->lb_boxes.ptr, st);
   CUDA_OK(cudaEventRecord(ctx->ev_prep[2], st));
   // bucket index: stable sort of (hash, row) -> runs are the buckets
   const size_t longest_scan = std::max<size_t>(rows, radix_sort_scratch_words(rows));
@@ -619,6 +629,16 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
       const uint32_t count = read_sel(ctx);
       cursor = count == 0 ? ctx->rows : ctx->h_sel[1];
       if (count > 0) {
+        // After two batches, see what the lower-bound filter has ruled out so far; on inputs
+        // where it finds nothing (noise), the rest of the search runs the kernel without it.
+        if (pruning && ctx->opt_lower_bound && !ctx->lb_decided && ctx->stats.batches >= 2) {
+          DeviceCounters c{};
+          CUDA_OK(cudaMemcpyAsync(&c, ctx->counters.ptr, sizeof(c), cudaMemcpyDeviceToHost, st));
+          sync_stream(ctx);
+          ctx->lb_active = c.lb_skipped * 20 >= c.lb_skipped + c.tile_live;  // >= 5 % of (candidate, tile) pairs
+          ctx->lb_decided = true;
+          s = ctx->state();
+        }
         ctx->stats.scanned_candidates += count;
         scan_batch(ctx, count, pruning);
       }
@@ -651,6 +671,7 @@ void collect_search_stats(tsdd_cuda_ctx* ctx) {
   ctx->stats.scan_kernel_terms = c.tile_terms;
   ctx->stats.tiles = c.tiles;
   ctx->stats.tile_live_candidates = c.tile_live;
+  ctx->stats.lb_skipped = c.lb_skipped;
   double total = 0.0;
   for (size_t e = 0; e + 1 < ctx->events_used; e += 2) {
     float ms = 0.f;
@@ -673,6 +694,8 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   const uint64_t prep_launches = ctx->stats.kernel_launches;
   (void)prep_launches;
   ctx->stats.batches = 0;
+  ctx->lb_active = true;
+  ctx->lb_decided = false;
   ctx->stats.scanned_candidates = 0;
   ctx->stats.scan_kernel_launches = 0;
   ctx->events_used = 0;
@@ -924,6 +947,8 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
       ctx->opt_kernel = static_cast<int>(value);
     } else if (key == "wide_tile") {
       ctx->opt_wide_tile = value != 0;
+    } else if (key == "lower_bound") {
+      ctx->opt_lower_bound = value != 0;
     } else if (key == "share_bounds") {
       ctx->opt_share_bounds = value != 0;
     } else if (key == "time_kernels") {

@@ -13,6 +13,8 @@
 
 namespace tsdd_b200 {
 
+constexpr int kLbSegments = 16;    // segment means per row for the lower-bound tile filter
+constexpr uint32_t kLbBoxRows = 16; // rows per bounding box of segment means
 constexpr int kTileRows = 128;     // candidates per tile == neighbours per tile
 #ifndef TSDD_SCAN_CHUNK
 #define TSDD_SCAN_CHUNK 64
@@ -35,6 +37,11 @@ int launch_window_encode(const double* d_series, uint32_t rows, uint32_t n, uint
 // float32 z-normalised matrix, rows x stride, padding columns zero.
 int launch_build_rows(const double* d_series, const double* d_mean, const double* d_inv_sigma,
                       uint32_t rows, uint32_t n, uint32_t stride, float* d_rows, cudaStream_t stream);
+
+// Segment means of every matrix row [rows x kLbSegments] and their per-kLbBoxRows-rows
+// bounding boxes [ceil(rows / kLbBoxRows) x 2 x kLbSegments] (min then max).
+int launch_lower_bound_summaries(const float* d_rows, uint32_t rows, uint32_t stride, float* d_means,
+                                 float* d_boxes, cudaStream_t stream);
 
 // Stable LSD radix sort of (key, value) pairs on bits [0, key_bits).  Result is
 // left in (*keys, *vals); the alt buffers are scratch.  `hist` needs
@@ -75,6 +82,9 @@ struct SearchState {
   uint64_t* best;           // 1 best key
   DeviceCounters* counters;
   float margin;             // 1 + delta of the discard test (common.cuh: dead_bound)
+  const float* lb_means;    // N x kLbSegments segment means, or nullptr: no tile filter
+  const float* lb_boxes;    // their bounding boxes per kLbBoxRows rows
+  float lb_scale;           // columns per segment (stride / kLbSegments)
 };
 
 int launch_reset_search(SearchState s, cudaStream_t stream);

@@ -144,6 +144,59 @@ k_build_rows(const double* __restrict__ x, const double* __restrict__ mean,
   }
 }
 
+// ------------------------------------------------------------------ lower-bound summaries
+// For the covering scan's tile filter (search_kernels.cu): kLbSegments segment means of
+// every float32 matrix row (over the padded stride, so every segment has stride / 16
+// columns), and, per kLbBoxRows consecutive rows, the per-segment minimum and maximum.
+// For two rows a, b:  sum_t (a_t - b_t)^2  >=  (stride / 16) * sum_k (A_k - B_k)^2
+// (Cauchy-Schwarz per segment), and replacing B_k by the nearest point of a box
+// [lo_k, hi_k] that contains it can only lower the right-hand side further.
+__global__ void __launch_bounds__(256)
+k_row_segment_means(const float* __restrict__ rows, uint32_t n_rows, uint32_t stride, float* __restrict__ means) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= n_rows) return;
+  const uint32_t seg_cols = stride / kLbSegments;  // a multiple of 4: stride is a multiple of 64
+  const float4* p = reinterpret_cast<const float4*>(rows + static_cast<size_t>(row) * stride);
+  float acc[kLbSegments];
+#pragma unroll
+  for (int k = 0; k < kLbSegments; ++k) acc[k] = 0.f;
+  for (uint32_t q = lane; q < stride / 4; q += 32) {
+    const float4 v = __ldg(p + q);
+    const float sum = (v.x + v.y) + (v.z + v.w);
+    const uint32_t k = (4 * q) / seg_cols;
+#pragma unroll
+    for (int kk = 0; kk < kLbSegments; ++kk) acc[kk] += (static_cast<uint32_t>(kk) == k) ? sum : 0.f;
+  }
+#pragma unroll
+  for (int k = 0; k < kLbSegments; ++k) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) acc[k] += __shfl_xor_sync(0xFFFFFFFFu, acc[k], d);
+  }
+  if (lane < kLbSegments) {
+    float mine = 0.f;
+#pragma unroll
+    for (int k = 0; k < kLbSegments; ++k) mine = (lane == static_cast<uint32_t>(k)) ? acc[k] : mine;
+    means[static_cast<size_t>(row) * kLbSegments + lane] = mine / static_cast<float>(seg_cols);
+  }
+}
+
+// boxes[unit][0..15] = min, boxes[unit][16..31] = max over the unit's rows; one thread per (unit, segment)
+__global__ void k_segment_boxes(const float* __restrict__ means, uint32_t n_rows, float* __restrict__ boxes) {
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t unit = idx / kLbSegments, k = idx % kLbSegments;
+  const uint32_t units = (n_rows + kLbBoxRows - 1) / kLbBoxRows;
+  if (unit >= units) return;
+  float lo = 3.0e38f, hi = -3.0e38f;
+  for (uint32_t r = unit * kLbBoxRows; r < min(n_rows, (unit + 1) * kLbBoxRows); ++r) {
+    const float v = means[static_cast<size_t>(r) * kLbSegments + k];
+    lo = fminf(lo, v);
+    hi = fmaxf(hi, v);
+  }
+  boxes[static_cast<size_t>(unit) * 2 * kLbSegments + k] = lo;
+  boxes[static_cast<size_t>(unit) * 2 * kLbSegments + kLbSegments + k] = hi;
+}
+
 // ------------------------------------------------------------------ scan
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
@@ -360,6 +413,15 @@ int launch_build_rows(const double* d_series, const double* d_mean, const double
   dim3 grid(blocks_for(rows, kBuildRows), blocks_for(stride, kBuildCols));
   k_build_rows<<<grid, kBuildThreads, 0, stream>>>(d_series, d_mean, d_inv_sigma, rows, n, stride, d_rows);
   return 1;
+}
+
+int launch_lower_bound_summaries(const float* d_rows, uint32_t rows, uint32_t stride, float* d_means,
+                                 float* d_boxes, cudaStream_t stream) {
+  k_row_segment_means<<<blocks_for(static_cast<size_t>(rows) * 32, 256), 256, 0, stream>>>(d_rows, rows, stride,
+                                                                                          d_means);
+  const size_t cells = static_cast<size_t>((rows + kLbBoxRows - 1) / kLbBoxRows) * kLbSegments;
+  k_segment_boxes<<<blocks_for(cells, 256), 256, 0, stream>>>(d_means, rows, d_boxes);
+  return 2;
 }
 
 size_t scan_scratch_words(uint32_t count) {

@@ -16,6 +16,8 @@
 
 #include "kernels.hpp"
 
+#include <type_traits>
+
 
 namespace tsdd_b200 {
 
@@ -42,7 +44,7 @@ __global__ void k_reset_search(SearchState s) {
   }
   if (i == 0) {
     *s.best = 0;
-    *s.counters = DeviceCounters{0, 0, 0, 0, 0, 0, 0};
+    *s.counters = DeviceCounters{0, 0, 0, 0, 0, 0, 0, 0};
   }
 }
 
@@ -323,7 +325,10 @@ __device__ __forceinline__ void issue_stage(unsigned char* stage, const float* a
   for (int q = 0; q < kCand * kPieces / kScanThreads; ++q) {  // candidate rows
     const uint32_t piece = threadIdx.x + q * kScanThreads;
     const uint32_t r = piece / kPieces, kc = piece % kPieces;
-    cp_async16(stage + r * kRowBytes + ((kc ^ (r & 7)) << 4), a_tile + static_cast<size_t>(r) * stride + col0 + kc * 4);
+    // candidate rows are swizzled by (r >> 3): a thread's 8 rows 8 ty .. 8 ty + 7 then share one
+    // slot pattern, and the two thread rows of a warp (ty, ty + 1) get different ones
+    cp_async16(stage + r * kRowBytes + ((kc ^ ((r >> 3) & 7)) << 4),
+               a_tile + static_cast<size_t>(r) * stride + col0 + kc * 4);
   }
 #pragma unroll
   for (int q = 0; q < kNbr * kPieces / kScanThreads; ++q) {  // neighbour rows
@@ -410,7 +415,8 @@ struct ScanArgs {
 //   kTy 16, kW 8: 128 x 128  255 registers, one CTA per SM ("wide_tile", measured 7 % slower).
 // Tile numbers k (ScanArgs) always count 128 neighbour rows; a shape with 64-row
 // neighbour tiles walks the two halves of each.
-template <bool kPacked, bool kSymmetric, int kTy, int kW>
+// kLb compiles the lower-bound tile filter in; the plain variant carries none of its code.
+template <bool kPacked, bool kSymmetric, int kTy, int kW, bool kLb>
 __global__ void __launch_bounds__(kScanThreads, kW == 4 ? 2 : 1)
 k_scan_tiles(SearchState s, ScanArgs a) {
   constexpr int kU = 8;
@@ -421,6 +427,11 @@ k_scan_tiles(SearchState s, ScanArgs a) {
   constexpr int kCandBytes = kCand * kRowBytes;
   constexpr int kStageBytes = (kCand + kNbr) * kRowBytes;
   static_assert(kCand <= kTileRows && kNbr <= kTileRows && kTileRows % kNbr == 0, "tile shape");
+  // Candidate row (inside the tile) of pair-row u of thread row ty: 8 ty + u.  A warp holds
+  // one ty (kTy = 8) or two (kTy = 16), so its candidates are CONTIGUOUS rows of the
+  // word-sorted batch (16 w .. 16 w + 15 for warp w): a warp's candidates want, and abandon,
+  // the same neighbour tiles.
+  auto cand_of = [](uint32_t ty_, int u) -> uint32_t { return ty_ * kU + u; };
   extern __shared__ __align__(1024) unsigned char smem[];
   float* s_thr = reinterpret_cast<float*>(smem + kStages * kStageBytes);  // candidate thresholds
   uint32_t* s_cand = reinterpret_cast<uint32_t*>(s_thr + kTileRows);      // candidate rows
@@ -428,7 +439,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
   uint32_t* s_jrow = reinterpret_cast<uint32_t*>(s_nub + kTileRows);      // neighbour rows, ~0 = none
   uint32_t* s_brow = s_jrow + kTileRows;                                  // rows to load (none -> zero row)
   float* s_loc = reinterpret_cast<float*>(s_brow + kTileRows);            // bounds this CTA found itself
-  __shared__ unsigned long long s_calls, s_abandoned, s_terms, s_tiles, s_tile_live;
+  __shared__ unsigned long long s_calls, s_abandoned, s_terms, s_tiles, s_tile_live, s_lb_skipped;
 
   const uint32_t count = a.sel[0];
   const uint32_t cand0 = blockIdx.y * kCand;
@@ -443,6 +454,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
     s_terms = 0;
     s_tiles = 0;
     s_tile_live = 0;
+    s_lb_skipped = 0;
   }
   const bool window = a.nbr_index != nullptr;
   const uint32_t slot_tiles = (s.n_rows + kTileRows - 1) / kTileRows;
@@ -518,6 +530,50 @@ k_scan_tiles(SearchState s, ScanArgs a) {
     }
     const int n_live = __syncthreads_count(live);
     if (n_live == 0) break;  // every candidate of this tile is dead: nothing left to do
+    // ---- lower-bound filter (covering scan only): a candidate whose segment means lie
+    // further from every 16-row box of this tile than its threshold cannot find a
+    // neighbour below it here; it sits this tile out (threshold -1 for this tile).
+    if (kLb && !window && a.pruning && s.lb_means != nullptr) {
+      bool needed = live;
+      if (live && slot0 < s.n_rows) {
+        const uint32_t row = s_cand[tid];
+        const float limit = s_thr[tid] * 1.001f;  // rounding slack of the float32 means
+        float mine[kLbSegments];
+        const float4* pm = reinterpret_cast<const float4*>(s.lb_means + static_cast<size_t>(row) * kLbSegments);
+#pragma unroll
+        for (int q = 0; q < kLbSegments / 4; ++q) {
+          const float4 v = __ldg(pm + q);
+          mine[4 * q] = v.x, mine[4 * q + 1] = v.y, mine[4 * q + 2] = v.z, mine[4 * q + 3] = v.w;
+        }
+        const uint32_t first_unit = slot0 / kLbBoxRows;
+        const uint32_t last_unit = (min(slot0 + kNbr, s.n_rows) - 1) / kLbBoxRows;
+        needed = false;
+        for (uint32_t unit = first_unit; unit <= last_unit && !needed; ++unit) {
+          const float4* pb = reinterpret_cast<const float4*>(s.lb_boxes + static_cast<size_t>(unit) * 2 * kLbSegments);
+          float lb = 0.f;
+#pragma unroll
+          for (int q = 0; q < kLbSegments / 4; ++q) {
+            const float4 lo = __ldg(pb + q), hi = __ldg(pb + kLbSegments / 4 + q);
+            float g;
+            g = fmaxf(fmaxf(lo.x - mine[4 * q], mine[4 * q] - hi.x), 0.f), lb = fmaf(g, g, lb);
+            g = fmaxf(fmaxf(lo.y - mine[4 * q + 1], mine[4 * q + 1] - hi.y), 0.f), lb = fmaf(g, g, lb);
+            g = fmaxf(fmaxf(lo.z - mine[4 * q + 2], mine[4 * q + 2] - hi.z), 0.f), lb = fmaf(g, g, lb);
+            g = fmaxf(fmaxf(lo.w - mine[4 * q + 3], mine[4 * q + 3] - hi.w), 0.f), lb = fmaf(g, g, lb);
+          }
+          needed = !(lb * s.lb_scale > limit);
+        }
+        if (!needed) {
+          s_thr[tid] = -1.f;
+          live = false;
+        }
+      }
+      const int n_needed = __syncthreads_count(needed);  // also publishes the lowered thresholds
+      if (tid == 0) s_lb_skipped += static_cast<unsigned long long>(n_live - n_needed);
+      if (n_needed == 0) {  // nobody needs this tile: no loads, no arithmetic
+        if (tt + 1 < a.tiles_per_cta && k + 1 < h_end) prefetch(k + 1);
+        continue;
+      }
+    }
     if (tid == 0) {
       s_tiles += 1;
       s_tile_live += n_live;
@@ -549,7 +605,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
 
     float thr[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) thr[u] = s_thr[ty + kTy * u];
+    for (int u = 0; u < kU; ++u) thr[u] = s_thr[cand_of(ty, u)];
 
     Acc<kPacked, kU, kW> acc;
     acc.zero();
@@ -561,7 +617,12 @@ k_scan_tiles(SearchState s, ScanArgs a) {
       cp_async_commit();
     }
 
-    bool mine_abandoned = false, warp_done = false, cta_abandoned = false;
+    // a thread none of whose candidates takes part in this tile (dead, or ruled out by the
+    // lower bound) has abandoned before it starts; so has a warp of such threads
+    bool mine_abandoned = true;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) mine_abandoned = mine_abandoned && thr[u] < 0.f;
+    bool warp_done = __all_sync(0xFFFFFFFFu, mine_abandoned), cta_abandoned = false;
     uint32_t warp_chunks = 0;
     for (uint32_t c = 0; c < chunks; ++c) {
       cp_async_wait<kStages - 2>();
@@ -574,7 +635,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
                           s.stride, (c + kStages - 1) * kChunk);
       cp_async_commit();
       if (!warp_done) {
-        const unsigned char* a_s = smem + (c % kStages) * kStageBytes + ty * kRowBytes;
+        const unsigned char* a_s = smem + (c % kStages) * kStageBytes + cand_of(ty, 0) * kRowBytes;
         const unsigned char* b_s = smem + (c % kStages) * kStageBytes + kCandBytes + tx * kRowBytes;  // rows tx + kTx*w
 #pragma unroll 2
         for (int kc = 0; kc < kPieces; ++kc) {
@@ -582,7 +643,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
           if constexpr (kW == 8) {
             float4 na[kU];
 #pragma unroll
-            for (int u = 0; u < kU; ++u) na[u] = *reinterpret_cast<const float4*>(a_s + u * (kTy * kRowBytes) + off_a);
+            for (int u = 0; u < kU; ++u) na[u] = *reinterpret_cast<const float4*>(a_s + u * kRowBytes + off_a);
 #pragma unroll
             for (int w = 0; w < kW; ++w) {
               const float4 b = *reinterpret_cast<const float4*>(b_s + w * (kTx * kRowBytes) + off_b);
@@ -597,7 +658,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
             for (int w = 0; w < kW; ++w) b[w] = *reinterpret_cast<const float4*>(b_s + w * (kTx * kRowBytes) + off_b);
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
-              const float4 na = *reinterpret_cast<const float4*>(a_s + u * (kTy * kRowBytes) + off_a);
+              const float4 na = *reinterpret_cast<const float4*>(a_s + u * kRowBytes + off_a);
 #pragma unroll
               for (int w = 0; w < kW; ++w) acc.add(u, w, na, b[w]);
             }
@@ -644,7 +705,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
     for (int w = 0; w < kW; ++w) jrow[w] = s_jrow[tx + kTx * w];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const uint32_t row = s_cand[ty + kTy * u];
+      const uint32_t row = s_cand[cand_of(ty, u)];
       uint32_t d_min = 0xFFFFFFFFu, j_min = 0xFFFFFFFFu;  // this thread's best (distance bits, neighbour)
 #pragma unroll
       for (int w = 0; w < kW; ++w) {
@@ -670,7 +731,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
       for (int d = kTx / 2; d > 0; d >>= 1) g_j = min(g_j, __shfl_xor_sync(0xFFFFFFFFu, g_j, d));
       if (tx == 0 && g_j != 0xFFFFFFFFu) {
         atomicMin(as_ull(s.nn + row), static_cast<unsigned long long>(nn_key(g_min, g_j)));
-        s_loc[ty + kTy * u] = fminf(s_loc[ty + kTy * u], __uint_as_float(g_min));
+        s_loc[cand_of(ty, u)] = fminf(s_loc[cand_of(ty, u)], __uint_as_float(g_min));
       }
     }
   }
@@ -687,6 +748,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
       atomicAdd(&s.counters->tiles, s_tiles);
       atomicAdd(&s.counters->tile_live, s_tile_live);
     }
+    if (s_lb_skipped) atomicAdd(&s.counters->lb_skipped, s_lb_skipped);
   }
 }
 
@@ -1206,6 +1268,7 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
                       const uint32_t* d_nbr_index, uint32_t k_begin, uint32_t k_end, uint32_t rotation,
                       bool pruning, bool symmetric, cudaStream_t stream) {
   if (k_end <= k_begin || live_upper_bound == 0) return 0;
+  const bool lb = pruning && d_nbr_index == nullptr && s.lb_means != nullptr && g_scan_variant != 2;
   // tile shape: 64-candidate tiles once the batch has shrunk to that, else 128
   const bool narrow = !g_wide_tile && g_scan_variant != 2 && live_upper_bound <= 64;
   const uint32_t cand_rows = narrow ? 64 : 128;
@@ -1235,20 +1298,23 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     kernel<<<grid, kScanThreads, smem, stream>>>(s, a);
   };
-  const int shape = (g_packed_default ? 8 : 0) | (symmetric ? 4 : 0) | (g_wide_tile ? 2 : narrow ? 1 : 0);
-  switch (shape) {
-    case 14: launch(k_scan_tiles<true, true, 16, 8>); break;
-    case 13: launch(k_scan_tiles<true, true, 8, 4>); break;
-    case 12: launch(k_scan_tiles<true, true, 16, 4>); break;
-    case 10: launch(k_scan_tiles<true, false, 16, 8>); break;
-    case 9: launch(k_scan_tiles<true, false, 8, 4>); break;
-    case 8: launch(k_scan_tiles<true, false, 16, 4>); break;
-    case 6: launch(k_scan_tiles<false, true, 16, 8>); break;
-    case 5: launch(k_scan_tiles<false, true, 8, 4>); break;
-    case 4: launch(k_scan_tiles<false, true, 16, 4>); break;
-    case 2: launch(k_scan_tiles<false, false, 16, 8>); break;
-    case 1: launch(k_scan_tiles<false, false, 8, 4>); break;
-    default: launch(k_scan_tiles<false, false, 16, 4>); break;
+  const int shape = (g_wide_tile ? 2 : narrow ? 1 : 0);
+  auto pick = [&](auto packed, auto sym, auto with_lb) {
+    constexpr bool kP = decltype(packed)::value, kS = decltype(sym)::value, kL = decltype(with_lb)::value;
+    if (shape == 2) launch(k_scan_tiles<kP, kS, 16, 8, kL>);
+    else if (shape == 1) launch(k_scan_tiles<kP, kS, 8, 4, kL>);
+    else launch(k_scan_tiles<kP, kS, 16, 4, kL>);
+  };
+  auto pick_lb = [&](auto packed, auto sym) {
+    if (lb) pick(packed, sym, std::true_type{});
+    else pick(packed, sym, std::false_type{});
+  };
+  if (g_packed_default) {
+    if (symmetric) pick_lb(std::true_type{}, std::true_type{});
+    else pick_lb(std::true_type{}, std::false_type{});
+  } else {
+    if (symmetric) pick_lb(std::false_type{}, std::true_type{});
+    else pick_lb(std::false_type{}, std::false_type{});
   }
   return 1;
 }
