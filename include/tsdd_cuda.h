@@ -59,7 +59,7 @@ typedef struct tsdd_cuda_stats {
   uint64_t scan_kernel_terms; /* terms accumulated by the tiled distance kernel only */
   double encode_ms;        /* preparation: window statistics + PAA/SAX/hash kernel */
   double build_rows_ms;    /* preparation: float32 matrix build (HBM write-bound) */
-  double index_ms;         /* preparation: radix sorts, run-length histogram, rarity order */
+  double index_ms;         /* preparation: lower-bound summaries, radix sorts, run-length histogram, rarity order */
   uint64_t tiles;          /* candidate-tile x neighbour-tile pairs the tile kernel started */
   uint64_t tile_live_candidates; /* live candidates summed over them (128 per tile = dense tiles) */
   uint64_t lb_skipped;     /* (candidate, neighbour tile) pairs ruled out by the lower-bound filter */

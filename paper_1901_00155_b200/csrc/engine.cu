@@ -128,7 +128,7 @@ struct tsdd_cuda_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
-  cudaEvent_t ev_prep[4] = {nullptr, nullptr, nullptr, nullptr};  // encode | build rows | index | end
+  cudaEvent_t ev_prep[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // encode | build rows | summaries+index | end
   std::string error;
 
   // tunables (tsdd_cuda_set_option)
@@ -304,9 +304,9 @@ void prepare_on_device(tsdd_cuda_ctx* ctx, size_t m, size_t n, size_t word_len, 
 
   ctx->lb_means.alloc(static_cast<size_t>(rows) * kLbSegments);
   ctx->lb_boxes.alloc(static_cast<size_t>((rows + kLbBoxRows - 1) / kLbBoxRows) * 2 * kLbSegments);
+  CUDA_OK(cudaEventRecord(ctx->ev_prep[2], st));
   launches += launch_lower_bound_summaries(ctx->matrix.ptr, rows, ctx->stride, ctx->lb_means.ptr,
                                            ctx->lb_boxes.ptr, st);
-  CUDA_OK(cudaEventRecord(ctx->ev_prep[2], st));
   // bucket index: stable sort of (hash, row) -> runs are the buckets
   const size_t longest_scan = std::max<size_t>(rows, radix_sort_scratch_words(rows));
   ctx->scan_scratch.alloc(scan_scratch_words(static_cast<uint32_t>(longest_scan)) + 1024);
