@@ -285,10 +285,23 @@ void prepare_on_device(tsdd_cuda_ctx* ctx, size_t m, size_t n, size_t word_len, 
   ctx->rows_padded = round_up_u32(rows + 1, kTileRows);  // at least one all-zero row after the last
   uint64_t launches = 0;
 
+  const size_t matrix_floats = static_cast<size_t>(ctx->rows_padded) * ctx->stride;
+  {
+    // The float32 matrix dominates the footprint; fail with a clear message instead of a
+    // bare cudaMalloc error when the series does not fit this GPU (no CPU fallback).
+    size_t free_bytes = 0, total_bytes = 0;
+    CUDA_OK(cudaMemGetInfo(&free_bytes, &total_bytes));
+    const size_t held = ctx->matrix.count * sizeof(float);  // reused when large enough
+    const size_t need = matrix_floats * sizeof(float) + static_cast<size_t>(rows) * 160 + (512u << 20);
+    if (need > free_bytes + held)
+      fail(TSDD_ERR_RUNTIME, "the subsequence matrix needs " + std::to_string(need >> 20) + " MiB of device memory (N=" +
+                                 std::to_string(rows) + " rows x " + std::to_string(ctx->stride) + " floats), " +
+                                 std::to_string((free_bytes + held) >> 20) + " MiB are free on device " +
+                                 std::to_string(ctx->device));
+  }
   ctx->mean.alloc(rows);
   ctx->inv_sigma.alloc(rows);
   ctx->hash0.alloc(rows);
-  const size_t matrix_floats = static_cast<size_t>(ctx->rows_padded) * ctx->stride;
   ctx->matrix.alloc(matrix_floats);
   CUDA_OK(cudaEventRecord(ctx->ev_prep[0], st));
   launches += launch_window_encode(ctx->series.ptr, rows, static_cast<uint32_t>(n),
