@@ -197,7 +197,8 @@ def run_cuda_arm(args) -> None:
         device_step()
     barrier()
     sampler = ClockSampler(local)
-    totals = {"calls": 0, "terms": 0, "scan_terms": 0, "scan_ms": 0.0, "scan_launches": 0, "launches": 0,
+    totals = {"calls": 0, "terms": 0, "scan_terms": 0, "scan_ms": 0.0, "scan_launches": 0, "ws_launches": 0,
+              "launches": 0,
               "prep_ms": 0.0, "search_ms": 0.0, "build_rows_ms": 0.0, "encode_ms": 0.0, "index_ms": 0.0}
     with sampler:
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -209,6 +210,7 @@ def run_cuda_arm(args) -> None:
             totals["scan_terms"] += st["scan_kernel_terms"]
             totals["scan_ms"] += st["scan_kernel_ms"]
             totals["scan_launches"] += st["scan_kernel_launches"]
+            totals["ws_launches"] += st["scan_kernel_ws_launches"]
             totals["launches"] += st["kernel_launches"]
             for key in ("prep_ms", "search_ms", "build_rows_ms", "encode_ms", "index_ms"):
                 totals[key] += st[key]
@@ -273,7 +275,10 @@ def run_cuda_arm(args) -> None:
             "e2e": {"value": all_e2e_calls / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(x.nbytes),
                     "d2h_bytes_per_step": int(k * 16 + 160), "topk_time_s": e2e_s / args.steps},
             "gpu_launches": int(totals["launches"]),
-            "roofline": {"bound": "fp32", "kernel": "k_scan_tiles", "achieved": achieved, "peak": peak,
+            "roofline": {"bound": "fp32",
+                         "kernel": "k_scan_tiles_ws + k_scan_tiles (the tile kernels: %d of %d launches warp-specialised)"
+                                   % (totals["ws_launches"], totals["scan_launches"]),
+                         "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
                          "peak_source": "live FFMA-only probe kernel x 2 FLOP (MEASURED_PEAKS.json has no FP32 "
                                         "entry; B200_PROFILING.md states no FP32 fallback)",

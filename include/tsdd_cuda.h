@@ -63,6 +63,7 @@ typedef struct tsdd_cuda_stats {
   uint64_t tiles;          /* candidate-tile x neighbour-tile pairs the tile kernel started */
   uint64_t tile_live_candidates; /* live candidates summed over them (128 per tile = dense tiles) */
   uint64_t lb_skipped;     /* (candidate, neighbour tile) pairs ruled out by the lower-bound filter */
+  uint64_t scan_kernel_ws_launches; /* of scan_kernel_launches, those of the warp-specialised kernel */
 } tsdd_cuda_stats;
 
 /* ---- lifetime ------------------------------------------------------------ */
@@ -93,8 +94,8 @@ int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream);
  * "margin_delta" (safety band of the float32 discard test; negative = from n), "symmetric" (0/1: completed tiles
  * also lower the neighbours' bounds), "packed" (0/1: f32x2 arithmetic),
  * "wide_tile" (0/1: 128 x 128 tiles, one CTA per SM, instead of 128 x 64, two),
- * "kernel" (1: cp.async tile kernel; 2: the warp-specialised cp.async.bulk +
- * mbarrier variant, experimental and currently slower), "rotate" (0/1), "share_bounds" (0/1), "lower_bound" (0/1: in the covering scan a
+ * "kernel" (0: per launch; 1: the cp.async tile kernel everywhere; 2: the
+ * warp-specialised cp.async.bulk + mbarrier kernel everywhere), "rotate" (0/1), "share_bounds" (0/1), "lower_bound" (0/1: in the covering scan a
  * candidate skips a neighbour tile whose segment-mean boxes are provably
  * further away than its threshold),
  * "time_kernels" (0/1: CUDA events around every tile-kernel launch).

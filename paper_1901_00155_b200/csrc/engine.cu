@@ -148,7 +148,7 @@ struct tsdd_cuda_ctx {
   bool opt_symmetric = true;
   bool opt_packed = true;
   bool opt_wide_tile = false;
-  int opt_kernel = 1;
+  int opt_kernel = 0;
   bool opt_time_kernels = true;
   bool opt_share_bounds = true;
   bool opt_lower_bound = true;      // tile filter by segment-mean lower bounds in the covering scan     // several ranks: min-reduce the nn bounds after every batch
@@ -615,6 +615,7 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
     if (ctx->opt_time_kernels) CUDA_OK(cudaEventRecord(e1, st));
     launches += launched;
     ctx->stats.scan_kernel_launches += launched;
+    if (launched && scan_last_launch_was_ws()) ctx->stats.scan_kernel_ws_launches += launched;
   }
   launches += launch_finalize_batch(s, list, ctx->sel.ptr, ctx->batch_capacity, pruning, st);
   ctx->stats.kernel_launches += launches;
@@ -711,6 +712,7 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   ctx->lb_decided = false;
   ctx->stats.scanned_candidates = 0;
   ctx->stats.scan_kernel_launches = 0;
+  ctx->stats.scan_kernel_ws_launches = 0;
   ctx->events_used = 0;
 
   CUDA_OK(cudaEventRecord(ctx->ev_a, st));
@@ -956,7 +958,7 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
     } else if (key == "packed") {
       ctx->opt_packed = value != 0;
     } else if (key == "kernel") {
-      if (value != 1 && value != 2) fail(TSDD_ERR_PARAMETER, "kernel must be 1 or 2");
+      if (value != 0 && value != 1 && value != 2) fail(TSDD_ERR_PARAMETER, "kernel must be 0, 1 or 2");
       ctx->opt_kernel = static_cast<int>(value);
     } else if (key == "wide_tile") {
       ctx->opt_wide_tile = value != 0;

@@ -129,6 +129,9 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
                       const uint32_t* d_nbr_index, uint32_t k_begin, uint32_t k_end, uint32_t rotation,
                       bool pruning, bool symmetric, cudaStream_t stream);
 
+// Whether the last launch_scan_tiles picked the warp-specialised kernel.
+bool scan_last_launch_was_ws();
+
 // Survivors of a complete scan are exact; each raises the best-so-far.
 int launch_finalize_batch(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,
                           uint32_t capacity, bool pruning, cudaStream_t stream);

@@ -754,37 +754,35 @@ k_scan_tiles(SearchState s, ScanArgs a) {
 
 // ------------------------------------------------------------------ warp-specialised tile kernel
 //
-// Same tiles, same arithmetic, different plumbing.  CTA = 8 consumer warps (the
-// 16 x 16 thread grid above, 8 x 4 pairs per thread) + 1 producer warp; two CTAs
-// per SM.  The producer streams 64-column stages — one 256-byte cp.async.bulk per
-// row (UBLKCP), completing on an mbarrier — through a 2-stage ring that runs
-// ACROSS tile boundaries, so the first stage of the next tile lands while the
-// consumers are still in the last chunk and epilogue of the current one.  It also
-// prepares each tile's thresholds / neighbour rows one tile ahead (two metadata
-// slots).  Consumers never meet in a CTA-wide barrier: each warp waits for a stage
-// (full mbarrier), reads the stage's tag (tile, chunk), computes, and releases the
-// stage (empty mbarrier).  A tile is abandoned when all 8 warps have voted
-// (shared counter); the producer then stops feeding it and moves on.  Rows sit in
-// shared memory at a 272-byte pitch (256 + 16), which makes the LDS.128 of the
-// 8 rows of a quarter-warp conflict-free without a swizzle.
+// Same arithmetic as k_scan_tiles on a 128 x 128 tile (8 x 8 pairs per thread), different
+// plumbing.  CTA = two consumer warpgroups (8 warps, the 16 x 16 thread grid) + one producer
+// warpgroup (one active warp); one CTA per SM, launched at 168 registers per thread and
+// rebalanced with setmaxnreg: 232 per consumer thread, 40 per producer thread
+// (256 x 232 + 128 x 40 = 64,512 = 384 x 168).  The producer streams 64-column stages — one
+// 256-byte cp.async.bulk per row (UBLKCP), completing on an mbarrier — through a 3-stage
+// ring that runs ACROSS tile boundaries, so the first stages of the next tile land while the
+// consumers are still in the last chunk and epilogue of the current one.  It also prepares
+// each tile's thresholds / neighbour rows one tile ahead (two metadata slots).  Consumers
+// never meet in a CTA-wide barrier: each warp waits for a stage (full mbarrier), reads the
+// stage's tag (tile, chunk), computes, and releases the stage (empty mbarrier).  A tile is
+// abandoned when all 8 warps have voted (shared counter); the producer then stops feeding
+// it and moves on.  Rows sit in shared memory at a 272-byte pitch (256 + 16), which makes
+// the LDS.128 of the 8 rows of a quarter-warp conflict-free without a swizzle.
 //
-// Status (round 1): results identical to k_scan_tiles on every test, but SLOWER
-// (cfg 5: 1.01e13 vs 1.33e13 terms/s).  ncu shows why: registers are allocated per
-// 4 warps, so the 9-warp CTA is charged for 12 and only ONE CTA fits an SM
-// (launch__occupancy_limit_registers = 1); with 2 consumer warps per scheduler the
-// LDS latency at the top of every 4-column step is exposed.  The copies themselves
-// keep up (consumers wait on a full barrier for ~5 % of their time).  Kept behind
-// the "kernel"=2 option as the starting point for a variant whose producer duty
-// fits an 8-warp CTA.
+// No lower-bound filter here: the producer shares a scheduler with two consumer warps, and
+// every instruction it issues is taken from them and, through the stage barriers, from every
+// warp (a producer that also ran the filter cost 9 % on cfg 5).  The launcher therefore uses
+// this kernel where the filter has nothing to offer — window rounds, and covering scans of
+// searches on which it has been switched off — and k_scan_tiles elsewhere.
 namespace ws {
 
-constexpr int kStagesWs = 2;
-constexpr int kNbrWs = 64;
+constexpr int kStagesWs = 3;
+constexpr int kNbrWs = 128;
 constexpr int kPitch = kChunk * 4 + 16;
 constexpr int kRowsPerStage = kTileRows + kNbrWs;
 constexpr int kStageBytesWs = kRowsPerStage * kPitch;
 constexpr int kConsumerWarps = 8;
-constexpr int kThreadsWs = (kConsumerWarps + 1) * 32;
+constexpr int kThreadsWs = (kConsumerWarps + 4) * 32;  // + one producer warpgroup
 constexpr uint32_t kTagDone = 0xFFFFFFFFu;
 
 struct TileMeta {
@@ -802,8 +800,8 @@ struct SharedWs {
   TileMeta meta[2];
   uint32_t cand[kTileRows];
   float loc[kTileRows];
-  uint32_t tag_tile[kStagesWs];
-  uint32_t tag_chunk[kStagesWs];
+  uint32_t tag_tile[kStagesWs + 1];
+  uint32_t tag_chunk[kStagesWs + 1];
   unsigned long long full[kStagesWs], empty[kStagesWs], meta_full[2], meta_empty[2];  // mbarriers
 };
 
@@ -836,11 +834,10 @@ __device__ __forceinline__ void bulk_copy_row(void* smem_dst, const void* gmem_s
                : "memory");
 }
 
-// 288 threads x 112 registers: two CTAs fit the 64 K registers of an SM.
 template <bool kSymmetric>
-__global__ void __maxnreg__(112)
+__global__ void __launch_bounds__(kThreadsWs, 1)
 k_scan_tiles_ws(SearchState s, ScanArgs a) {
-  constexpr int kU = 8, kW = 4, kTx = 16;
+  constexpr int kU = 8, kW = 8, kTx = 16;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   SharedWs& sh = *reinterpret_cast<SharedWs*>(smem_raw);
 
@@ -874,8 +871,10 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
   const uint32_t k_first = a.k_begin * kSub + blockIdx.x * a.tiles_per_cta, k_end = a.k_end * kSub;
   const uint32_t n_tiles = k_first < k_end ? min(static_cast<uint32_t>(a.tiles_per_cta), k_end - k_first) : 0u;
 
-  if (warp == kConsumerWarps) {
-    // ================================================================ producer warp
+  if (warp >= kConsumerWarps) {
+    // ================================================================ producer warpgroup
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    if (warp != kConsumerWarps) return;  // one warp does the work; the other three only round the CTA to 12 warps
     const uint32_t centre = window ? a.batch_slots[min(cand0 + kTileRows / 2, count - 1)] / kTileRows : 0u;
     const uint64_t best = a.pruning ? *s.best : 0ull;
     const float* a_tile = a.batch + static_cast<size_t>(cand0) * s.stride;
@@ -891,8 +890,8 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
       return unit * kTileRows + (h % kSub) * kNbrWs;
     };
     // bounds of the next tile, fetched while the current one streams
-    uint64_t cand_key[4], nbr_key[2];
-    uint32_t nbr_j[2];
+    uint64_t cand_key[4], nbr_key[4];
+    uint32_t nbr_j[4];
     auto fetch_bounds = [&](uint32_t k) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -901,7 +900,7 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
       }
       const uint32_t slot0 = slot0_of(k);
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
+      for (int q = 0; q < kNbrWs / 32; ++q) {
         const uint32_t slot = slot0 + lane + 32 * q;
         nbr_j[q] = 0xFFFFFFFFu;
         if (slot < s.n_rows) nbr_j[q] = window ? a.nbr_index[slot] : slot;
@@ -910,8 +909,10 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
     };
     if (n_tiles) fetch_bounds(k_first);
 
+    // The producer shares a scheduler with two consumer warps; it is kept lean (row pointers of
+    // the tile in registers, nothing recomputed per stage).
     uint32_t seq = 0;
-    unsigned long long calls_total = 0;
+    unsigned long long calls_total = 0, tiles_total = 0, live_total = 0;
 #pragma unroll 1
     for (uint32_t ti = 0; ti < n_tiles; ++ti) {
       const uint32_t k = k_first + ti, m = ti & 1, use = ti >> 1;
@@ -940,13 +941,14 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
         }
         meta.thr[r] = thr;
         any_live = any_live || live[q];
+        live_total += live[q] ? 1u : 0u;
       }
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const uint32_t t = lane + 32 * q, j = nbr_j[q];
-        meta.jrow[t] = j;
-        meta.brow[t] = j != 0xFFFFFFFFu ? j : s.n_rows;  // row n_rows is zero padding
-        meta.nub[t] = j != 0xFFFFFFFFu ? __uint_as_float(key_bits(nbr_key[q])) : -1.f;
+      for (int q = 0; q < kNbrWs / 32; ++q) {
+        const uint32_t e = lane + 32 * q, j = nbr_j[q];
+        meta.jrow[e] = j;
+        meta.brow[e] = j != 0xFFFFFFFFu ? j : s.n_rows;  // row n_rows is zero padding
+        meta.nub[e] = j != 0xFFFFFFFFu ? __uint_as_float(key_bits(nbr_key[q])) : -1.f;
       }
       any_live = __any_sync(0xFFFFFFFFu, any_live);
       __syncwarp();
@@ -984,12 +986,14 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
       if (lane == 0) mbar_arrive(&sh.meta_full[m]);
       if (!any_live) break;  // candidates only ever die: nothing is left for this CTA
       calls_total += calls;
+      tiles_total += 1;
 
-      const float* src[6];
+      const float* src[kRowsPerStage / 32];
 #pragma unroll
       for (int q = 0; q < 4; ++q) src[q] = a_tile + static_cast<size_t>(lane + 32 * q) * s.stride;
 #pragma unroll
-      for (int q = 0; q < 2; ++q) src[4 + q] = s.rows + static_cast<size_t>(meta.brow[lane + 32 * q]) * s.stride;
+      for (int q = 0; q < kNbrWs / 32; ++q)
+        src[4 + q] = s.rows + static_cast<size_t>(meta.brow[lane + 32 * q]) * s.stride;
       if (ti + 1 < n_tiles) fetch_bounds(k + 1);
 
       // ---- stream the tile's chunks; stop as soon as every consumer warp has abandoned it
@@ -1006,7 +1010,7 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
         __syncwarp();
         unsigned char* dst = sh.stages[st];
 #pragma unroll
-        for (int q = 0; q < 6; ++q)
+        for (int q = 0; q < kRowsPerStage / 32; ++q)
           bulk_copy_row(dst + (lane + 32 * q) * kPitch, src[q] + c * kChunk, kChunk * 4, &sh.full[st]);
         ++seq;
       }
@@ -1019,12 +1023,25 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
         mbar_arrive(&sh.full[st]);
       }
     }
-    if (lane == 0 && calls_total) atomicAdd(&s.counters->calls, calls_total);
+    if (lane == 0) {
+      if (calls_total) atomicAdd(&s.counters->calls, calls_total);
+      if (tiles_total) atomicAdd(&s.counters->tiles, tiles_total);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) live_total += __shfl_xor_sync(0xFFFFFFFFu, live_total, d);
+    if (lane == 0 && live_total) atomicAdd(&s.counters->tile_live, live_total);
     return;
   }
 
-  // ================================================================== consumer warps
+  // ================================================================== consumer warpgroups
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
   const uint32_t tx = tid % kTx, ty = tid / kTx;
+  // Candidate row of pair-row u of thread row ty: warp w (thread rows 2w, 2w + 1) owns the 16
+  // CONTIGUOUS rows 16w .. 16w + 15 of the word-sorted batch (they want, and abandon, the same
+  // tiles); the two rows a warp reads at once are adjacent, i.e. in different bank groups at
+  // the 272-byte pitch.
+  const uint32_t cand0_of_thread = (ty >> 1) * 16 + (ty & 1);  // + 2 u
+  constexpr uint32_t kCandStep = 2;
   Acc<true, kU, kW> acc;
   float thr[kU];
   uint32_t seq = 0, cur = kTagDone, m = 0, chunks_done = 0;
@@ -1046,26 +1063,32 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
       m = tile & 1;
       mbar_wait(&sh.meta_full[m], (tile >> 1) & 1);
 #pragma unroll
-      for (int u = 0; u < kU; ++u) thr[u] = sh.meta[m].thr[ty + 16 * u];
+      for (int u = 0; u < kU; ++u) thr[u] = sh.meta[m].thr[cand0_of_thread + kCandStep * u];
       acc.zero();
-      warp_done = false;
+      bool none = true;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) none = none && thr[u] < 0.f;
+      warp_done = __all_sync(0xFFFFFFFFu, none);  // none of this warp's candidates takes part in the tile
+      if (warp_done && lane == 0 && chunks > 1) {
+        if (atomicAdd(&sh.meta[m].done, 1u) == kConsumerWarps - 1) abandoned_total += sh.meta[m].calls;
+      }
       released = false;
       chunks_done = 0;
     }
     TileMeta& meta = sh.meta[m];
     if (!warp_done) {
-      const unsigned char* a_s = sh.stages[st] + ty * kPitch;
+      const unsigned char* a_s = sh.stages[st] + cand0_of_thread * kPitch;
       const unsigned char* b_s = sh.stages[st] + kTileRows * kPitch + tx * kPitch;
 #pragma unroll 2
       for (int kc = 0; kc < kPieces; ++kc) {
-        float4 b[kW];
+        float4 na[kU];
 #pragma unroll
-        for (int w = 0; w < kW; ++w) b[w] = *reinterpret_cast<const float4*>(b_s + w * (kTx * kPitch) + kc * 16);
+        for (int u = 0; u < kU; ++u) na[u] = *reinterpret_cast<const float4*>(a_s + u * (kCandStep * kPitch) + kc * 16);
 #pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const float4 na = *reinterpret_cast<const float4*>(a_s + u * (16 * kPitch) + kc * 16);
+        for (int w = 0; w < kW; ++w) {
+          const float4 b = *reinterpret_cast<const float4*>(b_s + w * (kTx * kPitch) + kc * 16);
 #pragma unroll
-          for (int w = 0; w < kW; ++w) acc.add(u, w, na, b[w]);
+          for (int u = 0; u < kU; ++u) acc.add(u, w, na[u], b);
         }
       }
       ++chunks_done;
@@ -1103,7 +1126,7 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
           for (int w = 0; w < kW; ++w) jrow[w] = meta.jrow[tx + kTx * w];
 #pragma unroll
           for (int u = 0; u < kU; ++u) {
-            const uint32_t row = sh.cand[ty + 16 * u];
+            const uint32_t row = sh.cand[cand0_of_thread + kCandStep * u];
             uint32_t d_min = 0xFFFFFFFFu, j_min = 0xFFFFFFFFu;
 #pragma unroll
             for (int w = 0; w < kW; ++w) {
@@ -1128,7 +1151,7 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
             for (int d = kTx / 2; d > 0; d >>= 1) g_j = min(g_j, __shfl_xor_sync(0xFFFFFFFFu, g_j, d));
             if (tx == 0 && g_j != 0xFFFFFFFFu) {
               atomicMin(as_ull(s.nn + row), static_cast<unsigned long long>(nn_key(g_min, g_j)));
-              sh.loc[ty + 16 * u] = fminf(sh.loc[ty + 16 * u], __uint_as_float(g_min));
+              sh.loc[cand0_of_thread + kCandStep * u] = fminf(sh.loc[cand0_of_thread + kCandStep * u], __uint_as_float(g_min));
             }
           }
         }
@@ -1203,7 +1226,8 @@ k_exact_nn(const double* __restrict__ x, const double* __restrict__ mean, const 
 }
 
 bool g_packed_default = true;
-int g_scan_variant = 1;  // 1: cp.async + CTA barriers (k_scan_tiles), 2: warp-specialised (k_scan_tiles_ws)
+bool g_last_launch_was_ws = false;
+int g_scan_variant = 0;  // 0: chosen per launch, 1: cp.async + CTA barriers (k_scan_tiles), 2: warp-specialised (k_scan_tiles_ws)
 bool g_wide_tile = false;  // true: 128 x 128 tile, one CTA per SM; false: 128 x 64 tile, two CTAs per SM
 
 }  // namespace
@@ -1269,20 +1293,26 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
                       bool pruning, bool symmetric, cudaStream_t stream) {
   if (k_end <= k_begin || live_upper_bound == 0) return 0;
   const bool lb = pruning && d_nbr_index == nullptr && s.lb_means != nullptr && g_scan_variant != 2;
+  // variant 0 (automatic): the warp-specialised kernel wherever the lower-bound filter has
+  // nothing to offer (window rounds; covering scans of searches on which it is switched off)
+  // and the batch still fills 128-candidate tiles; k_scan_tiles otherwise
+  const bool use_ws = g_scan_variant == 2 ||
+                      (g_scan_variant == 0 && g_packed_default && !g_wide_tile && !lb && live_upper_bound > 64);
   // tile shape: 64-candidate tiles once the batch has shrunk to that, else 128
-  const bool narrow = !g_wide_tile && g_scan_variant != 2 && live_upper_bound <= 64;
+  const bool narrow = !g_wide_tile && !use_ws && live_upper_bound <= 64;
   const uint32_t cand_rows = narrow ? 64 : 128;
-  const uint32_t nbr_rows = (g_scan_variant == 2) ? 64 : g_wide_tile ? 128 : narrow ? 128 : 64;
+  const uint32_t nbr_rows = use_ws ? 128 : g_wide_tile ? 128 : narrow ? 128 : 64;
   const uint32_t cand_tiles = (live_upper_bound + cand_rows - 1) / cand_rows;
   const uint64_t sub_tiles = static_cast<uint64_t>(k_end - k_begin) * (kTileRows / nbr_rows);
   // a few tiles per CTA (thresholds are refreshed per tile), several waves of CTAs per launch
-  const uint64_t resident = 148ull * ((g_wide_tile || g_scan_variant == 2) ? 1 : 2);
+  const uint64_t resident = 148ull * ((g_wide_tile || use_ws) ? 1 : 2);
   const uint64_t want = sub_tiles * cand_tiles / (resident * 8ull);
   const int tiles_per_cta = static_cast<int>(want < 1 ? 1 : want > 16 ? 16 : want);
   dim3 grid(static_cast<unsigned>((sub_tiles + tiles_per_cta - 1) / tiles_per_cta), cand_tiles);
   ScanArgs a{d_batch_matrix, d_batch_rows, d_batch_slots, d_sel, d_nbr_index, k_begin, k_end, rotation,
              tiles_per_cta, pruning ? 1 : 0};
-  if (g_scan_variant == 2) {
+  g_last_launch_was_ws = use_ws;
+  if (use_ws) {
     const int smem = static_cast<int>(sizeof(ws::SharedWs));
     if (symmetric) {
       cudaFuncSetAttribute(ws::k_scan_tiles_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1322,6 +1352,7 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
 void set_packed_math(bool on) { g_packed_default = on; }
 void set_wide_tile(bool on) { g_wide_tile = on; }
 void set_scan_variant(int variant) { g_scan_variant = variant; }
+bool scan_last_launch_was_ws() { return g_last_launch_was_ws; }
 
 int launch_finalize_batch(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,
                           uint32_t capacity, bool pruning, cudaStream_t stream) {

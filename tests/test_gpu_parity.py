@@ -179,7 +179,7 @@ def test_search_is_repeatable_and_independent_of_tunables(ctx):
     ctx.prepare(x, 128, 4, 4)
     base = ctx.search(3)
     for name, value in [("batch", 300), ("rounds", 1), ("rounds", 12), ("bucket_mates", 0),
-                        ("symmetric", 0), ("packed", 0), ("first_batch", 4096), ("wide_tile", 1), ("kernel", 2),
+                        ("symmetric", 0), ("packed", 0), ("first_batch", 4096), ("wide_tile", 1), ("kernel", 2), ("kernel", 1),
                         ("window_rounds", 0), ("rotate", 0), ("growth", 3.0), ("first_range", 128),
                         ("lower_bound", 0), ("margin_delta", 1e-3), ("batch_growth", 2)]:
         ctx.set_option(name, value)
@@ -187,7 +187,7 @@ def test_search_is_repeatable_and_independent_of_tunables(ctx):
         assert again[0] == base[0], name
         np.testing.assert_allclose(again[1], base[1], rtol=1e-6, err_msg=name)
     for name, value in [("batch", 65536), ("rounds", 64), ("bucket_mates", 8), ("symmetric", 1),
-                        ("packed", 1), ("first_batch", 256), ("wide_tile", 0), ("kernel", 1),
+                        ("packed", 1), ("first_batch", 256), ("wide_tile", 0), ("kernel", 0),
                         ("window_rounds", 4), ("rotate", 1), ("growth", 1.5), ("first_range", 2048),
                         ("lower_bound", 1), ("margin_delta", -1), ("batch_growth", 8)]:
         ctx.set_option(name, value)
