@@ -55,7 +55,7 @@ struct DeviceCounters {
   unsigned long long abandoned;  // of those, cut short by an abandoned tile
   unsigned long long terms;      // (x-y)^2 terms accumulated by any scan kernel
   unsigned long long tile_terms; // ... by the tiled kernel only
-  unsigned long long scanned;    // candidates that entered a full scan
+  unsigned long long reserved;   // (kept for layout stability)
   unsigned long long tiles;      // candidate-tile x neighbour-tile pairs started by the tiled kernel
   unsigned long long tile_live;  // live candidates summed over those tiles (128 per tile = dense)
   unsigned long long lb_skipped; // (candidate, neighbour tile) pairs the lower-bound filter ruled out

@@ -286,7 +286,7 @@ void prepare_on_device(tsdd_cuda_ctx* ctx, size_t m, size_t n, size_t word_len, 
   uint64_t launches = 0;
 
   const size_t matrix_floats = static_cast<size_t>(ctx->rows_padded) * ctx->stride;
-  {
+  if (matrix_floats > ctx->matrix.count) {  // only when the matrix has to grow (cudaMemGetInfo is slow)
     // The float32 matrix dominates the footprint; fail with a clear message instead of a
     // bare cudaMalloc error when the series does not fit this GPU (no CPU fallback).
     size_t free_bytes = 0, total_bytes = 0;
@@ -312,14 +312,13 @@ void prepare_on_device(tsdd_cuda_ctx* ctx, size_t m, size_t n, size_t word_len, 
   if (ctx->rows_padded > rows)
     CUDA_OK(cudaMemsetAsync(ctx->matrix.ptr + static_cast<size_t>(rows) * ctx->stride, 0,
                             static_cast<size_t>(ctx->rows_padded - rows) * ctx->stride * sizeof(float), st));
-  launches += launch_build_rows(ctx->series.ptr, ctx->mean.ptr, ctx->inv_sigma.ptr, rows,
-                                static_cast<uint32_t>(n), ctx->stride, ctx->matrix.ptr, st);
-
   ctx->lb_means.alloc(static_cast<size_t>(rows) * kLbSegments);
   ctx->lb_boxes.alloc(static_cast<size_t>((rows + kLbBoxRows - 1) / kLbBoxRows) * 2 * kLbSegments);
+  launches += launch_build_rows(ctx->series.ptr, ctx->mean.ptr, ctx->inv_sigma.ptr, rows,
+                                static_cast<uint32_t>(n), ctx->stride, ctx->matrix.ptr, ctx->lb_means.ptr, st);
+
   CUDA_OK(cudaEventRecord(ctx->ev_prep[2], st));
-  launches += launch_lower_bound_summaries(ctx->matrix.ptr, rows, ctx->stride, ctx->lb_means.ptr,
-                                           ctx->lb_boxes.ptr, st);
+  launches += launch_segment_boxes(ctx->lb_means.ptr, rows, ctx->lb_boxes.ptr, st);
   // bucket index: stable sort of (hash, row) -> runs are the buckets
   const size_t longest_scan = std::max<size_t>(rows, radix_sort_scratch_words(rows));
   ctx->scan_scratch.alloc(scan_scratch_words(static_cast<uint32_t>(longest_scan)) + 1024);

@@ -34,14 +34,15 @@ int launch_window_encode(const double* d_series, uint32_t rows, uint32_t n, uint
                          uint32_t alphabet, double* d_mean, double* d_inv_sigma, uint32_t* d_hash0,
                          double* d_paa, uint32_t* d_sax, cudaStream_t stream);
 
-// float32 z-normalised matrix, rows x stride, padding columns zero.
+// float32 z-normalised matrix, rows x stride, padding columns zero; and, when d_seg_means is
+// given, the kLbSegments segment means of every row (from the same staged samples).
 int launch_build_rows(const double* d_series, const double* d_mean, const double* d_inv_sigma,
-                      uint32_t rows, uint32_t n, uint32_t stride, float* d_rows, cudaStream_t stream);
+                      uint32_t rows, uint32_t n, uint32_t stride, float* d_rows, float* d_seg_means,
+                      cudaStream_t stream);
 
-// Segment means of every matrix row [rows x kLbSegments] and their per-kLbBoxRows-rows
-// bounding boxes [ceil(rows / kLbBoxRows) x 2 x kLbSegments] (min then max).
-int launch_lower_bound_summaries(const float* d_rows, uint32_t rows, uint32_t stride, float* d_means,
-                                 float* d_boxes, cudaStream_t stream);
+// Bounding boxes of the rows' segment means per kLbBoxRows rows:
+// [ceil(rows / kLbBoxRows) x 2 x kLbSegments] (minimum then maximum per segment).
+int launch_segment_boxes(const float* d_means, uint32_t rows, float* d_boxes, cudaStream_t stream);
 
 // Stable LSD radix sort of (key, value) pairs on bits [0, key_bits).  Result is
 // left in (*keys, *vals); the alt buffers are scratch.  `hist` needs

@@ -112,11 +112,18 @@ constexpr int kBuildRows = 32;
 constexpr int kBuildCols = 1024;
 constexpr int kBuildThreads = 256;
 
+//
+// The same staged samples also give the 16 segment means of every row (the lower-bound
+// summaries of the search): with P the prefix sums of the staged samples, the sum of row r
+// over columns [c0, c1) is ((P[r + c1] - P[r + c0]) - (c1 - c0) mu_r) / sigma_r.  A segment
+// that lies inside the block's columns is stored directly; one that straddles column blocks
+// (stride > 1024) is accumulated with atomicAdd into the pre-zeroed array.
 __global__ void __launch_bounds__(kBuildThreads)
 k_build_rows(const double* __restrict__ x, const double* __restrict__ mean,
              const double* __restrict__ inv_sigma, uint32_t rows, uint32_t n, uint32_t stride,
-             float* __restrict__ out) {
+             float* __restrict__ out, float* __restrict__ seg_means) {
   __shared__ double s_x[kBuildRows + kBuildCols];
+  __shared__ double s_p[kBuildRows + kBuildCols + 1];
   __shared__ double s_mu[kBuildRows], s_inv[kBuildRows];
   const uint32_t i0 = blockIdx.x * kBuildRows;
   const uint32_t t0 = blockIdx.y * kBuildCols;
@@ -133,6 +140,24 @@ k_build_rows(const double* __restrict__ x, const double* __restrict__ mean,
     s_inv[threadIdx.x] = inv_sigma[i0 + threadIdx.x];
   }
   __syncthreads();
+  if (seg_means != nullptr && threadIdx.x < 32) {  // one warp: prefix sums of the staged samples
+    const uint32_t total = n_rows + n_cols, per_lane = (total + 31) / 32;
+    const uint32_t lo = min(threadIdx.x * per_lane, total), hi = min(lo + per_lane, total);
+    double mine = 0.0;
+    for (uint32_t e = lo; e < hi; ++e) mine += s_x[e];
+    double incl = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double up = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+      if (threadIdx.x >= static_cast<uint32_t>(d)) incl += up;
+    }
+    double run = incl - mine;
+    for (uint32_t e = lo; e < hi; ++e) {
+      s_p[e] = run;
+      run += s_x[e];
+    }
+    if (threadIdx.x == 31) s_p[total] = run;  // lane 31's range ends at `total` (or is empty: run = grand total)
+  }
   for (uint32_t r = 0; r < n_rows; ++r) {
     const double mu = s_mu[r], inv = s_inv[r];
     float* dst = out + static_cast<size_t>(i0 + r) * stride + t0;
@@ -142,45 +167,34 @@ k_build_rows(const double* __restrict__ x, const double* __restrict__ mean,
       if (c < n_cols) dst[c] = (t0 + c < n) ? static_cast<float>((s_x[r + c] - mu) * inv) : 0.f;
     }
   }
+  if (seg_means == nullptr) return;
+  __syncthreads();  // s_p complete
+  const uint32_t seg_cols = stride / kLbSegments;
+  for (uint32_t item = threadIdx.x; item < n_rows * kLbSegments; item += kBuildThreads) {
+    const uint32_t r = item / kLbSegments, seg = item % kLbSegments;
+    // columns of the segment that lie in this block and inside the window (t < n)
+    const uint32_t c0 = max(seg * seg_cols, t0), c1 = min(min((seg + 1) * seg_cols, t0 + n_cols), n);
+    if (c1 <= c0) {
+      if (seg * seg_cols >= t0 && (seg + 1) * seg_cols <= t0 + n_cols)  // wholly padding: mean 0
+        seg_means[static_cast<size_t>(i0 + r) * kLbSegments + seg] = 0.f;
+      continue;
+    }
+    const double sum = ((s_p[r + c1 - t0] - s_p[r + c0 - t0]) - static_cast<double>(c1 - c0) * s_mu[r]) * s_inv[r];
+    const float part = static_cast<float>(sum / static_cast<double>(seg_cols));
+    float* dst = seg_means + static_cast<size_t>(i0 + r) * kLbSegments + seg;
+    if (seg * seg_cols >= t0 && (seg + 1) * seg_cols <= t0 + n_cols) *dst = part;  // the block holds the whole segment
+    else atomicAdd(dst, part);
+  }
 }
 
 // ------------------------------------------------------------------ lower-bound summaries
 // For the covering scan's tile filter (search_kernels.cu): kLbSegments segment means of
-// every float32 matrix row (over the padded stride, so every segment has stride / 16
-// columns), and, per kLbBoxRows consecutive rows, the per-segment minimum and maximum.
+// every matrix row (over the padded stride, so every segment has stride / 16 columns;
+// produced by k_build_rows), and, per kLbBoxRows consecutive rows, the per-segment minimum
+// and maximum (k_segment_boxes).
 // For two rows a, b:  sum_t (a_t - b_t)^2  >=  (stride / 16) * sum_k (A_k - B_k)^2
 // (Cauchy-Schwarz per segment), and replacing B_k by the nearest point of a box
 // [lo_k, hi_k] that contains it can only lower the right-hand side further.
-__global__ void __launch_bounds__(256)
-k_row_segment_means(const float* __restrict__ rows, uint32_t n_rows, uint32_t stride, float* __restrict__ means) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (row >= n_rows) return;
-  const uint32_t seg_cols = stride / kLbSegments;  // a multiple of 4: stride is a multiple of 64
-  const float4* p = reinterpret_cast<const float4*>(rows + static_cast<size_t>(row) * stride);
-  float acc[kLbSegments];
-#pragma unroll
-  for (int k = 0; k < kLbSegments; ++k) acc[k] = 0.f;
-  for (uint32_t q = lane; q < stride / 4; q += 32) {
-    const float4 v = __ldg(p + q);
-    const float sum = (v.x + v.y) + (v.z + v.w);
-    const uint32_t k = (4 * q) / seg_cols;
-#pragma unroll
-    for (int kk = 0; kk < kLbSegments; ++kk) acc[kk] += (static_cast<uint32_t>(kk) == k) ? sum : 0.f;
-  }
-#pragma unroll
-  for (int k = 0; k < kLbSegments; ++k) {
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) acc[k] += __shfl_xor_sync(0xFFFFFFFFu, acc[k], d);
-  }
-  if (lane < kLbSegments) {
-    float mine = 0.f;
-#pragma unroll
-    for (int k = 0; k < kLbSegments; ++k) mine = (lane == static_cast<uint32_t>(k)) ? acc[k] : mine;
-    means[static_cast<size_t>(row) * kLbSegments + lane] = mine / static_cast<float>(seg_cols);
-  }
-}
-
 // boxes[unit][0..15] = min, boxes[unit][16..31] = max over the unit's rows; one thread per (unit, segment)
 __global__ void k_segment_boxes(const float* __restrict__ means, uint32_t n_rows, float* __restrict__ boxes) {
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
@@ -408,20 +422,20 @@ int launch_window_encode(const double* d_series, uint32_t rows, uint32_t n, uint
 }
 
 int launch_build_rows(const double* d_series, const double* d_mean, const double* d_inv_sigma,
-                      uint32_t rows, uint32_t n, uint32_t stride, float* d_rows,
+                      uint32_t rows, uint32_t n, uint32_t stride, float* d_rows, float* d_seg_means,
                       cudaStream_t stream) {
   dim3 grid(blocks_for(rows, kBuildRows), blocks_for(stride, kBuildCols));
-  k_build_rows<<<grid, kBuildThreads, 0, stream>>>(d_series, d_mean, d_inv_sigma, rows, n, stride, d_rows);
+  if (d_seg_means != nullptr && grid.y > 1)  // segments straddle column blocks: they are accumulated
+    cudaMemsetAsync(d_seg_means, 0, static_cast<size_t>(rows) * kLbSegments * sizeof(float), stream);
+  k_build_rows<<<grid, kBuildThreads, 0, stream>>>(d_series, d_mean, d_inv_sigma, rows, n, stride, d_rows,
+                                                   d_seg_means);
   return 1;
 }
 
-int launch_lower_bound_summaries(const float* d_rows, uint32_t rows, uint32_t stride, float* d_means,
-                                 float* d_boxes, cudaStream_t stream) {
-  k_row_segment_means<<<blocks_for(static_cast<size_t>(rows) * 32, 256), 256, 0, stream>>>(d_rows, rows, stride,
-                                                                                          d_means);
+int launch_segment_boxes(const float* d_means, uint32_t rows, float* d_boxes, cudaStream_t stream) {
   const size_t cells = static_cast<size_t>((rows + kLbBoxRows - 1) / kLbBoxRows) * kLbSegments;
   k_segment_boxes<<<blocks_for(cells, 256), 256, 0, stream>>>(d_means, rows, d_boxes);
-  return 2;
+  return 1;
 }
 
 size_t scan_scratch_words(uint32_t count) {

@@ -45,7 +45,9 @@ def test_library_has_sm100a_code_and_blackwell_instructions():
     sass = subprocess.run(["cuobjdump", "-sass", engine.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in sass
     assert "FFMA2" in sass and "FADD2" in sass  # packed f32x2 arithmetic (sm_100+)
-    assert "LDGSTS" in sass                      # cp.async staging of the tiles
+    assert "LDGSTS" in sass                      # cp.async staging of the tiles (k_scan_tiles)
+    # the warp-specialised tile kernel: bulk async copies onto mbarriers, register rebalancing
+    assert "UBLKCP" in sass and "SYNCS" in sass and "USETMAXREG" in sass
 
 
 @pytest.mark.skipif(_has_gpu(), reason="checks the no-device failure mode")
