@@ -288,3 +288,29 @@ def test_cli_generate_writes_the_pinned_workloads(tmp_path, golden):
     assert _cli("generate", "--workload", 1, "--output", out64, "--format", "f64le").returncode == 0
     np.testing.assert_array_equal(np.fromfile(out64, dtype=np.float64), x.astype(np.float64))
     assert _cli("generate", "--workload", 9, "--output", out).returncode == 2
+
+
+# ------------------------------------------------------------------ bench.py contract (reference arm runs on CPU)
+def test_bench_reference_arm_prints_the_contract_line():
+    import json
+
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload", "1",
+                        "--gpus", "1", "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["metric"] == "subsequence_pair_distances_per_s"
+    assert line["value"] > 0 and line["e2e"]["value"] == line["value"]
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+    assert line["cpu_baseline"]["kind"] in ("reference", "port") and line["cpu_baseline"]["cores"] >= 1
+    assert line["config"]["workload"] == "cfg1" and line["vs_baseline"] is None
+
+
+def test_bench_reference_arm_other_ranks_exit_quietly():
+    env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload", "1",
+                        "--gpus", "2", "--steps", "1", "--warmup", "0"], capture_output=True, text=True, env=env,
+                       timeout=120)
+    assert p.returncode == 0 and p.stdout.strip() == ""
