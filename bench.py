@@ -14,9 +14,12 @@ top-k time of a step is reported beside it (`topk_time_s`).
           stream the kernels run on, max over ranks.
   e2e   : the reference-facing call (run_discovery with a HOST series in pinned memory):
           H2D copy + prepare + search + D2H of the result inside the timed region.
-  roofline : the tiled distance kernel against the FP32 CUDA-core peak.  One term
-          (x-y)^2 accumulated = 3 FLOP; `peak` is measured live with an
-          FFMA-only probe kernel (MEASURED_PEAKS.json has no FP32 entry) and
+  roofline : the tiled distance kernels against the FP32 CUDA-core peak.  `achieved` counts
+          the floating-point operations the kernels EXECUTE: a term in the direct form
+          (x-y)^2 = FADD + FFMA = 3 FLOP, a term in the dot-product form
+          (|a|^2 + |b|^2 - 2 a.b) = one FFMA = 2 FLOP; `algorithmic_tflops` is SURVEY.md
+          8d's figure (3 FLOP for every term, whatever the form).  `peak` is measured live
+          with an FFMA-only probe kernel (MEASURED_PEAKS.json has no FP32 entry) and
           `peak_nominal` = 148 SMs x 128 lanes x 2 x 1.965 GHz.
   cpu_baseline : the unmodified reference (oracle/_ref; else the C restatement) on the
           box's host cores, on a bounded sample (a prefix of the same series).
@@ -198,6 +201,7 @@ def run_cuda_arm(args) -> None:
     barrier()
     sampler = ClockSampler(local)
     totals = {"calls": 0, "terms": 0, "scan_terms": 0, "scan_ms": 0.0, "scan_launches": 0, "ws_launches": 0,
+              "dot_launches": 0, "dot_terms": 0,
               "launches": 0,
               "prep_ms": 0.0, "search_ms": 0.0, "build_rows_ms": 0.0, "encode_ms": 0.0, "index_ms": 0.0}
     with sampler:
@@ -211,6 +215,8 @@ def run_cuda_arm(args) -> None:
             totals["scan_ms"] += st["scan_kernel_ms"]
             totals["scan_launches"] += st["scan_kernel_launches"]
             totals["ws_launches"] += st["scan_kernel_ws_launches"]
+            totals["dot_launches"] += st["scan_kernel_dot_launches"]
+            totals["dot_terms"] += st["scan_kernel_dot_terms"]
             totals["launches"] += st["kernel_launches"]
             for key in ("prep_ms", "search_ms", "build_rows_ms", "encode_ms", "index_ms"):
                 totals[key] += st[key]
@@ -248,7 +254,10 @@ def run_cuda_arm(args) -> None:
         except OSError:
             pass
         scan_s = totals["scan_ms"] * 1e-3
-        achieved = 3.0 * totals["scan_terms"] / scan_s / 1e12 if scan_s > 0 else 0.0
+        direct_terms = totals["scan_terms"] - totals["dot_terms"]
+        executed_flop = 3.0 * direct_terms + 2.0 * totals["dot_terms"]
+        pipe_ops = 2.0 * direct_terms + 1.0 * totals["dot_terms"]  # FP32-pipe lane operations
+        achieved = executed_flop / scan_s / 1e12 if scan_s > 0 else 0.0
         peak = 2.0 * ffma_ops / 1e12
         nominal = 148 * 128 * 2 * 1.965e9 / 1e12
         traffic = None
@@ -276,15 +285,18 @@ def run_cuda_arm(args) -> None:
                     "d2h_bytes_per_step": int(k * 16 + 160), "topk_time_s": e2e_s / args.steps},
             "gpu_launches": int(totals["launches"]),
             "roofline": {"bound": "fp32",
-                         "kernel": "k_scan_tiles_ws + k_scan_tiles (the tile kernels: %d of %d launches warp-specialised)"
-                                   % (totals["ws_launches"], totals["scan_launches"]),
+                         "kernel": "k_scan_tiles_ws + k_scan_tiles (the tile kernels: %d of %d launches "
+                                   "warp-specialised, %d of those in the dot-product form)"
+                                   % (totals["ws_launches"], totals["scan_launches"], totals["dot_launches"]),
                          "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
                          "peak_source": "live FFMA-only probe kernel x 2 FLOP (MEASURED_PEAKS.json has no FP32 "
                                         "entry; B200_PROFILING.md states no FP32 fallback)",
                          "peak_nominal": nominal, "frac_nominal": achieved / nominal,
                          "terms_per_s": totals["scan_terms"] / scan_s if scan_s else 0.0,
-                         "fma_pipe_util": 2.0 * totals["scan_terms"] / scan_s / ffma_ops if scan_s else 0.0,
+                         "dot_form_share_of_terms": totals["dot_terms"] / max(1, totals["scan_terms"]),
+                         "algorithmic_tflops": 3.0 * totals["scan_terms"] / scan_s / 1e12 if scan_s else 0.0,
+                         "fma_pipe_util": pipe_ops / scan_s / ffma_ops if scan_s else 0.0,
                          "sub_fma_mix_probe_lane_ops_per_s": mix_ops, "ffma_probe_lane_ops_per_s": ffma_ops,
                          "launches": int(totals["scan_launches"]),
                          "avg_launch_ms": totals["scan_ms"] / max(1, totals["scan_launches"]),

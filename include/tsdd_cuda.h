@@ -64,6 +64,8 @@ typedef struct tsdd_cuda_stats {
   uint64_t tile_live_candidates; /* live candidates summed over them (128 per tile = dense tiles) */
   uint64_t lb_skipped;     /* (candidate, neighbour tile) pairs ruled out by the lower-bound filter */
   uint64_t scan_kernel_ws_launches; /* of scan_kernel_launches, those of the warp-specialised kernel */
+  uint64_t scan_kernel_dot_launches; /* of those, launches of its dot-product form (one FFMA per term) */
+  uint64_t scan_kernel_dot_terms;   /* of scan_kernel_terms, those computed as one FFMA */
 } tsdd_cuda_stats;
 
 /* ---- lifetime ------------------------------------------------------------ */
@@ -97,7 +99,10 @@ int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream);
  * "kernel" (0: per launch; 1: the cp.async tile kernel everywhere; 2: the
  * warp-specialised cp.async.bulk + mbarrier kernel everywhere), "rotate" (0/1), "share_bounds" (0/1), "lower_bound" (0/1: in the covering scan a
  * candidate skips a neighbour tile whose segment-mean boxes are provably
- * further away than its threshold),
+ * further away than its threshold), "dot_form" (the warp-specialised kernel
+ * computes d^2 as |a|^2 + |b|^2 - 2 a.b, one FFMA per term, with the discard band widened by
+ * its absolute error bound: 0 never; 1 once a search has found that tiles are not abandoned
+ * early anyway and the best-so-far dwarfs the bound; 2 from the first launch),
  * "time_kernels" (0/1: CUDA events around every tile-kernel launch).
  * Unknown name -> TSDD_ERR_PARAMETER.  None of them changes the result.     */
 int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value);

@@ -38,11 +38,15 @@ __host__ __device__ __forceinline__ uint32_t best_key_row(uint64_t key) {
 // among them is decided in float64 (k_exact_nn): float32 noise can then cost
 // work, never the answer.  A bound of exactly 0 is dead at once: nothing beats
 // the initial best-so-far 0 with it (discovery.cpp:90-93, hpp:45 `sq > best`).
-__device__ __forceinline__ bool dead_bound(float d2, uint64_t best, float margin) {
-  return d2 == 0.f || d2 * margin < __uint_as_float(key_bits(best));
+// `margin_abs` is 0 until a search has used the dot-product form of the distance
+// (search_kernels.cu: k_scan_tiles_ws<.., kDot>), whose rounding error is absolute
+// (cancellation in |a|^2 + |b|^2 - 2 a.b), not relative; from then on the band is
+// widened by twice that error bound.
+__device__ __forceinline__ bool dead_bound(float d2, uint64_t best, float margin, float margin_abs) {
+  return d2 == 0.f || fmaf(d2, margin, margin_abs) < __uint_as_float(key_bits(best));
 }
-__device__ __forceinline__ bool is_dead(uint64_t nn, uint64_t best, float margin) {
-  return dead_bound(__uint_as_float(key_bits(nn)), best, margin);
+__device__ __forceinline__ bool is_dead(uint64_t nn, uint64_t best, float margin, float margin_abs) {
+  return dead_bound(__uint_as_float(key_bits(nn)), best, margin, margin_abs);
 }
 
 __device__ __forceinline__ unsigned long long* as_ull(uint64_t* p) {
@@ -55,7 +59,7 @@ struct DeviceCounters {
   unsigned long long abandoned;  // of those, cut short by an abandoned tile
   unsigned long long terms;      // (x-y)^2 terms accumulated by any scan kernel
   unsigned long long tile_terms; // ... by the tiled kernel only
-  unsigned long long reserved;   // (kept for layout stability)
+  unsigned long long dot_terms;  // of tile_terms, those computed as one FFMA (dot-product form)
   unsigned long long tiles;      // candidate-tile x neighbour-tile pairs started by the tiled kernel
   unsigned long long tile_live;  // live candidates summed over those tiles (128 per tile = dense)
   unsigned long long lb_skipped; // (candidate, neighbour tile) pairs the lower-bound filter ruled out

@@ -151,7 +151,10 @@ struct tsdd_cuda_ctx {
   int opt_kernel = 0;
   bool opt_time_kernels = true;
   bool opt_share_bounds = true;
-  bool opt_lower_bound = true;      // tile filter by segment-mean lower bounds in the covering scan     // several ranks: min-reduce the nn bounds after every batch
+  bool opt_lower_bound = true;      // tile filter by segment-mean lower bounds in the covering scan
+  bool opt_tensor_map = true;       // covering scans of the ws kernel load tiles as TMA boxes
+  int opt_dot = 1;
+  int opt_dot_window_rounds = 2;    // window rounds of a batch that runs in the dot-product form                  // dot-product form of the ws kernel: 0 never, 1 when it pays, 2 always
 
   // prepared series
   bool prepared = false;
@@ -159,7 +162,8 @@ struct tsdd_cuda_ctx {
   uint32_t rows = 0, stride = 0, rows_padded = 0;
   DeviceArray<float> series_f32;
   DeviceArray<double> series, mean, inv_sigma;
-  DeviceArray<float> matrix, lb_means, lb_boxes;
+  DeviceArray<float> matrix, lb_means, lb_boxes, row_norms;
+  bool norms_ready = false;  // row_norms holds the norms of the prepared matrix
   DeviceArray<uint32_t> hash0, freq, offsets, slot_bucket, scalars, slot_of_row;
   DeviceArray<uint32_t> sort_buf[4], order_buf[4];
   uint32_t *sorted_hash = nullptr, *sorted_row = nullptr, *order = nullptr, *sorted_freq = nullptr;
@@ -177,6 +181,10 @@ struct tsdd_cuda_ctx {
   uint32_t batch_capacity = 0;
   bool lb_active = true;    // the lower-bound filter is still worth its (small) cost in this search
   bool lb_decided = false;
+  // Dot-product form (k_scan_tiles_ws<.., kDot>): wanted once tiles turn out not to be abandoned
+  // anyway; used (and the discard band widened by margin_abs, for the rest of the search) from the
+  // first batch on whose best-so-far dwarfs the error bound; dot_now: this batch launches it.
+  bool dot_wanted = false, dot_used = false, dot_now = false;
   uint32_t* h_sel = nullptr;      // pinned, 4 words + a ring of 4 x 4 words for lagged counts
   cudaEvent_t ev_ring[4] = {nullptr, nullptr, nullptr, nullptr};
   uint64_t* h_keys = nullptr;     // pinned, 4 keys
@@ -201,6 +209,18 @@ struct tsdd_cuda_ctx {
     return static_cast<float>(1.0 + delta);
   }
 
+  // Dot-form distances |a|^2 + |b|^2 - 2 a.b: two FFMA chains of n/2 products of magnitude
+  // <= |a||b| <= n, the two norms and three more roundings — within (n + 32) n 2^-24 of the
+  // float32 rows' true distance.  The band covers the error of a bound and of the best-so-far.
+  double dot_error() const {
+    return (static_cast<double>(n) + 32.0) * static_cast<double>(n) * 5.9604644775390625e-08;
+  }
+  bool dot_eligible(uint64_t best_key_now) const {
+    if (opt_dot == 2) return true;
+    const double best_d2 = static_cast<double>(float_from_bits(key_bits(best_key_now)));
+    return best_d2 >= 1000.0 * dot_error();  // the band is then below 0.2 % of the best-so-far
+  }
+
   SearchState state() {
     SearchState s;
     s.rows = matrix.ptr;
@@ -213,6 +233,8 @@ struct tsdd_cuda_ctx {
     s.best = best.ptr;
     s.counters = counters.ptr;
     s.margin = discard_margin();
+    s.margin_abs = dot_used ? static_cast<float>(2.0 * dot_error()) : 0.f;
+    s.row_norms = norms_ready ? row_norms.ptr : nullptr;
     s.lb_means = (opt_lower_bound && lb_active) ? lb_means.ptr : nullptr;
     s.lb_boxes = lb_boxes.ptr;
     s.lb_scale = static_cast<float>(stride / kLbSegments);
@@ -398,6 +420,7 @@ void finish_prepare(tsdd_cuda_ctx* ctx) {
 void reset_stats(tsdd_cuda_ctx* ctx) {
   std::memset(&ctx->stats, 0, sizeof(ctx->stats));
   ctx->prepared = false;
+  ctx->norms_ready = false;
 }
 
 template <typename T>
@@ -543,7 +566,11 @@ std::vector<Segment> plan_segments(const tsdd_cuda_ctx* ctx, bool pruning) {
     const uint32_t window_limit = slot_tiles / 8;
     double size = std::max<double>(ctx->opt_window_first, kTileRows);
     uint32_t at = 0;
-    for (int r = 0; r < ctx->opt_window_rounds && at < window_limit; ++r) {
+    // Dot form = a search whose tiles are never abandoned (noise-like rows): a word's
+    // neighbourhood is then hardly better than any other rows, and the windows' rows are met
+    // again by the covering scan — two rounds of them are enough.
+    const int window_rounds = ctx->dot_now ? std::min(ctx->opt_window_rounds, ctx->opt_dot_window_rounds) : ctx->opt_window_rounds;
+    for (int r = 0; r < window_rounds && at < window_limit; ++r) {
       const uint32_t upto = std::min<uint64_t>(window_limit, at + static_cast<uint64_t>(size) / tile);
       plan.push_back({true, at, upto});
       at = upto;
@@ -600,7 +627,8 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
       }
     }
     const uint32_t padded = round_up_u32(count, kTileRows);
-    launches += launch_gather_rows(s, list, ctx->sel.ptr, padded, ctx->batch_matrix.ptr, st);
+    const ScanChoice choice = choose_scan_kernel(s, count, plan[r].window, pruning, ctx->dot_now);
+    launches += launch_gather_rows(s, list, ctx->sel.ptr, padded, choice.tma, ctx->batch_matrix.ptr, st);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->opt_time_kernels) {
       e0 = next_event(ctx);
@@ -610,15 +638,27 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
     const int launched =
         launch_scan_tiles(s, ctx->batch_matrix.ptr, list, slots, ctx->sel.ptr, count,
                           plan[r].window ? ctx->sorted_row : nullptr, plan[r].k_begin, plan[r].k_end, rotation,
-                          pruning, ctx->opt_symmetric, st);
+                          pruning, ctx->opt_symmetric, ctx->dot_now, st);
     if (ctx->opt_time_kernels) CUDA_OK(cudaEventRecord(e1, st));
+    if (const char* err = scan_launch_error()) fail(TSDD_ERR_RUNTIME, err);
     launches += launched;
     ctx->stats.scan_kernel_launches += launched;
     if (launched && scan_last_launch_was_ws()) ctx->stats.scan_kernel_ws_launches += launched;
+    if (launched && scan_last_launch_was_dot()) ctx->stats.scan_kernel_dot_launches += launched;
   }
   launches += launch_finalize_batch(s, list, ctx->sel.ptr, ctx->batch_capacity, pruning, st);
   ctx->stats.kernel_launches += launches;
   ctx->stats.batches += 1;
+}
+
+// Whether early abandoning inside tiles has been worth anything so far in this search
+// (< 5 % of the started pair distances were cut short): then the dot-product form, which
+// cannot abandon inside a tile but needs half the FP32 instructions, is the better kernel.
+bool few_abandoned(tsdd_cuda_ctx* ctx) {
+  DeviceCounters c{};
+  CUDA_OK(cudaMemcpyAsync(&c, ctx->counters.ptr, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
+  sync_stream(ctx);
+  return c.calls > 0 && c.abandoned * 20 < c.calls;
 }
 
 // One exact arg-max pass over this rank's share of the rarity order.
@@ -652,6 +692,24 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
           ctx->lb_decided = true;
           s = ctx->state();
         }
+        if ((pruning && ctx->opt_dot) || ctx->opt_dot == 2) {
+          // Dot form or not, for this batch.  One rank decides from its own counters; several
+          // agree on `wanted` / `used` in the per-batch exchange below (the band must widen
+          // on every rank before dot-form bounds travel between them).
+          const bool alone = !(ctx->world > 1 || ctx->comm);
+          CUDA_OK(cudaMemcpyAsync(ctx->h_keys + 3, ctx->best.ptr, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+          if (alone && !ctx->dot_wanted && ctx->stats.batches >= 2) ctx->dot_wanted = few_abandoned(ctx);
+          sync_stream(ctx);
+          const uint64_t best_now = ctx->h_keys[3];
+          if (alone && ctx->dot_wanted && ctx->dot_eligible(best_now)) ctx->dot_used = true;
+          ctx->dot_now = ctx->dot_used && ctx->dot_eligible(best_now);
+          if (ctx->dot_now && !ctx->norms_ready) {
+            ctx->row_norms.alloc(static_cast<size_t>(ctx->rows) + 1);
+            ctx->stats.kernel_launches += launch_row_norms(ctx->matrix.ptr, ctx->rows + 1, ctx->stride, ctx->row_norms.ptr, st);
+            ctx->norms_ready = true;
+          }
+          s = ctx->state();
+        }
         ctx->stats.scanned_candidates += count;
         scan_batch(ctx, count, pruning);
       }
@@ -661,8 +719,12 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
       CUDA_OK(cudaMemcpyAsync(ctx->h_keys, ctx->best.ptr, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
       sync_stream(ctx);
       ctx->h_keys[1] = cursor < ctx->rows ? 1 : 0;
-      exchange_keys(ctx, ctx->h_keys, 2);
+      ctx->h_keys[2] = 0;
+      if (pruning && ctx->opt_dot && !ctx->dot_wanted && ctx->stats.batches >= 2) ctx->h_keys[2] = few_abandoned(ctx) ? 1 : 0;
+      exchange_keys(ctx, ctx->h_keys, 3);
       CUDA_OK(cudaMemcpyAsync(ctx->best.ptr, ctx->h_keys, sizeof(uint64_t), cudaMemcpyHostToDevice, st));
+      if (ctx->h_keys[2]) ctx->dot_wanted = true;  // the same on every rank, like the best-so-far
+      if (pruning && ctx->opt_dot && ctx->dot_wanted && ctx->dot_eligible(ctx->h_keys[0])) ctx->dot_used = true;
       const bool finished = ctx->h_keys[1] == 0;
       if (!finished) exchange_bounds(ctx);
       if (finished) break;
@@ -685,6 +747,7 @@ void collect_search_stats(tsdd_cuda_ctx* ctx) {
   ctx->stats.tiles = c.tiles;
   ctx->stats.tile_live_candidates = c.tile_live;
   ctx->stats.lb_skipped = c.lb_skipped;
+  ctx->stats.scan_kernel_dot_terms = c.dot_terms;
   double total = 0.0;
   for (size_t e = 0; e + 1 < ctx->events_used; e += 2) {
     float ms = 0.f;
@@ -701,6 +764,7 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   set_packed_math(ctx->opt_packed);
   set_wide_tile(ctx->opt_wide_tile);
   set_scan_variant(ctx->opt_packed ? ctx->opt_kernel : 1);
+  set_tensor_map_loads(ctx->opt_tensor_map);
   const bool pruning = (flags & TSDD_SEARCH_DISABLE_PRUNING) == 0;
   cudaStream_t st = ctx->stream;
   SearchState s = ctx->state();
@@ -709,6 +773,10 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   ctx->stats.batches = 0;
   ctx->lb_active = true;
   ctx->lb_decided = false;
+  ctx->dot_wanted = ctx->dot_used = ctx->opt_dot == 2;
+  ctx->dot_now = false;
+  s = ctx->state();
+  ctx->stats.scan_kernel_dot_launches = 0;
   ctx->stats.scanned_candidates = 0;
   ctx->stats.scan_kernel_launches = 0;
   ctx->stats.scan_kernel_ws_launches = 0;
@@ -760,7 +828,8 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
         sync_stream(ctx);
         // start from an upper bound just above the float32 value so that most rows abandon early
         const double start = static_cast<double>(float_from_bits(key_bits(nn_key_host))) *
-                             static_cast<double>(s.margin) * static_cast<double>(s.margin);
+                                 static_cast<double>(s.margin) * static_cast<double>(s.margin) +
+                             2.0 * static_cast<double>(ctx->state().margin_abs);
         unsigned long long bits;
         std::memcpy(&bits, &start, sizeof(bits));
         CUDA_OK(cudaMemcpyAsync(ctx->nn_bits.ptr, &bits, sizeof(bits), cudaMemcpyHostToDevice, st));
@@ -963,6 +1032,14 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
       ctx->opt_wide_tile = value != 0;
     } else if (key == "lower_bound") {
       ctx->opt_lower_bound = value != 0;
+    } else if (key == "dot_window_rounds") {
+      if (value < 0 || value > 64) fail(TSDD_ERR_PARAMETER, "dot_window_rounds must be in 0..64");
+      ctx->opt_dot_window_rounds = static_cast<int>(value);
+    } else if (key == "tensor_map") {
+      ctx->opt_tensor_map = value != 0;
+    } else if (key == "dot_form") {
+      if (value != 0 && value != 1 && value != 2) fail(TSDD_ERR_PARAMETER, "dot_form must be 0, 1 or 2");
+      ctx->opt_dot = static_cast<int>(value);
     } else if (key == "share_bounds") {
       ctx->opt_share_bounds = value != 0;
     } else if (key == "time_kernels") {

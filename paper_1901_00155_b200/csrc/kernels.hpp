@@ -83,6 +83,8 @@ struct SearchState {
   uint64_t* best;           // 1 best key
   DeviceCounters* counters;
   float margin;             // 1 + delta of the discard test (common.cuh: dead_bound)
+  float margin_abs;         // 0, or twice the absolute error bound of dot-form distances once a search uses them
+  const float* row_norms;   // N + 1 squared norms of the float32 rows (dot form), or nullptr
   const float* lb_means;    // N x kLbSegments segment means, or nullptr: no tile filter
   const float* lb_boxes;    // their bounding boxes per kLbBoxRows rows
   float lb_scale;           // columns per segment (stride / kLbSegments)
@@ -116,8 +118,22 @@ int launch_batch_slots(const uint32_t* d_batch_rows, const uint32_t* d_sel, cons
                        uint32_t capacity, uint32_t* d_keys, cudaStream_t stream);
 
 // Copies the batch's matrix rows into a dense [capacity_padded x stride] buffer.
+// tma_layout: the row order inside each 128-row tile that the tensor-map variant of the
+// warp-specialised kernel reads (search_kernels.cu: tma_row_of_candidate).
 int launch_gather_rows(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,
-                       uint32_t capacity_padded, float* d_batch_matrix, cudaStream_t stream);
+                       uint32_t capacity_padded, bool tma_layout, float* d_batch_matrix, cudaStream_t stream);
+
+// Which kernel launch_scan_tiles will pick for a launch (the gather before it needs `tma`).
+struct ScanChoice {
+  bool lb;   // k_scan_tiles with the lower-bound tile filter
+  bool ws;   // the warp-specialised kernel
+  bool tma;  // ... fed by tensor-map box loads (covering scans)
+  bool dot;  // ... in the dot-product form
+};
+ScanChoice choose_scan_kernel(const SearchState& s, uint32_t live_upper_bound, bool window, bool pruning,
+                              bool dot_form);
+void set_tensor_map_loads(bool on);
+const char* scan_launch_error();  // message of a failed launch_scan_tiles since the last call, or nullptr
 
 // The tiled early-abandoning distance kernel: batch candidates x neighbour units
 // [k_begin, k_end), one unit = 128 rows.  d_nbr_index == nullptr: unit k holds the rows of
@@ -128,10 +144,16 @@ int launch_gather_rows(SearchState s, const uint32_t* d_batch_rows, const uint32
 int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t* d_batch_rows,
                       const uint32_t* d_batch_slots, const uint32_t* d_sel, uint32_t live_upper_bound,
                       const uint32_t* d_nbr_index, uint32_t k_begin, uint32_t k_end, uint32_t rotation,
-                      bool pruning, bool symmetric, cudaStream_t stream);
+                      bool pruning, bool symmetric, bool dot_form, cudaStream_t stream);
 
-// Whether the last launch_scan_tiles picked the warp-specialised kernel.
+// Whether the last launch_scan_tiles picked the warp-specialised kernel / its dot-product form.
 bool scan_last_launch_was_ws();
+bool scan_last_launch_was_dot();
+
+// Squared norms of the float32 rows (rows 0 .. n_rows; row n_rows is the zero row), for the
+// dot-product form d^2 = |a|^2 + |b|^2 - 2 a.b of the warp-specialised tile kernel.
+int launch_row_norms(const float* d_rows, uint32_t n_rows_plus_one, uint32_t stride, float* d_norms,
+                     cudaStream_t stream);
 
 // Survivors of a complete scan are exact; each raises the best-so-far.
 int launch_finalize_batch(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,

@@ -16,6 +16,9 @@
 
 #include "kernels.hpp"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <type_traits>
 
 
@@ -142,7 +145,7 @@ __global__ void k_flag_live(SearchState s, const uint32_t* __restrict__ order, u
   if (e >= s.n_rows) return;
   const uint32_t row = order[e];
   bool live = (e % world == rank) && !s.excluded[row] && !s.exact[row];
-  if (live && pruning) live = !is_dead(s.nn[row], *s.best, s.margin);
+  if (live && pruning) live = !is_dead(s.nn[row], *s.best, s.margin, s.margin_abs);
   flags[t] = live ? 1u : 0u;
 }
 
@@ -186,7 +189,7 @@ k_compact_batch(SearchState s, const uint32_t* __restrict__ in, const uint32_t* 
     if (idx < count) {
       row = in[idx];
       slot = in_slots[idx];
-      keep = !pruning || !is_dead(load_key(s.nn + row), best, s.margin);
+      keep = !pruning || !is_dead(load_key(s.nn + row), best, s.margin, s.margin_abs);
     }
     const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, keep);
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -227,16 +230,29 @@ __global__ void k_batch_slots(const uint32_t* __restrict__ batch_rows, const uin
 // Dense copy of the batch's rows, NEGATED, so that the tile kernel forms
 // x - y as one add (and, packed, one add.f32x2).  Rows past the batch size
 // are zero.  One warp per row.
+//
+// The tensor-map variant of the warp-specialised kernel receives a candidate tile as TMA boxes
+// with the hardware's 128-byte swizzle (16-byte piece p of row r lands at piece p ^ (r & 7)).  Its
+// thread row ty reads 8 rows that share r & 7, so that the XOR is one per-thread constant:
+// rows (ty & 7) + 64 (ty >> 3) + 8 u.  For a warp (thread rows 2w, 2w + 1) to still own 16
+// CONSECUTIVE candidates of the word-sorted batch, candidate L = 16 w + 2 u + b of a tile is
+// stored at row 2 (w & 3) + b + 8 u + 64 (w >> 2).
+__host__ __device__ __forceinline__ uint32_t tma_row_of_candidate(uint32_t l) {
+  const uint32_t w = l >> 4, u = (l >> 1) & 7u, b = l & 1u;
+  return 2u * (w & 3u) + b + 8u * u + 64u * (w >> 2);
+}
 __global__ void __launch_bounds__(256)
 k_gather_rows(SearchState s, const uint32_t* __restrict__ batch_rows, const uint32_t* __restrict__ sel,
-              uint32_t capacity_padded, float* __restrict__ out) {
+              uint32_t capacity_padded, int tma_layout, float* __restrict__ out) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (r >= capacity_padded) return;
   const uint32_t count = sel[0];
   // only the tiles the scan will touch need refreshing
   if (r >= (count + kTileRows - 1) / kTileRows * kTileRows) return;
-  float4* dst = reinterpret_cast<float4*>(out + static_cast<size_t>(r) * s.stride);
+  // tma_layout: candidate L of a tile sits at row tma_row_of_candidate(L) of the tile
+  const uint32_t at = tma_layout ? (r & ~(kTileRows - 1u)) + tma_row_of_candidate(r & (kTileRows - 1u)) : r;
+  float4* dst = reinterpret_cast<float4*>(out + static_cast<size_t>(at) * s.stride);
   const uint32_t quads = s.stride / 4;
   if (r < count) {
     const float4* src =
@@ -263,7 +279,7 @@ k_finalize_batch(SearchState s, const uint32_t* __restrict__ batch_rows,
   if (idx < count) {
     const uint32_t row = batch_rows[idx];
     const uint64_t key = s.nn[row];
-    if (!pruning || !is_dead(key, best, s.margin)) {
+    if (!pruning || !is_dead(key, best, s.margin, s.margin_abs)) {
       s.exact[row] = 1;
       if (key_bits(key) != kInfBits) mine = best_key(key_bits(key), row);
     }
@@ -380,6 +396,12 @@ struct Acc<true, kU, kW> {
     v[u][w] = __ffma2_rn(d, d, v[u][w]);
     d = __fadd2_rn(make_float2(b.z, b.w), make_float2(na.z, na.w));
     v[u][w] = __ffma2_rn(d, d, v[u][w]);
+  }
+  // dot-product form: one FFMA2 per two columns; the candidate rows are stored negated, so
+  // this accumulates -(a . b)
+  __device__ __forceinline__ void dot(int u, int w, const float4& na, const float4& b) {
+    v[u][w] = __ffma2_rn(make_float2(b.x, b.y), make_float2(na.x, na.y), v[u][w]);
+    v[u][w] = __ffma2_rn(make_float2(b.z, b.w), make_float2(na.z, na.w), v[u][w]);
   }
 };
 
@@ -515,7 +537,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
           live = true;
         } else {
           const float bound = fminf(__uint_as_float(key_bits(pf_key)), s_loc[tid]);
-          if (!dead_bound(bound, best, s.margin)) {
+          if (!dead_bound(bound, best, s.margin, s.margin_abs)) {
             thr = bound;
             live = true;
           }
@@ -790,16 +812,26 @@ struct TileMeta {
   float nub[kNbrWs];         // neighbours' own bounds, -1 = none
   uint32_t jrow[kNbrWs];     // neighbour rows, ~0 = none
   uint32_t brow[kNbrWs];     // rows to load (none -> the zero row)
+  float nnorm[kNbrWs];       // dot form: squared norms of the neighbour rows
   unsigned long long calls;  // pair distances this tile starts
   uint32_t done;             // consumer warps that have abandoned the tile
   uint32_t pad;
 };
 
-struct SharedWs {
-  unsigned char stages[kStagesWs][kStageBytesWs];
+// Tensor-map variant: a stage is four TMA boxes of 128 rows x 32 columns (128 bytes a row,
+// 128-byte swizzle): candidates columns 0-31, 32-63, then neighbours likewise.
+constexpr int kBoxCols = 32;
+constexpr int kBoxBytes = kTileRows * kBoxCols * 4;
+constexpr int kStageBytesTma = 4 * kBoxBytes;
+static_assert(kChunk == 2 * kBoxCols, "a chunk is two boxes wide");
+
+template <bool kTma>
+struct SharedWsT {
+  unsigned char stages[kStagesWs][kTma ? kStageBytesTma : kStageBytesWs];
   TileMeta meta[2];
   uint32_t cand[kTileRows];
   float loc[kTileRows];
+  float cnorm[kTileRows];  // dot form: squared norms of the candidate rows
   uint32_t tag_tile[kStagesWs + 1];
   uint32_t tag_chunk[kStagesWs + 1];
   unsigned long long full[kStagesWs], empty[kStagesWs], meta_full[2], meta_empty[2];  // mbarriers
@@ -826,6 +858,14 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_box(void* smem_dst, const CUtensorMap* map, uint32_t col, uint32_t row,
+                                             unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_addr(smem_dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(col), "r"(row), "r"(smem_addr(bar))
+      : "memory");
+}
 __device__ __forceinline__ void bulk_copy_row(void* smem_dst, const void* gmem_src, uint32_t bytes,
                                               unsigned long long* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -834,10 +874,25 @@ __device__ __forceinline__ void bulk_copy_row(void* smem_dst, const void* gmem_s
                : "memory");
 }
 
-template <bool kSymmetric>
+// kDot: the distance as |a|^2 + |b|^2 - 2 a.b — ONE FFMA per term instead of FADD + FFMA, at
+// the price of (1) an absolute rounding error (n + 32) n 2^-24 instead of a relative one, which
+// the discard band absorbs (SearchState::margin_abs) and the float64 decision settles, and
+// (2) no early abandoning inside a tile (partial dot products are not monotone).  The engine
+// picks it for searches whose tiles are not being abandoned anyway (noise-like data) once
+// the best-so-far dwarfs the error bound.
+//
+// kTma (covering scans: the neighbour rows of a tile are consecutive matrix rows): a stage is
+// filled by FOUR cp.async.bulk.tensor instructions (two 128 x 32 boxes of the candidate tile,
+// two of the neighbour tile, hardware-swizzled) instead of 256 row copies.  The producer warp
+// shares a scheduler with two consumer warps, and the per-row copies (one elect / R2UR /
+// UBLKCP round per row: ~2,500 instructions per chunk) held that scheduler's consumers back.
+// Window launches gather scattered rows and keep the per-row copies.
+template <bool kSymmetric, bool kDot, bool kTma>
 __global__ void __launch_bounds__(kThreadsWs, 1)
-k_scan_tiles_ws(SearchState s, ScanArgs a) {
+k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap map_a,
+                const __grid_constant__ CUtensorMap map_b) {
   constexpr int kU = 8, kW = 8, kTx = 16;
+  using SharedWs = SharedWsT<kTma>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   SharedWs& sh = *reinterpret_cast<SharedWs*>(smem_raw);
 
@@ -848,8 +903,10 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float inf = __uint_as_float(kInfBits);
   if (tid < kTileRows) {
-    sh.cand[tid] = (cand0 + tid < count) ? a.batch_rows[cand0 + tid] : 0xFFFFFFFFu;
+    const uint32_t row = (cand0 + tid < count) ? a.batch_rows[cand0 + tid] : 0xFFFFFFFFu;
+    sh.cand[tid] = row;
     sh.loc[tid] = inf;
+    if constexpr (kDot) sh.cnorm[tid] = row != 0xFFFFFFFFu ? s.row_norms[row] : 0.f;
   }
   if (tid == 0) {
     for (int i = 0; i < kStagesWs; ++i) {
@@ -890,13 +947,14 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
       return unit * kTileRows + (h % kSub) * kNbrWs;
     };
     // bounds of the next tile, fetched while the current one streams
-    uint64_t cand_key[4], nbr_key[4];
+    uint32_t cand_ub[4], nbr_ub[4];  // float bits of the nn upper bounds
     uint32_t nbr_j[4];
+    float nbr_norm[kDot ? 4 : 1];
     auto fetch_bounds = [&](uint32_t k) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const uint32_t row = sh.cand[lane + 32 * q];
-        cand_key[q] = (row != 0xFFFFFFFFu && a.pruning) ? load_key(s.nn + row) : 0ull;
+        cand_ub[q] = (row != 0xFFFFFFFFu && a.pruning) ? key_bits(load_key(s.nn + row)) : 0u;
       }
       const uint32_t slot0 = slot0_of(k);
 #pragma unroll
@@ -904,7 +962,8 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
         const uint32_t slot = slot0 + lane + 32 * q;
         nbr_j[q] = 0xFFFFFFFFu;
         if (slot < s.n_rows) nbr_j[q] = window ? a.nbr_index[slot] : slot;
-        nbr_key[q] = nbr_j[q] != 0xFFFFFFFFu ? load_key(s.nn + nbr_j[q]) : 0ull;
+        nbr_ub[q] = nbr_j[q] != 0xFFFFFFFFu ? key_bits(load_key(s.nn + nbr_j[q])) : 0u;
+        if constexpr (kDot) nbr_norm[q] = nbr_j[q] != 0xFFFFFFFFu ? s.row_norms[nbr_j[q]] : 0.f;
       }
     };
     if (n_tiles) fetch_bounds(k_first);
@@ -932,8 +991,8 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
             thr = inf;
             live[q] = true;
           } else {
-            const float bound = fminf(__uint_as_float(key_bits(cand_key[q])), sh.loc[r]);
-            if (!dead_bound(bound, best, s.margin)) {
+            const float bound = fminf(__uint_as_float(cand_ub[q]), sh.loc[r]);
+            if (!dead_bound(bound, best, s.margin, s.margin_abs)) {
               thr = bound;
               live[q] = true;
             }
@@ -948,7 +1007,8 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
         const uint32_t e = lane + 32 * q, j = nbr_j[q];
         meta.jrow[e] = j;
         meta.brow[e] = j != 0xFFFFFFFFu ? j : s.n_rows;  // row n_rows is zero padding
-        meta.nub[e] = j != 0xFFFFFFFFu ? __uint_as_float(key_bits(nbr_key[q])) : -1.f;
+        meta.nub[e] = j != 0xFFFFFFFFu ? __uint_as_float(nbr_ub[q]) : -1.f;
+        if constexpr (kDot) meta.nnorm[e] = nbr_norm[q];
       }
       any_live = __any_sync(0xFFFFFFFFu, any_live);
       __syncwarp();
@@ -988,12 +1048,14 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
       calls_total += calls;
       tiles_total += 1;
 
-      const float* src[kRowsPerStage / 32];
+      const float* src[kTma ? 1 : kRowsPerStage / 32];
+      if constexpr (!kTma) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) src[q] = a_tile + static_cast<size_t>(lane + 32 * q) * s.stride;
+        for (int q = 0; q < 4; ++q) src[q] = a_tile + static_cast<size_t>(lane + 32 * q) * s.stride;
 #pragma unroll
-      for (int q = 0; q < kNbrWs / 32; ++q)
-        src[4 + q] = s.rows + static_cast<size_t>(meta.brow[lane + 32 * q]) * s.stride;
+        for (int q = 0; q < kNbrWs / 32; ++q)
+          src[4 + q] = s.rows + static_cast<size_t>(meta.brow[lane + 32 * q]) * s.stride;
+      }
       if (ti + 1 < n_tiles) fetch_bounds(k + 1);
 
       // ---- stream the tile's chunks; stop as soon as every consumer warp has abandoned it
@@ -1007,11 +1069,21 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
           sh.tag_chunk[st] = c;
           mbar_arrive_expect_tx(&sh.full[st], kRowsPerStage * kChunk * 4);
         }
-        __syncwarp();
         unsigned char* dst = sh.stages[st];
+        if constexpr (kTma) {
+          if (lane == 0) {
+            const uint32_t col = c * kChunk;
+            tma_load_box(dst, &map_a, col, cand0, &sh.full[st]);
+            tma_load_box(dst + kBoxBytes, &map_a, col + kBoxCols, cand0, &sh.full[st]);
+            tma_load_box(dst + 2 * kBoxBytes, &map_b, col, slot0, &sh.full[st]);
+            tma_load_box(dst + 3 * kBoxBytes, &map_b, col + kBoxCols, slot0, &sh.full[st]);
+          }
+        } else {
+          __syncwarp();
 #pragma unroll
-        for (int q = 0; q < kRowsPerStage / 32; ++q)
-          bulk_copy_row(dst + (lane + 32 * q) * kPitch, src[q] + c * kChunk, kChunk * 4, &sh.full[st]);
+          for (int q = 0; q < kRowsPerStage / 32; ++q)
+            bulk_copy_row(dst + (lane + 32 * q) * kPitch, src[q] + c * kChunk, kChunk * 4, &sh.full[st]);
+        }
         ++seq;
       }
     }
@@ -1077,30 +1149,43 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
     }
     TileMeta& meta = sh.meta[m];
     if (!warp_done) {
-      const unsigned char* a_s = sh.stages[st] + cand0_of_thread * kPitch;
-      const unsigned char* b_s = sh.stages[st] + kTileRows * kPitch + tx * kPitch;
+      // kTma: rows of 128 bytes, 16-byte piece p of row r at piece p ^ (r & 7); this thread's
+      // candidate rows (ty & 7) + 64 (ty >> 3) + 8 u and neighbour rows tx + 16 w keep r & 7
+      constexpr int kAStep = kTma ? 8 * 128 : kCandStep * kPitch;
+      constexpr int kBStep = kTma ? kTx * 128 : kTx * kPitch;
+      const unsigned char* a_s =
+          kTma ? sh.stages[st] + ((ty & 7u) + 64u * (ty >> 3)) * 128u : sh.stages[st] + cand0_of_thread * kPitch;
+      const unsigned char* b_s =
+          kTma ? sh.stages[st] + 2 * kBoxBytes + tx * 128u : sh.stages[st] + kTileRows * kPitch + tx * kPitch;
 #pragma unroll 2
       for (int kc = 0; kc < kPieces; ++kc) {
+        const uint32_t a_off = kTma ? (kc >> 3) * kBoxBytes + ((((kc & 7u) ^ ty) & 7u) << 4) : kc * 16u;
+        const uint32_t b_off = kTma ? (kc >> 3) * kBoxBytes + ((((kc & 7u) ^ tx) & 7u) << 4) : kc * 16u;
         float4 na[kU];
 #pragma unroll
-        for (int u = 0; u < kU; ++u) na[u] = *reinterpret_cast<const float4*>(a_s + u * (kCandStep * kPitch) + kc * 16);
+        for (int u = 0; u < kU; ++u) na[u] = *reinterpret_cast<const float4*>(a_s + u * kAStep + a_off);
 #pragma unroll
         for (int w = 0; w < kW; ++w) {
-          const float4 b = *reinterpret_cast<const float4*>(b_s + w * (kTx * kPitch) + kc * 16);
+          const float4 b = *reinterpret_cast<const float4*>(b_s + w * kBStep + b_off);
 #pragma unroll
-          for (int u = 0; u < kU; ++u) acc.add(u, w, na[u], b);
+          for (int u = 0; u < kU; ++u) {
+            if constexpr (kDot) acc.dot(u, w, na[u], b);
+            else acc.add(u, w, na[u], b);
+          }
         }
       }
       ++chunks_done;
       ++chunks_total;
-      bool all_over = true;
+      if constexpr (!kDot) {
+        bool all_over = true;
 #pragma unroll
-      for (int u = 0; u < kU; ++u)
+        for (int u = 0; u < kU; ++u)
 #pragma unroll
-        for (int w = 0; w < kW; ++w) all_over = all_over && (acc.get(u, w) > thr[u]);
-      warp_done = __all_sync(0xFFFFFFFFu, all_over);
-      if (warp_done && c + 1 < chunks && lane == 0) {
-        if (atomicAdd(&meta.done, 1u) == kConsumerWarps - 1) abandoned_total += meta.calls;  // the last vote
+          for (int w = 0; w < kW; ++w) all_over = all_over && (acc.get(u, w) > thr[u]);
+        warp_done = __all_sync(0xFFFFFFFFu, all_over);
+        if (warp_done && c + 1 < chunks && lane == 0) {
+          if (atomicAdd(&meta.done, 1u) == kConsumerWarps - 1) abandoned_total += meta.calls;  // the last vote
+        }
       }
     }
     __syncwarp();
@@ -1112,12 +1197,25 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
         float nub[kW];
 #pragma unroll
         for (int w = 0; w < kW; ++w) nub[w] = kSymmetric ? meta.nub[tx + kTx * w] : -1.f;
+        // dot form: d^2 = |a|^2 + |b|^2 + 2 acc (acc = -(a . b)), never below the error bound
+        float cn[kDot ? kU : 1], bn[kDot ? kW : 1];
+        if constexpr (kDot) {
+#pragma unroll
+          for (int u = 0; u < kU; ++u) cn[u] = sh.cnorm[cand0_of_thread + kCandStep * u];
+#pragma unroll
+          for (int w = 0; w < kW; ++w) bn[w] = meta.nnorm[tx + kTx * w];
+        }
+        const float d_floor = 0.5f * s.margin_abs;
+        auto dist = [&](int u, int w) -> float {
+          if constexpr (kDot) return fmaxf(fmaf(2.f, acc.get(u, w), cn[u] + bn[w]), d_floor);
+          else return acc.get(u, w);
+        };
         bool hit = false;
 #pragma unroll
         for (int u = 0; u < kU; ++u)
 #pragma unroll
           for (int w = 0; w < kW; ++w) {
-            const float d = acc.get(u, w);
+            const float d = dist(u, w);
             hit = hit || d <= thr[u] || d < nub[w];
           }
         if (__any_sync(0xFFFFFFFFu, hit)) {
@@ -1131,7 +1229,7 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
 #pragma unroll
             for (int w = 0; w < kW; ++w) {
               const uint32_t j = jrow[w];
-              const float d = acc.get(u, w);
+              const float d = dist(u, w);
               const bool pair_ok = row != 0xFFFFFFFFu && j != 0xFFFFFFFFu && gap_u32(row, j) >= s.n;
               if (pair_ok && d <= thr[u]) {
                 const uint32_t bits = __float_as_uint(d);
@@ -1167,12 +1265,29 @@ k_scan_tiles_ws(SearchState s, ScanArgs a) {
     if (terms) {
       atomicAdd(&s.counters->terms, terms);
       atomicAdd(&s.counters->tile_terms, terms);
+      if constexpr (kDot) atomicAdd(&s.counters->dot_terms, terms);
     }
     if (abandoned_total) atomicAdd(&s.counters->abandoned, abandoned_total);
   }
 }
 
 }  // namespace ws
+
+// Squared norm of every float32 row (padding columns are zero): one warp per row.
+__global__ void __launch_bounds__(256)
+k_row_norms(const float* __restrict__ rows, uint32_t n_rows, uint32_t stride, float* __restrict__ norms) {
+  const uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= n_rows) return;
+  const float4* p = reinterpret_cast<const float4*>(rows + static_cast<size_t>(row) * stride);
+  float acc = 0.f;
+  for (uint32_t c = lane; c < stride / 4; c += 32) {
+    const float4 v = p[c];
+    acc += (v.x * v.x + v.y * v.y) + (v.z * v.z + v.w * v.w);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, d);
+  if (lane == 0) norms[row] = acc;
+}
 
 // ------------------------------------------------------------------ finalists, decided in float64
 __global__ void __launch_bounds__(256)
@@ -1181,7 +1296,7 @@ k_collect_finalists(SearchState s, uint32_t* __restrict__ list, uint32_t cap, ui
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < s.n_rows; i += gridDim.x * blockDim.x) {
     if (!s.exact[i] || s.excluded[i]) continue;
     const uint64_t key = s.nn[i];
-    if (key_bits(key) == kInfBits || is_dead(key, best, s.margin)) continue;
+    if (key_bits(key) == kInfBits || is_dead(key, best, s.margin, s.margin_abs)) continue;
     const uint32_t at = atomicAdd(count, 1u);
     if (at < cap) list[at] = i;
   }
@@ -1227,6 +1342,10 @@ k_exact_nn(const double* __restrict__ x, const double* __restrict__ mean, const 
 
 bool g_packed_default = true;
 bool g_last_launch_was_ws = false;
+bool g_last_launch_was_dot = false;
+bool g_tma_enabled = true;
+const char* g_launch_error = nullptr;
+inline uint32_t slot_tiles_of(uint32_t rows) { return (rows + kTileRows - 1) / kTileRows; }
 int g_scan_variant = 0;  // 0: chosen per launch, 1: cp.async + CTA barriers (k_scan_tiles), 2: warp-specialised (k_scan_tiles_ws)
 bool g_wide_tile = false;  // true: 128 x 128 tile, one CTA per SM; false: 128 x 64 tile, two CTAs per SM
 
@@ -1281,23 +1400,60 @@ int launch_batch_slots(const uint32_t* d_batch_rows, const uint32_t* d_sel, cons
 }
 
 int launch_gather_rows(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,
-                       uint32_t capacity_padded, float* d_batch_matrix, cudaStream_t stream) {
+                       uint32_t capacity_padded, bool tma_layout, float* d_batch_matrix, cudaStream_t stream) {
   k_gather_rows<<<blocks_for(static_cast<size_t>(capacity_padded) * 32, 256), 256, 0, stream>>>(
-      s, d_batch_rows, d_sel, capacity_padded, d_batch_matrix);
+      s, d_batch_rows, d_sel, capacity_padded, tma_layout ? 1 : 0, d_batch_matrix);
   return 1;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no link against libcuda).
+PFN_cuTensorMapEncodeTiled tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult status = cudaDriverEntryPointSymbolNotFound;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &status) != cudaSuccess ||
+        status != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    (void)cudaGetLastError();
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(p);
+  }();
+  return fn;
+}
+
+// float32 matrix [n_rows x stride], boxes of 128 rows x 32 columns, 128-byte swizzle
+bool make_row_map(CUtensorMap* map, const float* base, uint64_t n_rows, uint32_t stride) {
+  PFN_cuTensorMapEncodeTiled encode = tensor_map_encoder();
+  if (!encode) return false;
+  const cuuint64_t dims[2] = {stride, n_rows};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(stride) * sizeof(float)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(ws::kBoxCols), static_cast<cuuint32_t>(kTileRows)};
+  const cuuint32_t elem[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, elem,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+ScanChoice choose_scan_kernel(const SearchState& s, uint32_t live_upper_bound, bool window, bool pruning,
+                              bool dot_form) {
+  ScanChoice c{};
+  c.lb = pruning && !window && s.lb_means != nullptr && g_scan_variant != 2;
+  // variant 0 (automatic): the warp-specialised kernel wherever the lower-bound filter has
+  // nothing to offer (window rounds; covering scans of searches on which it is switched off)
+  // and the batch still fills 128-candidate tiles; k_scan_tiles otherwise
+  c.ws = g_scan_variant == 2 ||
+         (g_scan_variant == 0 && g_packed_default && !g_wide_tile && !c.lb && live_upper_bound > 64);
+  c.tma = c.ws && !window && g_tma_enabled && tensor_map_encoder() != nullptr;
+  c.dot = c.ws && dot_form && s.row_norms != nullptr;
+  return c;
 }
 
 int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t* d_batch_rows,
                       const uint32_t* d_batch_slots, const uint32_t* d_sel, uint32_t live_upper_bound,
                       const uint32_t* d_nbr_index, uint32_t k_begin, uint32_t k_end, uint32_t rotation,
-                      bool pruning, bool symmetric, cudaStream_t stream) {
+                      bool pruning, bool symmetric, bool dot_form, cudaStream_t stream) {
   if (k_end <= k_begin || live_upper_bound == 0) return 0;
-  const bool lb = pruning && d_nbr_index == nullptr && s.lb_means != nullptr && g_scan_variant != 2;
-  // variant 0 (automatic): the warp-specialised kernel wherever the lower-bound filter has
-  // nothing to offer (window rounds; covering scans of searches on which it is switched off)
-  // and the batch still fills 128-candidate tiles; k_scan_tiles otherwise
-  const bool use_ws = g_scan_variant == 2 ||
-                      (g_scan_variant == 0 && g_packed_default && !g_wide_tile && !lb && live_upper_bound > 64);
+  const ScanChoice choice = choose_scan_kernel(s, live_upper_bound, d_nbr_index != nullptr, pruning, dot_form);
+  const bool lb = choice.lb, use_ws = choice.ws;
   // tile shape: 64-candidate tiles once the batch has shrunk to that, else 128
   const bool narrow = !g_wide_tile && !use_ws && live_upper_bound <= 64;
   const uint32_t cand_rows = narrow ? 64 : 128;
@@ -1312,15 +1468,31 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
   ScanArgs a{d_batch_matrix, d_batch_rows, d_batch_slots, d_sel, d_nbr_index, k_begin, k_end, rotation,
              tiles_per_cta, pruning ? 1 : 0};
   g_last_launch_was_ws = use_ws;
+  g_last_launch_was_dot = choice.dot;
   if (use_ws) {
-    const int smem = static_cast<int>(sizeof(ws::SharedWs));
-    if (symmetric) {
-      cudaFuncSetAttribute(ws::k_scan_tiles_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      ws::k_scan_tiles_ws<true><<<grid, ws::kThreadsWs, smem, stream>>>(s, a);
-    } else {
-      cudaFuncSetAttribute(ws::k_scan_tiles_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      ws::k_scan_tiles_ws<false><<<grid, ws::kThreadsWs, smem, stream>>>(s, a);
+    CUtensorMap map_a{}, map_b{};
+    bool tma = choice.tma;
+    if (tma)
+      tma = make_row_map(&map_a, d_batch_matrix, static_cast<uint64_t>(cand_tiles) * kTileRows, s.stride) &&
+            make_row_map(&map_b, s.rows, static_cast<uint64_t>(slot_tiles_of(s.n_rows + 1)) * kTileRows, s.stride);
+    if (choice.tma && !tma) {  // the gather already used the tensor-map row order: no way back
+      g_launch_error = "cuTensorMapEncodeTiled failed";
+      return 0;
     }
+    auto launch_ws = [&](auto kernel, size_t smem_bytes) {
+      const int smem = static_cast<int>(smem_bytes);
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      kernel<<<grid, ws::kThreadsWs, smem, stream>>>(s, a, map_a, map_b);
+    };
+    auto pick_ws = [&](auto sym) {
+      constexpr bool kS = decltype(sym)::value;
+      if (tma && choice.dot) launch_ws(ws::k_scan_tiles_ws<kS, true, true>, sizeof(ws::SharedWsT<true>));
+      else if (tma) launch_ws(ws::k_scan_tiles_ws<kS, false, true>, sizeof(ws::SharedWsT<true>));
+      else if (choice.dot) launch_ws(ws::k_scan_tiles_ws<kS, true, false>, sizeof(ws::SharedWsT<false>));
+      else launch_ws(ws::k_scan_tiles_ws<kS, false, false>, sizeof(ws::SharedWsT<false>));
+    };
+    if (symmetric) pick_ws(std::true_type{});
+    else pick_ws(std::false_type{});
     return 1;
   }
   auto launch = [&](auto kernel) {
@@ -1353,6 +1525,20 @@ void set_packed_math(bool on) { g_packed_default = on; }
 void set_wide_tile(bool on) { g_wide_tile = on; }
 void set_scan_variant(int variant) { g_scan_variant = variant; }
 bool scan_last_launch_was_ws() { return g_last_launch_was_ws; }
+bool scan_last_launch_was_dot() { return g_last_launch_was_dot; }
+void set_tensor_map_loads(bool on) { g_tma_enabled = on; }
+const char* scan_launch_error() {
+  const char* e = g_launch_error;
+  g_launch_error = nullptr;
+  return e;
+}
+
+int launch_row_norms(const float* d_rows, uint32_t n_rows_plus_one, uint32_t stride, float* d_norms,
+                     cudaStream_t stream) {
+  k_row_norms<<<blocks_for(static_cast<size_t>(n_rows_plus_one) * 32, 256), 256, 0, stream>>>(d_rows, n_rows_plus_one,
+                                                                                            stride, d_norms);
+  return 1;
+}
 
 int launch_finalize_batch(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,
                           uint32_t capacity, bool pruning, cudaStream_t stream) {

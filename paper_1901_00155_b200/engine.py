@@ -61,7 +61,9 @@ class Stats(ctypes.Structure):
                 ("encode_ms", ctypes.c_double), ("build_rows_ms", ctypes.c_double),
                 ("index_ms", ctypes.c_double), ("tiles", ctypes.c_uint64),
                 ("tile_live_candidates", ctypes.c_uint64), ("lb_skipped", ctypes.c_uint64),
-                ("scan_kernel_ws_launches", ctypes.c_uint64)]
+                ("scan_kernel_ws_launches", ctypes.c_uint64),
+                ("scan_kernel_dot_launches", ctypes.c_uint64),
+                ("scan_kernel_dot_terms", ctypes.c_uint64)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}

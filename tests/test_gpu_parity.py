@@ -181,7 +181,8 @@ def test_search_is_repeatable_and_independent_of_tunables(ctx):
     for name, value in [("batch", 300), ("rounds", 1), ("rounds", 12), ("bucket_mates", 0),
                         ("symmetric", 0), ("packed", 0), ("first_batch", 4096), ("wide_tile", 1), ("kernel", 2), ("kernel", 1),
                         ("window_rounds", 0), ("rotate", 0), ("growth", 3.0), ("first_range", 128),
-                        ("lower_bound", 0), ("margin_delta", 1e-3), ("batch_growth", 2)]:
+                        ("lower_bound", 0), ("margin_delta", 1e-3), ("batch_growth", 2), ("dot_form", 2),
+                        ("dot_form", 0)]:
         ctx.set_option(name, value)
         again = ctx.search(3)
         assert again[0] == base[0], name
@@ -189,7 +190,7 @@ def test_search_is_repeatable_and_independent_of_tunables(ctx):
     for name, value in [("batch", 65536), ("rounds", 64), ("bucket_mates", 8), ("symmetric", 1),
                         ("packed", 1), ("first_batch", 256), ("wide_tile", 0), ("kernel", 0),
                         ("window_rounds", 4), ("rotate", 1), ("growth", 1.5), ("first_range", 2048),
-                        ("lower_bound", 1), ("margin_delta", -1), ("batch_growth", 8)]:
+                        ("lower_bound", 1), ("margin_delta", -1), ("batch_growth", 8), ("dot_form", 1)]:
         ctx.set_option(name, value)
 
 
@@ -285,6 +286,39 @@ def test_rank_count_does_not_change_the_result(chk, world, share):  # the analog
         assert results[r][0] == want["positions"], (r, results[r])
         np.testing.assert_allclose(results[r][1], want["distances"], rtol=DIST_RTOL)
     assert ex.calls > 0
+
+
+@pytest.mark.parametrize("dot", [1, 2])
+def test_ranks_agree_on_the_dot_product_form(chk, dot):
+    """Noise, two ranks: the switch to the dot-product form (and the wider discard band that
+    goes with it) travels in the per-batch exchange, so both ranks take it together."""
+    x = np.random.default_rng(11).random(30000).astype(np.float32)
+    want = chk.topk(x, 96, 6, 4, 2)
+    world, ex = 2, _ThreadExchange(2)
+    results, used, errors = [None] * world, [0] * world, []
+
+    def run(rank):
+        try:
+            with Context(0) as c:
+                c.set_option("batch", 4096)
+                c.set_option("dot_form", dot)
+                c.set_exchange(ex.hook(rank), world, rank)
+                c.prepare(x, 96, 6, 4)
+                results[rank] = c.search(2)
+                used[rank] = c.stats()["scan_kernel_dot_launches"]
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+            ex.barrier.abort()
+
+    threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not errors, errors
+    for r in range(world):
+        assert_discords_match(chk, x, 96, results[r][0], results[r][1], want)
+        assert used[r] > 0
 
 
 def test_sharing_bounds_between_ranks_saves_work():
@@ -443,6 +477,55 @@ def test_randomised_small_cases_match_the_oracle(ctx, chk, seed, kind, n):
     pos, dist = ctx.search(k)
     want = chk.topk(x, n, w, a, k)
     assert_discords_match(chk, x, n, pos, dist, want)
+
+
+@pytest.mark.parametrize("seed,kind,n", FUZZ, ids=[f"{k}-n{n}" for _, k, n in FUZZ])
+def test_dot_product_form_matches_the_oracle(ctx, chk, seed, kind, n):
+    """The warp-specialised kernel's one-FFMA-per-term form, forced on from the first launch
+    (the engine itself waits until the best-so-far dwarfs the form's absolute error): the
+    wider discard band and the float64 decision must still give the reference's answer."""
+    rng = np.random.default_rng(7000 + seed)
+    m = int(rng.integers(2 * n + 200, 2 * n + 3000))
+    w = int(rng.integers(1, min(n, 8) + 1))
+    a = int(rng.integers(2, 7))
+    k = int(rng.integers(1, 4))
+    x = _fuzz_series(rng, kind, m)
+    ctx.set_option("dot_form", 2)
+    try:
+        ctx.prepare(x, n, w, a)
+        pos, dist = ctx.search(k)
+        used = ctx.stats()["scan_kernel_dot_launches"]
+    finally:
+        ctx.set_option("dot_form", 1)
+    want = chk.topk(x, n, w, a, k)
+    assert_discords_match(chk, x, n, pos, dist, want)
+    assert used > 0 or m - n + 1 <= 64 * 4  # (tiny batches run on the 64-candidate tile kernel)
+
+
+def test_dot_product_form_is_chosen_where_tiles_are_never_abandoned(ctx, chk):
+    """i.i.d. noise (BASELINE.json workload 5 in small): no tile is ever abandoned, so after
+    two batches the search switches to the dot-product form; on a random walk with a planted
+    anomaly the tiles are abandoned early and it stays with the direct form."""
+    x = np.random.default_rng(5).random(40000).astype(np.float32)
+    ctx.prepare(x, 128, 8, 4)
+    pos, dist = ctx.search(2)
+    st = ctx.stats()
+    assert st["scan_kernel_dot_launches"] > 0 and 0 < st["scan_kernel_dot_terms"] <= st["scan_kernel_terms"]
+    want = chk.topk(x, 128, 8, 4, 2)
+    assert_discords_match(chk, x, 128, pos, dist, want)
+    ctx.set_option("dot_form", 0)
+    try:
+        again = ctx.search(2)
+        assert ctx.stats()["scan_kernel_dot_launches"] == 0
+    finally:
+        ctx.set_option("dot_form", 1)
+    assert again[0] == pos
+    np.testing.assert_allclose(again[1], dist, rtol=1e-9)  # both decided in float64
+
+    y = planted_walk(3, 40000, 128)
+    ctx.prepare(y, 128, 4, 4)
+    ctx.search(1)
+    assert ctx.stats()["scan_kernel_dot_launches"] == 0
 
 
 def test_smallest_feasible_and_k_beyond_the_series(ctx, chk):
