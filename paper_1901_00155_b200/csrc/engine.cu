@@ -162,8 +162,9 @@ struct tsdd_cuda_ctx {
   uint32_t rows = 0, stride = 0, rows_padded = 0;
   DeviceArray<float> series_f32;
   DeviceArray<double> series, mean, inv_sigma;
-  DeviceArray<float> matrix, lb_means, lb_boxes, row_norms;
-  bool norms_ready = false;  // row_norms holds the norms of the prepared matrix
+  DeviceArray<float> matrix, lb_means, lb_boxes, row_norms, matrix_sorted;
+  bool norms_ready = false;   // row_norms holds the norms of the prepared matrix
+  bool sorted_ready = false;  // matrix_sorted holds the prepared matrix in the hash-sorted order
   DeviceArray<uint32_t> hash0, freq, offsets, slot_bucket, scalars, slot_of_row;
   DeviceArray<uint32_t> sort_buf[4], order_buf[4];
   uint32_t *sorted_hash = nullptr, *sorted_row = nullptr, *order = nullptr, *sorted_freq = nullptr;
@@ -235,6 +236,7 @@ struct tsdd_cuda_ctx {
     s.margin = discard_margin();
     s.margin_abs = dot_used ? static_cast<float>(2.0 * dot_error()) : 0.f;
     s.row_norms = norms_ready ? row_norms.ptr : nullptr;
+    s.rows_sorted = sorted_ready ? matrix_sorted.ptr : nullptr;
     s.lb_means = (opt_lower_bound && lb_active) ? lb_means.ptr : nullptr;
     s.lb_boxes = lb_boxes.ptr;
     s.lb_scale = static_cast<float>(stride / kLbSegments);
@@ -421,6 +423,7 @@ void reset_stats(tsdd_cuda_ctx* ctx) {
   std::memset(&ctx->stats, 0, sizeof(ctx->stats));
   ctx->prepared = false;
   ctx->norms_ready = false;
+  ctx->sorted_ready = false;
 }
 
 template <typename T>
@@ -566,10 +569,10 @@ std::vector<Segment> plan_segments(const tsdd_cuda_ctx* ctx, bool pruning) {
     const uint32_t window_limit = slot_tiles / 8;
     double size = std::max<double>(ctx->opt_window_first, kTileRows);
     uint32_t at = 0;
-    // Dot form = a search whose tiles are never abandoned (noise-like rows): a word's
-    // neighbourhood is then hardly better than any other rows, and the windows' rows are met
-    // again by the covering scan — two rounds of them are enough.
-    const int window_rounds = ctx->dot_now ? std::min(ctx->opt_window_rounds, ctx->opt_dot_window_rounds) : ctx->opt_window_rounds;
+    // Dot form without the hash-sorted copy of the matrix (memory was short): window tiles are
+    // then fed by per-row copies, which the dot form outruns — two rounds of them are enough.
+    const int window_rounds = (ctx->dot_now && !ctx->sorted_ready) ? std::min(ctx->opt_window_rounds, ctx->opt_dot_window_rounds)
+                                                                      : ctx->opt_window_rounds;
     for (int r = 0; r < window_rounds && at < window_limit; ++r) {
       const uint32_t upto = std::min<uint64_t>(window_limit, at + static_cast<uint64_t>(size) / tile);
       plan.push_back({true, at, upto});
@@ -707,6 +710,19 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
             ctx->row_norms.alloc(static_cast<size_t>(ctx->rows) + 1);
             ctx->stats.kernel_launches += launch_row_norms(ctx->matrix.ptr, ctx->rows + 1, ctx->stride, ctx->row_norms.ptr, st);
             ctx->norms_ready = true;
+          }
+          if (ctx->dot_now && !ctx->sorted_ready && ctx->opt_tensor_map && ctx->opt_window_rounds > 0) {
+            // a second copy of the matrix, in the hash-sorted order, so that window tiles are
+            // consecutive rows too (tensor-map loads); skipped when memory is short
+            const size_t floats = static_cast<size_t>(ctx->rows_padded) * ctx->stride;
+            size_t free_b = 0, total_b = 0;
+            CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
+            if (ctx->matrix_sorted.count >= floats || free_b > floats * sizeof(float) + (size_t{2} << 30)) {
+              ctx->matrix_sorted.alloc(floats);
+              ctx->stats.kernel_launches += launch_permute_rows(ctx->matrix.ptr, ctx->sorted_row, ctx->rows,
+                                                                ctx->rows_padded, ctx->stride, ctx->matrix_sorted.ptr, st);
+              ctx->sorted_ready = true;
+            }
           }
           s = ctx->state();
         }

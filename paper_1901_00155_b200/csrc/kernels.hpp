@@ -85,6 +85,7 @@ struct SearchState {
   float margin;             // 1 + delta of the discard test (common.cuh: dead_bound)
   float margin_abs;         // 0, or twice the absolute error bound of dot-form distances once a search uses them
   const float* row_norms;   // N + 1 squared norms of the float32 rows (dot form), or nullptr
+  const float* rows_sorted; // the matrix in the hash-sorted order (tensor-map loads of window tiles), or nullptr
   const float* lb_means;    // N x kLbSegments segment means, or nullptr: no tile filter
   const float* lb_boxes;    // their bounding boxes per kLbBoxRows rows
   float lb_scale;           // columns per segment (stride / kLbSegments)
@@ -152,6 +153,8 @@ bool scan_last_launch_was_dot();
 
 // Squared norms of the float32 rows (rows 0 .. n_rows; row n_rows is the zero row), for the
 // dot-product form d^2 = |a|^2 + |b|^2 - 2 a.b of the warp-specialised tile kernel.
+int launch_permute_rows(const float* d_rows, const uint32_t* d_sorted_row, uint32_t n_rows, uint32_t rows_padded,
+                        uint32_t stride, float* d_out, cudaStream_t stream);
 int launch_row_norms(const float* d_rows, uint32_t n_rows_plus_one, uint32_t stride, float* d_norms,
                      cudaStream_t stream);
 

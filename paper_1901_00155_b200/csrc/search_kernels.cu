@@ -1025,6 +1025,9 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
           const uint32_t z0 = row >= s.n - 1 ? row - (s.n - 1) : 0, z1 = row + s.n;
           const uint32_t o0 = max(slot0, z0), o1 = min(slot0 + valid, z1);
           overlap = o1 > o0 ? o1 - o0 : 0;
+        } else if constexpr (kTma && kDot) {
+          // the consumers count the self-match pairs of a window tile in their epilogue (the dot
+          // form completes every tile it starts) and take them off the counter at the end
         } else {
           const uint4* jr = reinterpret_cast<const uint4*>(meta.jrow);
 #pragma unroll 4
@@ -1119,6 +1122,7 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
   uint32_t seq = 0, cur = kTagDone, m = 0, chunks_done = 0;
   bool released = true, warp_done = false;
   unsigned long long chunks_total = 0, abandoned_total = 0;
+  uint32_t overlap_total = 0;
 #pragma unroll 1
   for (;;) {
     const uint32_t st = seq % kStagesWs, round = seq / kStagesWs;
@@ -1205,6 +1209,20 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
 #pragma unroll
           for (int w = 0; w < kW; ++w) bn[w] = meta.nnorm[tx + kTx * w];
         }
+        if constexpr (kTma && kDot) {
+          if (window) {  // self-match pairs among this thread's 8 x 8 (see the producer's `calls`)
+            uint32_t jr[kW];
+#pragma unroll
+            for (int w = 0; w < kW; ++w) jr[w] = meta.jrow[tx + kTx * w];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+              if (thr[u] < 0.f) continue;
+              const uint32_t row = sh.cand[cand0_of_thread + kCandStep * u];
+#pragma unroll
+              for (int w = 0; w < kW; ++w) overlap_total += gap_u32(row, jr[w]) < s.n ? 1u : 0u;
+            }
+          }
+        }
         const float d_floor = 0.5f * s.margin_abs;
         auto dist = [&](int u, int w) -> float {
           if constexpr (kDot) return fmaxf(fmaf(2.f, acc.get(u, w), cn[u] + bn[w]), d_floor);
@@ -1268,6 +1286,12 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
       if constexpr (kDot) atomicAdd(&s.counters->dot_terms, terms);
     }
     if (abandoned_total) atomicAdd(&s.counters->abandoned, abandoned_total);
+  }
+  if constexpr (kTma && kDot) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) overlap_total += __shfl_xor_sync(0xFFFFFFFFu, overlap_total, d);
+    if (lane == 0 && overlap_total)  // calls -= overlap (the producer counted live x valid)
+      atomicAdd(&s.counters->calls, ~static_cast<unsigned long long>(overlap_total) + 1ull);
   }
 }
 
@@ -1442,8 +1466,10 @@ ScanChoice choose_scan_kernel(const SearchState& s, uint32_t live_upper_bound, b
   // and the batch still fills 128-candidate tiles; k_scan_tiles otherwise
   c.ws = g_scan_variant == 2 ||
          (g_scan_variant == 0 && g_packed_default && !g_wide_tile && !c.lb && live_upper_bound > 64);
-  c.tma = c.ws && !window && g_tma_enabled && tensor_map_encoder() != nullptr;
   c.dot = c.ws && dot_form && s.row_norms != nullptr;
+  // window launches read scattered rows unless the engine keeps a copy of the matrix in the
+  // hash-sorted order (it does once a search runs in the dot form)
+  c.tma = c.ws && g_tma_enabled && tensor_map_encoder() != nullptr && (!window || (c.dot && s.rows_sorted != nullptr));
   return c;
 }
 
@@ -1474,7 +1500,8 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
     bool tma = choice.tma;
     if (tma)
       tma = make_row_map(&map_a, d_batch_matrix, static_cast<uint64_t>(cand_tiles) * kTileRows, s.stride) &&
-            make_row_map(&map_b, s.rows, static_cast<uint64_t>(slot_tiles_of(s.n_rows + 1)) * kTileRows, s.stride);
+            make_row_map(&map_b, d_nbr_index != nullptr ? s.rows_sorted : s.rows,
+                         static_cast<uint64_t>(slot_tiles_of(s.n_rows + 1)) * kTileRows, s.stride);
     if (choice.tma && !tma) {  // the gather already used the tensor-map row order: no way back
       g_launch_error = "cuTensorMapEncodeTiled failed";
       return 0;
@@ -1531,6 +1558,28 @@ const char* scan_launch_error() {
   const char* e = g_launch_error;
   g_launch_error = nullptr;
   return e;
+}
+
+// The matrix in the hash-sorted order: slot p holds row sorted_row[p]; slots from n_rows on are zero.
+__global__ void __launch_bounds__(256)
+k_permute_rows(const float* __restrict__ rows, const uint32_t* __restrict__ sorted_row, uint32_t n_rows,
+               uint32_t rows_padded, uint32_t stride, float* __restrict__ out) {
+  const uint32_t slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (slot >= rows_padded) return;
+  float4* dst = reinterpret_cast<float4*>(out + static_cast<size_t>(slot) * stride);
+  if (slot < n_rows) {
+    const float4* src = reinterpret_cast<const float4*>(rows + static_cast<size_t>(sorted_row[slot]) * stride);
+    for (uint32_t c = lane; c < stride / 4; c += 32) dst[c] = __ldg(src + c);
+  } else {
+    for (uint32_t c = lane; c < stride / 4; c += 32) dst[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+int launch_permute_rows(const float* d_rows, const uint32_t* d_sorted_row, uint32_t n_rows, uint32_t rows_padded,
+                        uint32_t stride, float* d_out, cudaStream_t stream) {
+  k_permute_rows<<<blocks_for(static_cast<size_t>(rows_padded) * 32, 256), 256, 0, stream>>>(
+      d_rows, d_sorted_row, n_rows, rows_padded, stride, d_out);
+  return 1;
 }
 
 int launch_row_norms(const float* d_rows, uint32_t n_rows_plus_one, uint32_t stride, float* d_norms,

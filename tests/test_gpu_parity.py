@@ -479,6 +479,9 @@ def test_randomised_small_cases_match_the_oracle(ctx, chk, seed, kind, n):
     assert_discords_match(chk, x, n, pos, dist, want)
 
 
+_DOT_LAUNCHES = []
+
+
 @pytest.mark.parametrize("seed,kind,n", FUZZ, ids=[f"{k}-n{n}" for _, k, n in FUZZ])
 def test_dot_product_form_matches_the_oracle(ctx, chk, seed, kind, n):
     """The warp-specialised kernel's one-FFMA-per-term form, forced on from the first launch
@@ -491,15 +494,21 @@ def test_dot_product_form_matches_the_oracle(ctx, chk, seed, kind, n):
     k = int(rng.integers(1, 4))
     x = _fuzz_series(rng, kind, m)
     ctx.set_option("dot_form", 2)
+    ctx.set_option("lower_bound", 0)  # (covering scans on the warp-specialised kernel as well)
     try:
         ctx.prepare(x, n, w, a)
         pos, dist = ctx.search(k)
-        used = ctx.stats()["scan_kernel_dot_launches"]
+        _DOT_LAUNCHES.append(ctx.stats()["scan_kernel_dot_launches"])
     finally:
         ctx.set_option("dot_form", 1)
+        ctx.set_option("lower_bound", 1)
     want = chk.topk(x, n, w, a, k)
     assert_discords_match(chk, x, n, pos, dist, want)
-    assert used > 0 or m - n + 1 <= 64 * 4  # (tiny batches run on the 64-candidate tile kernel)
+
+
+def test_dot_product_form_cases_did_run_the_dot_kernel():
+    # batches that have shrunk to <= 64 live candidates use the 64-candidate tile kernel instead
+    assert len(_DOT_LAUNCHES) == len(FUZZ) and sum(1 for v in _DOT_LAUNCHES if v > 0) >= len(FUZZ) * 3 // 4, _DOT_LAUNCHES
 
 
 def test_dot_product_form_is_chosen_where_tiles_are_never_abandoned(ctx, chk):
