@@ -103,6 +103,13 @@ int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream);
  * computes d^2 as |a|^2 + |b|^2 - 2 a.b, one FFMA per term, with the discard band widened by
  * its absolute error bound: 0 never; 1 once a search has found that tiles are not abandoned
  * early anyway and the best-so-far dwarfs the bound; 2 from the first launch),
+ * "tensor_map" (0/1: the warp-specialised kernel loads the tiles of covering scans — and, in
+ * the dot-product form, of window rounds, from a copy of the matrix kept in the hash-sorted
+ * order — as cp.async.bulk.tensor boxes instead of one bulk copy per row),
+ * "dot_window_rounds" (window rounds of a dot-form batch whose window tiles load that way),
+ * "seed_rows" (before the first scan, the best-so-far is seeded with the greatest LOWER bound of
+ * a nearest-neighbour distance among this many first entries of the rarity order, from the
+ * segment-mean boxes; 0 = start from zero as the reference does),
  * "time_kernels" (0/1: CUDA events around every tile-kernel launch).
  * Unknown name -> TSDD_ERR_PARAMETER.  None of them changes the result.     */
 int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value);

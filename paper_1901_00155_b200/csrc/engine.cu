@@ -133,12 +133,12 @@ struct tsdd_cuda_ctx {
 
   // tunables (tsdd_cuda_set_option)
   uint32_t opt_batch = 65536;
-  uint32_t opt_first_batch = 256;
+  uint32_t opt_first_batch = 128;
   uint32_t opt_batch_growth = 8;
   int opt_rounds = 64;            // upper limit on neighbour ranges per batch
-  uint32_t opt_first_range = 2048;  // rows in the first range
+  uint32_t opt_first_range = 8192;  // rows in the first range
   double opt_growth = 1.5;          // each range is this much larger than the one before
-  int opt_window_rounds = 4;        // same-word-neighbourhood rounds before the covering scan
+  int opt_window_rounds = 2;        // same-word-neighbourhood rounds before the covering scan
   uint32_t opt_window_first = 2048; // slots in the first of them
   double opt_window_growth = 3.0;
   bool opt_rotate = true;           // each batch starts its covering scan at a different row
@@ -152,9 +152,10 @@ struct tsdd_cuda_ctx {
   bool opt_time_kernels = true;
   bool opt_share_bounds = true;
   bool opt_lower_bound = true;      // tile filter by segment-mean lower bounds in the covering scan
+  uint32_t opt_seed_rows = 4096;    // rows whose lower bounds seed the best-so-far of the first pass (0 = none)
   bool opt_tensor_map = true;       // covering scans of the ws kernel load tiles as TMA boxes
   int opt_dot = 1;
-  int opt_dot_window_rounds = 2;    // window rounds of a batch that runs in the dot-product form                  // dot-product form of the ws kernel: 0 never, 1 when it pays, 2 always
+  int opt_dot_window_rounds = 4;    // ... of a batch in the dot-product form whose window tiles load as tensor-map boxes                  // dot-product form of the ws kernel: 0 never, 1 when it pays, 2 always
 
   // prepared series
   bool prepared = false;
@@ -177,7 +178,7 @@ struct tsdd_cuda_ctx {
   DeviceArray<uint32_t> flags, batch_rows, batch_alt, batch_slots, batch_slots_alt, sel;
   DeviceArray<float> batch_matrix;
   DeviceArray<double> zrow;
-  DeviceArray<uint32_t> finalists;
+  DeviceArray<uint32_t> finalists, seed_lb;
   DeviceArray<unsigned long long> nn_bits;
   uint32_t batch_capacity = 0;
   bool lb_active = true;    // the lower-bound filter is still worth its (small) cost in this search
@@ -569,10 +570,11 @@ std::vector<Segment> plan_segments(const tsdd_cuda_ctx* ctx, bool pruning) {
     const uint32_t window_limit = slot_tiles / 8;
     double size = std::max<double>(ctx->opt_window_first, kTileRows);
     uint32_t at = 0;
-    // Dot form without the hash-sorted copy of the matrix (memory was short): window tiles are
-    // then fed by per-row copies, which the dot form outruns — two rounds of them are enough.
-    const int window_rounds = (ctx->dot_now && !ctx->sorted_ready) ? std::min(ctx->opt_window_rounds, ctx->opt_dot_window_rounds)
-                                                                      : ctx->opt_window_rounds;
+    // Window tiles of a dot-form batch stream at the full rate of the covering scan (tensor-map
+    // boxes from the hash-sorted copy of the matrix), and on the noise-like inputs that run in
+    // the dot form more rounds pay; the direct form feeds them with per-row copies.
+    const int window_rounds = (ctx->dot_now && ctx->sorted_ready) ? std::max(ctx->opt_window_rounds, ctx->opt_dot_window_rounds)
+                                                                  : ctx->opt_window_rounds;
     for (int r = 0; r < window_rounds && at < window_limit; ++r) {
       const uint32_t upto = std::min<uint64_t>(window_limit, at + static_cast<uint64_t>(size) / tile);
       plan.push_back({true, at, upto});
@@ -711,7 +713,8 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
             ctx->stats.kernel_launches += launch_row_norms(ctx->matrix.ptr, ctx->rows + 1, ctx->stride, ctx->row_norms.ptr, st);
             ctx->norms_ready = true;
           }
-          if (ctx->dot_now && !ctx->sorted_ready && ctx->opt_tensor_map && ctx->opt_window_rounds > 0) {
+          if (ctx->dot_now && !ctx->sorted_ready && ctx->opt_tensor_map && ctx->opt_window_rounds > 0 &&
+              ctx->opt_dot_window_rounds > 0) {
             // a second copy of the matrix, in the hash-sorted order, so that window tiles are
             // consecutive rows too (tensor-map loads); skipped when memory is short
             const size_t floats = static_cast<size_t>(ctx->rows_padded) * ctx->stride;
@@ -800,7 +803,15 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
 
   CUDA_OK(cudaEventRecord(ctx->ev_a, st));
   ctx->stats.kernel_launches += launch_reset_search(s, st);
-  if (pruning)
+  bool seeded = false;
+  if (pruning && ctx->opt_lower_bound && ctx->opt_seed_rows > 0 && s.lb_means != nullptr) {
+    // (the seed costs seed_rows x N / 16 box tests: keep it at 1/64 of the rows on small inputs)
+    const uint32_t seed_rows = std::min(ctx->opt_seed_rows, std::max(256u, ctx->rows / 64));
+    ctx->seed_lb.alloc(seed_rows);
+    ctx->stats.kernel_launches += launch_seed_lower_bound(s, ctx->order, seed_rows, ctx->seed_lb.ptr, st);
+    seeded = true;
+  }
+  if (pruning)  // (after the seed: a row whose first mates already put it below the seed stops there)
     ctx->stats.kernel_launches +=
         launch_bucket_mates(s, ctx->sorted_row, ctx->slot_bucket.ptr, ctx->offsets.ptr, ctx->opt_mates, st);
 
@@ -809,7 +820,14 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
       CUDA_OK(cudaMemsetAsync(ctx->best.ptr, 0, sizeof(uint64_t), st));
       ctx->stats.kernel_launches += launch_seed_best(s, st);
     }
-    const uint64_t key = run_pass(ctx, pruning, pass);
+    uint64_t key = run_pass(ctx, pruning, pass);
+    if (pass == 0 && seeded && key != 0 && best_key_row(key) == 0xFFFFFFFFu) {
+      // no candidate rose above the seeded bound (it can only happen through float32 rounding at
+      // an exact tie): drop the seed and let the pass finish on its own best-so-far
+      CUDA_OK(cudaMemsetAsync(ctx->best.ptr, 0, sizeof(uint64_t), st));
+      ctx->stats.kernel_launches += launch_seed_best(s, st);
+      key = run_pass(ctx, pruning, pass);
+    }
     if (key == 0 || key_bits(key) == 0) {  // nothing beat 0: the reference's fallback (discovery.cpp:90-93)
       positions[pass] = 1;
       distances[pass] = 0.0;
@@ -1048,6 +1066,9 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
       ctx->opt_wide_tile = value != 0;
     } else if (key == "lower_bound") {
       ctx->opt_lower_bound = value != 0;
+    } else if (key == "seed_rows") {
+      if (value < 0 || value > 1048576) fail(TSDD_ERR_PARAMETER, "seed_rows must be in 0..1048576");
+      ctx->opt_seed_rows = static_cast<uint32_t>(value);
     } else if (key == "dot_window_rounds") {
       if (value < 0 || value > 64) fail(TSDD_ERR_PARAMETER, "dot_window_rounds must be in 0..64");
       ctx->opt_dot_window_rounds = static_cast<int>(value);

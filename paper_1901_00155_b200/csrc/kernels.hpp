@@ -162,6 +162,11 @@ int launch_row_norms(const float* d_rows, uint32_t n_rows_plus_one, uint32_t str
 int launch_finalize_batch(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,
                           uint32_t capacity, bool pruning, cudaStream_t stream);
 
+// A valid best-so-far before the first scan: the greatest lower bound of a nearest-neighbour
+// distance among the first seed_rows entries of the rarity order, from the segment-mean
+// boxes (needs s.lb_means / s.lb_boxes).  d_seed_lb: seed_rows words of scratch.
+int launch_seed_lower_bound(SearchState s, const uint32_t* d_order, uint32_t seed_rows, uint32_t* d_seed_lb,
+                            cudaStream_t stream);
 // best = max over exact, allowed rows (start of a top-k pass).
 int launch_seed_best(SearchState s, cudaStream_t stream);
 int launch_exclude_zone(SearchState s, uint32_t row, cudaStream_t stream);

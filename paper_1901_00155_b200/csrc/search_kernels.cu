@@ -78,6 +78,80 @@ __global__ void __launch_bounds__(256) k_seed_best(SearchState s) {
   if ((threadIdx.x & 31) == 0 && mine) atomicMax(as_ull(s.best), static_cast<unsigned long long>(mine));
 }
 
+// ------------------------------------------------------------------ a best-so-far before the first scan
+// The first batch of a search has no best-so-far to discard with until one of its candidates
+// has met every row.  The lower-bound summaries give one for free: for a row i,
+//   L(i) = min over 16-row boxes u that hold at least one non-self match of i of
+//          (stride / 16) * sum_k dist(mean_k(i), [lo_k(u), hi_k(u)])^2
+// is a lower bound of i's nearest-neighbour distance (prep_kernels.cu: Cauchy-Schwarz per
+// segment), and the discord's distance is >= nn(i) >= L(i) for EVERY i — so max_i L(i) over
+// any set of rows (here the first entries of the rarity order) is a valid, if stale,
+// best-so-far (discovery.hpp:34-36: a smaller best-so-far prunes less, never more).
+// It is installed with the row field of the key empty: any real candidate wins a tie.
+constexpr int kSeedUnits = 128;  // boxes staged per block
+__global__ void __launch_bounds__(256)
+k_seed_lower_bound(SearchState s, const uint32_t* __restrict__ order, uint32_t seed_rows,
+                   uint32_t* __restrict__ seed_lb) {
+  __shared__ float4 s_box[kSeedUnits * 2 * kLbSegments / 4];
+  const uint32_t units = (s.n_rows + kLbBoxRows - 1) / kLbBoxRows;
+  const uint32_t unit0 = blockIdx.x * kSeedUnits;
+  const uint32_t n_units = min(static_cast<uint32_t>(kSeedUnits), units - unit0);
+  const float4* src = reinterpret_cast<const float4*>(s.lb_boxes + static_cast<size_t>(unit0) * 2 * kLbSegments);
+  for (uint32_t t = threadIdx.x; t < n_units * 2 * kLbSegments / 4; t += blockDim.x) s_box[t] = __ldg(src + t);
+  __syncthreads();
+  const uint32_t e = blockIdx.y * blockDim.x + threadIdx.x;  // one seed row per thread
+  if (e < seed_rows) {
+    const uint32_t row = order[e];
+    float mine[kLbSegments];
+    const float4* pm = reinterpret_cast<const float4*>(s.lb_means + static_cast<size_t>(row) * kLbSegments);
+#pragma unroll
+    for (int q = 0; q < kLbSegments / 4; ++q) {
+      const float4 v = __ldg(pm + q);
+      mine[4 * q] = v.x, mine[4 * q + 1] = v.y, mine[4 * q + 2] = v.z, mine[4 * q + 3] = v.w;
+    }
+    float best = __uint_as_float(kInfBits);
+    for (uint32_t u = 0; u < n_units; ++u) {
+      // a box all of whose rows are self matches of `row` holds no neighbour of it
+      const uint32_t r0 = (unit0 + u) * kLbBoxRows, r1 = min(r0 + kLbBoxRows, s.n_rows) - 1;
+      if (gap_u32(row, r0) < s.n && gap_u32(row, r1) < s.n) continue;
+      const float4* pb = s_box + u * (2 * kLbSegments / 4);
+      float lb = 0.f;
+#pragma unroll
+      for (int q = 0; q < kLbSegments / 4; ++q) {
+        const float4 lo = pb[q], hi = pb[kLbSegments / 4 + q];
+        float g;
+        g = fmaxf(fmaxf(lo.x - mine[4 * q], mine[4 * q] - hi.x), 0.f), lb = fmaf(g, g, lb);
+        g = fmaxf(fmaxf(lo.y - mine[4 * q + 1], mine[4 * q + 1] - hi.y), 0.f), lb = fmaf(g, g, lb);
+        g = fmaxf(fmaxf(lo.z - mine[4 * q + 2], mine[4 * q + 2] - hi.z), 0.f), lb = fmaf(g, g, lb);
+        g = fmaxf(fmaxf(lo.w - mine[4 * q + 3], mine[4 * q + 3] - hi.w), 0.f), lb = fmaf(g, g, lb);
+      }
+      best = fminf(best, lb);
+    }
+    if (best != __uint_as_float(kInfBits)) atomicMin(seed_lb + e, __float_as_uint(best));  // >= 0: bits order like floats
+  }
+}
+
+__global__ void __launch_bounds__(256)
+k_install_seed(SearchState s, const uint32_t* __restrict__ seed_lb, uint32_t seed_rows) {
+  __shared__ float s_max[8];
+  float mine = 0.f;
+  for (uint32_t e = threadIdx.x; e < seed_rows; e += blockDim.x) {
+    const uint32_t bits = seed_lb[e];
+    if (bits < 0x7F000000u) mine = fmaxf(mine, __uint_as_float(bits));  // (unset slots hold 0x7F7F7F7F)
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) mine = fmaxf(mine, __shfl_xor_sync(0xFFFFFFFFu, mine, d));
+  if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = mine;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) mine = fmaxf(mine, s_max[w]);
+    // 0.5 % below the bound: the means and boxes are float32 (the tile filter allows 0.1 %)
+    const float seed = mine * s.lb_scale * 0.995f;
+    if (seed > 0.f)
+      atomicMax(as_ull(s.best), static_cast<unsigned long long>(best_key(__float_as_uint(seed), 0xFFFFFFFFu)));
+  }
+}
+
 // ------------------------------------------------------------------ same-word neighbours
 // One warp per slot of the hash-sorted order.  The row is measured against up
 // to `mates` rows spread evenly over its own bucket (positions at least n
@@ -105,7 +179,12 @@ k_bucket_mates(SearchState s, const uint32_t* __restrict__ sorted_row,
     tries = len - 1;
   }
   unsigned long long calls = 0, terms = 0;
+  // With a best-so-far already in place (k_install_seed), a row stops as soon as one of its
+  // mates has pushed its bound below it: it is dead, more mates would change nothing.
+  const uint64_t best = *s.best;
+  float bound_i = __uint_as_float(kInfBits);
   for (uint32_t q = 1; q <= tries; ++q) {
+    if (dead_bound(bound_i, best, s.margin, s.margin_abs)) break;
     const uint32_t other = b0 + (slot - b0 + q * step) % len;
     const uint32_t row_j = sorted_row[other];
     if (gap_u32(row_i, row_j) < s.n) continue;
@@ -121,6 +200,7 @@ k_bucket_mates(SearchState s, const uint32_t* __restrict__ sorted_row,
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, d);
+    bound_i = fminf(bound_i, sum);
     if (lane == 0) {
       const uint32_t bits = __float_as_uint(sum);
       atomicMin(as_ull(s.nn + row_i), static_cast<unsigned long long>(nn_key(bits, row_j)));
@@ -798,6 +878,9 @@ k_scan_tiles(SearchState s, ScanArgs a) {
 // searches on which it has been switched off — and k_scan_tiles elsewhere.
 namespace ws {
 
+#ifndef TSDD_WS_LANES48
+#define TSDD_WS_LANES48 1
+#endif
 constexpr int kStagesWs = 3;
 constexpr int kNbrWs = 128;
 constexpr int kPitch = kChunk * 4 + 16;
@@ -1110,7 +1193,15 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
 
   // ================================================================== consumer warpgroups
   asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+#if TSDD_WS_LANES48
+  // A warp is 4 thread rows x 8 thread columns: the 16 lanes of a half-warp then read only 8
+  // distinct neighbour rows (128 bytes, one shared-memory wavefront) per LDS.128 instead of 16.
+  const uint32_t tx = (lane & 7u) | ((warp & 1u) << 3), ty = (lane >> 3) | ((warp >> 1) << 2);
+  constexpr int kTxLanes = 8;  // thread columns inside one warp
+#else
   const uint32_t tx = tid % kTx, ty = tid / kTx;
+  constexpr int kTxLanes = kTx;
+#endif
   // Candidate row of pair-row u of thread row ty: warp w (thread rows 2w, 2w + 1) owns the 16
   // CONTIGUOUS rows 16w .. 16w + 15 of the word-sorted batch (they want, and abandon, the same
   // tiles); the two rows a warp reads at once are adjacent, i.e. in different bank groups at
@@ -1261,13 +1352,14 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
             }
             uint32_t g_min = d_min;
 #pragma unroll
-            for (int d = kTx / 2; d > 0; d >>= 1) g_min = min(g_min, __shfl_xor_sync(0xFFFFFFFFu, g_min, d));
+            for (int d = kTxLanes / 2; d > 0; d >>= 1) g_min = min(g_min, __shfl_xor_sync(0xFFFFFFFFu, g_min, d));
             uint32_t g_j = d_min == g_min ? j_min : 0xFFFFFFFFu;
 #pragma unroll
-            for (int d = kTx / 2; d > 0; d >>= 1) g_j = min(g_j, __shfl_xor_sync(0xFFFFFFFFu, g_j, d));
-            if (tx == 0 && g_j != 0xFFFFFFFFu) {
+            for (int d = kTxLanes / 2; d > 0; d >>= 1) g_j = min(g_j, __shfl_xor_sync(0xFFFFFFFFu, g_j, d));
+            if ((tx & (kTxLanes - 1)) == 0 && g_j != 0xFFFFFFFFu) {
               atomicMin(as_ull(s.nn + row), static_cast<unsigned long long>(nn_key(g_min, g_j)));
-              sh.loc[cand0_of_thread + kCandStep * u] = fminf(sh.loc[cand0_of_thread + kCandStep * u], __uint_as_float(g_min));
+              // (squared distances are >= 0: their bits order like the floats; two warps may share a candidate)
+              atomicMin(reinterpret_cast<uint32_t*>(&sh.loc[cand0_of_thread + kCandStep * u]), g_min);
             }
           }
         }
@@ -1593,6 +1685,18 @@ int launch_finalize_batch(SearchState s, const uint32_t* d_batch_rows, const uin
                           uint32_t capacity, bool pruning, cudaStream_t stream) {
   k_finalize_batch<<<blocks_for(capacity, 256), 256, 0, stream>>>(s, d_batch_rows, d_sel, pruning ? 1 : 0);
   return 1;
+}
+
+int launch_seed_lower_bound(SearchState s, const uint32_t* d_order, uint32_t seed_rows, uint32_t* d_seed_lb,
+                            cudaStream_t stream) {
+  if (s.lb_means == nullptr || seed_rows == 0) return 0;
+  seed_rows = seed_rows < s.n_rows ? seed_rows : s.n_rows;
+  cudaMemsetAsync(d_seed_lb, 0x7F, seed_rows * sizeof(uint32_t), stream);  // 0x7F7F7F7F: above every bound
+  const uint32_t units = (s.n_rows + kLbBoxRows - 1) / kLbBoxRows;
+  const dim3 grid((units + kSeedUnits - 1) / kSeedUnits, (seed_rows + 255) / 256);
+  k_seed_lower_bound<<<grid, 256, 0, stream>>>(s, d_order, seed_rows, d_seed_lb);
+  k_install_seed<<<1, 256, 0, stream>>>(s, d_seed_lb, seed_rows);
+  return 2;
 }
 
 int launch_seed_best(SearchState s, cudaStream_t stream) {

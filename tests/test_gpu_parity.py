@@ -182,15 +182,17 @@ def test_search_is_repeatable_and_independent_of_tunables(ctx):
                         ("symmetric", 0), ("packed", 0), ("first_batch", 4096), ("wide_tile", 1), ("kernel", 2), ("kernel", 1),
                         ("window_rounds", 0), ("rotate", 0), ("growth", 3.0), ("first_range", 128),
                         ("lower_bound", 0), ("margin_delta", 1e-3), ("batch_growth", 2), ("dot_form", 2),
-                        ("dot_form", 0)]:
+                        ("dot_form", 0), ("seed_rows", 0), ("tensor_map", 0), ("dot_window_rounds", 0),
+                        ("window_rounds", 4)]:
         ctx.set_option(name, value)
         again = ctx.search(3)
         assert again[0] == base[0], name
         np.testing.assert_allclose(again[1], base[1], rtol=1e-6, err_msg=name)
     for name, value in [("batch", 65536), ("rounds", 64), ("bucket_mates", 8), ("symmetric", 1),
-                        ("packed", 1), ("first_batch", 256), ("wide_tile", 0), ("kernel", 0),
-                        ("window_rounds", 4), ("rotate", 1), ("growth", 1.5), ("first_range", 2048),
-                        ("lower_bound", 1), ("margin_delta", -1), ("batch_growth", 8), ("dot_form", 1)]:
+                        ("packed", 1), ("first_batch", 128), ("wide_tile", 0), ("kernel", 0),
+                        ("window_rounds", 2), ("rotate", 1), ("growth", 1.5), ("first_range", 8192),
+                        ("lower_bound", 1), ("margin_delta", -1), ("batch_growth", 8), ("dot_form", 1),
+                        ("seed_rows", 4096), ("tensor_map", 1), ("dot_window_rounds", 4)]:
         ctx.set_option(name, value)
 
 
@@ -535,6 +537,27 @@ def test_dot_product_form_is_chosen_where_tiles_are_never_abandoned(ctx, chk):
     ctx.prepare(y, 128, 4, 4)
     ctx.search(1)
     assert ctx.stats()["scan_kernel_dot_launches"] == 0
+
+
+def test_seeded_best_so_far_saves_work_and_keeps_the_result(ctx, chk):
+    """The first pass starts from the greatest lower bound of a nearest-neighbour distance among
+    the rarest rows (segment-mean boxes) instead of zero: fewer pair distances, same discords."""
+    x, _ = W.series(2)
+    x = x[:120000]
+    ctx.prepare(x, 256, 8, 4)
+    ctx.set_option("seed_rows", 0)
+    try:
+        plain = ctx.search(3)
+        plain_calls = ctx.stats()["calls"]
+    finally:
+        ctx.set_option("seed_rows", 4096)
+    seeded = ctx.search(3)
+    seeded_calls = ctx.stats()["calls"]
+    assert seeded[0] == plain[0]
+    np.testing.assert_allclose(seeded[1], plain[1], rtol=1e-9)
+    assert seeded_calls < plain_calls
+    want = chk.topk(x, 256, 8, 4, 3)
+    assert_discords_match(chk, x, 256, seeded[0], seeded[1], want)
 
 
 def test_smallest_feasible_and_k_beyond_the_series(ctx, chk):
