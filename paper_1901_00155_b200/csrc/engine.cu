@@ -869,7 +869,8 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
         CUDA_OK(cudaMemcpyAsync(ctx->nn_bits.ptr, &bits, sizeof(bits), cudaMemcpyHostToDevice, st));
         ctx->stats.kernel_launches +=
             launch_exact_nn(ctx->series.ptr, ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->rows, static_cast<uint32_t>(ctx->n),
-                            cand, ctx->zrow.ptr, ctx->nn_bits.ptr, st);
+                            cand, ctx->zrow.ptr, ctx->opt_lower_bound ? ctx->lb_means.ptr : nullptr,
+                            static_cast<float>(ctx->stride / kLbSegments), ctx->nn_bits.ptr, st);
         CUDA_OK(cudaMemcpyAsync(&bits, ctx->nn_bits.ptr, sizeof(bits), cudaMemcpyDeviceToHost, st));
         sync_stream(ctx);
         double exact;

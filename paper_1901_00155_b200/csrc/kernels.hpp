@@ -180,7 +180,7 @@ int launch_collect_finalists(SearchState s, uint32_t* d_list, uint32_t cap, uint
 // straight from the series: d_out_bits[0] = bits of the minimum (must be preset to the
 // bits of an upper bound, e.g. +inf), with early abandoning against it.
 int launch_exact_nn(const double* d_series, const double* d_mean, const double* d_inv_sigma,
-                    uint32_t n_rows, uint32_t n, uint32_t row, double* d_zrow,
+                    uint32_t n_rows, uint32_t n, uint32_t row, double* d_zrow, const float* d_lb_means, float lb_scale,
                     unsigned long long* d_out_bits, cudaStream_t stream);
 
 // ------------------------------------------------------------------ probes

@@ -1427,16 +1427,31 @@ __global__ void k_zrow(const double* __restrict__ x, const double* __restrict__ 
 }
 
 // One thread per neighbour j (adjacent threads read adjacent samples: coalesced),
-// float64 throughout, early abandoning against the running minimum.
+// float64 throughout, early abandoning against the running minimum.  A neighbour whose
+// segment means already put it further away than that minimum (the lower bound of
+// prep_kernels.cu, with the tile filter's 0.1 % slack for the float32 means) is not measured.
 __global__ void __launch_bounds__(256)
 k_exact_nn(const double* __restrict__ x, const double* __restrict__ mean, const double* __restrict__ inv_sigma,
            uint32_t n_rows, uint32_t n, uint32_t row, const double* __restrict__ z,
-           unsigned long long* out_bits) {
+           const float* __restrict__ lb_means, float lb_scale, unsigned long long* out_bits) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   double mine = __longlong_as_double(0x7FF0000000000000ll);  // +inf
-  if (j < n_rows && gap_u32(row, j) >= n) {
-    const double bound = __longlong_as_double(static_cast<long long>(
-        __ldcg(reinterpret_cast<const unsigned long long*>(out_bits))));
+  bool wanted = j < n_rows && gap_u32(row, j) >= n;
+  const double bound = __longlong_as_double(static_cast<long long>(
+      __ldcg(reinterpret_cast<const unsigned long long*>(out_bits))));
+  if (wanted && lb_means != nullptr) {
+    const float4* pi = reinterpret_cast<const float4*>(lb_means + static_cast<size_t>(row) * kLbSegments);
+    const float4* pj = reinterpret_cast<const float4*>(lb_means + static_cast<size_t>(j) * kLbSegments);
+    float lb = 0.f;
+#pragma unroll
+    for (int q = 0; q < kLbSegments / 4; ++q) {
+      const float4 a = __ldg(pi + q), b = __ldg(pj + q);
+      const float dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z, dw = a.w - b.w;
+      lb = fmaf(dx, dx, lb), lb = fmaf(dy, dy, lb), lb = fmaf(dz, dz, lb), lb = fmaf(dw, dw, lb);
+    }
+    wanted = !(static_cast<double>(lb * lb_scale) > bound * 1.001);
+  }
+  if (wanted) {
     const double mu = mean[j], inv = inv_sigma[j];
     const double* p = x + j;
     double sum = 0.0;
@@ -1717,11 +1732,11 @@ int launch_collect_finalists(SearchState s, uint32_t* d_list, uint32_t cap, uint
 }
 
 int launch_exact_nn(const double* d_series, const double* d_mean, const double* d_inv_sigma,
-                    uint32_t n_rows, uint32_t n, uint32_t row, double* d_zrow,
-                    unsigned long long* d_out_bits, cudaStream_t stream) {
+                    uint32_t n_rows, uint32_t n, uint32_t row, double* d_zrow, const float* d_lb_means,
+                    float lb_scale, unsigned long long* d_out_bits, cudaStream_t stream) {
   k_zrow<<<blocks_for(n, 256), 256, 0, stream>>>(d_series, d_mean, d_inv_sigma, n, row, d_zrow);
   k_exact_nn<<<blocks_for(n_rows, 256), 256, 0, stream>>>(d_series, d_mean, d_inv_sigma, n_rows, n, row,
-                                                         d_zrow, d_out_bits);
+                                                         d_zrow, d_lb_means, lb_scale, d_out_bits);
   return 2;
 }
 
