@@ -813,7 +813,8 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   }
   if (pruning)  // (after the seed: a row whose first mates already put it below the seed stops there)
     ctx->stats.kernel_launches +=
-        launch_bucket_mates(s, ctx->sorted_row, ctx->slot_bucket.ptr, ctx->offsets.ptr, ctx->opt_mates, st);
+        launch_bucket_mates(s, ctx->series.ptr, ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->sorted_row,
+                            ctx->slot_bucket.ptr, ctx->offsets.ptr, ctx->opt_mates, st);
 
   for (int pass = 0; pass < k; ++pass) {
     if (pass > 0) {

@@ -95,7 +95,8 @@ int launch_reset_search(SearchState s, cudaStream_t stream);
 
 // Same-word neighbours first (the HOTSAX inner heuristic, discovery.cpp:51-63):
 // every row is measured against up to `mates` rows of its own bucket.
-int launch_bucket_mates(SearchState s, const uint32_t* d_sorted_row, const uint32_t* d_slot_bucket,
+int launch_bucket_mates(SearchState s, const double* d_series, const double* d_mean, const double* d_inv_sigma,
+                        const uint32_t* d_sorted_row, const uint32_t* d_slot_bucket,
                         const uint32_t* d_offsets, int mates, cudaStream_t stream);
 
 // Outer-loop batch selection: the next `batch` live entries of the rarity

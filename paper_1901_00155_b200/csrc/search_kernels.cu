@@ -156,10 +156,14 @@ k_install_seed(SearchState s, const uint32_t* __restrict__ seed_lb, uint32_t see
 // One warp per slot of the hash-sorted order.  The row is measured against up
 // to `mates` rows spread evenly over its own bucket (positions at least n
 // apart); every completed distance lowers the bound of BOTH rows, d(i,j) =
-// d(j,i).  Lanes stride over the row with float4 loads (512 contiguous bytes
-// per warp per step); the sum is folded with warp shuffles.
+// d(j,i).  The rows are taken from the SERIES (float64 samples, window mean and 1/sigma), not
+// from the matrix: consecutive slots of a bucket are consecutive positions in time, so the
+// windows of neighbouring warps overlap almost entirely and come from L1 / L2, where the
+// matrix rows (16 GB at workload 4, each read once) had to come from HBM.  Lanes stride over
+// the window (256 contiguous bytes per warp per step); the sum is folded with warp shuffles.
 __global__ void __launch_bounds__(256)
-k_bucket_mates(SearchState s, const uint32_t* __restrict__ sorted_row,
+k_bucket_mates(SearchState s, const double* __restrict__ x, const double* __restrict__ mean,
+               const double* __restrict__ inv_sigma, const uint32_t* __restrict__ sorted_row,
                const uint32_t* __restrict__ slot_bucket, const uint32_t* __restrict__ offsets,
                int mates) {
   const uint32_t lane = threadIdx.x & 31;
@@ -170,8 +174,8 @@ k_bucket_mates(SearchState s, const uint32_t* __restrict__ sorted_row,
   const uint32_t len = b1 - b0;
   if (len < 2) return;
   const uint32_t row_i = sorted_row[slot];
-  const float4* pi = reinterpret_cast<const float4*>(s.rows + static_cast<size_t>(row_i) * s.stride);
-  const uint32_t quads = s.stride / 4;
+  const double* pi = x + row_i;
+  const double mu_i = mean[row_i], inv_i = inv_sigma[row_i];
   uint32_t tries = static_cast<uint32_t>(mates);
   uint32_t step = len / (tries + 1);
   if (step == 0) {
@@ -188,25 +192,23 @@ k_bucket_mates(SearchState s, const uint32_t* __restrict__ sorted_row,
     const uint32_t other = b0 + (slot - b0 + q * step) % len;
     const uint32_t row_j = sorted_row[other];
     if (gap_u32(row_i, row_j) < s.n) continue;
-    const float4* pj = reinterpret_cast<const float4*>(s.rows + static_cast<size_t>(row_j) * s.stride);
-    float sum = 0.f;
-    for (uint32_t c = lane; c < quads; c += 32) {
-      const float4 a = pi[c], b = __ldg(pj + c);
-      const float dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z, dw = a.w - b.w;
-      sum = fmaf(dx, dx, sum);
-      sum = fmaf(dy, dy, sum);
-      sum = fmaf(dz, dz, sum);
-      sum = fmaf(dw, dw, sum);
+    const double* pj = x + row_j;
+    const double mu_j = mean[row_j], inv_j = inv_sigma[row_j];
+    double sum64 = 0.0;
+    for (uint32_t t = lane; t < s.n; t += 32) {
+      const double d = (pi[t] - mu_i) * inv_i - (__ldg(pj + t) - mu_j) * inv_j;
+      sum64 = fma(d, d, sum64);
     }
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, d);
+    for (int d = 16; d > 0; d >>= 1) sum64 += __shfl_xor_sync(0xFFFFFFFFu, sum64, d);
+    const float sum = static_cast<float>(sum64);
     bound_i = fminf(bound_i, sum);
     if (lane == 0) {
       const uint32_t bits = __float_as_uint(sum);
       atomicMin(as_ull(s.nn + row_i), static_cast<unsigned long long>(nn_key(bits, row_j)));
       atomicMin(as_ull(s.nn + row_j), static_cast<unsigned long long>(nn_key(bits, row_i)));
       calls += 1;
-      terms += s.stride;
+      terms += s.n;
     }
   }
   if (lane == 0 && calls) {
@@ -1488,11 +1490,12 @@ int launch_reset_search(SearchState s, cudaStream_t stream) {
   return 1;
 }
 
-int launch_bucket_mates(SearchState s, const uint32_t* d_sorted_row, const uint32_t* d_slot_bucket,
+int launch_bucket_mates(SearchState s, const double* d_series, const double* d_mean, const double* d_inv_sigma,
+                        const uint32_t* d_sorted_row, const uint32_t* d_slot_bucket,
                         const uint32_t* d_offsets, int mates, cudaStream_t stream) {
   if (mates <= 0) return 0;
   k_bucket_mates<<<blocks_for(static_cast<size_t>(s.n_rows) * 32, 256), 256, 0, stream>>>(
-      s, d_sorted_row, d_slot_bucket, d_offsets, mates);
+      s, d_series, d_mean, d_inv_sigma, d_sorted_row, d_slot_bucket, d_offsets, mates);
   return 1;
 }
 
