@@ -300,7 +300,11 @@ def run_cuda_arm(args) -> None:
                          "sub_fma_mix_probe_lane_ops_per_s": mix_ops, "ffma_probe_lane_ops_per_s": ffma_ops,
                          "launches": int(totals["scan_launches"]),
                          "avg_launch_ms": totals["scan_ms"] / max(1, totals["scan_launches"]),
-                         "kernel_share_of_step": totals["scan_ms"] / elapsed_ms, "traffic": traffic},
+                         "kernel_share_of_step": totals["scan_ms"] / elapsed_ms, "traffic": traffic,
+                         "traffic_source": "ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum of ONE captured "
+                                           "launch (%s; %s ms) — compare with that launch, not with avg_launch_ms"
+                                           % (prof.get("captured_kernel", "see profiles/scan_tiles_summary.json"),
+                                              prof.get("captured_launch_ms", "?"))},
             "roofline_prep": {"bound": "hbm", "kernel": "k_build_rows", "unit": "GB/s",
                               "achieved": matrix_bytes * args.steps / (totals["build_rows_ms"] * 1e-3) / 1e9
                               if totals["build_rows_ms"] else None,

@@ -48,6 +48,7 @@ def test_library_has_sm100a_code_and_blackwell_instructions():
     assert "LDGSTS" in sass                      # cp.async staging of the tiles (k_scan_tiles)
     # the warp-specialised tile kernel: bulk async copies onto mbarriers, register rebalancing
     assert "UBLKCP" in sass and "SYNCS" in sass and "USETMAXREG" in sass
+    assert "UTMALDG" in sass                     # ... and its tiles as tensor-map (TMA) boxes
 
 
 @pytest.mark.skipif(_has_gpu(), reason="checks the no-device failure mode")
