@@ -883,6 +883,7 @@ namespace ws {
 #ifndef TSDD_WS_LANES48
 #define TSDD_WS_LANES48 1
 #endif
+
 constexpr int kStagesWs = 3;
 constexpr int kNbrWs = 128;
 constexpr int kPitch = kChunk * 4 + 16;
@@ -1210,6 +1211,14 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
   // the 272-byte pitch.
   const uint32_t cand0_of_thread = (ty >> 1) * 16 + (ty & 1);  // + 2 u
   constexpr uint32_t kCandStep = 2;
+  // per-thread constants of the shared-memory addressing, pinned in registers (opaque to the
+  // optimiser, which otherwise rematerialises them from the thread id inside the hot loop)
+  uint32_t xa = (ty & 7u) << 4, xb = (tx & 7u) << 4;  // kTma: the 128-byte swizzle terms
+  uint32_t a_row_off = kTma ? ((ty & 7u) + 64u * (ty >> 3)) * 128u : cand0_of_thread * kPitch;
+  uint32_t b_row_off = kTma ? 2 * kBoxBytes + tx * 128u : kTileRows * kPitch + tx * kPitch;
+  // (an identity shuffle: ptxas cannot see through it, an empty asm it can)
+  xa = __shfl_sync(0xFFFFFFFFu, xa, lane), xb = __shfl_sync(0xFFFFFFFFu, xb, lane);
+  a_row_off = __shfl_sync(0xFFFFFFFFu, a_row_off, lane), b_row_off = __shfl_sync(0xFFFFFFFFu, b_row_off, lane);
   Acc<true, kU, kW> acc;
   float thr[kU];
   uint32_t seq = 0, cur = kTagDone, m = 0, chunks_done = 0;
@@ -1250,14 +1259,14 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
       // candidate rows (ty & 7) + 64 (ty >> 3) + 8 u and neighbour rows tx + 16 w keep r & 7
       constexpr int kAStep = kTma ? 8 * 128 : kCandStep * kPitch;
       constexpr int kBStep = kTma ? kTx * 128 : kTx * kPitch;
-      const unsigned char* a_s =
-          kTma ? sh.stages[st] + ((ty & 7u) + 64u * (ty >> 3)) * 128u : sh.stages[st] + cand0_of_thread * kPitch;
-      const unsigned char* b_s =
-          kTma ? sh.stages[st] + 2 * kBoxBytes + tx * 128u : sh.stages[st] + kTileRows * kPitch + tx * kPitch;
+      const unsigned char* a_s = sh.stages[st] + a_row_off;
+      const unsigned char* b_s = sh.stages[st] + b_row_off;
+      // (two steps per iteration: unrolled further, the loop body outgrows the instruction cache
+      // — all 16 steps at once ran 25 % slower)
 #pragma unroll 2
       for (int kc = 0; kc < kPieces; ++kc) {
-        const uint32_t a_off = kTma ? (kc >> 3) * kBoxBytes + ((((kc & 7u) ^ ty) & 7u) << 4) : kc * 16u;
-        const uint32_t b_off = kTma ? (kc >> 3) * kBoxBytes + ((((kc & 7u) ^ tx) & 7u) << 4) : kc * 16u;
+        const uint32_t a_off = kTma ? (kc >> 3) * kBoxBytes + (((kc & 7u) << 4) ^ xa) : kc * 16u;
+        const uint32_t b_off = kTma ? (kc >> 3) * kBoxBytes + (((kc & 7u) << 4) ^ xb) : kc * 16u;
         float4 na[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) na[u] = *reinterpret_cast<const float4*>(a_s + u * kAStep + a_off);
@@ -1294,6 +1303,10 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
         float nub[kW];
 #pragma unroll
         for (int w = 0; w < kW; ++w) nub[w] = kSymmetric ? meta.nub[tx + kTx * w] : -1.f;
+        if constexpr (kDot) {  // not used between the tile's first stage and here: not kept in registers
+#pragma unroll
+          for (int u = 0; u < kU; ++u) thr[u] = meta.thr[cand0_of_thread + kCandStep * u];
+        }
         // dot form: d^2 = |a|^2 + |b|^2 + 2 acc (acc = -(a . b)), never below the error bound
         float cn[kDot ? kU : 1], bn[kDot ? kW : 1];
         if constexpr (kDot) {
