@@ -176,6 +176,14 @@ inline void check_host_fields(const TimeSeries& series, const DiscoveryConfig& c
 
 // tsdd::run_discovery for Engine::cuda: validate everything, then the two
 // timed stages.  `all`, when given, receives the k discords (best first).
+// Counters and device timings of the last run_discovery on this thread, one entry per rank
+// (tsdd_cuda_stats: terms, tile-kernel time, ... — what the bench harness reports beside the
+// reference's columns).
+inline std::vector<tsdd_cuda_stats>& last_run_stats() {
+  thread_local std::vector<tsdd_cuda_stats> stats;
+  return stats;
+}
+
 inline RunOutcome run_discovery(const TimeSeries& series, const DiscoveryConfig& config, int k = 1,
                                 std::vector<DiscordResult>* all = nullptr, int device = 0) {
   check_host_fields(series, config);
@@ -184,6 +192,7 @@ inline RunOutcome run_discovery(const TimeSeries& series, const DiscoveryConfig&
   session.prepare(series, config.n, config.word_len, config.alphabet);
   std::vector<DiscordResult> found = session.search(k, config.disable_pruning);
   const tsdd_cuda_stats st = session.stats();
+  last_run_stats().assign(1, st);
   RunOutcome outcome;
   outcome.result = found.front();
   outcome.m = series.length();
@@ -289,6 +298,7 @@ inline RunOutcome run_discovery(const TimeSeries& series, const DiscoveryConfig&
   for (std::thread& t : workers) t.join();
   for (const std::exception_ptr& e : errors)
     if (e) std::rethrow_exception(e);
+  last_run_stats() = stats;
   RunOutcome outcome;
   outcome.result = found[0].front();
   outcome.m = series.length();

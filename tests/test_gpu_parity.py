@@ -427,7 +427,7 @@ def test_cli_bench_sweep(chk, tmp_path):  # run_bench / write_bench_csv, src/ben
     assert p.returncode == 0, p.stderr
     lines = p.stdout.strip().splitlines()
     assert lines[0] == ("engine,m,n,threads,wall_time_s,calls,pos,dist,speedup,efficiency,"
-                        "gpus,prep_time_s,search_time_s")
+                        "gpus,prep_time_s,search_time_s,terms,fma_pipe_util")
     rows = [dict(zip(lines[0].split(","), ln.split(","))) for ln in lines[1:]]
     assert [(int(r["n"]), int(r["gpus"])) for r in rows] == [(32, 1), (32, 2), (64, 1), (64, 2)]
     for r in rows:
@@ -436,6 +436,7 @@ def test_cli_bench_sweep(chk, tmp_path):  # run_bench / write_bench_csv, src/ben
         if int(r["gpus"]) == 1:
             assert float(r["speedup"]) == 1.0 and float(r["efficiency"]) == 1.0
         assert float(r["efficiency"]) == pytest.approx(float(r["speedup"]) / int(r["gpus"]), rel=1e-5)
+        assert int(r["terms"]) > 0 and 0.0 < float(r["fma_pipe_util"]) < 1.0
 
 
 # ------------------------------------------------------------------ randomised small cases (edge shapes)

@@ -280,13 +280,23 @@ int run_bench(const Flags& flags) {
   const tsdd::TimeSeries series = acquire_series(flags);
 
   std::ostringstream csv;
-  csv << "engine,m,n,threads,wall_time_s,calls,pos,dist,speedup,efficiency,gpus,prep_time_s,search_time_s\n";
+  // FP32 lane-operations per second of one device (FFMA-only probe): the denominator of fma_pipe_util
+  double lane_ops_per_s = 0.0;
+  {
+    tsdd::cuda::Session probe(0);
+    double ms = 0.0;
+    if (tsdd_cuda_fp32_probe(probe.handle(), 0, &lane_ops_per_s, &ms) != TSDD_OK) lane_ops_per_s = 0.0;
+  }
+  csv << "engine,m,n,threads,wall_time_s,calls,pos,dist,speedup,efficiency,gpus,prep_time_s,search_time_s,terms,"
+         "fma_pipe_util\n";
   for (const std::size_t n : n_values) {
     config.n = n;
     struct Row {
       std::size_t gpus;
       double wall, prep, search;
       tsdd::DiscordResult result;
+      unsigned long long terms;  // distance terms accumulated by the tile kernels, all ranks
+      double fma_pipe_util;      // their FP32-pipe lane operations / (tile-kernel time x measured lane rate), per GPU
     };
     std::vector<Row> rows;
     double t1 = 0.0;
@@ -299,16 +309,26 @@ int run_bench(const Flags& flags) {
         preps.push_back(last.prep_time_s);
         searches.push_back(last.search_time_s);
       }
-      rows.push_back({gpus, median_of(times), median_of(preps), median_of(searches), last.result});
+      unsigned long long terms = 0;
+      double lane_ops = 0.0, kernel_s = 0.0;
+      for (const tsdd_cuda_stats& st : tsdd::cuda::last_run_stats()) {
+        terms += st.scan_kernel_terms;
+        // a term is FADD + FFMA in the direct form, one FFMA in the dot-product form
+        lane_ops += 2.0 * static_cast<double>(st.scan_kernel_terms - st.scan_kernel_dot_terms) +
+                    static_cast<double>(st.scan_kernel_dot_terms);
+        kernel_s += st.scan_kernel_ms * 1e-3;
+      }
+      const double util = (kernel_s > 0.0 && lane_ops_per_s > 0.0) ? lane_ops / (kernel_s * lane_ops_per_s) : 0.0;
+      rows.push_back({gpus, median_of(times), median_of(preps), median_of(searches), last.result, terms, util});
       if (gpus == 1) t1 = rows.back().wall;
     }
     for (const Row& row : rows) {
       const double speedup = t1 / row.wall;
       char line[512];
-      std::snprintf(line, sizeof(line), "cuda,%zu,%zu,%d,%.9f,%llu,%zu,%.17g,%.6f,%.6f,%zu,%.9f,%.9f\n", series.length(),
-                    n, config.threads, row.wall, static_cast<unsigned long long>(row.result.calls),
+      std::snprintf(line, sizeof(line), "cuda,%zu,%zu,%d,%.9f,%llu,%zu,%.17g,%.6f,%.6f,%zu,%.9f,%.9f,%llu,%.4f\n",
+                    series.length(), n, config.threads, row.wall, static_cast<unsigned long long>(row.result.calls),
                     row.result.position, row.result.distance, speedup, speedup / static_cast<double>(row.gpus),
-                    row.gpus, row.prep, row.search);
+                    row.gpus, row.prep, row.search, row.terms, row.fma_pipe_util);
       csv << line;
     }
   }
