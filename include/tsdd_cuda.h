@@ -107,6 +107,9 @@ int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream);
  * the dot-product form, of window rounds, from a copy of the matrix kept in the hash-sorted
  * order — as cp.async.bulk.tensor boxes instead of one bulk copy per row),
  * "dot_window_rounds" (window rounds of a dot-form batch whose window tiles load that way),
+ * "filter_in_ws" (0/1: covering scans with the lower-bound filter run on the warp-specialised
+ * kernel, the filter on the four warps of its producer warpgroup, instead of on the cp.async
+ * tile kernel; measured slower on the BASELINE workloads, off by default),
  * "seed_rows" (before the first scan, the best-so-far is seeded with the greatest LOWER bound of
  * a nearest-neighbour distance among this many first entries of the rarity order, from the
  * segment-mean boxes; 0 = start from zero as the reference does),

@@ -153,6 +153,10 @@ struct tsdd_cuda_ctx {
   bool opt_share_bounds = true;
   bool opt_lower_bound = true;      // tile filter by segment-mean lower bounds in the covering scan
   uint32_t opt_seed_rows = 4096;    // rows whose lower bounds seed the best-so-far of the first pass (0 = none)
+  // the lower-bound filter on the ws kernel's producer warpgroup (needs tensor_map).  Correct, and
+  // faster per term, but its 128-row neighbour tiles rule out and abandon less than k_scan_tiles'
+  // 64-row ones: 25 % more terms, 3-5 % slower on workloads 3 and 4 — off by default
+  bool opt_lb_in_ws = false;
   bool opt_tensor_map = true;       // covering scans of the ws kernel load tiles as TMA boxes
   int opt_dot = 1;
   int opt_dot_window_rounds = 4;    // ... of a batch in the dot-product form whose window tiles load as tensor-map boxes                  // dot-product form of the ws kernel: 0 never, 1 when it pays, 2 always
@@ -784,6 +788,7 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   set_wide_tile(ctx->opt_wide_tile);
   set_scan_variant(ctx->opt_packed ? ctx->opt_kernel : 1);
   set_tensor_map_loads(ctx->opt_tensor_map);
+  set_filter_in_ws(ctx->opt_lb_in_ws);
   const bool pruning = (flags & TSDD_SEARCH_DISABLE_PRUNING) == 0;
   cudaStream_t st = ctx->stream;
   SearchState s = ctx->state();
@@ -1074,6 +1079,8 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
     } else if (key == "dot_window_rounds") {
       if (value < 0 || value > 64) fail(TSDD_ERR_PARAMETER, "dot_window_rounds must be in 0..64");
       ctx->opt_dot_window_rounds = static_cast<int>(value);
+    } else if (key == "filter_in_ws") {
+      ctx->opt_lb_in_ws = value != 0;
     } else if (key == "tensor_map") {
       ctx->opt_tensor_map = value != 0;
     } else if (key == "dot_form") {

@@ -135,6 +135,7 @@ struct ScanChoice {
 ScanChoice choose_scan_kernel(const SearchState& s, uint32_t live_upper_bound, bool window, bool pruning,
                               bool dot_form);
 void set_tensor_map_loads(bool on);
+void set_filter_in_ws(bool on);  // covering scans with the lower-bound filter: warp-specialised kernel (kLb) or k_scan_tiles
 const char* scan_launch_error();  // message of a failed launch_scan_tiles since the last call, or nullptr
 
 // The tiled early-abandoning distance kernel: batch candidates x neighbour units

@@ -893,7 +893,7 @@ constexpr int kConsumerWarps = 8;
 constexpr int kThreadsWs = (kConsumerWarps + 4) * 32;  // + one producer warpgroup
 constexpr uint32_t kTagDone = 0xFFFFFFFFu;
 
-struct TileMeta {
+struct alignas(16) TileMeta {  // (jrow is read as uint4)
   float thr[kTileRows];      // candidate thresholds, -1 = dead / none
   float nub[kNbrWs];         // neighbours' own bounds, -1 = none
   uint32_t jrow[kNbrWs];     // neighbour rows, ~0 = none
@@ -911,9 +911,24 @@ constexpr int kBoxBytes = kTileRows * kBoxCols * 4;
 constexpr int kStageBytesTma = 4 * kBoxBytes;
 static_assert(kChunk == 2 * kBoxCols, "a chunk is two boxes wide");
 
-template <bool kTma>
+// What the four warps of the producer warpgroup need for the lower-bound tile filter (kLb).
+struct LbPart {
+  uint32_t live, needed;     // this warp's candidates: alive / taking part in the tile
+  unsigned long long calls;  // pair distances they start in it
+};
+template <bool kLb>
+struct LbShared {};
+template <>
+struct LbShared<true> {
+  float cmeans[kLbSegments][kTileRows];  // segment means of the CTA's candidates, transposed (conflict-free per lane)
+  float4 boxes[4][kTileRows / kLbBoxRows * 2 * kLbSegments / 4];  // per warp: the neighbour tile's 8 boxes
+  LbPart part[2][4];                     // per tile parity, per warp
+};
+
+template <bool kTma, bool kLb = false>
 struct SharedWsT {
   unsigned char stages[kStagesWs][kTma ? kStageBytesTma : kStageBytesWs];
+  LbShared<kLb> lb;
   TileMeta meta[2];
   uint32_t cand[kTileRows];
   float loc[kTileRows];
@@ -973,12 +988,22 @@ __device__ __forceinline__ void bulk_copy_row(void* smem_dst, const void* gmem_s
 // shares a scheduler with two consumer warps, and the per-row copies (one elect / R2UR /
 // UBLKCP round per row: ~2,500 instructions per chunk) held that scheduler's consumers back.
 // Window launches gather scattered rows and keep the per-row copies.
-template <bool kSymmetric, bool kDot, bool kTma>
+//
+// kLb (covering scans of the direct form, tensor-map loads): the lower-bound tile filter of
+// k_scan_tiles, run by ALL FOUR warps of the producer warpgroup — 32 candidates each, one per
+// lane — now that tensor maps have left them idle.  Per neighbour tile a lane tests its
+// candidate's 16 segment means against the tile's 8 boxes; a candidate the boxes rule out
+// gets threshold -1 for this tile, a tile nobody needs is never streamed (the consumers do
+// not even hear of it: tiles are announced under a running number), and the consumers, who
+// meet no CTA-wide barrier, never wait for a warp that has nothing to do.  The four warps
+// meet once per tile in a named barrier (bar.sync 1, 128) to add up their counts.
+template <bool kSymmetric, bool kDot, bool kTma, bool kLb = false>
 __global__ void __launch_bounds__(kThreadsWs, 1)
 k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap map_a,
                 const __grid_constant__ CUtensorMap map_b) {
+  static_assert(!kLb || (kTma && !kDot), "the filter variant is the direct form fed by tensor maps");
   constexpr int kU = 8, kW = 8, kTx = 16;
-  using SharedWs = SharedWsT<kTma>;
+  using SharedWs = SharedWsT<kTma, kLb>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   SharedWs& sh = *reinterpret_cast<SharedWs*>(smem_raw);
 
@@ -993,6 +1018,15 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
     sh.cand[tid] = row;
     sh.loc[tid] = inf;
     if constexpr (kDot) sh.cnorm[tid] = row != 0xFFFFFFFFu ? s.row_norms[row] : 0.f;
+    if constexpr (kLb) {
+      const float4* pm = reinterpret_cast<const float4*>(s.lb_means + static_cast<size_t>(row) * kLbSegments);
+#pragma unroll
+      for (int q = 0; q < kLbSegments / 4; ++q) {
+        const float4 v = row != 0xFFFFFFFFu ? __ldg(pm + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        sh.lb.cmeans[4 * q][tid] = v.x, sh.lb.cmeans[4 * q + 1][tid] = v.y;
+        sh.lb.cmeans[4 * q + 2][tid] = v.z, sh.lb.cmeans[4 * q + 3][tid] = v.w;
+      }
+    }
   }
   if (tid == 0) {
     for (int i = 0; i < kStagesWs; ++i) {
@@ -1017,6 +1051,156 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
   if (warp >= kConsumerWarps) {
     // ================================================================ producer warpgroup
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    if constexpr (kLb) {
+      // ============================================================ producer warpgroup, with the filter
+      const uint32_t pw = warp - kConsumerWarps;      // 0..3
+      const uint32_t c = 32 * pw + lane;              // this lane's candidate
+      const uint32_t row = sh.cand[c];
+      const uint64_t best = *s.best;
+      const uint32_t units_total = (s.n_rows + kLbBoxRows - 1) / kLbBoxRows;
+      constexpr uint32_t kUnits = kTileRows / kLbBoxRows;          // 8 boxes per neighbour tile
+      constexpr uint32_t kBoxQuads = 2 * kLbSegments / 4;          // float4 per box
+      float4* my_boxes = sh.lb.boxes[pw];
+      uint32_t seq = 0, sti = 0;  // stages issued; tiles announced to the consumers
+      unsigned long long calls_total = 0, tiles_total = 0, live_total = 0, skipped_total = 0;
+#pragma unroll 1
+      for (uint32_t ti = 0; ti < n_tiles; ++ti) {
+        const uint32_t k = k_first + ti, m = sti & 1, use = sti >> 1;
+        TileMeta& meta = sh.meta[m];
+        if (use >= 1) mbar_wait(&sh.meta_empty[m], (use - 1) & 1);  // every consumer has left announced tile sti - 2
+        const uint32_t slot0 = ((k + a.rotation) % slot_tiles) * kTileRows;
+        const uint32_t unit0 = slot0 / kLbBoxRows;
+        // ---- loads first: the candidate's bound, the tile's boxes (this warp's own copy), the neighbours' bounds
+        const uint32_t cand_ub = row != 0xFFFFFFFFu ? key_bits(load_key(s.nn + row)) : 0u;
+        {
+          const float4* src = reinterpret_cast<const float4*>(s.lb_boxes + static_cast<size_t>(unit0) * 2 * kLbSegments);
+#pragma unroll
+          for (int q = 0; q < static_cast<int>(kUnits * kBoxQuads) / 32; ++q) {
+            const uint32_t at = lane + 32 * q;  // float4 index inside the tile's boxes; box = at / kBoxQuads
+            my_boxes[at] = unit0 + at / kBoxQuads < units_total ? __ldg(src + at) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+        uint32_t nbr_j = 0xFFFFFFFFu, nbr_ub = 0u;
+        {
+          const uint32_t slot = slot0 + c;  // the four warps share the 128 neighbours as well
+          if (slot < s.n_rows) {
+            nbr_j = slot;
+            nbr_ub = key_bits(load_key(s.nn + slot));
+          }
+        }
+        __syncwarp();
+        // ---- this candidate: dead, ruled out by the boxes, or taking part
+        float thr = -1.f;
+        bool live = false, needed = false;
+        if (row != 0xFFFFFFFFu) {
+          const float bound = fminf(__uint_as_float(cand_ub), sh.loc[c]);
+          live = !dead_bound(bound, best, s.margin, s.margin_abs);
+          if (live) {
+            const float limit = bound * 1.001f;  // rounding slack of the float32 means
+            const uint32_t n_units = min(kUnits, units_total - unit0);
+            float lb[kUnits];
+#pragma unroll
+            for (int u = 0; u < static_cast<int>(kUnits); ++u) lb[u] = 0.f;
+#pragma unroll
+            for (int q = 0; q < kLbSegments / 4; ++q) {
+              const float m0 = sh.lb.cmeans[4 * q][c], m1 = sh.lb.cmeans[4 * q + 1][c];
+              const float m2 = sh.lb.cmeans[4 * q + 2][c], m3 = sh.lb.cmeans[4 * q + 3][c];
+#pragma unroll
+              for (int u = 0; u < static_cast<int>(kUnits); ++u) {
+                const float4 lo = my_boxes[u * kBoxQuads + q], hi = my_boxes[u * kBoxQuads + kLbSegments / 4 + q];
+                float g;
+                g = fmaxf(fmaxf(lo.x - m0, m0 - hi.x), 0.f), lb[u] = fmaf(g, g, lb[u]);
+                g = fmaxf(fmaxf(lo.y - m1, m1 - hi.y), 0.f), lb[u] = fmaf(g, g, lb[u]);
+                g = fmaxf(fmaxf(lo.z - m2, m2 - hi.z), 0.f), lb[u] = fmaf(g, g, lb[u]);
+                g = fmaxf(fmaxf(lo.w - m3, m3 - hi.w), 0.f), lb[u] = fmaf(g, g, lb[u]);
+              }
+            }
+            float lb_min = __uint_as_float(kInfBits);
+#pragma unroll
+            for (int u = 0; u < static_cast<int>(kUnits); ++u)
+              if (static_cast<uint32_t>(u) < n_units) lb_min = fminf(lb_min, lb[u]);
+            needed = !(lb_min * s.lb_scale > limit);
+            if (needed) thr = bound;
+          }
+        }
+        meta.thr[c] = thr;
+        meta.jrow[c] = nbr_j;
+        meta.nub[c] = nbr_j != 0xFFFFFFFFu ? __uint_as_float(nbr_ub) : -1.f;
+        // pair distances this candidate starts in the tile (series.hpp:120): neighbours at least n away
+        const uint32_t valid = slot0 < s.n_rows ? min(static_cast<uint32_t>(kNbrWs), s.n_rows - slot0) : 0u;
+        unsigned long long calls = 0;
+        if (needed) {
+          const uint32_t z0 = row >= s.n - 1 ? row - (s.n - 1) : 0, z1 = row + s.n;
+          const uint32_t o0 = max(slot0, z0), o1 = min(slot0 + valid, z1);
+          calls = valid - (o1 > o0 ? o1 - o0 : 0);
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) calls += __shfl_xor_sync(0xFFFFFFFFu, calls, d);
+        const uint32_t n_live = __popc(__ballot_sync(0xFFFFFFFFu, live));
+        const uint32_t n_needed = __popc(__ballot_sync(0xFFFFFFFFu, needed));
+        LbPart* part = sh.lb.part[ti & 1];
+        if (lane == 0) part[pw] = LbPart{n_live, n_needed, calls};
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // the four warps; also publishes thr / jrow / nub
+        uint32_t all_live = 0, all_needed = 0;
+        unsigned long long all_calls = 0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          all_live += part[w].live;
+          all_needed += part[w].needed;
+          all_calls += part[w].calls;
+        }
+        if (all_live == 0) break;  // candidates only ever die: nothing is left for this CTA
+        skipped_total += all_live - all_needed;
+        if (all_needed == 0) continue;  // nobody needs this tile: not streamed, not announced
+        live_total += all_live;
+        calls_total += all_calls;
+        tiles_total += 1;
+        if (pw == 0) {
+          if (lane == 0) {
+            meta.calls = all_calls;
+            meta.done = 0;
+            mbar_arrive(&sh.meta_full[m]);
+          }
+          // ---- stream the tile's chunks; stop as soon as every consumer warp has abandoned it
+#pragma unroll 1
+          for (uint32_t ch = 0; ch < chunks; ++ch) {
+            if (*reinterpret_cast<volatile uint32_t*>(&meta.done) == kConsumerWarps) break;
+            const uint32_t st = seq % kStagesWs, round = seq / kStagesWs;
+            if (round >= 1) mbar_wait(&sh.empty[st], (round - 1) & 1);
+            if (lane == 0) {
+              sh.tag_tile[st] = sti;
+              sh.tag_chunk[st] = ch;
+              mbar_arrive_expect_tx(&sh.full[st], kRowsPerStage * kChunk * 4);
+              unsigned char* dst = sh.stages[st];
+              const uint32_t col = ch * kChunk;
+              tma_load_box(dst, &map_a, col, cand0, &sh.full[st]);
+              tma_load_box(dst + kBoxBytes, &map_a, col + kBoxCols, cand0, &sh.full[st]);
+              tma_load_box(dst + 2 * kBoxBytes, &map_b, col, slot0, &sh.full[st]);
+              tma_load_box(dst + 3 * kBoxBytes, &map_b, col + kBoxCols, slot0, &sh.full[st]);
+            }
+            ++seq;
+          }
+        }
+        ++sti;
+      }
+      if (pw == 0) {
+        {  // the end-of-work tag
+          const uint32_t st = seq % kStagesWs, round = seq / kStagesWs;
+          if (round >= 1) mbar_wait(&sh.empty[st], (round - 1) & 1);
+          if (lane == 0) {
+            sh.tag_tile[st] = kTagDone;
+            mbar_arrive(&sh.full[st]);
+          }
+        }
+        if (lane == 0) {
+          if (calls_total) atomicAdd(&s.counters->calls, calls_total);
+          if (tiles_total) atomicAdd(&s.counters->tiles, tiles_total);
+          if (live_total) atomicAdd(&s.counters->tile_live, live_total);
+          if (skipped_total) atomicAdd(&s.counters->lb_skipped, skipped_total);
+        }
+      }
+      return;
+    }
     if (warp != kConsumerWarps) return;  // one warp does the work; the other three only round the CTA to 12 warps
     const uint32_t centre = window ? a.batch_slots[min(cand0 + kTileRows / 2, count - 1)] / kTileRows : 0u;
     const uint64_t best = a.pruning ? *s.best : 0ull;
@@ -1490,6 +1674,7 @@ bool g_packed_default = true;
 bool g_last_launch_was_ws = false;
 bool g_last_launch_was_dot = false;
 bool g_tma_enabled = true;
+bool g_lb_in_ws = false;
 const char* g_launch_error = nullptr;
 inline uint32_t slot_tiles_of(uint32_t rows) { return (rows + kTileRows - 1) / kTileRows; }
 int g_scan_variant = 0;  // 0: chosen per launch, 1: cp.async + CTA barriers (k_scan_tiles), 2: warp-specialised (k_scan_tiles_ws)
@@ -1587,12 +1772,15 @@ ScanChoice choose_scan_kernel(const SearchState& s, uint32_t live_upper_bound, b
   // variant 0 (automatic): the warp-specialised kernel wherever the lower-bound filter has
   // nothing to offer (window rounds; covering scans of searches on which it is switched off)
   // and the batch still fills 128-candidate tiles; k_scan_tiles otherwise
-  c.ws = g_scan_variant == 2 ||
-         (g_scan_variant == 0 && g_packed_default && !g_wide_tile && !c.lb && live_upper_bound > 64);
-  c.dot = c.ws && dot_form && s.row_norms != nullptr;
+  const bool tma_ok = g_tma_enabled && tensor_map_encoder() != nullptr;
+  // ... or, with tensor-map loads, where the filter runs on the producer warpgroup (kLb)
+  const bool lb_in_ws = c.lb && tma_ok && g_lb_in_ws;
+  c.ws = g_scan_variant == 2 || (g_scan_variant == 0 && g_packed_default && !g_wide_tile && (!c.lb || lb_in_ws) &&
+                                 live_upper_bound > 64);
+  c.dot = c.ws && !c.lb && dot_form && s.row_norms != nullptr;
   // window launches read scattered rows unless the engine keeps a copy of the matrix in the
   // hash-sorted order (it does once a search runs in the dot form)
-  c.tma = c.ws && g_tma_enabled && tensor_map_encoder() != nullptr && (!window || (c.dot && s.rows_sorted != nullptr));
+  c.tma = c.ws && tma_ok && (!window || (c.dot && s.rows_sorted != nullptr));
   return c;
 }
 
@@ -1636,7 +1824,8 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
     };
     auto pick_ws = [&](auto sym) {
       constexpr bool kS = decltype(sym)::value;
-      if (tma && choice.dot) launch_ws(ws::k_scan_tiles_ws<kS, true, true>, sizeof(ws::SharedWsT<true>));
+      if (tma && lb) launch_ws(ws::k_scan_tiles_ws<kS, false, true, true>, sizeof(ws::SharedWsT<true, true>));
+      else if (tma && choice.dot) launch_ws(ws::k_scan_tiles_ws<kS, true, true>, sizeof(ws::SharedWsT<true>));
       else if (tma) launch_ws(ws::k_scan_tiles_ws<kS, false, true>, sizeof(ws::SharedWsT<true>));
       else if (choice.dot) launch_ws(ws::k_scan_tiles_ws<kS, true, false>, sizeof(ws::SharedWsT<false>));
       else launch_ws(ws::k_scan_tiles_ws<kS, false, false>, sizeof(ws::SharedWsT<false>));
@@ -1677,6 +1866,7 @@ void set_scan_variant(int variant) { g_scan_variant = variant; }
 bool scan_last_launch_was_ws() { return g_last_launch_was_ws; }
 bool scan_last_launch_was_dot() { return g_last_launch_was_dot; }
 void set_tensor_map_loads(bool on) { g_tma_enabled = on; }
+void set_filter_in_ws(bool on) { g_lb_in_ws = on; }
 const char* scan_launch_error() {
   const char* e = g_launch_error;
   g_launch_error = nullptr;

@@ -540,6 +540,42 @@ def test_dot_product_form_is_chosen_where_tiles_are_never_abandoned(ctx, chk):
     assert ctx.stats()["scan_kernel_dot_launches"] == 0
 
 
+@pytest.mark.parametrize("seed,kind,n", FUZZ[::2], ids=[f"{k}-n{n}" for _, k, n in FUZZ[::2]])
+def test_filter_on_the_producer_warpgroup_matches_the_oracle(ctx, chk, seed, kind, n):
+    """"filter_in_ws": covering scans with the lower-bound filter on the warp-specialised kernel
+    (tensor-map loads, the filter on the four producer warps) instead of k_scan_tiles."""
+    rng = np.random.default_rng(9000 + seed)
+    m = int(rng.integers(2 * n + 400, 2 * n + 4000))
+    w = int(rng.integers(1, min(n, 8) + 1))
+    a = int(rng.integers(2, 7))
+    k = int(rng.integers(1, 4))
+    x = _fuzz_series(rng, kind, m)
+    ctx.set_option("filter_in_ws", 1)
+    try:
+        ctx.prepare(x, n, w, a)
+        pos, dist = ctx.search(k)
+    finally:
+        ctx.set_option("filter_in_ws", 0)
+    want = chk.topk(x, n, w, a, k)
+    assert_discords_match(chk, x, n, pos, dist, want)
+
+
+def test_filter_on_the_producer_warpgroup_rules_tiles_out(ctx, chk):
+    x, _ = W.series(2)
+    x = x[:120000]
+    ctx.prepare(x, 256, 8, 4)
+    base = ctx.search(3)
+    ctx.set_option("filter_in_ws", 1)
+    try:
+        got = ctx.search(3)
+        st = ctx.stats()
+    finally:
+        ctx.set_option("filter_in_ws", 0)
+    assert got[0] == base[0]
+    np.testing.assert_allclose(got[1], base[1], rtol=1e-9)
+    assert st["lb_skipped"] > 0 and st["scan_kernel_ws_launches"] > 0
+
+
 def test_seeded_best_so_far_saves_work_and_keeps_the_result(ctx, chk):
     """The first pass starts from the greatest lower bound of a nearest-neighbour distance among
     the rarest rows (segment-mean boxes) instead of zero: fewer pair distances, same discords."""
