@@ -816,10 +816,15 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
     ctx->stats.kernel_launches += launch_seed_lower_bound(s, ctx->order, seed_rows, ctx->seed_lb.ptr, st);
     seeded = true;
   }
-  if (pruning)  // (after the seed: a row whose first mates already put it below the seed stops there)
-    ctx->stats.kernel_launches +=
-        launch_bucket_mates(s, ctx->series.ptr, ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->sorted_row,
-                            ctx->slot_bucket.ptr, ctx->offsets.ptr, ctx->opt_mates, st);
+  if (pruning) {  // (after the seed: a row whose first mates already put it below the seed stops there)
+    // Ranks that share their bounds split this stage too (slot p belongs to rank p mod world)
+    // and merge the results with the same min-exchange that follows every batch.
+    const bool split = (ctx->world > 1 || ctx->comm) && ctx->opt_share_bounds && ctx->opt_mates > 0;
+    ctx->stats.kernel_launches += launch_bucket_mates(
+        s, ctx->series.ptr, ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->sorted_row, ctx->slot_bucket.ptr, ctx->offsets.ptr,
+        ctx->opt_mates, split ? static_cast<uint32_t>(ctx->world) : 1u, split ? static_cast<uint32_t>(ctx->rank) : 0u, st);
+    if (split) exchange_bounds(ctx);
+  }
 
   for (int pass = 0; pass < k; ++pass) {
     if (pass > 0) {

@@ -97,7 +97,7 @@ int launch_reset_search(SearchState s, cudaStream_t stream);
 // every row is measured against up to `mates` rows of its own bucket.
 int launch_bucket_mates(SearchState s, const double* d_series, const double* d_mean, const double* d_inv_sigma,
                         const uint32_t* d_sorted_row, const uint32_t* d_slot_bucket,
-                        const uint32_t* d_offsets, int mates, cudaStream_t stream);
+                        const uint32_t* d_offsets, int mates, uint32_t world, uint32_t rank, cudaStream_t stream);
 
 // Outer-loop batch selection: the next `batch` live entries of the rarity
 // order at or after `cursor` that belong to this rank.  d_sel[0] = count,

@@ -165,9 +165,10 @@ __global__ void __launch_bounds__(256)
 k_bucket_mates(SearchState s, const double* __restrict__ x, const double* __restrict__ mean,
                const double* __restrict__ inv_sigma, const uint32_t* __restrict__ sorted_row,
                const uint32_t* __restrict__ slot_bucket, const uint32_t* __restrict__ offsets,
-               int mates) {
+               int mates, uint32_t world, uint32_t rank) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t slot = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  // several ranks that share their bounds afterwards (engine: exchange_bounds) split the slots
+  const uint32_t slot = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * world + rank;
   if (slot >= s.n_rows) return;
   const uint32_t bucket = slot_bucket[slot];
   const uint32_t b0 = offsets[bucket], b1 = offsets[bucket + 1];
@@ -1690,10 +1691,11 @@ int launch_reset_search(SearchState s, cudaStream_t stream) {
 
 int launch_bucket_mates(SearchState s, const double* d_series, const double* d_mean, const double* d_inv_sigma,
                         const uint32_t* d_sorted_row, const uint32_t* d_slot_bucket,
-                        const uint32_t* d_offsets, int mates, cudaStream_t stream) {
+                        const uint32_t* d_offsets, int mates, uint32_t world, uint32_t rank, cudaStream_t stream) {
   if (mates <= 0) return 0;
-  k_bucket_mates<<<blocks_for(static_cast<size_t>(s.n_rows) * 32, 256), 256, 0, stream>>>(
-      s, d_series, d_mean, d_inv_sigma, d_sorted_row, d_slot_bucket, d_offsets, mates);
+  const size_t slots = (static_cast<size_t>(s.n_rows) + world - 1) / world;
+  k_bucket_mates<<<blocks_for(slots * 32, 256), 256, 0, stream>>>(
+      s, d_series, d_mean, d_inv_sigma, d_sorted_row, d_slot_bucket, d_offsets, mates, world, rank);
   return 1;
 }
 
