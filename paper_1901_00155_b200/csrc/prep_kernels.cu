@@ -100,6 +100,125 @@ k_window_encode(const double* __restrict__ x, uint32_t rows, uint32_t n, uint32_
   hash0[i] = static_cast<uint32_t>(h);
 }
 
+// The same, four consecutive windows per thread.  k_window_encode is bound by the L1 data path
+// (every window reads its n samples twice, 8 bytes each); here a block stages the samples of
+// its 1,024 windows in shared memory once, interleaved by four (sample j at quarter j & 3,
+// index j >> 2) so that the threads of a warp — whose windows start four samples apart — still
+// read consecutive words, and a thread slides a four-sample register window along: one
+// LDS.64 per step feeds four windows.  Every window's sums run in the same sequence order as
+// before (bit-identical mean, sigma, PAA, symbols: the parity tests compare every array).
+constexpr int kEncWindows = 4;
+constexpr int kEncThreads = 256;
+constexpr size_t encode4_smem_bytes(uint32_t n) {
+  return (static_cast<size_t>(kEncThreads) * kEncWindows + n + 16) * sizeof(double);
+}
+
+__global__ void __launch_bounds__(kEncThreads)
+k_window_encode4(const double* __restrict__ x, uint32_t rows, uint32_t n, uint32_t word_len,
+                 uint32_t alphabet, double* __restrict__ mean, double* __restrict__ inv_sigma,
+                 uint32_t* __restrict__ hash0, double* __restrict__ paa_out,
+                 uint32_t* __restrict__ sax_out) {
+  extern __shared__ double s_x[];
+  const uint32_t w0 = blockIdx.x * (kEncThreads * kEncWindows);  // first window of the block
+  const uint32_t span = kEncThreads * kEncWindows + n + 4;       // samples any of its threads touches
+  const uint32_t quarter = (span + 3) / 4 + 1;
+  const size_t m = static_cast<size_t>(rows) + n - 1;
+  for (uint32_t j = threadIdx.x; j < span; j += kEncThreads) {
+    const size_t at = static_cast<size_t>(w0) + j;
+    s_x[(j & 3u) * quarter + (j >> 2)] = at < m ? x[at] : 0.0;
+  }
+  __syncthreads();
+  const uint32_t base = kEncWindows * threadIdx.x;  // this thread's first window, relative to w0
+  auto sample = [&](uint32_t j) -> double { return s_x[(j & 3u) * quarter + (j >> 2)]; };
+
+  // ---- mean, sigma (series.cpp:21-37)
+  double w[kEncWindows], sum[kEncWindows], sum_sq[kEncWindows];
+#pragma unroll
+  for (int r = 0; r < kEncWindows; ++r) w[r] = sample(base + r), sum[r] = 0.0, sum_sq[r] = 0.0;
+  for (uint32_t t = 0; t < n; ++t) {
+#pragma unroll
+    for (int r = 0; r < kEncWindows; ++r) {
+      const double v = w[r];
+      sum[r] += v;
+      sum_sq[r] += v * v;
+    }
+#pragma unroll
+    for (int r = 0; r + 1 < kEncWindows; ++r) w[r] = w[r + 1];
+    w[kEncWindows - 1] = sample(base + t + kEncWindows);
+  }
+  const double dn = static_cast<double>(n);
+  double mu[kEncWindows], inv[kEncWindows];
+  bool flat[kEncWindows];
+#pragma unroll
+  for (int r = 0; r < kEncWindows; ++r) {
+    mu[r] = sum[r] / dn;
+    const double var = sum_sq[r] / dn - mu[r] * mu[r];
+    const double sigma = var > 0.0 ? sqrt(var) : 0.0;
+    flat[r] = sigma < 1e-12;
+    inv[r] = flat[r] ? 0.0 : 1.0 / sigma;
+    const uint32_t i = w0 + base + r;
+    if (i < rows) {
+      mean[i] = mu[r];
+      inv_sigma[i] = inv[r];
+    }
+  }
+
+  // ---- PAA, symbols, hash (sax.cpp:53-80,121-132)
+  const double* bp = c_breaks[alphabet - 2];
+  uint64_t h[kEncWindows];
+#pragma unroll
+  for (int r = 0; r < kEncWindows; ++r) w[r] = sample(base + r), h[r] = 0;
+  uint32_t cur = 0;  // w[r] holds local sample cur of window r
+  const double full_units = static_cast<double>(word_len);
+  for (uint32_t k = 0; k < word_len; ++k) {
+    const uint64_t lo = static_cast<uint64_t>(k) * n;
+    const uint64_t hi = lo + n;
+    const uint32_t t_first = static_cast<uint32_t>(lo / word_len);
+    const uint32_t t_last = static_cast<uint32_t>((hi - 1) / word_len);
+    double acc[kEncWindows];
+#pragma unroll
+    for (int r = 0; r < kEncWindows; ++r) acc[r] = 0.0;
+    for (uint32_t t = t_first; t <= t_last; ++t) {
+      while (cur < t) {  // (segments meet in at most one shared sample: the window only moves forward)
+#pragma unroll
+        for (int r = 0; r + 1 < kEncWindows; ++r) w[r] = w[r + 1];
+        w[kEncWindows - 1] = sample(base + cur + kEncWindows);
+        ++cur;
+      }
+      // a sample strictly inside the segment counts word_len units of the n*w grid; only the
+      // first and the last can be cut by the segment's ends
+      double units_d = full_units;
+      if (t == t_first || t == t_last) {
+        const uint64_t el = static_cast<uint64_t>(t) * word_len;
+        const uint64_t eh = el + word_len;
+        units_d = static_cast<double>((eh < hi ? eh : hi) - (el > lo ? el : lo));
+      }
+#pragma unroll
+      for (int r = 0; r < kEncWindows; ++r) {
+        const double v = flat[r] ? 0.0 : (w[r] - mu[r]) * inv[r];
+        acc[r] += units_d * v;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kEncWindows; ++r) {
+      const double seg = acc[r] / dn;
+      uint32_t sym = 1;
+      for (uint32_t b = 0; b + 1 < alphabet; ++b) sym += (bp[b] <= seg) ? 1u : 0u;
+      const uint32_t i = w0 + base + r;
+      if (i < rows) {
+        if (paa_out) paa_out[static_cast<size_t>(i) * word_len + k] = seg;
+        if (sax_out) sax_out[static_cast<size_t>(i) * word_len + k] = sym;
+      }
+      h[r] = h[r] * alphabet + (sym - 1);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kEncWindows; ++r) {
+    const uint32_t i = w0 + base + r;
+    if (i < rows) hash0[i] = static_cast<uint32_t>(h[r]);
+  }
+}
+
 // Subsequence matrix (series.cpp:46-74), float32: element (i, t) is the
 // float64 value (x[i+t] - mu_i) * (1/sigma_i) rounded once.  HBM write-bound:
 // a block owns kBuildRows consecutive rows x kBuildCols columns, whose samples
@@ -415,6 +534,13 @@ int launch_widen_series(const float* d_in, double* d_out, size_t m, cudaStream_t
 int launch_window_encode(const double* d_series, uint32_t rows, uint32_t n, uint32_t word_len,
                          uint32_t alphabet, double* d_mean, double* d_inv_sigma, uint32_t* d_hash0,
                          double* d_paa, uint32_t* d_sax, cudaStream_t stream) {
+  const size_t smem = encode4_smem_bytes(n);
+  if (smem <= 200 * 1024) {  // (longer windows than ~24,000 samples: the one-window-per-thread kernel)
+    cudaFuncSetAttribute(k_window_encode4, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_window_encode4<<<blocks_for(rows, kEncThreads * kEncWindows), kEncThreads, smem, stream>>>(
+        d_series, rows, n, word_len, alphabet, d_mean, d_inv_sigma, d_hash0, d_paa, d_sax);
+    return 1;
+  }
   k_window_encode<<<blocks_for(rows, 256), 256, 0, stream>>>(d_series, rows, n, word_len, alphabet,
                                                              d_mean, d_inv_sigma, d_hash0, d_paa,
                                                              d_sax);
