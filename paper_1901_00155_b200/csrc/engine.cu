@@ -157,6 +157,7 @@ struct tsdd_cuda_ctx {
   // faster per term, but its 128-row neighbour tiles rule out and abandon less than k_scan_tiles'
   // 64-row ones: 25 % more terms, 3-5 % slower on workloads 3 and 4 — off by default
   bool opt_lb_in_ws = false;
+  bool opt_tile16 = true;           // dot form: 256-candidate tiles, 16 x 8 pairs per thread (k_scan_tiles_ws16)
   bool opt_tensor_map = true;       // covering scans of the ws kernel load tiles as TMA boxes
   int opt_dot = 1;
   int opt_dot_window_rounds = 4;    // ... of a batch in the dot-product form whose window tiles load as tensor-map boxes                  // dot-product form of the ws kernel: 0 never, 1 when it pays, 2 always
@@ -520,7 +521,7 @@ cudaEvent_t next_event(tsdd_cuda_ctx* ctx) {
 }
 
 void ensure_batch_capacity(tsdd_cuda_ctx* ctx, uint32_t batch) {
-  const uint32_t padded = round_up_u32(batch, kTileRows);
+  const uint32_t padded = round_up_u32(batch, 2 * kTileRows);  // (the 16 x 8 kernel works on 256-candidate tiles)
   if (padded <= ctx->batch_capacity) return;
   ctx->batch_rows.alloc(padded);
   ctx->batch_alt.alloc(padded);
@@ -635,9 +636,10 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
         if (count == 0) break;
       }
     }
-    const uint32_t padded = round_up_u32(count, kTileRows);
     const ScanChoice choice = choose_scan_kernel(s, count, plan[r].window, pruning, ctx->dot_now);
-    launches += launch_gather_rows(s, list, ctx->sel.ptr, padded, choice.tma, ctx->batch_matrix.ptr, st);
+    const uint32_t padded = round_up_u32(count, choice.tile16 ? 2 * kTileRows : kTileRows);
+    launches += launch_gather_rows(s, list, ctx->sel.ptr, padded, choice.tile16 ? 2 : choice.tma ? 1 : 0,
+                                   ctx->batch_matrix.ptr, st);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->opt_time_kernels) {
       e0 = next_event(ctx);
@@ -789,6 +791,7 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   set_scan_variant(ctx->opt_packed ? ctx->opt_kernel : 1);
   set_tensor_map_loads(ctx->opt_tensor_map);
   set_filter_in_ws(ctx->opt_lb_in_ws);
+  set_dot_tile16(ctx->opt_tile16);
   const bool pruning = (flags & TSDD_SEARCH_DISABLE_PRUNING) == 0;
   cudaStream_t st = ctx->stream;
   SearchState s = ctx->state();
@@ -1084,6 +1087,8 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
     } else if (key == "dot_window_rounds") {
       if (value < 0 || value > 64) fail(TSDD_ERR_PARAMETER, "dot_window_rounds must be in 0..64");
       ctx->opt_dot_window_rounds = static_cast<int>(value);
+    } else if (key == "dot_tile16") {
+      ctx->opt_tile16 = value != 0;
     } else if (key == "filter_in_ws") {
       ctx->opt_lb_in_ws = value != 0;
     } else if (key == "tensor_map") {

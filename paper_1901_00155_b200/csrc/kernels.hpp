@@ -120,10 +120,12 @@ int launch_batch_slots(const uint32_t* d_batch_rows, const uint32_t* d_sel, cons
                        uint32_t capacity, uint32_t* d_keys, cudaStream_t stream);
 
 // Copies the batch's matrix rows into a dense [capacity_padded x stride] buffer.
-// tma_layout: the row order inside each 128-row tile that the tensor-map variant of the
-// warp-specialised kernel reads (search_kernels.cu: tma_row_of_candidate).
+// tma_layout 1: the row order inside each 128-row tile that the tensor-map variant of the
+// warp-specialised kernel reads (search_kernels.cu: tma_row_of_candidate); 2: 256-row tiles of
+// pairwise interleaved rows for its 16 x 8 variant (tma16_pair_of_candidate); capacity_padded is
+// then a multiple of 256.
 int launch_gather_rows(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,
-                       uint32_t capacity_padded, bool tma_layout, float* d_batch_matrix, cudaStream_t stream);
+                       uint32_t capacity_padded, int tma_layout, float* d_batch_matrix, cudaStream_t stream);
 
 // Which kernel launch_scan_tiles will pick for a launch (the gather before it needs `tma`).
 struct ScanChoice {
@@ -131,10 +133,12 @@ struct ScanChoice {
   bool ws;   // the warp-specialised kernel
   bool tma;  // ... fed by tensor-map box loads (covering scans)
   bool dot;  // ... in the dot-product form
+  bool tile16;  // ... on 256-candidate tiles, 16 x 8 pairs per thread (k_scan_tiles_ws16)
 };
 ScanChoice choose_scan_kernel(const SearchState& s, uint32_t live_upper_bound, bool window, bool pruning,
                               bool dot_form);
 void set_tensor_map_loads(bool on);
+void set_dot_tile16(bool on);
 void set_filter_in_ws(bool on);  // covering scans with the lower-bound filter: warp-specialised kernel (kLb) or k_scan_tiles
 const char* scan_launch_error();  // message of a failed launch_scan_tiles since the last call, or nullptr
 

@@ -324,6 +324,13 @@ __host__ __device__ __forceinline__ uint32_t tma_row_of_candidate(uint32_t l) {
   const uint32_t w = l >> 4, u = (l >> 1) & 7u, b = l & 1u;
   return 2u * (w & 3u) + b + 8u * u + 64u * (w >> 2);
 }
+// The 16 x 8 variant (k_scan_tiles_ws16): tiles of 256 candidates stored as 128 row PAIRS, the two
+// rows of a pair interleaved column by column.  Candidate L = 16 ty + 2 i + h of a tile is half h
+// of pair (ty & 7) + 8 i + 64 (ty >> 3).
+__host__ __device__ __forceinline__ uint32_t tma16_pair_of_candidate(uint32_t l) {
+  const uint32_t ty = l >> 4, i = (l >> 1) & 7u;
+  return (ty & 7u) + 8u * i + 64u * (ty >> 3);
+}
 __global__ void __launch_bounds__(256)
 k_gather_rows(SearchState s, const uint32_t* __restrict__ batch_rows, const uint32_t* __restrict__ sel,
               uint32_t capacity_padded, int tma_layout, float* __restrict__ out) {
@@ -332,11 +339,28 @@ k_gather_rows(SearchState s, const uint32_t* __restrict__ batch_rows, const uint
   if (r >= capacity_padded) return;
   const uint32_t count = sel[0];
   // only the tiles the scan will touch need refreshing
-  if (r >= (count + kTileRows - 1) / kTileRows * kTileRows) return;
-  // tma_layout: candidate L of a tile sits at row tma_row_of_candidate(L) of the tile
+  const uint32_t tile_rows = tma_layout == 2 ? 256u : static_cast<uint32_t>(kTileRows);
+  if (r >= (count + tile_rows - 1) / tile_rows * tile_rows) return;
+  const uint32_t quads = s.stride / 4;
+  if (tma_layout == 2) {  // pairwise interleaved (k_scan_tiles_ws16)
+    const uint32_t l = r & 255u, pair = (r >> 8) * 128u + tma16_pair_of_candidate(l);
+    float2* dst2 = reinterpret_cast<float2*>(out + static_cast<size_t>(pair) * 2 * s.stride);
+    float* dst1 = reinterpret_cast<float*>(dst2) + (l & 1u);
+    if (r < count) {
+      const float4* src = reinterpret_cast<const float4*>(s.rows + static_cast<size_t>(batch_rows[r]) * s.stride);
+      for (uint32_t c = lane; c < quads; c += 32) {
+        const float4 v = __ldg(src + c);
+        dst1[8 * c] = -v.x, dst1[8 * c + 2] = -v.y, dst1[8 * c + 4] = -v.z, dst1[8 * c + 6] = -v.w;
+      }
+    } else {
+      for (uint32_t c = lane; c < quads; c += 32)
+        dst1[8 * c] = 0.f, dst1[8 * c + 2] = 0.f, dst1[8 * c + 4] = 0.f, dst1[8 * c + 6] = 0.f;
+    }
+    return;
+  }
+  // tma_layout 1: candidate L of a tile sits at row tma_row_of_candidate(L) of the tile
   const uint32_t at = tma_layout ? (r & ~(kTileRows - 1u)) + tma_row_of_candidate(r & (kTileRows - 1u)) : r;
   float4* dst = reinterpret_cast<float4*>(out + static_cast<size_t>(at) * s.stride);
-  const uint32_t quads = s.stride / 4;
   if (r < count) {
     const float4* src =
         reinterpret_cast<const float4*>(s.rows + static_cast<size_t>(batch_rows[r]) * s.stride);
@@ -1587,6 +1611,369 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
   }
 }
 
+
+// ------------------------------------------------------------------ 16 x 8 pairs per thread (dot form)
+// What bounds k_scan_tiles_ws in the dot form is not the FMA pipe but its shared-memory loads: 16
+// LDS.128 per 64 FFMA2 with 8 x 8 pairs per thread, each LDS.128 costing the scheduler about four
+// issue cycles.  This variant doubles the candidates per thread — 16 x 8 pairs, 24
+// LDS.128 per 256 FFMA2 — and still fits 232 registers because a pair needs ONE accumulator
+// instead of an even / odd couple: an FFMA2 serves two CANDIDATES at once,
+//     (acc[2p][w], acc[2p+1][w]) += (a[2p][k], a[2p+1][k]) * (b[w][k], b[w][k]),
+// the neighbour value broadcast to both halves (ptxas folds the duplicate into the FFMA2's scalar
+// .F32 operand form: no extra instruction).  For the left operand to arrive as a register pair,
+// k_gather_rows stores the candidate rows pairwise interleaved (its layout is ours): row pair p of
+// a tile is [a(2p,0), a(2p+1,0), a(2p,1), a(2p+1,1), ...].  A probe of exactly this loop runs at
+// 0.97 of the FFMA peak with two warps per scheduler.
+//   tile: 256 candidates x 128 neighbours; stage: 32 columns = two candidate boxes (128 row
+//   pairs x 16 columns x 2) + one neighbour box (128 rows x 32 columns), 48 KB, four stages;
+//   thread (ty, tx): row pairs (ty & 7) + 64 (ty >> 3) + 8 i, i < 8 (so that the 128-byte swizzle
+//   term is one constant per thread), neighbours tx + 16 w, w < 8; candidate 16 ty + 2 i + h of
+//   the tile sits in half h of that pair (tma16_pair_of_candidate).
+constexpr int kCand16 = 256;
+constexpr int kCols16 = 32;
+constexpr int kStages16 = 4;
+constexpr int kBox16 = 128 * 128;                   // bytes of one box: 128 rows of 128 bytes
+constexpr int kStageBytes16 = 3 * kBox16;
+
+struct alignas(16) TileMeta16 {
+  float thr[kCand16];
+  float nub[kNbrWs];
+  uint32_t jrow[kNbrWs];
+  float nnorm[kNbrWs];
+  unsigned long long calls;
+  uint32_t done;
+  uint32_t pad;
+};
+
+struct Shared16 {
+  unsigned char stages[kStages16][kStageBytes16];
+  TileMeta16 meta[2];
+  uint32_t cand[kCand16];
+  float loc[kCand16];
+  float cnorm[kCand16];
+  uint32_t tag_tile[kStages16 + 1];
+  uint32_t tag_chunk[kStages16 + 1];
+  unsigned long long full[kStages16], empty[kStages16], meta_full[2], meta_empty[2];  // mbarriers
+};
+
+template <bool kSymmetric>
+__global__ void __launch_bounds__(kThreadsWs, 1)
+k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap map_a,
+                  const __grid_constant__ CUtensorMap map_b) {
+  constexpr int kP = 8, kW = 8, kTx = 16;  // row pairs and neighbours per thread
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  Shared16& sh = *reinterpret_cast<Shared16*>(smem_raw);
+
+  const uint32_t count = a.sel[0];
+  const uint32_t cand0 = blockIdx.y * kCand16;
+  if (cand0 >= count) return;
+
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float inf = __uint_as_float(kInfBits);
+  if (tid < kCand16) {
+    const uint32_t row = (cand0 + tid < count) ? a.batch_rows[cand0 + tid] : 0xFFFFFFFFu;
+    sh.cand[tid] = row;
+    sh.loc[tid] = inf;
+    sh.cnorm[tid] = row != 0xFFFFFFFFu ? s.row_norms[row] : 0.f;
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kStages16; ++i) {
+      mbar_init(&sh.full[i], 1);
+      mbar_init(&sh.empty[i], kConsumerWarps);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sh.meta_full[i], 1);
+      mbar_init(&sh.meta_empty[i], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const bool window = a.nbr_index != nullptr;
+  const uint32_t slot_tiles = (s.n_rows + kTileRows - 1) / kTileRows;
+  const uint32_t chunks = s.stride / kCols16;
+  const uint32_t k_first = a.k_begin + blockIdx.x * a.tiles_per_cta, k_end = a.k_end;
+  const uint32_t n_tiles = k_first < k_end ? min(static_cast<uint32_t>(a.tiles_per_cta), k_end - k_first) : 0u;
+
+  if (warp >= kConsumerWarps) {
+    // ================================================================ producer warpgroup
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+    if (warp != kConsumerWarps) return;
+    const uint32_t centre = window ? a.batch_slots[min(cand0 + kCand16 / 2, count - 1)] / kTileRows : 0u;
+    const uint64_t best = a.pruning ? *s.best : 0ull;
+    auto slot0_of = [&](uint32_t k) -> uint32_t {
+      uint32_t unit;
+      if (!window) {
+        unit = (k + a.rotation) % slot_tiles;
+      } else {
+        const uint32_t step = (k + 1) >> 1;
+        unit = (k & 1) ? (centre + step) % slot_tiles : (centre + slot_tiles - step % slot_tiles) % slot_tiles;
+      }
+      return unit * kTileRows;
+    };
+    uint32_t seq = 0;
+    unsigned long long calls_total = 0, tiles_total = 0, live_total = 0;
+#pragma unroll 1
+    for (uint32_t ti = 0; ti < n_tiles; ++ti) {
+      const uint32_t k = k_first + ti, m = ti & 1, use = ti >> 1;
+      TileMeta16& meta = sh.meta[m];
+      if (use >= 1) mbar_wait(&sh.meta_empty[m], (use - 1) & 1);
+      const uint32_t slot0 = slot0_of(k);
+      const uint32_t valid = slot0 < s.n_rows ? min(static_cast<uint32_t>(kNbrWs), s.n_rows - slot0) : 0u;
+      // ---- candidates: thresholds, and the pair distances they start in this tile
+      bool any_live = false;
+      unsigned long long calls = 0;
+#pragma unroll
+      for (int q = 0; q < kCand16 / 32; ++q) {
+        const uint32_t r = lane + 32 * q, row = sh.cand[r];
+        float thr = -1.f;
+        if (row != 0xFFFFFFFFu) {
+          if (!a.pruning) {
+            thr = inf;
+          } else {
+            const float bound = fminf(__uint_as_float(key_bits(load_key(s.nn + row))), sh.loc[r]);
+            if (!dead_bound(bound, best, s.margin, s.margin_abs)) thr = bound;
+          }
+        }
+        meta.thr[r] = thr;
+        if (thr >= 0.f) {
+          any_live = true;
+          live_total += 1;
+          uint32_t overlap = 0;
+          if (!window) {  // (window tiles: the consumers count the self-match pairs)
+            const uint32_t z0 = row >= s.n - 1 ? row - (s.n - 1) : 0, z1 = row + s.n;
+            const uint32_t o0 = max(slot0, z0), o1 = min(slot0 + valid, z1);
+            overlap = o1 > o0 ? o1 - o0 : 0;
+          }
+          calls += valid - overlap;
+        }
+      }
+      // ---- neighbours
+#pragma unroll
+      for (int q = 0; q < kNbrWs / 32; ++q) {
+        const uint32_t e = lane + 32 * q, slot = slot0 + e;
+        uint32_t j = 0xFFFFFFFFu;
+        if (slot < s.n_rows) j = window ? a.nbr_index[slot] : slot;
+        meta.jrow[e] = j;
+        meta.nub[e] = j != 0xFFFFFFFFu ? __uint_as_float(key_bits(load_key(s.nn + j))) : -1.f;
+        meta.nnorm[e] = j != 0xFFFFFFFFu ? s.row_norms[j] : 0.f;
+      }
+      any_live = __any_sync(0xFFFFFFFFu, any_live);
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) calls += __shfl_xor_sync(0xFFFFFFFFu, calls, d);
+      if (lane == 0) {
+        meta.calls = calls;
+        meta.done = 0;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.meta_full[m]);
+      if (!any_live) break;
+      calls_total += calls;
+      tiles_total += 1;
+#pragma unroll 1
+      for (uint32_t c = 0; c < chunks; ++c) {
+        if (a.pruning && *reinterpret_cast<volatile uint32_t*>(&meta.done) == kConsumerWarps) break;
+        const uint32_t st = seq % kStages16, round = seq / kStages16;
+        if (round >= 1) mbar_wait(&sh.empty[st], (round - 1) & 1);
+        if (lane == 0) {
+          sh.tag_tile[st] = ti;
+          sh.tag_chunk[st] = c;
+          mbar_arrive_expect_tx(&sh.full[st], kStageBytes16);
+          unsigned char* dst = sh.stages[st];
+          // candidate boxes: the interleaved matrix has 2 floats per column; row coordinate = row pair
+          tma_load_box(dst, &map_a, 2 * c * kCols16, cand0 / 2, &sh.full[st]);
+          tma_load_box(dst + kBox16, &map_a, 2 * c * kCols16 + 32, cand0 / 2, &sh.full[st]);
+          tma_load_box(dst + 2 * kBox16, &map_b, c * kCols16, slot0, &sh.full[st]);
+        }
+        ++seq;
+      }
+    }
+    {  // the end-of-work tag
+      const uint32_t st = seq % kStages16, round = seq / kStages16;
+      if (round >= 1) mbar_wait(&sh.empty[st], (round - 1) & 1);
+      if (lane == 0) {
+        sh.tag_tile[st] = kTagDone;
+        mbar_arrive(&sh.full[st]);
+      }
+    }
+    if (lane == 0) {
+      if (calls_total) atomicAdd(&s.counters->calls, calls_total);
+      if (tiles_total) atomicAdd(&s.counters->tiles, tiles_total);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) live_total += __shfl_xor_sync(0xFFFFFFFFu, live_total, d);
+    if (lane == 0 && live_total) atomicAdd(&s.counters->tile_live, live_total);
+    return;
+  }
+
+  // ================================================================== consumer warpgroups
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;");
+  const uint32_t tx = (lane & 7u) | ((warp & 1u) << 3), ty = (lane >> 3) | ((warp >> 1) << 2);
+  constexpr int kTxLanes = 8;
+  const uint32_t cand_of_thread = 16u * ty;  // + 2 i + h
+  uint32_t xa = (ty & 7u) << 4, xb = (tx & 7u) << 4;
+  uint32_t a_row_off = ((ty & 7u) + 64u * (ty >> 3)) * 128u, b_row_off = 2 * kBox16 + tx * 128u;
+  xa = __shfl_sync(0xFFFFFFFFu, xa, lane), xb = __shfl_sync(0xFFFFFFFFu, xb, lane);
+  a_row_off = __shfl_sync(0xFFFFFFFFu, a_row_off, lane), b_row_off = __shfl_sync(0xFFFFFFFFu, b_row_off, lane);
+  float2 acc[kP][kW];
+  uint32_t seq = 0, cur = kTagDone, m = 0, chunks_done = 0;
+  bool released = true, warp_done = false;
+  unsigned long long chunks_total = 0;
+  uint32_t overlap_total = 0;
+#pragma unroll 1
+  for (;;) {
+    const uint32_t st = seq % kStages16, round = seq / kStages16;
+    mbar_wait(&sh.full[st], round & 1);
+    const uint32_t tile = *reinterpret_cast<volatile uint32_t*>(&sh.tag_tile[st]);
+    if (tile == kTagDone) break;
+    const uint32_t c = *reinterpret_cast<volatile uint32_t*>(&sh.tag_chunk[st]);
+    if (tile != cur) {
+      if (!released) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sh.meta_empty[m]);
+      }
+      cur = tile;
+      m = tile & 1;
+      mbar_wait(&sh.meta_full[m], (tile >> 1) & 1);
+      bool none = true;
+#pragma unroll
+      for (int q = 0; q < 2 * kP; ++q) none = none && sh.meta[m].thr[cand_of_thread + q] < 0.f;
+      warp_done = __all_sync(0xFFFFFFFFu, none);
+      if (warp_done && lane == 0 && chunks > 1) atomicAdd(&sh.meta[m].done, 1u);
+#pragma unroll
+      for (int i = 0; i < kP; ++i)
+#pragma unroll
+        for (int w = 0; w < kW; ++w) acc[i][w] = make_float2(0.f, 0.f);
+      released = false;
+      chunks_done = 0;
+    }
+    TileMeta16& meta = sh.meta[m];
+    if (!warp_done) {
+      const unsigned char* a_s = sh.stages[st] + a_row_off;
+      const unsigned char* b_s = sh.stages[st] + b_row_off;
+#pragma unroll 2
+      for (int kc = 0; kc < kCols16 / 4; ++kc) {
+        // columns 4 kc .. 4 kc + 3: candidate box kc >> 2, its 16-byte pieces 2 (kc & 3) and + 1
+        // (a piece = two columns of a row pair); neighbour piece kc
+        const uint32_t a_off0 = (kc >> 2) * kBox16 + ((((kc & 3u) * 2u) << 4) ^ xa);
+        const uint32_t a_off1 = (kc >> 2) * kBox16 + ((((kc & 3u) * 2u + 1u) << 4) ^ xa);
+        const uint32_t b_off = (static_cast<uint32_t>(kc) << 4) ^ xb;
+        float4 b[kW];
+#pragma unroll
+        for (int w = 0; w < kW; ++w) b[w] = *reinterpret_cast<const float4*>(b_s + w * (kTx * 128) + b_off);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float4 a01[kP / 2], a23[kP / 2];
+#pragma unroll
+          for (int p = 0; p < kP / 2; ++p) {
+            a01[p] = *reinterpret_cast<const float4*>(a_s + (h * (kP / 2) + p) * (8 * 128) + a_off0);
+            a23[p] = *reinterpret_cast<const float4*>(a_s + (h * (kP / 2) + p) * (8 * 128) + a_off1);
+          }
+#pragma unroll
+          for (int p = 0; p < kP / 2; ++p)
+#pragma unroll
+            for (int w = 0; w < kW; ++w) {
+              float2& v = acc[h * (kP / 2) + p][w];
+              v = __ffma2_rn(make_float2(a01[p].x, a01[p].y), make_float2(b[w].x, b[w].x), v);
+              v = __ffma2_rn(make_float2(a01[p].z, a01[p].w), make_float2(b[w].y, b[w].y), v);
+              v = __ffma2_rn(make_float2(a23[p].x, a23[p].y), make_float2(b[w].z, b[w].z), v);
+              v = __ffma2_rn(make_float2(a23[p].z, a23[p].w), make_float2(b[w].w, b[w].w), v);
+            }
+        }
+      }
+      ++chunks_done;
+      ++chunks_total;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sh.empty[st]);
+
+    if (c + 1 == chunks) {
+      if (chunks_done == chunks) {
+        // ---- completed tile: d^2 = |a|^2 + |b|^2 + 2 acc (acc = -(a . b)), never below the error bound
+        float nub[kW], bn[kW];
+        uint32_t jrow[kW];
+#pragma unroll
+        for (int w = 0; w < kW; ++w) {
+          nub[w] = kSymmetric ? meta.nub[tx + kTx * w] : -1.f;
+          bn[w] = meta.nnorm[tx + kTx * w];
+          jrow[w] = meta.jrow[tx + kTx * w];
+        }
+        const float d_floor = 0.5f * s.margin_abs;
+        bool hit = false;
+#pragma unroll
+        for (int i = 0; i < kP; ++i)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t l = cand_of_thread + 2 * i + h;
+            const float thr = meta.thr[l], cn = sh.cnorm[l];
+            if (window && thr >= 0.f) {  // self-match pairs of a window tile (see the producer's `calls`)
+              const uint32_t row = sh.cand[l];
+#pragma unroll
+              for (int w = 0; w < kW; ++w) overlap_total += gap_u32(row, jrow[w]) < s.n ? 1u : 0u;
+            }
+#pragma unroll
+            for (int w = 0; w < kW; ++w) {
+              const float d = fmaxf(fmaf(2.f, h ? acc[i][w].y : acc[i][w].x, cn + bn[w]), d_floor);
+              hit = hit || d <= thr || d < nub[w];
+            }
+          }
+        if (__any_sync(0xFFFFFFFFu, hit)) {
+#pragma unroll
+          for (int i = 0; i < kP; ++i)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t l = cand_of_thread + 2 * i + h;
+              const uint32_t row = sh.cand[l];
+              const float thr = meta.thr[l], cn = sh.cnorm[l];
+              uint32_t d_min = 0xFFFFFFFFu, j_min = 0xFFFFFFFFu;
+#pragma unroll
+              for (int w = 0; w < kW; ++w) {
+                const uint32_t j = jrow[w];
+                const float d = fmaxf(fmaf(2.f, h ? acc[i][w].y : acc[i][w].x, cn + bn[w]), d_floor);
+                const bool pair_ok = row != 0xFFFFFFFFu && j != 0xFFFFFFFFu && gap_u32(row, j) >= s.n;
+                if (pair_ok && d <= thr) {
+                  const uint32_t bits = __float_as_uint(d);
+                  if (bits < d_min || (bits == d_min && j < j_min)) {
+                    d_min = bits;
+                    j_min = j;
+                  }
+                }
+                if (pair_ok && d < nub[w])
+                  atomicMin(as_ull(s.nn + j), static_cast<unsigned long long>(nn_key(__float_as_uint(d), row)));
+              }
+              uint32_t g_min = d_min;
+#pragma unroll
+              for (int d = kTxLanes / 2; d > 0; d >>= 1) g_min = min(g_min, __shfl_xor_sync(0xFFFFFFFFu, g_min, d));
+              uint32_t g_j = d_min == g_min ? j_min : 0xFFFFFFFFu;
+#pragma unroll
+              for (int d = kTxLanes / 2; d > 0; d >>= 1) g_j = min(g_j, __shfl_xor_sync(0xFFFFFFFFu, g_j, d));
+              if ((tx & (kTxLanes - 1)) == 0 && g_j != 0xFFFFFFFFu) {
+                atomicMin(as_ull(s.nn + row), static_cast<unsigned long long>(nn_key(g_min, g_j)));
+                atomicMin(reinterpret_cast<uint32_t*>(&sh.loc[l]), g_min);
+              }
+            }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sh.meta_empty[m]);
+      released = true;
+    }
+    ++seq;
+  }
+  if (lane == 0) {
+    const unsigned long long terms = chunks_total * kCols16 * 32ull * (2 * kP) * kW;
+    if (terms) {
+      atomicAdd(&s.counters->terms, terms);
+      atomicAdd(&s.counters->tile_terms, terms);
+      atomicAdd(&s.counters->dot_terms, terms);
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) overlap_total += __shfl_xor_sync(0xFFFFFFFFu, overlap_total, d);
+  if (lane == 0 && overlap_total)
+    atomicAdd(&s.counters->calls, ~static_cast<unsigned long long>(overlap_total) + 1ull);
+}
+
 }  // namespace ws
 
 // Squared norm of every float32 row (padding columns are zero): one warp per row.
@@ -1676,6 +2063,7 @@ bool g_last_launch_was_ws = false;
 bool g_last_launch_was_dot = false;
 bool g_tma_enabled = true;
 bool g_lb_in_ws = false;
+bool g_tile16 = true;
 const char* g_launch_error = nullptr;
 inline uint32_t slot_tiles_of(uint32_t rows) { return (rows + kTileRows - 1) / kTileRows; }
 int g_scan_variant = 0;  // 0: chosen per launch, 1: cp.async + CTA barriers (k_scan_tiles), 2: warp-specialised (k_scan_tiles_ws)
@@ -1734,9 +2122,9 @@ int launch_batch_slots(const uint32_t* d_batch_rows, const uint32_t* d_sel, cons
 }
 
 int launch_gather_rows(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,
-                       uint32_t capacity_padded, bool tma_layout, float* d_batch_matrix, cudaStream_t stream) {
+                       uint32_t capacity_padded, int tma_layout, float* d_batch_matrix, cudaStream_t stream) {
   k_gather_rows<<<blocks_for(static_cast<size_t>(capacity_padded) * 32, 256), 256, 0, stream>>>(
-      s, d_batch_rows, d_sel, capacity_padded, tma_layout ? 1 : 0, d_batch_matrix);
+      s, d_batch_rows, d_sel, capacity_padded, tma_layout, d_batch_matrix);
   return 1;
 }
 
@@ -1755,7 +2143,7 @@ PFN_cuTensorMapEncodeTiled tensor_map_encoder() {
 }
 
 // float32 matrix [n_rows x stride], boxes of 128 rows x 32 columns, 128-byte swizzle
-bool make_row_map(CUtensorMap* map, const float* base, uint64_t n_rows, uint32_t stride) {
+bool make_row_map(CUtensorMap* map, const float* base, uint64_t n_rows, uint64_t stride) {
   PFN_cuTensorMapEncodeTiled encode = tensor_map_encoder();
   if (!encode) return false;
   const cuuint64_t dims[2] = {stride, n_rows};
@@ -1783,6 +2171,8 @@ ScanChoice choose_scan_kernel(const SearchState& s, uint32_t live_upper_bound, b
   // window launches read scattered rows unless the engine keeps a copy of the matrix in the
   // hash-sorted order (it does once a search runs in the dot form)
   c.tma = c.ws && tma_ok && (!window || (c.dot && s.rows_sorted != nullptr));
+  // the dot form on 256-candidate tiles, 16 x 8 pairs per thread, while the batch fills them
+  c.tile16 = c.dot && c.tma && g_tile16 && live_upper_bound > 192;
   return c;
 }
 
@@ -1795,7 +2185,7 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
   const bool lb = choice.lb, use_ws = choice.ws;
   // tile shape: 64-candidate tiles once the batch has shrunk to that, else 128
   const bool narrow = !g_wide_tile && !use_ws && live_upper_bound <= 64;
-  const uint32_t cand_rows = narrow ? 64 : 128;
+  const uint32_t cand_rows = choice.tile16 ? 256 : narrow ? 64 : 128;
   const uint32_t nbr_rows = use_ws ? 128 : g_wide_tile ? 128 : narrow ? 128 : 64;
   const uint32_t cand_tiles = (live_upper_bound + cand_rows - 1) / cand_rows;
   const uint64_t sub_tiles = static_cast<uint64_t>(k_end - k_begin) * (kTileRows / nbr_rows);
@@ -1812,7 +2202,9 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
     CUtensorMap map_a{}, map_b{};
     bool tma = choice.tma;
     if (tma)
-      tma = make_row_map(&map_a, d_batch_matrix, static_cast<uint64_t>(cand_tiles) * kTileRows, s.stride) &&
+      tma = (choice.tile16  // row pairs, two floats per column
+                 ? make_row_map(&map_a, d_batch_matrix, static_cast<uint64_t>(cand_tiles) * 128, 2ull * s.stride)
+                 : make_row_map(&map_a, d_batch_matrix, static_cast<uint64_t>(cand_tiles) * kTileRows, s.stride)) &&
             make_row_map(&map_b, d_nbr_index != nullptr ? s.rows_sorted : s.rows,
                          static_cast<uint64_t>(slot_tiles_of(s.n_rows + 1)) * kTileRows, s.stride);
     if (choice.tma && !tma) {  // the gather already used the tensor-map row order: no way back
@@ -1826,7 +2218,8 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
     };
     auto pick_ws = [&](auto sym) {
       constexpr bool kS = decltype(sym)::value;
-      if (tma && lb) launch_ws(ws::k_scan_tiles_ws<kS, false, true, true>, sizeof(ws::SharedWsT<true, true>));
+      if (choice.tile16) launch_ws(ws::k_scan_tiles_ws16<kS>, sizeof(ws::Shared16));
+      else if (tma && lb) launch_ws(ws::k_scan_tiles_ws<kS, false, true, true>, sizeof(ws::SharedWsT<true, true>));
       else if (tma && choice.dot) launch_ws(ws::k_scan_tiles_ws<kS, true, true>, sizeof(ws::SharedWsT<true>));
       else if (tma) launch_ws(ws::k_scan_tiles_ws<kS, false, true>, sizeof(ws::SharedWsT<true>));
       else if (choice.dot) launch_ws(ws::k_scan_tiles_ws<kS, true, false>, sizeof(ws::SharedWsT<false>));
@@ -1869,6 +2262,7 @@ bool scan_last_launch_was_ws() { return g_last_launch_was_ws; }
 bool scan_last_launch_was_dot() { return g_last_launch_was_dot; }
 void set_tensor_map_loads(bool on) { g_tma_enabled = on; }
 void set_filter_in_ws(bool on) { g_lb_in_ws = on; }
+void set_dot_tile16(bool on) { g_tile16 = on; }
 const char* scan_launch_error() {
   const char* e = g_launch_error;
   g_launch_error = nullptr;

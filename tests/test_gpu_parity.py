@@ -509,6 +509,33 @@ def test_dot_product_form_matches_the_oracle(ctx, chk, seed, kind, n):
     assert_discords_match(chk, x, n, pos, dist, want)
 
 
+@pytest.mark.parametrize("seed,kind,n", FUZZ[::3], ids=[f"{k}-n{n}" for _, k, n in FUZZ[::3]])
+def test_dot_product_form_on_256_candidate_tiles(ctx, chk, seed, kind, n):
+    """k_scan_tiles_ws16 (16 x 8 pairs per thread, candidate rows pairwise interleaved): batches
+    large enough to fill 256-candidate tiles from the first launch on, dot form forced."""
+    rng = np.random.default_rng(11000 + seed)
+    m = int(rng.integers(2 * n + 5000, 2 * n + 9000))
+    w = int(rng.integers(1, min(n, 8) + 1))
+    a = int(rng.integers(2, 7))
+    k = int(rng.integers(1, 4))
+    x = _fuzz_series(rng, kind, m)
+    for name, value in [("dot_form", 2), ("lower_bound", 0), ("first_batch", 4096)]:
+        ctx.set_option(name, value)
+    try:
+        ctx.prepare(x, n, w, a)
+        pos, dist = ctx.search(k)
+        used = ctx.stats()["scan_kernel_dot_launches"]
+        ctx.set_option("dot_tile16", 0)
+        again = ctx.search(k)
+    finally:
+        for name, value in [("dot_form", 1), ("lower_bound", 1), ("first_batch", 128), ("dot_tile16", 1)]:
+            ctx.set_option(name, value)
+    want = chk.topk(x, n, w, a, k)
+    assert_discords_match(chk, x, n, pos, dist, want)
+    assert again[0] == pos and used > 0
+    np.testing.assert_allclose(again[1], dist, rtol=1e-9)
+
+
 def test_dot_product_form_cases_did_run_the_dot_kernel():
     # batches that have shrunk to <= 64 live candidates use the 64-candidate tile kernel instead
     assert len(_DOT_LAUNCHES) == len(FUZZ) and sum(1 for v in _DOT_LAUNCHES if v > 0) >= len(FUZZ) * 3 // 4, _DOT_LAUNCHES
