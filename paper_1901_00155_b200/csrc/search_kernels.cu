@@ -1899,7 +1899,9 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
           jrow[w] = meta.jrow[tx + kTx * w];
         }
         const float d_floor = 0.5f * s.margin_abs;
-        bool hit = false;
+        // which of this thread's 16 candidates have a pair under their own or the neighbour's bound
+        // (tested without the floor: a distance below it can only add a false alarm)
+        uint32_t hits = 0;
 #pragma unroll
         for (int i = 0; i < kP; ++i)
 #pragma unroll
@@ -1911,17 +1913,24 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
 #pragma unroll
               for (int w = 0; w < kW; ++w) overlap_total += gap_u32(row, jrow[w]) < s.n ? 1u : 0u;
             }
+            bool hit = false;
 #pragma unroll
             for (int w = 0; w < kW; ++w) {
-              const float d = fmaxf(fmaf(2.f, h ? acc[i][w].y : acc[i][w].x, cn + bn[w]), d_floor);
+              const float d = fmaf(2.f, h ? acc[i][w].y : acc[i][w].x, cn + bn[w]);
               hit = hit || d <= thr || d < nub[w];
             }
+            hits |= (hit ? 1u : 0u) << (2 * i + h);
           }
-        if (__any_sync(0xFFFFFFFFu, hit)) {
+        // the candidates of a thread row are shared by the 8 lanes of its thread columns
+        uint32_t row_hits = hits;
+#pragma unroll
+        for (int d = kTxLanes / 2; d > 0; d >>= 1) row_hits |= __shfl_xor_sync(0xFFFFFFFFu, row_hits, d);
+        if (__any_sync(0xFFFFFFFFu, row_hits != 0)) {
 #pragma unroll
           for (int i = 0; i < kP; ++i)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
+              if (!__any_sync(0xFFFFFFFFu, (row_hits >> (2 * i + h)) & 1u)) continue;  // (warp-uniform)
               const uint32_t l = cand_of_thread + 2 * i + h;
               const uint32_t row = sh.cand[l];
               const float thr = meta.thr[l], cn = sh.cnorm[l];
@@ -1941,15 +1950,14 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
                 if (pair_ok && d < nub[w])
                   atomicMin(as_ull(s.nn + j), static_cast<unsigned long long>(nn_key(__float_as_uint(d), row)));
               }
+              // smallest distance among the 8 thread columns; the lane(s) holding it publish it (the
+              // 64-bit atomicMin settles a tie towards the smaller neighbour row)
               uint32_t g_min = d_min;
 #pragma unroll
               for (int d = kTxLanes / 2; d > 0; d >>= 1) g_min = min(g_min, __shfl_xor_sync(0xFFFFFFFFu, g_min, d));
-              uint32_t g_j = d_min == g_min ? j_min : 0xFFFFFFFFu;
-#pragma unroll
-              for (int d = kTxLanes / 2; d > 0; d >>= 1) g_j = min(g_j, __shfl_xor_sync(0xFFFFFFFFu, g_j, d));
-              if ((tx & (kTxLanes - 1)) == 0 && g_j != 0xFFFFFFFFu) {
-                atomicMin(as_ull(s.nn + row), static_cast<unsigned long long>(nn_key(g_min, g_j)));
-                atomicMin(reinterpret_cast<uint32_t*>(&sh.loc[l]), g_min);
+              if (d_min == g_min && j_min != 0xFFFFFFFFu) {
+                atomicMin(as_ull(s.nn + row), static_cast<unsigned long long>(nn_key(d_min, j_min)));
+                atomicMin(reinterpret_cast<uint32_t*>(&sh.loc[l]), d_min);
               }
             }
         }
