@@ -1899,8 +1899,13 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
           jrow[w] = meta.jrow[tx + kTx * w];
         }
         const float d_floor = 0.5f * s.margin_abs;
-        // which of this thread's 16 candidates have a pair under their own or the neighbour's bound
-        // (tested without the floor: a distance below it can only add a false alarm)
+        // Which of this thread's 16 candidates can have a pair under their own or a neighbour's
+        // bound?  A cheap sufficient test per candidate: its smallest accumulator against ONE limit,
+        // max(thr, greatest neighbour bound) - |a|^2 - smallest |b|^2 (no floor: a distance below
+        // it can only add a false alarm).  Flagged candidates are then measured pair by pair.
+        float nub_max = nub[0], bn_min = bn[0];
+#pragma unroll
+        for (int w = 1; w < kW; ++w) nub_max = fmaxf(nub_max, nub[w]), bn_min = fminf(bn_min, bn[w]);
         uint32_t hits = 0;
 #pragma unroll
         for (int i = 0; i < kP; ++i)
@@ -1913,12 +1918,10 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
 #pragma unroll
               for (int w = 0; w < kW; ++w) overlap_total += gap_u32(row, jrow[w]) < s.n ? 1u : 0u;
             }
-            bool hit = false;
+            float a_min = h ? acc[i][0].y : acc[i][0].x;
 #pragma unroll
-            for (int w = 0; w < kW; ++w) {
-              const float d = fmaf(2.f, h ? acc[i][w].y : acc[i][w].x, cn + bn[w]);
-              hit = hit || d <= thr || d < nub[w];
-            }
+            for (int w = 1; w < kW; ++w) a_min = fminf(a_min, h ? acc[i][w].y : acc[i][w].x);
+            const bool hit = fmaf(2.f, a_min, cn + bn_min) <= fmaxf(thr, nub_max);
             hits |= (hit ? 1u : 0u) << (2 * i + h);
           }
         // the candidates of a thread row are shared by the 8 lanes of its thread columns
