@@ -160,6 +160,8 @@ struct tsdd_cuda_ctx {
   bool opt_tile16 = true;           // dot form: 256-candidate tiles, 16 x 8 pairs per thread (k_scan_tiles_ws16)
   bool opt_tensor_map = true;       // covering scans of the ws kernel load tiles as TMA boxes
   int opt_dot = 1;
+  double opt_dot_growth = 1.3;      // ... range growth of a dot-form batch: no abandoning inside tiles, so dead
+                                    // candidates cost full price until the next compaction — compact more often
   int opt_dot_window_rounds = 4;    // ... of a batch in the dot-product form whose window tiles load as tensor-map boxes                  // dot-product form of the ws kernel: 0 never, 1 when it pays, 2 always
 
   // prepared series
@@ -588,7 +590,8 @@ std::vector<Segment> plan_segments(const tsdd_cuda_ctx* ctx, bool pruning) {
     }
   }
   const std::vector<uint32_t> bounds =
-      range_bounds(ctx->rows, ctx->opt_rounds, ctx->opt_first_range, ctx->opt_growth, pruning);
+      range_bounds(ctx->rows, ctx->opt_rounds, ctx->opt_first_range,
+                   ctx->dot_now ? std::min(ctx->opt_growth, ctx->opt_dot_growth) : ctx->opt_growth, pruning);
   for (size_t r = 0; r + 1 < bounds.size(); ++r)
     plan.push_back({false, bounds[r] / tile, (bounds[r + 1] + tile - 1) / tile});
   return plan;
@@ -1084,6 +1087,9 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
     } else if (key == "seed_rows") {
       if (value < 0 || value > 1048576) fail(TSDD_ERR_PARAMETER, "seed_rows must be in 0..1048576");
       ctx->opt_seed_rows = static_cast<uint32_t>(value);
+    } else if (key == "dot_growth") {
+      if (value < 1.0 || value > 16.0) fail(TSDD_ERR_PARAMETER, "dot_growth must be in 1..16");
+      ctx->opt_dot_growth = value;
     } else if (key == "dot_window_rounds") {
       if (value < 0 || value > 64) fail(TSDD_ERR_PARAMETER, "dot_window_rounds must be in 0..64");
       ctx->opt_dot_window_rounds = static_cast<int>(value);

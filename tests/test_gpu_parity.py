@@ -182,7 +182,8 @@ def test_search_is_repeatable_and_independent_of_tunables(ctx):
                         ("symmetric", 0), ("packed", 0), ("first_batch", 4096), ("wide_tile", 1), ("kernel", 2), ("kernel", 1),
                         ("window_rounds", 0), ("rotate", 0), ("growth", 3.0), ("first_range", 128),
                         ("lower_bound", 0), ("margin_delta", 1e-3), ("batch_growth", 2), ("dot_form", 2),
-                        ("dot_form", 0), ("seed_rows", 0), ("tensor_map", 0), ("dot_window_rounds", 0),
+                        ("dot_form", 0), ("seed_rows", 0), ("tensor_map", 0), ("dot_window_rounds", 0), ("dot_growth", 2.0),
+                        ("dot_tile16", 0),
                         ("window_rounds", 4)]:
         ctx.set_option(name, value)
         again = ctx.search(3)
@@ -192,7 +193,8 @@ def test_search_is_repeatable_and_independent_of_tunables(ctx):
                         ("packed", 1), ("first_batch", 128), ("wide_tile", 0), ("kernel", 0),
                         ("window_rounds", 2), ("rotate", 1), ("growth", 1.5), ("first_range", 8192),
                         ("lower_bound", 1), ("margin_delta", -1), ("batch_growth", 8), ("dot_form", 1),
-                        ("seed_rows", 4096), ("tensor_map", 1), ("dot_window_rounds", 4)]:
+                        ("seed_rows", 4096), ("tensor_map", 1), ("dot_window_rounds", 4), ("dot_growth", 1.3),
+                        ("dot_tile16", 1)]:
         ctx.set_option(name, value)
 
 
