@@ -12,6 +12,15 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (run on the B200 box via gpurun)")
 
 
+@pytest.fixture(scope="session", autouse=True)
+def _built_tree():
+    """The in-tree build outputs are not tracked: build whatever is missing or stale (nvcc
+    cross-compiles sm_100a without a GPU) before the first test needs the library or the CLI."""
+    from paper_1901_00155_b200 import build as native
+
+    native.build_all()
+
+
 @pytest.fixture(scope="session")
 def golden():
     import json
