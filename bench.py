@@ -285,8 +285,9 @@ def run_cuda_arm(args) -> None:
                     "d2h_bytes_per_step": int(k * 16 + 160), "topk_time_s": e2e_s / args.steps},
             "gpu_launches": int(totals["launches"]),
             "roofline": {"bound": "fp32",
-                         "kernel": "k_scan_tiles_ws + k_scan_tiles (the tile kernels: %d of %d launches "
-                                   "warp-specialised, %d of those in the dot-product form)"
+                         "kernel": "k_scan_tiles_ws16 / k_scan_tiles_ws / k_scan_tiles (the tile kernels: %d of %d "
+                                   "launches warp-specialised, %d of those in the dot-product form, which "
+                                   "runs on k_scan_tiles_ws16 while a batch fills 256-candidate tiles)"
                                    % (totals["ws_launches"], totals["scan_launches"], totals["dot_launches"]),
                          "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
