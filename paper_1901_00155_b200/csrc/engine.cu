@@ -137,7 +137,7 @@ struct tsdd_cuda_ctx {
   uint32_t opt_batch_growth = 8;
   int opt_rounds = 64;            // upper limit on neighbour ranges per batch
   uint32_t opt_first_range = 8192;  // rows in the first range
-  double opt_growth = 1.5;          // each range is this much larger than the one before
+  double opt_growth = 2.0;          // each range is this much larger than the one before (dot form: opt_dot_growth)
   int opt_window_rounds = 2;        // same-word-neighbourhood rounds before the covering scan
   uint32_t opt_window_first = 2048; // slots in the first of them
   double opt_window_growth = 3.0;
