@@ -668,7 +668,11 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
 // Whether early abandoning inside tiles has been worth anything so far in this search
 // (< 5 % of the started pair distances were cut short): then the dot-product form, which
 // cannot abandon inside a tile but needs half the FP32 instructions, is the better kernel.
+// Only asked once the lower-bound filter has been found useless on this input as well (or is
+// switched off): where the filter rules tiles out, covering scans stay with it and the dot
+// form would only reach the window rounds.
 bool few_abandoned(tsdd_cuda_ctx* ctx) {
+  if (ctx->opt_lower_bound && !(ctx->lb_decided && !ctx->lb_active)) return false;
   DeviceCounters c{};
   CUDA_OK(cudaMemcpyAsync(&c, ctx->counters.ptr, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
   sync_stream(ctx);
