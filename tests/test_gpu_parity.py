@@ -538,6 +538,39 @@ def test_dot_product_form_on_256_candidate_tiles(ctx, chk, seed, kind, n):
     np.testing.assert_allclose(again[1], dist, rtol=1e-9)
 
 
+def _hard_series(kind, m, rng):
+    if kind == "spikes":      # a few huge outliers: windows whose energy sits in one sample
+        x = rng.standard_normal(m).astype(np.float32)
+        x[rng.integers(0, m, 12)] += np.float32(1e4)
+        return x
+    if kind == "offset":      # small noise on a large offset: mean^2 / variance ~ 1e10
+        return (np.float32(1e4) + np.float32(0.1) * rng.standard_normal(m)).astype(np.float32)
+    if kind == "steps":       # piecewise constant with noise: many near-flat windows
+        x = np.repeat(rng.integers(-3, 4, m // 500 + 1), 500)[:m].astype(np.float32)
+        return x + np.float32(1e-3) * rng.standard_normal(m).astype(np.float32)
+    if kind == "ramp":        # strong trend
+        return (np.arange(m, dtype=np.float32) * np.float32(0.01) + rng.standard_normal(m).astype(np.float32))
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("dot", [1, 2])
+@pytest.mark.parametrize("kind", ["spikes", "offset", "steps", "ramp"])
+def test_awkward_value_distributions(ctx, chk, kind, dot):
+    """Inputs that stress the float32 matrix and the dot-product form's absolute error band."""
+    rng = np.random.default_rng({"spikes": 31, "offset": 32, "steps": 33, "ramp": 34}[kind])
+    x = _hard_series(kind, 12000, rng)
+    for name, value in [("dot_form", dot), ("first_batch", 1024 if dot == 2 else 128)]:
+        ctx.set_option(name, value)
+    try:
+        ctx.prepare(x, 96, 6, 4)
+        pos, dist = ctx.search(3)
+    finally:
+        ctx.set_option("dot_form", 1)
+        ctx.set_option("first_batch", 128)
+    want = chk.topk(x, 96, 6, 4, 3)
+    assert_discords_match(chk, x, 96, pos, dist, want)
+
+
 def test_dot_product_form_cases_did_run_the_dot_kernel():
     # batches that have shrunk to <= 64 live candidates use the 64-candidate tile kernel instead
     assert len(_DOT_LAUNCHES) == len(FUZZ) and sum(1 for v in _DOT_LAUNCHES if v > 0) >= len(FUZZ) * 3 // 4, _DOT_LAUNCHES
