@@ -1,0 +1,52 @@
+"""Randomised soak of the CUDA engine against the CPU oracle (not part of the test suite):
+   python tools/soak.py [cases] [seed]"""
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import oracle  # noqa: E402
+from paper_1901_00155_b200 import Context  # noqa: E402
+
+
+def main():
+    cases = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+    rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+    chk = oracle.best()
+    bad = 0
+    with Context(0) as ctx:
+        for c in range(cases):
+            kind = rng.choice(["noise", "walk", "sine"])
+            m = int(rng.integers(15000, 45000))
+            n = int(rng.choice([24, 50, 64, 100, 128, 200, 256, 300]))
+            w = int(rng.integers(2, 9))
+            a = int(rng.integers(2, 7))
+            k = int(rng.integers(1, 4))
+            if kind == "noise":
+                x = rng.random(m).astype(np.float32)
+            elif kind == "walk":
+                x = np.cumsum(rng.standard_normal(m)).astype(np.float32)
+            else:
+                t = np.arange(m)
+                x = (np.sin(2 * np.pi * t / rng.integers(20, 200)) + 0.3 * rng.standard_normal(m)).astype(np.float32)
+            opts = {"dot_form": int(rng.choice([1, 2])), "first_batch": int(rng.choice([128, 4096])),
+                    "lower_bound": int(rng.choice([0, 1])), "filter_in_ws": int(rng.choice([0, 1]))}
+            for name, value in opts.items():
+                ctx.set_option(name, value)
+            t0 = time.time()
+            ctx.prepare(x, n, w, a)
+            pos, dist = ctx.search(k)
+            t1 = time.time()
+            want = chk.topk(x, n, w, a, k)
+            ok = pos == want["positions"] and np.allclose(dist, want["distances"], rtol=1e-4)
+            st = ctx.stats()
+            print(c, kind, m, n, w, a, k, opts, "ok" if ok else f"MISMATCH {pos} {want['positions']}",
+                  f"gpu {t1 - t0:.3f}s cpu {time.time() - t1:.1f}s dot {st['scan_kernel_dot_launches']}", flush=True)
+            bad += 0 if ok else 1
+    print("mismatches:", bad)
+    return 1 if bad else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
