@@ -52,6 +52,13 @@ def _run(cmd: list[str]) -> None:
 def build_cuda(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     target = os.path.join(LIB, "libtsdd_cuda.so")
+    # objects built with other flags (TSDD_NVCC_EXTRA) are stale whatever their age
+    stamp = os.path.join(OBJ, "flags.txt")
+    flags = " ".join(NVCC_FLAGS)
+    if not os.path.exists(stamp) or open(stamp).read() != flags:
+        force = True
+        with open(stamp, "w") as f:
+            f.write(flags)
     headers = [h if os.path.isabs(h) else os.path.join(CSRC, h) for h in CUDA_HEADERS]
     objects = []
     for src in CUDA_SOURCES:

@@ -1630,10 +1630,19 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
 //   term is one constant per thread), neighbours tx + 16 w, w < 8; candidate 16 ty + 2 i + h of
 //   the tile sits in half h of that pair (tma16_pair_of_candidate).
 constexpr int kCand16 = 256;
-constexpr int kCols16 = 32;
-constexpr int kStages16 = 4;
+#ifndef TSDD_WS16_COLS
+#define TSDD_WS16_COLS 32
+#endif
+#ifndef TSDD_WS16_STAGES
+#define TSDD_WS16_STAGES 4
+#endif
+
+constexpr int kCols16 = TSDD_WS16_COLS;             // columns per stage
+constexpr int kStages16 = TSDD_WS16_STAGES;
 constexpr int kBox16 = 128 * 128;                   // bytes of one box: 128 rows of 128 bytes
-constexpr int kStageBytes16 = 3 * kBox16;
+constexpr int kABoxes16 = kCols16 / 16;             // candidate boxes per stage: 16 columns x 2 rows of a pair each
+constexpr int kBBoxes16 = kCols16 / 32;             // neighbour boxes per stage: 32 columns each
+constexpr int kStageBytes16 = (kABoxes16 + kBBoxes16) * kBox16;
 
 struct alignas(16) TileMeta16 {
   float thr[kCand16];
@@ -1781,9 +1790,12 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
           mbar_arrive_expect_tx(&sh.full[st], kStageBytes16);
           unsigned char* dst = sh.stages[st];
           // candidate boxes: the interleaved matrix has 2 floats per column; row coordinate = row pair
-          tma_load_box(dst, &map_a, 2 * c * kCols16, cand0 / 2, &sh.full[st]);
-          tma_load_box(dst + kBox16, &map_a, 2 * c * kCols16 + 32, cand0 / 2, &sh.full[st]);
-          tma_load_box(dst + 2 * kBox16, &map_b, c * kCols16, slot0, &sh.full[st]);
+#pragma unroll
+          for (int q = 0; q < kABoxes16; ++q)
+            tma_load_box(dst + q * kBox16, &map_a, 2 * c * kCols16 + 32 * q, cand0 / 2, &sh.full[st]);
+#pragma unroll
+          for (int q = 0; q < kBBoxes16; ++q)
+            tma_load_box(dst + (kABoxes16 + q) * kBox16, &map_b, c * kCols16 + 32 * q, slot0, &sh.full[st]);
         }
         ++seq;
       }
@@ -1812,7 +1824,7 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
   constexpr int kTxLanes = 8;
   const uint32_t cand_of_thread = 16u * ty;  // + 2 i + h
   uint32_t xa = (ty & 7u) << 4, xb = (tx & 7u) << 4;
-  uint32_t a_row_off = ((ty & 7u) + 64u * (ty >> 3)) * 128u, b_row_off = 2 * kBox16 + tx * 128u;
+  uint32_t a_row_off = ((ty & 7u) + 64u * (ty >> 3)) * 128u, b_row_off = kABoxes16 * kBox16 + tx * 128u;
   xa = __shfl_sync(0xFFFFFFFFu, xa, lane), xb = __shfl_sync(0xFFFFFFFFu, xb, lane);
   a_row_off = __shfl_sync(0xFFFFFFFFu, a_row_off, lane), b_row_off = __shfl_sync(0xFFFFFFFFu, b_row_off, lane);
   float2 acc[kP][kW];
@@ -1857,7 +1869,7 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
         // (a piece = two columns of a row pair); neighbour piece kc
         const uint32_t a_off0 = (kc >> 2) * kBox16 + ((((kc & 3u) * 2u) << 4) ^ xa);
         const uint32_t a_off1 = (kc >> 2) * kBox16 + ((((kc & 3u) * 2u + 1u) << 4) ^ xa);
-        const uint32_t b_off = (static_cast<uint32_t>(kc) << 4) ^ xb;
+        const uint32_t b_off = (kc >> 3) * kBox16 + (((static_cast<uint32_t>(kc) & 7u) << 4) ^ xb);
         float4 b[kW];
 #pragma unroll
         for (int w = 0; w < kW; ++w) b[w] = *reinterpret_cast<const float4*>(b_s + w * (kTx * 128) + b_off);
