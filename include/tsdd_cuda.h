@@ -107,6 +107,7 @@ int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream);
  * the dot-product form, of window rounds, from a copy of the matrix kept in the hash-sorted
  * order — as cp.async.bulk.tensor boxes instead of one bulk copy per row),
  * "dot_window_rounds" (window rounds of a dot-form batch whose window tiles load that way),
+ * "dot_window_growth" (growth of those rounds, at most "window_growth"),
  * "dot_growth" (range growth of a dot-form batch, at most "growth": without abandoning inside
  * tiles a dead candidate costs full price until the next compaction),
  * "dot_tile16" (0/1: the dot-product form runs on 256-candidate tiles with 16 x 8 pairs per

@@ -162,7 +162,8 @@ struct tsdd_cuda_ctx {
   int opt_dot = 1;
   double opt_dot_growth = 1.3;      // ... range growth of a dot-form batch: no abandoning inside tiles, so dead
                                     // candidates cost full price until the next compaction — compact more often
-  int opt_dot_window_rounds = 4;    // ... of a batch in the dot-product form whose window tiles load as tensor-map boxes                  // dot-product form of the ws kernel: 0 never, 1 when it pays, 2 always
+  double opt_dot_window_growth = 1.6;
+  int opt_dot_window_rounds = 8;    // ... of a batch in the dot-product form whose window tiles load as tensor-map boxes                  // dot-product form of the ws kernel: 0 never, 1 when it pays, 2 always
 
   // prepared series
   bool prepared = false;
@@ -579,14 +580,18 @@ std::vector<Segment> plan_segments(const tsdd_cuda_ctx* ctx, bool pruning) {
     uint32_t at = 0;
     // Window tiles of a dot-form batch stream at the full rate of the covering scan (tensor-map
     // boxes from the hash-sorted copy of the matrix), and on the noise-like inputs that run in
-    // the dot form more rounds pay; the direct form feeds them with per-row copies.
-    const int window_rounds = (ctx->dot_now && ctx->sorted_ready) ? std::max(ctx->opt_window_rounds, ctx->opt_dot_window_rounds)
-                                                                  : ctx->opt_window_rounds;
+    // the dot form more rounds pay; the direct form feeds them with per-row copies.  They also
+    // grow more gently there: nothing is abandoned inside a dot-form tile, so a candidate that
+    // dies costs full price until the round ends (the widest round of a 3x schedule ran with a
+    // quarter of its candidate slots dead).
+    const bool dot_windows = ctx->dot_now && ctx->sorted_ready;
+    const int window_rounds = dot_windows ? std::max(ctx->opt_window_rounds, ctx->opt_dot_window_rounds) : ctx->opt_window_rounds;
+    const double window_growth = dot_windows ? std::min(ctx->opt_window_growth, ctx->opt_dot_window_growth) : ctx->opt_window_growth;
     for (int r = 0; r < window_rounds && at < window_limit; ++r) {
       const uint32_t upto = std::min<uint64_t>(window_limit, at + static_cast<uint64_t>(size) / tile);
       plan.push_back({true, at, upto});
       at = upto;
-      size *= ctx->opt_window_growth;
+      size *= window_growth;
     }
   }
   const std::vector<uint32_t> bounds =
@@ -1094,6 +1099,9 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
     } else if (key == "dot_growth") {
       if (value < 1.0 || value > 16.0) fail(TSDD_ERR_PARAMETER, "dot_growth must be in 1..16");
       ctx->opt_dot_growth = value;
+    } else if (key == "dot_window_growth") {
+      if (value < 1.0 || value > 16.0) fail(TSDD_ERR_PARAMETER, "dot_window_growth must be in 1..16");
+      ctx->opt_dot_window_growth = value;
     } else if (key == "dot_window_rounds") {
       if (value < 0 || value > 64) fail(TSDD_ERR_PARAMETER, "dot_window_rounds must be in 0..64");
       ctx->opt_dot_window_rounds = static_cast<int>(value);

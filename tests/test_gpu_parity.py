@@ -193,7 +193,7 @@ def test_search_is_repeatable_and_independent_of_tunables(ctx):
                         ("packed", 1), ("first_batch", 128), ("wide_tile", 0), ("kernel", 0),
                         ("window_rounds", 2), ("rotate", 1), ("growth", 2.0), ("first_range", 8192),
                         ("lower_bound", 1), ("margin_delta", -1), ("batch_growth", 8), ("dot_form", 1),
-                        ("seed_rows", 4096), ("tensor_map", 1), ("dot_window_rounds", 4), ("dot_growth", 1.3),
+                        ("seed_rows", 4096), ("tensor_map", 1), ("dot_window_rounds", 8), ("dot_growth", 1.3),
                         ("dot_tile16", 1)]:
         ctx.set_option(name, value)
 
