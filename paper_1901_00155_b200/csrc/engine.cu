@@ -632,7 +632,8 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
   const std::vector<Segment> plan = plan_segments(ctx, pruning);
   for (size_t r = 0; r < plan.size(); ++r) {
     if (r > 0 && pruning) {
-      launches += launch_compact_batch(s, list, slots, list_alt, slots_alt, pruning, ctx->sel.ptr, st);
+      launches += launch_compact_batch(s, list, slots, list_alt, slots_alt, pruning, ctx->sel.ptr, count,
+                                       ctx->flags.ptr, st);
       std::swap(list, list_alt);
       std::swap(slots, slots_alt);
       uint32_t* slot_now = ctx->h_sel + 4 + 4 * (r & 3);

@@ -110,7 +110,8 @@ int launch_select_batch(SearchState s, const uint32_t* d_order, uint32_t cursor,
 // Drops dead candidates from the batch list (stable); rows and hash-order slots move
 // together; count lives in d_sel[0].
 int launch_compact_batch(SearchState s, uint32_t* d_batch_rows, uint32_t* d_batch_slots, uint32_t* d_rows_alt,
-                         uint32_t* d_slots_alt, bool pruning, uint32_t* d_sel, cudaStream_t stream);
+                         uint32_t* d_slots_alt, bool pruning, uint32_t* d_sel, uint32_t live_upper_bound,
+                         uint32_t* d_scratch, cudaStream_t stream);
 
 // slot_of_row = inverse permutation of the hash-sorted row list.
 int launch_invert_order(const uint32_t* d_sorted_row, uint32_t rows, uint32_t* d_slot_of_row,

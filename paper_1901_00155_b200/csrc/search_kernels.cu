@@ -296,6 +296,62 @@ k_compact_batch(SearchState s, const uint32_t* __restrict__ in, const uint32_t* 
   if (threadIdx.x == 0) sel[0] = carry;
 }
 
+// The same compaction over many blocks, for batches worth it: k_compact_flag marks the entries
+// that stay and counts them per block of 1,024; k_compact_scatter places each block after the
+// ones before it (stable), the last block stores the new size.  Both read the size from sel[0];
+// nothing else runs on the stream in between, so the marks are the ones the counts were made of.
+__global__ void __launch_bounds__(1024)
+k_compact_flag(SearchState s, const uint32_t* __restrict__ in, int pruning, const uint32_t* __restrict__ sel,
+               uint32_t* __restrict__ keep_flags, uint32_t* __restrict__ block_counts) {
+  const uint32_t count = sel[0];
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  bool keep = false;
+  if (idx < count) keep = !pruning || !is_dead(load_key(s.nn + in[idx]), *s.best, s.margin, s.margin_abs);
+  if (idx < count) keep_flags[idx] = keep ? 1u : 0u;
+  const int kept = __syncthreads_count(keep);
+  if (threadIdx.x == 0) block_counts[blockIdx.x] = static_cast<uint32_t>(kept);
+}
+
+__global__ void __launch_bounds__(1024)
+k_compact_scatter(const uint32_t* __restrict__ in, const uint32_t* __restrict__ in_slots,
+                  uint32_t* __restrict__ out, uint32_t* __restrict__ out_slots,
+                  const uint32_t* __restrict__ keep_flags, const uint32_t* __restrict__ block_counts,
+                  uint32_t* sel) {
+  __shared__ uint32_t warp_sums[32];
+  __shared__ uint32_t s_base;
+  const uint32_t count = sel[0];
+  const uint32_t blocks_used = (count + blockDim.x - 1) / blockDim.x;
+  if (blockIdx.x >= blocks_used && !(blockIdx.x == 0 && count == 0)) return;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp == 0) {  // entries kept by the blocks before this one (at most a few hundred counts)
+    uint32_t before = 0;
+    for (uint32_t b = lane; b < blockIdx.x; b += 32) before += block_counts[b];
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) before += __shfl_xor_sync(0xFFFFFFFFu, before, d);
+    if (lane == 0) s_base = before;
+  }
+  const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool keep = idx < count && keep_flags[idx] != 0;
+  const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, keep);
+  if (lane == 0) warp_sums[warp] = __popc(ballot);
+  __syncthreads();
+  uint32_t before = s_base;
+  for (uint32_t w = 0; w < warp; ++w) before += warp_sums[w];
+  if (keep) {
+    const uint32_t at = before + __popc(ballot & ((1u << lane) - 1u));
+    out[at] = in[idx];
+    out_slots[at] = in_slots[idx];
+  }
+  __syncthreads();
+  if (blockIdx.x + 1 == max(blocks_used, 1u) && threadIdx.x == 0) {
+    uint32_t total = s_base;
+    for (uint32_t w = 0; w < blockDim.x / 32; ++w) total += warp_sums[w];
+    sel[2] = total;  // parked: other blocks may still be reading sel[0]; k_compact_publish moves it there
+  }
+}
+
+__global__ void k_compact_publish(uint32_t* sel) { sel[0] = sel[2]; }
+
 // slot_of_row[sorted_row[s]] = s: where each row sits in the hash-sorted order.
 __global__ void k_invert_order(const uint32_t* __restrict__ sorted_row, uint32_t rows,
                                uint32_t* __restrict__ slot_of_row) {
@@ -2126,7 +2182,18 @@ int launch_select_batch(SearchState s, const uint32_t* d_order, uint32_t cursor,
 }
 
 int launch_compact_batch(SearchState s, uint32_t* d_batch_rows, uint32_t* d_batch_slots, uint32_t* d_rows_alt,
-                         uint32_t* d_slots_alt, bool pruning, uint32_t* d_sel, cudaStream_t stream) {
+                         uint32_t* d_slots_alt, bool pruning, uint32_t* d_sel, uint32_t live_upper_bound,
+                         uint32_t* d_scratch, cudaStream_t stream) {
+  if (live_upper_bound > 4096 && d_scratch != nullptr) {  // many blocks: flags, per-block counts, scatter, publish
+    const unsigned blocks = (live_upper_bound + 1023) / 1024;
+    uint32_t* d_flags = d_scratch;
+    uint32_t* d_counts = d_scratch + static_cast<size_t>(blocks) * 1024;
+    k_compact_flag<<<blocks, 1024, 0, stream>>>(s, d_batch_rows, pruning ? 1 : 0, d_sel, d_flags, d_counts);
+    k_compact_scatter<<<blocks, 1024, 0, stream>>>(d_batch_rows, d_batch_slots, d_rows_alt, d_slots_alt, d_flags,
+                                                   d_counts, d_sel);
+    k_compact_publish<<<1, 1, 0, stream>>>(d_sel);
+    return 3;
+  }
   k_compact_batch<<<1, 1024, 0, stream>>>(s, d_batch_rows, d_batch_slots, d_rows_alt, d_slots_alt,
                                           pruning ? 1 : 0, d_sel);
   return 1;
