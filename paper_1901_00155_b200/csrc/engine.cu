@@ -682,6 +682,7 @@ bool few_abandoned(tsdd_cuda_ctx* ctx) {
   DeviceCounters c{};
   CUDA_OK(cudaMemcpyAsync(&c, ctx->counters.ptr, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
   sync_stream(ctx);
+  if (ctx->stats.batches < 2) return c.calls > 0 && c.abandoned == 0;  // after one batch: only if nothing at all
   return c.calls > 0 && c.abandoned * 20 < c.calls;
 }
 
@@ -708,13 +709,17 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
       if (count > 0) {
         // After two batches, see what the lower-bound filter has ruled out so far; on inputs
         // where it finds nothing (noise), the rest of the search runs the kernel without it.
-        if (pruning && ctx->opt_lower_bound && !ctx->lb_decided && ctx->stats.batches >= 2) {
+        // (After ONE batch only on the plainest evidence: not a single pair ruled out.  Anything
+        // less than that waits for the second batch — cfg 4 looks harmless after its first.)
+        if (pruning && ctx->opt_lower_bound && !ctx->lb_decided && ctx->stats.batches >= 1) {
           DeviceCounters c{};
           CUDA_OK(cudaMemcpyAsync(&c, ctx->counters.ptr, sizeof(c), cudaMemcpyDeviceToHost, st));
           sync_stream(ctx);
-          ctx->lb_active = c.lb_skipped * 20 >= c.lb_skipped + c.tile_live;  // >= 5 % of (candidate, tile) pairs
-          ctx->lb_decided = true;
-          s = ctx->state();
+          if (ctx->stats.batches >= 2 || (c.lb_skipped == 0 && c.tile_live > 0)) {
+            ctx->lb_active = c.lb_skipped * 20 >= c.lb_skipped + c.tile_live;  // >= 5 % of (candidate, tile) pairs
+            ctx->lb_decided = true;
+            s = ctx->state();
+          }
         }
         if ((pruning && ctx->opt_dot) || ctx->opt_dot == 2) {
           // Dot form or not, for this batch.  One rank decides from its own counters; several
@@ -722,7 +727,7 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
           // on every rank before dot-form bounds travel between them).
           const bool alone = !(ctx->world > 1 || ctx->comm);
           CUDA_OK(cudaMemcpyAsync(ctx->h_keys + 3, ctx->best.ptr, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-          if (alone && !ctx->dot_wanted && ctx->stats.batches >= 2) ctx->dot_wanted = few_abandoned(ctx);
+          if (alone && !ctx->dot_wanted && ctx->stats.batches >= 1) ctx->dot_wanted = few_abandoned(ctx);
           sync_stream(ctx);
           const uint64_t best_now = ctx->h_keys[3];
           if (alone && ctx->dot_wanted && ctx->dot_eligible(best_now)) ctx->dot_used = true;
@@ -758,7 +763,7 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
       sync_stream(ctx);
       ctx->h_keys[1] = cursor < ctx->rows ? 1 : 0;
       ctx->h_keys[2] = 0;
-      if (pruning && ctx->opt_dot && !ctx->dot_wanted && ctx->stats.batches >= 2) ctx->h_keys[2] = few_abandoned(ctx) ? 1 : 0;
+      if (pruning && ctx->opt_dot && !ctx->dot_wanted && ctx->stats.batches >= 1) ctx->h_keys[2] = few_abandoned(ctx) ? 1 : 0;
       exchange_keys(ctx, ctx->h_keys, 3);
       CUDA_OK(cudaMemcpyAsync(ctx->best.ptr, ctx->h_keys, sizeof(uint64_t), cudaMemcpyHostToDevice, st));
       if (ctx->h_keys[2]) ctx->dot_wanted = true;  // the same on every rank, like the best-so-far
