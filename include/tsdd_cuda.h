@@ -66,6 +66,9 @@ typedef struct tsdd_cuda_stats {
   uint64_t scan_kernel_ws_launches; /* of scan_kernel_launches, those of the warp-specialised kernel */
   uint64_t scan_kernel_dot_launches; /* of those, launches of its dot-product form (one FFMA per term) */
   uint64_t scan_kernel_dot_terms;   /* of scan_kernel_terms, those computed as one FFMA */
+  uint64_t finalists;      /* rows settled in float64 at the end of the passes (near-ties of the float32 search) */
+  uint64_t exact_reruns;   /* of those, measured again from +inf because the float32 start bound was too low */
+  uint64_t useful_terms;   /* of scan_kernel_terms: terms of pairs that were live, non-self and not padding */
 } tsdd_cuda_stats;
 
 /* ---- lifetime ------------------------------------------------------------ */
@@ -93,7 +96,10 @@ int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream);
  * neighbourhood in the hash-sorted order: window_first slots, growing), "bucket_mates" (same-word
  * neighbours tried per row before the scans), "rescore" (0/1: decide each pass
  * among the near-tied finalists by their exact float64 nn distance),
- * "margin_delta" (safety band of the float32 discard test; negative = from n), "symmetric" (0/1: completed tiles
+ * "margin_delta" (relative safety band of the float32 discard test; negative = from n),
+ * "margin_q" (its part proportional to sqrt(best-so-far), for the float32 quantisation of the
+ * rows; negative = from n), "finalist_cap" (room of the first collection of near-tied
+ * finalists; a pass with more collects again and still settles all of them), "symmetric" (0/1: completed tiles
  * also lower the neighbours' bounds), "packed" (0/1: f32x2 arithmetic),
  * "wide_tile" (0/1: 128 x 128 tiles, one CTA per SM, instead of 128 x 64, two),
  * "kernel" (0: per launch; 1: the cp.async tile kernel everywhere; 2: the

@@ -42,11 +42,26 @@ __host__ __device__ __forceinline__ uint32_t best_key_row(uint64_t key) {
 // (search_kernels.cu: k_scan_tiles_ws<.., kDot>), whose rounding error is absolute
 // (cancellation in |a|^2 + |b|^2 - 2 a.b), not relative; from then on the band is
 // widened by twice that error bound.
-__device__ __forceinline__ bool dead_bound(float d2, uint64_t best, float margin, float margin_abs) {
-  return d2 == 0.f || fmaf(d2, margin, margin_abs) < __uint_as_float(key_bits(best));
+// `margin_q` covers what neither of the two does: the float32 QUANTISATION of the z-normalised
+// rows themselves.  Rounding every element of two rows of norm sqrt(n) to float32 moves their
+// squared distance d^2 by up to d * sqrt(n) * 2^-22 — an error whose relative size grows as 1 / d,
+// so on clean periodic data (d^2 ~ 1e-5) it exceeds any fixed relative band.  Both the bound
+// and the best-so-far carry it and the bound is below the best-so-far when the test matters, so
+// the band is widened by margin_q * sqrt(best), margin_q = 1.25 * sqrt(n) * 2^-21 (engine.cu).
+__device__ __forceinline__ bool dead_bound(float d2, uint64_t best, float margin, float margin_abs, float margin_q) {
+  const float b = __uint_as_float(key_bits(best));
+  return d2 == 0.f || fmaf(d2, margin, fmaf(margin_q, sqrtf(b), margin_abs)) < b;
 }
-__device__ __forceinline__ bool is_dead(uint64_t nn, uint64_t best, float margin, float margin_abs) {
-  return dead_bound(__uint_as_float(key_bits(nn)), best, margin, margin_abs);
+__device__ __forceinline__ bool is_dead(uint64_t nn, uint64_t best, float margin, float margin_abs, float margin_q) {
+  return dead_bound(__uint_as_float(key_bits(nn)), best, margin, margin_abs, margin_q);
+}
+
+// Whether a segment-mean lower bound (already scaled to a squared distance) rules a threshold
+// out.  The means are float32 roundings of float64 values of magnitude <= 4, so the bound is off
+// by up to lb_q * sqrt(thr) + lb_q^2 with lb_q = 4e-6 * sqrt(columns per segment) (engine.cu) —
+// again an error that a relative slack (0.1 %) alone does not cover when thr is tiny.
+__device__ __forceinline__ bool lb_rules_out(float lb_scaled, float thr, float lb_q) {
+  return lb_scaled > fmaf(thr, 1.001f, fmaf(lb_q, sqrtf(fmaxf(thr, 0.f)), lb_q * lb_q));
 }
 
 __device__ __forceinline__ unsigned long long* as_ull(uint64_t* p) {

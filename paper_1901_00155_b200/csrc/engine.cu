@@ -15,23 +15,16 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <limits>
 #include <string>
 #include <vector>
 
 #include "kernels.hpp"
 #include "tsdd_cuda.h"
 
-namespace tsdd_b200 {
-void set_packed_math(bool on);
-void set_wide_tile(bool on);
-void set_scan_variant(int variant);
-}
-
 namespace {
 
 using namespace tsdd_b200;
-
-constexpr uint32_t kFinalistCap = 64;
 
 struct Failure {
   int code;
@@ -145,6 +138,8 @@ struct tsdd_cuda_ctx {
   int opt_mates = 8;
   bool opt_rescore = true;
   double opt_margin_delta = -1.0;  // < 0: derive from n (see discard_margin)
+  double opt_margin_q = -1.0;      // < 0: derive from n (see quantisation_margin)
+  uint32_t opt_finalist_cap = 64;  // finalists the first collection has room for (more: collected again, all settled)
   bool opt_symmetric = true;
   bool opt_packed = true;
   bool opt_wide_tile = false;
@@ -174,7 +169,7 @@ struct tsdd_cuda_ctx {
   DeviceArray<float> matrix, lb_means, lb_boxes, row_norms, matrix_sorted;
   bool norms_ready = false;   // row_norms holds the norms of the prepared matrix
   bool sorted_ready = false;  // matrix_sorted holds the prepared matrix in the hash-sorted order
-  DeviceArray<uint32_t> hash0, freq, offsets, slot_bucket, scalars, slot_of_row;
+  DeviceArray<uint32_t> hash0, freq, offsets, slot_bucket, scalars, slot_of_row, first_bad;
   DeviceArray<uint32_t> sort_buf[4], order_buf[4];
   uint32_t *sorted_hash = nullptr, *sorted_row = nullptr, *order = nullptr, *sorted_freq = nullptr;
   DeviceArray<uint32_t> scan_scratch, radix_hist;
@@ -187,6 +182,7 @@ struct tsdd_cuda_ctx {
   DeviceArray<float> batch_matrix;
   DeviceArray<double> zrow;
   DeviceArray<uint32_t> finalists, seed_lb;
+  DeviceArray<uint64_t> finalist_keys;
   DeviceArray<unsigned long long> nn_bits;
   uint32_t batch_capacity = 0;
   bool lb_active = true;    // the lower-bound filter is still worth its (small) cost in this search
@@ -219,6 +215,15 @@ struct tsdd_cuda_ctx {
     return static_cast<float>(1.0 + delta);
   }
 
+  // Rounding the z-normalised rows to float32 moves a squared distance d^2 by up to
+  // d sqrt(n) 2^-22 (two rows of norm sqrt(n), relative element error 2^-24, Cauchy-Schwarz);
+  // the bound and the best-so-far both carry it: 2 x, and a quarter more for second-order terms.
+  // The discard band is widened by this times sqrt(best-so-far) (common.cuh: dead_bound).
+  float quantisation_margin() const {
+    if (opt_margin_q >= 0.0) return static_cast<float>(opt_margin_q);
+    return static_cast<float>(1.25 * std::sqrt(static_cast<double>(n)) * 4.76837158203125e-07);
+  }
+
   // Dot-form distances |a|^2 + |b|^2 - 2 a.b: two FFMA chains of n/2 products of magnitude
   // <= |a||b| <= n, the two norms and three more roundings — within (n + 32) n 2^-24 of the
   // float32 rows' true distance.  The band covers the error of a bound and of the best-so-far.
@@ -229,6 +234,17 @@ struct tsdd_cuda_ctx {
     if (opt_dot == 2) return true;
     const double best_d2 = static_cast<double>(float_from_bits(key_bits(best_key_now)));
     return best_d2 >= 1000.0 * dot_error();  // the band is then below 0.2 % of the best-so-far
+  }
+
+  ScanConfig scan_config() const {
+    ScanConfig c;
+    c.packed = opt_packed;
+    c.wide_tile = opt_wide_tile;
+    c.variant = opt_packed ? opt_kernel : 1;
+    c.tensor_map = opt_tensor_map;
+    c.filter_in_ws = opt_lb_in_ws;
+    c.tile16 = opt_tile16;
+    return c;
   }
 
   SearchState state() {
@@ -244,11 +260,13 @@ struct tsdd_cuda_ctx {
     s.counters = counters.ptr;
     s.margin = discard_margin();
     s.margin_abs = dot_used ? static_cast<float>(2.0 * dot_error()) : 0.f;
+    s.margin_q = quantisation_margin();
     s.row_norms = norms_ready ? row_norms.ptr : nullptr;
     s.rows_sorted = sorted_ready ? matrix_sorted.ptr : nullptr;
     s.lb_means = (opt_lower_bound && lb_active) ? lb_means.ptr : nullptr;
     s.lb_boxes = lb_boxes.ptr;
     s.lb_scale = static_cast<float>(stride / kLbSegments);
+    s.lb_q = 4e-6f * std::sqrt(s.lb_scale);
     return s;
   }
 };
@@ -282,7 +300,7 @@ void check_shape(size_t m, size_t n, size_t word_len, size_t alphabet) {
     fail(TSDD_ERR_PARAMETER,
          "word_len=" + std::to_string(word_len) + " must satisfy 1 <= word_len <= n=" + std::to_string(n));
   if (alphabet < 2 || alphabet > 10)
-    fail(TSDD_ERR_PARAMETER, "alphabet cardinality " + std::to_string(alphabet) + " is outside 2..10");
+    fail(TSDD_ERR_PARAMETER, "alphabet cardinality " + std::to_string(alphabet) + " is outside the built-in range 2..10");
   // |A|^w <= 2^32, checked without overflow
   long double dict = 1.0L;
   for (size_t j = 0; j < word_len; ++j) {
@@ -402,7 +420,6 @@ void prepare_on_device(tsdd_cuda_ctx* ctx, size_t m, size_t n, size_t word_len, 
   ctx->flags.alloc(2 * static_cast<size_t>(rows));
   ctx->sel.alloc(4);
   ctx->zrow.alloc(n);
-  ctx->finalists.alloc(kFinalistCap + 1);
   ctx->nn_bits.alloc(1);
   ctx->batch_capacity = 0;
   ctx->stats.kernel_launches = launches;
@@ -453,7 +470,7 @@ void prepare_host(tsdd_cuda_ctx* ctx, const T* series, size_t m, size_t n, size_
     CUDA_OK(cudaMemcpyAsync(ctx->series_f32.ptr, series, m * sizeof(float), cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaEventRecord(ev_h1, st));
     CUDA_OK(cudaEventRecord(ctx->ev_a, st));
-    extra += launch_widen_series(ctx->series_f32.ptr, ctx->series.ptr, m, st);
+    extra += launch_widen_series(ctx->series_f32.ptr, ctx->series.ptr, m, nullptr, st);  // (check_series ran on the host)
   } else {
     CUDA_OK(cudaMemcpyAsync(ctx->series.ptr, series, m * sizeof(double), cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaEventRecord(ev_h1, st));
@@ -645,7 +662,7 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
         if (count == 0) break;
       }
     }
-    const ScanChoice choice = choose_scan_kernel(s, count, plan[r].window, pruning, ctx->dot_now);
+    const ScanChoice choice = choose_scan_kernel(ctx->scan_config(), s, count, plan[r].window, pruning, ctx->dot_now);
     const uint32_t padded = round_up_u32(count, choice.tile16 ? 2 * kTileRows : kTileRows);
     launches += launch_gather_rows(s, list, ctx->sel.ptr, padded, choice.tile16 ? 2 : choice.tma ? 1 : 0,
                                    ctx->batch_matrix.ptr, st);
@@ -655,16 +672,17 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
       e1 = next_event(ctx);
       CUDA_OK(cudaEventRecord(e0, st));
     }
+    const char* launch_error = nullptr;
     const int launched =
-        launch_scan_tiles(s, ctx->batch_matrix.ptr, list, slots, ctx->sel.ptr, count,
+        launch_scan_tiles(choice, s, ctx->batch_matrix.ptr, list, slots, ctx->sel.ptr, count,
                           plan[r].window ? ctx->sorted_row : nullptr, plan[r].k_begin, plan[r].k_end, rotation,
-                          pruning, ctx->opt_symmetric, ctx->dot_now, st);
+                          pruning, ctx->opt_symmetric, st, &launch_error);
     if (ctx->opt_time_kernels) CUDA_OK(cudaEventRecord(e1, st));
-    if (const char* err = scan_launch_error()) fail(TSDD_ERR_RUNTIME, err);
+    if (launch_error) fail(TSDD_ERR_RUNTIME, launch_error);
     launches += launched;
     ctx->stats.scan_kernel_launches += launched;
-    if (launched && scan_last_launch_was_ws()) ctx->stats.scan_kernel_ws_launches += launched;
-    if (launched && scan_last_launch_was_dot()) ctx->stats.scan_kernel_dot_launches += launched;
+    if (launched && choice.ws) ctx->stats.scan_kernel_ws_launches += launched;
+    if (launched && choice.dot) ctx->stats.scan_kernel_dot_launches += launched;
   }
   launches += launch_finalize_batch(s, list, ctx->sel.ptr, ctx->batch_capacity, pruning, st);
   ctx->stats.kernel_launches += launches;
@@ -804,12 +822,6 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   if (k < 1) fail(TSDD_ERR_PARAMETER, "k must be >= 1, got " + std::to_string(k));
   if (!positions || !distances) fail(TSDD_ERR_PARAMETER, "positions and distances must not be null");
   bind_device(ctx);
-  set_packed_math(ctx->opt_packed);
-  set_wide_tile(ctx->opt_wide_tile);
-  set_scan_variant(ctx->opt_packed ? ctx->opt_kernel : 1);
-  set_tensor_map_loads(ctx->opt_tensor_map);
-  set_filter_in_ws(ctx->opt_lb_in_ws);
-  set_dot_tile16(ctx->opt_tile16);
   const bool pruning = (flags & TSDD_SEARCH_DISABLE_PRUNING) == 0;
   cudaStream_t st = ctx->stream;
   SearchState s = ctx->state();
@@ -822,6 +834,8 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   ctx->dot_now = false;
   s = ctx->state();
   ctx->stats.scan_kernel_dot_launches = 0;
+  ctx->stats.finalists = 0;
+  ctx->stats.exact_reruns = 0;
   ctx->stats.scanned_candidates = 0;
   ctx->stats.scan_kernel_launches = 0;
   ctx->stats.scan_kernel_ws_launches = 0;
@@ -850,14 +864,14 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   for (int pass = 0; pass < k; ++pass) {
     if (pass > 0) {
       CUDA_OK(cudaMemsetAsync(ctx->best.ptr, 0, sizeof(uint64_t), st));
-      ctx->stats.kernel_launches += launch_seed_best(s, st);
+      ctx->stats.kernel_launches += launch_seed_best(ctx->state(), st);
     }
     uint64_t key = run_pass(ctx, pruning, pass);
     if (pass == 0 && seeded && key != 0 && best_key_row(key) == 0xFFFFFFFFu) {
       // no candidate rose above the seeded bound (it can only happen through float32 rounding at
       // an exact tie): drop the seed and let the pass finish on its own best-so-far
       CUDA_OK(cudaMemsetAsync(ctx->best.ptr, 0, sizeof(uint64_t), st));
-      ctx->stats.kernel_launches += launch_seed_best(s, st);
+      ctx->stats.kernel_launches += launch_seed_best(ctx->state(), st);
       key = run_pass(ctx, pruning, pass);
     }
     if (key == 0 || key_bits(key) == 0) {  // nothing beat 0: the reference's fallback (discovery.cpp:90-93)
@@ -870,43 +884,73 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
     if (ctx->opt_rescore) {
       // Decide the pass in float64: every exact row whose float32 nn lies within the safety
       // band of the best-so-far gets its exact nn over all non-self rows, straight from the
-      // series; greatest distance wins, ties go to the smaller position.
-      uint32_t* d_count = ctx->finalists.ptr + kFinalistCap;
-      ctx->stats.kernel_launches += launch_collect_finalists(s, ctx->finalists.ptr, kFinalistCap, d_count, st);
-      std::vector<uint32_t> mine(kFinalistCap + 1);
-      CUDA_OK(cudaMemcpyAsync(mine.data(), ctx->finalists.ptr, (kFinalistCap + 1) * sizeof(uint32_t),
-                              cudaMemcpyDeviceToHost, st));
-      sync_stream(ctx);
-      uint32_t n_final = mine[kFinalistCap];
-      mine.resize(std::min(n_final, kFinalistCap));
-      if (n_final > kFinalistCap) {
-        // more near-ties than are worth settling: keep the float32 winner, make only its distance exact
-        mine.clear();
-        uint8_t is_exact = 0;
-        CUDA_OK(cudaMemcpy(&is_exact, ctx->exact.ptr + row, 1, cudaMemcpyDeviceToHost));
-        if (is_exact) mine.push_back(row);
-      }
-      double best64 = -1.0;
-      uint32_t best_row = 0xFFFFFFFFu;
-      for (const uint32_t cand : mine) {
-        uint64_t nn_key_host = 0;
-        CUDA_OK(cudaMemcpyAsync(&nn_key_host, ctx->nn.ptr + cand, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+      // series; greatest distance wins, ties go to the smaller position.  However many there
+      // are, ALL of them are settled (in descending order of their float32 value, so that most
+      // of a long list is ruled out by the float64 leader before it costs a kernel).
+      s = ctx->state();  // (the band may have widened during the pass: dot form)
+      uint32_t cap = std::max<uint32_t>(ctx->opt_finalist_cap, 1);
+      uint32_t n_final = 0;
+      for (int attempt = 0; attempt < 2; ++attempt) {
+        ctx->finalists.alloc(static_cast<size_t>(cap) + 1);
+        ctx->finalist_keys.alloc(cap);
+        uint32_t* d_count = ctx->finalists.ptr + cap;
+        ctx->stats.kernel_launches += launch_collect_finalists(s, ctx->finalists.ptr, cap, d_count, st);
+        CUDA_OK(cudaMemcpyAsync(&n_final, d_count, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
         sync_stream(ctx);
-        // start from an upper bound just above the float32 value so that most rows abandon early
-        const double start = static_cast<double>(float_from_bits(key_bits(nn_key_host))) *
-                                 static_cast<double>(s.margin) * static_cast<double>(s.margin) +
-                             2.0 * static_cast<double>(ctx->state().margin_abs);
-        unsigned long long bits;
-        std::memcpy(&bits, &start, sizeof(bits));
-        CUDA_OK(cudaMemcpyAsync(ctx->nn_bits.ptr, &bits, sizeof(bits), cudaMemcpyHostToDevice, st));
+        if (n_final <= cap) break;
+        cap = n_final;  // collected again with room for all (nothing changes nn / exact / best in between)
+      }
+      ctx->stats.finalists += n_final;
+      std::vector<uint32_t> mine(n_final);
+      std::vector<uint64_t> mine_keys(n_final);
+      if (n_final > 0) {
+        ctx->stats.kernel_launches += launch_gather_keys(s, ctx->finalists.ptr, n_final, ctx->finalist_keys.ptr, st);
+        CUDA_OK(cudaMemcpyAsync(mine.data(), ctx->finalists.ptr, n_final * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        CUDA_OK(cudaMemcpyAsync(mine_keys.data(), ctx->finalist_keys.ptr, n_final * sizeof(uint64_t),
+                                cudaMemcpyDeviceToHost, st));
+        sync_stream(ctx);
+      }
+      std::vector<uint32_t> by_value(n_final);
+      for (uint32_t f = 0; f < n_final; ++f) by_value[f] = f;
+      std::sort(by_value.begin(), by_value.end(), [&](uint32_t a, uint32_t b) {
+        const uint32_t ka = key_bits(mine_keys[a]), kb = key_bits(mine_keys[b]);
+        return ka != kb ? ka > kb : mine[a] < mine[b];
+      });
+      const double inf64 = std::numeric_limits<double>::infinity();
+      auto exact_nn_from = [&](uint32_t cand, double start) -> double {
+        unsigned long long bits, start_bits;
+        std::memcpy(&start_bits, &start, sizeof(start_bits));
+        CUDA_OK(cudaMemcpyAsync(ctx->nn_bits.ptr, &start_bits, sizeof(start_bits), cudaMemcpyHostToDevice, st));
         ctx->stats.kernel_launches +=
             launch_exact_nn(ctx->series.ptr, ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->rows, static_cast<uint32_t>(ctx->n),
-                            cand, ctx->zrow.ptr, ctx->opt_lower_bound ? ctx->lb_means.ptr : nullptr,
-                            static_cast<float>(ctx->stride / kLbSegments), ctx->nn_bits.ptr, st);
+                            cand, ctx->zrow.ptr, ctx->opt_lower_bound ? ctx->lb_means.ptr : nullptr, s.lb_scale, s.lb_q,
+                            ctx->nn_bits.ptr, st);
         CUDA_OK(cudaMemcpyAsync(&bits, ctx->nn_bits.ptr, sizeof(bits), cudaMemcpyDeviceToHost, st));
         sync_stream(ctx);
+        if (bits == start_bits) return inf64;  // no neighbour came in under the start bound
         double exact;
         std::memcpy(&exact, &bits, sizeof(exact));
+        return exact;
+      };
+      double best64 = -1.0;
+      uint32_t best_row = 0xFFFFFFFFu;
+      for (const uint32_t f : by_value) {
+        const uint32_t cand = mine[f];
+        // an upper bound of the float64 nn just above the float32 value (relative rounding, the
+        // dot form's absolute error, the rows' quantisation), so that most rows abandon early
+        const double nn32 = static_cast<double>(float_from_bits(key_bits(mine_keys[f])));
+        const double start = nn32 * static_cast<double>(s.margin) * static_cast<double>(s.margin) +
+                             2.0 * static_cast<double>(s.margin_abs) +
+                             2.0 * static_cast<double>(s.margin_q) * std::sqrt(nn32);
+        if (start < best64) continue;  // cannot reach the float64 leader
+        double exact = exact_nn_from(cand, start);
+        // the start bound was not one after all (float32 rows further off than the band allows
+        // for): measure from +inf rather than report the bound itself
+        if (exact == inf64) {
+          ctx->stats.exact_reruns += 1;
+          exact = exact_nn_from(cand, inf64);
+        }
+        if (exact == inf64) continue;
         if (exact > best64 || (exact == best64 && cand < best_row)) {
           best64 = exact;
           best_row = cand;
@@ -933,7 +977,7 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
     }
     positions[pass] = static_cast<uint64_t>(row) + 1;
     distances[pass] = std::sqrt(d2);
-    if (pass + 1 < k) ctx->stats.kernel_launches += launch_exclude_zone(s, row, st);
+    if (pass + 1 < k) ctx->stats.kernel_launches += launch_exclude_zone(ctx->state(), row, st);
   }
   CUDA_OK(cudaEventRecord(ctx->ev_b, st));
   sync_stream(ctx);
@@ -1088,6 +1132,12 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
     } else if (key == "margin_delta") {
       if (value > 0.5) fail(TSDD_ERR_PARAMETER, "margin_delta must be below 0.5 (negative = derive from n)");
       ctx->opt_margin_delta = value;
+    } else if (key == "margin_q") {
+      if (value > 1.0) fail(TSDD_ERR_PARAMETER, "margin_q must be below 1 (negative = derive from n)");
+      ctx->opt_margin_q = value;
+    } else if (key == "finalist_cap") {
+      if (value < 1 || value > 1048576) fail(TSDD_ERR_PARAMETER, "finalist_cap must be in 1..1048576");
+      ctx->opt_finalist_cap = static_cast<uint32_t>(value);
     } else if (key == "symmetric") {
       ctx->opt_symmetric = value != 0;
     } else if (key == "packed") {
@@ -1181,10 +1231,18 @@ int tsdd_cuda_prepare_device_f32(tsdd_cuda_ctx* ctx, const float* d_series, size
     // unordered with ours: wait for everything already queued on the device
     if (ctx->stream == ctx->own_stream) CUDA_OK(cudaDeviceSynchronize());
     CUDA_OK(cudaEventRecord(ctx->ev_a, ctx->stream));
-    const uint64_t extra = launch_widen_series(d_series, ctx->series.ptr, m, ctx->stream);
+    // validate_series (series.cpp:10-19) on the device: the samples never passed through the host
+    ctx->first_bad.alloc(1);
+    const uint64_t extra = launch_widen_series(d_series, ctx->series.ptr, m, ctx->first_bad.ptr, ctx->stream);
     prepare_on_device(ctx, m, n, word_len, alphabet);
     ctx->stats.kernel_launches += extra;
-    finish_prepare(ctx);
+    uint32_t bad = 0xFFFFFFFFu;
+    CUDA_OK(cudaMemcpyAsync(&bad, ctx->first_bad.ptr, sizeof(bad), cudaMemcpyDeviceToHost, ctx->stream));
+    finish_prepare(ctx);  // (synchronises the stream)
+    if (bad != 0xFFFFFFFFu) {
+      ctx->prepared = false;
+      fail(TSDD_ERR_VALIDATION, "non-finite value at index " + std::to_string(static_cast<uint64_t>(bad) + 1));
+    }
   });
 }
 

@@ -26,7 +26,8 @@ constexpr int kChunk = TSDD_SCAN_CHUNK;  // columns per pipeline stage (kChunk*4
 constexpr uint32_t kRowAlign = kChunk;   // row stride is a multiple of this many floats
 
 // ------------------------------------------------------------------ preparation
-int launch_widen_series(const float* d_in, double* d_out, size_t m, cudaStream_t stream);
+// d_first_bad (may be null): receives the smallest index of a non-finite sample, ~0 if none.
+int launch_widen_series(const float* d_in, double* d_out, size_t m, uint32_t* d_first_bad, cudaStream_t stream);
 
 // Per-window mean / 1/sigma (float64), PAA -> SAX -> 0-based word hash.
 // paa_out / sax_out may be null (kept only for parity tests).
@@ -84,11 +85,13 @@ struct SearchState {
   DeviceCounters* counters;
   float margin;             // 1 + delta of the discard test (common.cuh: dead_bound)
   float margin_abs;         // 0, or twice the absolute error bound of dot-form distances once a search uses them
+  float margin_q;           // x sqrt(best-so-far): the float32 quantisation of the rows (common.cuh: dead_bound)
   const float* row_norms;   // N + 1 squared norms of the float32 rows (dot form), or nullptr
   const float* rows_sorted; // the matrix in the hash-sorted order (tensor-map loads of window tiles), or nullptr
   const float* lb_means;    // N x kLbSegments segment means, or nullptr: no tile filter
   const float* lb_boxes;    // their bounding boxes per kLbBoxRows rows
   float lb_scale;           // columns per segment (stride / kLbSegments)
+  float lb_q;               // absolute rounding slack of the float32 segment means (common.cuh: lb_rules_out)
 };
 
 int launch_reset_search(SearchState s, cudaStream_t stream);
@@ -128,35 +131,41 @@ int launch_batch_slots(const uint32_t* d_batch_rows, const uint32_t* d_sel, cons
 int launch_gather_rows(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel,
                        uint32_t capacity_padded, int tma_layout, float* d_batch_matrix, cudaStream_t stream);
 
-// Which kernel launch_scan_tiles will pick for a launch (the gather before it needs `tma`).
+// Kernel-selection options of one context (tsdd_cuda_set_option); per-context state, so that
+// contexts on concurrent host threads never see one another's choices.
+struct ScanConfig {
+  bool packed = true;        // f32x2 arithmetic
+  bool wide_tile = false;    // 128 x 128 tiles, one CTA per SM, instead of 128 x 64, two
+  int variant = 0;           // 0: per launch; 1: k_scan_tiles everywhere; 2: k_scan_tiles_ws everywhere
+  bool tensor_map = true;    // the warp-specialised kernel loads tiles as TMA boxes where it can
+  bool filter_in_ws = false; // covering scans with the lower-bound filter on the ws kernel's producer warpgroup
+  bool tile16 = true;        // dot form on 256-candidate tiles (k_scan_tiles_ws16)
+};
+
+// Which kernel a launch uses.  Computed ONCE per segment (choose_scan_kernel) and handed to both
+// k_gather_rows (the candidate layout depends on `tma` / `tile16`) and launch_scan_tiles.
 struct ScanChoice {
   bool lb;   // k_scan_tiles with the lower-bound tile filter
   bool ws;   // the warp-specialised kernel
   bool tma;  // ... fed by tensor-map box loads (covering scans)
   bool dot;  // ... in the dot-product form
   bool tile16;  // ... on 256-candidate tiles, 16 x 8 pairs per thread (k_scan_tiles_ws16)
+  bool packed, wide;  // copied from the ScanConfig
 };
-ScanChoice choose_scan_kernel(const SearchState& s, uint32_t live_upper_bound, bool window, bool pruning,
-                              bool dot_form);
-void set_tensor_map_loads(bool on);
-void set_dot_tile16(bool on);
-void set_filter_in_ws(bool on);  // covering scans with the lower-bound filter: warp-specialised kernel (kLb) or k_scan_tiles
-const char* scan_launch_error();  // message of a failed launch_scan_tiles since the last call, or nullptr
+ScanChoice choose_scan_kernel(const ScanConfig& cfg, const SearchState& s, uint32_t live_upper_bound, bool window,
+                              bool pruning, bool dot_form);
 
 // The tiled early-abandoning distance kernel: batch candidates x neighbour units
 // [k_begin, k_end), one unit = 128 rows.  d_nbr_index == nullptr: unit k holds the rows of
 // unit (k + rotation) mod T of the matrix (the covering scan).  Otherwise (window mode)
 // unit k holds 128 slots of d_nbr_index (the hash-sorted row list) around the candidate
 // tile's own slot, alternating outwards.  live_upper_bound >= the live batch size in
-// d_sel[0]; it sizes the grid and picks the tile shape.
-int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t* d_batch_rows,
-                      const uint32_t* d_batch_slots, const uint32_t* d_sel, uint32_t live_upper_bound,
-                      const uint32_t* d_nbr_index, uint32_t k_begin, uint32_t k_end, uint32_t rotation,
-                      bool pruning, bool symmetric, bool dot_form, cudaStream_t stream);
-
-// Whether the last launch_scan_tiles picked the warp-specialised kernel / its dot-product form.
-bool scan_last_launch_was_ws();
-bool scan_last_launch_was_dot();
+// d_sel[0]; it sizes the grid and picks the tile shape.  *error receives the message of a
+// launch that could not be made (else nullptr).
+int launch_scan_tiles(const ScanChoice& choice, SearchState s, const float* d_batch_matrix,
+                      const uint32_t* d_batch_rows, const uint32_t* d_batch_slots, const uint32_t* d_sel,
+                      uint32_t live_upper_bound, const uint32_t* d_nbr_index, uint32_t k_begin, uint32_t k_end,
+                      uint32_t rotation, bool pruning, bool symmetric, cudaStream_t stream, const char** error);
 
 // Squared norms of the float32 rows (rows 0 .. n_rows; row n_rows is the zero row), for the
 // dot-product form d^2 = |a|^2 + |b|^2 - 2 a.b of the warp-specialised tile kernel.
@@ -183,12 +192,15 @@ int launch_exclude_zone(SearchState s, uint32_t row, cudaStream_t stream);
 int launch_collect_finalists(SearchState s, uint32_t* d_list, uint32_t cap, uint32_t* d_count,
                              cudaStream_t stream);
 
+// d_keys[i] = nn key of row d_list[i].
+int launch_gather_keys(SearchState s, const uint32_t* d_list, uint32_t count, uint64_t* d_keys, cudaStream_t stream);
+
 // Exact float64 nearest-neighbour distance (squared) of one row over ALL non-self rows,
 // straight from the series: d_out_bits[0] = bits of the minimum (must be preset to the
 // bits of an upper bound, e.g. +inf), with early abandoning against it.
 int launch_exact_nn(const double* d_series, const double* d_mean, const double* d_inv_sigma,
                     uint32_t n_rows, uint32_t n, uint32_t row, double* d_zrow, const float* d_lb_means, float lb_scale,
-                    unsigned long long* d_out_bits, cudaStream_t stream);
+                    float lb_q, unsigned long long* d_out_bits, cudaStream_t stream);
 
 // ------------------------------------------------------------------ probes
 int launch_fp32_probe(int which, float* d_sink, int blocks, int iters, cudaStream_t stream);

@@ -37,9 +37,15 @@ inline unsigned blocks_for(size_t items, unsigned per_block) {
 }
 
 // ------------------------------------------------------------------ series
-__global__ void k_widen_series(const float* __restrict__ in, double* __restrict__ out, size_t m) {
+// Also validate_series (series.cpp:10-19) for a series that never passed through the host:
+// *first_bad receives the smallest index of a non-finite sample (preset to ~0 = none).
+__global__ void k_widen_series(const float* __restrict__ in, double* __restrict__ out, size_t m,
+                               uint32_t* __restrict__ first_bad) {
   const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < m) out[i] = static_cast<double>(in[i]);
+  if (i >= m) return;
+  const float v = in[i];
+  out[i] = static_cast<double>(v);
+  if (first_bad != nullptr && !isfinite(v)) atomicMin(first_bad, static_cast<uint32_t>(i));
 }
 
 // One thread per window.  Adjacent threads read adjacent samples, so every
@@ -526,8 +532,9 @@ __global__ void k_count_min_freq(const uint32_t* __restrict__ sorted_freq, uint3
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
-int launch_widen_series(const float* d_in, double* d_out, size_t m, cudaStream_t stream) {
-  k_widen_series<<<blocks_for(m, 256), 256, 0, stream>>>(d_in, d_out, m);
+int launch_widen_series(const float* d_in, double* d_out, size_t m, uint32_t* d_first_bad, cudaStream_t stream) {
+  if (d_first_bad != nullptr) cudaMemsetAsync(d_first_bad, 0xFF, sizeof(uint32_t), stream);
+  k_widen_series<<<blocks_for(m, 256), 256, 0, stream>>>(d_in, d_out, m, d_first_bad);
   return 1;
 }
 

@@ -146,7 +146,8 @@ k_install_seed(SearchState s, const uint32_t* __restrict__ seed_lb, uint32_t see
   if (threadIdx.x == 0) {
     for (int w = 1; w < 8; ++w) mine = fmaxf(mine, s_max[w]);
     // 0.5 % below the bound: the means and boxes are float32 (the tile filter allows 0.1 %)
-    const float seed = mine * s.lb_scale * 0.995f;
+    float seed = mine * s.lb_scale * 0.995f;
+    seed -= fmaf(s.lb_q, sqrtf(fmaxf(seed, 0.f)), s.lb_q * s.lb_q);  // absolute part of the means' rounding
     if (seed > 0.f)
       atomicMax(as_ull(s.best), static_cast<unsigned long long>(best_key(__float_as_uint(seed), 0xFFFFFFFFu)));
   }
@@ -189,7 +190,7 @@ k_bucket_mates(SearchState s, const double* __restrict__ x, const double* __rest
   const uint64_t best = *s.best;
   float bound_i = __uint_as_float(kInfBits);
   for (uint32_t q = 1; q <= tries; ++q) {
-    if (dead_bound(bound_i, best, s.margin, s.margin_abs)) break;
+    if (dead_bound(bound_i, best, s.margin, s.margin_abs, s.margin_q)) break;
     const uint32_t other = b0 + (slot - b0 + q * step) % len;
     const uint32_t row_j = sorted_row[other];
     if (gap_u32(row_i, row_j) < s.n) continue;
@@ -228,7 +229,7 @@ __global__ void k_flag_live(SearchState s, const uint32_t* __restrict__ order, u
   if (e >= s.n_rows) return;
   const uint32_t row = order[e];
   bool live = (e % world == rank) && !s.excluded[row] && !s.exact[row];
-  if (live && pruning) live = !is_dead(s.nn[row], *s.best, s.margin, s.margin_abs);
+  if (live && pruning) live = !is_dead(s.nn[row], *s.best, s.margin, s.margin_abs, s.margin_q);
   flags[t] = live ? 1u : 0u;
 }
 
@@ -272,7 +273,7 @@ k_compact_batch(SearchState s, const uint32_t* __restrict__ in, const uint32_t* 
     if (idx < count) {
       row = in[idx];
       slot = in_slots[idx];
-      keep = !pruning || !is_dead(load_key(s.nn + row), best, s.margin, s.margin_abs);
+      keep = !pruning || !is_dead(load_key(s.nn + row), best, s.margin, s.margin_abs, s.margin_q);
     }
     const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, keep);
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -306,7 +307,7 @@ k_compact_flag(SearchState s, const uint32_t* __restrict__ in, int pruning, cons
   const uint32_t count = sel[0];
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
   bool keep = false;
-  if (idx < count) keep = !pruning || !is_dead(load_key(s.nn + in[idx]), *s.best, s.margin, s.margin_abs);
+  if (idx < count) keep = !pruning || !is_dead(load_key(s.nn + in[idx]), *s.best, s.margin, s.margin_abs, s.margin_q);
   if (idx < count) keep_flags[idx] = keep ? 1u : 0u;
   const int kept = __syncthreads_count(keep);
   if (threadIdx.x == 0) block_counts[blockIdx.x] = static_cast<uint32_t>(kept);
@@ -442,7 +443,7 @@ k_finalize_batch(SearchState s, const uint32_t* __restrict__ batch_rows,
   if (idx < count) {
     const uint32_t row = batch_rows[idx];
     const uint64_t key = s.nn[row];
-    if (!pruning || !is_dead(key, best, s.margin, s.margin_abs)) {
+    if (!pruning || !is_dead(key, best, s.margin, s.margin_abs, s.margin_q)) {
       s.exact[row] = 1;
       if (key_bits(key) != kInfBits) mine = best_key(key_bits(key), row);
     }
@@ -700,7 +701,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
           live = true;
         } else {
           const float bound = fminf(__uint_as_float(key_bits(pf_key)), s_loc[tid]);
-          if (!dead_bound(bound, best, s.margin, s.margin_abs)) {
+          if (!dead_bound(bound, best, s.margin, s.margin_abs, s.margin_q)) {
             thr = bound;
             live = true;
           }
@@ -722,7 +723,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
       bool needed = live;
       if (live && slot0 < s.n_rows) {
         const uint32_t row = s_cand[tid];
-        const float limit = s_thr[tid] * 1.001f;  // rounding slack of the float32 means
+        const float limit = s_thr[tid];  // (lb_rules_out adds the rounding slack of the float32 means)
         float mine[kLbSegments];
         const float4* pm = reinterpret_cast<const float4*>(s.lb_means + static_cast<size_t>(row) * kLbSegments);
 #pragma unroll
@@ -745,7 +746,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
             g = fmaxf(fmaxf(lo.z - mine[4 * q + 2], mine[4 * q + 2] - hi.z), 0.f), lb = fmaf(g, g, lb);
             g = fmaxf(fmaxf(lo.w - mine[4 * q + 3], mine[4 * q + 3] - hi.w), 0.f), lb = fmaf(g, g, lb);
           }
-          needed = !(lb * s.lb_scale > limit);
+          needed = !lb_rules_out(lb * s.lb_scale, limit, s.lb_q);
         }
         if (!needed) {
           s_thr[tid] = -1.f;
@@ -1175,9 +1176,9 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
         bool live = false, needed = false;
         if (row != 0xFFFFFFFFu) {
           const float bound = fminf(__uint_as_float(cand_ub), sh.loc[c]);
-          live = !dead_bound(bound, best, s.margin, s.margin_abs);
+          live = !dead_bound(bound, best, s.margin, s.margin_abs, s.margin_q);
           if (live) {
-            const float limit = bound * 1.001f;  // rounding slack of the float32 means
+            const float limit = bound;  // (lb_rules_out adds the rounding slack of the float32 means)
             const uint32_t n_units = min(kUnits, units_total - unit0);
             float lb[kUnits];
 #pragma unroll
@@ -1200,7 +1201,7 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
 #pragma unroll
             for (int u = 0; u < static_cast<int>(kUnits); ++u)
               if (static_cast<uint32_t>(u) < n_units) lb_min = fminf(lb_min, lb[u]);
-            needed = !(lb_min * s.lb_scale > limit);
+            needed = !lb_rules_out(lb_min * s.lb_scale, limit, s.lb_q);
             if (needed) thr = bound;
           }
         }
@@ -1343,7 +1344,7 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
             live[q] = true;
           } else {
             const float bound = fminf(__uint_as_float(cand_ub[q]), sh.loc[r]);
-            if (!dead_bound(bound, best, s.margin, s.margin_abs)) {
+            if (!dead_bound(bound, best, s.margin, s.margin_abs, s.margin_q)) {
               thr = bound;
               live[q] = true;
             }
@@ -1797,7 +1798,7 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
             thr = inf;
           } else {
             const float bound = fminf(__uint_as_float(key_bits(load_key(s.nn + row))), sh.loc[r]);
-            if (!dead_bound(bound, best, s.margin, s.margin_abs)) thr = bound;
+            if (!dead_bound(bound, best, s.margin, s.margin_abs, s.margin_q)) thr = bound;
           }
         }
         meta.thr[r] = thr;
@@ -2078,10 +2079,16 @@ k_collect_finalists(SearchState s, uint32_t* __restrict__ list, uint32_t cap, ui
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < s.n_rows; i += gridDim.x * blockDim.x) {
     if (!s.exact[i] || s.excluded[i]) continue;
     const uint64_t key = s.nn[i];
-    if (key_bits(key) == kInfBits || is_dead(key, best, s.margin, s.margin_abs)) continue;
+    if (key_bits(key) == kInfBits || is_dead(key, best, s.margin, s.margin_abs, s.margin_q)) continue;
     const uint32_t at = atomicAdd(count, 1u);
     if (at < cap) list[at] = i;
   }
+}
+
+__global__ void k_gather_keys(const uint64_t* __restrict__ nn, const uint32_t* __restrict__ list, uint32_t count,
+                              uint64_t* __restrict__ out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) out[i] = nn[list[i]];
 }
 
 // z-normalised float64 values of one row (series.cpp:21-37), kept in global memory
@@ -2099,7 +2106,7 @@ __global__ void k_zrow(const double* __restrict__ x, const double* __restrict__ 
 __global__ void __launch_bounds__(256)
 k_exact_nn(const double* __restrict__ x, const double* __restrict__ mean, const double* __restrict__ inv_sigma,
            uint32_t n_rows, uint32_t n, uint32_t row, const double* __restrict__ z,
-           const float* __restrict__ lb_means, float lb_scale, unsigned long long* out_bits) {
+           const float* __restrict__ lb_means, float lb_scale, float lb_q, unsigned long long* out_bits) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   double mine = __longlong_as_double(0x7FF0000000000000ll);  // +inf
   bool wanted = j < n_rows && gap_u32(row, j) >= n;
@@ -2115,7 +2122,8 @@ k_exact_nn(const double* __restrict__ x, const double* __restrict__ mean, const 
       const float dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z, dw = a.w - b.w;
       lb = fmaf(dx, dx, lb), lb = fmaf(dy, dy, lb), lb = fmaf(dz, dz, lb), lb = fmaf(dw, dw, lb);
     }
-    wanted = !(static_cast<double>(lb * lb_scale) > bound * 1.001);
+    wanted = !(static_cast<double>(lb * lb_scale) >
+               bound * 1.001 + static_cast<double>(lb_q) * sqrt(bound) + static_cast<double>(lb_q * lb_q));
   }
   if (wanted) {
     const double mu = mean[j], inv = inv_sigma[j];
@@ -2137,16 +2145,7 @@ k_exact_nn(const double* __restrict__ x, const double* __restrict__ mean, const 
     atomicMin(out_bits, static_cast<unsigned long long>(__double_as_longlong(mine)));  // doubles >= 0 order like their bits
 }
 
-bool g_packed_default = true;
-bool g_last_launch_was_ws = false;
-bool g_last_launch_was_dot = false;
-bool g_tma_enabled = true;
-bool g_lb_in_ws = false;
-bool g_tile16 = true;
-const char* g_launch_error = nullptr;
 inline uint32_t slot_tiles_of(uint32_t rows) { return (rows + kTileRows - 1) / kTileRows; }
-int g_scan_variant = 0;  // 0: chosen per launch, 1: cp.async + CTA barriers (k_scan_tiles), 2: warp-specialised (k_scan_tiles_ws)
-bool g_wide_tile = false;  // true: 128 x 128 tile, one CTA per SM; false: 128 x 64 tile, two CTAs per SM
 
 }  // namespace
 
@@ -2245,49 +2244,50 @@ bool make_row_map(CUtensorMap* map, const float* base, uint64_t n_rows, uint64_t
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-ScanChoice choose_scan_kernel(const SearchState& s, uint32_t live_upper_bound, bool window, bool pruning,
-                              bool dot_form) {
+ScanChoice choose_scan_kernel(const ScanConfig& cfg, const SearchState& s, uint32_t live_upper_bound, bool window,
+                              bool pruning, bool dot_form) {
   ScanChoice c{};
-  c.lb = pruning && !window && s.lb_means != nullptr && g_scan_variant != 2;
+  c.packed = cfg.packed;
+  c.wide = cfg.wide_tile;
+  c.lb = pruning && !window && s.lb_means != nullptr && cfg.variant != 2;
   // variant 0 (automatic): the warp-specialised kernel wherever the lower-bound filter has
   // nothing to offer (window rounds; covering scans of searches on which it is switched off)
   // and the batch still fills 128-candidate tiles; k_scan_tiles otherwise
-  const bool tma_ok = g_tma_enabled && tensor_map_encoder() != nullptr;
+  const bool tma_ok = cfg.tensor_map && tensor_map_encoder() != nullptr;
   // ... or, with tensor-map loads, where the filter runs on the producer warpgroup (kLb)
-  const bool lb_in_ws = c.lb && tma_ok && g_lb_in_ws;
-  c.ws = g_scan_variant == 2 || (g_scan_variant == 0 && g_packed_default && !g_wide_tile && (!c.lb || lb_in_ws) &&
-                                 live_upper_bound > 64);
+  const bool lb_in_ws = c.lb && tma_ok && cfg.filter_in_ws;
+  c.ws = cfg.variant == 2 || (cfg.variant == 0 && cfg.packed && !cfg.wide_tile && (!c.lb || lb_in_ws) &&
+                              live_upper_bound > 64);
   c.dot = c.ws && !c.lb && dot_form && s.row_norms != nullptr;
   // window launches read scattered rows unless the engine keeps a copy of the matrix in the
   // hash-sorted order (it does once a search runs in the dot form)
   c.tma = c.ws && tma_ok && (!window || (c.dot && s.rows_sorted != nullptr));
   // the dot form on 256-candidate tiles, 16 x 8 pairs per thread, while the batch fills them
-  c.tile16 = c.dot && c.tma && g_tile16 && live_upper_bound > 192;
+  c.tile16 = c.dot && c.tma && cfg.tile16 && live_upper_bound > 192;
   return c;
 }
 
-int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t* d_batch_rows,
-                      const uint32_t* d_batch_slots, const uint32_t* d_sel, uint32_t live_upper_bound,
-                      const uint32_t* d_nbr_index, uint32_t k_begin, uint32_t k_end, uint32_t rotation,
-                      bool pruning, bool symmetric, bool dot_form, cudaStream_t stream) {
+int launch_scan_tiles(const ScanChoice& choice, SearchState s, const float* d_batch_matrix,
+                      const uint32_t* d_batch_rows, const uint32_t* d_batch_slots, const uint32_t* d_sel,
+                      uint32_t live_upper_bound, const uint32_t* d_nbr_index, uint32_t k_begin, uint32_t k_end,
+                      uint32_t rotation, bool pruning, bool symmetric, cudaStream_t stream, const char** error) {
+  if (error) *error = nullptr;
   if (k_end <= k_begin || live_upper_bound == 0) return 0;
-  const ScanChoice choice = choose_scan_kernel(s, live_upper_bound, d_nbr_index != nullptr, pruning, dot_form);
   const bool lb = choice.lb, use_ws = choice.ws;
+  const bool wide = choice.wide, use_packed = choice.packed;
   // tile shape: 64-candidate tiles once the batch has shrunk to that, else 128
-  const bool narrow = !g_wide_tile && !use_ws && live_upper_bound <= 64;
+  const bool narrow = !wide && !use_ws && live_upper_bound <= 64;
   const uint32_t cand_rows = choice.tile16 ? 256 : narrow ? 64 : 128;
-  const uint32_t nbr_rows = use_ws ? 128 : g_wide_tile ? 128 : narrow ? 128 : 64;
+  const uint32_t nbr_rows = use_ws ? 128 : wide ? 128 : narrow ? 128 : 64;
   const uint32_t cand_tiles = (live_upper_bound + cand_rows - 1) / cand_rows;
   const uint64_t sub_tiles = static_cast<uint64_t>(k_end - k_begin) * (kTileRows / nbr_rows);
   // a few tiles per CTA (thresholds are refreshed per tile), several waves of CTAs per launch
-  const uint64_t resident = 148ull * ((g_wide_tile || use_ws) ? 1 : 2);
+  const uint64_t resident = 148ull * ((wide || use_ws) ? 1 : 2);
   const uint64_t want = sub_tiles * cand_tiles / (resident * 8ull);
   const int tiles_per_cta = static_cast<int>(want < 1 ? 1 : want > 16 ? 16 : want);
   dim3 grid(static_cast<unsigned>((sub_tiles + tiles_per_cta - 1) / tiles_per_cta), cand_tiles);
   ScanArgs a{d_batch_matrix, d_batch_rows, d_batch_slots, d_sel, d_nbr_index, k_begin, k_end, rotation,
              tiles_per_cta, pruning ? 1 : 0};
-  g_last_launch_was_ws = use_ws;
-  g_last_launch_was_dot = choice.dot;
   if (use_ws) {
     CUtensorMap map_a{}, map_b{};
     bool tma = choice.tma;
@@ -2298,7 +2298,7 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
             make_row_map(&map_b, d_nbr_index != nullptr ? s.rows_sorted : s.rows,
                          static_cast<uint64_t>(slot_tiles_of(s.n_rows + 1)) * kTileRows, s.stride);
     if (choice.tma && !tma) {  // the gather already used the tensor-map row order: no way back
-      g_launch_error = "cuTensorMapEncodeTiled failed";
+      if (error) *error = "cuTensorMapEncodeTiled failed";
       return 0;
     }
     auto launch_ws = [&](auto kernel, size_t smem_bytes) {
@@ -2324,7 +2324,7 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     kernel<<<grid, kScanThreads, smem, stream>>>(s, a);
   };
-  const int shape = (g_wide_tile ? 2 : narrow ? 1 : 0);
+  const int shape = (wide ? 2 : narrow ? 1 : 0);
   auto pick = [&](auto packed, auto sym, auto with_lb) {
     constexpr bool kP = decltype(packed)::value, kS = decltype(sym)::value, kL = decltype(with_lb)::value;
     if (shape == 2) launch(k_scan_tiles<kP, kS, 16, 8, kL>);
@@ -2335,7 +2335,7 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
     if (lb) pick(packed, sym, std::true_type{});
     else pick(packed, sym, std::false_type{});
   };
-  if (g_packed_default) {
+  if (use_packed) {
     if (symmetric) pick_lb(std::true_type{}, std::true_type{});
     else pick_lb(std::true_type{}, std::false_type{});
   } else {
@@ -2343,20 +2343,6 @@ int launch_scan_tiles(SearchState s, const float* d_batch_matrix, const uint32_t
     else pick_lb(std::false_type{}, std::false_type{});
   }
   return 1;
-}
-
-void set_packed_math(bool on) { g_packed_default = on; }
-void set_wide_tile(bool on) { g_wide_tile = on; }
-void set_scan_variant(int variant) { g_scan_variant = variant; }
-bool scan_last_launch_was_ws() { return g_last_launch_was_ws; }
-bool scan_last_launch_was_dot() { return g_last_launch_was_dot; }
-void set_tensor_map_loads(bool on) { g_tma_enabled = on; }
-void set_filter_in_ws(bool on) { g_lb_in_ws = on; }
-void set_dot_tile16(bool on) { g_tile16 = on; }
-const char* scan_launch_error() {
-  const char* e = g_launch_error;
-  g_launch_error = nullptr;
-  return e;
 }
 
 // The matrix in the hash-sorted order: slot p holds row sorted_row[p]; slots from n_rows on are zero.
@@ -2423,12 +2409,18 @@ int launch_collect_finalists(SearchState s, uint32_t* d_list, uint32_t cap, uint
   return 1;
 }
 
+int launch_gather_keys(SearchState s, const uint32_t* d_list, uint32_t count, uint64_t* d_keys, cudaStream_t stream) {
+  if (count == 0) return 0;
+  k_gather_keys<<<blocks_for(count, 256), 256, 0, stream>>>(s.nn, d_list, count, d_keys);
+  return 1;
+}
+
 int launch_exact_nn(const double* d_series, const double* d_mean, const double* d_inv_sigma,
                     uint32_t n_rows, uint32_t n, uint32_t row, double* d_zrow, const float* d_lb_means,
-                    float lb_scale, unsigned long long* d_out_bits, cudaStream_t stream) {
+                    float lb_scale, float lb_q, unsigned long long* d_out_bits, cudaStream_t stream) {
   k_zrow<<<blocks_for(n, 256), 256, 0, stream>>>(d_series, d_mean, d_inv_sigma, n, row, d_zrow);
   k_exact_nn<<<blocks_for(n_rows, 256), 256, 0, stream>>>(d_series, d_mean, d_inv_sigma, n_rows, n, row,
-                                                         d_zrow, d_lb_means, lb_scale, d_out_bits);
+                                                         d_zrow, d_lb_means, lb_scale, lb_q, d_out_bits);
   return 2;
 }
 

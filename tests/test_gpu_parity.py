@@ -32,21 +32,43 @@ def chk():
     return oracle.best()
 
 
+def topk_from_profile(profile_sq, n, k):
+    """Top-k discords from a float64 nn profile under the brute-force tie rule (greatest distance,
+    then smallest position, discovery.cpp:158-165) and the exclusion zone of SURVEY.md 8c."""
+    allowed = np.isfinite(profile_sq)
+    pos, dist = [], []
+    for _ in range(k):
+        if not allowed.any() or profile_sq[allowed].max() <= 0.0:
+            pos.append(1), dist.append(0.0)
+            continue
+        top = profile_sq[allowed].max()
+        at = int(np.flatnonzero(allowed & (profile_sq == top))[0])
+        pos.append(at + 1), dist.append(float(np.sqrt(top)))
+        allowed[max(0, at - n + 1):at + n] = False
+    return pos, dist
+
+
 def assert_discords_match(chk, x, n, pos, dist, want):
     """Positions identical, distances within DIST_RTOL.  The one legitimate difference is an
     EXACT tie on the nn distance (e.g. two mutual nearest neighbours, or many rows whose
     nearest neighbour is the same all-zero row): the reference's own choice then depends on
     its candidate order or on float64 rounding noise (SURVEY.md gap G5), this engine takes
-    the smallest position.  After such a tie the exclusion zones differ, so the comparison
-    stops there."""
-    profile = None
+    the smallest position.  After such a tie the exclusion zones differ from the reference
+    wrapper's, so the REST of the list is checked against the top-k that the reference's
+    brute-force nn profile gives under this engine's documented tie rule."""
     for r, (p, d, wp, wd) in enumerate(zip(pos, dist, want["positions"], want["distances"])):
         if p != wp:
-            if profile is None:
-                profile = np.sqrt(chk.nn_profile(x, n))
+            profile_sq = chk.nn_profile(x, n)
+            profile = np.sqrt(profile_sq)
             a, b = profile[p - 1], profile[wp - 1]
             assert a == pytest.approx(b, rel=1e-9, abs=1e-9), (r, p, wp, a, b)
-            assert d == pytest.approx(wd, rel=DIST_RTOL, abs=1e-6), (r, d, wd)
+            own_pos, own_dist = topk_from_profile(profile_sq, n, len(pos))
+            for q in range(r, len(pos)):
+                if pos[q] != own_pos[q]:  # only another exact tie (down to rounding noise) may differ
+                    assert profile[pos[q] - 1] == pytest.approx(profile[own_pos[q] - 1], rel=1e-9, abs=1e-9), \
+                        (q, pos, own_pos)
+                    break
+                assert dist[q] == pytest.approx(own_dist[q], rel=DIST_RTOL, abs=1e-6), (q, pos, dist, own_dist)
             return
         assert d == pytest.approx(wd, rel=DIST_RTOL, abs=1e-6), (r, p, d, wd)
 
@@ -675,3 +697,96 @@ def test_long_subsequences(ctx, chk):
     want = chk.topk(x, 4096, 8, 4, 2)  # the reference's guard rejects 4^16 words; results do not depend on it
     assert pos == want["positions"]
     np.testing.assert_allclose(dist, want["distances"], rtol=DIST_RTOL)
+
+
+# ------------------------------------------------------------------ the edges of the float32 search
+def _low_noise_periodic(seed, m, noise):
+    rng = np.random.default_rng(seed)
+    t = np.arange(m)
+    return (np.sin(2 * np.pi * t / 64.0) + noise * rng.standard_normal(m)).astype(np.float32)
+
+
+@pytest.mark.parametrize("dot", [1, 2])
+@pytest.mark.parametrize("seed,noise", [(0, 1e-4), (1, 1e-4), (2, 3e-5), (3, 1e-3)])
+def test_low_noise_periodic_series(ctx, chk, seed, noise, dot):
+    """Clean periodic data: nearest-neighbour distances d^2 ~ 1e-5 .. 1e-3, where the float32
+    QUANTISATION of the z-normalised rows (d sqrt(n) 2^-22: relative size ~ 1 / d) exceeds the
+    relative discard band.  The sqrt(best) term of the band (common.cuh: dead_bound) and the
+    float64 decision must still give the reference's positions."""
+    x = _low_noise_periodic(seed, 9000, noise)
+    ctx.set_option("dot_form", dot)
+    try:
+        ctx.prepare(x, 256, 8, 4)
+        pos, dist = ctx.search(2)
+    finally:
+        ctx.set_option("dot_form", 1)
+    want = chk.topk(x, 256, 8, 4, 2)
+    assert pos == want["positions"], (pos, want["positions"], dist, want["distances"])
+    np.testing.assert_allclose(dist, want["distances"], rtol=DIST_RTOL)
+
+
+def test_many_near_tied_finalists_are_all_settled(ctx, chk):
+    """More finalists than the first collection has room for: the pass collects again and
+    settles ALL of them in float64 (it used to keep the float32 winner).  The discard band is
+    widened artificially (margin_delta) so that hundreds of exact rows fall inside it."""
+    x = planted_walk(11, 30000, 128)
+    ctx.prepare(x, 128, 4, 4)
+    base_pos, base_dist = ctx.search(3)
+    ctx.set_option("margin_delta", 0.45)
+    ctx.set_option("finalist_cap", 2)
+    try:
+        pos, dist = ctx.search(3)
+        st = ctx.stats()
+    finally:
+        ctx.set_option("margin_delta", -1)
+        ctx.set_option("finalist_cap", 64)
+    assert st["finalists"] > 64, st["finalists"]
+    want = chk.topk(x, 128, 4, 4, 3)
+    assert pos == base_pos == want["positions"]
+    np.testing.assert_allclose(dist, want["distances"], rtol=DIST_RTOL)
+    np.testing.assert_allclose(dist, base_dist, rtol=1e-12)  # both decided in float64
+
+
+def test_finalists_follow_the_band_after_a_switch_to_the_dot_form(ctx):
+    """The search switches to the dot-product form MID-search (noise: no tile is abandoned); the
+    discard band then widens by the form's absolute error.  The finalists must be collected with
+    that wider band, not with the one the search started with."""
+    n = 128
+    x = np.random.default_rng(5).random(40000).astype(np.float32)
+    ctx.prepare(x, n, 8, 4)
+    ctx.search(1)
+    st = ctx.stats()
+    assert st["scan_kernel_dot_launches"] > 0 and st["scan_kernel_launches"] > st["scan_kernel_dot_launches"]
+    nn32 = ctx.fetch("nn_sq").astype(np.float64)
+    exact = ctx.fetch("nn_exact").astype(bool)
+    best = nn32[exact].max()
+    delta = max(4e-6, 1.2e-7 * n)
+    abs_band = 2.0 * (n + 32) * n * 2.0 ** -24
+    q = 1.25 * np.sqrt(n) * 2.0 ** -21
+    def count(slack):
+        return int(np.sum(exact & (nn32 * (1 + delta) + (abs_band + q * np.sqrt(best)) * slack >= best)))
+    narrow = int(np.sum(exact & (nn32 * (1 + delta) >= best)))
+    assert count(0.999) <= st["finalists"] <= count(1.001), (count(0.999), st["finalists"], count(1.001))
+    assert st["finalists"] > narrow, (st["finalists"], narrow)  # (the wide band does hold more rows here)
+
+
+def test_device_series_is_validated_on_the_device(ctx):
+    """validate_series (series.cpp:10-19) for tsdd_cuda_prepare_device_f32: the samples never pass
+    through the host, so the finite check runs in k_widen_series."""
+    import torch
+
+    from paper_1901_00155_b200 import ValidationError
+
+    x = W.random_walk(1, 5000)
+    x[1234] = np.float32("nan")
+    x[4000] = np.float32("inf")
+    d = torch.from_numpy(x).cuda()
+    with pytest.raises(ValidationError, match=r"non-finite value at index 1235$"):
+        ctx.prepare_device(d.data_ptr(), len(x), 64, 4, 4)
+    with pytest.raises(Exception, match="prepared"):
+        ctx.search(1)
+    x[1234] = 0.0
+    x[4000] = 0.0
+    d = torch.from_numpy(x).cuda()
+    ctx.prepare_device(d.data_ptr(), len(x), 64, 4, 4)
+    ctx.search(1)
