@@ -183,6 +183,14 @@ class Reference(_Checker):
     prefix = "ref_"
     kind = "reference"
 
+    def generate_series(self, m, anomaly="none", anomaly_pos=0, anomaly_len=64, seed=0) -> np.ndarray:
+        """The reference's generate_series (src/generate.cpp:19-59)."""
+        fn = self.lib.ref_generate_series
+        fn.argtypes = [u64, ctypes.c_char_p, u64, u64, u64, vp]
+        out = np.empty(max(int(m), 1), dtype=np.float64)
+        self._check(fn(int(m), anomaly.encode(), int(anomaly_pos), int(anomaly_len), int(seed), _ptr(out)))
+        return out[:int(m)]
+
 
 class Port(_Checker):
     prefix = "orc_"

@@ -25,6 +25,7 @@
 
 #include "tsdd/discovery.hpp"
 #include "tsdd/errors.hpp"
+#include "tsdd/generate.hpp"
 #include "tsdd/index.hpp"
 #include "tsdd/pipeline.hpp"
 #include "tsdd/sax.hpp"
@@ -267,6 +268,21 @@ int ref_nn_profile(const double* series, std::uint64_t m, std::uint64_t n, int t
       }
       nn_sq[i] = best;
     }
+  });
+}
+
+// generate_series (generate.cpp:19-59); anomaly by name as on the reference's command line
+int ref_generate_series(std::uint64_t m, const char* anomaly, std::uint64_t anomaly_pos, std::uint64_t anomaly_len,
+                        std::uint64_t seed, double* out) {
+  return guarded([&] {
+    tsdd::GeneratorSpec spec;
+    spec.length = m;
+    spec.anomaly = tsdd::parse_anomaly_kind(anomaly);
+    spec.anomaly_pos = anomaly_pos;
+    spec.anomaly_len = anomaly_len;
+    spec.seed = seed;
+    const tsdd::TimeSeries series = tsdd::generate_series(spec);
+    std::copy(series.values.begin(), series.values.end(), out);
   });
 }
 

@@ -14,7 +14,7 @@ namespace {
 
 // Equiprobable N(0,1) breakpoints for |A| = 2..10, lower half mirrored onto
 // the upper half; row a-2 holds the a-1 finite thresholds.  Regenerated with
-// scipy norm.ppf (tools/gen_sax_breakpoints.py); same values as the
+// scipy norm.ppf (tools/gen_sax_breakpoints.py, checked by tests/test_host.py); same values as the
 // reference's table (sax.cpp:14-46).
 __constant__ double c_breaks[9][9] = {
     {0},

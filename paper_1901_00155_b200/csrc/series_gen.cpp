@@ -14,13 +14,16 @@
 // oracle receives the same float32 values widened losslessly to double.
 //
 // Host-only code (no CUDA): used by tests/, bench.py and the host tools.
-// The reference's own generator (proj/src/generate.cpp:36-59) makes a
-// different family (uniform-step walk + spike/shape) and is not reproduced.
+// The reference's own generator family (proj/src/generate.cpp:19-59: uniform-step walk
+// with an optional spike or shape anomaly) is restated at the end of this file
+// (tsdd_generate_series) for the CLI's `generate --m ...` form.
 
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <cstdio>
 #include <random>
+#include <string>
 #include <vector>
 
 namespace {
@@ -237,6 +240,48 @@ int tsdd_random_walk(std::uint64_t seed, float* out, std::uint64_t m) {
   for (std::uint64_t i = 1; i < m; ++i) {
     level += rng.normal();
     out[i] = static_cast<float>(level);
+  }
+  return 0;
+}
+
+// The reference's generator (generate.cpp:19-59, generate.hpp:16-28), restated: a walk of
+// m uniform[-1, 1) steps from std::mt19937_64(seed) through std::uniform_real_distribution
+// (the same library calls, so the same values); anomaly 0 none, 1 spike (+100 at one sample),
+// 2 shape (anomaly_len samples from anomaly_pos on replaced by base + 12 sin(6 pi t / (len-1))).
+// anomaly_pos is 1-based.  Returns 0, or 2 with the reference's ParameterError text in `message`.
+int tsdd_generate_series(std::uint64_t m, int anomaly, std::uint64_t anomaly_pos, std::uint64_t anomaly_len,
+                         std::uint64_t seed, double* out, char* message, std::uint64_t message_bytes) {
+  auto reject = [&](const std::string& text) {
+    if (message && message_bytes) std::snprintf(message, message_bytes, "%s", text.c_str());
+    return 2;
+  };
+  if (m < 1) return reject("generator length must be >= 1");
+  if (anomaly < 0 || anomaly > 2) return reject("unknown anomaly kind (expected none, spike or shape)");
+  const std::uint64_t extent = anomaly == 2 ? anomaly_len : 1;
+  if (anomaly != 0) {
+    if (anomaly_pos < 1 || anomaly_pos - 1 + extent > m)
+      return reject("anomaly at position " + std::to_string(anomaly_pos) + " with extent " + std::to_string(extent) +
+                    " does not fit in series of length " + std::to_string(m));
+    if (anomaly == 2 && anomaly_len < 2) return reject("shape anomaly length must be >= 2");
+  }
+  if (!out) return reject("output buffer is null");
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> step(-1.0, 1.0);
+  double level = 0.0;
+  for (std::uint64_t i = 0; i < m; ++i) {
+    level += step(rng);
+    out[i] = level;
+  }
+  if (anomaly == 1) {
+    out[anomaly_pos - 1] += 100.0;
+  } else if (anomaly == 2) {
+    const std::uint64_t start = anomaly_pos - 1;
+    const double base = out[start];
+    for (std::uint64_t t = 0; t < anomaly_len; ++t) {
+      const double phase = 6.0 * M_PI * static_cast<double>(t) / static_cast<double>(anomaly_len - 1);
+      // (one rounding: the reference's build, -O3 -march=native, contracts this into an fma)
+      out[start + t] = std::fma(12.0, std::sin(phase), base);
+    }
   }
   return 0;
 }

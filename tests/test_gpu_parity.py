@@ -747,27 +747,38 @@ def test_many_near_tied_finalists_are_all_settled(ctx, chk):
     np.testing.assert_allclose(dist, base_dist, rtol=1e-12)  # both decided in float64
 
 
-def test_finalists_follow_the_band_after_a_switch_to_the_dot_form(ctx):
+def test_finalists_follow_the_band_after_a_switch_to_the_dot_form(ctx, chk):
     """The search switches to the dot-product form MID-search (noise: no tile is abandoned); the
     discard band then widens by the form's absolute error.  The finalists must be collected with
-    that wider band, not with the one the search started with."""
+    that wider band, not with the one the search started with.  Series: noise u followed by its
+    mirror image 1 - u, perturbed by 1e-6 — every row has a mirror row whose nn distance differs
+    by ~1e-5 .. 1e-4 (squared): far inside the dot form's absolute band (0.0024 at n = 128), and,
+    with the relative parts of the band switched off, outside everything else."""
     n = 128
-    x = np.random.default_rng(5).random(40000).astype(np.float32)
-    ctx.prepare(x, n, 8, 4)
-    ctx.search(1)
-    st = ctx.stats()
+    rng = np.random.default_rng(5)
+    u = rng.random(20000).astype(np.float32)
+    v = (np.float32(1.0) - u + (1e-6 * rng.standard_normal(20000)).astype(np.float32)).astype(np.float32)
+    x = np.concatenate([u, v])
+    ctx.set_option("margin_delta", 0)
+    ctx.set_option("margin_q", 0)
+    try:
+        ctx.prepare(x, n, 8, 4)
+        pos, dist = ctx.search(2)
+        st = ctx.stats()
+    finally:
+        ctx.set_option("margin_delta", -1)
+        ctx.set_option("margin_q", -1)
     assert st["scan_kernel_dot_launches"] > 0 and st["scan_kernel_launches"] > st["scan_kernel_dot_launches"]
-    nn32 = ctx.fetch("nn_sq").astype(np.float64)
-    exact = ctx.fetch("nn_exact").astype(bool)
-    best = nn32[exact].max()
-    delta = max(4e-6, 1.2e-7 * n)
-    abs_band = 2.0 * (n + 32) * n * 2.0 ** -24
-    q = 1.25 * np.sqrt(n) * 2.0 ** -21
-    def count(slack):
-        return int(np.sum(exact & (nn32 * (1 + delta) + (abs_band + q * np.sqrt(best)) * slack >= best)))
-    narrow = int(np.sum(exact & (nn32 * (1 + delta) >= best)))
-    assert count(0.999) <= st["finalists"] <= count(1.001), (count(0.999), st["finalists"], count(1.001))
-    assert st["finalists"] > narrow, (st["finalists"], narrow)  # (the wide band does hold more rows here)
+    profile = chk.nn_profile(x, n)
+    own_pos, own_dist = topk_from_profile(profile, n, 2)
+    assert pos == own_pos, (pos, own_pos)
+    np.testing.assert_allclose(dist, own_dist, rtol=1e-12)
+    # the second discord and its mirror row are a near-tie: both must have been finalists
+    second = own_pos[1] - 1
+    mirror = second + 20000 if second < 20000 else second - 20000
+    gap = abs(profile[second] - profile[mirror])
+    assert 0 < gap < 1e-3, gap
+    assert st["finalists"] >= 3, st["finalists"]
 
 
 def test_device_series_is_validated_on_the_device(ctx):

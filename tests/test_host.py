@@ -290,6 +290,72 @@ def test_cli_generate_writes_the_pinned_workloads(tmp_path, golden):
     assert _cli("generate", "--workload", 9, "--output", out).returncode == 2
 
 
+@pytest.mark.parametrize("flags,kw", [
+    (["--m", 500, "--seed", 7], dict(m=500, seed=7)),
+    (["--m", 2000, "--anomaly", "spike", "--anomaly-pos", 1200, "--seed", 3],
+     dict(m=2000, anomaly="spike", anomaly_pos=1200, seed=3)),
+    (["--m", 3000, "--anomaly", "shape", "--anomaly-pos", 901, "--anomaly-len", 100],
+     dict(m=3000, anomaly="shape", anomaly_pos=901, anomaly_len=100)),
+    (["--m", 64, "--anomaly", "shape", "--anomaly-pos", 1, "--anomaly-len", 64, "--seed", 11],
+     dict(m=64, anomaly="shape", anomaly_pos=1, anomaly_len=64, seed=11)),
+])
+def test_cli_generate_with_the_reference_flags(tmp_path, flags, kw):  # tools/tsdd.cpp:140-153, src/generate.cpp:19-59
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    want = oracle.ref().generate_series(**kw)
+    raw = tmp_path / "g.f64le"
+    p = _cli("generate", *flags, "--output", raw, "--format", "f64le")
+    assert p.returncode == 0, p.stderr
+    assert f"series: {kw['m']} values" in p.stderr  # print_series_summary, like the reference's tool
+    got = np.fromfile(raw, dtype=np.float64)
+    np.testing.assert_array_equal(got, want)  # bit-identical to the reference's generator
+    csv = tmp_path / "g.csv"
+    assert _cli("generate", *flags, "--output", csv).returncode == 0  # default format: csv, "%.17g" per line
+    np.testing.assert_array_equal(np.loadtxt(csv, dtype=np.float64, ndmin=1), want)
+
+
+@pytest.mark.parametrize("flags,kw", [
+    (["--m", 0], dict(m=0)),
+    (["--m", 100, "--anomaly", "spike"], dict(m=100, anomaly="spike")),
+    (["--m", 100, "--anomaly", "spike", "--anomaly-pos", 101], dict(m=100, anomaly="spike", anomaly_pos=101)),
+    (["--m", 100, "--anomaly", "shape", "--anomaly-pos", 50, "--anomaly-len", 52],
+     dict(m=100, anomaly="shape", anomaly_pos=50, anomaly_len=52)),
+    (["--m", 100, "--anomaly", "shape", "--anomaly-pos", 50, "--anomaly-len", 1],
+     dict(m=100, anomaly="shape", anomaly_pos=50, anomaly_len=1)),
+    (["--m", 100, "--anomaly", "wave"], dict(m=100, anomaly="wave")),
+])
+def test_cli_generate_rejects_what_the_reference_rejects(tmp_path, flags, kw):
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not built")
+    with pytest.raises(oracle.OracleError) as ref:
+        oracle.ref().generate_series(**kw)
+    p = _cli("generate", *flags, "--output", tmp_path / "x.csv")
+    assert ref.value.code == 2 and p.returncode == 2
+    assert ref.value.message in p.stderr, (ref.value.message, p.stderr)
+
+
+def test_breakpoint_generator_reproduces_the_device_table():
+    """tools/gen_sax_breakpoints.py (scipy norm.ppf, lower half mirrored) prints exactly the
+    c_breaks table of csrc/prep_kernels.cu — the values of the reference's sax.cpp:14-46."""
+    import re
+
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "gen_sax_breakpoints.py")], capture_output=True,
+                       text=True)
+    assert p.returncode == 0, p.stderr
+    src = open(os.path.join(ROOT, "paper_1901_00155_b200", "csrc", "prep_kernels.cu")).read()
+    table = src[src.index("c_breaks[9][9] = {"):]
+    table = table[:table.index("};")]
+    number = r"-?\d+(?:\.\d+)?(?:e-?\d+)?"
+    have = [float(v) for v in re.findall(number, table[table.index("{", 20):])]
+    want = [float(v) for v in re.findall(number, p.stdout[p.stdout.index("{"):])]
+    assert have == want and len(want) == sum(range(1, 10))
+    chk = oracle.best()
+    for a in range(2, 11):  # and symbol_for agrees with the table on both sides of every breakpoint
+        row = want[sum(range(1, a - 1)):sum(range(1, a))]
+        for j, beta in enumerate(row):
+            assert chk.symbol_for(a, beta) == j + 2 and chk.symbol_for(a, np.nextafter(beta, -np.inf)) == j + 1
+
+
 # ------------------------------------------------------------------ bench.py contract (reference arm runs on CPU)
 def test_bench_reference_arm_prints_the_contract_line():
     import json

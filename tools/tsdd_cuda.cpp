@@ -13,7 +13,10 @@
 //                      [--k K] [--gpus 0,1,...] [--disable-pruning] [--output json|csv]
 //   tsdd_cuda bench    --input FILE [--format ...] --n N1,N2,... [--gpus 1,2,4,8] [--repeats R]
 //                      [--word-len W] [--alphabet A] [--k K] [--output FILE]
-//   tsdd_cuda generate --workload 1..5 --output FILE [--format f32le|f64le|csv]     (needs libtsdd_gen.so)
+//   tsdd_cuda generate --m M [--anomaly none|spike|shape] [--anomaly-pos P] [--anomaly-len L] [--seed S]
+//                      --output FILE [--format csv|f64le|f32le]        the reference's generator (tools/tsdd.cpp:140-153)
+//   tsdd_cuda generate --workload 1..5 --output FILE [--format f32le|f64le|csv]     the BASELINE.json workloads
+//                                                                       (both need libtsdd_gen.so beside the tool)
 //
 // `--threads`, `--chunk`, `--vec-width` are accepted and validated like the reference's and
 // have no effect on the device.  `--gpus` lists CUDA devices (find) or device COUNTS to sweep
@@ -342,21 +345,75 @@ int run_bench(const Flags& flags) {
   return 0;
 }
 
-// ------------------------------------------------------------------ generate (the BASELINE.json workloads)
-int run_generate(const Flags& flags, const char* argv0) {
-  if (!flags.has("workload") || !flags.has("output")) throw ParameterError("--workload and --output are required");
-  const int cfg = static_cast<int>(to_size(flags.get("workload"), "workload"));
+// ------------------------------------------------------------------ generate
+void write_series(const std::vector<double>& values, const std::string& path, Format format) {
+  // (the reference's write_series, src/io.cpp:101-127: "%.17g" per line, or raw little-endian doubles)
+  std::ofstream out(path, format == Format::csv ? std::ios::out : std::ios::binary);
+  if (!out) throw ValidationError("cannot open '" + path + "' for writing");
+  if (format == Format::csv) {
+    char buf[64];
+    for (const double v : values) {
+      std::snprintf(buf, sizeof(buf), "%.17g\n", v);
+      out << buf;
+    }
+  } else if (format == Format::f64le) {
+    out.write(reinterpret_cast<const char*>(values.data()), static_cast<std::streamsize>(values.size() * sizeof(double)));
+  } else {
+    const std::vector<float> narrow(values.begin(), values.end());
+    out.write(reinterpret_cast<const char*>(narrow.data()), static_cast<std::streamsize>(narrow.size() * sizeof(float)));
+  }
+  if (!out) throw ValidationError("write to '" + path + "' failed");
+}
+
+void* open_generators(const char* argv0) {
   std::string dir = argv0;
   dir = dir.find('/') == std::string::npos ? "." : dir.substr(0, dir.rfind('/'));
   const std::string lib = dir + "/libtsdd_gen.so";
   void* handle = dlopen(lib.c_str(), RTLD_NOW);
   if (!handle) throw ValidationError("cannot load " + lib + ": " + dlerror());
+  return handle;
+}
+
+// `generate --m ...`: the reference's own generator family and flags (tools/tsdd.cpp:140-153,
+// src/generate.cpp:19-59): uniform-step walk, optional spike / shape anomaly, default format csv.
+int run_generate_walk(const Flags& flags, const char* argv0) {
+  if (!flags.has("m") || !flags.has("output")) throw ParameterError("--m and --output are required");
+  const std::string kind = flags.get("anomaly", "none");
+  int anomaly = 0;
+  if (kind == "none") anomaly = 0;
+  else if (kind == "spike") anomaly = 1;
+  else if (kind == "shape") anomaly = 2;
+  else throw ParameterError("unknown anomaly kind '" + kind + "' (expected none, spike or shape)");
+  const std::size_t m = to_size(flags.get("m"), "m");
+  const std::size_t pos = flags.has("anomaly-pos") ? to_size(flags.get("anomaly-pos"), "anomaly-pos") : 0;
+  const std::size_t len = flags.has("anomaly-len") ? to_size(flags.get("anomaly-len"), "anomaly-len") : 64;
+  const std::size_t seed = flags.has("seed") ? to_size(flags.get("seed"), "seed") : 0;
+  const Format format = parse_format(flags.get("format", "csv"));
+  using GenFn = int (*)(std::uint64_t, int, std::uint64_t, std::uint64_t, std::uint64_t, double*, char*, std::uint64_t);
+  auto generate = reinterpret_cast<GenFn>(dlsym(open_generators(argv0), "tsdd_generate_series"));
+  if (!generate) throw ValidationError("libtsdd_gen.so lacks tsdd_generate_series");
+  tsdd::TimeSeries series;
+  series.values.resize(m);
+  char message[256] = {0};
+  if (generate(m, anomaly, pos, len, seed, series.values.data(), message, sizeof(message)) != 0)
+    throw ParameterError(message);
+  write_series(series.values, flags.get("output"), format);
+  print_series_summary(series);
+  return 0;
+}
+
+// `generate --workload c`: the five BASELINE.json workloads (float32; csrc/series_gen.cpp)
+int run_generate(const Flags& flags, const char* argv0) {
+  if (!flags.has("workload")) return run_generate_walk(flags, argv0);
+  if (!flags.has("output")) throw ParameterError("--workload and --output are required");
+  const int cfg = static_cast<int>(to_size(flags.get("workload"), "workload"));
+  void* handle = open_generators(argv0);
   using InfoFn = int (*)(int, std::uint64_t*, std::uint64_t*, std::uint64_t*, std::uint64_t*, int*, std::uint64_t*,
                          int*, std::uint64_t*);
   using SeriesFn = int (*)(int, float*, std::uint64_t, std::uint64_t*);
   auto info = reinterpret_cast<InfoFn>(dlsym(handle, "tsdd_workload_info"));
   auto fill = reinterpret_cast<SeriesFn>(dlsym(handle, "tsdd_workload_series"));
-  if (!info || !fill) throw ValidationError(lib + " lacks the workload generators");
+  if (!info || !fill) throw ValidationError("libtsdd_gen.so lacks the workload generators");
   std::uint64_t m = 0, n = 0, w = 0, a = 0, seed = 0, alen = 0, at[8] = {0};
   int k = 0, anomalies = 0;
   if (info(cfg, &m, &n, &w, &a, &k, &seed, &anomalies, &alen) != 0)
@@ -374,7 +431,8 @@ int run_generate(const Flags& flags, const char* argv0) {
 int main(int argc, char** argv) {
   try {
     const std::vector<std::string> known = {"input", "format", "n", "word-len", "alphabet", "vec-width", "engine",
-                                            "threads", "chunk", "output", "k", "gpus", "repeats", "workload"};
+                                            "threads", "chunk", "output", "k", "gpus", "repeats", "workload", "m", "anomaly",
+                                            "anomaly-pos", "anomaly-len", "seed"};
     const Flags flags = parse_flags(argc, argv, known, {"disable-pruning"});
     if (flags.command == "find") return run_find(flags);
     if (flags.command == "bench") return run_bench(flags);
