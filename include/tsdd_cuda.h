@@ -156,6 +156,13 @@ int tsdd_cuda_prepare_f64(tsdd_cuda_ctx* ctx, const double* series, size_t m, si
 int tsdd_cuda_prepare_device_f32(tsdd_cuda_ctx* ctx, const float* d_series, size_t m, size_t n,
                                  size_t word_len, size_t alphabet);
 
+/* Rebuilds only what depends on the SAX shape — window encoding (sax.cpp:82-132) and
+ * DiscordIndexes::build (index.cpp:101-109) — on a prepared context, keeping the resident
+ * series and subsequence matrix.  This is what lets the C++ mirrors in
+ * include/tsdd/cuda_engine.hpp follow the reference's two-step preparation
+ * (SubsequenceMatrix::build, then DiscordIndexes::build).                    */
+int tsdd_cuda_reindex(tsdd_cuda_ctx* ctx, size_t word_len, size_t alphabet);
+
 /* ---- search stage (replaces phidd_discord, discovery.cpp:360-373) -------- */
 
 #define TSDD_SEARCH_DISABLE_PRUNING 1u /* DiscoveryOptions::disable_pruning (discovery.hpp:31) */
@@ -195,6 +202,10 @@ size_t tsdd_cuda_row_stride(const tsdd_cuda_ctx* ctx);
 
 /* Copies one prepared array to host memory.  bytes must be the exact size. */
 int tsdd_cuda_fetch(tsdd_cuda_ctx* ctx, int what, void* dst, size_t bytes);
+
+/* Rows [first_row, first_row + n_rows) of the matrix (0-based, n_rows * stride floats):
+ * SubsequenceMatrix::row (series.hpp:53) without moving the whole matrix.   */
+int tsdd_cuda_fetch_rows(tsdd_cuda_ctx* ctx, size_t first_row, size_t n_rows, float* dst);
 
 /* ---- several GPUs: candidates sharded, best-so-far max-reduced ----------- */
 

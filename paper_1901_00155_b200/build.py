@@ -98,9 +98,24 @@ def build_tools(force: bool = False) -> str:
     return target
 
 
+def build_test_programs(force: bool = False) -> str:
+    """tests/cpp/mirror_check: the reference-shaped C++ entry points (SubsequenceMatrix::build ->
+    DiscordIndexes::build -> phidd_discord) of include/tsdd/cuda_engine.hpp, driven by the GPU tests."""
+    target = os.path.join(LIB, "mirror_check")
+    src = os.path.join(ROOT, "tests", "cpp", "mirror_check.cpp")
+    deps = [src, os.path.join(INCLUDE, "tsdd", "cuda_engine.hpp"), os.path.join(INCLUDE, "tsdd_cuda.h"),
+            os.path.join(LIB, "libtsdd_cuda.so")]
+    if force or _stale(target, deps):
+        cxx = HOST_CXX if os.path.exists(HOST_CXX) else "g++"
+        _run([cxx, "-std=c++17", "-O2", "-Wall", "-Wextra", "-I", INCLUDE, "-o", target, src, "-L", LIB,
+              "-ltsdd_cuda", "-ldl", "-lpthread", "-Wl,-rpath,$ORIGIN"])
+    return target
+
+
 def build_all(force: bool = False, verbose: bool = False) -> dict:
     out = {"gen": build_gen(force), "cuda": build_cuda(force, verbose)}
     out["cli"] = build_tools(force)
+    out["mirror_check"] = build_test_programs(force)
     return out
 
 

@@ -323,6 +323,56 @@ uint64_t dict_size_of(size_t word_len, size_t alphabet) {
 }
 
 // ------------------------------------------------------------------ preparation
+// The SAX-word bucket / frequency / rarity index of the hashes in ctx->hash0 (index.cpp:12-109):
+// stable radix sort of (hash, row) -> runs are the buckets; run-length histogram -> frequencies;
+// stable sort of (frequency, row) -> rarity order.  Returns the kernels launched.
+uint64_t build_index(tsdd_cuda_ctx* ctx) {
+  cudaStream_t st = ctx->stream;
+  const uint32_t rows = ctx->rows;
+  const size_t word_len = ctx->word_len, alphabet = ctx->alphabet;
+  uint64_t launches = 0;
+  // bucket index: stable sort of (hash, row) -> runs are the buckets
+  const size_t longest_scan = std::max<size_t>(rows, radix_sort_scratch_words(rows));
+  ctx->scan_scratch.alloc(scan_scratch_words(static_cast<uint32_t>(longest_scan)) + 1024);
+  ctx->radix_hist.alloc(radix_sort_scratch_words(rows));
+  for (auto& b : ctx->sort_buf) b.alloc(rows);
+  for (auto& b : ctx->order_buf) b.alloc(rows);
+  CUDA_OK(cudaMemcpyAsync(ctx->sort_buf[0].ptr, ctx->hash0.ptr, rows * sizeof(uint32_t),
+                          cudaMemcpyDeviceToDevice, st));
+  launches += launch_iota(ctx->sort_buf[1].ptr, rows, st);
+  uint32_t *k0 = ctx->sort_buf[0].ptr, *v0 = ctx->sort_buf[1].ptr, *k1 = ctx->sort_buf[2].ptr,
+           *v1 = ctx->sort_buf[3].ptr;
+  const int hash_bits = bits_for(dict_size_of(word_len, alphabet) - 1);
+  launches += launch_radix_sort_pairs(&k0, &v0, &k1, &v1, rows, hash_bits, ctx->radix_hist.ptr,
+                                      ctx->scan_scratch.ptr, st);
+  ctx->sorted_hash = k0;
+  ctx->sorted_row = v0;
+  ctx->slot_of_row.alloc(rows);
+  launches += launch_invert_order(ctx->sorted_row, rows, ctx->slot_of_row.ptr, st);
+
+  ctx->slot_bucket.alloc(rows);
+  ctx->offsets.alloc(static_cast<size_t>(rows) + 1);
+  ctx->freq.alloc(rows);
+  ctx->scalars.alloc(4);
+  CUDA_OK(cudaMemsetAsync(ctx->scalars.ptr, 0, 4 * sizeof(uint32_t), st));
+  launches += launch_bucket_index(ctx->sorted_hash, ctx->sorted_row, rows, /*heads=*/k1, ctx->slot_bucket.ptr,
+                                  ctx->offsets.ptr, ctx->freq.ptr, ctx->scalars.ptr, ctx->scan_scratch.ptr, st);
+
+  // rarity order: stable sort of (freq, row): rarest words first, ties by position
+  CUDA_OK(cudaMemcpyAsync(ctx->order_buf[0].ptr, ctx->freq.ptr, rows * sizeof(uint32_t),
+                          cudaMemcpyDeviceToDevice, st));
+  launches += launch_iota(ctx->order_buf[1].ptr, rows, st);
+  uint32_t *f0 = ctx->order_buf[0].ptr, *o0 = ctx->order_buf[1].ptr, *f1 = ctx->order_buf[2].ptr,
+           *o1 = ctx->order_buf[3].ptr;
+  launches += launch_radix_sort_pairs(&f0, &o0, &f1, &o1, rows, bits_for(rows), ctx->radix_hist.ptr,
+                                      ctx->scan_scratch.ptr, st);
+  ctx->sorted_freq = f0;
+  ctx->order = o0;
+  launches += launch_count_min_freq(ctx->sorted_freq, rows, ctx->scalars.ptr, st);
+
+  return launches;
+}
+
 void prepare_on_device(tsdd_cuda_ctx* ctx, size_t m, size_t n, size_t word_len, size_t alphabet) {
   // ctx->series_f32 or ctx->series already holds the samples; `have_f64` says which
   cudaStream_t st = ctx->stream;
@@ -370,44 +420,7 @@ void prepare_on_device(tsdd_cuda_ctx* ctx, size_t m, size_t n, size_t word_len, 
 
   CUDA_OK(cudaEventRecord(ctx->ev_prep[2], st));
   launches += launch_segment_boxes(ctx->lb_means.ptr, rows, ctx->lb_boxes.ptr, st);
-  // bucket index: stable sort of (hash, row) -> runs are the buckets
-  const size_t longest_scan = std::max<size_t>(rows, radix_sort_scratch_words(rows));
-  ctx->scan_scratch.alloc(scan_scratch_words(static_cast<uint32_t>(longest_scan)) + 1024);
-  ctx->radix_hist.alloc(radix_sort_scratch_words(rows));
-  for (auto& b : ctx->sort_buf) b.alloc(rows);
-  for (auto& b : ctx->order_buf) b.alloc(rows);
-  CUDA_OK(cudaMemcpyAsync(ctx->sort_buf[0].ptr, ctx->hash0.ptr, rows * sizeof(uint32_t),
-                          cudaMemcpyDeviceToDevice, st));
-  launches += launch_iota(ctx->sort_buf[1].ptr, rows, st);
-  uint32_t *k0 = ctx->sort_buf[0].ptr, *v0 = ctx->sort_buf[1].ptr, *k1 = ctx->sort_buf[2].ptr,
-           *v1 = ctx->sort_buf[3].ptr;
-  const int hash_bits = bits_for(dict_size_of(word_len, alphabet) - 1);
-  launches += launch_radix_sort_pairs(&k0, &v0, &k1, &v1, rows, hash_bits, ctx->radix_hist.ptr,
-                                      ctx->scan_scratch.ptr, st);
-  ctx->sorted_hash = k0;
-  ctx->sorted_row = v0;
-  ctx->slot_of_row.alloc(rows);
-  launches += launch_invert_order(ctx->sorted_row, rows, ctx->slot_of_row.ptr, st);
-
-  ctx->slot_bucket.alloc(rows);
-  ctx->offsets.alloc(static_cast<size_t>(rows) + 1);
-  ctx->freq.alloc(rows);
-  ctx->scalars.alloc(4);
-  CUDA_OK(cudaMemsetAsync(ctx->scalars.ptr, 0, 4 * sizeof(uint32_t), st));
-  launches += launch_bucket_index(ctx->sorted_hash, ctx->sorted_row, rows, /*heads=*/k1, ctx->slot_bucket.ptr,
-                                  ctx->offsets.ptr, ctx->freq.ptr, ctx->scalars.ptr, ctx->scan_scratch.ptr, st);
-
-  // rarity order: stable sort of (freq, row): rarest words first, ties by position
-  CUDA_OK(cudaMemcpyAsync(ctx->order_buf[0].ptr, ctx->freq.ptr, rows * sizeof(uint32_t),
-                          cudaMemcpyDeviceToDevice, st));
-  launches += launch_iota(ctx->order_buf[1].ptr, rows, st);
-  uint32_t *f0 = ctx->order_buf[0].ptr, *o0 = ctx->order_buf[1].ptr, *f1 = ctx->order_buf[2].ptr,
-           *o1 = ctx->order_buf[3].ptr;
-  launches += launch_radix_sort_pairs(&f0, &o0, &f1, &o1, rows, bits_for(rows), ctx->radix_hist.ptr,
-                                      ctx->scan_scratch.ptr, st);
-  ctx->sorted_freq = f0;
-  ctx->order = o0;
-  launches += launch_count_min_freq(ctx->sorted_freq, rows, ctx->scalars.ptr, st);
+  launches += build_index(ctx);
   CUDA_OK(cudaEventRecord(ctx->ev_prep[3], st));
 
   // search-state storage
@@ -1243,6 +1256,50 @@ int tsdd_cuda_prepare_device_f32(tsdd_cuda_ctx* ctx, const float* d_series, size
       ctx->prepared = false;
       fail(TSDD_ERR_VALIDATION, "non-finite value at index " + std::to_string(static_cast<uint64_t>(bad) + 1));
     }
+  });
+}
+
+int tsdd_cuda_reindex(tsdd_cuda_ctx* ctx, size_t word_len, size_t alphabet) {
+  if (!ctx) return TSDD_ERR_PARAMETER;
+  return guarded(ctx, [&] {
+    if (!ctx->prepared) fail(TSDD_ERR_PARAMETER, "tsdd_cuda_reindex needs a prepared context");
+    check_shape(ctx->m, ctx->n, word_len, alphabet);
+    bind_device(ctx);
+    cudaStream_t st = ctx->stream;
+    ctx->word_len = word_len;
+    ctx->alphabet = alphabet;
+    ctx->sorted_ready = false;  // (the hash-sorted copy of the matrix follows the OLD order)
+    CUDA_OK(cudaEventRecord(ctx->ev_a, st));
+    uint64_t launches = launch_window_encode(ctx->series.ptr, ctx->rows, static_cast<uint32_t>(ctx->n),
+                                             static_cast<uint32_t>(word_len), static_cast<uint32_t>(alphabet),
+                                             ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->hash0.ptr, nullptr, nullptr, st);
+    launches += build_index(ctx);
+    uint32_t scalars[4] = {0, 0, 0, 0};
+    CUDA_OK(cudaMemcpyAsync(scalars, ctx->scalars.ptr, sizeof(scalars), cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaEventRecord(ctx->ev_b, st));
+    sync_stream(ctx);
+    float ms = 0.f;
+    CUDA_OK(cudaEventElapsedTime(&ms, ctx->ev_a, ctx->ev_b));
+    ctx->stats.index_ms = ms;
+    ctx->stats.prep_ms += ms;
+    ctx->stats.kernel_launches += launches;
+    ctx->stats.buckets = scalars[0];
+    ctx->stats.min_freq_candidates = scalars[1];
+  });
+}
+
+int tsdd_cuda_fetch_rows(tsdd_cuda_ctx* ctx, size_t first_row, size_t n_rows, float* dst) {
+  if (!ctx) return TSDD_ERR_PARAMETER;
+  return guarded(ctx, [&] {
+    if (!ctx->prepared) fail(TSDD_ERR_PARAMETER, "tsdd_cuda_fetch_rows needs a prepared context");
+    if (!dst) fail(TSDD_ERR_PARAMETER, "dst must not be null");
+    if (first_row > ctx->rows || n_rows > ctx->rows - first_row)
+      fail(TSDD_ERR_PARAMETER, "rows " + std::to_string(first_row) + " .. " + std::to_string(first_row + n_rows) +
+                                   " are outside 0 .. " + std::to_string(ctx->rows));
+    bind_device(ctx);
+    sync_stream(ctx);
+    CUDA_OK(cudaMemcpy(dst, ctx->matrix.ptr + first_row * ctx->stride, n_rows * ctx->stride * sizeof(float),
+                       cudaMemcpyDeviceToHost));
   });
 }
 

@@ -85,6 +85,8 @@ SYMBOLS = {
     "tsdd_cuda_prepare_f32": (_int, [_vp, _vp, _sz, _sz, _sz, _sz]),
     "tsdd_cuda_prepare_f64": (_int, [_vp, _vp, _sz, _sz, _sz, _sz]),
     "tsdd_cuda_prepare_device_f32": (_int, [_vp, _vp, _sz, _sz, _sz, _sz]),
+    "tsdd_cuda_reindex": (_int, [_vp, _sz, _sz]),
+    "tsdd_cuda_fetch_rows": (_int, [_vp, _sz, _sz, _vp]),
     "tsdd_cuda_search": (_int, [_vp, _int, ctypes.c_uint, _vp, _vp]),
     "tsdd_cuda_get_stats": (_int, [_vp, ctypes.POINTER(Stats)]),
     "tsdd_cuda_row_stride": (_sz, [_vp]),
@@ -242,6 +244,17 @@ class Context:
         """float32 series already in device memory (e.g. ``torch_tensor.data_ptr()``)."""
         self._check(self._lib.tsdd_cuda_prepare_device_f32(self._h, d_series_ptr, m, n, word_len, alphabet))
         self._shape = (m, n, word_len, alphabet)
+
+    def reindex(self, word_len: int, alphabet: int):
+        """Window encoding + DiscordIndexes::build again for another SAX shape; the matrix stays."""
+        self._check(self._lib.tsdd_cuda_reindex(self._h, word_len, alphabet))
+        m, n, _, _ = self._shape
+        self._shape = (m, n, word_len, alphabet)
+
+    def fetch_rows(self, first: int, count: int) -> np.ndarray:
+        out = np.empty((count, self.row_stride()), dtype=np.float32)
+        self._check(self._lib.tsdd_cuda_fetch_rows(self._h, first, count, out.ctypes.data))
+        return out
 
     def search(self, k: int = 1, disable_pruning: bool = False):
         pos = np.zeros(max(k, 1), dtype=np.uint64)

@@ -801,3 +801,101 @@ def test_device_series_is_validated_on_the_device(ctx):
     d = torch.from_numpy(x).cuda()
     ctx.prepare_device(d.data_ptr(), len(x), 64, 4, 4)
     ctx.search(1)
+
+
+# ------------------------------------------------------------------ the reference-shaped C++ boundary
+import json  # noqa: E402
+import os  # noqa: E402
+import subprocess  # noqa: E402
+
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+MIRROR_CHECK = os.path.join(_ROOT, "paper_1901_00155_b200", "_lib", "mirror_check")
+TSDD_PATCHED = os.path.join(_ROOT, "oracle", "_ref", "tsdd_patched")
+
+
+@pytest.mark.parametrize("m,n,w,a,k", [(3000, 64, 4, 4, 1), (2500, 50, 3, 5, 2), (5000, 128, 6, 3, 3)])
+def test_cpp_mirrors_of_the_reference_types(chk, tmp_path, m, n, w, a, k):
+    """tsdd::cuda::SubsequenceMatrix::build -> DiscordIndexes::build -> phidd_discord
+    (include/tsdd/cuda_engine.hpp), chained as pipeline.cpp:60-87 chains the reference's:
+    every accessor the mirrors expose against the reference's own arrays."""
+    x = planted_walk(m + n, m, n).astype(np.float64)
+    path = tmp_path / "s.f64le"
+    x.tofile(path)
+    rows_wanted = [0, 1, m - n, (m - n) // 2]
+    p = subprocess.run([MIRROR_CHECK, str(path), str(n), str(w), str(a), str(k), ",".join(map(str, rows_wanted))],
+                       capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr
+    got = json.loads(p.stdout)
+    ref = chk.prepare(x, n, w, a)
+    N = m - n + 1
+    assert got["rows"] == N and got["n"] == n and got["stride"] == (n + 63) // 64 * 64
+    assert got["pad"] == got["stride"] - n and got["vec_width"] == 8
+    np.testing.assert_array_equal(np.array(got["hashes"], dtype=np.uint64), ref["hashes"])
+    np.testing.assert_array_equal(np.array(got["freq"], dtype=np.uint32), ref["freq"])
+    np.testing.assert_array_equal(np.array(got["candidates"], dtype=np.uint64), ref["candidates"])
+    assert got["bucket_count"] == a ** w and got["total_positions"] == N
+    # WordIndex::bucket(h) (index.hpp:29): ascending 1-based positions of every occupied word
+    want_buckets = {}
+    for pos in ref["bucket_positions"]:
+        want_buckets.setdefault(int(ref["hashes"][int(pos) - 1]), []).append(int(pos))
+    assert {int(h): v for h, v in got["buckets"].items()} == want_buckets
+    for r in rows_wanted:  # SubsequenceMatrix::row(i) (series.hpp:53), float32 on the device
+        row = np.array(got["row_values"][str(r)])
+        np.testing.assert_allclose(row[:n], ref["rows"][r], rtol=0, atol=2e-6)
+        assert not row[n:].any()
+    want = chk.topk(x, n, w, a, k)
+    assert got["positions"] == want["positions"] and got["pos"] == want["positions"][0]
+    np.testing.assert_allclose(got["distances"], want["distances"], rtol=DIST_RTOL)
+    assert got["calls"] > 0 and got["abandoned"] <= got["calls"]
+
+
+def test_cpp_mirrors_keep_the_reference_error_contract(tmp_path):
+    """series.cpp:46-56 (validation, then n, then vec_width), discovery.cpp:22-29,114-121."""
+    path = tmp_path / "s.f64le"
+    np.arange(20.0).tofile(path)
+    p = subprocess.run([MIRROR_CHECK, str(path), "16", "2", "4"], capture_output=True, text=True)
+    assert p.returncode == 4 and "N=5 <= n=16 (need series length m >= 2n)" in p.stderr, p.stderr
+    p = subprocess.run([MIRROR_CHECK, str(path), "21", "2", "4"], capture_output=True, text=True)
+    assert p.returncode == 2 and "subsequence length n=21 must satisfy 1 <= n <= m=20" in p.stderr, p.stderr
+    p = subprocess.run([MIRROR_CHECK, str(path), "4", "5", "4"], capture_output=True, text=True)
+    assert p.returncode == 2 and "word_len=5 must satisfy 1 <= word_len <= n=4" in p.stderr, p.stderr
+    p = subprocess.run([MIRROR_CHECK, str(path), "4", "2", "11"], capture_output=True, text=True)
+    assert p.returncode == 2 and "outside the built-in range 2..10" in p.stderr, p.stderr
+    bad = np.arange(20.0)
+    bad[4] = np.nan
+    bad.tofile(path)
+    p = subprocess.run([MIRROR_CHECK, str(path), "4", "2", "4"], capture_output=True, text=True)
+    assert p.returncode == 3 and "non-finite value at index 5" in p.stderr, p.stderr
+
+
+def test_patched_reference_runs_the_cuda_engine(golden, chk, tmp_path):
+    """oracle/_ref/tsdd_patched = the reference's own sources with INTEGRATION.md's patch
+    (tools/patch_reference.py), compiled with TSDD_CUDA_WITH_REFERENCE_HEADERS and linked against
+    libtsdd_cuda.so.  `cuda` enters through the reference's tsdd::run_discovery and must return
+    what its own CPU engine returns from the same binary — and the golden cfg1 result."""
+    if not os.path.exists(TSDD_PATCHED):
+        pytest.skip("oracle/_ref/tsdd_patched is built where /root/reference exists")
+    x, _ = W.series(1)
+    w = W.workload(1)
+    path = tmp_path / "cfg1.f64le"
+    x.astype(np.float64).tofile(path)
+
+    def run(engine, *extra):
+        p = subprocess.run([TSDD_PATCHED, str(path), engine, str(w.n), str(w.word_len), str(w.alphabet), *extra],
+                           capture_output=True, text=True)
+        assert p.returncode == 0, p.stderr
+        return json.loads(p.stdout)
+
+    cuda = run("cuda")
+    cpu = run("phidd", str(os.cpu_count() or 1))
+    rec = golden["cfg1"]["oracle"]
+    assert cuda["engine"] == "cuda" and cpu["engine"] == "phidd"
+    assert cuda["pos"] == cpu["pos"] == rec["positions"][0]
+    assert cuda["dist"] == pytest.approx(cpu["dist"], rel=DIST_RTOL)
+    assert cuda["dist"] == pytest.approx(rec["distances"][0], rel=DIST_RTOL)
+    assert cuda["m"] == w.m and cuda["calls"] > 0 and cuda["search_time_s"] > 0
+    # the reference's error contract through the patched entry point (tools/tsdd.cpp:212-223)
+    p = subprocess.run([TSDD_PATCHED, str(path), "cuda", str(w.m), "4", "4"], capture_output=True, text=True)
+    assert p.returncode == 2 and "no subsequence has a non-self match" in p.stderr, p.stderr
+    p = subprocess.run([TSDD_PATCHED, str(path), "gpu", "128", "4", "4"], capture_output=True, text=True)
+    assert p.returncode == 2 and "unknown engine 'gpu'" in p.stderr, p.stderr

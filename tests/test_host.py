@@ -380,3 +380,40 @@ def test_bench_reference_arm_other_ranks_exit_quietly():
                         "--gpus", "2", "--steps", "1", "--warmup", "0"], capture_output=True, text=True, env=env,
                        timeout=120)
     assert p.returncode == 0 and p.stdout.strip() == ""
+
+
+# ------------------------------------------------------------------ the patched reference
+TSDD_PATCHED = os.path.join(ROOT, "oracle", "_ref", "tsdd_patched")
+REFERENCE = "/root/reference/proj"
+
+
+def test_patched_reference_builds_against_the_engine_header(tmp_path):
+    """tools/patch_reference.py applies INTEGRATION.md's four edits to a COPY of the reference;
+    the copy compiles with TSDD_CUDA_WITH_REFERENCE_HEADERS (the reference's own types under
+    include/tsdd/cuda_engine.hpp) and links against libtsdd_cuda.so.  Without a GPU the CPU
+    engines of that binary still answer like the oracle, and `cuda` fails loudly."""
+    if not os.path.isdir(REFERENCE):
+        pytest.skip("the reference tree is not on this machine; oracle/_ref/tsdd_patched travels prebuilt")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "patch_reference.py"), REFERENCE,
+                        str(tmp_path / "proj")], capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr
+    patched = open(tmp_path / "proj" / "src" / "pipeline.cpp").read()
+    assert "TSDD_CUDA_WITH_REFERENCE_HEADERS" in patched and "tsdd::cuda::run_discovery(series, config)" in patched
+    assert "cuda" in open(tmp_path / "proj" / "include" / "tsdd" / "discovery.hpp").read()
+    assert "cuda" not in open(os.path.join(REFERENCE, "include", "tsdd", "discovery.hpp")).read()  # untouched
+    p = subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "_ref/tsdd_patched"], capture_output=True, text=True)
+    assert p.returncode == 0, p.stdout + p.stderr
+    x = W.random_walk(3, 3000).astype(np.float64)
+    x[1500:1564] += 3.0 * np.sin(np.arange(64))
+    path = tmp_path / "s.f64le"
+    x.tofile(path)
+    p = subprocess.run([TSDD_PATCHED, str(path), "phidd", "64", "4", "4", "2"], capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr
+    import json
+    got = json.loads(p.stdout)
+    want = oracle.best().run_discovery(x, 64, 4, 4, threads=2)
+    assert got["engine"] == "phidd" and got["pos"] == want["position"] and got["dist"] == want["distance"]
+    import torch
+    if not torch.cuda.is_available():
+        p = subprocess.run([TSDD_PATCHED, str(path), "cuda", "64", "4", "4"], capture_output=True, text=True)
+        assert p.returncode == 1 and "no CUDA device" in p.stderr, p.stderr  # no CPU fallback behind `cuda`
