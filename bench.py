@@ -18,11 +18,16 @@ top-k time of a step is reported beside it (`topk_time_s`).
           the floating-point operations the kernels EXECUTE: a term in the direct form
           (x-y)^2 = FADD + FFMA = 3 FLOP, a term in the dot-product form
           (|a|^2 + |b|^2 - 2 a.b) = one FFMA = 2 FLOP; `algorithmic_tflops` is SURVEY.md
-          8d's figure (3 FLOP for every term, whatever the form).  `peak` is measured live
-          with an FFMA-only probe kernel (MEASURED_PEAKS.json has no FP32 entry) and
-          `peak_nominal` = 148 SMs x 128 lanes x 2 x 1.965 GHz.
+          8d's figure (3 FLOP for every term, whatever the form).  `peak` is NOMINAL:
+          148 SMs x 128 lanes x 2 FLOP x the maximum SM clock (MEASURED_PEAKS.json has no FP32
+          entry); an FFMA-only probe kernel measured live is reported beside it
+          (`peak_probe`).  `useful_frac` counts only the terms of live candidates against
+          existing rows in real columns (no dead tile slots, no padding).
   cpu_baseline : the unmodified reference (oracle/_ref; else the C restatement) on the
-          box's host cores, on a bounded sample (a prefix of the same series).
+          box's host cores, on a bounded sample (a prefix of the same series) — and the GPU
+          on EXACTLY that sample beside it (`gpu_same_input_topk_time_s`).
+  --gpus N without a launcher (no WORLD_SIZE in the environment): bench.py starts the N
+          ranks itself, one process per GPU, each with the engine's own NCCL communicator.
 
 The oracle is used here only as the timed CPU baseline, never on the product path.
 """
@@ -31,6 +36,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -98,13 +104,13 @@ def workload_inputs(cfg: int):
     return w, x
 
 
-def cpu_reference_run(cfg: int, x: np.ndarray, w, threads: int | None = None) -> dict:
+def cpu_reference_run(cfg: int, x: np.ndarray, w, threads: int | None = None, sample_m: int | None = None) -> dict:
     """The reference's own CPU path (prepare + phidd search, exclusion-zone wrapper for k > 1)
     on a prefix of the workload's series.  The one place bench.py executes oracle/."""
     import oracle
 
     chk = oracle.best()
-    sample_m = min(CPU_SAMPLE[cfg], len(x))
+    sample_m = sample_m or min(CPU_SAMPLE[cfg], len(x))
     word_len, alphabet = ORACLE_SHAPE.get(cfg, (w.word_len, w.alphabet))
     threads = threads or os.cpu_count() or 1
     t0 = time.perf_counter()
@@ -119,7 +125,8 @@ def cpu_reference_run(cfg: int, x: np.ndarray, w, threads: int | None = None) ->
     return {"value": calls / step_s, "unit": UNIT, "cores": threads, "kind": chk.kind,
             "sample": f"prefix of {sample_m} samples of cfg{cfg} (n={w.n}, k={w.k}, SAX {word_len}x{alphabet}), "
                       f"engine=phidd chunk=64",
-            "calls": calls, "prep_s": prep_s, "search_s": search_s, "wall_s": wall, "topk_time_s": step_s}
+            "calls": calls, "prep_s": prep_s, "search_s": search_s, "wall_s": wall, "topk_time_s": step_s,
+            "sample_m": sample_m, "positions": out.get("positions", [out.get("position")])}
 
 
 def run_reference_arm(args) -> None:
@@ -127,8 +134,12 @@ def run_reference_arm(args) -> None:
     if rank != 0:
         return
     w, x = workload_inputs(args.workload)
+    sample_m = min(CPU_SAMPLE[args.workload], len(x))
+    # warm-up: W short runs (thread pool, page faults, code) on a 20,000-sample prefix — a full
+    # sample run costs 10+ s and a CPU search keeps no state between runs
+    warm_m = min(20000, sample_m)
     for _ in range(args.warmup):
-        pass  # a CPU run has no warm-up state worth paying 10+ s for; the count is still reported
+        cpu_reference_run(args.workload, x, w, sample_m=warm_m)
     runs = [cpu_reference_run(args.workload, x, w) for _ in range(max(1, args.steps))]
     step_s = [r["topk_time_s"] for r in runs]
     calls = runs[0]["calls"]
@@ -139,7 +150,11 @@ def run_reference_arm(args) -> None:
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": len(runs), "warmup": args.warmup, "ms_per_step": 1e3 * sum(step_s) / len(runs),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cfg{args.workload}", "m": w.m, "n": w.n, "k": w.k, "sample": base["sample"]},
+        # the series the CPU arm really searches: a PREFIX of the workload (the full one takes the
+        # reference about an hour); the CUDA arm times this same prefix as well
+        # (cpu_baseline.gpu_same_input_topk_time_s on its line)
+        "config": {"workload": f"cfg{args.workload}", "m": sample_m, "n": w.n, "k": w.k, "full_m": w.m,
+                   "sample": base["sample"], "warmup_sample": f"prefix of {warm_m} samples"},
         "cpu_baseline": {k: base[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "topk_time_s": sum(step_s) / len(runs), "calls_per_step": calls, "gpu_launches": 0,
@@ -175,7 +190,8 @@ def run_cuda_arm(args) -> None:
         name, val = opt.split("=")
         ctx.set_option(name, float(val))
     if world > 1:
-        parallel.attach_nccl(ctx)
+        parallel.attach_nccl(ctx)  # the engine's own communicator (ncclCommInitRank inside libtsdd_cuda.so)
+    comm_nranks = ctx.comm_size()
 
     def barrier():
         if world > 1:
@@ -201,7 +217,7 @@ def run_cuda_arm(args) -> None:
     barrier()
     sampler = ClockSampler(local)
     totals = {"calls": 0, "terms": 0, "scan_terms": 0, "scan_ms": 0.0, "scan_launches": 0, "ws_launches": 0,
-              "dot_launches": 0, "dot_terms": 0,
+              "dot_launches": 0, "dot_terms": 0, "useful_terms": 0,
               "launches": 0,
               "prep_ms": 0.0, "search_ms": 0.0, "build_rows_ms": 0.0, "encode_ms": 0.0, "index_ms": 0.0}
     with sampler:
@@ -217,6 +233,7 @@ def run_cuda_arm(args) -> None:
             totals["ws_launches"] += st["scan_kernel_ws_launches"]
             totals["dot_launches"] += st["scan_kernel_dot_launches"]
             totals["dot_terms"] += st["scan_kernel_dot_terms"]
+            totals["useful_terms"] += st["useful_terms"]
             totals["launches"] += st["kernel_launches"]
             for key in ("prep_ms", "search_ms", "build_rows_ms", "encode_ms", "index_ms"):
                 totals[key] += st[key]
@@ -245,27 +262,32 @@ def run_cuda_arm(args) -> None:
     all_calls, all_e2e_calls = float(c[0]), float(c[1])
 
     if rank == 0:
-        golden_ok = None
+        golden_ok, golden_all = None, {}
         try:
-            golden = json.load(open(os.path.join(ROOT, "tests", "golden", "workloads.json")))
-            rec = golden.get(f"cfg{args.workload}")
+            golden_all = json.load(open(os.path.join(ROOT, "tests", "golden", "workloads.json")))
+            rec = golden_all.get(f"cfg{args.workload}")
             if rec:
                 golden_ok = pos == rec["oracle"]["positions"]
         except OSError:
             pass
         scan_s = totals["scan_ms"] * 1e-3
         direct_terms = totals["scan_terms"] - totals["dot_terms"]
+        useful_share = totals["useful_terms"] / max(1, totals["scan_terms"])
         executed_flop = 3.0 * direct_terms + 2.0 * totals["dot_terms"]
         pipe_ops = 2.0 * direct_terms + 1.0 * totals["dot_terms"]  # FP32-pipe lane operations
         achieved = executed_flop / scan_s / 1e12 if scan_s > 0 else 0.0
-        peak = 2.0 * ffma_ops / 1e12
-        nominal = 148 * 128 * 2 * 1.965e9 / 1e12
-        traffic = None
+        clocks = sampler.summary()
+        sm_max_mhz = clocks.get("sm_max_mhz") or _measured_peak("sm_max_mhz", 1965.0)[0]
+        props = torch.cuda.get_device_properties(local)
+        peak = props.multi_processor_count * 128 * 2 * sm_max_mhz * 1e6 / 1e12  # nominal FP32 FMA peak
+        peak_probe = 2.0 * ffma_ops / 1e12
+        # DRAM traffic of the dominant kernel: only from an ncu capture of THIS workload
+        traffic, prof = None, {}
         try:
-            prof = json.load(open(os.path.join(ROOT, "profiles", "scan_tiles_summary.json")))
+            prof = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json"))).get(f"cfg{args.workload}", {})
             traffic = prof.get("dram_bytes_per_launch")
         except (OSError, ValueError):
-            prof = {}
+            pass
         N = w.m - w.n + 1
         matrix_bytes = 4.0 * N * ((w.n + 31) // 32 * 32)
         line = {
@@ -291,21 +313,30 @@ def run_cuda_arm(args) -> None:
                                    % (totals["ws_launches"], totals["scan_launches"], totals["dot_launches"]),
                          "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
-                         "peak_source": "live FFMA-only probe kernel x 2 FLOP (MEASURED_PEAKS.json has no FP32 "
-                                        "entry; B200_PROFILING.md states no FP32 fallback)",
-                         "peak_nominal": nominal, "frac_nominal": achieved / nominal,
+                         "peak_source": "nominal: %d SMs x 128 FP32 lanes x 2 FLOP x %.0f MHz (the maximum SM clock; "
+                                        "MEASURED_PEAKS.json has no FP32 entry and B200_PROFILING.md states no FP32 "
+                                        "fallback)" % (props.multi_processor_count, sm_max_mhz),
+                         "peak_probe": peak_probe, "frac_probe": achieved / peak_probe if peak_probe else None,
+                         "peak_probe_source": "live FFMA-only probe kernel (csrc/probe_kernels.cu: 16 independent "
+                                              "FFMA chains per thread, nothing else in the loop) x 2 FLOP",
+                         "useful_share_of_terms": useful_share, "useful_frac": achieved * useful_share / peak,
+                         "useful_definition": "terms of (live candidate, existing neighbour row) pairs in columns "
+                                              "t < n: no dead or empty candidate slots of a tile, no slots past the "
+                                              "last row, no zero padding of the row stride",
                          "terms_per_s": totals["scan_terms"] / scan_s if scan_s else 0.0,
                          "dot_form_share_of_terms": totals["dot_terms"] / max(1, totals["scan_terms"]),
                          "algorithmic_tflops": 3.0 * totals["scan_terms"] / scan_s / 1e12 if scan_s else 0.0,
-                         "fma_pipe_util": pipe_ops / scan_s / ffma_ops if scan_s else 0.0,
+                         "fma_pipe_util": pipe_ops / scan_s / (peak * 1e12 / 2.0) if scan_s else 0.0,
+                         "fma_pipe_util_vs_probe": pipe_ops / scan_s / ffma_ops if scan_s else 0.0,
                          "sub_fma_mix_probe_lane_ops_per_s": mix_ops, "ffma_probe_lane_ops_per_s": ffma_ops,
                          "launches": int(totals["scan_launches"]),
                          "avg_launch_ms": totals["scan_ms"] / max(1, totals["scan_launches"]),
                          "kernel_share_of_step": totals["scan_ms"] / elapsed_ms, "traffic": traffic,
-                         "traffic_source": "ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum of ONE captured "
-                                           "launch (%s; %s ms) — compare with that launch, not with avg_launch_ms"
-                                           % (prof.get("captured_kernel", "see profiles/scan_tiles_summary.json"),
-                                              prof.get("captured_launch_ms", "?"))},
+                         "traffic_source": ("ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum of ONE captured "
+                                            "launch of this workload (%s; %s ms; %s) — compare with that launch, not "
+                                            "with avg_launch_ms" % (prof.get("captured_kernel"), prof.get("captured_launch_ms"),
+                                                                    prof.get("source"))) if traffic else
+                                           "no ncu capture of this workload's dominant kernel is on file"},
             "roofline_prep": {"bound": "hbm", "kernel": "k_build_rows", "unit": "GB/s",
                               "achieved": matrix_bytes * args.steps / (totals["build_rows_ms"] * 1e-3) / 1e9
                               if totals["build_rows_ms"] else None,
@@ -314,18 +345,79 @@ def run_cuda_arm(args) -> None:
             "stage_ms_per_step": {key: totals[key] / args.steps for key in
                                   ("prep_ms", "encode_ms", "build_rows_ms", "index_ms", "search_ms")},
             "calls_per_step": all_calls / args.steps, "terms_per_step": totals["terms"] / args.steps,
-            "clocks": sampler.summary(),
+            "clocks": clocks,
+            "comm": {"nranks": comm_nranks, "backend": "the engine's own NCCL communicator (tsdd_cuda_comm_init -> "
+                     "ncclCommInitRank; nranks from ncclCommCount)" if world > 1 else "none (one rank)"},
         }
         rp = line["roofline_prep"]
         rp["frac"] = rp["achieved"] / rp["peak"] if rp["achieved"] else None
+        if world == 1 and not args.no_secondary and args.workload != 4:
+            line["other_workloads"] = {"cfg4": time_other_workload(ctx, 4, local, golden_all)}
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_reference_run(args.workload, x, w)
             line["cpu_baseline"] = {key: cb[key] for key in ("value", "unit", "cores", "kind", "sample",
                                                              "calls", "topk_time_s")}
+            # the GPU on EXACTLY the series the CPU arm searched (same prefix, same n / k; the
+            # workload's own SAX shape — results do not depend on it): time against time
+            same = time_same_input(ctx, x[:cb["sample_m"]], w, local)
+            line["cpu_baseline"].update({
+                "gpu_same_input_topk_time_s": same["topk_time_s"], "gpu_same_input_e2e_topk_time_s": same["e2e_topk_time_s"],
+                "gpu_same_input_positions_match": same["positions"] == cb["positions"],
+                "time_ratio_cpu_over_gpu_same_input": cb["topk_time_s"] / same["e2e_topk_time_s"]})
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def time_same_input(ctx, sample: np.ndarray, w, device: int, repeats: int = 3) -> dict:
+    """Device-resident and end-to-end (host series) top-k time of `sample`, median of `repeats`."""
+    import torch
+
+    from paper_1901_00155_b200 import DiscoveryConfig, run_discovery
+
+    host = torch.from_numpy(np.ascontiguousarray(sample)).pin_memory()
+    dev = host.to(f"cuda:{device}")
+    cfg = DiscoveryConfig(n=w.n, word_len=w.word_len, alphabet=w.alphabet, k=w.k, device=device)
+    resident, e2e, pos = [], [], None
+    for r in range(repeats + 1):  # (the first run allocates)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ctx.prepare_device(dev.data_ptr(), len(sample), w.n, w.word_len, w.alphabet)
+        pos, _ = ctx.search(w.k)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        run_discovery(host.numpy(), cfg, context=ctx)
+        t2 = time.perf_counter()
+        if r:
+            resident.append(t1 - t0)
+            e2e.append(t2 - t1)
+    return {"topk_time_s": statistics.median(resident), "e2e_topk_time_s": statistics.median(e2e), "positions": pos}
+
+
+def time_other_workload(ctx, cfg: int, device: int, golden: dict, repeats: int = 3) -> dict:
+    """A secondary figure on the same line: one more BASELINE.json workload, device-resident,
+    median of `repeats` complete top-k searches (preparation + search, CUDA events)."""
+    import torch
+
+    w, x = workload_inputs(cfg)
+    dev = torch.from_numpy(x).to(f"cuda:{device}")
+    stream = torch.cuda.current_stream()
+    times, pos, st = [], None, {}
+    for r in range(repeats + 1):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ctx.prepare_device(dev.data_ptr(), w.m, w.n, w.word_len, w.alphabet)
+        pos, _ = ctx.search(w.k)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if r:
+            times.append(e0.elapsed_time(e1) * 1e-3)
+        st = ctx.stats()
+    rec = golden.get(f"cfg{cfg}")
+    return {"m": w.m, "n": w.n, "k": w.k, "topk_time_s": statistics.median(times), "runs": repeats,
+            "prep_ms": st["prep_ms"], "search_ms": st["search_ms"], "calls": st["calls"],
+            "matches_golden": (pos == rec["oracle"]["positions"]) if rec else None}
 
 
 def _measured_peak(key: str, fallback: float):
@@ -344,11 +436,34 @@ def main():
     ap.add_argument("--workload", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--opt", action="append", default=[], help="engine tunable name=value")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the cfg4 figure on the cfg5 line")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(spawn_ranks(args.gpus))
     else:
         run_cuda_arm(args)
+
+
+def spawn_ranks(n: int) -> int:
+    """`python bench.py --gpus N` without a launcher: start the N ranks here, one process per GPU
+    (RANK / LOCAL_RANK / WORLD_SIZE / MASTER_* as torchrun would set them).  Rank 0 prints the line."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n:
+        raise SystemExit(f"bench.py: --gpus {n} needs {n} CUDA devices, this machine has {have}")
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    procs = []
+    for rank in range(n):
+        env = dict(os.environ, RANK=str(rank), LOCAL_RANK=str(rank), WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), *sys.argv[1:]], env=env))
+    codes = [p.wait() for p in procs]
+    return max(abs(c) for c in codes)
 
 
 if __name__ == "__main__":

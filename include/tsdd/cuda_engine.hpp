@@ -23,13 +23,11 @@
 #ifndef TSDD_CUDA_ENGINE_HPP
 #define TSDD_CUDA_ENGINE_HPP
 
-#include <condition_variable>
 #include <cstddef>
 #include <memory>
 #include <utility>
 #include <cstdint>
 #include <exception>
-#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -414,99 +412,54 @@ inline RunOutcome run_discovery(const TimeSeries& series, const DiscoveryConfig&
 }
 
 // ---- several GPUs from one process ------------------------------------------
-// One host thread and one Session per device; the per-batch exchange of the
-// packed best-so-far is an in-process max-reduction between the threads
-// (tsdd_cuda_set_exchange).  The kernels of different devices never wait on one
-// another — only the host threads meet.  (One process per GPU with NCCL is the
-// other way: tsdd_cuda_comm_init.)  The same device may be listed twice, which
-// is how the tests exercise the path on a single GPU.
-namespace detail {
-
-class MaxExchange {
- public:
-  explicit MaxExchange(int world) : world_(world), slots_(static_cast<std::size_t>(world)) {}
-
-  // every rank calls this with the same count; on return keys hold the element-wise max
-  int reduce(int rank, std::uint64_t* keys, std::size_t count) {
-    std::unique_lock<std::mutex> lock(mu_);
-    if (failed_) return 1;
-    slots_[static_cast<std::size_t>(rank)].assign(keys, keys + count);
-    const std::uint64_t round = round_;
-    if (++arrived_ == world_) {
-      merged_.assign(count, 0);
-      for (const auto& slot : slots_)
-        for (std::size_t i = 0; i < count && i < slot.size(); ++i)
-          if (slot[i] > merged_[i]) merged_[i] = slot[i];
-      arrived_ = 0;
-      ++round_;
-      cv_.notify_all();
-    } else {
-      cv_.wait(lock, [&] { return round_ != round || failed_; });
-      if (failed_) return 1;
-    }
-    for (std::size_t i = 0; i < count; ++i) keys[i] = merged_[i];
-    return 0;
-  }
-
-  void fail() {
-    std::lock_guard<std::mutex> lock(mu_);
-    failed_ = true;
-    cv_.notify_all();
-  }
-
- private:
-  const int world_;
-  std::mutex mu_;
-  std::condition_variable cv_;
-  std::vector<std::vector<std::uint64_t>> slots_;
-  std::vector<std::uint64_t> merged_;
-  int arrived_ = 0;
-  std::uint64_t round_ = 0;
-  bool failed_ = false;
-};
-
-struct RankHook {
-  MaxExchange* exchange;
-  int rank;
-};
-
-inline int exchange_trampoline(void* user, std::uint64_t* keys, std::size_t count) {
-  auto* hook = static_cast<RankHook*>(user);
-  return hook->exchange->reduce(hook->rank, keys, count);
-}
-
-}  // namespace detail
-
+// One host thread and one Session per device, linked into a group of ranks
+// (tsdd_cuda_group_create): the rarity-ordered candidates are dealt round-robin, the ranks
+// meet in a host barrier after every batch and exchange ON THE DEVICES — each rank
+// min-reduces its peers' nn bounds straight from their memory (NVLink P2P) and the window
+// statistics are computed in per-rank slices and gathered.  The kernels of different devices
+// never wait on one another — only the host threads meet.  (One process per GPU with NCCL is
+// the other way: tsdd_cuda_comm_init.)  The same device may be listed twice, which is how
+// the tests exercise the path on a single GPU.
 inline RunOutcome run_discovery(const TimeSeries& series, const DiscoveryConfig& config, int k,
                                 std::vector<DiscordResult>* all, const std::vector<int>& devices) {
   if (devices.size() <= 1) return run_discovery(series, config, k, all, devices.empty() ? 0 : devices[0]);
   check_host_fields(series, config);
   if (k < 1) throw ParameterError("k must be >= 1, got " + std::to_string(k));
   const int world = static_cast<int>(devices.size());
-  detail::MaxExchange exchange(world);
-  std::vector<detail::RankHook> hooks(devices.size());
+  std::vector<std::unique_ptr<Session>> sessions;
+  std::vector<tsdd_cuda_ctx*> handles;
+  for (const int device : devices) {
+    sessions.push_back(std::make_unique<Session>(device));
+    handles.push_back(sessions.back()->handle());
+  }
+  const int rc = tsdd_cuda_group_create(handles.data(), world);
+  if (rc != TSDD_OK) raise_for(rc, tsdd_cuda_last_error(handles[0]));
   std::vector<std::vector<DiscordResult>> found(devices.size());
   std::vector<tsdd_cuda_stats> stats(devices.size());
   std::vector<std::exception_ptr> errors(devices.size());
   std::vector<std::thread> workers;
   for (int rank = 0; rank < world; ++rank) {
-    hooks[static_cast<std::size_t>(rank)] = {&exchange, rank};
     workers.emplace_back([&, rank] {
       const std::size_t r = static_cast<std::size_t>(rank);
-      try {
-        Session session(devices[r]);
-        const int rc = tsdd_cuda_set_exchange(session.handle(), &detail::exchange_trampoline, &hooks[r], world, rank);
-        if (rc != TSDD_OK) raise_for(rc, tsdd_cuda_last_error(session.handle()));
-        session.prepare(series, config.n, config.word_len, config.alphabet);
-        found[r] = session.search(k, config.disable_pruning);
-        stats[r] = session.stats();
+      try {  // (a failure inside the library releases the other ranks from the group's barrier)
+        sessions[r]->prepare(series, config.n, config.word_len, config.alphabet);
+        found[r] = sessions[r]->search(k, config.disable_pruning);
+        stats[r] = sessions[r]->stats();
       } catch (...) {
         errors[r] = std::current_exception();
-        exchange.fail();  // release the other ranks
       }
     });
   }
   for (std::thread& t : workers) t.join();
+  // the rank that failed first carries the cause; the others only report that a peer failed
+  for (const std::exception_ptr& e : errors) {
+    if (!e) continue;
+    try {
+      std::rethrow_exception(e);
+    } catch (const DeviceError& d) {
+      if (std::string(d.what()).find("another rank of the group failed") == std::string::npos) throw;
+    }
+  }
   for (const std::exception_ptr& e : errors)
     if (e) std::rethrow_exception(e);
   last_run_stats() = stats;

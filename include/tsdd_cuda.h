@@ -125,6 +125,8 @@ int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream);
  * "seed_rows" (before the first scan, the best-so-far is seeded with the greatest LOWER bound of
  * a nearest-neighbour distance among this many first entries of the rarity order, from the
  * segment-mean boxes; 0 = start from zero as the reference does),
+ * "shard_prep" (0/1, default 1: ranks joined by an NCCL communicator or an in-process group
+ * each compute the window statistics and hashes of ONE slice of the rows and all-gather them),
  * "time_kernels" (0/1: CUDA events around every tile-kernel launch).
  * Unknown name -> TSDD_ERR_PARAMETER.  None of them changes the result.     */
 int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value);
@@ -220,6 +222,19 @@ int tsdd_cuda_fetch_rows(tsdd_cuda_ctx* ctx, size_t first_row, size_t n_rows, fl
  * and hands the 128 bytes to the other ranks (any transport).               */
 int tsdd_cuda_comm_unique_id(char id[128]);
 int tsdd_cuda_comm_init(tsdd_cuda_ctx* ctx, const char id[128], int world, int rank);
+/* Ranks of the context's exchange: what ncclCommCount reports for its NCCL communicator, else
+ * the world size it was given (1 for a single context).                     */
+int tsdd_cuda_comm_size(const tsdd_cuda_ctx* ctx, int* nranks);
+
+/* In-process path: `world` contexts of ONE process (one per device; the same device may carry
+ * several) become ranks 0 .. world-1 of a group, each driven by its own host thread.  The
+ * ranks meet in a host barrier and exchange on the devices: the per-batch keys through the
+ * barrier, the N nn bounds by a kernel that min-reduces the peers' arrays read straight from
+ * their memory (cudaDeviceEnablePeerAccess: NVLink / NVSwitch; staged through cudaMemcpyPeer
+ * where two devices cannot map one another).  Call once, from one thread, before the rank
+ * threads start; every rank must then make the same prepare / search calls.  A failure on one
+ * rank releases the others with TSDD_ERR_RUNTIME.                            */
+int tsdd_cuda_group_create(tsdd_cuda_ctx** ctxs, int world);
 
 /* Host-hook path (tests, or a caller that already owns a communicator): the
  * engine hands `count` packed keys on the host; the hook must return, in

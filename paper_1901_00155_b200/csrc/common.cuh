@@ -78,6 +78,11 @@ struct DeviceCounters {
   unsigned long long tiles;      // candidate-tile x neighbour-tile pairs started by the tiled kernel
   unsigned long long tile_live;  // live candidates summed over those tiles (128 per tile = dense)
   unsigned long long lb_skipped; // (candidate, neighbour tile) pairs the lower-bound filter ruled out
+  // of tile_terms, the terms of pairs (live candidate, existing neighbour row) in real columns
+  // (t < n): what is left after taking out the dead or empty candidate slots of a tile, the slots
+  // past the last row, and the zero padding of the row stride.  (Self-match pairs inside a tile,
+  // at most (2n - 1) / N of all pairs, are not taken out.)
+  unsigned long long useful_terms;
 };
 
 }  // namespace tsdd_b200

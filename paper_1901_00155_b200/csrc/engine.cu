@@ -13,6 +13,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
+#include <memory>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <limits>
@@ -85,9 +88,12 @@ struct NcclApi {
   int (*GetUniqueId)(UniqueId*) = nullptr;
   int (*CommInitRank)(Comm*, int, UniqueId, int) = nullptr;
   int (*AllReduce)(const void*, void*, size_t, int, int, Comm, cudaStream_t) = nullptr;
+  int (*AllGather)(const void*, void*, size_t, int, Comm, cudaStream_t) = nullptr;
+  int (*CommCount)(Comm, int*) = nullptr;
   int (*CommDestroy)(Comm) = nullptr;
   const char* (*GetErrorString)(int) = nullptr;
   void* handle = nullptr;
+  static constexpr int kUint8 = 1;   // ncclUint8
   static constexpr int kUint64 = 5;  // ncclUint64
   static constexpr int kMax = 2;     // ncclMax
   static constexpr int kMin = 3;     // ncclMin
@@ -103,9 +109,11 @@ struct NcclApi {
     GetUniqueId = reinterpret_cast<decltype(GetUniqueId)>(dlsym(handle, "ncclGetUniqueId"));
     CommInitRank = reinterpret_cast<decltype(CommInitRank)>(dlsym(handle, "ncclCommInitRank"));
     AllReduce = reinterpret_cast<decltype(AllReduce)>(dlsym(handle, "ncclAllReduce"));
+    AllGather = reinterpret_cast<decltype(AllGather)>(dlsym(handle, "ncclAllGather"));
+    CommCount = reinterpret_cast<decltype(CommCount)>(dlsym(handle, "ncclCommCount"));
     CommDestroy = reinterpret_cast<decltype(CommDestroy)>(dlsym(handle, "ncclCommDestroy"));
     GetErrorString = reinterpret_cast<decltype(GetErrorString)>(dlsym(handle, "ncclGetErrorString"));
-    if (!GetUniqueId || !CommInitRank || !AllReduce || !CommDestroy || !GetErrorString)
+    if (!GetUniqueId || !CommInitRank || !AllReduce || !AllGather || !CommCount || !CommDestroy || !GetErrorString)
       fail(TSDD_ERR_RUNTIME, "libnccl.so.2 lacks an expected symbol");
   }
   void check(int rc, const char* what) const {
@@ -113,6 +121,50 @@ struct NcclApi {
   }
 };
 NcclApi g_nccl;
+
+// Several contexts of ONE process working as ranks (tsdd_cuda_group_create): one host thread
+// per context.  The ranks meet in a host barrier; what they exchange stays on the devices — a
+// rank reads its peers' arrays straight from their memory (NVLink P2P, or same-device pointers
+// when several ranks share a GPU), staged through cudaMemcpyPeer where P2P is unavailable.
+struct PeerGroup {
+  explicit PeerGroup(int world_) : world(world_), members(static_cast<size_t>(world_), nullptr), slots(static_cast<size_t>(world_)) {}
+  const int world;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::vector<tsdd_cuda_ctx*> members;        // by rank; nullptr once a member is destroyed
+  std::vector<std::vector<uint64_t>> slots;   // keys of the running max-reduction
+  std::vector<uint64_t> merged;
+  int arrived = 0;
+  uint64_t round = 0;
+  bool failed = false;
+  bool peer_access = true;                     // every pair of distinct devices can map the other's memory
+
+  // Barrier + element-wise max of `count` keys (count 0: barrier only).  False once any rank has failed.
+  bool reduce_max(int rank, uint64_t* keys, size_t count) {
+    std::unique_lock<std::mutex> lock(mu);
+    if (failed) return false;
+    slots[static_cast<size_t>(rank)].assign(keys, keys + count);
+    const uint64_t my_round = round;
+    if (++arrived == world) {
+      merged.assign(count, 0);
+      for (const auto& slot : slots)
+        for (size_t i = 0; i < count && i < slot.size(); ++i) merged[i] = std::max(merged[i], slot[i]);
+      arrived = 0;
+      ++round;
+      cv.notify_all();
+    } else {
+      cv.wait(lock, [&] { return round != my_round || failed; });
+      if (round == my_round) return false;  // released by a failure
+    }
+    for (size_t i = 0; i < count; ++i) keys[i] = merged[i];
+    return true;
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lock(mu);
+    failed = true;
+    cv.notify_all();
+  }
+};
 
 }  // namespace
 
@@ -203,6 +255,11 @@ struct tsdd_cuda_ctx {
   tsdd_exchange_fn exchange_fn = nullptr;
   void* exchange_user = nullptr;
   NcclApi::Comm comm = nullptr;
+  std::shared_ptr<PeerGroup> group;  // in-process ranks (tsdd_cuda_group_create)
+  DeviceArray<uint64_t> peer_stage;  // staging for peers' bounds where P2P mapping is unavailable
+  bool several() const { return world > 1 || comm != nullptr || group != nullptr; }
+  uint32_t shard_rows = 0;           // > 0: window statistics / hashes are computed in per-rank slices of this many rows
+  bool opt_shard_prep = true;
 
   tsdd_cuda_stats stats{};
 
@@ -323,6 +380,40 @@ uint64_t dict_size_of(size_t word_len, size_t alphabet) {
 }
 
 // ------------------------------------------------------------------ preparation
+// All-gather of the per-rank slices of mean / 1/sigma / hash0 (slice s of every array belongs
+// to rank s; arrays hold world x slice entries).
+void gather_slices(tsdd_cuda_ctx* ctx, uint32_t slice) {
+  cudaStream_t st = ctx->stream;
+  const size_t at = static_cast<size_t>(slice) * ctx->rank;
+  if (ctx->comm) {  // in place: send buffer = receive buffer + rank x count
+    g_nccl.check(g_nccl.AllGather(ctx->mean.ptr + at, ctx->mean.ptr, slice * sizeof(double), NcclApi::kUint8, ctx->comm, st),
+                 "ncclAllGather(mean)");
+    g_nccl.check(g_nccl.AllGather(ctx->inv_sigma.ptr + at, ctx->inv_sigma.ptr, slice * sizeof(double), NcclApi::kUint8,
+                                  ctx->comm, st),
+                 "ncclAllGather(inv_sigma)");
+    g_nccl.check(g_nccl.AllGather(ctx->hash0.ptr + at, ctx->hash0.ptr, slice * sizeof(uint32_t), NcclApi::kUint8,
+                                  ctx->comm, st),
+                 "ncclAllGather(hash)");
+    return;
+  }
+  PeerGroup& g = *ctx->group;
+  sync_stream(ctx);  // this rank's slice is complete ...
+  if (!g.reduce_max(ctx->rank, nullptr, 0)) fail(TSDD_ERR_RUNTIME, "another rank of the group failed");  // ... so is everyone's
+  for (int r = 0; r < g.world; ++r) {
+    if (r == ctx->rank) continue;
+    const tsdd_cuda_ctx* other = g.members[static_cast<size_t>(r)];
+    if (!other || other->shard_rows != slice || other->rows != ctx->rows)
+      fail(TSDD_ERR_RUNTIME, "the ranks of a group must prepare the same series with the same parameters");
+    const size_t from = static_cast<size_t>(slice) * r;
+    CUDA_OK(cudaMemcpyPeerAsync(ctx->mean.ptr + from, ctx->device, other->mean.ptr + from, other->device,
+                                slice * sizeof(double), st));
+    CUDA_OK(cudaMemcpyPeerAsync(ctx->inv_sigma.ptr + from, ctx->device, other->inv_sigma.ptr + from, other->device,
+                                slice * sizeof(double), st));
+    CUDA_OK(cudaMemcpyPeerAsync(ctx->hash0.ptr + from, ctx->device, other->hash0.ptr + from, other->device,
+                                slice * sizeof(uint32_t), st));
+  }
+}
+
 // The SAX-word bucket / frequency / rarity index of the hashes in ctx->hash0 (index.cpp:12-109):
 // stable radix sort of (hash, row) -> runs are the buckets; run-length histogram -> frequencies;
 // stable sort of (frequency, row) -> rarity order.  Returns the kernels launched.
@@ -400,14 +491,30 @@ void prepare_on_device(tsdd_cuda_ctx* ctx, size_t m, size_t n, size_t word_len, 
                                  std::to_string((free_bytes + held) >> 20) + " MiB are free on device " +
                                  std::to_string(ctx->device));
   }
-  ctx->mean.alloc(rows);
-  ctx->inv_sigma.alloc(rows);
-  ctx->hash0.alloc(rows);
+  // Window statistics and hashes: replicated on one rank; with several ranks that can move device
+  // memory between them (NCCL communicator or in-process group) each rank encodes ONE slice of
+  // the rows and the slices are all-gathered — 20 bytes a row instead of the float64 arithmetic
+  // of every window on every rank (the matrix itself stays replicated: every rank scans all rows).
+  const uint32_t world = static_cast<uint32_t>(ctx->world);
+  const bool shard = ctx->opt_shard_prep && world > 1 && (ctx->comm || ctx->group);
+  const uint32_t slice = shard ? round_up_u32((rows + world - 1) / world, 1024) : rows;
+  ctx->shard_rows = shard ? slice : 0;
+  const size_t padded_rows = shard ? static_cast<size_t>(slice) * world : rows;
+  ctx->mean.alloc(padded_rows);
+  ctx->inv_sigma.alloc(padded_rows);
+  ctx->hash0.alloc(padded_rows);
   ctx->matrix.alloc(matrix_floats);
   CUDA_OK(cudaEventRecord(ctx->ev_prep[0], st));
-  launches += launch_window_encode(ctx->series.ptr, rows, static_cast<uint32_t>(n),
-                                   static_cast<uint32_t>(word_len), static_cast<uint32_t>(alphabet),
-                                   ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->hash0.ptr, nullptr, nullptr, st);
+  {
+    const uint32_t row0 = shard ? std::min<uint64_t>(static_cast<uint64_t>(slice) * ctx->rank, rows) : 0;
+    const uint32_t count = shard ? std::min(slice, rows - row0) : rows;
+    if (count > 0)
+      launches += launch_window_encode(ctx->series.ptr + row0, count, static_cast<uint32_t>(n),
+                                       static_cast<uint32_t>(word_len), static_cast<uint32_t>(alphabet),
+                                       ctx->mean.ptr + row0, ctx->inv_sigma.ptr + row0, ctx->hash0.ptr + row0, nullptr,
+                                       nullptr, st);
+  }
+  if (shard) gather_slices(ctx, slice);
 
   CUDA_OK(cudaEventRecord(ctx->ev_prep[1], st));
   if (ctx->rows_padded > rows)
@@ -456,6 +563,9 @@ void finish_prepare(tsdd_cuda_ctx* ctx) {
   ctx->stats.buckets = scalars[0];
   ctx->stats.min_freq_candidates = scalars[1];
   ctx->prepared = true;
+  // (a rank of a group must not start another prepare while a peer still copies from its slices)
+  if (ctx->group && ctx->shard_rows && !ctx->group->reduce_max(ctx->rank, nullptr, 0))
+    fail(TSDD_ERR_RUNTIME, "another rank of the group failed");
 }
 
 void reset_stats(tsdd_cuda_ctx* ctx) {
@@ -502,7 +612,7 @@ void prepare_host(tsdd_cuda_ctx* ctx, const T* series, size_t m, size_t n, size_
 // ------------------------------------------------------------------ exchange
 // In place, element-wise max of `count` (<= 4) keys over all ranks.
 void exchange_keys(tsdd_cuda_ctx* ctx, uint64_t* keys, size_t count) {
-  if (ctx->world <= 1 && !ctx->comm) return;
+  if (!ctx->several()) return;
   if (ctx->comm) {
     CUDA_OK(cudaMemcpyAsync(ctx->xchg.ptr, keys, count * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
     g_nccl.check(g_nccl.AllReduce(ctx->xchg.ptr, ctx->xchg.ptr, count, NcclApi::kUint64, NcclApi::kMax,
@@ -510,6 +620,10 @@ void exchange_keys(tsdd_cuda_ctx* ctx, uint64_t* keys, size_t count) {
                  "ncclAllReduce");
     CUDA_OK(cudaMemcpyAsync(keys, ctx->xchg.ptr, count * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
     sync_stream(ctx);
+    return;
+  }
+  if (ctx->group) {
+    if (!ctx->group->reduce_max(ctx->rank, keys, count)) fail(TSDD_ERR_RUNTIME, "another rank of the group failed");
     return;
   }
   if (!ctx->exchange_fn) fail(TSDD_ERR_RUNTIME, "world > 1 but no exchange is configured");
@@ -523,11 +637,38 @@ void exchange_keys(tsdd_cuda_ctx* ctx, uint64_t* keys, size_t count) {
 // pruning of the sharded search at the level of the single-GPU one.  One
 // ncclAllReduce(ncclMin, ncclUint64, N) over NVLink per batch: 8 MB at N = 1 M.
 void exchange_bounds(tsdd_cuda_ctx* ctx) {
-  if (!ctx->opt_share_bounds || (ctx->world <= 1 && !ctx->comm)) return;
+  if (!ctx->opt_share_bounds || !ctx->several()) return;
   if (ctx->comm) {
     g_nccl.check(g_nccl.AllReduce(ctx->nn.ptr, ctx->nn.ptr, ctx->rows, NcclApi::kUint64, NcclApi::kMin, ctx->comm,
                                   ctx->stream),
                  "ncclAllReduce(min)");
+    return;
+  }
+  if (ctx->group) {
+    // Device-side min over the peers' arrays.  Every rank first finishes its own batch, then all
+    // meet; from then on a peer's nn only ever DEcreases (its next batch's atomicMin), so whatever
+    // a read races with is still a valid upper bound.  Each rank's reads complete before it
+    // reaches the next barrier (it synchronises its stream there), so nothing is reset under them.
+    PeerGroup& g = *ctx->group;
+    sync_stream(ctx);
+    if (!g.reduce_max(ctx->rank, nullptr, 0)) fail(TSDD_ERR_RUNTIME, "another rank of the group failed");
+    PeerPointers peers{};
+    for (int r = 0; r < g.world; ++r) {
+      if (r == ctx->rank) continue;
+      const tsdd_cuda_ctx* other = g.members[static_cast<size_t>(r)];
+      if (!other || other->rows != ctx->rows) fail(TSDD_ERR_RUNTIME, "the ranks of a group must prepare the same series");
+      if (g.peer_access || other->device == ctx->device) {
+        peers.ptr[peers.count++] = other->nn.ptr;
+      } else {  // no P2P mapping between the two devices: stage the peer's bounds, then fold them in
+        ctx->peer_stage.alloc(ctx->rows);
+        CUDA_OK(cudaMemcpyPeerAsync(ctx->peer_stage.ptr, ctx->device, other->nn.ptr, other->device,
+                                    static_cast<size_t>(ctx->rows) * sizeof(uint64_t), ctx->stream));
+        PeerPointers one{};
+        one.ptr[one.count++] = ctx->peer_stage.ptr;
+        ctx->stats.kernel_launches += launch_min_from_peers(ctx->nn.ptr, one, ctx->rows, ctx->stream);
+      }
+    }
+    if (peers.count) ctx->stats.kernel_launches += launch_min_from_peers(ctx->nn.ptr, peers, ctx->rows, ctx->stream);
     return;
   }
   // host hook: it only knows max; keys stay below 2^63, so max of (2^63 - 1 - key) is min of key
@@ -756,7 +897,7 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
           // Dot form or not, for this batch.  One rank decides from its own counters; several
           // agree on `wanted` / `used` in the per-batch exchange below (the band must widen
           // on every rank before dot-form bounds travel between them).
-          const bool alone = !(ctx->world > 1 || ctx->comm);
+          const bool alone = !ctx->several();
           CUDA_OK(cudaMemcpyAsync(ctx->h_keys + 3, ctx->best.ptr, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
           if (alone && !ctx->dot_wanted && ctx->stats.batches >= 1) ctx->dot_wanted = few_abandoned(ctx);
           sync_stream(ctx);
@@ -789,7 +930,7 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
       }
       batch_now = static_cast<uint32_t>(std::min<uint64_t>(static_cast<uint64_t>(batch_now) * ctx->opt_batch_growth, ctx->opt_batch));
     }
-    if (ctx->world > 1 || ctx->comm) {  // a 1-rank communicator still runs the exchange
+    if (ctx->several()) {  // a 1-rank communicator still runs the exchange
       CUDA_OK(cudaMemcpyAsync(ctx->h_keys, ctx->best.ptr, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
       sync_stream(ctx);
       ctx->h_keys[1] = cursor < ctx->rows ? 1 : 0;
@@ -822,6 +963,7 @@ void collect_search_stats(tsdd_cuda_ctx* ctx) {
   ctx->stats.tile_live_candidates = c.tile_live;
   ctx->stats.lb_skipped = c.lb_skipped;
   ctx->stats.scan_kernel_dot_terms = c.dot_terms;
+  ctx->stats.useful_terms = c.useful_terms;
   double total = 0.0;
   for (size_t e = 0; e + 1 < ctx->events_used; e += 2) {
     float ms = 0.f;
@@ -867,7 +1009,7 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   if (pruning) {  // (after the seed: a row whose first mates already put it below the seed stops there)
     // Ranks that share their bounds split this stage too (slot p belongs to rank p mod world)
     // and merge the results with the same min-exchange that follows every batch.
-    const bool split = (ctx->world > 1 || ctx->comm) && ctx->opt_share_bounds && ctx->opt_mates > 0;
+    const bool split = ctx->several() && ctx->opt_share_bounds && ctx->opt_mates > 0;
     ctx->stats.kernel_launches += launch_bucket_mates(
         s, ctx->series.ptr, ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->sorted_row, ctx->slot_bucket.ptr, ctx->offsets.ptr,
         ctx->opt_mates, split ? static_cast<uint32_t>(ctx->world) : 1u, split ? static_cast<uint32_t>(ctx->rank) : 0u, st);
@@ -969,7 +1111,7 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
           best_row = cand;
         }
       }
-      if (ctx->world > 1 || ctx->comm) {
+      if (ctx->several()) {
         // the finalists are spread over the ranks: greatest float64 distance, then smallest row
         uint64_t value_bits = 0;
         if (best_row != 0xFFFFFFFFu) std::memcpy(&value_bits, &best64, sizeof(value_bits));
@@ -1008,12 +1150,24 @@ int guarded(tsdd_cuda_ctx* ctx, Fn&& fn) {
   } catch (const Failure& f) {
     if (ctx) ctx->error = f.message;
     else g_create_error = f.message;
+    if (ctx && ctx->group) ctx->group->abort();  // release the ranks waiting for this one
     return f.code;
   } catch (const std::exception& e) {
     if (ctx) ctx->error = e.what();
     else g_create_error = e.what();
+    if (ctx && ctx->group) ctx->group->abort();
     return TSDD_ERR_RUNTIME;
   }
+}
+
+void leave_group(tsdd_cuda_ctx* ctx) {
+  if (!ctx->group) return;
+  {
+    std::lock_guard<std::mutex> lock(ctx->group->mu);
+    for (auto& member : ctx->group->members)
+      if (member == ctx) member = nullptr;
+  }
+  ctx->group.reset();
 }
 
 template <typename Src, typename Dst>
@@ -1075,6 +1229,7 @@ void tsdd_cuda_destroy(tsdd_cuda_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  leave_group(ctx);
   if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
   for (cudaEvent_t e : ctx->event_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->ev_prep)
@@ -1183,6 +1338,8 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
     } else if (key == "dot_form") {
       if (value != 0 && value != 1 && value != 2) fail(TSDD_ERR_PARAMETER, "dot_form must be 0, 1 or 2");
       ctx->opt_dot = static_cast<int>(value);
+    } else if (key == "shard_prep") {
+      ctx->opt_shard_prep = value != 0;
     } else if (key == "share_bounds") {
       ctx->opt_share_bounds = value != 0;
     } else if (key == "time_kernels") {
@@ -1421,9 +1578,64 @@ int tsdd_cuda_comm_init(tsdd_cuda_ctx* ctx, const char id[128], int world, int r
     NcclApi::UniqueId uid;
     std::memcpy(uid.internal, id, 128);
     g_nccl.check(g_nccl.CommInitRank(&ctx->comm, world, uid, rank), "ncclCommInitRank");
+    leave_group(ctx);
     ctx->world = world;
     ctx->rank = rank;
     ctx->exchange_fn = nullptr;
+  });
+}
+
+int tsdd_cuda_comm_size(const tsdd_cuda_ctx* ctx, int* nranks) {
+  if (!ctx || !nranks) return TSDD_ERR_PARAMETER;
+  *nranks = ctx->world;
+  if (ctx->comm) {  // what NCCL itself says about the communicator
+    int count = 0;
+    if (g_nccl.CommCount(ctx->comm, &count) != 0) return TSDD_ERR_RUNTIME;
+    *nranks = count;
+  }
+  return TSDD_OK;
+}
+
+int tsdd_cuda_group_create(tsdd_cuda_ctx** ctxs, int world) {
+  if (!ctxs || world < 1 || world > kMaxPeers + 1) return TSDD_ERR_PARAMETER;
+  for (int r = 0; r < world; ++r)
+    if (!ctxs[r]) return TSDD_ERR_PARAMETER;
+  return guarded(ctxs[0], [&] {
+    auto group = std::make_shared<PeerGroup>(world);
+    for (int r = 0; r < world; ++r) {
+      for (int q = 0; q < r; ++q)
+        if (ctxs[q] == ctxs[r]) fail(TSDD_ERR_PARAMETER, "a context can be only one rank of a group");
+      group->members[static_cast<size_t>(r)] = ctxs[r];
+    }
+    // map every other device's memory where the hardware can (NVLink / NVSwitch, or PCIe P2P)
+    for (int r = 0; r < world; ++r) {
+      for (int q = 0; q < world; ++q) {
+        const int a = ctxs[r]->device, b = ctxs[q]->device;
+        if (a == b) continue;
+        int can = 0;
+        CUDA_OK(cudaDeviceCanAccessPeer(&can, a, b));
+        if (!can) {
+          group->peer_access = false;
+          continue;
+        }
+        CUDA_OK(cudaSetDevice(a));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) cuda_check(e, "cudaDeviceEnablePeerAccess");
+        (void)cudaGetLastError();
+      }
+    }
+    for (int r = 0; r < world; ++r) {
+      tsdd_cuda_ctx* ctx = ctxs[r];
+      leave_group(ctx);
+      if (ctx->comm) {
+        g_nccl.CommDestroy(ctx->comm);
+        ctx->comm = nullptr;
+      }
+      ctx->exchange_fn = nullptr;
+      ctx->world = world;
+      ctx->rank = r;
+      ctx->group = world > 1 ? group : nullptr;
+    }
   });
 }
 
@@ -1436,6 +1648,7 @@ int tsdd_cuda_set_exchange(tsdd_cuda_ctx* ctx, tsdd_exchange_fn fn, void* user, 
       g_nccl.CommDestroy(ctx->comm);
       ctx->comm = nullptr;
     }
+    leave_group(ctx);
     ctx->exchange_fn = fn;
     ctx->exchange_user = user;
     ctx->world = world;

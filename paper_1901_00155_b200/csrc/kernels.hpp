@@ -96,6 +96,15 @@ struct SearchState {
 
 int launch_reset_search(SearchState s, cudaStream_t stream);
 
+// nn[i] = min(nn[i], peer[0][i], peer[1][i], ...): the per-batch min-reduction of the bounds
+// between the ranks of one process, read straight from the peers' device memory (NVLink P2P).
+constexpr int kMaxPeers = 15;
+struct PeerPointers {
+  const uint64_t* ptr[kMaxPeers];
+  int count;
+};
+int launch_min_from_peers(uint64_t* d_nn, PeerPointers peers, uint32_t rows, cudaStream_t stream);
+
 // Same-word neighbours first (the HOTSAX inner heuristic, discovery.cpp:51-63):
 // every row is measured against up to `mates` rows of its own bucket.
 int launch_bucket_mates(SearchState s, const double* d_series, const double* d_mean, const double* d_inv_sigma,

@@ -45,7 +45,10 @@ k_fp32_probe(float* sink, int iters) {
             acc[c] = fmaf(d, d, acc[c]);
           }
         }
-        b += 1e-7f;
+        // the sub+fma mix needs a moving operand (a loop-invariant a - b would be hoisted); that
+        // one FADD per kProbeChains pairs is COUNTED (fp32_probe_ops).  The FFMA-only stream is
+        // a chain of dependent, non-associative operations as it stands and carries nothing else.
+        if constexpr (kWhich == 1) b += 1e-7f;
       }
     }
     float total = 0.f;
@@ -72,7 +75,7 @@ k_fp32_probe(float* sink, int iters) {
             acc[c] = __ffma2_rn(d, d, acc[c]);
           }
         }
-        b.x += 1e-7f;
+        if constexpr (kWhich == 3) b.x += 1e-7f;  // (counted, see above)
       }
     }
     float total = 0.f;
@@ -149,12 +152,14 @@ double fp32_probe_ops(int which, int blocks, int iters) {
   if (which >= 16) {
     const int packed = which == 16 ? 8 : which == 17 ? 12 : which == 18 ? 12 : 14;
     const int scalar = which == 16 ? 8 : which == 17 ? 6 : which == 18 ? 4 : 2;
-    return lanes * static_cast<double>(iters) * kProbeUnroll * (packed * 4.0 + scalar * 2.0);
+    return lanes * static_cast<double>(iters) * kProbeUnroll * (packed * 4.0 + scalar * 2.0 + 1.0);  // + the moving operand's FADD
   }
   const double per_lane = static_cast<double>(iters) * kProbeUnroll * kProbeChains;
   const double instr = (which == 0 || which == 2) ? 1.0 : 2.0;  // instructions per chain step
   const double width = (which >= 2) ? 2.0 : 1.0;                 // lanes per instruction
-  return lanes * per_lane * instr * width;
+  // the mixes move one operand with ONE scalar FADD per unroll step; it runs on the same pipe and is counted
+  const double moving = (which == 1 || which == 3) ? static_cast<double>(iters) * kProbeUnroll : 0.0;
+  return lanes * (per_lane * instr * width + moving);
 }
 
 }  // namespace tsdd_b200

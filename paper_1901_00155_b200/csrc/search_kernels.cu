@@ -47,7 +47,29 @@ __global__ void k_reset_search(SearchState s) {
   }
   if (i == 0) {
     *s.best = 0;
-    *s.counters = DeviceCounters{0, 0, 0, 0, 0, 0, 0, 0};
+    *s.counters = DeviceCounters{0, 0, 0, 0, 0, 0, 0, 0, 0};
+  }
+}
+
+// Two keys per thread (one 16-byte access per array): each array is streamed once, coalesced.
+__global__ void __launch_bounds__(256)
+k_min_from_peers(uint64_t* __restrict__ nn, PeerPointers peers, uint32_t rows) {
+  const uint32_t i = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+  if (i + 1 < rows) {
+    ulonglong2 mine = *reinterpret_cast<const ulonglong2*>(nn + i);
+    for (int p = 0; p < peers.count; ++p) {
+      const ulonglong2 other = __ldcg(reinterpret_cast<const ulonglong2*>(peers.ptr[p] + i));
+      mine.x = other.x < mine.x ? other.x : mine.x;
+      mine.y = other.y < mine.y ? other.y : mine.y;
+    }
+    *reinterpret_cast<ulonglong2*>(nn + i) = mine;
+  } else if (i < rows) {
+    uint64_t mine = nn[i];
+    for (int p = 0; p < peers.count; ++p) {
+      const uint64_t other = load_key(peers.ptr[p] + i);
+      mine = other < mine ? other : mine;
+    }
+    nn[i] = mine;
   }
 }
 
@@ -625,7 +647,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
   uint32_t* s_jrow = reinterpret_cast<uint32_t*>(s_nub + kTileRows);      // neighbour rows, ~0 = none
   uint32_t* s_brow = s_jrow + kTileRows;                                  // rows to load (none -> zero row)
   float* s_loc = reinterpret_cast<float*>(s_brow + kTileRows);            // bounds this CTA found itself
-  __shared__ unsigned long long s_calls, s_abandoned, s_terms, s_tiles, s_tile_live, s_lb_skipped;
+  __shared__ unsigned long long s_calls, s_abandoned, s_terms, s_tiles, s_tile_live, s_lb_skipped, s_useful;
 
   const uint32_t count = a.sel[0];
   const uint32_t cand0 = blockIdx.y * kCand;
@@ -641,6 +663,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
     s_tiles = 0;
     s_tile_live = 0;
     s_lb_skipped = 0;
+    s_useful = 0;
   }
   const bool window = a.nbr_index != nullptr;
   const uint32_t slot_tiles = (s.n_rows + kTileRows - 1) / kTileRows;
@@ -862,8 +885,21 @@ k_scan_tiles(SearchState s, ScanArgs a) {
     }
     cp_async_wait<0>();
 
-    // ---- accounting (per warp: the terms its lanes really accumulated)
-    if (lane == 0) atomicAdd(&s_terms, static_cast<unsigned long long>(warp_chunks) * kChunk * 32 * kU * kW);
+    // ---- accounting (per warp: the terms its lanes really accumulated, and how many of them
+    // belonged to a live candidate, an existing neighbour row and a real column)
+    {
+      uint32_t taking_part = 0;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) taking_part += thr[u] >= 0.f ? 1u : 0u;
+      // a warp holds 32 / kTx thread rows; lane 0 of each carries that row's count
+      uint32_t warp_live = __shfl_sync(0xFFFFFFFFu, taking_part, 0);
+      if (kTx < 32) warp_live += __shfl_sync(0xFFFFFFFFu, taking_part, kTx % 32);
+      if (lane == 0 && warp_chunks) {
+        const uint32_t rows_here = slot0 < s.n_rows ? min(static_cast<uint32_t>(kNbr), s.n_rows - slot0) : 0u;
+        atomicAdd(&s_terms, static_cast<unsigned long long>(warp_chunks) * kChunk * 32 * kU * kW);
+        atomicAdd(&s_useful, static_cast<unsigned long long>(min(warp_chunks * kChunk, s.n)) * warp_live * rows_here);
+      }
+    }
     if (my_calls) {
       atomicAdd(&s_calls, my_calls);
       if (cta_abandoned) atomicAdd(&s_abandoned, my_calls);
@@ -929,6 +965,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
     if (s_terms) {
       atomicAdd(&s.counters->terms, s_terms);
       atomicAdd(&s.counters->tile_terms, s_terms);
+      atomicAdd(&s.counters->useful_terms, s_useful);
     }
     if (s_tiles) {
       atomicAdd(&s.counters->tiles, s_tiles);
@@ -983,7 +1020,7 @@ struct alignas(16) TileMeta {  // (jrow is read as uint4)
   float nnorm[kNbrWs];       // dot form: squared norms of the neighbour rows
   unsigned long long calls;  // pair distances this tile starts
   uint32_t done;             // consumer warps that have abandoned the tile
-  uint32_t pad;
+  uint32_t valid;            // neighbour slots of the tile that hold a row (the first `valid` of them)
 };
 
 // Tensor-map variant: a stage is four TMA boxes of 128 rows x 32 columns (128 bytes a row,
@@ -1241,6 +1278,7 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
           if (lane == 0) {
             meta.calls = all_calls;
             meta.done = 0;
+            meta.valid = valid;
             mbar_arrive(&sh.meta_full[m]);
           }
           // ---- stream the tile's chunks; stop as soon as every consumer warp has abandoned it
@@ -1396,6 +1434,7 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
       if (lane == 0) {
         meta.calls = calls;
         meta.done = 0;
+        meta.valid = valid;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.meta_full[m]);
@@ -1489,8 +1528,8 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
   float thr[kU];
   uint32_t seq = 0, cur = kTagDone, m = 0, chunks_done = 0;
   bool released = true, warp_done = false;
-  unsigned long long chunks_total = 0, abandoned_total = 0;
-  uint32_t overlap_total = 0;
+  unsigned long long chunks_total = 0, abandoned_total = 0, useful_total = 0;
+  uint32_t overlap_total = 0, pairs_w = 0;
 #pragma unroll 1
   for (;;) {
     const uint32_t st = seq % kStagesWs, round = seq / kStagesWs;
@@ -1515,6 +1554,20 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
       warp_done = __all_sync(0xFFFFFFFFu, none);  // none of this warp's candidates takes part in the tile
       if (warp_done && lane == 0 && chunks > 1) {
         if (atomicAdd(&sh.meta[m].done, 1u) == kConsumerWarps - 1) abandoned_total += sh.meta[m].calls;
+      }
+      {  // (live candidates) x (existing neighbour rows) among this warp's pairs: the useful share of its terms
+        uint32_t cc = 0, cn = 0;
+        const uint32_t valid = sh.meta[m].valid;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) cc += thr[u] >= 0.f ? 1u : 0u;
+#pragma unroll
+        for (int w = 0; w < kW; ++w) cn += tx + kTx * w < valid ? 1u : 0u;
+        uint32_t live_w = 0;
+#pragma unroll
+        for (int g = 0; g < 32; g += kTxLanes) live_w += __shfl_sync(0xFFFFFFFFu, cc, g);
+#pragma unroll
+        for (int d = kTxLanes / 2; d > 0; d >>= 1) cn += __shfl_xor_sync(0xFFFFFFFFu, cn, d);
+        pairs_w = live_w * cn;
       }
       released = false;
       chunks_done = 0;
@@ -1548,6 +1601,7 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
       }
       ++chunks_done;
       ++chunks_total;
+      useful_total += static_cast<unsigned long long>(pairs_w) * min(static_cast<uint32_t>(kChunk), s.n - min(s.n, c * kChunk));
       if constexpr (!kDot) {
         bool all_over = true;
 #pragma unroll
@@ -1656,6 +1710,7 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
     if (terms) {
       atomicAdd(&s.counters->terms, terms);
       atomicAdd(&s.counters->tile_terms, terms);
+      atomicAdd(&s.counters->useful_terms, useful_total);
       if constexpr (kDot) atomicAdd(&s.counters->dot_terms, terms);
     }
     if (abandoned_total) atomicAdd(&s.counters->abandoned, abandoned_total);
@@ -1708,7 +1763,7 @@ struct alignas(16) TileMeta16 {
   float nnorm[kNbrWs];
   unsigned long long calls;
   uint32_t done;
-  uint32_t pad;
+  uint32_t valid;  // neighbour slots of the tile that hold a row
 };
 
 struct Shared16 {
@@ -1830,6 +1885,7 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
       if (lane == 0) {
         meta.calls = calls;
         meta.done = 0;
+        meta.valid = valid;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&sh.meta_full[m]);
@@ -1887,8 +1943,8 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
   float2 acc[kP][kW];
   uint32_t seq = 0, cur = kTagDone, m = 0, chunks_done = 0;
   bool released = true, warp_done = false;
-  unsigned long long chunks_total = 0;
-  uint32_t overlap_total = 0;
+  unsigned long long chunks_total = 0, useful_total = 0;
+  uint32_t overlap_total = 0, pairs_w = 0;
 #pragma unroll 1
   for (;;) {
     const uint32_t st = seq % kStages16, round = seq / kStages16;
@@ -1904,11 +1960,22 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
       cur = tile;
       m = tile & 1;
       mbar_wait(&sh.meta_full[m], (tile >> 1) & 1);
-      bool none = true;
+      uint32_t cc = 0, cn = 0;
 #pragma unroll
-      for (int q = 0; q < 2 * kP; ++q) none = none && sh.meta[m].thr[cand_of_thread + q] < 0.f;
-      warp_done = __all_sync(0xFFFFFFFFu, none);
+      for (int q = 0; q < 2 * kP; ++q) cc += sh.meta[m].thr[cand_of_thread + q] >= 0.f ? 1u : 0u;
+      warp_done = __all_sync(0xFFFFFFFFu, cc == 0);
       if (warp_done && lane == 0 && chunks > 1) atomicAdd(&sh.meta[m].done, 1u);
+      {  // (live candidates) x (existing neighbour rows) among this warp's pairs: the useful share of its terms
+        const uint32_t valid = sh.meta[m].valid;
+#pragma unroll
+        for (int w = 0; w < kW; ++w) cn += tx + kTx * w < valid ? 1u : 0u;
+        uint32_t live_w = 0;
+#pragma unroll
+        for (int g = 0; g < 32; g += kTxLanes) live_w += __shfl_sync(0xFFFFFFFFu, cc, g);
+#pragma unroll
+        for (int d = kTxLanes / 2; d > 0; d >>= 1) cn += __shfl_xor_sync(0xFFFFFFFFu, cn, d);
+        pairs_w = live_w * cn;
+      }
 #pragma unroll
       for (int i = 0; i < kP; ++i)
 #pragma unroll
@@ -1952,6 +2019,7 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
       }
       ++chunks_done;
       ++chunks_total;
+      useful_total += static_cast<unsigned long long>(pairs_w) * min(static_cast<uint32_t>(kCols16), s.n - min(s.n, c * kCols16));
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sh.empty[st]);
@@ -2046,6 +2114,7 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
       atomicAdd(&s.counters->terms, terms);
       atomicAdd(&s.counters->tile_terms, terms);
       atomicAdd(&s.counters->dot_terms, terms);
+      atomicAdd(&s.counters->useful_terms, useful_total);
     }
   }
 #pragma unroll
@@ -2152,6 +2221,12 @@ inline uint32_t slot_tiles_of(uint32_t rows) { return (rows + kTileRows - 1) / k
 // ------------------------------------------------------------------ launchers
 int launch_reset_search(SearchState s, cudaStream_t stream) {
   k_reset_search<<<blocks_for(s.n_rows, 256), 256, 0, stream>>>(s);
+  return 1;
+}
+
+int launch_min_from_peers(uint64_t* d_nn, PeerPointers peers, uint32_t rows, cudaStream_t stream) {
+  if (peers.count == 0 || rows == 0) return 0;
+  k_min_from_peers<<<blocks_for((static_cast<size_t>(rows) + 1) / 2, 256), 256, 0, stream>>>(d_nn, peers, rows);
   return 1;
 }
 

@@ -93,6 +93,8 @@ SYMBOLS = {
     "tsdd_cuda_fetch": (_int, [_vp, _int, _vp, _sz]),
     "tsdd_cuda_comm_unique_id": (_int, [ctypes.c_char_p]),
     "tsdd_cuda_comm_init": (_int, [_vp, ctypes.c_char_p, _int, _int]),
+    "tsdd_cuda_comm_size": (_int, [_vp, ctypes.POINTER(_int)]),
+    "tsdd_cuda_group_create": (_int, [ctypes.POINTER(_vp), _int]),
     "tsdd_cuda_set_exchange": (_int, [_vp, EXCHANGE_FN, _vp, _int, _int]),
     "tsdd_cuda_fp32_probe": (_int, [_vp, _int, ctypes.POINTER(_dbl), ctypes.POINTER(_dbl)]),
     "tsdd_cuda_nn_profile": (_int, [_vp, _vp]),
@@ -322,6 +324,20 @@ class Context:
 
     def comm_init(self, unique_id: bytes, world: int, rank: int):
         self._check(self._lib.tsdd_cuda_comm_init(self._h, unique_id, world, rank))
+
+    def comm_size(self) -> int:
+        n = ctypes.c_int()
+        self._check(self._lib.tsdd_cuda_comm_size(self._h, ctypes.byref(n)))
+        return n.value
+
+
+def group_create(contexts) -> None:
+    """Links contexts of this process into ranks 0 .. len-1 that exchange over device memory
+    (tsdd_cuda_group_create); each must then be driven by its own host thread."""
+    handles = (ctypes.c_void_p * len(contexts))(*[c._h.value for c in contexts])
+    rc = load_library().tsdd_cuda_group_create(handles, len(contexts))
+    if rc != OK:
+        _raise(rc, load_library().tsdd_cuda_last_error(contexts[0]._h).decode())
 
 
 def comm_unique_id() -> bytes:

@@ -6,6 +6,8 @@ preparation stage (symbols, hashes, frequencies, candidate set, buckets) identic
 The oracle is the unmodified reference when oracle/_ref is present, else the pinned C
 restatement (tests/test_oracle_pin.py).
 """
+import json
+import os
 import threading
 
 import numpy as np
@@ -16,6 +18,7 @@ from paper_1901_00155_b200 import (Context, DiscoveryConfig, InfeasibleInputErro
                                    workloads as W)
 
 pytestmark = pytest.mark.gpu
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 DIST_RTOL = 1e-4  # north_star: "discord distances must agree to 1e-4 relative"
 
@@ -373,6 +376,211 @@ def test_sharing_bounds_between_ranks_saves_work():
         scanned[share] = (out[0][0], out[0][1] + out[1][1], out[0][2] + out[1][2])
     assert scanned[0][0] == scanned[1][0]              # same discord either way
     assert scanned[1][2] <= scanned[0][2]              # and fewer pair distances with sharing
+
+
+def _run_group(world, x, n, w, a, k, options=(), devices=None):
+    """`world` contexts of this process as the ranks of one group (tsdd_cuda_group_create), one
+    host thread each; returns per rank (positions, distances, stats)."""
+    from paper_1901_00155_b200.engine import group_create
+
+    ctxs = [Context((devices or [0] * world)[r]) for r in range(world)]
+    out, errors = [None] * world, []
+    try:
+        for c in ctxs:
+            for name, value in options:
+                c.set_option(name, value)
+        group_create(ctxs)
+
+        def run(rank):
+            try:
+                c = ctxs[rank]
+                c.prepare(x, n, w, a)
+                pos, dist = c.search(k)
+                out[rank] = (pos, dist, c.stats(), c.fetch("hash"), c.fetch("mean"), c.fetch("inv_sigma"))
+            except Exception as e:  # noqa: BLE001
+                errors.append(e)
+
+        threads = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join(timeout=300)
+    finally:
+        for c in ctxs:
+            c.close()
+    assert not errors, errors
+    return out
+
+
+@pytest.mark.parametrize("shard", [1, 0])
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_group_of_ranks_in_one_process(chk, world, shard):
+    """The in-process multi-GPU mode: bounds min-reduced on the device from the peers' memory,
+    window statistics / hashes computed in per-rank slices and gathered (option shard_prep)."""
+    x = planted_walk(15, 16000, 64)
+    want = chk.topk(x, 64, 4, 4, 3)
+    ref = chk.prepare(x, 64, 4, 4, want_rows=False)
+    out = _run_group(world, x, 64, 4, 4, 3, options=[("batch", 512), ("shard_prep", shard)])
+    with Context(0) as single:
+        single.prepare(x, 64, 4, 4)
+        mean1, inv1 = single.fetch("mean"), single.fetch("inv_sigma")
+    for r in range(world):
+        pos, dist, st, hashes, mean, inv = out[r]
+        assert pos == want["positions"], (r, pos)
+        np.testing.assert_allclose(dist, want["distances"], rtol=DIST_RTOL)
+        np.testing.assert_array_equal(hashes, ref["hashes"])   # every rank holds every slice
+        np.testing.assert_array_equal(mean, mean1)             # bit-identical to the unsharded preparation
+        np.testing.assert_array_equal(inv, inv1)
+    assert sum(o[2]["scanned_candidates"] for o in out) > 0
+
+
+def test_group_shares_bounds_on_the_device():
+    """Two ranks of a group scan fewer pair distances together than with share_bounds off."""
+    x = W.series(1)[0][:40000]
+    calls = {}
+    for share in (0, 1):
+        out = _run_group(2, x, 128, 4, 4, 1, options=[("batch", 1024), ("share_bounds", share)])
+        assert out[0][0] == out[1][0]
+        calls[share] = (out[0][0], out[0][2]["calls"] + out[1][2]["calls"])
+    assert calls[0][0] == calls[1][0] and calls[1][1] <= calls[0][1], calls
+
+
+def test_group_failure_on_one_rank_releases_the_others():
+    from paper_1901_00155_b200 import ParameterError
+    from paper_1901_00155_b200.engine import CudaRuntimeError, group_create
+
+    x = planted_walk(4, 6000, 64)
+    ctxs = [Context(0), Context(0)]
+    seen = [None, None]
+    try:
+        group_create(ctxs)
+
+        def run(rank):
+            try:
+                ctxs[rank].prepare(x, 64, 4, 4)
+                if rank == 1:
+                    ctxs[rank].search(0)   # k = 0: ParameterError on this rank only
+                else:
+                    ctxs[rank].search(1)
+            except Exception as e:  # noqa: BLE001
+                seen[rank] = e
+
+        threads = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join(timeout=120)
+            assert not t.is_alive(), "a rank is stuck in the group's barrier"
+    finally:
+        for c in ctxs:
+            c.close()
+    assert isinstance(seen[1], ParameterError)
+    assert isinstance(seen[0], CudaRuntimeError) and "another rank" in str(seen[0])
+
+
+_NCCL_WORKER = r"""
+import json, os, sys
+import numpy as np
+import torch
+import torch.distributed as dist
+sys.path.insert(0, os.environ["TSDD_ROOT"])
+from paper_1901_00155_b200 import Context, parallel, workloads as W
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+torch.cuda.set_device(rank)
+dist.init_process_group("gloo")           # carries only the 128-byte NCCL id
+x = W.series(1)[0][:30000]
+with Context(rank) as c:
+    parallel.attach_nccl(c)               # the ENGINE's communicator: ncclCommInitRank in libtsdd_cuda.so
+    c.prepare(x, 128, 4, 4)
+    pos, dd = c.search(2)
+    st = c.stats()
+    print(json.dumps({"rank": rank, "nranks": c.comm_size(), "pos": pos, "dist": dd,
+                      "scanned": st["scanned_candidates"], "calls": st["calls"],
+                      "hash_sum": int(c.fetch("hash").sum())}), flush=True)
+dist.destroy_process_group()
+"""
+
+
+def test_engine_nccl_communicator_across_processes(chk, tmp_path):
+    """One process per GPU, the engine's own NCCL communicator: per-batch ncclAllReduce(max) of the
+    keys, ncclAllReduce(min) of the N bounds, ncclAllGather of the sharded window statistics.
+    Needs two GPUs (NCCL refuses two ranks on one device)."""
+    import subprocess
+    import sys
+
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs: NCCL does not allow two ranks on one device")
+    world = 2
+    script = tmp_path / "worker.py"
+    script.write_text(_NCCL_WORKER)
+    procs = []
+    for rank in range(world):
+        env = dict(os.environ, RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT="29631", TSDD_ROOT=_ROOT)
+        procs.append(subprocess.Popen([sys.executable, str(script)], env=env, stdout=subprocess.PIPE,
+                                      stderr=subprocess.PIPE, text=True))
+    outs = [p.communicate(timeout=600) for p in procs]
+    for p, (so, se) in zip(procs, outs):
+        assert p.returncode == 0, se[-2000:]
+    lines = [json.loads(so.strip().splitlines()[-1]) for so, _ in outs]
+    x = W.series(1)[0][:30000]
+    want = chk.topk(x, 128, 4, 4, 2)
+    for line in lines:
+        assert line["nranks"] == world and line["pos"] == want["positions"]
+        np.testing.assert_allclose(line["dist"], want["distances"], rtol=DIST_RTOL)
+    assert lines[0]["hash_sum"] == lines[1]["hash_sum"]
+    assert all(line["scanned"] > 0 for line in lines)
+
+
+_GLOO_WORKER = r"""
+import json, os, sys
+import numpy as np
+import torch
+import torch.distributed as dist
+sys.path.insert(0, os.environ["TSDD_ROOT"])
+from paper_1901_00155_b200 import Context, parallel, workloads as W
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+dist.init_process_group("gloo")
+x = W.series(1)[0][:30000]
+with Context(0) as c:                      # both processes on GPU 0; only the HOSTS meet (gloo all_reduce)
+    ex = parallel.attach_torch(c)
+    c.prepare(x, 128, 4, 4)
+    pos, dd = c.search(2)
+    st = c.stats()
+    print(json.dumps({"rank": rank, "pos": pos, "dist": dd, "scanned": st["scanned_candidates"],
+                      "exchanges": ex.calls}), flush=True)
+dist.destroy_process_group()
+"""
+
+
+def test_engine_in_two_processes_with_a_torch_distributed_exchange(chk, tmp_path):
+    """One process per rank, torch.distributed (gloo) as the exchange hook: the multi-process
+    path of parallel.attach_torch with the real engine.  Both ranks share GPU 0 — their kernels
+    never wait on one another, only the host processes meet in the all_reduce."""
+    import subprocess
+    import sys
+
+    world = 2
+    script = tmp_path / "worker.py"
+    script.write_text(_GLOO_WORKER)
+    procs = []
+    for rank in range(world):
+        env = dict(os.environ, RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT="29641", TSDD_ROOT=_ROOT)
+        procs.append(subprocess.Popen([sys.executable, str(script)], env=env, stdout=subprocess.PIPE,
+                                      stderr=subprocess.PIPE, text=True))
+    outs = [p.communicate(timeout=600) for p in procs]
+    for p, (so, se) in zip(procs, outs):
+        assert p.returncode == 0, se[-2000:]
+    lines = [json.loads(so.strip().splitlines()[-1]) for so, _ in outs]
+    x = W.series(1)[0][:30000]
+    want = chk.topk(x, 128, 4, 4, 2)
+    for line in lines:
+        assert line["pos"] == want["positions"] and line["exchanges"] > 0
+        np.testing.assert_allclose(line["dist"], want["distances"], rtol=DIST_RTOL)
+    assert sum(line["scanned"] for line in lines) > 0
 
 
 def test_nccl_exchange_with_one_rank(chk):
@@ -804,11 +1012,8 @@ def test_device_series_is_validated_on_the_device(ctx):
 
 
 # ------------------------------------------------------------------ the reference-shaped C++ boundary
-import json  # noqa: E402
-import os  # noqa: E402
 import subprocess  # noqa: E402
 
-_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 MIRROR_CHECK = os.path.join(_ROOT, "paper_1901_00155_b200", "_lib", "mirror_check")
 TSDD_PATCHED = os.path.join(_ROOT, "oracle", "_ref", "tsdd_patched")
 

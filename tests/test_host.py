@@ -374,6 +374,16 @@ def test_bench_reference_arm_prints_the_contract_line():
     assert line["config"]["workload"] == "cfg1" and line["vs_baseline"] is None
 
 
+def test_bench_starts_its_own_ranks_and_refuses_without_the_devices():
+    """`python bench.py --gpus N` with no launcher starts N ranks itself (spawn_ranks); on a
+    machine with fewer CUDA devices it says so instead of running one rank and printing n_gpus 1."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "64", "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, env=env, timeout=300)
+    assert p.returncode != 0 and "--gpus 64 needs 64 CUDA devices" in p.stderr, p.stderr
+    assert p.stdout.strip() == ""
+
+
 def test_bench_reference_arm_other_ranks_exit_quietly():
     env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
     p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload", "1",
