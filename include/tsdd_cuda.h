@@ -69,6 +69,7 @@ typedef struct tsdd_cuda_stats {
   uint64_t finalists;      /* rows settled in float64 at the end of the passes (near-ties of the float32 search) */
   uint64_t exact_reruns;   /* of those, measured again from +inf because the float32 start bound was too low */
   uint64_t useful_terms;   /* of scan_kernel_terms: terms of pairs that were live, non-self and not padding */
+  uint64_t propagated;     /* pair distances measured by the time-topology step (option "propagate") */
 } tsdd_cuda_stats;
 
 /* ---- lifetime ------------------------------------------------------------ */
@@ -94,7 +95,9 @@ int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream);
  * dropped between ranges), "window_rounds" / "window_first" / "window_growth"
  * (before that covering scan, each candidate tile visits its own SAX word's
  * neighbourhood in the hash-sorted order: window_first slots, growing), "bucket_mates" (same-word
- * neighbours tried per row before the scans), "rescore" (0/1: decide each pass
+ * neighbours tried per row before the scans), "propagate" (time topology: at the start of a batch
+ * and after its window rounds every live candidate c measures up to this many pairs (c, j - delta)
+ * suggested by rows c + delta, |delta| <= 16, that already know a neighbour j; 0 = off), "rescore" (0/1: decide each pass
  * among the near-tied finalists by their exact float64 nn distance),
  * "margin_delta" (relative safety band of the float32 discard test; negative = from n),
  * "margin_q" (its part proportional to sqrt(best-so-far), for the float32 quantisation of the

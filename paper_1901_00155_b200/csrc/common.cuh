@@ -83,6 +83,7 @@ struct DeviceCounters {
   // past the last row, and the zero padding of the row stride.  (Self-match pairs inside a tile,
   // at most (2n - 1) / N of all pairs, are not taken out.)
   unsigned long long useful_terms;
+  unsigned long long propagated;  // pair distances measured by the time-topology step (k_propagate)
 };
 
 }  // namespace tsdd_b200

@@ -17,6 +17,7 @@
 #include <memory>
 #include <mutex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -188,6 +189,8 @@ struct tsdd_cuda_ctx {
   double opt_window_growth = 3.0;
   bool opt_rotate = true;           // each batch starts its covering scan at a different row
   int opt_mates = 8;
+  int opt_propagate = 8;            // time-topology tries per candidate and call (0 = off)
+  int opt_propagate_every = 2;      // ... called again after every this-many-th compaction of a batch (0: only at its start)
   bool opt_rescore = true;
   double opt_margin_delta = -1.0;  // < 0: derive from n (see discard_margin)
   double opt_margin_q = -1.0;      // < 0: derive from n (see quantisation_margin)
@@ -249,6 +252,16 @@ struct tsdd_cuda_ctx {
   double* h_double = nullptr;     // pinned, 1 value
   std::vector<cudaEvent_t> event_pool;
   size_t events_used = 0;
+  // TSDD_TRACE=1: one line per tile-kernel launch on stderr after the search (development aid)
+  struct LaunchNote {
+    int pass;
+    uint64_t batch;
+    bool window;
+    uint32_t k_begin, k_end, count;
+    ScanChoice choice;
+  };
+  std::vector<LaunchNote> trace;
+  int cur_pass = 0;
 
   // ranks
   int world = 1, rank = 0;
@@ -801,12 +814,23 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
   // CTAs exit at once), so the host never waits for the segment the GPU is working on and
   // the GPU never waits for the host.
   const std::vector<Segment> plan = plan_segments(ctx, pruning);
+  // time topology: before anything else, and again once the window rounds are over
+  if (pruning) launches += launch_propagate(s, list, ctx->sel.ptr, count, ctx->opt_propagate, st);
   for (size_t r = 0; r < plan.size(); ++r) {
     if (r > 0 && pruning) {
       launches += launch_compact_batch(s, list, slots, list_alt, slots_alt, pruning, ctx->sel.ptr, count,
                                        ctx->flags.ptr, st);
       std::swap(list, list_alt);
       std::swap(slots, slots_alt);
+      // time topology again: the rows around a survivor keep learning (symmetric updates)
+      if (ctx->opt_propagate_every > 0 && (r % static_cast<size_t>(ctx->opt_propagate_every) == 0 ||
+                                           (plan[r - 1].window && !plan[r].window))) {
+        launches += launch_propagate(s, list, ctx->sel.ptr, count, ctx->opt_propagate, st);
+        launches += launch_compact_batch(s, list, slots, list_alt, slots_alt, pruning, ctx->sel.ptr, count,
+                                         ctx->flags.ptr, st);
+        std::swap(list, list_alt);
+        std::swap(slots, slots_alt);
+      }
       uint32_t* slot_now = ctx->h_sel + 4 + 4 * (r & 3);
       CUDA_OK(cudaMemcpyAsync(slot_now, ctx->sel.ptr, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
       CUDA_OK(cudaEventRecord(ctx->ev_ring[r & 3], st));
@@ -833,6 +857,7 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
                           pruning, ctx->opt_symmetric, st, &launch_error);
     if (ctx->opt_time_kernels) CUDA_OK(cudaEventRecord(e1, st));
     if (launch_error) fail(TSDD_ERR_RUNTIME, launch_error);
+    if (ctx->opt_time_kernels) ctx->trace.push_back({ctx->cur_pass, ctx->stats.batches, plan[r].window, plan[r].k_begin, plan[r].k_end, count, choice});
     launches += launched;
     ctx->stats.scan_kernel_launches += launched;
     if (launched && choice.ws) ctx->stats.scan_kernel_ws_launches += launched;
@@ -964,12 +989,24 @@ void collect_search_stats(tsdd_cuda_ctx* ctx) {
   ctx->stats.lb_skipped = c.lb_skipped;
   ctx->stats.scan_kernel_dot_terms = c.dot_terms;
   ctx->stats.useful_terms = c.useful_terms;
+  ctx->stats.propagated = c.propagated;
   double total = 0.0;
   for (size_t e = 0; e + 1 < ctx->events_used; e += 2) {
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, ctx->event_pool[e], ctx->event_pool[e + 1]) == cudaSuccess) total += ms;
   }
   ctx->stats.scan_kernel_ms = total;
+  if (const char* env = std::getenv("TSDD_TRACE"); env && env[0] == '1') {
+    for (size_t t = 0; t < ctx->trace.size() && 2 * t + 1 < ctx->events_used; ++t) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->event_pool[2 * t], ctx->event_pool[2 * t + 1]);
+      const auto& n = ctx->trace[t];
+      std::fprintf(stderr, "trace pass %d batch %llu %s tiles %u..%u live<=%u kernel %s%s%s%s%s  %.3f ms\n", n.pass,
+                   static_cast<unsigned long long>(n.batch), n.window ? "window" : "cover ", n.k_begin, n.k_end, n.count,
+                   n.choice.ws ? "ws" : "cp", n.choice.lb ? "+lb" : "", n.choice.tma ? "+tma" : "",
+                   n.choice.dot ? "+dot" : "", n.choice.tile16 ? "+16" : "", ms);
+    }
+  }
 }
 
 void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, double* distances) {
@@ -995,6 +1032,7 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   ctx->stats.scan_kernel_launches = 0;
   ctx->stats.scan_kernel_ws_launches = 0;
   ctx->events_used = 0;
+  ctx->trace.clear();
 
   CUDA_OK(cudaEventRecord(ctx->ev_a, st));
   ctx->stats.kernel_launches += launch_reset_search(s, st);
@@ -1017,6 +1055,7 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   }
 
   for (int pass = 0; pass < k; ++pass) {
+    ctx->cur_pass = pass;
     if (pass > 0) {
       CUDA_OK(cudaMemsetAsync(ctx->best.ptr, 0, sizeof(uint64_t), st));
       ctx->stats.kernel_launches += launch_seed_best(ctx->state(), st);
@@ -1295,6 +1334,12 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
     } else if (key == "bucket_mates") {
       if (value < 0 || value > 1024) fail(TSDD_ERR_PARAMETER, "bucket_mates must be in 0..1024");
       ctx->opt_mates = static_cast<int>(value);
+    } else if (key == "propagate") {
+      if (value < 0 || value > 32) fail(TSDD_ERR_PARAMETER, "propagate must be in 0..32");
+      ctx->opt_propagate = static_cast<int>(value);
+    } else if (key == "propagate_every") {
+      if (value < 0 || value > 64) fail(TSDD_ERR_PARAMETER, "propagate_every must be in 0..64");
+      ctx->opt_propagate_every = static_cast<int>(value);
     } else if (key == "rescore") {
       ctx->opt_rescore = value != 0;
     } else if (key == "margin_delta") {

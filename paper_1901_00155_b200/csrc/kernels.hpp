@@ -111,6 +111,12 @@ int launch_bucket_mates(SearchState s, const double* d_series, const double* d_m
                         const uint32_t* d_sorted_row, const uint32_t* d_slot_bucket,
                         const uint32_t* d_offsets, int mates, uint32_t world, uint32_t rank, cudaStream_t stream);
 
+// Time topology: every live batch candidate c tries the matches of its neighbours in time,
+// shifted along (row c + delta knows neighbour j  ->  measure (c, j - delta)); up to `tries`
+// pair distances per candidate, each lowering the bounds of both rows.
+int launch_propagate(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel, uint32_t live_upper_bound,
+                     int tries, cudaStream_t stream);
+
 // Outer-loop batch selection: the next `batch` live entries of the rarity
 // order at or after `cursor` that belong to this rank.  d_sel[0] = count,
 // d_sel[1] = next cursor.

@@ -47,7 +47,7 @@ __global__ void k_reset_search(SearchState s) {
   }
   if (i == 0) {
     *s.best = 0;
-    *s.counters = DeviceCounters{0, 0, 0, 0, 0, 0, 0, 0, 0};
+    *s.counters = DeviceCounters{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   }
 }
 
@@ -238,6 +238,78 @@ k_bucket_mates(SearchState s, const double* __restrict__ x, const double* __rest
   if (lane == 0 && calls) {
     atomicAdd(&s.counters->calls, calls);
     atomicAdd(&s.counters->terms, terms);
+  }
+}
+
+// ------------------------------------------------------------------ time topology
+// Overlapping windows have overlapping matches.  If row a = c + delta has found a neighbour j at
+// distance d, then rows c and j - delta are those same two windows, both shifted by delta
+// samples: all but |delta| of their columns were part of d(a, j), so d(c, j - delta) is usually
+// close to d.  One warp per batch candidate: each lane looks at one row a within kReach
+// positions of c and proposes j - delta; the proposals backed by the smallest bounds are
+// measured (up to `tries` of them, full float32 distance from the matrix), and each result
+// lowers the bound of BOTH rows.  In time series whose anomalies are short, almost every row
+// has a neighbour in time that already knows a good match — from the bucket mates, the window
+// rounds, or the symmetric updates of earlier scans — and is discarded here, for the price of
+// one or two pair distances, before it ever enters a tile.  (Only real pair distances lower
+// bounds, so exactness is untouched; the reference has no such step — it is the "time
+// topology" heuristic of later HOTSAX variants.)
+constexpr int kReach = 16;
+__global__ void __launch_bounds__(256)
+k_propagate(SearchState s, const uint32_t* __restrict__ batch_rows, const uint32_t* __restrict__ sel, int tries) {
+  const uint32_t idx = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (idx >= sel[0]) return;
+  const uint32_t c = batch_rows[idx];
+  const uint64_t best = *s.best;
+  uint64_t key_c = load_key(s.nn + c);
+  if (is_dead(key_c, best, s.margin, s.margin_abs, s.margin_q)) return;
+  const int delta = lane < kReach ? -static_cast<int>(lane + 1) : static_cast<int>(lane) - (kReach - 1);
+  const long long a = static_cast<long long>(c) + delta;
+  uint64_t proposal = ~0ull;  // (anchor's bound bits << 32) | lane; ~0 = none
+  uint32_t jj = 0xFFFFFFFFu;
+  if (a >= 0 && a < static_cast<long long>(s.n_rows)) {
+    const uint64_t key_a = load_key(s.nn + a);
+    const uint32_t j = static_cast<uint32_t>(key_a);
+    const long long shifted = static_cast<long long>(j) - delta;
+    if (j != 0xFFFFFFFFu && shifted >= 0 && shifted < static_cast<long long>(s.n_rows) &&
+        gap_u32(c, static_cast<uint32_t>(shifted)) >= s.n && static_cast<uint32_t>(shifted) != static_cast<uint32_t>(key_c)) {
+      jj = static_cast<uint32_t>(shifted);
+      proposal = (static_cast<uint64_t>(key_bits(key_a)) << 32) | lane;
+    }
+  }
+  const float4* pc = reinterpret_cast<const float4*>(s.rows + static_cast<size_t>(c) * s.stride);
+  unsigned long long calls = 0;
+  for (int t = 0; t < tries; ++t) {
+    uint64_t winner = proposal;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      const uint64_t other = __shfl_xor_sync(0xFFFFFFFFu, winner, d);
+      winner = other < winner ? other : winner;
+    }
+    if (winner == ~0ull) break;
+    const uint32_t j_now = __shfl_sync(0xFFFFFFFFu, jj, static_cast<int>(winner & 31u));
+    if (jj == j_now) proposal = ~0ull;  // (this proposal, and every other lane's copy of it)
+    const float4* pj = reinterpret_cast<const float4*>(s.rows + static_cast<size_t>(j_now) * s.stride);
+    float sum = 0.f;
+    for (uint32_t q = lane; q < s.stride / 4; q += 32) {
+      const float4 x = __ldg(pc + q), y = __ldg(pj + q);
+      const float d0 = x.x - y.x, d1 = x.y - y.y, d2 = x.z - y.z, d3 = x.w - y.w;
+      sum = fmaf(d0, d0, sum), sum = fmaf(d1, d1, sum), sum = fmaf(d2, d2, sum), sum = fmaf(d3, d3, sum);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, d);
+    calls += 1;
+    if (lane == 0) {
+      const uint32_t bits = __float_as_uint(sum);
+      atomicMin(as_ull(s.nn + c), static_cast<unsigned long long>(nn_key(bits, j_now)));
+      atomicMin(as_ull(s.nn + j_now), static_cast<unsigned long long>(nn_key(bits, c)));
+    }
+    if (dead_bound(sum, best, s.margin, s.margin_abs, s.margin_q)) break;  // (warp-uniform)
+  }
+  if (lane == 0 && calls) {
+    atomicAdd(&s.counters->calls, calls);
+    atomicAdd(&s.counters->terms, calls * s.n);
+    atomicAdd(&s.counters->propagated, calls);
   }
 }
 
@@ -1528,8 +1600,8 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
   float thr[kU];
   uint32_t seq = 0, cur = kTagDone, m = 0, chunks_done = 0;
   bool released = true, warp_done = false;
-  unsigned long long chunks_total = 0, abandoned_total = 0, useful_total = 0;
-  uint32_t overlap_total = 0, pairs_w = 0;
+  unsigned long long chunks_total = 0, abandoned_total = 0;
+  uint32_t overlap_total = 0, pairs_w = 0, useful_units = 0;
 #pragma unroll 1
   for (;;) {
     const uint32_t st = seq % kStagesWs, round = seq / kStagesWs;
@@ -1601,7 +1673,7 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
       }
       ++chunks_done;
       ++chunks_total;
-      useful_total += static_cast<unsigned long long>(pairs_w) * min(static_cast<uint32_t>(kChunk), s.n - min(s.n, c * kChunk));
+      useful_units += pairs_w * min(static_cast<uint32_t>(kChunk), s.n - min(s.n, c * kChunk));  // (< 2^32 per CTA)
       if constexpr (!kDot) {
         bool all_over = true;
 #pragma unroll
@@ -1710,7 +1782,7 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
     if (terms) {
       atomicAdd(&s.counters->terms, terms);
       atomicAdd(&s.counters->tile_terms, terms);
-      atomicAdd(&s.counters->useful_terms, useful_total);
+      atomicAdd(&s.counters->useful_terms, static_cast<unsigned long long>(useful_units));
       if constexpr (kDot) atomicAdd(&s.counters->dot_terms, terms);
     }
     if (abandoned_total) atomicAdd(&s.counters->abandoned, abandoned_total);
@@ -1943,8 +2015,8 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
   float2 acc[kP][kW];
   uint32_t seq = 0, cur = kTagDone, m = 0, chunks_done = 0;
   bool released = true, warp_done = false;
-  unsigned long long chunks_total = 0, useful_total = 0;
-  uint32_t overlap_total = 0, pairs_w = 0;
+  unsigned long long chunks_total = 0;
+  uint32_t overlap_total = 0, pairs_w = 0, useful_units = 0;
 #pragma unroll 1
   for (;;) {
     const uint32_t st = seq % kStages16, round = seq / kStages16;
@@ -2019,7 +2091,7 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
       }
       ++chunks_done;
       ++chunks_total;
-      useful_total += static_cast<unsigned long long>(pairs_w) * min(static_cast<uint32_t>(kCols16), s.n - min(s.n, c * kCols16));
+      useful_units += pairs_w * min(static_cast<uint32_t>(kCols16), s.n - min(s.n, c * kCols16));  // (< 2^32 per CTA)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sh.empty[st]);
@@ -2114,7 +2186,7 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
       atomicAdd(&s.counters->terms, terms);
       atomicAdd(&s.counters->tile_terms, terms);
       atomicAdd(&s.counters->dot_terms, terms);
-      atomicAdd(&s.counters->useful_terms, useful_total);
+      atomicAdd(&s.counters->useful_terms, static_cast<unsigned long long>(useful_units));
     }
   }
 #pragma unroll
@@ -2237,6 +2309,13 @@ int launch_bucket_mates(SearchState s, const double* d_series, const double* d_m
   const size_t slots = (static_cast<size_t>(s.n_rows) + world - 1) / world;
   k_bucket_mates<<<blocks_for(slots * 32, 256), 256, 0, stream>>>(
       s, d_series, d_mean, d_inv_sigma, d_sorted_row, d_slot_bucket, d_offsets, mates, world, rank);
+  return 1;
+}
+
+int launch_propagate(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel, uint32_t live_upper_bound,
+                     int tries, cudaStream_t stream) {
+  if (tries <= 0 || live_upper_bound == 0) return 0;
+  k_propagate<<<blocks_for(static_cast<size_t>(live_upper_bound) * 32, 256), 256, 0, stream>>>(s, d_batch_rows, d_sel, tries);
   return 1;
 }
 
