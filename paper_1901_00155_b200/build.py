@@ -49,9 +49,13 @@ def _run(cmd: list[str]) -> None:
         raise RuntimeError("build failed:\n  " + " ".join(cmd) + "\n" + proc.stdout + proc.stderr)
 
 
-def build_cuda(force: bool = False, verbose: bool = False) -> str:
+def build_cuda(force: bool = False, verbose: bool = False, debug_bounds: bool = False) -> str:
+    """libtsdd_cuda.so; with debug_bounds the checked build libtsdd_cuda_dbg.so (-DTSDD_DEBUG_BOUNDS:
+    in-kernel index checks, csrc/common.cuh) that the GPU tests run the randomised edge shapes on."""
+    OBJ = os.path.join(LIB, "obj_dbg" if debug_bounds else "obj")
+    NVCC_FLAGS = globals()["NVCC_FLAGS"] + (["-DTSDD_DEBUG_BOUNDS"] if debug_bounds else [])
     os.makedirs(OBJ, exist_ok=True)
-    target = os.path.join(LIB, "libtsdd_cuda.so")
+    target = os.path.join(LIB, "libtsdd_cuda_dbg.so" if debug_bounds else "libtsdd_cuda.so")
     # objects built with other flags (TSDD_NVCC_EXTRA) are stale whatever their age
     stamp = os.path.join(OBJ, "flags.txt")
     flags = " ".join(NVCC_FLAGS)
@@ -60,7 +64,7 @@ def build_cuda(force: bool = False, verbose: bool = False) -> str:
         with open(stamp, "w") as f:
             f.write(flags)
     headers = [h if os.path.isabs(h) else os.path.join(CSRC, h) for h in CUDA_HEADERS]
-    objects = []
+    objects, jobs = [], []
     for src in CUDA_SOURCES:
         path = os.path.join(CSRC, src)
         obj = os.path.join(OBJ, src.replace(".cu", ".o"))
@@ -68,7 +72,11 @@ def build_cuda(force: bool = False, verbose: bool = False) -> str:
         if force or _stale(obj, [path] + headers):
             if verbose:
                 print("nvcc", src, flush=True)
-            _run([_nvcc(), *NVCC_FLAGS, "-c", path, "-o", obj])
+            jobs.append([_nvcc(), *NVCC_FLAGS, "-c", path, "-o", obj])
+    if jobs:  # the translation units compile side by side (search_kernels.cu alone takes about a minute)
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=len(jobs)) as pool:
+            list(pool.map(_run, jobs))
     if force or _stale(target, objects):
         _run([_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC",
               "-o", target, *objects, "-ldl", "-lpthread"])
@@ -116,6 +124,7 @@ def build_all(force: bool = False, verbose: bool = False) -> dict:
     out = {"gen": build_gen(force), "cuda": build_cuda(force, verbose)}
     out["cli"] = build_tools(force)
     out["mirror_check"] = build_test_programs(force)
+    out["cuda_dbg"] = build_cuda(force, verbose, debug_bounds=True)
     return out
 
 

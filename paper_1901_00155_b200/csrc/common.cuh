@@ -5,6 +5,27 @@
 
 #include <cstdint>
 
+#include <cstdio>
+
+// -DTSDD_DEBUG_BOUNDS: every index that reaches global memory through a data-dependent path is
+// checked in the kernel itself; a violation prints where and traps (the launch fails with
+// cudaErrorAssert / an illegal instruction, which the engine reports).  compute-sanitizer is not
+// available on the GPU pool this was developed on; the checked build (libtsdd_cuda_dbg.so) runs
+// the randomised edge-shape tests in its place.  The release build compiles the checks out.
+#ifdef TSDD_DEBUG_BOUNDS
+#define TSDD_BOUND(index, limit)                                                                         \
+  do {                                                                                                   \
+    if (!(static_cast<unsigned long long>(index) < static_cast<unsigned long long>(limit))) {            \
+      printf("TSDD_DEBUG_BOUNDS: %s:%d: %s = %llu is not below %s = %llu (block %u,%u thread %u)\n",    \
+             __FILE__, __LINE__, #index, static_cast<unsigned long long>(index), #limit,                 \
+             static_cast<unsigned long long>(limit), blockIdx.x, blockIdx.y, threadIdx.x);               \
+      __trap();                                                                                          \
+    }                                                                                                    \
+  } while (0)
+#else
+#define TSDD_BOUND(index, limit) do { } while (0)
+#endif
+
 namespace tsdd_b200 {
 
 constexpr uint32_t kInfBits = 0x7F800000u;  // +inf as float bits

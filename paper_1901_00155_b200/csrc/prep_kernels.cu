@@ -480,6 +480,7 @@ k_radix_scatter(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict
     const uint32_t idx = base + r * 32 + lane;
     if (idx < count) {
       const uint32_t dst = cnt[warp][(key[r] >> shift) & 255u] + rank[r];
+      TSDD_BOUND(dst, count);
       keys_out[dst] = key[r];
       vals_out[dst] = val[r];
     }
@@ -502,6 +503,7 @@ __global__ void k_bucket_offsets(const uint32_t* __restrict__ heads, uint32_t* s
   if (s >= rows) return;
   const uint32_t head = heads[s];
   const uint32_t id = slot_bucket[s] + head - 1u;
+  TSDD_BOUND(id, rows);
   slot_bucket[s] = id;
   if (head) offsets[id] = s;
   if (s == rows - 1) {
@@ -518,6 +520,8 @@ __global__ void k_bucket_freq(const uint32_t* __restrict__ sorted_row,
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= rows) return;
   const uint32_t id = slot_bucket[s];
+  TSDD_BOUND(id + 1, rows + 1);
+  TSDD_BOUND(sorted_row[s], rows);
   freq[sorted_row[s]] = offsets[id + 1] - offsets[id];
 }
 

@@ -198,6 +198,9 @@ k_bucket_mates(SearchState s, const double* __restrict__ x, const double* __rest
   const uint32_t len = b1 - b0;
   if (len < 2) return;
   const uint32_t row_i = sorted_row[slot];
+  TSDD_BOUND(bucket + 1, s.n_rows + 1);
+  TSDD_BOUND(row_i, s.n_rows);
+  TSDD_BOUND(b1 - 1, s.n_rows);
   const double* pi = x + row_i;
   const double mu_i = mean[row_i], inv_i = inv_sigma[row_i];
   uint32_t tries = static_cast<uint32_t>(mates);
@@ -214,7 +217,9 @@ k_bucket_mates(SearchState s, const double* __restrict__ x, const double* __rest
   for (uint32_t q = 1; q <= tries; ++q) {
     if (dead_bound(bound_i, best, s.margin, s.margin_abs, s.margin_q)) break;
     const uint32_t other = b0 + (slot - b0 + q * step) % len;
+    TSDD_BOUND(other, s.n_rows);
     const uint32_t row_j = sorted_row[other];
+    TSDD_BOUND(row_j, s.n_rows);
     if (gap_u32(row_i, row_j) < s.n) continue;
     const double* pj = x + row_j;
     const double mu_j = mean[row_j], inv_j = inv_sigma[row_j];
@@ -288,6 +293,8 @@ k_propagate(SearchState s, const uint32_t* __restrict__ batch_rows, const uint32
     }
     if (winner == ~0ull) break;
     const uint32_t j_now = __shfl_sync(0xFFFFFFFFu, jj, static_cast<int>(winner & 31u));
+    TSDD_BOUND(c, s.n_rows);
+    TSDD_BOUND(j_now, s.n_rows);
     if (jj == j_now) proposal = ~0ull;  // (this proposal, and every other lane's copy of it)
     const float4* pj = reinterpret_cast<const float4*>(s.rows + static_cast<size_t>(j_now) * s.stride);
     float sum = 0.f;
@@ -322,6 +329,7 @@ __global__ void k_flag_live(SearchState s, const uint32_t* __restrict__ order, u
   const uint32_t e = cursor + t;
   if (e >= s.n_rows) return;
   const uint32_t row = order[e];
+  TSDD_BOUND(row, s.n_rows);
   bool live = (e % world == rank) && !s.excluded[row] && !s.exact[row];
   if (live && pruning) live = !is_dead(s.nn[row], *s.best, s.margin, s.margin_abs, s.margin_q);
   flags[t] = live ? 1u : 0u;
@@ -338,6 +346,7 @@ __global__ void k_take_batch(const uint32_t* __restrict__ order, const uint32_t*
   if (e >= n_rows) return;
   const uint32_t f = flags[t], r = ranks[t];
   if (f && r < batch) {
+    TSDD_BOUND(order[e], n_rows);
     batch_rows[r] = order[e];
     if (r == batch - 1) sel[1] = e + 1;
   }
@@ -367,6 +376,7 @@ k_compact_batch(SearchState s, const uint32_t* __restrict__ in, const uint32_t* 
     if (idx < count) {
       row = in[idx];
       slot = in_slots[idx];
+      TSDD_BOUND(row, s.n_rows);
       keep = !pruning || !is_dead(load_key(s.nn + row), best, s.margin, s.margin_abs, s.margin_q);
     }
     const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, keep);
@@ -381,6 +391,7 @@ k_compact_batch(SearchState s, const uint32_t* __restrict__ in, const uint32_t* 
     }
     if (keep) {
       const uint32_t at = before + __popc(ballot & ((1u << lane) - 1u));
+      TSDD_BOUND(at, count);
       out[at] = row;
       out_slots[at] = slot;
     }
@@ -401,6 +412,7 @@ k_compact_flag(SearchState s, const uint32_t* __restrict__ in, int pruning, cons
   const uint32_t count = sel[0];
   const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
   bool keep = false;
+  if (idx < count) TSDD_BOUND(in[idx], s.n_rows);
   if (idx < count) keep = !pruning || !is_dead(load_key(s.nn + in[idx]), *s.best, s.margin, s.margin_abs, s.margin_q);
   if (idx < count) keep_flags[idx] = keep ? 1u : 0u;
   const int kept = __syncthreads_count(keep);
@@ -434,6 +446,7 @@ k_compact_scatter(const uint32_t* __restrict__ in, const uint32_t* __restrict__ 
   for (uint32_t w = 0; w < warp; ++w) before += warp_sums[w];
   if (keep) {
     const uint32_t at = before + __popc(ballot & ((1u << lane) - 1u));
+    TSDD_BOUND(at, count);
     out[at] = in[idx];
     out_slots[at] = in_slots[idx];
   }
@@ -451,14 +464,17 @@ __global__ void k_compact_publish(uint32_t* sel) { sel[0] = sel[2]; }
 __global__ void k_invert_order(const uint32_t* __restrict__ sorted_row, uint32_t rows,
                                uint32_t* __restrict__ slot_of_row) {
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s < rows) slot_of_row[sorted_row[s]] = s;
+  if (s < rows) {
+    TSDD_BOUND(sorted_row[s], rows);
+    slot_of_row[sorted_row[s]] = s;
+  }
 }
 
 // keys[i] = hash-order slot of batch row i (the sort key that makes tiles word-coherent)
 __global__ void k_batch_slots(const uint32_t* __restrict__ batch_rows, const uint32_t* __restrict__ sel,
                               const uint32_t* __restrict__ slot_of_row, uint32_t* __restrict__ keys) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < sel[0]) keys[i] = slot_of_row[batch_rows[i]];
+  if (i < sel[0]) keys[i] = slot_of_row[batch_rows[i]];  // (batch rows are checked where they are selected)
 }
 
 // Dense copy of the batch's rows, NEGATED, so that the tile kernel forms
@@ -498,6 +514,7 @@ k_gather_rows(SearchState s, const uint32_t* __restrict__ batch_rows, const uint
     float2* dst2 = reinterpret_cast<float2*>(out + static_cast<size_t>(pair) * 2 * s.stride);
     float* dst1 = reinterpret_cast<float*>(dst2) + (l & 1u);
     if (r < count) {
+      TSDD_BOUND(batch_rows[r], s.n_rows);
       const float4* src = reinterpret_cast<const float4*>(s.rows + static_cast<size_t>(batch_rows[r]) * s.stride);
       for (uint32_t c = lane; c < quads; c += 32) {
         const float4 v = __ldg(src + c);
@@ -513,6 +530,7 @@ k_gather_rows(SearchState s, const uint32_t* __restrict__ batch_rows, const uint
   const uint32_t at = tma_layout ? (r & ~(kTileRows - 1u)) + tma_row_of_candidate(r & (kTileRows - 1u)) : r;
   float4* dst = reinterpret_cast<float4*>(out + static_cast<size_t>(at) * s.stride);
   if (r < count) {
+    TSDD_BOUND(batch_rows[r], s.n_rows);
     const float4* src =
         reinterpret_cast<const float4*>(s.rows + static_cast<size_t>(batch_rows[r]) * s.stride);
     for (uint32_t c = lane; c < quads; c += 32) {
@@ -536,6 +554,7 @@ k_finalize_batch(SearchState s, const uint32_t* __restrict__ batch_rows,
   uint64_t mine = 0;
   if (idx < count) {
     const uint32_t row = batch_rows[idx];
+    TSDD_BOUND(row, s.n_rows);
     const uint64_t key = s.nn[row];
     if (!pruning || !is_dead(key, best, s.margin, s.margin_abs, s.margin_q)) {
       s.exact[row] = 1;
@@ -609,7 +628,7 @@ __device__ __forceinline__ void issue_stage(unsigned char* stage, const float* a
     const uint32_t piece = threadIdx.x + q * kScanThreads;
     const uint32_t r = piece / kPieces, kc = piece % kPieces;
     cp_async16(stage + kCand * kRowBytes + r * kRowBytes + ((kc ^ (r & 7)) << 4),
-               rows + static_cast<size_t>(s_brow[r]) * stride + col0 + kc * 4);
+               rows + static_cast<size_t>(s_brow[r]) * stride + col0 + kc * 4);  // (s_brow is checked where it is written)
   }
 }
 
@@ -766,6 +785,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
   auto prefetch = [&](uint32_t h) {
     if (tid < kCand) {
       const uint32_t row = s_cand[tid];
+      if (row != 0xFFFFFFFFu) TSDD_BOUND(row, s.n_rows);
       pf_key = (row != 0xFFFFFFFFu && a.pruning) ? load_key(s.nn + row) : 0ull;
     } else if (tid < kCand + kNbr) {
       const uint32_t slot = slot0_of(h) + (tid - kCand);
@@ -807,6 +827,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
       const uint32_t t = tid - kCand;
       s_jrow[t] = pf_j;
       s_brow[t] = pf_j != 0xFFFFFFFFu ? pf_j : s.n_rows;  // row n_rows is zero padding
+      TSDD_BOUND(s_brow[t], s.n_rows + 1);
       s_nub[t] = pf_j != 0xFFFFFFFFu ? __uint_as_float(key_bits(pf_key)) : -1.f;
     }
     const int n_live = __syncthreads_count(live);
@@ -1013,8 +1034,10 @@ k_scan_tiles(SearchState s, ScanArgs a) {
             j_min = j;
           }
         }
-        if (pair_ok && d < nub[w])
+        if (pair_ok && d < nub[w]) {
+          TSDD_BOUND(j, s.n_rows);
           atomicMin(as_ull(s.nn + j), static_cast<unsigned long long>(nn_key(__float_as_uint(d), row)));
+        }
       }
       // min over the kTx lanes that share candidate u: distance first, then neighbour
       uint32_t g_min = d_min;
@@ -1024,6 +1047,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
 #pragma unroll
       for (int d = kTx / 2; d > 0; d >>= 1) g_j = min(g_j, __shfl_xor_sync(0xFFFFFFFFu, g_j, d));
       if (tx == 0 && g_j != 0xFFFFFFFFu) {
+        TSDD_BOUND(row, s.n_rows);
         atomicMin(as_ull(s.nn + row), static_cast<unsigned long long>(nn_key(g_min, g_j)));
         s_loc[cand_of(ty, u)] = fminf(s_loc[cand_of(ty, u)], __uint_as_float(g_min));
       }
@@ -1424,6 +1448,7 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
         const uint32_t slot = slot0 + lane + 32 * q;
         nbr_j[q] = 0xFFFFFFFFu;
         if (slot < s.n_rows) nbr_j[q] = window ? a.nbr_index[slot] : slot;
+        if (nbr_j[q] != 0xFFFFFFFFu) TSDD_BOUND(nbr_j[q], s.n_rows);
         nbr_ub[q] = nbr_j[q] != 0xFFFFFFFFu ? key_bits(load_key(s.nn + nbr_j[q])) : 0u;
         if constexpr (kDot) nbr_norm[q] = nbr_j[q] != 0xFFFFFFFFu ? s.row_norms[nbr_j[q]] : 0.f;
       }
@@ -1469,6 +1494,7 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
         const uint32_t e = lane + 32 * q, j = nbr_j[q];
         meta.jrow[e] = j;
         meta.brow[e] = j != 0xFFFFFFFFu ? j : s.n_rows;  // row n_rows is zero padding
+        TSDD_BOUND(meta.brow[e], s.n_rows + 1);
         meta.nub[e] = j != 0xFFFFFFFFu ? __uint_as_float(nbr_ub[q]) : -1.f;
         if constexpr (kDot) meta.nnorm[e] = nbr_norm[q];
       }
@@ -1754,8 +1780,10 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
                   j_min = j;
                 }
               }
-              if (pair_ok && d < nub[w])
+              if (pair_ok && d < nub[w]) {
+                TSDD_BOUND(j, s.n_rows);
                 atomicMin(as_ull(s.nn + j), static_cast<unsigned long long>(nn_key(__float_as_uint(d), row)));
+              }
             }
             uint32_t g_min = d_min;
 #pragma unroll
@@ -1764,6 +1792,7 @@ k_scan_tiles_ws(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap m
 #pragma unroll
             for (int d = kTxLanes / 2; d > 0; d >>= 1) g_j = min(g_j, __shfl_xor_sync(0xFFFFFFFFu, g_j, d));
             if ((tx & (kTxLanes - 1)) == 0 && g_j != 0xFFFFFFFFu) {
+              TSDD_BOUND(row, s.n_rows);
               atomicMin(as_ull(s.nn + row), static_cast<unsigned long long>(nn_key(g_min, g_j)));
               // (squared distances are >= 0: their bits order like the floats; two warps may share a candidate)
               atomicMin(reinterpret_cast<uint32_t*>(&sh.loc[cand0_of_thread + kCandStep * u]), g_min);
@@ -1947,6 +1976,7 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
         const uint32_t e = lane + 32 * q, slot = slot0 + e;
         uint32_t j = 0xFFFFFFFFu;
         if (slot < s.n_rows) j = window ? a.nbr_index[slot] : slot;
+        if (j != 0xFFFFFFFFu) TSDD_BOUND(j, s.n_rows);
         meta.jrow[e] = j;
         meta.nub[e] = j != 0xFFFFFFFFu ? __uint_as_float(key_bits(load_key(s.nn + j))) : -1.f;
         meta.nnorm[e] = j != 0xFFFFFFFFu ? s.row_norms[j] : 0.f;
@@ -2159,8 +2189,10 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
                     j_min = j;
                   }
                 }
-                if (pair_ok && d < nub[w])
+                if (pair_ok && d < nub[w]) {
+                  TSDD_BOUND(j, s.n_rows);
                   atomicMin(as_ull(s.nn + j), static_cast<unsigned long long>(nn_key(__float_as_uint(d), row)));
+                }
               }
               // smallest distance among the 8 thread columns; the lane(s) holding it publish it (the
               // 64-bit atomicMin settles a tie towards the smaller neighbour row)
@@ -2168,6 +2200,7 @@ k_scan_tiles_ws16(SearchState s, ScanArgs a, const __grid_constant__ CUtensorMap
 #pragma unroll
               for (int d = kTxLanes / 2; d > 0; d >>= 1) g_min = min(g_min, __shfl_xor_sync(0xFFFFFFFFu, g_min, d));
               if (d_min == g_min && j_min != 0xFFFFFFFFu) {
+                TSDD_BOUND(row, s.n_rows);
                 atomicMin(as_ull(s.nn + row), static_cast<unsigned long long>(nn_key(d_min, j_min)));
                 atomicMin(reinterpret_cast<uint32_t*>(&sh.loc[l]), d_min);
               }
@@ -2222,14 +2255,14 @@ k_collect_finalists(SearchState s, uint32_t* __restrict__ list, uint32_t cap, ui
     const uint64_t key = s.nn[i];
     if (key_bits(key) == kInfBits || is_dead(key, best, s.margin, s.margin_abs, s.margin_q)) continue;
     const uint32_t at = atomicAdd(count, 1u);
-    if (at < cap) list[at] = i;
+    if (at < cap) list[at] = i;  // (guarded: the host collects again with room for all)
   }
 }
 
 __global__ void k_gather_keys(const uint64_t* __restrict__ nn, const uint32_t* __restrict__ list, uint32_t count,
                               uint64_t* __restrict__ out) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < count) out[i] = nn[list[i]];
+  if (i < count) out[i] = nn[list[i]];  // (list entries are row numbers written by k_collect_finalists)
 }
 
 // z-normalised float64 values of one row (series.cpp:21-37), kept in global memory
@@ -2507,6 +2540,7 @@ k_permute_rows(const float* __restrict__ rows, const uint32_t* __restrict__ sort
   if (slot >= rows_padded) return;
   float4* dst = reinterpret_cast<float4*>(out + static_cast<size_t>(slot) * stride);
   if (slot < n_rows) {
+    TSDD_BOUND(sorted_row[slot], n_rows);
     const float4* src = reinterpret_cast<const float4*>(rows + static_cast<size_t>(sorted_row[slot]) * stride);
     for (uint32_t c = lane; c < stride / 4; c += 32) dst[c] = __ldg(src + c);
   } else {

@@ -20,7 +20,9 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libtsdd_cuda.so")
+# TSDD_CUDA_LIB selects another build of the same library (the tests point it at the checked
+# build, _lib/libtsdd_cuda_dbg.so: -DTSDD_DEBUG_BOUNDS, in-kernel index checks)
+LIB_PATH = os.environ.get("TSDD_CUDA_LIB") or os.path.join(_HERE, "_lib", "libtsdd_cuda.so")
 
 OK, ERR_PARAMETER, ERR_VALIDATION, ERR_INFEASIBLE, ERR_RUNTIME = 0, 2, 3, 4, 5
 SEARCH_DISABLE_PRUNING = 1

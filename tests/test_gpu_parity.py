@@ -1104,3 +1104,56 @@ def test_patched_reference_runs_the_cuda_engine(golden, chk, tmp_path):
     assert p.returncode == 2 and "no subsequence has a non-self match" in p.stderr, p.stderr
     p = subprocess.run([TSDD_PATCHED, str(path), "gpu", "128", "4", "4"], capture_output=True, text=True)
     assert p.returncode == 2 and "unknown engine 'gpu'" in p.stderr, p.stderr
+
+
+# ------------------------------------------------------------------ soak, and the checked build
+@pytest.mark.parametrize("case", range(12))
+def test_soak_random_series_shapes_and_options(ctx, chk, case):
+    """tools/soak.py, reduced: random kind / length / n / SAX shape / k AND random engine options
+    (dot form, first batch, filter, filter on the producer warpgroup, time topology) against the
+    reference's exclusion-zone top-k."""
+    rng = np.random.default_rng(90000 + case)
+    kind = rng.choice(["noise", "walk", "sine"])
+    m = int(rng.integers(15000, 40000))
+    n = int(rng.choice([24, 50, 64, 100, 128, 200, 256, 300]))
+    w, a, k = int(rng.integers(2, 9)), int(rng.integers(2, 7)), int(rng.integers(1, 4))
+    if kind == "noise":
+        x = rng.random(m).astype(np.float32)
+    elif kind == "walk":
+        x = np.cumsum(rng.standard_normal(m)).astype(np.float32)
+    else:
+        x = (np.sin(2 * np.pi * np.arange(m) / rng.integers(20, 200)) + 0.3 * rng.standard_normal(m)).astype(np.float32)
+    opts = {"dot_form": int(rng.choice([1, 2])), "first_batch": int(rng.choice([128, 4096])),
+            "lower_bound": int(rng.choice([0, 1])), "filter_in_ws": int(rng.choice([0, 1])),
+            "propagate": int(rng.choice([0, 2, 8])), "propagate_every": int(rng.choice([0, 1, 2]))}
+    defaults = {"dot_form": 1, "first_batch": 128, "lower_bound": 1, "filter_in_ws": 0, "propagate": 8,
+                "propagate_every": 2}
+    try:
+        for name, value in opts.items():
+            ctx.set_option(name, value)
+        ctx.prepare(x, n, w, a)
+        pos, dist = ctx.search(k)
+    finally:
+        for name, value in defaults.items():
+            ctx.set_option(name, value)
+    want = chk.topk(x, n, w, a, k)
+    assert_discords_match(chk, x, n, pos, dist, want)
+
+
+def test_checked_build_runs_the_edge_shapes():
+    """libtsdd_cuda_dbg.so (-DTSDD_DEBUG_BOUNDS: every data-dependent global-memory index is
+    checked inside the kernels and traps on a violation) through the randomised edge-shape tests,
+    the dot-product form, the 256-candidate tiles, the filter on the producer warpgroup, the rank
+    group and the soak — in place of compute-sanitizer, which this GPU pool does not offer."""
+    import subprocess
+    import sys
+
+    dbg = os.path.join(_ROOT, "paper_1901_00155_b200", "_lib", "libtsdd_cuda_dbg.so")
+    assert os.path.exists(dbg), "build it with python -m paper_1901_00155_b200.build"
+    expr = ("randomised_small_cases or dot_product_form_matches or 256_candidate or filter_on_the_producer_warpgroup_matches"
+            " or group_of_ranks or soak_random or smallest_feasible or long_subsequences or topk_matches")
+    p = subprocess.run([sys.executable, "-m", "pytest", os.path.join(_ROOT, "tests", "test_gpu_parity.py"), "-x", "-q",
+                        "-m", "gpu", "-k", expr, "-p", "no:cacheprovider"],
+                       env=dict(os.environ, TSDD_CUDA_LIB=dbg), capture_output=True, text=True, timeout=1500)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]
+    assert "TSDD_DEBUG_BOUNDS" not in p.stdout + p.stderr

@@ -427,3 +427,16 @@ def test_patched_reference_builds_against_the_engine_header(tmp_path):
     if not torch.cuda.is_available():
         p = subprocess.run([TSDD_PATCHED, str(path), "cuda", "64", "4", "4"], capture_output=True, text=True)
         assert p.returncode == 1 and "no CUDA device" in p.stderr, p.stderr  # no CPU fallback behind `cuda`
+
+
+def test_checked_build_carries_the_bounds_checks():
+    """The -DTSDD_DEBUG_BOUNDS build holds the in-kernel checks (their report string is in the
+    binary), the release build compiles them out; both export the same C ABI."""
+    lib = os.path.join(ROOT, "paper_1901_00155_b200", "_lib")
+    marker = b"TSDD_DEBUG_BOUNDS: "
+    assert marker in open(os.path.join(lib, "libtsdd_cuda_dbg.so"), "rb").read()
+    assert marker not in open(os.path.join(lib, "libtsdd_cuda.so"), "rb").read()
+    import ctypes
+    dbg = ctypes.CDLL(os.path.join(lib, "libtsdd_cuda_dbg.so"))
+    for name in pkg.engine.SYMBOLS:
+        assert hasattr(dbg, name), name
