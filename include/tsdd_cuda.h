@@ -70,6 +70,8 @@ typedef struct tsdd_cuda_stats {
   uint64_t exact_reruns;   /* of those, measured again from +inf because the float32 start bound was too low */
   uint64_t useful_terms;   /* of scan_kernel_terms: terms of pairs that were live, non-self and not padding */
   uint64_t propagated;     /* pair distances measured by the time-topology step (option "propagate") */
+  uint64_t scan_kernel_tc_launches; /* of scan_kernel_dot_launches, those of the tensor-core tile kernel (dot_form 3 / 4) */
+  uint64_t scan_kernel_tc_terms;    /* of scan_kernel_dot_terms, those computed there (three tf32 MACs per term) */
 } tsdd_cuda_stats;
 
 /* ---- lifetime ------------------------------------------------------------ */
@@ -111,7 +113,10 @@ int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream);
  * further away than its threshold), "dot_form" (the warp-specialised kernel
  * computes d^2 as |a|^2 + |b|^2 - 2 a.b, one FFMA per term, with the discard band widened by
  * its absolute error bound: 0 never; 1 once a search has found that tiles are not abandoned
- * early anyway and the best-so-far dwarfs the bound; 2 from the first launch),
+ * early anyway and the best-so-far dwarfs the bound; 2 from the first launch; 3 / 4: as 1 / 2, with
+ * the dot-form tiles of batches that fill 128 candidates on the TENSOR CORES — tcgen05.mma
+ * kind::tf32 on rows split into two tf32 parts, three MMAs per 8 columns, accumulators in tensor
+ * memory; an experiment, the CUDA-core kernels stay the default),
  * "tensor_map" (0/1: the warp-specialised kernel loads the tiles of covering scans — and, in
  * the dot-product form, of window rounds, from a copy of the matrix kept in the hash-sorted
  * order — as cp.async.bulk.tensor boxes instead of one bulk copy per row),

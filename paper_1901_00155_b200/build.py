@@ -20,7 +20,7 @@ LIB = os.path.join(HERE, "_lib")
 OBJ = os.path.join(HERE, "_lib", "obj")
 INCLUDE = os.path.join(ROOT, "include")
 
-CUDA_SOURCES = ["prep_kernels.cu", "search_kernels.cu", "probe_kernels.cu", "engine.cu"]
+CUDA_SOURCES = ["prep_kernels.cu", "search_kernels.cu", "tc_kernels.cu", "probe_kernels.cu", "engine.cu"]
 CUDA_HEADERS = ["common.cuh", "kernels.hpp", os.path.join(INCLUDE, "tsdd_cuda.h")]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",

@@ -105,6 +105,7 @@ struct DeviceCounters {
   // at most (2n - 1) / N of all pairs, are not taken out.)
   unsigned long long useful_terms;
   unsigned long long propagated;  // pair distances measured by the time-topology step (k_propagate)
+  unsigned long long tc_terms;    // of dot_terms, those computed on the tensor cores (tc_kernels.cu: 3 tf32 MACs a term)
 };
 
 }  // namespace tsdd_b200

@@ -222,6 +222,10 @@ struct tsdd_cuda_ctx {
   DeviceArray<float> series_f32;
   DeviceArray<double> series, mean, inv_sigma;
   DeviceArray<float> matrix, lb_means, lb_boxes, row_norms, matrix_sorted;
+  // tensor-core experiment: the matrix, its hash-sorted copy and the batch split into tf32 parts
+  DeviceArray<float> matrix_hi, matrix_lo, sorted_hi, sorted_lo, batch_hi, batch_lo;
+  bool split_ready = false, sorted_split_ready = false;
+  bool opt_tensor_cores = false;
   bool norms_ready = false;   // row_norms holds the norms of the prepared matrix
   bool sorted_ready = false;  // matrix_sorted holds the prepared matrix in the hash-sorted order
   DeviceArray<uint32_t> hash0, freq, offsets, slot_bucket, scalars, slot_of_row, first_bad;
@@ -298,7 +302,9 @@ struct tsdd_cuda_ctx {
   // <= |a||b| <= n, the two norms and three more roundings — within (n + 32) n 2^-24 of the
   // float32 rows' true distance.  The band covers the error of a bound and of the best-so-far.
   double dot_error() const {
-    return (static_cast<double>(n) + 32.0) * static_cast<double>(n) * 5.9604644775390625e-08;
+    // (x 3 on the tensor cores: the tf32 split drops products below 3 x 2^-20 |a||b| <= 2.9e-6 n, and
+    // the float32 accumulation in tensor memory may truncate where the CUDA cores round)
+    return (opt_tensor_cores ? 3.0 : 1.0) * (static_cast<double>(n) + 32.0) * static_cast<double>(n) * 5.9604644775390625e-08;
   }
   bool dot_eligible(uint64_t best_key_now) const {
     if (opt_dot == 2) return true;
@@ -314,6 +320,7 @@ struct tsdd_cuda_ctx {
     c.tensor_map = opt_tensor_map;
     c.filter_in_ws = opt_lb_in_ws;
     c.tile16 = opt_tile16;
+    c.tensor_cores = opt_tensor_cores && split_ready;
     return c;
   }
 
@@ -586,6 +593,8 @@ void reset_stats(tsdd_cuda_ctx* ctx) {
   ctx->prepared = false;
   ctx->norms_ready = false;
   ctx->sorted_ready = false;
+  ctx->split_ready = false;
+  ctx->sorted_split_ready = false;
 }
 
 template <typename T>
@@ -715,6 +724,10 @@ void ensure_batch_capacity(tsdd_cuda_ctx* ctx, uint32_t batch) {
   ctx->batch_slots.alloc(padded);
   ctx->batch_slots_alt.alloc(padded);
   ctx->batch_matrix.alloc(static_cast<size_t>(padded) * ctx->stride);
+  if (ctx->opt_tensor_cores) {
+    ctx->batch_hi.alloc(static_cast<size_t>(padded) * ctx->stride);
+    ctx->batch_lo.alloc(static_cast<size_t>(padded) * ctx->stride);
+  }
   ctx->batch_capacity = padded;
 }
 
@@ -805,8 +818,10 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
   // ring of tiles), so that the rows whose bounds drop as a by-product (d(i,j) = d(j,i))
   // are spread over the whole series instead of always being the first ones.
   const uint32_t slot_tiles = (ctx->rows + kTileRows - 1) / kTileRows;
+  // (not with the tensor-core kernel: it walks 256-row tiles in place, and a batch whose segments
+  // mix it with the rotated kernels would leave rows unvisited)
   const uint32_t rotation =
-      (pruning && ctx->opt_rotate)
+      (pruning && ctx->opt_rotate && !(ctx->opt_tensor_cores && ctx->split_ready))
           ? static_cast<uint32_t>((ctx->stats.batches * 0.6180339887498949 - std::floor(ctx->stats.batches * 0.6180339887498949)) * slot_tiles) % slot_tiles
           : 0u;
   // The live count after each compaction is read back ONE segment late: segment r's grid is
@@ -841,9 +856,15 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
       }
     }
     const ScanChoice choice = choose_scan_kernel(ctx->scan_config(), s, count, plan[r].window, pruning, ctx->dot_now);
-    const uint32_t padded = round_up_u32(count, choice.tile16 ? 2 * kTileRows : kTileRows);
-    launches += launch_gather_rows(s, list, ctx->sel.ptr, padded, choice.tile16 ? 2 : choice.tma ? 1 : 0,
-                                   ctx->batch_matrix.ptr, st);
+    ScanChoice choice_now = choice;
+    if (choice_now.tc && plan[r].window && !ctx->sorted_split_ready) choice_now.tc = false;  // (no split copy of the sorted matrix)
+    if (choice.tc && !choice_now.tc) choice_now.tile16 = ctx->opt_tile16 && count > 192;
+    const uint32_t padded = round_up_u32(count, choice_now.tile16 ? 2 * kTileRows : kTileRows);
+    if (choice_now.tc)
+      launches += launch_gather_rows_split(s, list, ctx->sel.ptr, padded, ctx->batch_hi.ptr, ctx->batch_lo.ptr, st);
+    else
+      launches += launch_gather_rows(s, list, ctx->sel.ptr, padded, choice_now.tile16 ? 2 : choice_now.tma ? 1 : 0,
+                                     ctx->batch_matrix.ptr, st);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->opt_time_kernels) {
       e0 = next_event(ctx);
@@ -851,17 +872,25 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
       CUDA_OK(cudaEventRecord(e0, st));
     }
     const char* launch_error = nullptr;
-    const int launched =
-        launch_scan_tiles(choice, s, ctx->batch_matrix.ptr, list, slots, ctx->sel.ptr, count,
-                          plan[r].window ? ctx->sorted_row : nullptr, plan[r].k_begin, plan[r].k_end, rotation,
-                          pruning, ctx->opt_symmetric, st, &launch_error);
+    int launched = 0;
+    if (choice_now.tc) {
+      const TcOperands op{ctx->batch_hi.ptr, ctx->batch_lo.ptr, ctx->matrix_hi.ptr, ctx->matrix_lo.ptr,
+                          ctx->sorted_hi.ptr, ctx->sorted_lo.ptr, ctx->rows_padded};
+      launched = launch_scan_tiles_tc(s, op, list, slots, ctx->sel.ptr, count, plan[r].window ? ctx->sorted_row : nullptr,
+                                      plan[r].k_begin, plan[r].k_end, pruning, ctx->opt_symmetric, st, &launch_error);
+      if (launched) ctx->stats.scan_kernel_tc_launches += launched;
+    } else {
+      launched = launch_scan_tiles(choice_now, s, ctx->batch_matrix.ptr, list, slots, ctx->sel.ptr, count,
+                                   plan[r].window ? ctx->sorted_row : nullptr, plan[r].k_begin, plan[r].k_end, rotation,
+                                   pruning, ctx->opt_symmetric, st, &launch_error);
+    }
     if (ctx->opt_time_kernels) CUDA_OK(cudaEventRecord(e1, st));
     if (launch_error) fail(TSDD_ERR_RUNTIME, launch_error);
-    if (ctx->opt_time_kernels) ctx->trace.push_back({ctx->cur_pass, ctx->stats.batches, plan[r].window, plan[r].k_begin, plan[r].k_end, count, choice});
+    if (ctx->opt_time_kernels) ctx->trace.push_back({ctx->cur_pass, ctx->stats.batches, plan[r].window, plan[r].k_begin, plan[r].k_end, count, choice_now});
     launches += launched;
     ctx->stats.scan_kernel_launches += launched;
-    if (launched && choice.ws) ctx->stats.scan_kernel_ws_launches += launched;
-    if (launched && choice.dot) ctx->stats.scan_kernel_dot_launches += launched;
+    if (launched && choice_now.ws) ctx->stats.scan_kernel_ws_launches += launched;
+    if (launched && choice_now.dot) ctx->stats.scan_kernel_dot_launches += launched;
   }
   launches += launch_finalize_batch(s, list, ctx->sel.ptr, ctx->batch_capacity, pruning, st);
   ctx->stats.kernel_launches += launches;
@@ -948,6 +977,28 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
               ctx->sorted_ready = true;
             }
           }
+          if (ctx->dot_now && ctx->opt_tensor_cores && !ctx->split_ready) {
+            // the tensor-core experiment: tf32 hi / lo parts of the matrix (and of its hash-sorted copy)
+            const size_t floats = static_cast<size_t>(ctx->rows_padded) * ctx->stride;
+            size_t free_b = 0, total_b = 0;
+            CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
+            const size_t need = floats * sizeof(float) * (ctx->sorted_ready ? 4 : 2);
+            if (ctx->matrix_hi.count >= floats || free_b > need + (size_t{2} << 30)) {
+              ctx->matrix_hi.alloc(floats);
+              ctx->matrix_lo.alloc(floats);
+              ctx->stats.kernel_launches += launch_split_tf32(ctx->matrix.ptr, floats, ctx->matrix_hi.ptr, ctx->matrix_lo.ptr, st);
+              if (ctx->sorted_ready) {
+                ctx->sorted_hi.alloc(floats);
+                ctx->sorted_lo.alloc(floats);
+                ctx->stats.kernel_launches +=
+                    launch_split_tf32(ctx->matrix_sorted.ptr, floats, ctx->sorted_hi.ptr, ctx->sorted_lo.ptr, st);
+                ctx->sorted_split_ready = true;
+              }
+              ctx->split_ready = true;
+              ctx->batch_capacity = 0;  // (the batch buffers grow their split twins at the next ensure_batch_capacity)
+              ensure_batch_capacity(ctx, batch_now);
+            }
+          }
           s = ctx->state();
         }
         ctx->stats.scanned_candidates += count;
@@ -990,6 +1041,7 @@ void collect_search_stats(tsdd_cuda_ctx* ctx) {
   ctx->stats.scan_kernel_dot_terms = c.dot_terms;
   ctx->stats.useful_terms = c.useful_terms;
   ctx->stats.propagated = c.propagated;
+  ctx->stats.scan_kernel_tc_terms = c.tc_terms;
   double total = 0.0;
   for (size_t e = 0; e + 1 < ctx->events_used; e += 2) {
     float ms = 0.f;
@@ -1004,7 +1056,7 @@ void collect_search_stats(tsdd_cuda_ctx* ctx) {
       std::fprintf(stderr, "trace pass %d batch %llu %s tiles %u..%u live<=%u kernel %s%s%s%s%s  %.3f ms\n", n.pass,
                    static_cast<unsigned long long>(n.batch), n.window ? "window" : "cover ", n.k_begin, n.k_end, n.count,
                    n.choice.ws ? "ws" : "cp", n.choice.lb ? "+lb" : "", n.choice.tma ? "+tma" : "",
-                   n.choice.dot ? "+dot" : "", n.choice.tile16 ? "+16" : "", ms);
+                   n.choice.dot ? "+dot" : "", n.choice.tc ? "+tc" : n.choice.tile16 ? "+16" : "", ms);
     }
   }
 }
@@ -1026,6 +1078,7 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   ctx->dot_now = false;
   s = ctx->state();
   ctx->stats.scan_kernel_dot_launches = 0;
+  ctx->stats.scan_kernel_tc_launches = 0;
   ctx->stats.finalists = 0;
   ctx->stats.exact_reruns = 0;
   ctx->stats.scanned_candidates = 0;
@@ -1381,8 +1434,10 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
     } else if (key == "tensor_map") {
       ctx->opt_tensor_map = value != 0;
     } else if (key == "dot_form") {
-      if (value != 0 && value != 1 && value != 2) fail(TSDD_ERR_PARAMETER, "dot_form must be 0, 1 or 2");
-      ctx->opt_dot = static_cast<int>(value);
+      if (value != 0 && value != 1 && value != 2 && value != 3 && value != 4)
+        fail(TSDD_ERR_PARAMETER, "dot_form must be 0, 1, 2, 3 or 4");
+      ctx->opt_dot = value >= 3 ? static_cast<int>(value) - 2 : static_cast<int>(value);  // 3 / 4: as 1 / 2 ...
+      ctx->opt_tensor_cores = value >= 3;                                                 // ... on the tensor cores
     } else if (key == "shard_prep") {
       ctx->opt_shard_prep = value != 0;
     } else if (key == "share_bounds") {
@@ -1471,6 +1526,7 @@ int tsdd_cuda_reindex(tsdd_cuda_ctx* ctx, size_t word_len, size_t alphabet) {
     ctx->word_len = word_len;
     ctx->alphabet = alphabet;
     ctx->sorted_ready = false;  // (the hash-sorted copy of the matrix follows the OLD order)
+    ctx->sorted_split_ready = false;
     CUDA_OK(cudaEventRecord(ctx->ev_a, st));
     uint64_t launches = launch_window_encode(ctx->series.ptr, ctx->rows, static_cast<uint32_t>(ctx->n),
                                              static_cast<uint32_t>(word_len), static_cast<uint32_t>(alphabet),

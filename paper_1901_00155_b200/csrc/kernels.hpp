@@ -155,6 +155,7 @@ struct ScanConfig {
   bool tensor_map = true;    // the warp-specialised kernel loads tiles as TMA boxes where it can
   bool filter_in_ws = false; // covering scans with the lower-bound filter on the ws kernel's producer warpgroup
   bool tile16 = true;        // dot form on 256-candidate tiles (k_scan_tiles_ws16)
+  bool tensor_cores = false; // dot form on the tensor cores (k_scan_tiles_tc) while a batch fills 128-candidate tiles
 };
 
 // Which kernel a launch uses.  Computed ONCE per segment (choose_scan_kernel) and handed to both
@@ -165,6 +166,7 @@ struct ScanChoice {
   bool tma;  // ... fed by tensor-map box loads (covering scans)
   bool dot;  // ... in the dot-product form
   bool tile16;  // ... on 256-candidate tiles, 16 x 8 pairs per thread (k_scan_tiles_ws16)
+  bool tc;      // ... on the tensor cores (tc_kernels.cu: k_scan_tiles_tc)
   bool packed, wide;  // copied from the ScanConfig
 };
 ScanChoice choose_scan_kernel(const ScanConfig& cfg, const SearchState& s, uint32_t live_upper_bound, bool window,
@@ -181,6 +183,23 @@ int launch_scan_tiles(const ScanChoice& choice, SearchState s, const float* d_ba
                       const uint32_t* d_batch_rows, const uint32_t* d_batch_slots, const uint32_t* d_sel,
                       uint32_t live_upper_bound, const uint32_t* d_nbr_index, uint32_t k_begin, uint32_t k_end,
                       uint32_t rotation, bool pruning, bool symmetric, cudaStream_t stream, const char** error);
+
+// ---- tensor-core tile kernel (tc_kernels.cu; experiment behind the option "tensor_cores")
+struct TcOperands {
+  const float *batch_hi, *batch_lo;    // the batch's rows split into tf32 parts (launch_gather_rows_split)
+  const float *rows_hi, *rows_lo;      // the matrix, split (launch_split_tf32)
+  const float *sorted_hi, *sorted_lo;  // its hash-sorted copy, split (window tiles)
+  uint64_t rows_padded;                // rows of each of the four neighbour arrays
+};
+int launch_split_tf32(const float* d_in, size_t floats, float* d_hi, float* d_lo, cudaStream_t stream);
+int launch_gather_rows_split(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel, uint32_t capacity_padded,
+                             float* d_hi, float* d_lo, cudaStream_t stream);
+int launch_scan_tiles_tc(SearchState s, const TcOperands& op, const uint32_t* d_batch_rows, const uint32_t* d_batch_slots,
+                         const uint32_t* d_sel, uint32_t live_upper_bound, const uint32_t* d_nbr_index, uint32_t k_begin,
+                         uint32_t k_end, bool pruning, bool symmetric, cudaStream_t stream, const char** error);
+// float32 matrix [n_rows x stride] as a tensor map with boxes of box_rows x box_cols, 128-byte swizzle
+// (box_cols * 4 = 128) or the 64-byte one (box_cols * 4 = 64); false when the driver lacks cuTensorMapEncodeTiled.  `map` is a CUtensorMap.
+bool make_row_map_boxed(void* map, const float* base, uint64_t n_rows, uint64_t stride, uint32_t box_cols, uint32_t box_rows);
 
 // Squared norms of the float32 rows (rows 0 .. n_rows; row n_rows is the zero row), for the
 // dot-product form d^2 = |a|^2 + |b|^2 - 2 a.b of the warp-specialised tile kernel.

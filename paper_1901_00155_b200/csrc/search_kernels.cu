@@ -47,7 +47,7 @@ __global__ void k_reset_search(SearchState s) {
   }
   if (i == 0) {
     *s.best = 0;
-    *s.counters = DeviceCounters{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    *s.counters = DeviceCounters{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   }
 }
 
@@ -2431,6 +2431,19 @@ bool make_row_map(CUtensorMap* map, const float* base, uint64_t n_rows, uint64_t
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool make_row_map_boxed(void* map, const float* base, uint64_t n_rows, uint64_t stride, uint32_t box_cols, uint32_t box_rows) {
+  PFN_cuTensorMapEncodeTiled encode = tensor_map_encoder();
+  if (!encode) return false;
+  const cuuint64_t dims[2] = {stride, n_rows};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(stride) * sizeof(float)};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t elem[2] = {1, 1};
+  const CUtensorMapSwizzle swizzle = box_cols * 4 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+  return encode(static_cast<CUtensorMap*>(map), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+                box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 ScanChoice choose_scan_kernel(const ScanConfig& cfg, const SearchState& s, uint32_t live_upper_bound, bool window,
                               bool pruning, bool dot_form) {
   ScanChoice c{};
@@ -2451,6 +2464,9 @@ ScanChoice choose_scan_kernel(const ScanConfig& cfg, const SearchState& s, uint3
   c.tma = c.ws && tma_ok && (!window || (c.dot && s.rows_sorted != nullptr));
   // the dot form on 256-candidate tiles, 16 x 8 pairs per thread, while the batch fills them
   c.tile16 = c.dot && c.tma && cfg.tile16 && live_upper_bound > 192;
+  // ... or on the tensor cores, while it fills 128-candidate tiles (the engine keeps the split operands then)
+  c.tc = c.dot && c.tma && cfg.tensor_cores && live_upper_bound > 96;
+  if (c.tc) c.tile16 = false;
   return c;
 }
 

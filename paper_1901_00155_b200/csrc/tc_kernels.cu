@@ -1,0 +1,548 @@
+// The dot-product form of the tile kernel on the 5th-generation tensor cores (tcgen05 + TMEM).
+//
+// EXPERIMENT, behind the option "tensor_cores" (dot_form = 3 / 4); the CUDA-core kernels of
+// search_kernels.cu stay the default and stay the FP32 roofline evidence.  The dot form of the
+// distance, d^2 = |a|^2 + |b|^2 - 2 a.b, is a dense contraction: a tile of 128 candidates x 256
+// neighbours is the matrix product A (128 x n) . B^T (n x 256).  Float32 inputs do not fit the
+// tensor cores' TF32 format (10 explicit mantissa bits), so every row is split once into
+//     x = hi + lo,   hi = x with the low 13 mantissa bits cleared,   lo = (x - hi) likewise cleared,
+// (x - hi is exact in float32) and a tile is THREE tf32 MMAs per 8 columns,
+//     A_hi.B_hi + A_hi.B_lo + A_lo.B_hi        (the missing lo.lo term is below 2^-20 |a||b|),
+// accumulated in float32 in tensor memory.  The split and the accumulation leave an absolute
+// error of the same kind as the CUDA-core dot form's, about three times its bound; the engine
+// widens the discard band accordingly (SearchState::margin_abs) and the float64 decision at the
+// end of a pass is unchanged — positions stay those of the reference.
+//
+// Kernel anatomy (one CTA per SM, 256 threads, no CTA-wide barrier after the set-up):
+//   warp 3      per tile, one tile ahead: the candidates' thresholds and the neighbours' rows / bounds / norms;
+//   warp 0      producer: per 16-column stage four TMA boxes (A_hi, A_lo: 128 rows; B_hi, B_lo:
+//               256 rows; 64-byte swizzle; 48 KB) onto a "full" mbarrier, four stages deep;
+//   warp 1      MMA issuer: one elected lane issues 6 tcgen05.mma.kind::tf32 per stage (M 128,
+//               N 256, K 8; operands straight from the swizzled shared-memory tiles through
+//               matrix descriptors) and tcgen05.commit's the stage back to the producer; the
+//               accumulators of tile t+1 go to the other half of tensor memory (2 x 256 columns);
+//   warp 2      allocates / frees the 512 TMEM columns;
+//   warps 4..7  epilogue: thread m of the warpgroup owns candidate m (TMEM lane m); it reads its
+//               256 accumulators with tcgen05.ld (32 columns at a time), forms the distances and
+//               keeps the smallest — no shuffle, no shared-memory reduction; one atomicMin per
+//               candidate per tile, plus the symmetric updates of the neighbours.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "kernels.hpp"
+
+namespace tsdd_b200 {
+
+namespace {
+
+constexpr int kM = 128;                    // candidates per tile = TMEM lanes
+constexpr int kN = 256;                    // neighbours per tile = accumulator columns
+#ifndef TSDD_TC_STAGE_COLS
+#define TSDD_TC_STAGE_COLS 16
+#endif
+constexpr int kStageCols = TSDD_TC_STAGE_COLS;  // columns per stage: one swizzled row piece (16: 64-byte swizzle, 32: 128-byte)
+constexpr int kUmmaK = 8;                  // columns per tf32 MMA
+constexpr int kTcStages = kStageCols == 16 ? 4 : 2;  // (a stage of 16 columns is 48 KB, of 32 columns 96 KB)
+constexpr int kABytes = kM * kStageCols * 4;   // 16 KB
+constexpr int kBBytes = kN * kStageCols * 4;   // 32 KB
+constexpr int kTcStageBytes = 2 * kABytes + 2 * kBBytes;  // A_hi | A_lo | B_hi | B_lo = 96 KB
+constexpr int kTcThreads = 256;
+constexpr uint32_t kTmemCols = 512;        // two accumulator sets of 256 columns
+
+struct alignas(16) TcMeta {
+  float thr[kM];
+  float nub[kN];
+  uint32_t jrow[kN];
+  float nnorm[kN];
+  unsigned long long calls;
+  uint32_t valid;   // neighbour slots of the tile that hold a row
+  uint32_t stop;    // no tile follows: every candidate of the CTA is dead
+  uint32_t slot0;   // first neighbour slot of the tile
+  uint32_t pad[3];
+};
+
+struct SharedTc {
+  alignas(1024) unsigned char stages[kTcStages][kTcStageBytes];
+  TcMeta meta[2];
+  uint32_t cand[kM];
+  float cnorm[kM];
+  float loc[kM];
+  unsigned long long full[kTcStages], empty[kTcStages], tmem_full[2], tmem_empty[2], meta_full[2], meta_empty[2];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ uint32_t gap(uint32_t a, uint32_t b) { return a > b ? a - b : b - a; }
+__device__ __forceinline__ uint64_t ld_key(const uint64_t* p) {
+  return __ldcg(reinterpret_cast<const unsigned long long*>(p));
+}
+
+__device__ __forceinline__ void bar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void bar_arrive(unsigned long long* bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// Bounded wait: a pipeline that never completes traps (after kWaitLimitNs of wall time) instead
+// of hanging the GPU; `tag` says which wait it was.
+constexpr unsigned long long kWaitLimitNs = 2000000000ull;
+__device__ __noinline__ void bar_wait_slow(unsigned long long* bar, uint32_t parity, int tag) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t done = 0;
+    for (int spin = 0; spin < 1024 && !done; ++spin) {
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+          : "=r"(done)
+          : "r"(smem_u32(bar)), "r"(parity)
+          : "memory");
+    }
+    if (done) return;
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (t1 - t0 > kWaitLimitNs) {
+      printf("k_scan_tiles_tc: wait %d timed out (parity %u, block %u,%u thread %u)\n", tag, parity, blockIdx.x, blockIdx.y,
+             threadIdx.x);
+      __trap();
+    }
+  }
+}
+__device__ __forceinline__ void bar_wait(unsigned long long* bar, uint32_t parity, int tag) {
+  uint32_t done = 0;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  if (!done) bar_wait_slow(bar, parity, tag);
+}
+__device__ __forceinline__ void tma_box(void* dst, const CUtensorMap* map, uint32_t col, uint32_t row, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(col), "r"(row), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Shared-memory matrix descriptor of a K-major tile whose rows are kStageCols * 4 bytes (64 or 128)
+// with the swizzle of that width (what the TMA boxes write): start address >> 4 | leading offset
+// (unused for swizzled K-major) | stride between 8-row groups = 8 rows | descriptor version 1 |
+// layout type (SWIZZLE_64B = 4, SWIZZLE_128B = 2).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t smem_addr) {
+  constexpr uint64_t kGroupBytes = 8 * kStageCols * 4;
+  constexpr uint64_t kLayout = kStageCols == 16 ? 4 : 2;
+  return static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4) | (1ull << 16) | ((kGroupBytes >> 4) << 32) | (1ull << 46) |
+         (kLayout << 61);
+}
+// Instruction descriptor: D float32, A / B tf32, both K-major, N = 256, M = 128.
+constexpr uint32_t kInstrDesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(kN >> 3) << 17) |
+                                (static_cast<uint32_t>(kM >> 4) << 24);
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(desc_a), "l"(desc_b), "r"(kInstrDesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(unsigned long long* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, "
+      "%18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]),
+        "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+        "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
+        "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+struct TcArgs {
+  const uint32_t* batch_rows;
+  const uint32_t* batch_slots;
+  const uint32_t* sel;
+  const uint32_t* nbr_index;  // hash-sorted row list (window mode) or nullptr
+  uint32_t u_begin, u_end;    // 256-row neighbour tiles of this launch
+  int tiles_per_cta;
+  int pruning;
+};
+
+template <bool kSymmetric>
+__global__ void __launch_bounds__(kTcThreads, 1)
+k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map_a_hi,
+                const __grid_constant__ CUtensorMap map_a_lo, const __grid_constant__ CUtensorMap map_b_hi,
+                const __grid_constant__ CUtensorMap map_b_lo) {
+  extern __shared__ unsigned char smem_raw[];
+  // (the 128-byte swizzle wants 1024-byte aligned tiles: align by hand, the launch adds the slack)
+  SharedTc& sh = *reinterpret_cast<SharedTc*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+
+  const uint32_t count = a.sel[0];
+  // (candidate tiles are the FAST grid dimension: the CTAs that run side by side walk the same
+  // neighbour tiles — in a covering scan literally, in a window round nearly — so those come from L2)
+  const uint32_t cand0 = blockIdx.x * kM;
+  if (cand0 >= count) return;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float inf = __uint_as_float(kInfBits);
+
+  if (tid < kM) {
+    const uint32_t row = (cand0 + tid < count) ? a.batch_rows[cand0 + tid] : 0xFFFFFFFFu;
+    if (row != 0xFFFFFFFFu) TSDD_BOUND(row, s.n_rows);
+    sh.cand[tid] = row;
+    sh.loc[tid] = inf;
+    sh.cnorm[tid] = row != 0xFFFFFFFFu ? s.row_norms[row] : 0.f;
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kTcStages; ++i) bar_init(&sh.full[i], 1), bar_init(&sh.empty[i], 1);
+    for (int i = 0; i < 2; ++i) {
+      bar_init(&sh.tmem_full[i], 1);
+      bar_init(&sh.tmem_empty[i], 4);   // the four epilogue warps
+      bar_init(&sh.meta_full[i], 1);
+      bar_init(&sh.meta_empty[i], 6);   // the four epilogue warps, the MMA warp and the producer
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {  // tensor memory: all 512 columns (one CTA per SM)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sh.tmem_base)), "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = sh.tmem_base;
+
+  const bool window = a.nbr_index != nullptr;
+  const uint32_t units = (s.n_rows + kN - 1) / kN;  // 256-row units of the (hash-sorted or positional) row order
+  const uint32_t chunks = s.stride / kStageCols;
+  const uint32_t u_first = a.u_begin + blockIdx.y * a.tiles_per_cta;
+  const uint32_t n_tiles = u_first < a.u_end ? min(static_cast<uint32_t>(a.tiles_per_cta), a.u_end - u_first) : 0u;
+  const uint32_t centre = window ? a.batch_slots[min(cand0 + kM / 2, count - 1)] / kN : 0u;
+  // window mode: units around the candidate tile's own, alternating outwards; covering mode: unit u itself
+  auto slot0_of = [&](uint32_t u) -> uint32_t {
+    if (!window) return u * kN;
+    const uint32_t step = (u + 1) >> 1;
+    const uint32_t unit = (u & 1) ? (centre + step) % units : (centre + units - step % units) % units;
+    return unit * kN;
+  };
+
+  if (warp == 3) {
+    // ================================================================ metadata, one tile ahead of the streams
+    const uint64_t best = a.pruning ? *s.best : 0ull;
+    unsigned long long calls_total = 0, tiles_total = 0, live_total = 0;
+    for (uint32_t ti = 0; ti <= n_tiles; ++ti) {
+      const uint32_t m = ti & 1, use = ti >> 1;
+      TcMeta& meta = sh.meta[m];
+      if (use >= 1) bar_wait(&sh.meta_empty[m], (use - 1) & 1, 1);
+      bool any_live = false;
+      unsigned long long calls = 0;
+      uint32_t slot0 = 0, valid = 0;
+      if (ti < n_tiles) {
+        slot0 = slot0_of(u_first + ti);
+        valid = slot0 < s.n_rows ? min(static_cast<uint32_t>(kN), s.n_rows - slot0) : 0u;
+#pragma unroll
+        for (int q = 0; q < kM / 32; ++q) {
+          const uint32_t r = lane + 32 * q, row = sh.cand[r];
+          float thr = -1.f;
+          if (row != 0xFFFFFFFFu) {
+            if (!a.pruning) {
+              thr = inf;
+            } else {
+              const float bound = fminf(__uint_as_float(key_bits(ld_key(s.nn + row))), sh.loc[r]);
+              if (!dead_bound(bound, best, s.margin, s.margin_abs, s.margin_q)) thr = bound;
+            }
+          }
+          meta.thr[r] = thr;
+          if (thr >= 0.f) {
+            any_live = true;
+            live_total += 1;
+            uint32_t overlap = 0;
+            if (!window) {  // (window tiles: the epilogue counts the self-match pairs)
+              const uint32_t z0 = row >= s.n - 1 ? row - (s.n - 1) : 0, z1 = row + s.n;
+              const uint32_t o0 = max(slot0, z0), o1 = min(slot0 + valid, z1);
+              overlap = o1 > o0 ? o1 - o0 : 0;
+            }
+            calls += valid - overlap;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kN / 32; ++q) {
+          const uint32_t e = lane + 32 * q, slot = slot0 + e;
+          uint32_t j = 0xFFFFFFFFu;
+          if (slot < s.n_rows) j = window ? a.nbr_index[slot] : slot;
+          if (j != 0xFFFFFFFFu) TSDD_BOUND(j, s.n_rows);
+          meta.jrow[e] = j;
+          meta.nub[e] = j != 0xFFFFFFFFu ? __uint_as_float(key_bits(ld_key(s.nn + j))) : -1.f;
+          meta.nnorm[e] = j != 0xFFFFFFFFu ? s.row_norms[j] : 0.f;
+        }
+        any_live = __any_sync(0xFFFFFFFFu, any_live);
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) calls += __shfl_xor_sync(0xFFFFFFFFu, calls, d);
+      }
+      if (lane == 0) {
+        meta.calls = calls;
+        meta.valid = valid;
+        meta.slot0 = slot0;
+        meta.stop = any_live ? 0u : 1u;  // (also the slot after the last tile)
+      }
+      __syncwarp();
+      if (lane == 0) bar_arrive(&sh.meta_full[m]);
+      if (!any_live) break;
+      calls_total += calls;
+      tiles_total += 1;
+    }
+    if (lane == 0) {
+      if (calls_total) atomicAdd(&s.counters->calls, calls_total);
+      if (tiles_total) atomicAdd(&s.counters->tiles, tiles_total);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) live_total += __shfl_xor_sync(0xFFFFFFFFu, live_total, d);
+    if (lane == 0 && live_total) atomicAdd(&s.counters->tile_live, live_total);
+  } else if (warp == 0) {
+    // ================================================================ producer: the TMA streams
+    uint32_t seq = 0;
+    for (uint32_t ti = 0;; ++ti) {
+      const uint32_t m = ti & 1;
+      bar_wait(&sh.meta_full[m], (ti >> 1) & 1, 2);
+      const bool stop = *reinterpret_cast<volatile uint32_t*>(&sh.meta[m].stop) != 0;
+      const uint32_t slot0 = *reinterpret_cast<volatile uint32_t*>(&sh.meta[m].slot0);
+      __syncwarp();
+      if (lane == 0) bar_arrive(&sh.meta_empty[m]);
+      if (stop) break;
+      for (uint32_t c = 0; c < chunks; ++c) {
+        const uint32_t st = seq % kTcStages, round = seq / kTcStages;
+        if (round >= 1) bar_wait(&sh.empty[st], (round - 1) & 1, 3);
+        if (lane == 0) {
+          bar_expect_tx(&sh.full[st], kTcStageBytes);
+          unsigned char* dst = sh.stages[st];
+          const uint32_t col = c * kStageCols;
+          tma_box(dst, &map_a_hi, col, cand0, &sh.full[st]);
+          tma_box(dst + kABytes, &map_a_lo, col, cand0, &sh.full[st]);
+          tma_box(dst + 2 * kABytes, &map_b_hi, col, slot0, &sh.full[st]);
+          tma_box(dst + 2 * kABytes + kBBytes, &map_b_lo, col, slot0, &sh.full[st]);
+        }
+        ++seq;
+      }
+    }
+  } else if (warp == 1) {
+    // ================================================================ MMA issuer
+    uint32_t seq = 0;
+    for (uint32_t ti = 0;; ++ti) {
+      const uint32_t m = ti & 1, buf = ti & 1;
+      bar_wait(&sh.meta_full[m], (ti >> 1) & 1, 4);
+      const bool stop = *reinterpret_cast<volatile uint32_t*>(&sh.meta[m].stop) != 0;
+      __syncwarp();
+      if (lane == 0) bar_arrive(&sh.meta_empty[m]);
+      if (stop) break;
+      if (ti >= 2) bar_wait(&sh.tmem_empty[buf], ((ti >> 1) - 1) & 1, 5);  // the epilogue has drained this accumulator set
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t tmem_d = tmem_base + buf * kN;
+      for (uint32_t c = 0; c < chunks; ++c) {
+        const uint32_t st = seq % kTcStages, round = seq / kTcStages;
+        bar_wait(&sh.full[st], round & 1, 6);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
+          const uint32_t base = smem_u32(sh.stages[st]);
+          const uint64_t a_hi = umma_desc(base), a_lo = umma_desc(base + kABytes);
+          const uint64_t b_hi = umma_desc(base + 2 * kABytes), b_lo = umma_desc(base + 2 * kABytes + kBBytes);
+#pragma unroll
+          for (uint32_t k = 0; k < kStageCols / kUmmaK; ++k) {
+            const uint64_t step = static_cast<uint64_t>((k * kUmmaK * 4) >> 4);  // 32 bytes along the swizzled row piece
+            umma_tf32(tmem_d, a_hi + step, b_hi + step, (c | k) != 0 ? 1u : 0u);
+            umma_tf32(tmem_d, a_hi + step, b_lo + step, 1u);
+            umma_tf32(tmem_d, a_lo + step, b_hi + step, 1u);
+          }
+          umma_commit(&sh.empty[st]);                          // the stage is free once these MMAs have read it
+          if (c + 1 == chunks) umma_commit(&sh.tmem_full[buf]);  // ... and the tile's accumulators are complete
+        }
+        __syncwarp();
+        ++seq;
+      }
+    }
+  } else if (warp >= 4) {
+    // ================================================================ epilogue: thread = candidate = TMEM lane
+    const uint32_t mrow = tid - 128;                 // candidate (TMEM lane) of this thread
+    const uint32_t lane_base = (warp & 3u) * 32u;    // the TMEM lanes this warp may read
+    const uint32_t row = sh.cand[mrow];
+    const float cn = sh.cnorm[mrow];
+    const float d_floor = 0.5f * s.margin_abs;
+    unsigned long long tiles_done = 0, useful = 0;
+    uint32_t overlap_total = 0;
+    for (uint32_t ti = 0;; ++ti) {
+      const uint32_t m = ti & 1, buf = ti & 1;
+      bar_wait(&sh.meta_full[m], (ti >> 1) & 1, 7);
+      TcMeta& meta = sh.meta[m];
+      if (*reinterpret_cast<volatile uint32_t*>(&meta.stop) != 0) {
+        __syncwarp();
+        if (lane == 0) bar_arrive(&sh.meta_empty[m]);
+        break;
+      }
+      const float thr = meta.thr[mrow];
+      bar_wait(&sh.tmem_full[buf], (ti >> 1) & 1, 8);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t d_min = 0xFFFFFFFFu, j_min = 0xFFFFFFFFu;
+      const bool taking_part = thr >= 0.f && row != 0xFFFFFFFFu;
+#pragma unroll 1
+      for (uint32_t cc = 0; cc < kN / 32; ++cc) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + (lane_base << 16) + buf * kN + cc * 32, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const uint32_t n = cc * 32 + i;
+          const float nub = kSymmetric ? meta.nub[n] : -1.f;
+          const float d = fmaxf(fmaf(-2.f, __uint_as_float(v[i]), cn + meta.nnorm[n]), d_floor);
+          if (taking_part && (d <= thr || d < nub)) {
+            const uint32_t j = meta.jrow[n];
+            if (j != 0xFFFFFFFFu && gap(row, j) >= s.n) {
+              const uint32_t bits = __float_as_uint(d);
+              if (d <= thr && (bits < d_min || (bits == d_min && j < j_min))) d_min = bits, j_min = j;
+              if (d < nub) {
+                TSDD_BOUND(j, s.n_rows);
+                atomicMin(as_ull(s.nn + j), static_cast<unsigned long long>(nn_key(bits, row)));
+              }
+            }
+          }
+        }
+        if (window && taking_part) {  // self-match pairs of a window tile (the producer counted live x valid)
+#pragma unroll 8
+          for (int i = 0; i < 32; ++i) overlap_total += gap(row, meta.jrow[cc * 32 + i]) < s.n ? 1u : 0u;
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) bar_arrive(&sh.tmem_empty[buf]);
+      if (j_min != 0xFFFFFFFFu) {
+        TSDD_BOUND(row, s.n_rows);
+        atomicMin(as_ull(s.nn + row), static_cast<unsigned long long>(nn_key(d_min, j_min)));
+        sh.loc[mrow] = fminf(sh.loc[mrow], __uint_as_float(d_min));
+      }
+      useful += taking_part ? static_cast<unsigned long long>(meta.valid) * s.n : 0ull;
+      tiles_done += 1;
+      __syncwarp();
+      if (lane == 0) bar_arrive(&sh.meta_empty[m]);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      useful += __shfl_xor_sync(0xFFFFFFFFu, useful, d);
+      overlap_total += __shfl_xor_sync(0xFFFFFFFFu, overlap_total, d);
+    }
+    if (lane == 0) {
+      if (warp == 4 && tiles_done) {
+        const unsigned long long terms = tiles_done * kM * kN * static_cast<unsigned long long>(s.stride);
+        atomicAdd(&s.counters->terms, terms);
+        atomicAdd(&s.counters->tile_terms, terms);
+        atomicAdd(&s.counters->dot_terms, terms);
+        atomicAdd(&s.counters->tc_terms, terms);
+      }
+      if (useful) atomicAdd(&s.counters->useful_terms, useful);
+      if (overlap_total) atomicAdd(&s.counters->calls, ~static_cast<unsigned long long>(overlap_total) + 1ull);
+    }
+  }
+
+  // ---- teardown: every role is done with tensor memory before it is freed
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
+  }
+}
+
+// x = hi + lo with both parts exactly representable in tf32 (low 13 mantissa bits clear)
+__global__ void __launch_bounds__(256)
+k_split_tf32(const float4* __restrict__ in, size_t quads, float4* __restrict__ hi, float4* __restrict__ lo) {
+  const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= quads) return;
+  const float4 x = in[i];
+  auto top = [](float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); };
+  const float4 h = make_float4(top(x.x), top(x.y), top(x.z), top(x.w));
+  hi[i] = h;
+  lo[i] = make_float4(top(x.x - h.x), top(x.y - h.y), top(x.z - h.z), top(x.w - h.w));
+}
+
+// The batch's rows, split the same way, dense in batch order; rows past the batch size are zero.
+__global__ void __launch_bounds__(256)
+k_gather_rows_split(SearchState s, const uint32_t* __restrict__ batch_rows, const uint32_t* __restrict__ sel,
+                    uint32_t capacity_padded, float* __restrict__ hi, float* __restrict__ lo) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (r >= capacity_padded) return;
+  const uint32_t count = sel[0];
+  if (r >= (count + kM - 1) / kM * kM) return;  // only the tiles the scan will touch
+  float4* dh = reinterpret_cast<float4*>(hi + static_cast<size_t>(r) * s.stride);
+  float4* dl = reinterpret_cast<float4*>(lo + static_cast<size_t>(r) * s.stride);
+  auto top = [](float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); };
+  if (r < count) {
+    TSDD_BOUND(batch_rows[r], s.n_rows);
+    const float4* src = reinterpret_cast<const float4*>(s.rows + static_cast<size_t>(batch_rows[r]) * s.stride);
+    for (uint32_t c = lane; c < s.stride / 4; c += 32) {
+      const float4 x = __ldg(src + c);
+      const float4 h = make_float4(top(x.x), top(x.y), top(x.z), top(x.w));
+      dh[c] = h;
+      dl[c] = make_float4(top(x.x - h.x), top(x.y - h.y), top(x.z - h.z), top(x.w - h.w));
+    }
+  } else {
+    for (uint32_t c = lane; c < s.stride / 4; c += 32) dh[c] = dl[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+inline unsigned blocks_of(size_t items, unsigned per_block) { return static_cast<unsigned>((items + per_block - 1) / per_block); }
+
+}  // namespace
+
+int launch_split_tf32(const float* d_in, size_t floats, float* d_hi, float* d_lo, cudaStream_t stream) {
+  const size_t quads = floats / 4;
+  k_split_tf32<<<blocks_of(quads, 256), 256, 0, stream>>>(reinterpret_cast<const float4*>(d_in), quads,
+                                                         reinterpret_cast<float4*>(d_hi), reinterpret_cast<float4*>(d_lo));
+  return 1;
+}
+
+int launch_gather_rows_split(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel, uint32_t capacity_padded,
+                             float* d_hi, float* d_lo, cudaStream_t stream) {
+  k_gather_rows_split<<<blocks_of(static_cast<size_t>(capacity_padded) * 32, 256), 256, 0, stream>>>(
+      s, d_batch_rows, d_sel, capacity_padded, d_hi, d_lo);
+  return 1;
+}
+
+int launch_scan_tiles_tc(SearchState s, const TcOperands& op, const uint32_t* d_batch_rows, const uint32_t* d_batch_slots,
+                         const uint32_t* d_sel, uint32_t live_upper_bound, const uint32_t* d_nbr_index, uint32_t k_begin,
+                         uint32_t k_end, bool pruning, bool symmetric, cudaStream_t stream, const char** error) {
+  if (error) *error = nullptr;
+  if (k_end <= k_begin || live_upper_bound == 0) return 0;
+  // 128-row units of the plan -> 256-row tiles (a half tile of overlap with the neighbouring segment is harmless)
+  const uint32_t u_begin = k_begin / 2, u_end = (k_end + 1) / 2;
+  const uint32_t cand_tiles = (live_upper_bound + kM - 1) / kM;
+  const uint64_t tiles = u_end - u_begin;
+  const uint64_t want = tiles * cand_tiles / (148ull * 8ull);
+  const int tiles_per_cta = static_cast<int>(want < 1 ? 1 : want > 16 ? 16 : want);
+  const bool window = d_nbr_index != nullptr;
+  CUtensorMap map_a_hi{}, map_a_lo{}, map_b_hi{}, map_b_lo{};
+  const float* b_hi = window ? op.sorted_hi : op.rows_hi;
+  const float* b_lo = window ? op.sorted_lo : op.rows_lo;
+  const uint64_t b_rows = op.rows_padded;  // (a box that reaches past the last row is zero-filled by the TMA unit)
+  if (!make_row_map_boxed(&map_a_hi, op.batch_hi, static_cast<uint64_t>(cand_tiles) * kM, s.stride, kStageCols, kM) ||
+      !make_row_map_boxed(&map_a_lo, op.batch_lo, static_cast<uint64_t>(cand_tiles) * kM, s.stride, kStageCols, kM) ||
+      !make_row_map_boxed(&map_b_hi, b_hi, b_rows, s.stride, kStageCols, kN) ||
+      !make_row_map_boxed(&map_b_lo, b_lo, b_rows, s.stride, kStageCols, kN)) {
+    if (error) *error = "cuTensorMapEncodeTiled failed (tensor-core tile kernel)";
+    return 0;
+  }
+  TcArgs a{d_batch_rows, d_batch_slots, d_sel, d_nbr_index, u_begin, u_end, tiles_per_cta, pruning ? 1 : 0};
+  dim3 grid(cand_tiles, static_cast<unsigned>((tiles + tiles_per_cta - 1) / tiles_per_cta));
+  const int smem = static_cast<int>(sizeof(SharedTc)) + 1024;
+  if (symmetric) {
+    cudaFuncSetAttribute(k_scan_tiles_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_scan_tiles_tc<true><<<grid, kTcThreads, smem, stream>>>(s, a, map_a_hi, map_a_lo, map_b_hi, map_b_lo);
+  } else {
+    cudaFuncSetAttribute(k_scan_tiles_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_scan_tiles_tc<false><<<grid, kTcThreads, smem, stream>>>(s, a, map_a_hi, map_a_lo, map_b_hi, map_b_lo);
+  }
+  return 1;
+}
+
+}  // namespace tsdd_b200

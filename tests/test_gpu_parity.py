@@ -768,6 +768,38 @@ def test_dot_product_form_on_256_candidate_tiles(ctx, chk, seed, kind, n):
     np.testing.assert_allclose(again[1], dist, rtol=1e-9)
 
 
+@pytest.mark.parametrize("seed,kind,n", FUZZ[::3], ids=[f"{k}-n{n}" for _, k, n in FUZZ[::3]])
+def test_dot_product_form_on_the_tensor_cores(ctx, chk, seed, kind, n):
+    """k_scan_tiles_tc (dot_form = 4: tcgen05.mma kind::tf32 on rows split into two tf32 parts,
+    accumulators in tensor memory; csrc/tc_kernels.cu), forced from the first launch on batches
+    that fill 128-candidate tiles: the wider band and the float64 decision must still give the
+    reference's answer, and the answer of the CUDA-core dot form."""
+    rng = np.random.default_rng(13000 + seed)
+    m = int(rng.integers(2 * n + 5000, 2 * n + 9000))
+    w = int(rng.integers(1, min(n, 8) + 1))
+    a = int(rng.integers(2, 7))
+    k = int(rng.integers(1, 4))
+    x = _fuzz_series(rng, kind, m)
+    for name, value in [("dot_form", 4), ("lower_bound", 0), ("first_batch", 4096)]:
+        ctx.set_option(name, value)
+    try:
+        ctx.prepare(x, n, w, a)
+        pos, dist = ctx.search(k)
+        st = ctx.stats()
+        ctx.set_option("dot_form", 2)
+        again = ctx.search(k)
+    finally:
+        for name, value in [("dot_form", 1), ("lower_bound", 1), ("first_batch", 128)]:
+            ctx.set_option(name, value)
+    want = chk.topk(x, n, w, a, k)
+    assert_discords_match(chk, x, n, pos, dist, want)
+    assert st["scan_kernel_tc_launches"] > 0 and 0 < st["scan_kernel_tc_terms"] <= st["scan_kernel_dot_terms"]
+    assert_discords_match(chk, x, n, again[0], again[1], want)
+    if n >= 8:  # (tiny n: exact ties everywhere, and which of the tied rows gets scanned to the end depends on the path)
+        assert again[0] == pos
+        np.testing.assert_allclose(again[1], dist, rtol=1e-9)  # both decided in float64
+
+
 def _hard_series(kind, m, rng):
     if kind == "spikes":      # a few huge outliers: windows whose energy sits in one sample
         x = rng.standard_normal(m).astype(np.float32)
@@ -1123,7 +1155,7 @@ def test_soak_random_series_shapes_and_options(ctx, chk, case):
         x = np.cumsum(rng.standard_normal(m)).astype(np.float32)
     else:
         x = (np.sin(2 * np.pi * np.arange(m) / rng.integers(20, 200)) + 0.3 * rng.standard_normal(m)).astype(np.float32)
-    opts = {"dot_form": int(rng.choice([1, 2])), "first_batch": int(rng.choice([128, 4096])),
+    opts = {"dot_form": int(rng.choice([1, 2, 3, 4])), "first_batch": int(rng.choice([128, 4096])),
             "lower_bound": int(rng.choice([0, 1])), "filter_in_ws": int(rng.choice([0, 1])),
             "propagate": int(rng.choice([0, 2, 8])), "propagate_every": int(rng.choice([0, 1, 2]))}
     defaults = {"dot_form": 1, "first_batch": 128, "lower_bound": 1, "filter_in_ws": 0, "propagate": 8,
@@ -1151,7 +1183,7 @@ def test_checked_build_runs_the_edge_shapes():
     dbg = os.path.join(_ROOT, "paper_1901_00155_b200", "_lib", "libtsdd_cuda_dbg.so")
     assert os.path.exists(dbg), "build it with python -m paper_1901_00155_b200.build"
     expr = ("randomised_small_cases or dot_product_form_matches or 256_candidate or filter_on_the_producer_warpgroup_matches"
-            " or group_of_ranks or soak_random or smallest_feasible or long_subsequences or topk_matches")
+            " or group_of_ranks or soak_random or smallest_feasible or long_subsequences or topk_matches or on_the_tensor_cores")
     p = subprocess.run([sys.executable, "-m", "pytest", os.path.join(_ROOT, "tests", "test_gpu_parity.py"), "-x", "-q",
                         "-m", "gpu", "-k", expr, "-p", "no:cacheprovider"],
                        env=dict(os.environ, TSDD_CUDA_LIB=dbg), capture_output=True, text=True, timeout=1500)
