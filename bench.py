@@ -353,6 +353,10 @@ def run_cuda_arm(args) -> None:
         rp["frac"] = rp["achieved"] / rp["peak"] if rp["achieved"] else None
         if world == 1 and not args.no_secondary and args.workload != 4:
             line["other_workloads"] = {"cfg4": time_other_workload(ctx, 4, local, golden_all)}
+        if world == 1 and not args.no_secondary and not any(o.startswith("dot_form") for o in args.opt):
+            # the tensor-core experiment (csrc/tc_kernels.cu) on the SAME workload; the default above is the CUDA-core path
+            line["tensor_core_experiment"] = time_other_workload(ctx, args.workload, local, golden_all, options={"dot_form": 3})
+            ctx.set_option("dot_form", 1)
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_reference_run(args.workload, x, w)
             line["cpu_baseline"] = {key: cb[key] for key in ("value", "unit", "cores", "kind", "sample",
@@ -395,15 +399,18 @@ def time_same_input(ctx, sample: np.ndarray, w, device: int, repeats: int = 3) -
     return {"topk_time_s": statistics.median(resident), "e2e_topk_time_s": statistics.median(e2e), "positions": pos}
 
 
-def time_other_workload(ctx, cfg: int, device: int, golden: dict, repeats: int = 3) -> dict:
-    """A secondary figure on the same line: one more BASELINE.json workload, device-resident,
-    median of `repeats` complete top-k searches (preparation + search, CUDA events)."""
+def time_other_workload(ctx, cfg: int, device: int, golden: dict, repeats: int = 3, options: dict | None = None) -> dict:
+    """A secondary figure on the same line: one more BASELINE.json workload (or the same one under
+    other engine options), device-resident, median of `repeats` complete top-k searches
+    (preparation + search, CUDA events)."""
     import torch
 
     w, x = workload_inputs(cfg)
     dev = torch.from_numpy(x).to(f"cuda:{device}")
     stream = torch.cuda.current_stream()
     times, pos, st = [], None, {}
+    for name, value in (options or {}).items():
+        ctx.set_option(name, value)
     for r in range(repeats + 1):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -415,9 +422,14 @@ def time_other_workload(ctx, cfg: int, device: int, golden: dict, repeats: int =
             times.append(e0.elapsed_time(e1) * 1e-3)
         st = ctx.stats()
     rec = golden.get(f"cfg{cfg}")
-    return {"m": w.m, "n": w.n, "k": w.k, "topk_time_s": statistics.median(times), "runs": repeats,
-            "prep_ms": st["prep_ms"], "search_ms": st["search_ms"], "calls": st["calls"],
-            "matches_golden": (pos == rec["oracle"]["positions"]) if rec else None}
+    out = {"m": w.m, "n": w.n, "k": w.k, "topk_time_s": statistics.median(times), "runs": repeats,
+           "prep_ms": st["prep_ms"], "search_ms": st["search_ms"], "calls": st["calls"],
+           "matches_golden": (pos == rec["oracle"]["positions"]) if rec else None}
+    if options:
+        out.update({"options": options, "scan_kernel_ms": st["scan_kernel_ms"],
+                    "tensor_core_launches": st["scan_kernel_tc_launches"],
+                    "tensor_core_share_of_terms": st["scan_kernel_tc_terms"] / max(1, st["scan_kernel_terms"])})
+    return out
 
 
 def _measured_peak(key: str, fallback: float):

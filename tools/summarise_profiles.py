@@ -79,5 +79,76 @@ def full(src, dst):
     print(json.dumps(summary))
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and sys.argv[1] in ("launches", "full"):
     {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
+
+
+def metrics(src, dst, workload):
+    """Per-kernel summary of an `ncu --metrics ... --csv` pass over one search: launches, time, DRAM bytes,
+    time-weighted pipe utilisations and the dominant stall reason.  Writes <dst>.json and <dst>.txt."""
+    rows = list(csv.reader(open(src, errors="replace")))
+    hdr = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    H = rows[hdr]
+    ci = {name: H.index(name) for name in ("ID", "Kernel Name", "Metric Name", "Metric Unit", "Metric Value", "Grid Size")}
+    launches = {}
+    for r in rows[hdr + 1:]:
+        if len(r) <= ci["Metric Value"]:
+            continue
+        rec = launches.setdefault(r[ci["ID"]], {"kernel": r[ci["Kernel Name"]].split("(")[0].replace("void ", "").replace("unnamed>::", ""),
+                                                "grid": r[ci["Grid Size"]]})
+        try:
+            value = float(r[ci["Metric Value"]].replace(",", ""))
+        except ValueError:
+            continue
+        unit = r[ci["Metric Unit"]]
+        scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "nsecond": 1e-6, "second": 1e3, "s": 1e3,
+                 "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "byte": 1.0}.get(unit, 1.0)
+        rec[r[ci["Metric Name"]]] = value * scale
+    agg = collections.OrderedDict()
+    for rec in launches.values():
+        a = agg.setdefault(rec["kernel"], {"launches": 0, "ms": 0.0, "dram_read": 0.0, "dram_write": 0.0, "weighted": collections.Counter(),
+                                           "longest": None})
+        ms = rec.get("gpu__time_duration.sum", 0.0)
+        a["launches"] += 1
+        a["ms"] += ms
+        a["dram_read"] += rec.get("dram__bytes_read.sum", 0.0)
+        a["dram_write"] += rec.get("dram__bytes_write.sum", 0.0)
+        for k, v in rec.items():
+            if k.endswith("pct_of_peak_sustained_active") or k.endswith("pct_of_peak_sustained_elapsed") or k.endswith(".ratio"):
+                a["weighted"][k] += v * ms
+        if a["longest"] is None or ms > a["longest"]["ms"]:
+            a["longest"] = {"ms": ms, "grid": rec["grid"], "dram_bytes": rec.get("dram__bytes_read.sum", 0.0) + rec.get("dram__bytes_write.sum", 0.0),
+                            "fma_pipe_pct": rec.get("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                            "dram_pct": rec.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")}
+    total = sum(a["ms"] for a in agg.values())
+    out = {"source": src, "workload": workload, "note": "ncu --metrics pass, cold-cache and serialised: compare shares, not absolutes",
+           "total_ms": total, "kernels": {}}
+    lines = [f"# {src}: per-kernel ncu metrics of one {workload} search (time-weighted averages; cold-cache, serialised)",
+             f"{'kernel':44} {'n':>4} {'ms':>8} {'share':>6} {'DRAM GB':>8} {'GB/s':>7} {'dram%':>6} {'fma%':>6} {'fp64%':>6} {'issue%':>6} {'occ%':>5}  top stall (per issue)"]
+    for name, a in sorted(agg.items(), key=lambda kv: -kv[1]["ms"]):
+        w = {k: v / a["ms"] for k, v in a["weighted"].items()} if a["ms"] else {}
+        stalls = {k.split("issue_stalled_")[1].replace("_per_issue_active.ratio", ""): v for k, v in w.items() if "issue_stalled" in k}
+        top = max(stalls.items(), key=lambda kv: kv[1]) if stalls else ("-", 0.0)
+        gb = (a["dram_read"] + a["dram_write"]) / 1e9
+        k = {"launches": a["launches"], "ms": a["ms"], "share": a["ms"] / total if total else 0.0, "dram_gb": gb,
+             "dram_gb_per_s": gb / (a["ms"] * 1e-3) if a["ms"] else 0.0,
+             "dram_pct_of_peak": w.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+             "fma_pipe_pct": w.get("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+             "fp64_pipe_pct": w.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+             "issue_active_pct": w.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+             "warps_active_pct": w.get("sm__warps_active.avg.pct_of_peak_sustained_active"),
+             "l1_throughput_pct": w.get("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+             "l2_throughput_pct": w.get("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+             "stalls_per_issue": dict(sorted(stalls.items(), key=lambda kv: -kv[1])[:4]), "top_stall": top[0], "longest_launch": a["longest"]}
+        out["kernels"][name] = k
+        f = lambda v: f"{v:6.1f}" if v is not None else "     -"
+        lines.append(f"{name[:44]:44} {a['launches']:4d} {a['ms']:8.3f} {100 * k['share']:5.1f}% {gb:8.3f} {k['dram_gb_per_s']:7.0f} "
+                     f"{f(k['dram_pct_of_peak'])} {f(k['fma_pipe_pct'])} {f(k['fp64_pipe_pct'])} {f(k['issue_active_pct'])} "
+                     f"{(k['warps_active_pct'] or 0):5.1f}  {top[0]} {top[1]:.2f}")
+    json.dump(out, open(dst + ".json", "w"), indent=1)
+    open(dst + ".txt", "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "metrics":
+    metrics(sys.argv[2], sys.argv[3], sys.argv[4])
