@@ -969,7 +969,7 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
             // consecutive rows too (tensor-map loads); skipped when memory is short
             const size_t floats = static_cast<size_t>(ctx->rows_padded) * ctx->stride;
             size_t free_b = 0, total_b = 0;
-            CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
+            if (ctx->matrix_sorted.count < floats) CUDA_OK(cudaMemGetInfo(&free_b, &total_b));  // (slow: only when it has to grow)
             if (ctx->matrix_sorted.count >= floats || free_b > floats * sizeof(float) + (size_t{2} << 30)) {
               ctx->matrix_sorted.alloc(floats);
               ctx->stats.kernel_launches += launch_permute_rows(ctx->matrix.ptr, ctx->sorted_row, ctx->rows,
@@ -981,9 +981,10 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
             // the tensor-core experiment: tf32 hi / lo parts of the matrix (and of its hash-sorted copy)
             const size_t floats = static_cast<size_t>(ctx->rows_padded) * ctx->stride;
             size_t free_b = 0, total_b = 0;
-            CUDA_OK(cudaMemGetInfo(&free_b, &total_b));
+            const bool have = ctx->matrix_hi.count >= floats && (!ctx->sorted_ready || ctx->sorted_hi.count >= floats);
+            if (!have) CUDA_OK(cudaMemGetInfo(&free_b, &total_b));  // (slow: only when the copies have to grow)
             const size_t need = floats * sizeof(float) * (ctx->sorted_ready ? 4 : 2);
-            if (ctx->matrix_hi.count >= floats || free_b > need + (size_t{2} << 30)) {
+            if (have || free_b > need + (size_t{2} << 30)) {
               ctx->matrix_hi.alloc(floats);
               ctx->matrix_lo.alloc(floats);
               ctx->stats.kernel_launches += launch_split_tf32(ctx->matrix.ptr, floats, ctx->matrix_hi.ptr, ctx->matrix_lo.ptr, st);
