@@ -178,14 +178,14 @@ struct tsdd_cuda_ctx {
   std::string error;
 
   // tunables (tsdd_cuda_set_option)
-  uint32_t opt_batch = 65536;
+  uint32_t opt_batch = 262144;
   uint32_t opt_first_batch = 128;
   uint32_t opt_batch_growth = 8;
   int opt_rounds = 64;            // upper limit on neighbour ranges per batch
   uint32_t opt_first_range = 8192;  // rows in the first range
   double opt_growth = 2.0;          // each range is this much larger than the one before (dot form: opt_dot_growth)
   int opt_window_rounds = 2;        // same-word-neighbourhood rounds before the covering scan
-  uint32_t opt_window_first = 2048; // slots in the first of them
+  uint32_t opt_window_first = 1024; // slots in the first of them
   double opt_window_growth = 3.0;
   bool opt_rotate = true;           // each batch starts its covering scan at a different row
   int opt_mates = 8;
