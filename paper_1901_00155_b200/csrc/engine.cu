@@ -226,6 +226,7 @@ struct tsdd_cuda_ctx {
   DeviceArray<float> matrix_hi, matrix_lo, sorted_hi, sorted_lo, batch_hi, batch_lo;
   bool split_ready = false, sorted_split_ready = false;
   bool opt_tensor_cores = false;
+  bool series_is_f32 = false; // series_f32 holds the prepared series' float32 originals (series = the same values, widened)
   bool norms_ready = false;   // row_norms holds the norms of the prepared matrix
   bool sorted_ready = false;  // matrix_sorted holds the prepared matrix in the hash-sorted order
   DeviceArray<uint32_t> hash0, freq, offsets, slot_bucket, scalars, slot_of_row, first_bad;
@@ -592,6 +593,7 @@ void reset_stats(tsdd_cuda_ctx* ctx) {
   std::memset(&ctx->stats, 0, sizeof(ctx->stats));
   ctx->prepared = false;
   ctx->norms_ready = false;
+  ctx->series_is_f32 = false;
   ctx->sorted_ready = false;
   ctx->split_ready = false;
   ctx->sorted_split_ready = false;
@@ -616,6 +618,7 @@ void prepare_host(tsdd_cuda_ctx* ctx, const T* series, size_t m, size_t n, size_
     CUDA_OK(cudaEventRecord(ev_h1, st));
     CUDA_OK(cudaEventRecord(ctx->ev_a, st));
     extra += launch_widen_series(ctx->series_f32.ptr, ctx->series.ptr, m, nullptr, st);  // (check_series ran on the host)
+    ctx->series_is_f32 = true;
   } else {
     CUDA_OK(cudaMemcpyAsync(ctx->series.ptr, series, m * sizeof(double), cudaMemcpyHostToDevice, st));
     CUDA_OK(cudaEventRecord(ev_h1, st));
@@ -1103,7 +1106,7 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
     // and merge the results with the same min-exchange that follows every batch.
     const bool split = ctx->several() && ctx->opt_share_bounds && ctx->opt_mates > 0;
     ctx->stats.kernel_launches += launch_bucket_mates(
-        s, ctx->series.ptr, ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->sorted_row, ctx->slot_bucket.ptr, ctx->offsets.ptr,
+        s, ctx->series.ptr, ctx->series_is_f32 ? ctx->series_f32.ptr : nullptr, ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->sorted_row, ctx->slot_bucket.ptr, ctx->offsets.ptr,
         ctx->opt_mates, split ? static_cast<uint32_t>(ctx->world) : 1u, split ? static_cast<uint32_t>(ctx->rank) : 0u, st);
     if (split) exchange_bounds(ctx);
   }
@@ -1504,6 +1507,10 @@ int tsdd_cuda_prepare_device_f32(tsdd_cuda_ctx* ctx, const float* d_series, size
     CUDA_OK(cudaEventRecord(ctx->ev_a, ctx->stream));
     // validate_series (series.cpp:10-19) on the device: the samples never passed through the host
     ctx->first_bad.alloc(1);
+    // (a copy of the caller's float32 samples: the caller's buffer is only borrowed for this call)
+    ctx->series_f32.alloc(m);
+    CUDA_OK(cudaMemcpyAsync(ctx->series_f32.ptr, d_series, m * sizeof(float), cudaMemcpyDeviceToDevice, ctx->stream));
+    ctx->series_is_f32 = true;
     const uint64_t extra = launch_widen_series(d_series, ctx->series.ptr, m, ctx->first_bad.ptr, ctx->stream);
     prepare_on_device(ctx, m, n, word_len, alphabet);
     ctx->stats.kernel_launches += extra;

@@ -107,8 +107,9 @@ int launch_min_from_peers(uint64_t* d_nn, PeerPointers peers, uint32_t rows, cud
 
 // Same-word neighbours first (the HOTSAX inner heuristic, discovery.cpp:51-63):
 // every row is measured against up to `mates` rows of its own bucket.
-int launch_bucket_mates(SearchState s, const double* d_series, const double* d_mean, const double* d_inv_sigma,
-                        const uint32_t* d_sorted_row, const uint32_t* d_slot_bucket,
+// d_series_f32: the float32 originals when the series arrived in that type (else nullptr): same values, half the bytes.
+int launch_bucket_mates(SearchState s, const double* d_series, const float* d_series_f32, const double* d_mean,
+                        const double* d_inv_sigma, const uint32_t* d_sorted_row, const uint32_t* d_slot_bucket,
                         const uint32_t* d_offsets, int mates, uint32_t world, uint32_t rank, cudaStream_t stream);
 
 // Time topology: every live batch candidate c tries the matches of its neighbours in time,

@@ -184,8 +184,12 @@ k_install_seed(SearchState s, const uint32_t* __restrict__ seed_lb, uint32_t see
 // windows of neighbouring warps overlap almost entirely and come from L1 / L2, where the
 // matrix rows (16 GB at workload 4, each read once) had to come from HBM.  Lanes stride over
 // the window (256 contiguous bytes per warp per step); the sum is folded with warp shuffles.
+// (kSample: float when the series arrived as float32 — the float64 copy holds exactly those values,
+// so reading the 4-byte originals and widening in registers gives bit-identical distances for
+// half the L1 / L2 traffic, which is what bounds this kernel.)
+template <typename kSample>
 __global__ void __launch_bounds__(256)
-k_bucket_mates(SearchState s, const double* __restrict__ x, const double* __restrict__ mean,
+k_bucket_mates(SearchState s, const kSample* __restrict__ x, const double* __restrict__ mean,
                const double* __restrict__ inv_sigma, const uint32_t* __restrict__ sorted_row,
                const uint32_t* __restrict__ slot_bucket, const uint32_t* __restrict__ offsets,
                int mates, uint32_t world, uint32_t rank) {
@@ -201,7 +205,7 @@ k_bucket_mates(SearchState s, const double* __restrict__ x, const double* __rest
   TSDD_BOUND(bucket + 1, s.n_rows + 1);
   TSDD_BOUND(row_i, s.n_rows);
   TSDD_BOUND(b1 - 1, s.n_rows);
-  const double* pi = x + row_i;
+  const kSample* pi = x + row_i;
   const double mu_i = mean[row_i], inv_i = inv_sigma[row_i];
   uint32_t tries = static_cast<uint32_t>(mates);
   uint32_t step = len / (tries + 1);
@@ -221,13 +225,27 @@ k_bucket_mates(SearchState s, const double* __restrict__ x, const double* __rest
     const uint32_t row_j = sorted_row[other];
     TSDD_BOUND(row_j, s.n_rows);
     if (gap_u32(row_i, row_j) < s.n) continue;
-    const double* pj = x + row_j;
+    const kSample* pj = x + row_j;
     const double mu_j = mean[row_j], inv_j = inv_sigma[row_j];
-    double sum64 = 0.0;
-    for (uint32_t t = lane; t < s.n; t += 32) {
-      const double d = (pi[t] - mu_i) * inv_i - (__ldg(pj + t) - mu_j) * inv_j;
-      sum64 = fma(d, d, sum64);
+    // eight loads in flight per lane before the first use (the kernel is bound by load latency,
+    // not arithmetic: ncu long_scoreboard), two accumulators; the order of the additions is not
+    // the reference's, nor does it have to be: this is an upper bound, settled later in float64
+    double sum_a = 0.0, sum_b = 0.0;
+    uint32_t t = lane;
+    for (; t + 96 < s.n; t += 128) {
+      const double a0 = static_cast<double>(pi[t]), a1 = static_cast<double>(pi[t + 32]), a2 = static_cast<double>(pi[t + 64]),
+                   a3 = static_cast<double>(pi[t + 96]);
+      const double b0 = static_cast<double>(__ldg(pj + t)), b1 = static_cast<double>(__ldg(pj + t + 32)),
+                   b2 = static_cast<double>(__ldg(pj + t + 64)), b3 = static_cast<double>(__ldg(pj + t + 96));
+      const double d0 = (a0 - mu_i) * inv_i - (b0 - mu_j) * inv_j, d1 = (a1 - mu_i) * inv_i - (b1 - mu_j) * inv_j;
+      const double d2 = (a2 - mu_i) * inv_i - (b2 - mu_j) * inv_j, d3 = (a3 - mu_i) * inv_i - (b3 - mu_j) * inv_j;
+      sum_a = fma(d0, d0, sum_a), sum_b = fma(d1, d1, sum_b), sum_a = fma(d2, d2, sum_a), sum_b = fma(d3, d3, sum_b);
     }
+    for (; t < s.n; t += 32) {
+      const double d = (static_cast<double>(pi[t]) - mu_i) * inv_i - (static_cast<double>(__ldg(pj + t)) - mu_j) * inv_j;
+      sum_a = fma(d, d, sum_a);
+    }
+    double sum64 = sum_a + sum_b;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) sum64 += __shfl_xor_sync(0xFFFFFFFFu, sum64, d);
     const float sum = static_cast<float>(sum64);
@@ -2335,13 +2353,17 @@ int launch_min_from_peers(uint64_t* d_nn, PeerPointers peers, uint32_t rows, cud
   return 1;
 }
 
-int launch_bucket_mates(SearchState s, const double* d_series, const double* d_mean, const double* d_inv_sigma,
-                        const uint32_t* d_sorted_row, const uint32_t* d_slot_bucket,
+int launch_bucket_mates(SearchState s, const double* d_series, const float* d_series_f32, const double* d_mean,
+                        const double* d_inv_sigma, const uint32_t* d_sorted_row, const uint32_t* d_slot_bucket,
                         const uint32_t* d_offsets, int mates, uint32_t world, uint32_t rank, cudaStream_t stream) {
   if (mates <= 0) return 0;
   const size_t slots = (static_cast<size_t>(s.n_rows) + world - 1) / world;
-  k_bucket_mates<<<blocks_for(slots * 32, 256), 256, 0, stream>>>(
-      s, d_series, d_mean, d_inv_sigma, d_sorted_row, d_slot_bucket, d_offsets, mates, world, rank);
+  if (d_series_f32 != nullptr)
+    k_bucket_mates<float><<<blocks_for(slots * 32, 256), 256, 0, stream>>>(
+        s, d_series_f32, d_mean, d_inv_sigma, d_sorted_row, d_slot_bucket, d_offsets, mates, world, rank);
+  else
+    k_bucket_mates<double><<<blocks_for(slots * 32, 256), 256, 0, stream>>>(
+        s, d_series, d_mean, d_inv_sigma, d_sorted_row, d_slot_bucket, d_offsets, mates, world, rank);
   return 1;
 }
 
