@@ -611,7 +611,7 @@ constexpr int kRowBytes = kChunk * 4;   // bytes of one row inside a stage
 constexpr int kPieces = kChunk / 4;     // 16-byte pieces per row and stage
 constexpr int kScanThreads = 256;
 constexpr size_t scan_smem_bytes(int cand_rows, int nbr_rows) {
-  return static_cast<size_t>(kStages) * (cand_rows + nbr_rows) * kChunk * 4 + 6 * kTileRows * 4;
+  return static_cast<size_t>(kStages) * (cand_rows + nbr_rows) * kChunk * 4 + 7 * kTileRows * 4;
 }
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
@@ -628,18 +628,23 @@ __device__ __forceinline__ void cp_async_wait() {
 // CTA).  The neighbour rows are addressed through s_brow (row numbers in shared
 // memory), so a tile may hold any 128 rows: every piece is still one 16-byte
 // part of a full 128-byte line.
+// s_map (may be null): slot r of the stage holds candidate s_map[r] of the tile for r < n_mapped —
+// the candidates that take part, packed to the front (k_scan_tiles, kLb); the slots behind them are
+// filled with the first of those rows (finite values; nobody looks at their sums).
 template <int kCand, int kNbr>
 __device__ __forceinline__ void issue_stage(unsigned char* stage, const float* a_tile,
                                             const float* rows, const uint32_t* s_brow,
-                                            uint32_t stride, uint32_t col0) {
+                                            uint32_t stride, uint32_t col0, const uint32_t* s_map = nullptr,
+                                            uint32_t n_mapped = 0) {
 #pragma unroll
   for (int q = 0; q < kCand * kPieces / kScanThreads; ++q) {  // candidate rows
     const uint32_t piece = threadIdx.x + q * kScanThreads;
     const uint32_t r = piece / kPieces, kc = piece % kPieces;
+    const uint32_t from = s_map ? s_map[r < n_mapped ? r : 0u] : r;
     // candidate rows are swizzled by (r >> 3): a thread's 8 rows 8 ty .. 8 ty + 7 then share one
     // slot pattern, and the two thread rows of a warp (ty, ty + 1) get different ones
     cp_async16(stage + r * kRowBytes + ((kc ^ ((r >> 3) & 7)) << 4),
-               a_tile + static_cast<size_t>(r) * stride + col0 + kc * 4);
+               a_tile + static_cast<size_t>(from) * stride + col0 + kc * 4);
   }
 #pragma unroll
   for (int q = 0; q < kNbr * kPieces / kScanThreads; ++q) {  // neighbour rows
@@ -756,6 +761,8 @@ k_scan_tiles(SearchState s, ScanArgs a) {
   uint32_t* s_jrow = reinterpret_cast<uint32_t*>(s_nub + kTileRows);      // neighbour rows, ~0 = none
   uint32_t* s_brow = s_jrow + kTileRows;                                  // rows to load (none -> zero row)
   float* s_loc = reinterpret_cast<float*>(s_brow + kTileRows);            // bounds this CTA found itself
+  uint32_t* s_map = reinterpret_cast<uint32_t*>(s_loc + kTileRows);       // kLb: the candidates taking part in a tile, packed
+  __shared__ uint32_t s_wcount[kScanThreads / 32];
   __shared__ unsigned long long s_calls, s_abandoned, s_terms, s_tiles, s_tile_live, s_lb_skipped, s_useful;
 
   const uint32_t count = a.sel[0];
@@ -850,6 +857,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
     }
     const int n_live = __syncthreads_count(live);
     if (n_live == 0) break;  // every candidate of this tile is dead: nothing left to do
+    uint32_t n_mapped = 0;   // > 0: the tile's candidates are packed through s_map (kLb)
     // ---- lower-bound filter (covering scan only): a candidate whose segment means lie
     // further from every 16-row box of this tile than its threshold cannot find a
     // neighbour below it here; it sits this tile out (threshold -1 for this tile).
@@ -887,12 +895,24 @@ k_scan_tiles(SearchState s, ScanArgs a) {
           live = false;
         }
       }
-      const int n_needed = __syncthreads_count(needed);  // also publishes the lowered thresholds
+      // The candidates that take part are PACKED to the front of the tile (s_map: slot -> candidate),
+      // so that they fill as few warps as possible: the filter leaves a started tile about one-sixth
+      // full on strongly pruned inputs, and a warp computes for all of its 8 slots or for none.
+      const uint32_t ballot = __ballot_sync(0xFFFFFFFFu, needed && tid < kCand);
+      if (lane == 0) s_wcount[tid >> 5] = __popc(ballot);
+      const int n_needed = __syncthreads_count(needed);  // also publishes the lowered thresholds and the counts
       if (tid == 0) s_lb_skipped += static_cast<unsigned long long>(n_live - n_needed);
       if (n_needed == 0) {  // nobody needs this tile: no loads, no arithmetic
         if (tt + 1 < a.tiles_per_cta && k + 1 < h_end) prefetch(k + 1);
         continue;
       }
+      if (needed && tid < kCand) {
+        uint32_t at = __popc(ballot & ((1u << lane) - 1u));
+        for (uint32_t w = 0; w < (tid >> 5); ++w) at += s_wcount[w];
+        s_map[at] = tid;
+      }
+      n_mapped = static_cast<uint32_t>(n_needed);
+      __syncthreads();  // s_map complete
     }
     if (tid == 0) {
       s_tiles += 1;
@@ -923,9 +943,16 @@ k_scan_tiles(SearchState s, ScanArgs a) {
       my_calls = valid - overlap;
     }
 
+    // candidate (index inside the tile) of this thread's pair-row u: slot 8 ty + u, through the packing if there is one
+    uint32_t cidx[kU];
     float thr[kU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) thr[u] = s_thr[cand_of(ty, u)];
+    for (int u = 0; u < kU; ++u) {
+      const uint32_t slot = cand_of(ty, u);
+      cidx[u] = n_mapped ? (slot < n_mapped ? s_map[slot] : 0xFFFFFFFFu) : slot;
+      thr[u] = cidx[u] != 0xFFFFFFFFu ? s_thr[cidx[u]] : -1.f;
+    }
+    const uint32_t* stage_map = n_mapped ? s_map : nullptr;
 
     Acc<kPacked, kU, kW> acc;
     acc.zero();
@@ -933,7 +960,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
 #pragma unroll
     for (int st = 0; st < kStages - 1; ++st) {
       if (static_cast<uint32_t>(st) < chunks)
-        issue_stage<kCand, kNbr>(smem + st * kStageBytes, a_tile, s.rows, s_brow, s.stride, st * kChunk);
+        issue_stage<kCand, kNbr>(smem + st * kStageBytes, a_tile, s.rows, s_brow, s.stride, st * kChunk, stage_map, n_mapped);
       cp_async_commit();
     }
 
@@ -952,7 +979,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
       }
       if (c + kStages - 1 < chunks)
         issue_stage<kCand, kNbr>(smem + ((c + kStages - 1) % kStages) * kStageBytes, a_tile, s.rows, s_brow,
-                          s.stride, (c + kStages - 1) * kChunk);
+                          s.stride, (c + kStages - 1) * kChunk, stage_map, n_mapped);
       cp_async_commit();
       if (!warp_done) {
         const unsigned char* a_s = smem + (c % kStages) * kStageBytes + cand_of(ty, 0) * kRowBytes;
@@ -1038,7 +1065,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
     for (int w = 0; w < kW; ++w) jrow[w] = s_jrow[tx + kTx * w];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      const uint32_t row = s_cand[cand_of(ty, u)];
+      const uint32_t row = cidx[u] != 0xFFFFFFFFu ? s_cand[cidx[u]] : 0xFFFFFFFFu;
       uint32_t d_min = 0xFFFFFFFFu, j_min = 0xFFFFFFFFu;  // this thread's best (distance bits, neighbour)
 #pragma unroll
       for (int w = 0; w < kW; ++w) {
@@ -1067,7 +1094,7 @@ k_scan_tiles(SearchState s, ScanArgs a) {
       if (tx == 0 && g_j != 0xFFFFFFFFu) {
         TSDD_BOUND(row, s.n_rows);
         atomicMin(as_ull(s.nn + row), static_cast<unsigned long long>(nn_key(g_min, g_j)));
-        s_loc[cand_of(ty, u)] = fminf(s_loc[cand_of(ty, u)], __uint_as_float(g_min));
+        s_loc[cidx[u]] = fminf(s_loc[cidx[u]], __uint_as_float(g_min));
       }
     }
   }
