@@ -226,6 +226,7 @@ struct tsdd_cuda_ctx {
   DeviceArray<float> matrix_hi, matrix_lo, sorted_hi, sorted_lo, batch_hi, batch_lo;
   bool split_ready = false, sorted_split_ready = false;
   bool opt_tensor_cores = false;
+  bool opt_tc_half = false;   // the split parts are fp16 (dot_form 5 / 6) instead of tf32 (3 / 4)
   bool series_is_f32 = false; // series_f32 holds the prepared series' float32 originals (series = the same values, widened)
   bool norms_ready = false;   // row_norms holds the norms of the prepared matrix
   bool sorted_ready = false;  // matrix_sorted holds the prepared matrix in the hash-sorted order
@@ -864,7 +865,7 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
     if (choice.tc && !choice_now.tc) choice_now.tile16 = ctx->opt_tile16 && count > 192;
     const uint32_t padded = round_up_u32(count, choice_now.tile16 ? 2 * kTileRows : kTileRows);
     if (choice_now.tc)
-      launches += launch_gather_rows_split(s, list, ctx->sel.ptr, padded, ctx->batch_hi.ptr, ctx->batch_lo.ptr, st);
+      launches += launch_gather_rows_split(s, list, ctx->sel.ptr, padded, ctx->opt_tc_half, ctx->batch_hi.ptr, ctx->batch_lo.ptr, st);
     else
       launches += launch_gather_rows(s, list, ctx->sel.ptr, padded, choice_now.tile16 ? 2 : choice_now.tma ? 1 : 0,
                                      ctx->batch_matrix.ptr, st);
@@ -878,7 +879,7 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
     int launched = 0;
     if (choice_now.tc) {
       const TcOperands op{ctx->batch_hi.ptr, ctx->batch_lo.ptr, ctx->matrix_hi.ptr, ctx->matrix_lo.ptr,
-                          ctx->sorted_hi.ptr, ctx->sorted_lo.ptr, ctx->rows_padded};
+                          ctx->sorted_hi.ptr, ctx->sorted_lo.ptr, ctx->rows_padded, ctx->opt_tc_half};
       launched = launch_scan_tiles_tc(s, op, list, slots, ctx->sel.ptr, count, plan[r].window ? ctx->sorted_row : nullptr,
                                       plan[r].k_begin, plan[r].k_end, pruning, ctx->opt_symmetric, st, &launch_error);
       if (launched) ctx->stats.scan_kernel_tc_launches += launched;
@@ -990,12 +991,12 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
             if (have || free_b > need + (size_t{2} << 30)) {
               ctx->matrix_hi.alloc(floats);
               ctx->matrix_lo.alloc(floats);
-              ctx->stats.kernel_launches += launch_split_tf32(ctx->matrix.ptr, floats, ctx->matrix_hi.ptr, ctx->matrix_lo.ptr, st);
+              ctx->stats.kernel_launches += launch_split_rows(ctx->matrix.ptr, floats, ctx->opt_tc_half, ctx->matrix_hi.ptr, ctx->matrix_lo.ptr, st);
               if (ctx->sorted_ready) {
                 ctx->sorted_hi.alloc(floats);
                 ctx->sorted_lo.alloc(floats);
                 ctx->stats.kernel_launches +=
-                    launch_split_tf32(ctx->matrix_sorted.ptr, floats, ctx->sorted_hi.ptr, ctx->sorted_lo.ptr, st);
+                    launch_split_rows(ctx->matrix_sorted.ptr, floats, ctx->opt_tc_half, ctx->sorted_hi.ptr, ctx->sorted_lo.ptr, st);
                 ctx->sorted_split_ready = true;
               }
               ctx->split_ready = true;
@@ -1438,10 +1439,11 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
     } else if (key == "tensor_map") {
       ctx->opt_tensor_map = value != 0;
     } else if (key == "dot_form") {
-      if (value != 0 && value != 1 && value != 2 && value != 3 && value != 4)
-        fail(TSDD_ERR_PARAMETER, "dot_form must be 0, 1, 2, 3 or 4");
-      ctx->opt_dot = value >= 3 ? static_cast<int>(value) - 2 : static_cast<int>(value);  // 3 / 4: as 1 / 2 ...
-      ctx->opt_tensor_cores = value >= 3;                                                 // ... on the tensor cores
+      if (value != std::floor(value) || value < 0 || value > 6) fail(TSDD_ERR_PARAMETER, "dot_form must be 0 .. 6");
+      const int form = static_cast<int>(value);
+      ctx->opt_dot = form >= 5 ? form - 4 : form >= 3 ? form - 2 : form;  // 3 / 4 and 5 / 6: as 1 / 2 ...
+      ctx->opt_tensor_cores = form >= 3;                                  // ... on the tensor cores,
+      ctx->opt_tc_half = form >= 5;                                       // ... with tf32 (3 / 4) or fp16 (5 / 6) parts
     } else if (key == "shard_prep") {
       ctx->opt_shard_prep = value != 0;
     } else if (key == "share_bounds") {

@@ -191,16 +191,18 @@ struct TcOperands {
   const float *rows_hi, *rows_lo;      // the matrix, split (launch_split_tf32)
   const float *sorted_hi, *sorted_lo;  // its hash-sorted copy, split (window tiles)
   uint64_t rows_padded;                // rows of each of the four neighbour arrays
+  bool half;                           // the parts are fp16 (kind::f16, 22 bits between them) instead of tf32 (kind::tf32, 21 bits)
 };
-int launch_split_tf32(const float* d_in, size_t floats, float* d_hi, float* d_lo, cudaStream_t stream);
+int launch_split_rows(const float* d_in, size_t floats, bool half, float* d_hi, float* d_lo, cudaStream_t stream);
 int launch_gather_rows_split(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel, uint32_t capacity_padded,
-                             float* d_hi, float* d_lo, cudaStream_t stream);
+                             bool half, float* d_hi, float* d_lo, cudaStream_t stream);
 int launch_scan_tiles_tc(SearchState s, const TcOperands& op, const uint32_t* d_batch_rows, const uint32_t* d_batch_slots,
                          const uint32_t* d_sel, uint32_t live_upper_bound, const uint32_t* d_nbr_index, uint32_t k_begin,
                          uint32_t k_end, bool pruning, bool symmetric, cudaStream_t stream, const char** error);
-// float32 matrix [n_rows x stride] as a tensor map with boxes of box_rows x box_cols, 128-byte swizzle
+// float32 (elem_bytes 4) or fp16 (2) matrix [n_rows x stride elements] as a tensor map with boxes of box_rows x box_cols, 128-byte swizzle
 // (box_cols * 4 = 128) or the 64-byte one (box_cols * 4 = 64); false when the driver lacks cuTensorMapEncodeTiled.  `map` is a CUtensorMap.
-bool make_row_map_boxed(void* map, const float* base, uint64_t n_rows, uint64_t stride, uint32_t box_cols, uint32_t box_rows);
+bool make_row_map_boxed(void* map, const void* base, uint64_t n_rows, uint64_t stride, uint32_t box_cols, uint32_t box_rows,
+                        uint32_t elem_bytes = 4);
 
 // Squared norms of the float32 rows (rows 0 .. n_rows; row n_rows is the zero row), for the
 // dot-product form d^2 = |a|^2 + |b|^2 - 2 a.b of the warp-specialised tile kernel.

@@ -2480,16 +2480,18 @@ bool make_row_map(CUtensorMap* map, const float* base, uint64_t n_rows, uint64_t
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-bool make_row_map_boxed(void* map, const float* base, uint64_t n_rows, uint64_t stride, uint32_t box_cols, uint32_t box_rows) {
+bool make_row_map_boxed(void* map, const void* base, uint64_t n_rows, uint64_t stride, uint32_t box_cols, uint32_t box_rows,
+                        uint32_t elem_bytes) {
   PFN_cuTensorMapEncodeTiled encode = tensor_map_encoder();
   if (!encode) return false;
   const cuuint64_t dims[2] = {stride, n_rows};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(stride) * sizeof(float)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(stride) * elem_bytes};
   const cuuint32_t box[2] = {box_cols, box_rows};
   const cuuint32_t elem[2] = {1, 1};
-  const CUtensorMapSwizzle swizzle = box_cols * 4 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
-  return encode(static_cast<CUtensorMap*>(map), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
-                box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  const CUtensorMapSwizzle swizzle = box_cols * elem_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B;
+  const CUtensorMapDataType type = elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  return encode(static_cast<CUtensorMap*>(map), type, 2, const_cast<void*>(base), dims, strides, box, elem,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 

@@ -28,6 +28,7 @@
 //               candidate per tile, plus the symmetric updates of the neighbours.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_fp16.h>
 
 #include "kernels.hpp"
 
@@ -37,15 +38,14 @@ namespace {
 
 constexpr int kM = 128;                    // candidates per tile = TMEM lanes
 constexpr int kN = 256;                    // neighbours per tile = accumulator columns
-#ifndef TSDD_TC_STAGE_COLS
-#define TSDD_TC_STAGE_COLS 16
-#endif
-constexpr int kStageCols = TSDD_TC_STAGE_COLS;  // columns per stage: one swizzled row piece (16: 64-byte swizzle, 32: 128-byte)
-constexpr int kUmmaK = 8;                  // columns per tf32 MMA
-constexpr int kTcStages = kStageCols == 16 ? 4 : 2;  // (a stage of 16 columns is 48 KB, of 32 columns 96 KB)
-constexpr int kABytes = kM * kStageCols * 4;   // 16 KB
-constexpr int kBBytes = kN * kStageCols * 4;   // 32 KB
-constexpr int kTcStageBytes = 2 * kABytes + 2 * kBBytes;  // A_hi | A_lo | B_hi | B_lo = 96 KB
+// A stage is one 64-byte piece of every row (64-byte swizzle): 16 tf32 columns or 32 fp16 columns,
+// i.e. two MMA k-steps of 32 bytes either way; the byte geometry does not depend on the format.
+constexpr int kRowPiece = 64;
+constexpr int kTcStages = 4;
+constexpr int kMetaSlots = 4;              // tiles whose metadata may be prepared ahead of the streams
+constexpr int kABytes = kM * kRowPiece;        //  8 KB
+constexpr int kBBytes = kN * kRowPiece;        // 16 KB
+constexpr int kTcStageBytes = 2 * kABytes + 2 * kBBytes;  // A_hi | A_lo | B_hi | B_lo = 48 KB
 constexpr int kTcThreads = 256;
 constexpr uint32_t kTmemCols = 512;        // two accumulator sets of 256 columns
 
@@ -63,11 +63,11 @@ struct alignas(16) TcMeta {
 
 struct SharedTc {
   alignas(1024) unsigned char stages[kTcStages][kTcStageBytes];
-  TcMeta meta[2];
+  TcMeta meta[kMetaSlots];
   uint32_t cand[kM];
   float cnorm[kM];
   float loc[kM];
-  unsigned long long full[kTcStages], empty[kTcStages], tmem_full[2], tmem_empty[2], meta_full[2], meta_empty[2];
+  unsigned long long full[kTcStages], empty[kTcStages], tmem_full[2], tmem_empty[2], meta_full[kMetaSlots], meta_empty[kMetaSlots];
   uint32_t tmem_base;
 };
 
@@ -129,25 +129,31 @@ __device__ __forceinline__ void tma_box(void* dst, const CUtensorMap* map, uint3
       : "memory");
 }
 
-// Shared-memory matrix descriptor of a K-major tile whose rows are kStageCols * 4 bytes (64 or 128)
-// with the swizzle of that width (what the TMA boxes write): start address >> 4 | leading offset
-// (unused for swizzled K-major) | stride between 8-row groups = 8 rows | descriptor version 1 |
-// layout type (SWIZZLE_64B = 4, SWIZZLE_128B = 2).
+// Shared-memory matrix descriptor of a K-major tile whose rows are 64 bytes with the 64-byte
+// swizzle (what the TMA boxes write): start address >> 4 | leading offset (unused for swizzled
+// K-major) | stride between 8-row groups = 512 bytes | descriptor version 1 | SWIZZLE_64B (4).
 __device__ __forceinline__ uint64_t umma_desc(uint32_t smem_addr) {
-  constexpr uint64_t kGroupBytes = 8 * kStageCols * 4;
-  constexpr uint64_t kLayout = kStageCols == 16 ? 4 : 2;
-  return static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4) | (1ull << 16) | ((kGroupBytes >> 4) << 32) | (1ull << 46) |
-         (kLayout << 61);
+  return static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4) | (1ull << 16) | (static_cast<uint64_t>((8 * kRowPiece) >> 4) << 32) |
+         (1ull << 46) | (4ull << 61);
 }
-// Instruction descriptor: D float32, A / B tf32, both K-major, N = 256, M = 128.
-constexpr uint32_t kInstrDesc = (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(kN >> 3) << 17) |
-                                (static_cast<uint32_t>(kM >> 4) << 24);
-
-__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t accumulate) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-      "l"(desc_a), "l"(desc_b), "r"(kInstrDesc), "r"(accumulate)
-      : "memory");
+// Instruction descriptor: D float32; A / B tf32 (format 2) or fp16 (format 0), both K-major; N = 256, M = 128.
+template <bool kHalf>
+struct InstrDesc {
+  static constexpr uint32_t value = (1u << 4) | ((kHalf ? 0u : 2u) << 7) | ((kHalf ? 0u : 2u) << 10) |
+                                    (static_cast<uint32_t>(kN >> 3) << 17) | (static_cast<uint32_t>(kM >> 4) << 24);
+};
+template <bool kHalf>
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t desc_a, uint64_t desc_b, uint32_t accumulate) {
+  if constexpr (kHalf)
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(desc_a), "l"(desc_b), "n"(InstrDesc<true>::value), "r"(accumulate)
+        : "memory");
+  else
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(desc_a), "l"(desc_b), "n"(InstrDesc<false>::value), "r"(accumulate)
+        : "memory");
 }
 __device__ __forceinline__ void umma_commit(unsigned long long* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -174,7 +180,7 @@ struct TcArgs {
   int pruning;
 };
 
-template <bool kSymmetric>
+template <bool kSymmetric, bool kHalf>
 __global__ void __launch_bounds__(kTcThreads, 1)
 k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map_a_hi,
                 const __grid_constant__ CUtensorMap map_a_lo, const __grid_constant__ CUtensorMap map_b_hi,
@@ -203,6 +209,8 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
     for (int i = 0; i < 2; ++i) {
       bar_init(&sh.tmem_full[i], 1);
       bar_init(&sh.tmem_empty[i], 4);   // the four epilogue warps
+    }
+    for (int i = 0; i < kMetaSlots; ++i) {
       bar_init(&sh.meta_full[i], 1);
       bar_init(&sh.meta_empty[i], 6);   // the four epilogue warps, the MMA warp and the producer
     }
@@ -219,6 +227,7 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
 
   const bool window = a.nbr_index != nullptr;
   const uint32_t units = (s.n_rows + kN - 1) / kN;  // 256-row units of the (hash-sorted or positional) row order
+  constexpr uint32_t kStageCols = kHalf ? 32 : 16;  // columns of one 64-byte row piece
   const uint32_t chunks = s.stride / kStageCols;
   const uint32_t u_first = a.u_begin + blockIdx.y * a.tiles_per_cta;
   const uint32_t n_tiles = u_first < a.u_end ? min(static_cast<uint32_t>(a.tiles_per_cta), a.u_end - u_first) : 0u;
@@ -236,7 +245,7 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
     const uint64_t best = a.pruning ? *s.best : 0ull;
     unsigned long long calls_total = 0, tiles_total = 0, live_total = 0;
     for (uint32_t ti = 0; ti <= n_tiles; ++ti) {
-      const uint32_t m = ti & 1, use = ti >> 1;
+      const uint32_t m = ti % kMetaSlots, use = ti / kMetaSlots;
       TcMeta& meta = sh.meta[m];
       if (use >= 1) bar_wait(&sh.meta_empty[m], (use - 1) & 1, 1);
       bool any_live = false;
@@ -307,8 +316,8 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
     // ================================================================ producer: the TMA streams
     uint32_t seq = 0;
     for (uint32_t ti = 0;; ++ti) {
-      const uint32_t m = ti & 1;
-      bar_wait(&sh.meta_full[m], (ti >> 1) & 1, 2);
+      const uint32_t m = ti % kMetaSlots;
+      bar_wait(&sh.meta_full[m], (ti / kMetaSlots) & 1, 2);
       const bool stop = *reinterpret_cast<volatile uint32_t*>(&sh.meta[m].stop) != 0;
       const uint32_t slot0 = *reinterpret_cast<volatile uint32_t*>(&sh.meta[m].slot0);
       __syncwarp();
@@ -333,8 +342,8 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
     // ================================================================ MMA issuer
     uint32_t seq = 0;
     for (uint32_t ti = 0;; ++ti) {
-      const uint32_t m = ti & 1, buf = ti & 1;
-      bar_wait(&sh.meta_full[m], (ti >> 1) & 1, 4);
+      const uint32_t m = ti % kMetaSlots, buf = ti & 1;
+      bar_wait(&sh.meta_full[m], (ti / kMetaSlots) & 1, 4);
       const bool stop = *reinterpret_cast<volatile uint32_t*>(&sh.meta[m].stop) != 0;
       __syncwarp();
       if (lane == 0) bar_arrive(&sh.meta_empty[m]);
@@ -351,11 +360,11 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
           const uint64_t a_hi = umma_desc(base), a_lo = umma_desc(base + kABytes);
           const uint64_t b_hi = umma_desc(base + 2 * kABytes), b_lo = umma_desc(base + 2 * kABytes + kBBytes);
 #pragma unroll
-          for (uint32_t k = 0; k < kStageCols / kUmmaK; ++k) {
-            const uint64_t step = static_cast<uint64_t>((k * kUmmaK * 4) >> 4);  // 32 bytes along the swizzled row piece
-            umma_tf32(tmem_d, a_hi + step, b_hi + step, (c | k) != 0 ? 1u : 0u);
-            umma_tf32(tmem_d, a_hi + step, b_lo + step, 1u);
-            umma_tf32(tmem_d, a_lo + step, b_hi + step, 1u);
+          for (uint32_t k = 0; k < 2; ++k) {  // two k-steps of 32 bytes (8 tf32 / 16 fp16 columns) per stage
+            const uint64_t step = static_cast<uint64_t>((k * 32) >> 4);
+            umma<kHalf>(tmem_d, a_hi + step, b_hi + step, (c | k) != 0 ? 1u : 0u);
+            umma<kHalf>(tmem_d, a_hi + step, b_lo + step, 1u);
+            umma<kHalf>(tmem_d, a_lo + step, b_hi + step, 1u);
           }
           umma_commit(&sh.empty[st]);                          // the stage is free once these MMAs have read it
           if (c + 1 == chunks) umma_commit(&sh.tmem_full[buf]);  // ... and the tile's accumulators are complete
@@ -374,8 +383,8 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
     unsigned long long tiles_done = 0, useful = 0;
     uint32_t overlap_total = 0;
     for (uint32_t ti = 0;; ++ti) {
-      const uint32_t m = ti & 1, buf = ti & 1;
-      bar_wait(&sh.meta_full[m], (ti >> 1) & 1, 7);
+      const uint32_t m = ti % kMetaSlots, buf = ti & 1;
+      bar_wait(&sh.meta_full[m], (ti / kMetaSlots) & 1, 7);
       TcMeta& meta = sh.meta[m];
       if (*reinterpret_cast<volatile uint32_t*>(&meta.stop) != 0) {
         __syncwarp();
@@ -465,7 +474,26 @@ k_split_tf32(const float4* __restrict__ in, size_t quads, float4* __restrict__ h
   lo[i] = make_float4(top(x.x - h.x), top(x.y - h.y), top(x.z - h.z), top(x.w - h.w));
 }
 
+// x = hi + lo with both parts fp16 (round to nearest): 22 bits between them
+__device__ __forceinline__ void split_half(const float4& x, uint2& h, uint2& l) {
+  const __half2 h0 = __floats2half2_rn(x.x, x.y), h1 = __floats2half2_rn(x.z, x.w);
+  const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
+  const __half2 l0 = __floats2half2_rn(x.x - f0.x, x.y - f0.y), l1 = __floats2half2_rn(x.z - f1.x, x.w - f1.y);
+  h = make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
+  l = make_uint2(*reinterpret_cast<const uint32_t*>(&l0), *reinterpret_cast<const uint32_t*>(&l1));
+}
+__global__ void __launch_bounds__(256)
+k_split_f16(const float4* __restrict__ in, size_t quads, uint2* __restrict__ hi, uint2* __restrict__ lo) {
+  const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= quads) return;
+  uint2 h, l;
+  split_half(in[i], h, l);
+  hi[i] = h;
+  lo[i] = l;
+}
+
 // The batch's rows, split the same way, dense in batch order; rows past the batch size are zero.
+template <bool kHalf>
 __global__ void __launch_bounds__(256)
 k_gather_rows_split(SearchState s, const uint32_t* __restrict__ batch_rows, const uint32_t* __restrict__ sel,
                     uint32_t capacity_padded, float* __restrict__ hi, float* __restrict__ lo) {
@@ -474,6 +502,18 @@ k_gather_rows_split(SearchState s, const uint32_t* __restrict__ batch_rows, cons
   if (r >= capacity_padded) return;
   const uint32_t count = sel[0];
   if (r >= (count + kM - 1) / kM * kM) return;  // only the tiles the scan will touch
+  if constexpr (kHalf) {
+    uint2* dh = reinterpret_cast<uint2*>(hi) + static_cast<size_t>(r) * (s.stride / 4);
+    uint2* dl = reinterpret_cast<uint2*>(lo) + static_cast<size_t>(r) * (s.stride / 4);
+    if (r < count) {
+      TSDD_BOUND(batch_rows[r], s.n_rows);
+      const float4* src = reinterpret_cast<const float4*>(s.rows + static_cast<size_t>(batch_rows[r]) * s.stride);
+      for (uint32_t c = lane; c < s.stride / 4; c += 32) split_half(__ldg(src + c), dh[c], dl[c]);
+    } else {
+      for (uint32_t c = lane; c < s.stride / 4; c += 32) dh[c] = dl[c] = make_uint2(0u, 0u);
+    }
+    return;
+  }
   float4* dh = reinterpret_cast<float4*>(hi + static_cast<size_t>(r) * s.stride);
   float4* dl = reinterpret_cast<float4*>(lo + static_cast<size_t>(r) * s.stride);
   auto top = [](float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); };
@@ -495,17 +535,22 @@ inline unsigned blocks_of(size_t items, unsigned per_block) { return static_cast
 
 }  // namespace
 
-int launch_split_tf32(const float* d_in, size_t floats, float* d_hi, float* d_lo, cudaStream_t stream) {
+int launch_split_rows(const float* d_in, size_t floats, bool half, float* d_hi, float* d_lo, cudaStream_t stream) {
   const size_t quads = floats / 4;
-  k_split_tf32<<<blocks_of(quads, 256), 256, 0, stream>>>(reinterpret_cast<const float4*>(d_in), quads,
-                                                         reinterpret_cast<float4*>(d_hi), reinterpret_cast<float4*>(d_lo));
+  if (half)
+    k_split_f16<<<blocks_of(quads, 256), 256, 0, stream>>>(reinterpret_cast<const float4*>(d_in), quads,
+                                                          reinterpret_cast<uint2*>(d_hi), reinterpret_cast<uint2*>(d_lo));
+  else
+    k_split_tf32<<<blocks_of(quads, 256), 256, 0, stream>>>(reinterpret_cast<const float4*>(d_in), quads,
+                                                           reinterpret_cast<float4*>(d_hi), reinterpret_cast<float4*>(d_lo));
   return 1;
 }
 
 int launch_gather_rows_split(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel, uint32_t capacity_padded,
-                             float* d_hi, float* d_lo, cudaStream_t stream) {
-  k_gather_rows_split<<<blocks_of(static_cast<size_t>(capacity_padded) * 32, 256), 256, 0, stream>>>(
-      s, d_batch_rows, d_sel, capacity_padded, d_hi, d_lo);
+                             bool half, float* d_hi, float* d_lo, cudaStream_t stream) {
+  const unsigned blocks = blocks_of(static_cast<size_t>(capacity_padded) * 32, 256);
+  if (half) k_gather_rows_split<true><<<blocks, 256, 0, stream>>>(s, d_batch_rows, d_sel, capacity_padded, d_hi, d_lo);
+  else k_gather_rows_split<false><<<blocks, 256, 0, stream>>>(s, d_batch_rows, d_sel, capacity_padded, d_hi, d_lo);
   return 1;
 }
 
@@ -525,22 +570,27 @@ int launch_scan_tiles_tc(SearchState s, const TcOperands& op, const uint32_t* d_
   const float* b_hi = window ? op.sorted_hi : op.rows_hi;
   const float* b_lo = window ? op.sorted_lo : op.rows_lo;
   const uint64_t b_rows = op.rows_padded;  // (a box that reaches past the last row is zero-filled by the TMA unit)
-  if (!make_row_map_boxed(&map_a_hi, op.batch_hi, static_cast<uint64_t>(cand_tiles) * kM, s.stride, kStageCols, kM) ||
-      !make_row_map_boxed(&map_a_lo, op.batch_lo, static_cast<uint64_t>(cand_tiles) * kM, s.stride, kStageCols, kM) ||
-      !make_row_map_boxed(&map_b_hi, b_hi, b_rows, s.stride, kStageCols, kN) ||
-      !make_row_map_boxed(&map_b_lo, b_lo, b_rows, s.stride, kStageCols, kN)) {
+  const uint32_t cols = op.half ? 32 : 16, elem = op.half ? 2 : 4;
+  if (!make_row_map_boxed(&map_a_hi, op.batch_hi, static_cast<uint64_t>(cand_tiles) * kM, s.stride, cols, kM, elem) ||
+      !make_row_map_boxed(&map_a_lo, op.batch_lo, static_cast<uint64_t>(cand_tiles) * kM, s.stride, cols, kM, elem) ||
+      !make_row_map_boxed(&map_b_hi, b_hi, b_rows, s.stride, cols, kN, elem) ||
+      !make_row_map_boxed(&map_b_lo, b_lo, b_rows, s.stride, cols, kN, elem)) {
     if (error) *error = "cuTensorMapEncodeTiled failed (tensor-core tile kernel)";
     return 0;
   }
   TcArgs a{d_batch_rows, d_batch_slots, d_sel, d_nbr_index, u_begin, u_end, tiles_per_cta, pruning ? 1 : 0};
   dim3 grid(cand_tiles, static_cast<unsigned>((tiles + tiles_per_cta - 1) / tiles_per_cta));
   const int smem = static_cast<int>(sizeof(SharedTc)) + 1024;
+  auto launch = [&](auto kernel) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    kernel<<<grid, kTcThreads, smem, stream>>>(s, a, map_a_hi, map_a_lo, map_b_hi, map_b_lo);
+  };
   if (symmetric) {
-    cudaFuncSetAttribute(k_scan_tiles_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_scan_tiles_tc<true><<<grid, kTcThreads, smem, stream>>>(s, a, map_a_hi, map_a_lo, map_b_hi, map_b_lo);
+    if (op.half) launch(k_scan_tiles_tc<true, true>);
+    else launch(k_scan_tiles_tc<true, false>);
   } else {
-    cudaFuncSetAttribute(k_scan_tiles_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    k_scan_tiles_tc<false><<<grid, kTcThreads, smem, stream>>>(s, a, map_a_hi, map_a_lo, map_b_hi, map_b_lo);
+    if (op.half) launch(k_scan_tiles_tc<false, true>);
+    else launch(k_scan_tiles_tc<false, false>);
   }
   return 1;
 }

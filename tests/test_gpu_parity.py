@@ -768,10 +768,11 @@ def test_dot_product_form_on_256_candidate_tiles(ctx, chk, seed, kind, n):
     np.testing.assert_allclose(again[1], dist, rtol=1e-9)
 
 
+@pytest.mark.parametrize("form", [4, 6], ids=["tf32", "fp16"])
 @pytest.mark.parametrize("seed,kind,n", FUZZ[::3], ids=[f"{k}-n{n}" for _, k, n in FUZZ[::3]])
-def test_dot_product_form_on_the_tensor_cores(ctx, chk, seed, kind, n):
-    """k_scan_tiles_tc (dot_form = 4: tcgen05.mma kind::tf32 on rows split into two tf32 parts,
-    accumulators in tensor memory; csrc/tc_kernels.cu), forced from the first launch on batches
+def test_dot_product_form_on_the_tensor_cores(ctx, chk, seed, kind, n, form):
+    """k_scan_tiles_tc (dot_form = 4: tcgen05.mma kind::tf32 on rows split into two tf32 parts; 6:
+    kind::f16 on two fp16 parts; accumulators in tensor memory; csrc/tc_kernels.cu), forced from the first launch on batches
     that fill 128-candidate tiles: the wider band and the float64 decision must still give the
     reference's answer, and the answer of the CUDA-core dot form."""
     rng = np.random.default_rng(13000 + seed)
@@ -780,7 +781,7 @@ def test_dot_product_form_on_the_tensor_cores(ctx, chk, seed, kind, n):
     a = int(rng.integers(2, 7))
     k = int(rng.integers(1, 4))
     x = _fuzz_series(rng, kind, m)
-    for name, value in [("dot_form", 4), ("lower_bound", 0), ("first_batch", 4096)]:
+    for name, value in [("dot_form", form), ("lower_bound", 0), ("first_batch", 4096)]:
         ctx.set_option(name, value)
     try:
         ctx.prepare(x, n, w, a)
@@ -1155,7 +1156,7 @@ def test_soak_random_series_shapes_and_options(ctx, chk, case):
         x = np.cumsum(rng.standard_normal(m)).astype(np.float32)
     else:
         x = (np.sin(2 * np.pi * np.arange(m) / rng.integers(20, 200)) + 0.3 * rng.standard_normal(m)).astype(np.float32)
-    opts = {"dot_form": int(rng.choice([1, 2, 3, 4])), "first_batch": int(rng.choice([128, 4096])),
+    opts = {"dot_form": int(rng.choice([1, 2, 3, 4, 5, 6])), "first_batch": int(rng.choice([128, 4096])),
             "lower_bound": int(rng.choice([0, 1])), "filter_in_ws": int(rng.choice([0, 1])),
             "propagate": int(rng.choice([0, 2, 8])), "propagate_every": int(rng.choice([0, 1, 2]))}
     defaults = {"dot_form": 1, "first_batch": 128, "lower_bound": 1, "filter_in_ws": 0, "propagate": 8,

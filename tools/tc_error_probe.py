@@ -1,5 +1,5 @@
 """Absolute error of the exhaustive nn profile (no pruning) under the dot-form kernels against the
-float64 oracle: CUDA cores (dot_form 2) vs tensor cores (dot_form 4).   python tools/tc_error_probe.py"""
+float64 oracle: CUDA cores (dot_form 2) vs tensor cores (dot_form 4: tf32 parts, 6: fp16 parts).   python tools/tc_error_probe.py"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -12,7 +12,7 @@ for kind, m, n in [("noise", 20000, 64), ("noise", 20000, 65), ("noise", 30000, 
     x = rng.random(m).astype(np.float32) if kind == "noise" else np.cumsum(rng.standard_normal(m)).astype(np.float32)
     want = chk.nn_profile(x, n)
     with Context(0) as c:
-        for form in (0, 2, 4):
+        for form in (0, 2, 4, 6):
             c.set_option("dot_form", form)
             c.prepare(x, n, 4, 4)
             got = c.nn_profile().astype(np.float64)
