@@ -30,6 +30,8 @@
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 
+#include <cstdlib>
+
 #include "kernels.hpp"
 
 namespace tsdd_b200 {
@@ -48,12 +50,15 @@ constexpr int kBBytes = kN * kRowPiece;        // 16 KB
 constexpr int kTcStageBytes = 2 * kABytes + 2 * kBBytes;  // A_hi | A_lo | B_hi | B_lo = 48 KB
 constexpr int kTcThreads = 256;
 constexpr uint32_t kTmemCols = 512;        // two accumulator sets of 256 columns
+constexpr int kBinWords = 256;             // 8,192 position bins per tile (a bit each)
 
 struct alignas(16) TcMeta {
   float thr[kM];
   float nub[kN];
   uint32_t jrow[kN];
   float nnorm[kN];
+  float nub_max[kN / 32];      // greatest neighbour bound of every 32-column chunk (the epilogue's one test per chunk)
+  uint32_t bins[kBinWords];    // window tiles: which position bins (row >> bin_shift, folded) hold a neighbour of the tile
   unsigned long long calls;
   uint32_t valid;   // neighbour slots of the tile that hold a row
   uint32_t stop;    // no tile follows: every candidate of the CTA is dead
@@ -167,8 +172,32 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]),
         "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// The registers of an earlier tmem_ld32 may be read after this (they are operands, so that no use moves above the wait).
+__device__ __forceinline__ void tmem_wait(uint32_t (&v)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]), "+r"(v[8]),
+                 "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]), "+r"(v[16]),
+                 "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]), "+r"(v[24]),
+                 "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
+               :
+               : "memory");
+}
+
+// -DTSDD_TC_PROFILE: cycles every role spends in each of its waits, printed by a few CTAs (development aid)
+#ifdef TSDD_TC_PROFILE
+#define TC_T0() const long long t0_ = clock64()
+#define TC_ACC(x) (x) += clock64() - t0_
+#else
+#define TC_T0()
+#define TC_ACC(x)
+#endif
+
+// -DTSDD_TC_EXP=bits: timing experiments (results are WRONG under them): 1 the epilogue only drains tensor
+// memory, 2 the producer leaves the neighbour boxes out, 4 one MMA per k-step instead of three, 8 no A boxes
+#ifndef TSDD_TC_EXP
+#define TSDD_TC_EXP 0
+#endif
 
 struct TcArgs {
   const uint32_t* batch_rows;
@@ -226,6 +255,7 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
   const uint32_t tmem_base = sh.tmem_base;
 
   const bool window = a.nbr_index != nullptr;
+  const uint32_t bin_shift = 31 - __clz(s.n);  // position bins of 2^bin_shift <= n rows (TcMeta::bins)
   const uint32_t units = (s.n_rows + kN - 1) / kN;  // 256-row units of the (hash-sorted or positional) row order
   constexpr uint32_t kStageCols = kHalf ? 32 : 16;  // columns of one 64-byte row piece
   const uint32_t chunks = s.stride / kStageCols;
@@ -244,16 +274,49 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
     // ================================================================ metadata, one tile ahead of the streams
     const uint64_t best = a.pruning ? *s.best : 0ull;
     unsigned long long calls_total = 0, tiles_total = 0, live_total = 0;
+    long long w_a = 0;
+    const long long t_start = clock64();
+    // Everything a tile needs from global memory is requested in ONE batch before anything is used
+    // (this warp is the head of the pipeline: with its loads one behind the other it, not the tensor
+    // cores, set the pace — 22,000 cycles a tile), and the neighbour rows of the NEXT tile, on which
+    // that tile's other loads depend, are requested a tile ahead.
+    auto rows_of = [&](uint32_t slot0, uint32_t (&j)[kN / 32]) {
+#pragma unroll
+      for (int q = 0; q < kN / 32; ++q) {
+        const uint32_t slot = slot0 + lane + 32 * q;
+        j[q] = slot < s.n_rows ? (window ? __ldg(a.nbr_index + slot) : slot) : 0xFFFFFFFFu;
+      }
+    };
+    uint32_t j_next[kN / 32];
+    if (n_tiles) rows_of(slot0_of(u_first), j_next);
     for (uint32_t ti = 0; ti <= n_tiles; ++ti) {
       const uint32_t m = ti % kMetaSlots, use = ti / kMetaSlots;
       TcMeta& meta = sh.meta[m];
-      if (use >= 1) bar_wait(&sh.meta_empty[m], (use - 1) & 1, 1);
       bool any_live = false;
       unsigned long long calls = 0;
       uint32_t slot0 = 0, valid = 0;
+      uint32_t j[kN / 32];
+      uint64_t key_n[kN / 32], key_c[kM / 32];
+      float norm_n[kN / 32];
       if (ti < n_tiles) {
         slot0 = slot0_of(u_first + ti);
         valid = slot0 < s.n_rows ? min(static_cast<uint32_t>(kN), s.n_rows - slot0) : 0u;
+#pragma unroll
+        for (int q = 0; q < kN / 32; ++q) {
+          j[q] = j_next[q];
+          if (j[q] != 0xFFFFFFFFu) TSDD_BOUND(j[q], s.n_rows);
+          key_n[q] = j[q] != 0xFFFFFFFFu ? ld_key(s.nn + j[q]) : 0ull;
+          norm_n[q] = j[q] != 0xFFFFFFFFu ? __ldg(s.row_norms + j[q]) : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < kM / 32; ++q) {
+          const uint32_t row = sh.cand[lane + 32 * q];
+          key_c[q] = (row != 0xFFFFFFFFu && a.pruning) ? ld_key(s.nn + row) : 0ull;
+        }
+        if (ti + 1 < n_tiles) rows_of(slot0_of(u_first + ti + 1), j_next);
+      }
+      if (use >= 1) { TC_T0(); bar_wait(&sh.meta_empty[m], (use - 1) & 1, 1); TC_ACC(w_a); }
+      if (ti < n_tiles) {
 #pragma unroll
         for (int q = 0; q < kM / 32; ++q) {
           const uint32_t r = lane + 32 * q, row = sh.cand[r];
@@ -262,7 +325,7 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
             if (!a.pruning) {
               thr = inf;
             } else {
-              const float bound = fminf(__uint_as_float(key_bits(ld_key(s.nn + row))), sh.loc[r]);
+              const float bound = fminf(__uint_as_float(key_bits(key_c[q])), sh.loc[r]);
               if (!dead_bound(bound, best, s.margin, s.margin_abs, s.margin_q)) thr = bound;
             }
           }
@@ -279,15 +342,36 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
             calls += valid - overlap;
           }
         }
+        if (window) {
+#pragma unroll
+          for (int q = 0; q < kBinWords / 32; ++q) meta.bins[lane + 32 * q] = 0u;
+          __syncwarp();
+        }
+        float top[kN / 32];
 #pragma unroll
         for (int q = 0; q < kN / 32; ++q) {
-          const uint32_t e = lane + 32 * q, slot = slot0 + e;
-          uint32_t j = 0xFFFFFFFFu;
-          if (slot < s.n_rows) j = window ? a.nbr_index[slot] : slot;
-          if (j != 0xFFFFFFFFu) TSDD_BOUND(j, s.n_rows);
-          meta.jrow[e] = j;
-          meta.nub[e] = j != 0xFFFFFFFFu ? __uint_as_float(key_bits(ld_key(s.nn + j))) : -1.f;
-          meta.nnorm[e] = j != 0xFFFFFFFFu ? s.row_norms[j] : 0.f;
+          const uint32_t e = lane + 32 * q;
+          meta.jrow[e] = j[q];
+          // A neighbour that is dead already (its bound cannot beat the best-so-far) has no use for a
+          // lower bound: it takes no symmetric updates, and does not trip the epilogue's per-chunk test.
+          float nub = j[q] != 0xFFFFFFFFu ? __uint_as_float(key_bits(key_n[q])) : -1.f;
+          if (a.pruning && nub >= 0.f && dead_bound(nub, best, s.margin, s.margin_abs, s.margin_q)) nub = -1.f;
+          meta.nub[e] = nub;
+          meta.nnorm[e] = norm_n[q];
+          top[q] = nub;
+          if (window && j[q] != 0xFFFFFFFFu) {
+            const uint32_t bin = (j[q] >> bin_shift) & (kBinWords * 32 - 1);
+            atomicOr(&meta.bins[bin >> 5], 1u << (bin & 31));
+          }
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+#pragma unroll
+          for (int q = 0; q < kN / 32; ++q) top[q] = fmaxf(top[q], __shfl_xor_sync(0xFFFFFFFFu, top[q], d));
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int q = 0; q < kN / 32; ++q) meta.nub_max[q] = top[q];
         }
         any_live = __any_sync(0xFFFFFFFFu, any_live);
 #pragma unroll
@@ -305,6 +389,10 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
       calls_total += calls;
       tiles_total += 1;
     }
+#ifdef TSDD_TC_PROFILE
+    if (lane == 0 && blockIdx.y == 0 && blockIdx.x % 64 == 0)
+      printf("tc meta cta %u: total %lld wait meta_empty %lld tiles %llu of %u\n", blockIdx.x, clock64() - t_start, w_a, tiles_total, n_tiles);
+#endif
     if (lane == 0) {
       if (calls_total) atomicAdd(&s.counters->calls, calls_total);
       if (tiles_total) atomicAdd(&s.counters->tiles, tiles_total);
@@ -315,9 +403,11 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
   } else if (warp == 0) {
     // ================================================================ producer: the TMA streams
     uint32_t seq = 0;
+    long long w_meta = 0, w_a = 0;
+    const long long t_start = clock64();
     for (uint32_t ti = 0;; ++ti) {
       const uint32_t m = ti % kMetaSlots;
-      bar_wait(&sh.meta_full[m], (ti / kMetaSlots) & 1, 2);
+      { TC_T0(); bar_wait(&sh.meta_full[m], (ti / kMetaSlots) & 1, 2); TC_ACC(w_meta); }
       const bool stop = *reinterpret_cast<volatile uint32_t*>(&sh.meta[m].stop) != 0;
       const uint32_t slot0 = *reinterpret_cast<volatile uint32_t*>(&sh.meta[m].slot0);
       __syncwarp();
@@ -325,35 +415,45 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
       if (stop) break;
       for (uint32_t c = 0; c < chunks; ++c) {
         const uint32_t st = seq % kTcStages, round = seq / kTcStages;
-        if (round >= 1) bar_wait(&sh.empty[st], (round - 1) & 1, 3);
+        if (round >= 1) { TC_T0(); bar_wait(&sh.empty[st], (round - 1) & 1, 3); TC_ACC(w_a); }
         if (lane == 0) {
-          bar_expect_tx(&sh.full[st], kTcStageBytes);
+          bar_expect_tx(&sh.full[st], ((TSDD_TC_EXP & 8) ? 0 : 2 * kABytes) + ((TSDD_TC_EXP & 2) ? 0 : 2 * kBBytes));
           unsigned char* dst = sh.stages[st];
           const uint32_t col = c * kStageCols;
-          tma_box(dst, &map_a_hi, col, cand0, &sh.full[st]);
-          tma_box(dst + kABytes, &map_a_lo, col, cand0, &sh.full[st]);
-          tma_box(dst + 2 * kABytes, &map_b_hi, col, slot0, &sh.full[st]);
-          tma_box(dst + 2 * kABytes + kBBytes, &map_b_lo, col, slot0, &sh.full[st]);
+          if (!(TSDD_TC_EXP & 8)) {
+            tma_box(dst, &map_a_hi, col, cand0, &sh.full[st]);
+            tma_box(dst + kABytes, &map_a_lo, col, cand0, &sh.full[st]);
+          }
+          if (!(TSDD_TC_EXP & 2)) {
+            tma_box(dst + 2 * kABytes, &map_b_hi, col, slot0, &sh.full[st]);
+            tma_box(dst + 2 * kABytes + kBBytes, &map_b_lo, col, slot0, &sh.full[st]);
+          }
         }
         ++seq;
       }
     }
+#ifdef TSDD_TC_PROFILE
+    if (lane == 0 && blockIdx.y == 0 && blockIdx.x % 64 == 0)
+      printf("tc producer cta %u: total %lld wait meta %lld wait empty %lld stages %u\n", blockIdx.x, clock64() - t_start, w_meta, w_a, seq);
+#endif
   } else if (warp == 1) {
     // ================================================================ MMA issuer
     uint32_t seq = 0;
+    long long w_meta = 0, w_a = 0, w_b = 0;
+    const long long t_start = clock64();
     for (uint32_t ti = 0;; ++ti) {
       const uint32_t m = ti % kMetaSlots, buf = ti & 1;
-      bar_wait(&sh.meta_full[m], (ti / kMetaSlots) & 1, 4);
+      { TC_T0(); bar_wait(&sh.meta_full[m], (ti / kMetaSlots) & 1, 4); TC_ACC(w_meta); }
       const bool stop = *reinterpret_cast<volatile uint32_t*>(&sh.meta[m].stop) != 0;
       __syncwarp();
       if (lane == 0) bar_arrive(&sh.meta_empty[m]);
       if (stop) break;
-      if (ti >= 2) bar_wait(&sh.tmem_empty[buf], ((ti >> 1) - 1) & 1, 5);  // the epilogue has drained this accumulator set
+      if (ti >= 2) { TC_T0(); bar_wait(&sh.tmem_empty[buf], ((ti >> 1) - 1) & 1, 5); TC_ACC(w_a); }  // the epilogue has drained this accumulator set
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t tmem_d = tmem_base + buf * kN;
       for (uint32_t c = 0; c < chunks; ++c) {
         const uint32_t st = seq % kTcStages, round = seq / kTcStages;
-        bar_wait(&sh.full[st], round & 1, 6);
+        { TC_T0(); bar_wait(&sh.full[st], round & 1, 6); TC_ACC(w_b); }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (lane == 0) {
           const uint32_t base = smem_u32(sh.stages[st]);
@@ -363,8 +463,10 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
           for (uint32_t k = 0; k < 2; ++k) {  // two k-steps of 32 bytes (8 tf32 / 16 fp16 columns) per stage
             const uint64_t step = static_cast<uint64_t>((k * 32) >> 4);
             umma<kHalf>(tmem_d, a_hi + step, b_hi + step, (c | k) != 0 ? 1u : 0u);
-            umma<kHalf>(tmem_d, a_hi + step, b_lo + step, 1u);
-            umma<kHalf>(tmem_d, a_lo + step, b_hi + step, 1u);
+            if (!(TSDD_TC_EXP & 4)) {
+              umma<kHalf>(tmem_d, a_hi + step, b_lo + step, 1u);
+              umma<kHalf>(tmem_d, a_lo + step, b_hi + step, 1u);
+            }
           }
           umma_commit(&sh.empty[st]);                          // the stage is free once these MMAs have read it
           if (c + 1 == chunks) umma_commit(&sh.tmem_full[buf]);  // ... and the tile's accumulators are complete
@@ -373,6 +475,10 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
         ++seq;
       }
     }
+#ifdef TSDD_TC_PROFILE
+    if (lane == 0 && blockIdx.y == 0 && blockIdx.x % 64 == 0)
+      printf("tc mma cta %u: total %lld wait meta %lld wait tmem_empty %lld wait full %lld stages %u\n", blockIdx.x, clock64() - t_start, w_meta, w_a, w_b, seq);
+#endif
   } else if (warp >= 4) {
     // ================================================================ epilogue: thread = candidate = TMEM lane
     const uint32_t mrow = tid - 128;                 // candidate (TMEM lane) of this thread
@@ -382,9 +488,14 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
     const float d_floor = 0.5f * s.margin_abs;
     unsigned long long tiles_done = 0, useful = 0;
     uint32_t overlap_total = 0;
+    long long w_meta = 0, w_a = 0;
+    const long long t_start = clock64();
+#ifdef TSDD_TC_PROFILE
+    uint32_t n_slow = 0, n_slow_thr = 0, n_near = 0, n_part = 0;
+#endif
     for (uint32_t ti = 0;; ++ti) {
       const uint32_t m = ti % kMetaSlots, buf = ti & 1;
-      bar_wait(&sh.meta_full[m], (ti / kMetaSlots) & 1, 7);
+      { TC_T0(); bar_wait(&sh.meta_full[m], (ti / kMetaSlots) & 1, 7); TC_ACC(w_meta); }
       TcMeta& meta = sh.meta[m];
       if (*reinterpret_cast<volatile uint32_t*>(&meta.stop) != 0) {
         __syncwarp();
@@ -392,39 +503,83 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
         break;
       }
       const float thr = meta.thr[mrow];
-      bar_wait(&sh.tmem_full[buf], (ti >> 1) & 1, 8);
+      { TC_T0(); bar_wait(&sh.tmem_full[buf], (ti >> 1) & 1, 8); TC_ACC(w_a); }
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       uint32_t d_min = 0xFFFFFFFFu, j_min = 0xFFFFFFFFu;
       const bool taking_part = thr >= 0.f && row != 0xFFFFFFFFu;
-#pragma unroll 1
-      for (uint32_t cc = 0; cc < kN / 32; ++cc) {
-        uint32_t v[32];
-        tmem_ld32(tmem_base + (lane_base << 16) + buf * kN + cc * 32, v);
+#ifdef TSDD_TC_PROFILE
+      n_part += taking_part ? 1 : 0;
+#endif
+      // Per 32-column chunk ONE test decides whether anything has to be looked at pair by pair: the
+      // chunk's smallest distance (32 FFMA + 32 FMNMX, no branch) against the candidate's threshold
+      // and the chunk's greatest neighbour bound.  (|b|^2 - 2 a.b) + |a|^2 and the floor are monotone,
+      // so the smallest of the 32 distances is exactly what the pair-by-pair path would compute.
+      // The accumulators of chunk c+1 are on their way from tensor memory while chunk c is measured.
+      const uint32_t taddr = tmem_base + (lane_base << 16) + buf * kN;
+      auto measure = [&](const uint32_t (&v)[32], uint32_t cc) {
+        float low = inf;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const uint32_t n = cc * 32 + i;
-          const float nub = kSymmetric ? meta.nub[n] : -1.f;
-          const float d = fmaxf(fmaf(-2.f, __uint_as_float(v[i]), cn + meta.nnorm[n]), d_floor);
-          if (taking_part && (d <= thr || d < nub)) {
-            const uint32_t j = meta.jrow[n];
-            if (j != 0xFFFFFFFFu && gap(row, j) >= s.n) {
-              const uint32_t bits = __float_as_uint(d);
-              if (d <= thr && (bits < d_min || (bits == d_min && j < j_min))) d_min = bits, j_min = j;
-              if (d < nub) {
-                TSDD_BOUND(j, s.n_rows);
-                atomicMin(as_ull(s.nn + j), static_cast<unsigned long long>(nn_key(bits, row)));
+        for (int i = 0; i < 32; ++i) low = fminf(low, fmaf(-2.f, __uint_as_float(v[i]), meta.nnorm[cc * 32 + i]));
+        const float d_low = fmaxf(low + cn, d_floor);
+        if ((TSDD_TC_EXP & 1) && d_low != 12345.678f) return;
+        if (taking_part && (d_low <= thr || (kSymmetric && d_low < meta.nub_max[cc]))) {
+#ifdef TSDD_TC_PROFILE
+          n_slow += 1; n_slow_thr += d_low <= thr ? 1 : 0;
+#endif
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {  // (fully unrolled: the accumulators stay in registers)
+            const uint32_t n = cc * 32 + i;
+            const float nub = kSymmetric ? meta.nub[n] : -1.f;
+            const float d = fmaxf(fmaf(-2.f, __uint_as_float(v[i]), meta.nnorm[n]) + cn, d_floor);
+            if (d <= thr || d < nub) {
+              const uint32_t j = meta.jrow[n];
+              if (j != 0xFFFFFFFFu && gap(row, j) >= s.n) {
+                const uint32_t bits = __float_as_uint(d);
+                if (d <= thr && (bits < d_min || (bits == d_min && j < j_min))) d_min = bits, j_min = j;
+                if (d < nub) {
+                  TSDD_BOUND(j, s.n_rows);
+                  atomicMin(as_ull(s.nn + j), static_cast<unsigned long long>(nn_key(bits, row)));
+                }
               }
             }
           }
         }
-        if (window && taking_part) {  // self-match pairs of a window tile (the producer counted live x valid)
-#pragma unroll 8
-          for (int i = 0; i < 32; ++i) overlap_total += gap(row, meta.jrow[cc * 32 + i]) < s.n ? 1u : 0u;
+      };
+      {
+        uint32_t v0[32], v1[32];
+        tmem_ld32(taddr, v0);
+#pragma unroll 1
+        for (uint32_t cc = 0; cc < kN / 32; cc += 2) {
+          tmem_wait(v0);
+          tmem_ld32(taddr + (cc + 1) * 32, v1);
+          measure(v0, cc);
+          __syncwarp();  // (the pair-by-pair path diverges; tcgen05.ld / wait are warp-wide)
+          tmem_wait(v1);
+          if (cc + 2 < kN / 32) tmem_ld32(taddr + (cc + 2) * 32, v0);
+          measure(v1, cc + 1);
+          __syncwarp();
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) bar_arrive(&sh.tmem_empty[buf]);
+      if (window && taking_part) {
+        // self-match pairs of a window tile (the metadata warp counted live x valid): only a candidate one of
+        // whose position bins holds a neighbour of the tile has any to count
+        const uint32_t z0 = row >= s.n - 1 ? row - (s.n - 1) : 0u, z1 = row + s.n - 1;
+        bool near = false;
+        for (uint32_t b = z0 >> bin_shift; b <= (z1 >> bin_shift); ++b) {
+          const uint32_t bin = b & (kBinWords * 32 - 1);
+          near |= (meta.bins[bin >> 5] >> (bin & 31)) & 1u;
+        }
+        if (near) {
+#ifdef TSDD_TC_PROFILE
+          n_near += 1;
+#endif
+#pragma unroll 8
+          for (int i = 0; i < kN; ++i) overlap_total += gap(row, meta.jrow[i]) < s.n ? 1u : 0u;
+        }
+      }
       if (j_min != 0xFFFFFFFFu) {
         TSDD_BOUND(row, s.n_rows);
         atomicMin(as_ull(s.nn + row), static_cast<unsigned long long>(nn_key(d_min, j_min)));
@@ -435,6 +590,15 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
       __syncwarp();
       if (lane == 0) bar_arrive(&sh.meta_empty[m]);
     }
+#ifdef TSDD_TC_PROFILE
+    if (blockIdx.y == 0 && blockIdx.x % 64 == 0) {
+      const uint32_t any_slow = __reduce_add_sync(0xFFFFFFFFu, n_slow), any_thr = __reduce_add_sync(0xFFFFFFFFu, n_slow_thr),
+                     any_near = __reduce_add_sync(0xFFFFFFFFu, n_near), any_part = __reduce_add_sync(0xFFFFFFFFu, n_part);
+      if (lane == 0)
+        printf("tc epilogue cta %u: total %lld wait meta %lld wait tmem_full %lld tiles %llu slow %u slowthr %u near %u part %u\n", blockIdx.x,
+               clock64() - t_start, w_meta, w_a, tiles_done, any_slow, any_thr, any_near, any_part);
+    }
+#endif
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
       useful += __shfl_xor_sync(0xFFFFFFFFu, useful, d);
@@ -563,8 +727,10 @@ int launch_scan_tiles_tc(SearchState s, const TcOperands& op, const uint32_t* d_
   const uint32_t u_begin = k_begin / 2, u_end = (k_end + 1) / 2;
   const uint32_t cand_tiles = (live_upper_bound + kM - 1) / kM;
   const uint64_t tiles = u_end - u_begin;
-  const uint64_t want = tiles * cand_tiles / (148ull * 8ull);
-  const int tiles_per_cta = static_cast<int>(want < 1 ? 1 : want > 16 ? 16 : want);
+  static const int waves = [] { const char* e = std::getenv("TSDD_TC_WAVES"); return e ? std::atoi(e) : 8; }();
+  static const int most = [] { const char* e = std::getenv("TSDD_TC_MOST"); return e ? std::atoi(e) : 16; }();
+  const uint64_t want = tiles * cand_tiles / (148ull * waves);
+  const int tiles_per_cta = static_cast<int>(want < 1 ? 1 : want > static_cast<uint64_t>(most) ? most : want);
   const bool window = d_nbr_index != nullptr;
   CUtensorMap map_a_hi{}, map_a_lo{}, map_b_hi{}, map_b_lo{};
   const float* b_hi = window ? op.sorted_hi : op.rows_hi;
