@@ -225,8 +225,9 @@ struct tsdd_cuda_ctx {
   // tensor-core experiment: the matrix, its hash-sorted copy and the batch split into tf32 parts
   DeviceArray<float> matrix_hi, matrix_lo, sorted_hi, sorted_lo, batch_hi, batch_lo;
   bool split_ready = false, sorted_split_ready = false;
-  bool opt_tensor_cores = false;
-  bool opt_tc_half = false;   // the split parts are fp16 (dot_form 5 / 6) instead of tf32 (3 / 4)
+  // the dot-product form runs on the tensor cores (csrc/tc_kernels.cu) with fp16 hi / lo parts: dot_form 5, the default
+  bool opt_tensor_cores = true;
+  bool opt_tc_half = true;    // the split parts are fp16 (dot_form 5 / 6) instead of tf32 (3 / 4)
   bool series_is_f32 = false; // series_f32 holds the prepared series' float32 originals (series = the same values, widened)
   bool norms_ready = false;   // row_norms holds the norms of the prepared matrix
   bool sorted_ready = false;  // matrix_sorted holds the prepared matrix in the hash-sorted order
@@ -242,7 +243,7 @@ struct tsdd_cuda_ctx {
   DeviceArray<uint32_t> flags, batch_rows, batch_alt, batch_slots, batch_slots_alt, sel;
   DeviceArray<float> batch_matrix;
   DeviceArray<double> zrow;
-  DeviceArray<uint32_t> finalists, seed_lb;
+  DeviceArray<uint32_t> finalists, seed_lb, tc_work;
   DeviceArray<uint64_t> finalist_keys;
   DeviceArray<unsigned long long> nn_bits;
   uint32_t batch_capacity = 0;
@@ -728,7 +729,7 @@ void ensure_batch_capacity(tsdd_cuda_ctx* ctx, uint32_t batch) {
   ctx->batch_slots.alloc(padded);
   ctx->batch_slots_alt.alloc(padded);
   ctx->batch_matrix.alloc(static_cast<size_t>(padded) * ctx->stride);
-  if (ctx->opt_tensor_cores) {
+  if (ctx->opt_tensor_cores && ctx->split_ready) {
     ctx->batch_hi.alloc(static_cast<size_t>(padded) * ctx->stride);
     ctx->batch_lo.alloc(static_cast<size_t>(padded) * ctx->stride);
   }
@@ -878,8 +879,9 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
     const char* launch_error = nullptr;
     int launched = 0;
     if (choice_now.tc) {
+      ctx->tc_work.alloc(1);
       const TcOperands op{ctx->batch_hi.ptr, ctx->batch_lo.ptr, ctx->matrix_hi.ptr, ctx->matrix_lo.ptr,
-                          ctx->sorted_hi.ptr, ctx->sorted_lo.ptr, ctx->rows_padded, ctx->opt_tc_half};
+                          ctx->sorted_hi.ptr, ctx->sorted_lo.ptr, ctx->rows_padded, ctx->opt_tc_half, ctx->tc_work.ptr};
       launched = launch_scan_tiles_tc(s, op, list, slots, ctx->sel.ptr, count, plan[r].window ? ctx->sorted_row : nullptr,
                                       plan[r].k_begin, plan[r].k_end, pruning, ctx->opt_symmetric, st, &launch_error);
       if (launched) ctx->stats.scan_kernel_tc_launches += launched;
@@ -982,19 +984,20 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
             }
           }
           if (ctx->dot_now && ctx->opt_tensor_cores && !ctx->split_ready) {
-            // the tensor-core experiment: tf32 hi / lo parts of the matrix (and of its hash-sorted copy)
+            // the tensor-core form: fp16 (or tf32) hi / lo parts of the matrix and of its hash-sorted copy
             const size_t floats = static_cast<size_t>(ctx->rows_padded) * ctx->stride;
+            const size_t words = ctx->opt_tc_half ? (floats + 1) / 2 : floats;  // (the arrays are float-typed; fp16 parts take half)
             size_t free_b = 0, total_b = 0;
-            const bool have = ctx->matrix_hi.count >= floats && (!ctx->sorted_ready || ctx->sorted_hi.count >= floats);
+            const bool have = ctx->matrix_hi.count >= words && (!ctx->sorted_ready || ctx->sorted_hi.count >= words);
             if (!have) CUDA_OK(cudaMemGetInfo(&free_b, &total_b));  // (slow: only when the copies have to grow)
-            const size_t need = floats * sizeof(float) * (ctx->sorted_ready ? 4 : 2);
+            const size_t need = words * sizeof(float) * (ctx->sorted_ready ? 4 : 2);
             if (have || free_b > need + (size_t{2} << 30)) {
-              ctx->matrix_hi.alloc(floats);
-              ctx->matrix_lo.alloc(floats);
+              ctx->matrix_hi.alloc(words);
+              ctx->matrix_lo.alloc(words);
               ctx->stats.kernel_launches += launch_split_rows(ctx->matrix.ptr, floats, ctx->opt_tc_half, ctx->matrix_hi.ptr, ctx->matrix_lo.ptr, st);
               if (ctx->sorted_ready) {
-                ctx->sorted_hi.alloc(floats);
-                ctx->sorted_lo.alloc(floats);
+                ctx->sorted_hi.alloc(words);
+                ctx->sorted_lo.alloc(words);
                 ctx->stats.kernel_launches +=
                     launch_split_rows(ctx->matrix_sorted.ptr, floats, ctx->opt_tc_half, ctx->sorted_hi.ptr, ctx->sorted_lo.ptr, st);
                 ctx->sorted_split_ready = true;
@@ -1443,6 +1446,7 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
       const int form = static_cast<int>(value);
       ctx->opt_dot = form >= 5 ? form - 4 : form >= 3 ? form - 2 : form;  // 3 / 4 and 5 / 6: as 1 / 2 ...
       ctx->opt_tensor_cores = form >= 3;                                  // ... on the tensor cores,
+      if (ctx->opt_tc_half != (form >= 5)) ctx->split_ready = ctx->sorted_split_ready = false;  // (copies in the other format)
       ctx->opt_tc_half = form >= 5;                                       // ... with tf32 (3 / 4) or fp16 (5 / 6) parts
     } else if (key == "shard_prep") {
       ctx->opt_shard_prep = value != 0;
@@ -1537,6 +1541,7 @@ int tsdd_cuda_reindex(tsdd_cuda_ctx* ctx, size_t word_len, size_t alphabet) {
     ctx->alphabet = alphabet;
     ctx->sorted_ready = false;  // (the hash-sorted copy of the matrix follows the OLD order)
     ctx->sorted_split_ready = false;
+    ctx->split_ready = false;   // (both split copies are rebuilt together at the next switch to the dot form)
     CUDA_OK(cudaEventRecord(ctx->ev_a, st));
     uint64_t launches = launch_window_encode(ctx->series.ptr, ctx->rows, static_cast<uint32_t>(ctx->n),
                                              static_cast<uint32_t>(word_len), static_cast<uint32_t>(alphabet),

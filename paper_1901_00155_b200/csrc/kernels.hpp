@@ -192,6 +192,7 @@ struct TcOperands {
   const float *sorted_hi, *sorted_lo;  // its hash-sorted copy, split (window tiles)
   uint64_t rows_padded;                // rows of each of the four neighbour arrays
   bool half;                           // the parts are fp16 (kind::f16, 22 bits between them) instead of tf32 (kind::tf32, 21 bits)
+  uint32_t* work;                      // one word of device memory: the launch's work-item counter
 };
 int launch_split_rows(const float* d_in, size_t floats, bool half, float* d_hi, float* d_lo, cudaStream_t stream);
 int launch_gather_rows_split(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel, uint32_t capacity_padded,

@@ -52,26 +52,26 @@ constexpr int kTcThreads = 256;
 constexpr uint32_t kTmemCols = 512;        // two accumulator sets of 256 columns
 constexpr int kBinWords = 256;             // 8,192 position bins per tile (a bit each)
 
+constexpr float kNoColumn = 1e30f;         // "norm" of a column that holds no row / takes no symmetric update: never the smallest
+
 struct alignas(16) TcMeta {
-  float thr[kM];
-  float nub[kN];
-  uint32_t jrow[kN];
-  float nnorm[kN];
-  float nub_max[kN / 32];      // greatest neighbour bound of every 32-column chunk (the epilogue's one test per chunk)
+  float thr[kM];               // the candidates' thresholds (their bounds; -1: dead or no candidate)
+  uint32_t cand[kM];           // ... their rows
+  float cnorm[kM];             // ... and squared norms
+  uint32_t jrow[kN];           // the neighbours' rows (0xFFFFFFFF: none)
+  float nnorm[kN];             // ... squared norms (kNoColumn: none)
+  float lim[kN];               // ... the distance below which a symmetric update kills the neighbour (-1: takes none)
+  float w[kN];                 // nnorm - lim (kNoColumn: takes none): the epilogue's one test per chunk
   uint32_t bins[kBinWords];    // window tiles: which position bins (row >> bin_shift, folded) hold a neighbour of the tile
-  unsigned long long calls;
   uint32_t valid;   // neighbour slots of the tile that hold a row
-  uint32_t stop;    // no tile follows: every candidate of the CTA is dead
+  uint32_t stop;    // no tile follows
   uint32_t slot0;   // first neighbour slot of the tile
-  uint32_t pad[3];
+  uint32_t cand0;   // first candidate slot of the tile (of the work item it belongs to)
 };
 
 struct SharedTc {
   alignas(1024) unsigned char stages[kTcStages][kTcStageBytes];
   TcMeta meta[kMetaSlots];
-  uint32_t cand[kM];
-  float cnorm[kM];
-  float loc[kM];
   unsigned long long full[kTcStages], empty[kTcStages], tmem_full[2], tmem_empty[2], meta_full[kMetaSlots], meta_empty[kMetaSlots];
   uint32_t tmem_base;
 };
@@ -205,8 +205,10 @@ struct TcArgs {
   const uint32_t* sel;
   const uint32_t* nbr_index;  // hash-sorted row list (window mode) or nullptr
   uint32_t u_begin, u_end;    // 256-row neighbour tiles of this launch
-  int tiles_per_cta;
+  uint32_t tiles_per_item;    // neighbour tiles of one work item
   int pruning;
+  uint32_t* work;             // the launch's work-item counter (zero at launch)
+  float lim_factor;
 };
 
 template <bool kSymmetric, bool kHalf>
@@ -215,24 +217,13 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
                 const __grid_constant__ CUtensorMap map_a_lo, const __grid_constant__ CUtensorMap map_b_hi,
                 const __grid_constant__ CUtensorMap map_b_lo) {
   extern __shared__ unsigned char smem_raw[];
-  // (the 128-byte swizzle wants 1024-byte aligned tiles: align by hand, the launch adds the slack)
+  // (swizzled tiles want 1024-byte alignment: align by hand, the launch adds the slack)
   SharedTc& sh = *reinterpret_cast<SharedTc*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
 
   const uint32_t count = a.sel[0];
-  // (candidate tiles are the FAST grid dimension: the CTAs that run side by side walk the same
-  // neighbour tiles — in a covering scan literally, in a window round nearly — so those come from L2)
-  const uint32_t cand0 = blockIdx.x * kM;
-  if (cand0 >= count) return;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float inf = __uint_as_float(kInfBits);
 
-  if (tid < kM) {
-    const uint32_t row = (cand0 + tid < count) ? a.batch_rows[cand0 + tid] : 0xFFFFFFFFu;
-    if (row != 0xFFFFFFFFu) TSDD_BOUND(row, s.n_rows);
-    sh.cand[tid] = row;
-    sh.loc[tid] = inf;
-    sh.cnorm[tid] = row != 0xFFFFFFFFu ? s.row_norms[row] : 0.f;
-  }
   if (tid == 0) {
     for (int i = 0; i < kTcStages; ++i) bar_init(&sh.full[i], 1), bar_init(&sh.empty[i], 1);
     for (int i = 0; i < 2; ++i) {
@@ -259,27 +250,37 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
   const uint32_t units = (s.n_rows + kN - 1) / kN;  // 256-row units of the (hash-sorted or positional) row order
   constexpr uint32_t kStageCols = kHalf ? 32 : 16;  // columns of one 64-byte row piece
   const uint32_t chunks = s.stride / kStageCols;
-  const uint32_t u_first = a.u_begin + blockIdx.y * a.tiles_per_cta;
-  const uint32_t n_tiles = u_first < a.u_end ? min(static_cast<uint32_t>(a.tiles_per_cta), a.u_end - u_first) : 0u;
-  const uint32_t centre = window ? a.batch_slots[min(cand0 + kM / 2, count - 1)] / kN : 0u;
-  // window mode: units around the candidate tile's own, alternating outwards; covering mode: unit u itself
-  auto slot0_of = [&](uint32_t u) -> uint32_t {
-    if (!window) return u * kN;
-    const uint32_t step = (u + 1) >> 1;
-    const uint32_t unit = (u & 1) ? (centre + step) % units : (centre + units - step % units) % units;
-    return unit * kN;
-  };
 
   if (warp == 3) {
-    // ================================================================ metadata, one tile ahead of the streams
+    // ================================================================ the head of the pipeline: work items and tile metadata
+    // The CTAs of a launch (one per SM) take work items — one candidate tile x `tiles_per_item`
+    // neighbour tiles, candidate tiles the fast index so that the CTAs running side by side walk
+    // the same neighbour tiles (those then come from L2) — off a global counter until none is
+    // left: no wave quantisation, and tensor memory, barriers and pipeline are set up once per SM
+    // and launch.  Everything the other roles need to know about a tile travels in its metadata
+    // slot, the candidate tile included, so an item boundary is no event for them.
     const uint64_t best = a.pruning ? *s.best : 0ull;
+    // the greatest distance that still kills a row (common.cuh: dead_bound); 0 while there is no best-so-far
+    const float best_d = __uint_as_float(key_bits(best));
+    const float kill = a.pruning ? fmaxf((best_d - fmaf(s.margin_q, sqrtf(best_d), s.margin_abs)) / s.margin, 0.f) : 0.f;
+    const uint32_t cand_tiles = (count + kM - 1) / kM;
+    const uint32_t span = a.u_end - a.u_begin;
+    const uint32_t items_per_cand = (span + a.tiles_per_item - 1) / a.tiles_per_item;
+    const uint32_t total_items = cand_tiles * items_per_cand;
     unsigned long long calls_total = 0, tiles_total = 0, live_total = 0;
-    long long w_a = 0;
-    const long long t_start = clock64();
+    [[maybe_unused]] long long w_a = 0;
+    [[maybe_unused]] const long long t_start = clock64();
+    auto slot0_of = [&](uint32_t u, uint32_t centre) -> uint32_t {
+      // window mode: units around the candidate tile's own, alternating outwards; covering mode: unit u itself
+      if (!window) return u * kN;
+      const uint32_t step = (u + 1) >> 1;
+      const uint32_t unit = (u & 1) ? (centre + step) % units : (centre + units - step % units) % units;
+      return unit * kN;
+    };
     // Everything a tile needs from global memory is requested in ONE batch before anything is used
-    // (this warp is the head of the pipeline: with its loads one behind the other it, not the tensor
-    // cores, set the pace — 22,000 cycles a tile), and the neighbour rows of the NEXT tile, on which
-    // that tile's other loads depend, are requested a tile ahead.
+    // (with its loads one behind the other this warp, not the tensor cores, set the pace: 22,000
+    // cycles a tile), and the neighbour rows of the NEXT tile, on which that tile's other loads
+    // depend, are requested a tile ahead.
     auto rows_of = [&](uint32_t slot0, uint32_t (&j)[kN / 32]) {
 #pragma unroll
       for (int q = 0; q < kN / 32; ++q) {
@@ -287,52 +288,72 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
         j[q] = slot < s.n_rows ? (window ? __ldg(a.nbr_index + slot) : slot) : 0xFFFFFFFFu;
       }
     };
-    uint32_t j_next[kN / 32];
-    if (n_tiles) rows_of(slot0_of(u_first), j_next);
-    for (uint32_t ti = 0; ti <= n_tiles; ++ti) {
-      const uint32_t m = ti % kMetaSlots, use = ti / kMetaSlots;
-      TcMeta& meta = sh.meta[m];
-      bool any_live = false;
-      unsigned long long calls = 0;
-      uint32_t slot0 = 0, valid = 0;
-      uint32_t j[kN / 32];
-      uint64_t key_n[kN / 32], key_c[kM / 32];
-      float norm_n[kN / 32];
-      if (ti < n_tiles) {
-        slot0 = slot0_of(u_first + ti);
-        valid = slot0 < s.n_rows ? min(static_cast<uint32_t>(kN), s.n_rows - slot0) : 0u;
+    uint32_t ti = 0;          // tiles published so far
+    bool slot_held = false;   // the next slot has been waited for already (a tile that was not published after all)
+    for (;;) {
+      uint32_t item = 0;
+      if (lane == 0) item = atomicAdd(a.work, 1u);
+      item = __shfl_sync(0xFFFFFFFFu, item, 0);
+      if (item >= total_items) break;
+      const uint32_t cand0 = (item % cand_tiles) * kM;
+      const uint32_t u0 = a.u_begin + (item / cand_tiles) * a.tiles_per_item;
+      const uint32_t n_tiles = min(static_cast<uint32_t>(a.tiles_per_item), a.u_end - u0);
+      uint32_t crow[kM / 32];
+      float cnorm[kM / 32];
+#pragma unroll
+      for (int q = 0; q < kM / 32; ++q) {
+        const uint32_t r = cand0 + lane + 32 * q;
+        crow[q] = r < count ? __ldg(a.batch_rows + r) : 0xFFFFFFFFu;
+      }
+      const uint32_t centre = window ? __ldg(a.batch_slots + min(cand0 + kM / 2, count - 1)) / kN : 0u;
+#pragma unroll
+      for (int q = 0; q < kM / 32; ++q) {
+        if (crow[q] != 0xFFFFFFFFu) TSDD_BOUND(crow[q], s.n_rows);
+        cnorm[q] = crow[q] != 0xFFFFFFFFu ? __ldg(s.row_norms + crow[q]) : 0.f;
+      }
+      uint32_t j_next[kN / 32];
+      rows_of(slot0_of(u0, centre), j_next);
+      for (uint32_t t = 0; t < n_tiles; ++t) {
+        const uint32_t m = ti % kMetaSlots, use = ti / kMetaSlots;
+        TcMeta& meta = sh.meta[m];
+        const uint32_t slot0 = slot0_of(u0 + t, centre);
+        const uint32_t valid = slot0 < s.n_rows ? min(static_cast<uint32_t>(kN), s.n_rows - slot0) : 0u;
+        uint32_t j[kN / 32];
+        uint64_t key_n[kN / 32], key_c[kM / 32];
+        float norm_n[kN / 32];
 #pragma unroll
         for (int q = 0; q < kN / 32; ++q) {
           j[q] = j_next[q];
           if (j[q] != 0xFFFFFFFFu) TSDD_BOUND(j[q], s.n_rows);
-          key_n[q] = j[q] != 0xFFFFFFFFu ? ld_key(s.nn + j[q]) : 0ull;
-          norm_n[q] = j[q] != 0xFFFFFFFFu ? __ldg(s.row_norms + j[q]) : 0.f;
+          key_n[q] = (j[q] != 0xFFFFFFFFu && kSymmetric && a.pruning) ? ld_key(s.nn + j[q]) : 0ull;
+          norm_n[q] = j[q] != 0xFFFFFFFFu ? __ldg(s.row_norms + j[q]) : kNoColumn;
         }
 #pragma unroll
-        for (int q = 0; q < kM / 32; ++q) {
-          const uint32_t row = sh.cand[lane + 32 * q];
-          key_c[q] = (row != 0xFFFFFFFFu && a.pruning) ? ld_key(s.nn + row) : 0ull;
-        }
-        if (ti + 1 < n_tiles) rows_of(slot0_of(u_first + ti + 1), j_next);
-      }
-      if (use >= 1) { TC_T0(); bar_wait(&sh.meta_empty[m], (use - 1) & 1, 1); TC_ACC(w_a); }
-      if (ti < n_tiles) {
+        for (int q = 0; q < kM / 32; ++q) key_c[q] = (crow[q] != 0xFFFFFFFFu && a.pruning) ? ld_key(s.nn + crow[q]) : 0ull;
+        if (t + 1 < n_tiles) rows_of(slot0_of(u0 + t + 1, centre), j_next);
+        if (use >= 1 && !slot_held) { TC_T0(); bar_wait(&sh.meta_empty[m], (use - 1) & 1, 1); TC_ACC(w_a); }
+        slot_held = true;
+        bool any_live = false;
+        unsigned long long calls = 0;
+        uint32_t live = 0;
 #pragma unroll
         for (int q = 0; q < kM / 32; ++q) {
-          const uint32_t r = lane + 32 * q, row = sh.cand[r];
+          const uint32_t r = lane + 32 * q, row = crow[q];
           float thr = -1.f;
           if (row != 0xFFFFFFFFu) {
             if (!a.pruning) {
               thr = inf;
             } else {
-              const float bound = fminf(__uint_as_float(key_bits(key_c[q])), sh.loc[r]);
+              const float bound = __uint_as_float(key_bits(key_c[q]));
               if (!dead_bound(bound, best, s.margin, s.margin_abs, s.margin_q)) thr = bound;
             }
           }
           meta.thr[r] = thr;
+          meta.cand[r] = row;
+          meta.cnorm[r] = cnorm[q];
           if (thr >= 0.f) {
             any_live = true;
-            live_total += 1;
+            live += 1;
             uint32_t overlap = 0;
             if (!window) {  // (window tiles: the epilogue counts the self-match pairs)
               const uint32_t z0 = row >= s.n - 1 ? row - (s.n - 1) : 0, z1 = row + s.n;
@@ -342,56 +363,59 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
             calls += valid - overlap;
           }
         }
+        any_live = __any_sync(0xFFFFFFFFu, any_live);
+        if (!any_live) break;  // every candidate of the tile is dead: the rest of the item is not needed (the slot stays held)
         if (window) {
 #pragma unroll
           for (int q = 0; q < kBinWords / 32; ++q) meta.bins[lane + 32 * q] = 0u;
           __syncwarp();
         }
-        float top[kN / 32];
 #pragma unroll
         for (int q = 0; q < kN / 32; ++q) {
           const uint32_t e = lane + 32 * q;
           meta.jrow[e] = j[q];
-          // A neighbour that is dead already (its bound cannot beat the best-so-far) has no use for a
-          // lower bound: it takes no symmetric updates, and does not trip the epilogue's per-chunk test.
-          float nub = j[q] != 0xFFFFFFFFu ? __uint_as_float(key_bits(key_n[q])) : -1.f;
-          if (a.pruning && nub >= 0.f && dead_bound(nub, best, s.margin, s.margin_abs, s.margin_q)) nub = -1.f;
-          meta.nub[e] = nub;
-          meta.nnorm[e] = norm_n[q];
-          top[q] = nub;
+          meta.nnorm[e] = norm_n[q];  // (kNoColumn where the slot holds no row: such a column never comes out smallest)
+          // Symmetric updates, d(i,j) = d(j,i), are only worth their price where they KILL the neighbour
+          // (in the dot form nothing else is gained from a lower bound: no tile is abandoned early): a
+          // neighbour that is dead already, or no best-so-far yet, and the column takes none.
+          float lim = -1.f;
+          if (kSymmetric && a.pruning && j[q] != 0xFFFFFFFFu && kill > 0.f &&
+              !dead_bound(__uint_as_float(key_bits(key_n[q])), best, s.margin, s.margin_abs, s.margin_q))
+            lim = fminf(__uint_as_float(key_bits(key_n[q])), kill * a.lim_factor);
+          meta.lim[e] = lim;
+          meta.w[e] = lim > 0.f ? norm_n[q] - lim : kNoColumn;  // |b|^2 - 2 a.b - lim < -|a|^2  <=>  d < lim
           if (window && j[q] != 0xFFFFFFFFu) {
             const uint32_t bin = (j[q] >> bin_shift) & (kBinWords * 32 - 1);
             atomicOr(&meta.bins[bin >> 5], 1u << (bin & 31));
           }
         }
 #pragma unroll
-        for (int d = 16; d > 0; d >>= 1) {
-#pragma unroll
-          for (int q = 0; q < kN / 32; ++q) top[q] = fmaxf(top[q], __shfl_xor_sync(0xFFFFFFFFu, top[q], d));
-        }
-        if (lane == 0) {
-#pragma unroll
-          for (int q = 0; q < kN / 32; ++q) meta.nub_max[q] = top[q];
-        }
-        any_live = __any_sync(0xFFFFFFFFu, any_live);
-#pragma unroll
         for (int d = 16; d > 0; d >>= 1) calls += __shfl_xor_sync(0xFFFFFFFFu, calls, d);
+        live_total += live;
+        if (lane == 0) {
+          meta.valid = valid;
+          meta.slot0 = slot0;
+          meta.cand0 = cand0;
+          meta.stop = 0u;
+        }
+        __syncwarp();
+        if (lane == 0) bar_arrive(&sh.meta_full[m]);
+        slot_held = false;
+        ++ti;
+        calls_total += calls;
+        tiles_total += 1;
       }
-      if (lane == 0) {
-        meta.calls = calls;
-        meta.valid = valid;
-        meta.slot0 = slot0;
-        meta.stop = any_live ? 0u : 1u;  // (also the slot after the last tile)
-      }
+    }
+    {  // the slot after the last tile: stop
+      const uint32_t m = ti % kMetaSlots, use = ti / kMetaSlots;
+      if (use >= 1 && !slot_held) bar_wait(&sh.meta_empty[m], (use - 1) & 1, 1);
+      if (lane == 0) sh.meta[m].stop = 1u;
       __syncwarp();
       if (lane == 0) bar_arrive(&sh.meta_full[m]);
-      if (!any_live) break;
-      calls_total += calls;
-      tiles_total += 1;
     }
 #ifdef TSDD_TC_PROFILE
-    if (lane == 0 && blockIdx.y == 0 && blockIdx.x % 64 == 0)
-      printf("tc meta cta %u: total %lld wait meta_empty %lld tiles %llu of %u\n", blockIdx.x, clock64() - t_start, w_a, tiles_total, n_tiles);
+    if (lane == 0 && blockIdx.x % 37 == 0)
+      printf("tc meta cta %u: total %lld wait meta_empty %lld tiles %llu\n", blockIdx.x, clock64() - t_start, w_a, tiles_total);
 #endif
     if (lane == 0) {
       if (calls_total) atomicAdd(&s.counters->calls, calls_total);
@@ -403,13 +427,14 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
   } else if (warp == 0) {
     // ================================================================ producer: the TMA streams
     uint32_t seq = 0;
-    long long w_meta = 0, w_a = 0;
-    const long long t_start = clock64();
+    [[maybe_unused]] long long w_meta = 0, w_a = 0;
+    [[maybe_unused]] const long long t_start = clock64();
     for (uint32_t ti = 0;; ++ti) {
       const uint32_t m = ti % kMetaSlots;
       { TC_T0(); bar_wait(&sh.meta_full[m], (ti / kMetaSlots) & 1, 2); TC_ACC(w_meta); }
       const bool stop = *reinterpret_cast<volatile uint32_t*>(&sh.meta[m].stop) != 0;
       const uint32_t slot0 = *reinterpret_cast<volatile uint32_t*>(&sh.meta[m].slot0);
+      const uint32_t cand0 = *reinterpret_cast<volatile uint32_t*>(&sh.meta[m].cand0);
       __syncwarp();
       if (lane == 0) bar_arrive(&sh.meta_empty[m]);
       if (stop) break;
@@ -433,14 +458,14 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
       }
     }
 #ifdef TSDD_TC_PROFILE
-    if (lane == 0 && blockIdx.y == 0 && blockIdx.x % 64 == 0)
+    if (lane == 0 && blockIdx.x % 37 == 0)
       printf("tc producer cta %u: total %lld wait meta %lld wait empty %lld stages %u\n", blockIdx.x, clock64() - t_start, w_meta, w_a, seq);
 #endif
   } else if (warp == 1) {
     // ================================================================ MMA issuer
     uint32_t seq = 0;
-    long long w_meta = 0, w_a = 0, w_b = 0;
-    const long long t_start = clock64();
+    [[maybe_unused]] long long w_meta = 0, w_a = 0, w_b = 0;
+    [[maybe_unused]] const long long t_start = clock64();
     for (uint32_t ti = 0;; ++ti) {
       const uint32_t m = ti % kMetaSlots, buf = ti & 1;
       { TC_T0(); bar_wait(&sh.meta_full[m], (ti / kMetaSlots) & 1, 4); TC_ACC(w_meta); }
@@ -476,20 +501,18 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
       }
     }
 #ifdef TSDD_TC_PROFILE
-    if (lane == 0 && blockIdx.y == 0 && blockIdx.x % 64 == 0)
+    if (lane == 0 && blockIdx.x % 37 == 0)
       printf("tc mma cta %u: total %lld wait meta %lld wait tmem_empty %lld wait full %lld stages %u\n", blockIdx.x, clock64() - t_start, w_meta, w_a, w_b, seq);
 #endif
   } else if (warp >= 4) {
     // ================================================================ epilogue: thread = candidate = TMEM lane
     const uint32_t mrow = tid - 128;                 // candidate (TMEM lane) of this thread
     const uint32_t lane_base = (warp & 3u) * 32u;    // the TMEM lanes this warp may read
-    const uint32_t row = sh.cand[mrow];
-    const float cn = sh.cnorm[mrow];
     const float d_floor = 0.5f * s.margin_abs;
     unsigned long long tiles_done = 0, useful = 0;
     uint32_t overlap_total = 0;
-    long long w_meta = 0, w_a = 0;
-    const long long t_start = clock64();
+    [[maybe_unused]] long long w_meta = 0, w_a = 0;
+    [[maybe_unused]] const long long t_start = clock64();
 #ifdef TSDD_TC_PROFILE
     uint32_t n_slow = 0, n_slow_thr = 0, n_near = 0, n_part = 0;
 #endif
@@ -503,40 +526,79 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
         break;
       }
       const float thr = meta.thr[mrow];
-      { TC_T0(); bar_wait(&sh.tmem_full[buf], (ti >> 1) & 1, 8); TC_ACC(w_a); }
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      uint32_t d_min = 0xFFFFFFFFu, j_min = 0xFFFFFFFFu;
+      const uint32_t row = meta.cand[mrow];
+      const float cn = meta.cnorm[mrow];
       const bool taking_part = thr >= 0.f && row != 0xFFFFFFFFu;
 #ifdef TSDD_TC_PROFILE
       n_part += taking_part ? 1 : 0;
 #endif
-      // Per 32-column chunk ONE test decides whether anything has to be looked at pair by pair: the
-      // chunk's smallest distance (32 FFMA + 32 FMNMX, no branch) against the candidate's threshold
-      // and the chunk's greatest neighbour bound.  (|b|^2 - 2 a.b) + |a|^2 and the floor are monotone,
-      // so the smallest of the 32 distances is exactly what the pair-by-pair path would compute.
-      // The accumulators of chunk c+1 are on their way from tensor memory while chunk c is measured.
+      // Can the tile hold a self match (|row - j| < n) of this candidate?  Covering tiles are consecutive
+      // rows; of a window tile the metadata warp has marked the position bins that hold a neighbour.
+      bool near = false;
+      if (taking_part) {
+        const uint32_t z0 = row >= s.n - 1 ? row - (s.n - 1) : 0u, z1 = row + s.n - 1;
+        if (!window) {
+          near = z0 < meta.slot0 + meta.valid && z1 >= meta.slot0;
+        } else {
+          for (uint32_t b = z0 >> bin_shift; b <= (z1 >> bin_shift); ++b) {
+            const uint32_t bin = b & (kBinWords * 32 - 1);
+            near |= (meta.bins[bin >> 5] >> (bin & 31)) & 1u;
+          }
+        }
+      }
+      { TC_T0(); bar_wait(&sh.tmem_full[buf], (ti >> 1) & 1, 8); TC_ACC(w_a); }
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      unsigned long long key_min = ~0ull;  // (distance bits << 32) | neighbour: the 64-bit minimum settles ties by the smaller row
+      // Per 32-column chunk two running minima, no branch: of |b|^2 - 2 a.b (against the candidate's own
+      // threshold) and of |b|^2 - 2 a.b - lim (against -|a|^2: a distance that kills its neighbour).
+      // Only a chunk in which one of them trips is looked at pair by pair — and a tile that may hold a
+      // self match of the candidate, whose pairs have to be told apart.  The accumulators of chunk
+      // c + 1 are on their way from tensor memory while chunk c is measured.
       const uint32_t taddr = tmem_base + (lane_base << 16) + buf * kN;
+      const float thr_own = taking_part ? thr : -inf;
       auto measure = [&](const uint32_t (&v)[32], uint32_t cc) {
-        float low = inf;
+        const float4* pn = reinterpret_cast<const float4*>(meta.nnorm + cc * 32);
+        const float4* pw = reinterpret_cast<const float4*>(meta.w + cc * 32);
+        // (four independent minima each: one warp per scheduler has nobody to hide a 32-deep dependent chain behind)
+        float l0 = inf, l1 = inf, l2 = inf, l3 = inf, w0 = inf, w1 = inf, w2 = inf, w3 = inf;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) low = fminf(low, fmaf(-2.f, __uint_as_float(v[i]), meta.nnorm[cc * 32 + i]));
-        const float d_low = fmaxf(low + cn, d_floor);
-        if ((TSDD_TC_EXP & 1) && d_low != 12345.678f) return;
-        if (taking_part && (d_low <= thr || (kSymmetric && d_low < meta.nub_max[cc]))) {
+        for (int q = 0; q < 8; ++q) {
+          const float4 nn4 = pn[q];
+          l0 = fminf(l0, fmaf(-2.f, __uint_as_float(v[4 * q]), nn4.x));
+          l1 = fminf(l1, fmaf(-2.f, __uint_as_float(v[4 * q + 1]), nn4.y));
+          l2 = fminf(l2, fmaf(-2.f, __uint_as_float(v[4 * q + 2]), nn4.z));
+          l3 = fminf(l3, fmaf(-2.f, __uint_as_float(v[4 * q + 3]), nn4.w));
+          if (kSymmetric) {
+            const float4 w4 = pw[q];
+            w0 = fminf(w0, fmaf(-2.f, __uint_as_float(v[4 * q]), w4.x));
+            w1 = fminf(w1, fmaf(-2.f, __uint_as_float(v[4 * q + 1]), w4.y));
+            w2 = fminf(w2, fmaf(-2.f, __uint_as_float(v[4 * q + 2]), w4.z));
+            w3 = fminf(w3, fmaf(-2.f, __uint_as_float(v[4 * q + 3]), w4.w));
+          }
+        }
+        const float low = fminf(fminf(l0, l1), fminf(l2, l3)), low_w = fminf(fminf(w0, w1), fminf(w2, w3));
+        if ((TSDD_TC_EXP & 1) && low != 12345.678f) return;
+        const bool own = fmaxf(low + cn, d_floor) <= thr_own;
+        const bool kills = kSymmetric && taking_part && low_w < -cn;
+        if (own || kills) {
 #ifdef TSDD_TC_PROFILE
-          n_slow += 1; n_slow_thr += d_low <= thr ? 1 : 0;
+          n_slow += 1; n_slow_thr += own ? 1 : 0;
 #endif
 #pragma unroll
           for (int i = 0; i < 32; ++i) {  // (fully unrolled: the accumulators stay in registers)
             const uint32_t n = cc * 32 + i;
-            const float nub = kSymmetric ? meta.nub[n] : -1.f;
-            const float d = fmaxf(fmaf(-2.f, __uint_as_float(v[i]), meta.nnorm[n]) + cn, d_floor);
-            if (d <= thr || d < nub) {
+            const float t = fmaf(-2.f, __uint_as_float(v[i]), meta.nnorm[n]);
+            const float d = fmaxf(t + cn, d_floor);
+            const float lim = kSymmetric ? meta.lim[n] : -1.f;
+            if (d <= thr_own || d < lim) {
               const uint32_t j = meta.jrow[n];
-              if (j != 0xFFFFFFFFu && gap(row, j) >= s.n) {
+              if (j != 0xFFFFFFFFu && (!near || gap(row, j) >= s.n)) {
                 const uint32_t bits = __float_as_uint(d);
-                if (d <= thr && (bits < d_min || (bits == d_min && j < j_min))) d_min = bits, j_min = j;
-                if (d < nub) {
+                if (d <= thr_own) {
+                  const unsigned long long key = nn_key(bits, j);
+                  key_min = key < key_min ? key : key_min;
+                }
+                if (d < lim) {
                   TSDD_BOUND(j, s.n_rows);
                   atomicMin(as_ull(s.nn + j), static_cast<unsigned long long>(nn_key(bits, row)));
                 }
@@ -563,27 +625,24 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) bar_arrive(&sh.tmem_empty[buf]);
-      if (window && taking_part) {
-        // self-match pairs of a window tile (the metadata warp counted live x valid): only a candidate one of
-        // whose position bins holds a neighbour of the tile has any to count
-        const uint32_t z0 = row >= s.n - 1 ? row - (s.n - 1) : 0u, z1 = row + s.n - 1;
-        bool near = false;
-        for (uint32_t b = z0 >> bin_shift; b <= (z1 >> bin_shift); ++b) {
-          const uint32_t bin = b & (kBinWords * 32 - 1);
-          near |= (meta.bins[bin >> 5] >> (bin & 31)) & 1u;
-        }
-        if (near) {
+      if (window) {
+        // Self-match pairs of a window tile (the metadata warp counted live x valid): the warp counts them
+        // together, candidate by candidate, each lane looking at eight of the tile's neighbours.
+        uint32_t todo = __ballot_sync(0xFFFFFFFFu, near);
+        while (todo) {
+          const int src = __ffs(todo) - 1;
+          todo &= todo - 1;
+          const uint32_t r = __shfl_sync(0xFFFFFFFFu, row, src);
 #ifdef TSDD_TC_PROFILE
-          n_near += 1;
+          n_near += lane == 0 ? 1 : 0;
 #endif
-#pragma unroll 8
-          for (int i = 0; i < kN; ++i) overlap_total += gap(row, meta.jrow[i]) < s.n ? 1u : 0u;
+#pragma unroll
+          for (int q = 0; q < kN / 32; ++q) overlap_total += gap(r, meta.jrow[lane + 32 * q]) < s.n ? 1u : 0u;
         }
       }
-      if (j_min != 0xFFFFFFFFu) {
+      if (key_min != ~0ull) {
         TSDD_BOUND(row, s.n_rows);
-        atomicMin(as_ull(s.nn + row), static_cast<unsigned long long>(nn_key(d_min, j_min)));
-        sh.loc[mrow] = fminf(sh.loc[mrow], __uint_as_float(d_min));
+        atomicMin(as_ull(s.nn + row), key_min);
       }
       useful += taking_part ? static_cast<unsigned long long>(meta.valid) * s.n : 0ull;
       tiles_done += 1;
@@ -591,7 +650,7 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
       if (lane == 0) bar_arrive(&sh.meta_empty[m]);
     }
 #ifdef TSDD_TC_PROFILE
-    if (blockIdx.y == 0 && blockIdx.x % 64 == 0) {
+    if (blockIdx.x % 37 == 0) {
       const uint32_t any_slow = __reduce_add_sync(0xFFFFFFFFu, n_slow), any_thr = __reduce_add_sync(0xFFFFFFFFu, n_slow_thr),
                      any_near = __reduce_add_sync(0xFFFFFFFFu, n_near), any_part = __reduce_add_sync(0xFFFFFFFFu, n_part);
       if (lane == 0)
@@ -625,6 +684,7 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTmemCols));
   }
 }
+
 
 // x = hi + lo with both parts exactly representable in tf32 (low 13 mantissa bits clear)
 __global__ void __launch_bounds__(256)
@@ -727,10 +787,19 @@ int launch_scan_tiles_tc(SearchState s, const TcOperands& op, const uint32_t* d_
   const uint32_t u_begin = k_begin / 2, u_end = (k_end + 1) / 2;
   const uint32_t cand_tiles = (live_upper_bound + kM - 1) / kM;
   const uint64_t tiles = u_end - u_begin;
-  static const int waves = [] { const char* e = std::getenv("TSDD_TC_WAVES"); return e ? std::atoi(e) : 8; }();
-  static const int most = [] { const char* e = std::getenv("TSDD_TC_MOST"); return e ? std::atoi(e) : 16; }();
-  const uint64_t want = tiles * cand_tiles / (148ull * waves);
-  const int tiles_per_cta = static_cast<int>(want < 1 ? 1 : want > static_cast<uint64_t>(most) ? most : want);
+  // Work items for the persistent CTAs (one per SM): about `per_sm` items per SM, so that the last ones to finish
+  // are short, of at most 16 tiles (an item whose candidates are all dead is dropped at its first tile)
+  static const int per_sm = [] { const char* e = std::getenv("TSDD_TC_ITEMS_PER_SM"); return e ? std::atoi(e) : 6; }();
+  static const int sms = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  static const float lim_factor = [] { const char* e = std::getenv("TSDD_TC_LIM"); return e ? static_cast<float>(std::atof(e)) : 1.f; }();
+  const uint64_t want = tiles * cand_tiles / (static_cast<uint64_t>(sms) * per_sm);
+  const uint32_t tiles_per_item = static_cast<uint32_t>(want < 1 ? 1 : want > 16 ? 16 : want);
+  const uint64_t items = static_cast<uint64_t>(cand_tiles) * ((tiles + tiles_per_item - 1) / tiles_per_item);
   const bool window = d_nbr_index != nullptr;
   CUtensorMap map_a_hi{}, map_a_lo{}, map_b_hi{}, map_b_lo{};
   const float* b_hi = window ? op.sorted_hi : op.rows_hi;
@@ -744,8 +813,9 @@ int launch_scan_tiles_tc(SearchState s, const TcOperands& op, const uint32_t* d_
     if (error) *error = "cuTensorMapEncodeTiled failed (tensor-core tile kernel)";
     return 0;
   }
-  TcArgs a{d_batch_rows, d_batch_slots, d_sel, d_nbr_index, u_begin, u_end, tiles_per_cta, pruning ? 1 : 0};
-  dim3 grid(cand_tiles, static_cast<unsigned>((tiles + tiles_per_cta - 1) / tiles_per_cta));
+  cudaMemsetAsync(op.work, 0, sizeof(uint32_t), stream);
+  TcArgs a{d_batch_rows, d_batch_slots, d_sel, d_nbr_index, u_begin, u_end, tiles_per_item, pruning ? 1 : 0, op.work, lim_factor};
+  dim3 grid(static_cast<unsigned>(items < static_cast<uint64_t>(sms) ? items : sms));
   const int smem = static_cast<int>(sizeof(SharedTc)) + 1024;
   auto launch = [&](auto kernel) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

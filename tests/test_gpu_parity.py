@@ -217,7 +217,7 @@ def test_search_is_repeatable_and_independent_of_tunables(ctx):
     for name, value in [("batch", 65536), ("rounds", 64), ("bucket_mates", 8), ("symmetric", 1),
                         ("packed", 1), ("first_batch", 128), ("wide_tile", 0), ("kernel", 0),
                         ("window_rounds", 2), ("rotate", 1), ("growth", 2.0), ("first_range", 8192),
-                        ("lower_bound", 1), ("margin_delta", -1), ("batch_growth", 8), ("dot_form", 1),
+                        ("lower_bound", 1), ("margin_delta", -1), ("batch_growth", 8), ("dot_form", 5),
                         ("seed_rows", 4096), ("tensor_map", 1), ("dot_window_rounds", 8), ("dot_growth", 1.3),
                         ("dot_tile16", 1)]:
         ctx.set_option(name, value)
@@ -735,7 +735,7 @@ def test_dot_product_form_matches_the_oracle(ctx, chk, seed, kind, n):
         pos, dist = ctx.search(k)
         _DOT_LAUNCHES.append(ctx.stats()["scan_kernel_dot_launches"])
     finally:
-        ctx.set_option("dot_form", 1)
+        ctx.set_option("dot_form", 5)
         ctx.set_option("lower_bound", 1)
     want = chk.topk(x, n, w, a, k)
     assert_discords_match(chk, x, n, pos, dist, want)
@@ -760,7 +760,7 @@ def test_dot_product_form_on_256_candidate_tiles(ctx, chk, seed, kind, n):
         ctx.set_option("dot_tile16", 0)
         again = ctx.search(k)
     finally:
-        for name, value in [("dot_form", 1), ("lower_bound", 1), ("first_batch", 128), ("dot_tile16", 1)]:
+        for name, value in [("dot_form", 5), ("lower_bound", 1), ("first_batch", 128), ("dot_tile16", 1)]:
             ctx.set_option(name, value)
     want = chk.topk(x, n, w, a, k)
     assert_discords_match(chk, x, n, pos, dist, want)
@@ -790,7 +790,7 @@ def test_dot_product_form_on_the_tensor_cores(ctx, chk, seed, kind, n, form):
         ctx.set_option("dot_form", 2)
         again = ctx.search(k)
     finally:
-        for name, value in [("dot_form", 1), ("lower_bound", 1), ("first_batch", 128)]:
+        for name, value in [("dot_form", 5), ("lower_bound", 1), ("first_batch", 128)]:
             ctx.set_option(name, value)
     want = chk.topk(x, n, w, a, k)
     assert_discords_match(chk, x, n, pos, dist, want)
@@ -828,7 +828,7 @@ def test_awkward_value_distributions(ctx, chk, kind, dot):
         ctx.prepare(x, 96, 6, 4)
         pos, dist = ctx.search(3)
     finally:
-        ctx.set_option("dot_form", 1)
+        ctx.set_option("dot_form", 5)
         ctx.set_option("first_batch", 128)
     want = chk.topk(x, 96, 6, 4, 3)
     assert_discords_match(chk, x, 96, pos, dist, want)
@@ -855,7 +855,7 @@ def test_dot_product_form_is_chosen_where_tiles_are_never_abandoned(ctx, chk):
         again = ctx.search(2)
         assert ctx.stats()["scan_kernel_dot_launches"] == 0
     finally:
-        ctx.set_option("dot_form", 1)
+        ctx.set_option("dot_form", 5)
     assert again[0] == pos
     np.testing.assert_allclose(again[1], dist, rtol=1e-9)  # both decided in float64
 
@@ -960,7 +960,7 @@ def test_low_noise_periodic_series(ctx, chk, seed, noise, dot):
         ctx.prepare(x, 256, 8, 4)
         pos, dist = ctx.search(2)
     finally:
-        ctx.set_option("dot_form", 1)
+        ctx.set_option("dot_form", 5)
     want = chk.topk(x, 256, 8, 4, 2)
     assert pos == want["positions"], (pos, want["positions"], dist, want["distances"])
     np.testing.assert_allclose(dist, want["distances"], rtol=DIST_RTOL)
@@ -1159,7 +1159,7 @@ def test_soak_random_series_shapes_and_options(ctx, chk, case):
     opts = {"dot_form": int(rng.choice([1, 2, 3, 4, 5, 6])), "first_batch": int(rng.choice([128, 4096])),
             "lower_bound": int(rng.choice([0, 1])), "filter_in_ws": int(rng.choice([0, 1])),
             "propagate": int(rng.choice([0, 2, 8])), "propagate_every": int(rng.choice([0, 1, 2]))}
-    defaults = {"dot_form": 1, "first_batch": 128, "lower_bound": 1, "filter_in_ws": 0, "propagate": 8,
+    defaults = {"dot_form": 5, "first_batch": 128, "lower_bound": 1, "filter_in_ws": 0, "propagate": 8,
                 "propagate_every": 2}
     try:
         for name, value in opts.items():
