@@ -14,15 +14,21 @@ top-k time of a step is reported beside it (`topk_time_s`).
           stream the kernels run on, max over ranks.
   e2e   : the reference-facing call (run_discovery with a HOST series in pinned memory):
           H2D copy + prepare + search + D2H of the result inside the timed region.
-  roofline : the tiled distance kernels against the FP32 CUDA-core peak.  `achieved` counts
-          the floating-point operations the kernels EXECUTE: a term in the direct form
-          (x-y)^2 = FADD + FFMA = 3 FLOP, a term in the dot-product form
-          (|a|^2 + |b|^2 - 2 a.b) = one FFMA = 2 FLOP; `algorithmic_tflops` is SURVEY.md
-          8d's figure (3 FLOP for every term, whatever the form).  `peak` is NOMINAL:
-          148 SMs x 128 lanes x 2 FLOP x the maximum SM clock (MEASURED_PEAKS.json has no FP32
-          entry); an FFMA-only probe kernel measured live is reported beside it
-          (`peak_probe`).  `useful_frac` counts only the terms of live candidates against
-          existing rows in real columns (no dead tile slots, no padding).
+  roofline : the dominant kernel of the workload.  On inputs whose search switches to the
+          dot-product form (cfg5) that is the tensor-core tile kernel k_scan_tiles_tc: `bound`
+          "tensor", peak = MEASURED_PEAKS.json's dense bf16 figure (fp16 runs at the same rate),
+          `achieved` = SURVEY.md 8d's 3 FLOP per term, `executed` = the 6 FLOP per term the kernel
+          really issues (three fp16 MMAs on hi / lo split rows).  `cuda_core_path` then repeats
+          the workload with the dot form on the CUDA cores (dot_form = 1) and carries the FP32
+          roofline north_star asks for.  On other inputs (cfg4) the tile kernels are CUDA-core
+          kernels and `roofline` is that FP32 line itself: `achieved` counts the floating-point
+          operations the kernels EXECUTE — a term in the direct form (x-y)^2 = FADD + FFMA =
+          3 FLOP, a term in the dot-product form = one FFMA = 2 FLOP; `algorithmic_tflops` is
+          SURVEY.md 8d's figure (3 FLOP for every term).  Its `peak` is NOMINAL: 148 SMs x 128
+          lanes x 2 FLOP x the maximum SM clock (MEASURED_PEAKS.json has no FP32 entry); an
+          FFMA-only probe kernel measured live is reported beside it (`peak_probe`).
+          `useful_frac` counts only the terms of live candidates against existing rows in
+          real columns (no dead tile slots, no padding).
   cpu_baseline : the unmodified reference (oracle/_ref; else the C restatement) on the
           box's host cores, on a bounded sample (a prefix of the same series) — and the GPU
           on EXACTLY that sample beside it (`gpu_same_input_topk_time_s`).
@@ -217,7 +223,7 @@ def run_cuda_arm(args) -> None:
     barrier()
     sampler = ClockSampler(local)
     totals = {"calls": 0, "terms": 0, "scan_terms": 0, "scan_ms": 0.0, "scan_launches": 0, "ws_launches": 0,
-              "dot_launches": 0, "dot_terms": 0, "useful_terms": 0,
+              "dot_launches": 0, "dot_terms": 0, "useful_terms": 0, "tc_terms": 0, "tc_ms": 0.0, "tc_launches": 0,
               "launches": 0,
               "prep_ms": 0.0, "search_ms": 0.0, "build_rows_ms": 0.0, "encode_ms": 0.0, "index_ms": 0.0}
     with sampler:
@@ -234,6 +240,9 @@ def run_cuda_arm(args) -> None:
             totals["dot_launches"] += st["scan_kernel_dot_launches"]
             totals["dot_terms"] += st["scan_kernel_dot_terms"]
             totals["useful_terms"] += st["useful_terms"]
+            totals["tc_terms"] += st["scan_kernel_tc_terms"]
+            totals["tc_ms"] += st["scan_kernel_tc_ms"]
+            totals["tc_launches"] += st["scan_kernel_tc_launches"]
             totals["launches"] += st["kernel_launches"]
             for key in ("prep_ms", "search_ms", "build_rows_ms", "encode_ms", "index_ms"):
                 totals[key] += st[key]
@@ -270,17 +279,9 @@ def run_cuda_arm(args) -> None:
                 golden_ok = pos == rec["oracle"]["positions"]
         except OSError:
             pass
-        scan_s = totals["scan_ms"] * 1e-3
-        direct_terms = totals["scan_terms"] - totals["dot_terms"]
-        useful_share = totals["useful_terms"] / max(1, totals["scan_terms"])
-        executed_flop = 3.0 * direct_terms + 2.0 * totals["dot_terms"]
-        pipe_ops = 2.0 * direct_terms + 1.0 * totals["dot_terms"]  # FP32-pipe lane operations
-        achieved = executed_flop / scan_s / 1e12 if scan_s > 0 else 0.0
         clocks = sampler.summary()
         sm_max_mhz = clocks.get("sm_max_mhz") or _measured_peak("sm_max_mhz", 1965.0)[0]
         props = torch.cuda.get_device_properties(local)
-        peak = props.multi_processor_count * 128 * 2 * sm_max_mhz * 1e6 / 1e12  # nominal FP32 FMA peak
-        peak_probe = 2.0 * ffma_ops / 1e12
         # DRAM traffic of the dominant kernel: only from an ncu capture of THIS workload
         traffic, prof = None, {}
         try:
@@ -306,37 +307,7 @@ def run_cuda_arm(args) -> None:
             "e2e": {"value": all_e2e_calls / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(x.nbytes),
                     "d2h_bytes_per_step": int(k * 16 + 160), "topk_time_s": e2e_s / args.steps},
             "gpu_launches": int(totals["launches"]),
-            "roofline": {"bound": "fp32",
-                         "kernel": "k_scan_tiles_ws16 / k_scan_tiles_ws / k_scan_tiles (the tile kernels: %d of %d "
-                                   "launches warp-specialised, %d of those in the dot-product form, which "
-                                   "runs on k_scan_tiles_ws16 while a batch fills 256-candidate tiles)"
-                                   % (totals["ws_launches"], totals["scan_launches"], totals["dot_launches"]),
-                         "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
-                         "peak_source": "nominal: %d SMs x 128 FP32 lanes x 2 FLOP x %.0f MHz (the maximum SM clock; "
-                                        "MEASURED_PEAKS.json has no FP32 entry and B200_PROFILING.md states no FP32 "
-                                        "fallback)" % (props.multi_processor_count, sm_max_mhz),
-                         "peak_probe": peak_probe, "frac_probe": achieved / peak_probe if peak_probe else None,
-                         "peak_probe_source": "live FFMA-only probe kernel (csrc/probe_kernels.cu: 16 independent "
-                                              "FFMA chains per thread, nothing else in the loop) x 2 FLOP",
-                         "useful_share_of_terms": useful_share, "useful_frac": achieved * useful_share / peak,
-                         "useful_definition": "terms of (live candidate, existing neighbour row) pairs in columns "
-                                              "t < n: no dead or empty candidate slots of a tile, no slots past the "
-                                              "last row, no zero padding of the row stride",
-                         "terms_per_s": totals["scan_terms"] / scan_s if scan_s else 0.0,
-                         "dot_form_share_of_terms": totals["dot_terms"] / max(1, totals["scan_terms"]),
-                         "algorithmic_tflops": 3.0 * totals["scan_terms"] / scan_s / 1e12 if scan_s else 0.0,
-                         "fma_pipe_util": pipe_ops / scan_s / (peak * 1e12 / 2.0) if scan_s else 0.0,
-                         "fma_pipe_util_vs_probe": pipe_ops / scan_s / ffma_ops if scan_s else 0.0,
-                         "sub_fma_mix_probe_lane_ops_per_s": mix_ops, "ffma_probe_lane_ops_per_s": ffma_ops,
-                         "launches": int(totals["scan_launches"]),
-                         "avg_launch_ms": totals["scan_ms"] / max(1, totals["scan_launches"]),
-                         "kernel_share_of_step": totals["scan_ms"] / elapsed_ms, "traffic": traffic,
-                         "traffic_source": ("ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum of ONE captured "
-                                            "launch of this workload (%s; %s ms; %s) — compare with that launch, not "
-                                            "with avg_launch_ms" % (prof.get("captured_kernel"), prof.get("captured_launch_ms"),
-                                                                    prof.get("source"))) if traffic else
-                                           "no ncu capture of this workload's dominant kernel is on file"},
+            "roofline": None,
             "roofline_prep": {"bound": "hbm", "kernel": "k_build_rows", "unit": "GB/s",
                               "achieved": matrix_bytes * args.steps / (totals["build_rows_ms"] * 1e-3) / 1e9
                               if totals["build_rows_ms"] else None,
@@ -351,12 +322,31 @@ def run_cuda_arm(args) -> None:
         }
         rp = line["roofline_prep"]
         rp["frac"] = rp["achieved"] / rp["peak"] if rp["achieved"] else None
+        fp32 = fp32_roofline(totals, elapsed_ms, props.multi_processor_count, sm_max_mhz, ffma_ops, mix_ops)
+        if totals["tc_terms"] > 0.5 * totals["scan_terms"]:
+            # the dominant kernel is the tensor-core tile kernel: the tensor roofline is the line's roofline,
+            # the CUDA-core tile kernels' FP32 line (the same workload with dot_form = 1) follows below
+            line["roofline"] = tensor_roofline(totals, elapsed_ms, traffic, prof)
+            line["dtype"] = "f32 (tile products: fp16 hi/lo parts on the tensor cores, float32 accumulation; decision in f64)"
+        else:
+            fp32.update({"traffic": traffic,
+                         "traffic_source": ("ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum of ONE captured "
+                                            "launch of this workload (%s; %s ms; %s) — compare with that launch, not "
+                                            "with avg_launch_ms" % (prof.get("captured_kernel"), prof.get("captured_launch_ms"),
+                                                                    prof.get("source"))) if traffic else
+                                           "no ncu capture of this workload's dominant kernel is on file"})
+            line["roofline"] = fp32
         if world == 1 and not args.no_secondary and args.workload != 4:
             line["other_workloads"] = {"cfg4": time_other_workload(ctx, 4, local, golden_all)}
-        if world == 1 and not args.no_secondary and not any(o.startswith("dot_form") for o in args.opt):
-            # the tensor-core experiment (csrc/tc_kernels.cu) on the SAME workload; the default above is the CUDA-core path
-            line["tensor_core_experiment"] = time_other_workload(ctx, args.workload, local, golden_all, options={"dot_form": 3})
-            ctx.set_option("dot_form", 1)
+        if (world == 1 and not args.no_secondary and not any(o.startswith("dot_form") for o in args.opt)
+                and line["roofline"]["bound"] == "tensor"):
+            # the SAME workload with the dot-product form on the CUDA cores (dot_form = 1: k_scan_tiles_ws16, the
+            # kernel north_star's FP32 roofline is about), with that path's own FP32 roofline
+            cc = time_other_workload(ctx, args.workload, local, golden_all, options={"dot_form": 1})
+            ctx.set_option("dot_form", 5)
+            t1 = cc.pop("totals")
+            cc["roofline"] = fp32_roofline(t1, t1["elapsed_ms"], props.multi_processor_count, sm_max_mhz, ffma_ops, mix_ops)
+            line["cuda_core_path"] = cc
         if world == 1 and not args.no_cpu_baseline:
             cb = cpu_reference_run(args.workload, x, w)
             line["cpu_baseline"] = {key: cb[key] for key in ("value", "unit", "cores", "kind", "sample",
@@ -372,6 +362,74 @@ def run_cuda_arm(args) -> None:
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def fp32_roofline(totals: dict, elapsed_ms: float, sms: int, sm_max_mhz: float, ffma_ops: float, mix_ops: float) -> dict:
+    """The CUDA-core tile kernels against the FP32 FMA peak: executed FLOP (3 per direct-form term, 2 per
+    dot-form term; tensor-core terms excluded) over the time inside those kernels."""
+    scan_s = (totals["scan_ms"] - totals["tc_ms"]) * 1e-3
+    cc_terms = totals["scan_terms"] - totals["tc_terms"]
+    dot_terms = totals["dot_terms"] - totals["tc_terms"]
+    direct_terms = cc_terms - dot_terms
+    useful_share = totals["useful_terms"] / max(1, totals["scan_terms"])
+    executed_flop = 3.0 * direct_terms + 2.0 * dot_terms
+    pipe_ops = 2.0 * direct_terms + 1.0 * dot_terms  # FP32-pipe lane operations
+    achieved = executed_flop / scan_s / 1e12 if scan_s > 0 else 0.0
+    peak = sms * 128 * 2 * sm_max_mhz * 1e6 / 1e12  # nominal FP32 FMA peak
+    peak_probe = 2.0 * ffma_ops / 1e12
+    launches = totals["scan_launches"] - totals["tc_launches"]
+    return {"bound": "fp32",
+            "kernel": "k_scan_tiles_ws16 / k_scan_tiles_ws / k_scan_tiles (the CUDA-core tile kernels: %d launches, "
+                      "%d warp-specialised, %d in the dot-product form, which runs on k_scan_tiles_ws16 while a "
+                      "batch fills 256-candidate tiles)" % (launches, totals["ws_launches"] - totals["tc_launches"],
+                                                            totals["dot_launches"] - totals["tc_launches"]),
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
+            "peak_source": "nominal: %d SMs x 128 FP32 lanes x 2 FLOP x %.0f MHz (the maximum SM clock; "
+                           "MEASURED_PEAKS.json has no FP32 entry and B200_PROFILING.md states no FP32 "
+                           "fallback)" % (sms, sm_max_mhz),
+            "peak_probe": peak_probe, "frac_probe": achieved / peak_probe if peak_probe else None,
+            "peak_probe_source": "live FFMA-only probe kernel (csrc/probe_kernels.cu: 16 independent "
+                                 "FFMA chains per thread, nothing else in the loop) x 2 FLOP",
+            "useful_share_of_terms": useful_share, "useful_frac": achieved * useful_share / peak,
+            "useful_definition": "terms of (live candidate, existing neighbour row) pairs in columns "
+                                 "t < n: no dead or empty candidate slots of a tile, no slots past the "
+                                 "last row, no zero padding of the row stride (share over ALL tile kernels)",
+            "terms_per_s": cc_terms / scan_s if scan_s else 0.0,
+            "dot_form_share_of_terms": dot_terms / max(1, cc_terms),
+            "algorithmic_tflops": 3.0 * cc_terms / scan_s / 1e12 if scan_s else 0.0,
+            "fma_pipe_util": pipe_ops / scan_s / (peak * 1e12 / 2.0) if scan_s else 0.0,
+            "fma_pipe_util_vs_probe": pipe_ops / scan_s / ffma_ops if scan_s else 0.0,
+            "sub_fma_mix_probe_lane_ops_per_s": mix_ops, "ffma_probe_lane_ops_per_s": ffma_ops,
+            "launches": int(launches), "avg_launch_ms": scan_s * 1e3 / max(1, launches),
+            "kernel_share_of_step": scan_s * 1e3 / elapsed_ms}
+
+
+def tensor_roofline(totals: dict, elapsed_ms: float, traffic, prof: dict) -> dict:
+    """k_scan_tiles_tc against the dense 16-bit tensor peak (MEASURED_PEAKS.json: cuBLAS bf16, burst; fp16
+    runs at the same rate).  `achieved` counts SURVEY 8(d)'s 3 FLOP per term; the kernel EXECUTES three
+    fp16 MMAs = 6 FLOP per term (hi.hi + hi.lo + lo.hi of the split rows): `executed` / `frac_executed`
+    say how busy the tensor pipe is."""
+    tc_s = totals["tc_ms"] * 1e-3
+    peak, src = _measured_peak("bf16_tflops", 2250.0)
+    algorithmic = 3.0 * totals["tc_terms"] / tc_s / 1e12
+    executed = 6.0 * totals["tc_terms"] / tc_s / 1e12
+    return {"bound": "tensor", "kernel": "k_scan_tiles_tc<symmetric, fp16> (csrc/tc_kernels.cu: tcgen05.mma kind::f16, "
+                                         "TMEM accumulators, TMA boxes; %d of %d tile-kernel launches, %.1f %% of all terms)"
+                                         % (totals["tc_launches"], totals["scan_launches"],
+                                            100.0 * totals["tc_terms"] / max(1, totals["scan_terms"])),
+            "achieved": algorithmic, "peak": peak, "unit": "TFLOP/s", "frac": algorithmic / peak,
+            "peak_source": src + " bf16_tflops (burst: the kernel's launches are timed one by one)",
+            "executed": executed, "frac_executed": executed / peak,
+            "flop_per_term": {"algorithmic": 3, "executed": 6},
+            "terms_per_s": totals["tc_terms"] / tc_s, "launches": int(totals["tc_launches"]),
+            "avg_launch_ms": totals["tc_ms"] / max(1, totals["tc_launches"]),
+            "kernel_share_of_step": totals["tc_ms"] / elapsed_ms,
+            "useful_share_of_terms": totals["useful_terms"] / max(1, totals["scan_terms"]),
+            "traffic": traffic,
+            "traffic_source": ("ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum of ONE captured launch of this "
+                               "workload (%s; %s ms; %s) — compare with that launch, not with avg_launch_ms"
+                               % (prof.get("captured_kernel"), prof.get("captured_launch_ms"), prof.get("source")))
+            if traffic else "no ncu capture of this workload's dominant kernel is on file"}
 
 
 def time_same_input(ctx, sample: np.ndarray, w, device: int, repeats: int = 3) -> dict:
@@ -428,7 +486,13 @@ def time_other_workload(ctx, cfg: int, device: int, golden: dict, repeats: int =
     if options:
         out.update({"options": options, "scan_kernel_ms": st["scan_kernel_ms"],
                     "tensor_core_launches": st["scan_kernel_tc_launches"],
-                    "tensor_core_share_of_terms": st["scan_kernel_tc_terms"] / max(1, st["scan_kernel_terms"])})
+                    "tensor_core_share_of_terms": st["scan_kernel_tc_terms"] / max(1, st["scan_kernel_terms"]),
+                    "totals": {"scan_ms": st["scan_kernel_ms"], "tc_ms": st["scan_kernel_tc_ms"],
+                               "scan_terms": st["scan_kernel_terms"], "tc_terms": st["scan_kernel_tc_terms"],
+                               "dot_terms": st["scan_kernel_dot_terms"], "useful_terms": st["useful_terms"],
+                               "scan_launches": st["scan_kernel_launches"], "tc_launches": st["scan_kernel_tc_launches"],
+                               "ws_launches": st["scan_kernel_ws_launches"], "dot_launches": st["scan_kernel_dot_launches"],
+                               "elapsed_ms": times[-1] * 1e3}})
     return out
 
 

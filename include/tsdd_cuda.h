@@ -70,8 +70,9 @@ typedef struct tsdd_cuda_stats {
   uint64_t exact_reruns;   /* of those, measured again from +inf because the float32 start bound was too low */
   uint64_t useful_terms;   /* of scan_kernel_terms: terms of pairs that were live, non-self and not padding */
   uint64_t propagated;     /* pair distances measured by the time-topology step (option "propagate") */
-  uint64_t scan_kernel_tc_launches; /* of scan_kernel_dot_launches, those of the tensor-core tile kernel (dot_form 3 / 4) */
-  uint64_t scan_kernel_tc_terms;    /* of scan_kernel_dot_terms, those computed there (three tf32 MACs per term) */
+  uint64_t scan_kernel_tc_launches; /* of scan_kernel_dot_launches, those of the tensor-core tile kernel (dot_form 3 .. 6) */
+  uint64_t scan_kernel_tc_terms;    /* of scan_kernel_dot_terms, those computed there (three MMA multiply-adds per term) */
+  double scan_kernel_tc_ms;         /* of scan_kernel_ms, the device time inside the tensor-core tile kernel */
 } tsdd_cuda_stats;
 
 /* ---- lifetime ------------------------------------------------------------ */

@@ -1050,12 +1050,16 @@ void collect_search_stats(tsdd_cuda_ctx* ctx) {
   ctx->stats.useful_terms = c.useful_terms;
   ctx->stats.propagated = c.propagated;
   ctx->stats.scan_kernel_tc_terms = c.tc_terms;
-  double total = 0.0;
+  double total = 0.0, total_tc = 0.0;
   for (size_t e = 0; e + 1 < ctx->events_used; e += 2) {
     float ms = 0.f;
-    if (cudaEventElapsedTime(&ms, ctx->event_pool[e], ctx->event_pool[e + 1]) == cudaSuccess) total += ms;
+    if (cudaEventElapsedTime(&ms, ctx->event_pool[e], ctx->event_pool[e + 1]) == cudaSuccess) {
+      total += ms;
+      if (e / 2 < ctx->trace.size() && ctx->trace[e / 2].choice.tc) total_tc += ms;
+    }
   }
   ctx->stats.scan_kernel_ms = total;
+  ctx->stats.scan_kernel_tc_ms = total_tc;
   if (const char* env = std::getenv("TSDD_TRACE"); env && env[0] == '1') {
     for (size_t t = 0; t < ctx->trace.size() && 2 * t + 1 < ctx->events_used; ++t) {
       float ms = 0.f;
