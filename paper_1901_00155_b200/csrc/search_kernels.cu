@@ -17,6 +17,8 @@
 #include "kernels.hpp"
 
 #include <cuda.h>
+
+#include <cstdlib>
 #include <cudaTypedefs.h>
 
 #include <type_traits>
@@ -249,6 +251,113 @@ k_bucket_mates(SearchState s, const kSample* __restrict__ x, const double* __res
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) sum64 += __shfl_xor_sync(0xFFFFFFFFu, sum64, d);
     const float sum = static_cast<float>(sum64);
+    bound_i = fminf(bound_i, sum);
+    if (lane == 0) {
+      const uint32_t bits = __float_as_uint(sum);
+      atomicMin(as_ull(s.nn + row_i), static_cast<unsigned long long>(nn_key(bits, row_j)));
+      atomicMin(as_ull(s.nn + row_j), static_cast<unsigned long long>(nn_key(bits, row_i)));
+      calls += 1;
+      terms += s.n;
+    }
+  }
+  if (lane == 0 && calls) {
+    atomicAdd(&s.counters->calls, calls);
+    atomicAdd(&s.counters->terms, terms);
+  }
+}
+
+// The same step for a float32 series and windows of up to 1,024 samples, in float32 and with every
+// load of a pair in flight at once (the float64 version above is bound by load latency: ncu
+// long_scoreboard 25 per issue at workload 4, and by its float64 <-> float32 conversions).  The row's own
+// window is z-normalised once and kept in registers (kPerLane values a lane); the mates' rows, means
+// and 1/sigma are fetched by one lane each, side by side, before the first pair; a pair is then
+// kPerLane independent loads followed by five float32 operations a term.  z = ((x - mu_hi) - mu_lo) *
+// inv with mu = mu_hi + mu_lo split into two floats: three roundings of 2^-24 relative to |z| besides
+// that of 1/sigma, against one for a row of the matrix — so the sum is INFLATED by a bound of its own
+// error (relative 1.2e-7 n for the accumulation, absolute 1e-6 sqrt(n d^2) for the four roundings of
+// the 2 sqrt(n)-long difference): what is published is an upper bound of the exact distance, which is
+// all a bound has to be.  Identical windows still give exactly 0.
+template <int kPerLane>
+__global__ void __launch_bounds__(256)
+k_bucket_mates_f32(SearchState s, const float* __restrict__ x, const double* __restrict__ mean,
+                   const double* __restrict__ inv_sigma, const uint32_t* __restrict__ sorted_row,
+                   const uint32_t* __restrict__ slot_bucket, const uint32_t* __restrict__ offsets, int mates,
+                   uint32_t world, uint32_t rank) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t slot = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * world + rank;
+  if (slot >= s.n_rows) return;
+  const uint32_t bucket = slot_bucket[slot];
+  const uint32_t b0 = offsets[bucket], b1 = offsets[bucket + 1];
+  const uint32_t len = b1 - b0;
+  if (len < 2) return;
+  const uint32_t row_i = sorted_row[slot];
+  TSDD_BOUND(bucket + 1, s.n_rows + 1);
+  TSDD_BOUND(row_i, s.n_rows);
+  TSDD_BOUND(b1 - 1, s.n_rows);
+  uint32_t tries = min(static_cast<uint32_t>(mates), 31u);
+  uint32_t step = len / (tries + 1);
+  if (step == 0) {
+    step = 1;
+    tries = min(len - 1, 31u);
+  }
+  // lane q fetches what is needed of mate q (q = 1 .. tries)
+  uint32_t my_row = 0xFFFFFFFFu;
+  float my_hi = 0.f, my_lo = 0.f, my_inv = 0.f;
+  if (lane >= 1 && lane <= tries) {
+    const uint32_t other = b0 + (slot - b0 + lane * step) % len;
+    TSDD_BOUND(other, s.n_rows);
+    const uint32_t r = sorted_row[other];
+    TSDD_BOUND(r, s.n_rows);
+    if (gap_u32(row_i, r) >= s.n) {
+      my_row = r;
+      const double mu = mean[r];
+      my_hi = static_cast<float>(mu);
+      my_lo = static_cast<float>(mu - static_cast<double>(my_hi));
+      my_inv = static_cast<float>(inv_sigma[r]);
+    }
+  }
+  float za[kPerLane];
+  {
+    const double mu = mean[row_i];
+    const float hi = static_cast<float>(mu), lo = static_cast<float>(mu - static_cast<double>(hi));
+    const float inv = static_cast<float>(inv_sigma[row_i]);
+    const float* pi = x + row_i;
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) {
+      const uint32_t t = lane + 32 * k;
+      za[k] = t < s.n ? ((pi[t] - hi) - lo) * inv : 0.f;
+    }
+  }
+  unsigned long long calls = 0, terms = 0;
+  const uint64_t best = *s.best;
+  const float grow = 1.f + fmaxf(4e-6f, 1.2e-7f * static_cast<float>(s.n)), root_n = sqrtf(static_cast<float>(s.n));
+  float bound_i = __uint_as_float(kInfBits);
+  for (uint32_t q = 1; q <= tries; ++q) {
+    if (dead_bound(bound_i, best, s.margin, s.margin_abs, s.margin_q)) break;
+    const uint32_t row_j = __shfl_sync(0xFFFFFFFFu, my_row, q);
+    const float hi = __shfl_sync(0xFFFFFFFFu, my_hi, q), lo = __shfl_sync(0xFFFFFFFFu, my_lo, q);
+    const float inv = __shfl_sync(0xFFFFFFFFu, my_inv, q);
+    if (row_j == 0xFFFFFFFFu) continue;
+    const float* pj = x + row_j;
+    float b[kPerLane];
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) {
+      const uint32_t t = lane + 32 * k;
+      b[k] = t < s.n ? __ldg(pj + t) : 0.f;
+    }
+    float sum_a = 0.f, sum_b = 0.f;
+#pragma unroll
+    for (int k = 0; k < kPerLane; ++k) {
+      const uint32_t t = lane + 32 * k;
+      const float zb = t < s.n ? ((b[k] - hi) - lo) * inv : 0.f;
+      const float d = za[k] - zb;
+      if (k & 1) sum_b = fmaf(d, d, sum_b);
+      else sum_a = fmaf(d, d, sum_a);
+    }
+    float sum = sum_a + sum_b;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, d);
+    sum = fmaf(sum, grow, 1e-6f * root_n * sqrtf(sum));  // an upper bound of the exact distance (see above)
     bound_i = fminf(bound_i, sum);
     if (lane == 0) {
       const uint32_t bits = __float_as_uint(sum);
@@ -2385,7 +2494,19 @@ int launch_bucket_mates(SearchState s, const double* d_series, const float* d_se
                         const uint32_t* d_offsets, int mates, uint32_t world, uint32_t rank, cudaStream_t stream) {
   if (mates <= 0) return 0;
   const size_t slots = (static_cast<size_t>(s.n_rows) + world - 1) / world;
-  if (d_series_f32 != nullptr)
+  static const bool old_form = [] { const char* e = std::getenv("TSDD_MATES_F64"); return e && e[0] == '1'; }();
+  if (d_series_f32 != nullptr && s.n <= 1024 && !old_form) {
+    const unsigned blocks = blocks_for(slots * 32, 256);
+    auto go = [&](auto kernel) {
+      kernel<<<blocks, 256, 0, stream>>>(s, d_series_f32, d_mean, d_inv_sigma, d_sorted_row, d_slot_bucket, d_offsets, mates, world,
+                                         rank);
+    };
+    if (s.n <= 64) go(k_bucket_mates_f32<2>);
+    else if (s.n <= 128) go(k_bucket_mates_f32<4>);
+    else if (s.n <= 256) go(k_bucket_mates_f32<8>);
+    else if (s.n <= 512) go(k_bucket_mates_f32<16>);
+    else go(k_bucket_mates_f32<32>);
+  } else if (d_series_f32 != nullptr)
     k_bucket_mates<float><<<blocks_for(slots * 32, 256), 256, 0, stream>>>(
         s, d_series_f32, d_mean, d_inv_sigma, d_sorted_row, d_slot_bucket, d_offsets, mates, world, rank);
   else
