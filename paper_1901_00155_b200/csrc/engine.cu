@@ -225,6 +225,7 @@ struct tsdd_cuda_ctx {
   // tensor-core experiment: the matrix, its hash-sorted copy and the batch split into tf32 parts
   DeviceArray<float> matrix_hi, matrix_lo, sorted_hi, sorted_lo, batch_hi, batch_lo;
   bool split_ready = false, sorted_split_ready = false;
+  uint32_t run_pairs = 0;     // slots whose successor in the hash-sorted order is the same word's next row
   // the dot-product form runs on the tensor cores (csrc/tc_kernels.cu) with fp16 hi / lo parts: dot_form 5, the default
   bool opt_tensor_cores = true;
   bool opt_tc_half = true;    // the split parts are fp16 (dot_form 5 / 6) instead of tf32 (3 / 4)
@@ -483,6 +484,7 @@ uint64_t build_index(tsdd_cuda_ctx* ctx) {
   ctx->sorted_freq = f0;
   ctx->order = o0;
   launches += launch_count_min_freq(ctx->sorted_freq, rows, ctx->scalars.ptr, st);
+  launches += launch_count_runs(ctx->sorted_hash, ctx->sorted_row, rows, ctx->scalars.ptr, st);
 
   return launches;
 }
@@ -585,6 +587,7 @@ void finish_prepare(tsdd_cuda_ctx* ctx) {
   ctx->stats.rows = ctx->rows;
   ctx->stats.buckets = scalars[0];
   ctx->stats.min_freq_candidates = scalars[1];
+  ctx->run_pairs = scalars[2];
   ctx->prepared = true;
   // (a rank of a group must not start another prepare while a peer still copies from its slices)
   if (ctx->group && ctx->shard_rows && !ctx->group->reduce_max(ctx->rank, nullptr, 0))
@@ -1110,12 +1113,12 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
     seeded = true;
   }
   if (pruning) {  // (after the seed: a row whose first mates already put it below the seed stops there)
-    // Ranks that share their bounds split this stage too (slot p belongs to rank p mod world)
+    // Ranks that share their bounds split this stage too (slot p, or 32-slot chunk p, belongs to rank p mod world)
     // and merge the results with the same min-exchange that follows every batch.
     const bool split = ctx->several() && ctx->opt_share_bounds && ctx->opt_mates > 0;
     ctx->stats.kernel_launches += launch_bucket_mates(
         s, ctx->series.ptr, ctx->series_is_f32 ? ctx->series_f32.ptr : nullptr, ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->sorted_row, ctx->slot_bucket.ptr, ctx->offsets.ptr,
-        ctx->opt_mates, split ? static_cast<uint32_t>(ctx->world) : 1u, split ? static_cast<uint32_t>(ctx->rank) : 0u, st);
+        ctx->opt_mates, ctx->run_pairs, split ? static_cast<uint32_t>(ctx->world) : 1u, split ? static_cast<uint32_t>(ctx->rank) : 0u, st);
     if (split) exchange_bounds(ctx);
   }
 
@@ -1562,6 +1565,7 @@ int tsdd_cuda_reindex(tsdd_cuda_ctx* ctx, size_t word_len, size_t alphabet) {
     ctx->stats.kernel_launches += launches;
     ctx->stats.buckets = scalars[0];
     ctx->stats.min_freq_candidates = scalars[1];
+    ctx->run_pairs = scalars[2];
   });
 }
 

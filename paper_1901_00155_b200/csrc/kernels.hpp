@@ -69,6 +69,9 @@ int launch_bucket_index(const uint32_t* d_sorted_hash, const uint32_t* d_sorted_
                         cudaStream_t stream);
 
 // d_scalars[1] = number of leading entries of the sorted frequencies equal to the minimum.
+// scalars[2] += slots whose successor in the hash-sorted order is the same word's next row (runs of consecutive rows)
+int launch_count_runs(const uint32_t* d_sorted_hash, const uint32_t* d_sorted_row, uint32_t rows, uint32_t* d_scalars,
+                      cudaStream_t stream);
 int launch_count_min_freq(const uint32_t* d_sorted_freq, uint32_t rows, uint32_t* d_scalars,
                           cudaStream_t stream);
 
@@ -110,7 +113,8 @@ int launch_min_from_peers(uint64_t* d_nn, PeerPointers peers, uint32_t rows, cud
 // d_series_f32: the float32 originals when the series arrived in that type (else nullptr): same values, half the bytes.
 int launch_bucket_mates(SearchState s, const double* d_series, const float* d_series_f32, const double* d_mean,
                         const double* d_inv_sigma, const uint32_t* d_sorted_row, const uint32_t* d_slot_bucket,
-                        const uint32_t* d_offsets, int mates, uint32_t world, uint32_t rank, cudaStream_t stream);
+                        const uint32_t* d_offsets, int mates, uint32_t run_pairs, uint32_t world, uint32_t rank,
+                        cudaStream_t stream);  // run_pairs: launch_count_runs
 
 // Time topology: every live batch candidate c tries the matches of its neighbours in time,
 // shifted along (row c + delta knows neighbour j  ->  measure (c, j - delta)); up to `tries`

@@ -533,6 +533,15 @@ __global__ void k_count_min_freq(const uint32_t* __restrict__ sorted_freq, uint3
   if (sorted_freq[s] == lowest && (s + 1 == rows || sorted_freq[s + 1] != lowest)) scalars[1] = s + 1;
 }
 
+__global__ void __launch_bounds__(256)
+k_count_runs(const uint32_t* __restrict__ sorted_hash, const uint32_t* __restrict__ sorted_row, uint32_t rows,
+             uint32_t* __restrict__ scalars) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool run = p + 1 < rows && sorted_hash[p + 1] == sorted_hash[p] && sorted_row[p + 1] == sorted_row[p] + 1;
+  const uint32_t n = __popc(__ballot_sync(0xFFFFFFFFu, run));
+  if ((threadIdx.x & 31) == 0 && n) atomicAdd(scalars + 2, n);
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
@@ -637,6 +646,12 @@ int launch_bucket_index(const uint32_t* d_sorted_hash, const uint32_t* d_sorted_
   k_bucket_offsets<<<blocks, 256, 0, stream>>>(d_head_scan, d_slot_bucket, rows, d_offsets, d_scalars);
   k_bucket_freq<<<blocks, 256, 0, stream>>>(d_sorted_row, d_slot_bucket, d_offsets, rows, d_freq);
   return launches + 2;
+}
+
+int launch_count_runs(const uint32_t* d_sorted_hash, const uint32_t* d_sorted_row, uint32_t rows, uint32_t* d_scalars,
+                      cudaStream_t stream) {
+  k_count_runs<<<blocks_for(rows, 256), 256, 0, stream>>>(d_sorted_hash, d_sorted_row, rows, d_scalars);
+  return 1;
 }
 
 int launch_count_min_freq(const uint32_t* d_sorted_freq, uint32_t rows, uint32_t* d_scalars,

@@ -373,6 +373,177 @@ k_bucket_mates_f32(SearchState s, const float* __restrict__ x, const double* __r
   }
 }
 
+// ------------------------------------------------------------------ same-word neighbours along runs of consecutive rows
+// Consecutive slots of a bucket are, for the most part, consecutive positions in time (a smooth
+// series keeps its word for a while), and so are their mates: the pairs (i, j), (i+1, j+1), ... of
+// one warp's 32 slots lie on a diagonal, along which the three sums a pair distance is made of,
+//   P = sum (x[i+t]-a)(x[j+t]-b),  SA = sum (x[i+t]-a)^2,  SB = sum (x[j+t]-b)^2      (t < n),
+// move by ONE product each per step:  P(i+1, j+1) = P(i, j) - (x[i]-a)(x[j]-b) + (x[i+n]-a)(x[j+n]-b).
+// So the warp evaluates the full sums only at the HEADS of its chains (the first lane, and every
+// lane whose row or mate does not continue its left neighbour's), all 32 lanes striding over the
+// window, and reaches the other lanes with a segmented prefix sum over their one-product deltas: a
+// pair costs about 50 instructions instead of 5 n / 32 — workload 4: 5.9 -> ... ms.  Float64
+// throughout, with the head's two window means as the shifts a, b: every product is of the size of
+// the windows' variance, the sums carry ~n 2^-53 of n sigma_i sigma_j, and the distance
+//   d^2 = SSi / sigma_i^2 + SSj / sigma_j^2 - 2 C / (sigma_i sigma_j),  SSi = SA - n (mu_i - a)^2, ...
+// — no use of sum z^2 = n, which holds only as far as sigma itself is exact — comes out to ~1e-9
+// absolute; it is inflated by 1e-6 relative + 1e-8 n absolute and rounded UP to float32: an upper bound.
+// A pair that comes out (almost) at zero is measured again directly, so that exact twins still
+// give exactly 0 (a bound of 0 is dead at once).
+template <typename kSample>
+__global__ void __launch_bounds__(256)
+k_bucket_mates_runs(SearchState s, const kSample* __restrict__ x, const double* __restrict__ mean,
+                    const double* __restrict__ inv_sigma, const uint32_t* __restrict__ sorted_row,
+                    const uint32_t* __restrict__ slot_bucket, const uint32_t* __restrict__ offsets, int mates,
+                    uint32_t world, uint32_t rank) {
+  const uint32_t lane = threadIdx.x & 31;
+  // several ranks that share their bounds afterwards split the 32-slot chunks
+  const uint32_t chunk = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * world + rank;
+  if (static_cast<uint64_t>(chunk) * 32 >= s.n_rows) return;
+  const uint32_t slot = chunk * 32 + lane;
+  const bool valid = slot < s.n_rows;
+  uint32_t b0 = 0, len = 0, row_i = 0xFFFFFFFFu;
+  double mu_i = 0.0, inv_i = 0.0;
+  if (valid) {
+    const uint32_t bucket = slot_bucket[slot];
+    TSDD_BOUND(bucket + 1, s.n_rows + 1);
+    b0 = offsets[bucket];
+    len = offsets[bucket + 1] - b0;
+    row_i = sorted_row[slot];
+    TSDD_BOUND(row_i, s.n_rows);
+    mu_i = mean[row_i];
+    inv_i = inv_sigma[row_i];
+  }
+  uint32_t tries = min(static_cast<uint32_t>(mates), 31u), step = len / (tries + 1);
+  if (step == 0) {
+    step = 1;
+    tries = len > 0 ? min(len - 1, 31u) : 0u;
+  }
+  if (!valid || len < 2) tries = 0;
+  uint32_t most = tries;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) most = max(most, __shfl_xor_sync(0xFFFFFFFFu, most, d));
+  const uint64_t best = *s.best;
+  const double dn = static_cast<double>(s.n);
+  float bound_i = __uint_as_float(kInfBits);
+  unsigned long long calls = 0, terms = 0;
+  for (uint32_t q = 1; q <= most; ++q) {
+    bool active = q <= tries && !dead_bound(bound_i, best, s.margin, s.margin_abs, s.margin_q);
+    uint32_t row_j = 0xFFFFFFFFu;
+    double mu_j = 0.0, inv_j = 0.0;
+    if (active) {
+      const uint32_t other = b0 + (slot - b0 + q * step) % len;
+      TSDD_BOUND(other, s.n_rows);
+      row_j = sorted_row[other];
+      TSDD_BOUND(row_j, s.n_rows);
+      if (gap_u32(row_i, row_j) < s.n) {
+        active = false;
+      } else {
+        mu_j = mean[row_j];
+        inv_j = inv_sigma[row_j];
+      }
+    }
+    const uint32_t act = __ballot_sync(0xFFFFFFFFu, active);
+    if (act == 0) {
+      if (__ballot_sync(0xFFFFFFFFu, q < tries && !dead_bound(bound_i, best, s.margin, s.margin_abs, s.margin_q)) == 0) break;
+      continue;
+    }
+    // chains: lane k continues lane k-1 when both its row and its mate are the next position
+    const uint32_t pi = __shfl_up_sync(0xFFFFFFFFu, row_i, 1), pj = __shfl_up_sync(0xFFFFFFFFu, row_j, 1);
+    const bool prev_active = lane > 0 && ((act >> (lane - 1)) & 1u);
+    const bool follows = active && prev_active && row_i == pi + 1 && row_j == pj + 1;
+    const bool head = active && !follows;
+    const uint32_t heads = __ballot_sync(0xFFFFFFFFu, head);
+    const uint32_t my_head = active ? 31u - __clz(heads & (0xFFFFFFFFu >> (31 - lane))) : lane;
+    const double a = __shfl_sync(0xFFFFFFFFu, mu_i, my_head), b = __shfl_sync(0xFFFFFFFFu, mu_j, my_head);
+    double P = 0.0, SA = 0.0, SB = 0.0;
+    if (follows) {  // one step along the diagonal: the window loses sample -1 and gains sample n-1
+      const double uo = static_cast<double>(x[row_i - 1]) - a, vo = static_cast<double>(x[row_j - 1]) - b;
+      const double un = static_cast<double>(x[row_i + s.n - 1]) - a, vn = static_cast<double>(x[row_j + s.n - 1]) - b;
+      P = un * vn - uo * vo;
+      SA = un * un - uo * uo;
+      SB = vn * vn - vo * vo;
+    }
+    for (uint32_t todo = heads; todo != 0; todo &= todo - 1) {  // the full sums of every chain's first pair
+      const int h = __ffs(todo) - 1;
+      const uint32_t ri = __shfl_sync(0xFFFFFFFFu, row_i, h), rj = __shfl_sync(0xFFFFFFFFu, row_j, h);
+      const double ha = __shfl_sync(0xFFFFFFFFu, mu_i, h), hb = __shfl_sync(0xFFFFFFFFu, mu_j, h);
+      const kSample* qi = x + ri;
+      const kSample* qj = x + rj;
+      double p0 = 0.0, p1 = 0.0, sa0 = 0.0, sa1 = 0.0, sb0 = 0.0, sb1 = 0.0;
+      uint32_t t = lane;
+      for (; t + 32 < s.n; t += 64) {
+        const kSample x0 = qi[t], x1 = qi[t + 32], y0 = __ldg(qj + t), y1 = __ldg(qj + t + 32);
+        const double u0 = static_cast<double>(x0) - ha, u1 = static_cast<double>(x1) - ha;
+        const double v0 = static_cast<double>(y0) - hb, v1 = static_cast<double>(y1) - hb;
+        p0 = fma(u0, v0, p0), p1 = fma(u1, v1, p1);
+        sa0 = fma(u0, u0, sa0), sa1 = fma(u1, u1, sa1);
+        sb0 = fma(v0, v0, sb0), sb1 = fma(v1, v1, sb1);
+      }
+      if (t < s.n) {
+        const double u0 = static_cast<double>(qi[t]) - ha, v0 = static_cast<double>(__ldg(qj + t)) - hb;
+        p0 = fma(u0, v0, p0), sa0 = fma(u0, u0, sa0), sb0 = fma(v0, v0, sb0);
+      }
+      double p = p0 + p1, sa = sa0 + sa1, sb = sb0 + sb1;
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) {
+        p += __shfl_xor_sync(0xFFFFFFFFu, p, d);
+        sa += __shfl_xor_sync(0xFFFFFFFFu, sa, d);
+        sb += __shfl_xor_sync(0xFFFFFFFFu, sb, d);
+      }
+      if (static_cast<int>(lane) == h) P = p, SA = sa, SB = sb;
+    }
+    // segmented inclusive prefix sums: a head holds its chain's full sums, a follower its delta
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double tp = __shfl_up_sync(0xFFFFFFFFu, P, d), ta = __shfl_up_sync(0xFFFFFFFFu, SA, d),
+                   tb = __shfl_up_sync(0xFFFFFFFFu, SB, d);
+      if (active && lane >= my_head + d) P += tp, SA += ta, SB += tb;
+    }
+    float sum = __uint_as_float(kInfBits);
+    bool again = false;
+    if (active) {
+      const double da = mu_i - a, db = mu_j - b;
+      const double ssi = SA - dn * da * da, ssj = SB - dn * db * db, cov = P - dn * da * db;
+      double d2 = inv_i * inv_i * ssi + inv_j * inv_j * ssj - 2.0 * inv_i * inv_j * cov;
+      d2 = fmax(d2, 0.0);
+      again = d2 < 1e-6 * dn;  // (almost) a twin: settled by the direct sum below
+      sum = __double2float_ru(fma(d2, 1.0 + 1e-6, 1e-8 * dn));
+    }
+    for (uint32_t todo = __ballot_sync(0xFFFFFFFFu, again); todo != 0; todo &= todo - 1) {
+      const int h = __ffs(todo) - 1;
+      const uint32_t ri = __shfl_sync(0xFFFFFFFFu, row_i, h), rj = __shfl_sync(0xFFFFFFFFu, row_j, h);
+      const double ma = __shfl_sync(0xFFFFFFFFu, mu_i, h), mb = __shfl_sync(0xFFFFFFFFu, mu_j, h);
+      const double ia = __shfl_sync(0xFFFFFFFFu, inv_i, h), ib = __shfl_sync(0xFFFFFFFFu, inv_j, h);
+      double acc = 0.0;
+      for (uint32_t t = lane; t < s.n; t += 32) {
+        const double d = (static_cast<double>(x[ri + t]) - ma) * ia - (static_cast<double>(__ldg(x + rj + t)) - mb) * ib;
+        acc = fma(d, d, acc);
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, d);
+      if (static_cast<int>(lane) == h) sum = __double2float_ru(acc);
+    }
+    if (active) {
+      bound_i = fminf(bound_i, sum);
+      const uint32_t bits = __float_as_uint(sum);
+      atomicMin(as_ull(s.nn + row_i), static_cast<unsigned long long>(nn_key(bits, row_j)));
+      atomicMin(as_ull(s.nn + row_j), static_cast<unsigned long long>(nn_key(bits, row_i)));
+      calls += 1;
+      terms += head || again ? s.n : 2u;
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    calls += __shfl_xor_sync(0xFFFFFFFFu, calls, d);
+    terms += __shfl_xor_sync(0xFFFFFFFFu, terms, d);
+  }
+  if (lane == 0 && calls) {
+    atomicAdd(&s.counters->calls, calls);
+    atomicAdd(&s.counters->terms, terms);
+  }
+}
+
 // ------------------------------------------------------------------ time topology
 // Overlapping windows have overlapping matches.  If row a = c + delta has found a neighbour j at
 // distance d, then rows c and j - delta are those same two windows, both shifted by delta
@@ -2491,10 +2662,23 @@ int launch_min_from_peers(uint64_t* d_nn, PeerPointers peers, uint32_t rows, cud
 
 int launch_bucket_mates(SearchState s, const double* d_series, const float* d_series_f32, const double* d_mean,
                         const double* d_inv_sigma, const uint32_t* d_sorted_row, const uint32_t* d_slot_bucket,
-                        const uint32_t* d_offsets, int mates, uint32_t world, uint32_t rank, cudaStream_t stream) {
+                        const uint32_t* d_offsets, int mates, uint32_t run_pairs, uint32_t world, uint32_t rank,
+                        cudaStream_t stream) {
   if (mates <= 0) return 0;
   const size_t slots = (static_cast<size_t>(s.n_rows) + world - 1) / world;
-  static const bool old_form = [] { const char* e = std::getenv("TSDD_MATES_F64"); return e && e[0] == '1'; }();
+  static const int form = [] { const char* e = std::getenv("TSDD_MATES_FORM"); return e ? std::atoi(e) : -1; }();
+  const bool old_form = form == 0;
+  // buckets that are mostly runs of consecutive rows: chains along the diagonals (k_bucket_mates_runs)
+  if (form == 2 || (form < 0 && static_cast<uint64_t>(run_pairs) * 2 >= s.n_rows)) {
+    const size_t chunks = ((static_cast<size_t>(s.n_rows) + 31) / 32 + world - 1) / world;
+    if (d_series_f32 != nullptr)
+      k_bucket_mates_runs<float><<<blocks_for(chunks * 32, 256), 256, 0, stream>>>(
+          s, d_series_f32, d_mean, d_inv_sigma, d_sorted_row, d_slot_bucket, d_offsets, mates, world, rank);
+    else
+      k_bucket_mates_runs<double><<<blocks_for(chunks * 32, 256), 256, 0, stream>>>(
+          s, d_series, d_mean, d_inv_sigma, d_sorted_row, d_slot_bucket, d_offsets, mates, world, rank);
+    return 1;
+  }
   if (d_series_f32 != nullptr && s.n <= 1024 && !old_form) {
     const unsigned blocks = blocks_for(slots * 32, 256);
     auto go = [&](auto kernel) {
