@@ -202,6 +202,7 @@ struct tsdd_cuda_ctx {
   bool opt_time_kernels = true;
   bool opt_share_bounds = true;
   bool opt_lower_bound = true;      // tile filter by segment-mean lower bounds in the covering scan
+  double opt_encode_tol_scale = 1.0;  // k_window_encode4<aligned>: x its tolerance around the breakpoints (0: the exact path only)
   uint32_t opt_seed_rows = 4096;    // rows whose lower bounds seed the best-so-far of the first pass (0 = none)
   // the lower-bound filter on the ws kernel's producer warpgroup (needs tensor_map).  Correct, and
   // faster per term, but its 128-row neighbour tiles rule out and abandon less than k_scan_tiles'
@@ -537,7 +538,7 @@ void prepare_on_device(tsdd_cuda_ctx* ctx, size_t m, size_t n, size_t word_len, 
       launches += launch_window_encode(ctx->series.ptr + row0, count, static_cast<uint32_t>(n),
                                        static_cast<uint32_t>(word_len), static_cast<uint32_t>(alphabet),
                                        ctx->mean.ptr + row0, ctx->inv_sigma.ptr + row0, ctx->hash0.ptr + row0, nullptr,
-                                       nullptr, st);
+                                       nullptr, st, ctx->opt_encode_tol_scale);
   }
   if (shard) gather_slices(ctx, slice);
 
@@ -1108,7 +1109,7 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   if (pruning && ctx->opt_lower_bound && ctx->opt_seed_rows > 0 && s.lb_means != nullptr) {
     // (the seed costs seed_rows x N / 16 box tests: keep it at 1/64 of the rows on small inputs)
     const uint32_t seed_rows = std::min(ctx->opt_seed_rows, std::max(256u, ctx->rows / 64));
-    ctx->seed_lb.alloc(seed_rows);
+    ctx->seed_lb.alloc(2 * static_cast<size_t>(seed_rows));  // (the two-pass seed keeps its selection there)
     ctx->stats.kernel_launches += launch_seed_lower_bound(s, ctx->order, seed_rows, ctx->seed_lb.ptr, st);
     seeded = true;
   }
@@ -1430,6 +1431,9 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
       ctx->opt_wide_tile = value != 0;
     } else if (key == "lower_bound") {
       ctx->opt_lower_bound = value != 0;
+    } else if (key == "encode_tol_scale") {
+      if (value < 0) fail(TSDD_ERR_PARAMETER, "encode_tol_scale must be >= 0");
+      ctx->opt_encode_tol_scale = value;
     } else if (key == "seed_rows") {
       if (value < 0 || value > 1048576) fail(TSDD_ERR_PARAMETER, "seed_rows must be in 0..1048576");
       ctx->opt_seed_rows = static_cast<uint32_t>(value);
@@ -1552,7 +1556,8 @@ int tsdd_cuda_reindex(tsdd_cuda_ctx* ctx, size_t word_len, size_t alphabet) {
     CUDA_OK(cudaEventRecord(ctx->ev_a, st));
     uint64_t launches = launch_window_encode(ctx->series.ptr, ctx->rows, static_cast<uint32_t>(ctx->n),
                                              static_cast<uint32_t>(word_len), static_cast<uint32_t>(alphabet),
-                                             ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->hash0.ptr, nullptr, nullptr, st);
+                                             ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->hash0.ptr, nullptr, nullptr, st,
+                                             ctx->opt_encode_tol_scale);
     launches += build_index(ctx);
     uint32_t scalars[4] = {0, 0, 0, 0};
     CUDA_OK(cudaMemcpyAsync(scalars, ctx->scalars.ptr, sizeof(scalars), cudaMemcpyDeviceToHost, st));

@@ -30,10 +30,11 @@ constexpr uint32_t kRowAlign = kChunk;   // row stride is a multiple of this man
 int launch_widen_series(const float* d_in, double* d_out, size_t m, uint32_t* d_first_bad, cudaStream_t stream);
 
 // Per-window mean / 1/sigma (float64), PAA -> SAX -> 0-based word hash.
-// paa_out / sax_out may be null (kept only for parity tests).
+// paa_out / sax_out may be null (kept only for parity tests).  tol_scale: the aligned form's distance-to-breakpoint
+// tolerance is multiplied by it (tests inflate it to force the exact path; 0 = exact path only).
 int launch_window_encode(const double* d_series, uint32_t rows, uint32_t n, uint32_t word_len,
                          uint32_t alphabet, double* d_mean, double* d_inv_sigma, uint32_t* d_hash0,
-                         double* d_paa, uint32_t* d_sax, cudaStream_t stream);
+                         double* d_paa, uint32_t* d_sax, cudaStream_t stream, double tol_scale = 1.0);
 
 // float32 z-normalised matrix, rows x stride, padding columns zero; and, when d_seg_means is
 // given, the kLbSegments segment means of every row (from the same staged samples).

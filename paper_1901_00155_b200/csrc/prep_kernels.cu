@@ -8,6 +8,8 @@
 
 #include "kernels.hpp"
 
+#include <cstdlib>
+
 namespace tsdd_b200 {
 
 namespace {
@@ -115,15 +117,26 @@ k_window_encode(const double* __restrict__ x, uint32_t rows, uint32_t n, uint32_
 // before (bit-identical mean, sigma, PAA, symbols: the parity tests compare every array).
 constexpr int kEncWindows = 4;
 constexpr int kEncThreads = 256;
-constexpr size_t encode4_smem_bytes(uint32_t n) {
-  return (static_cast<size_t>(kEncThreads) * kEncWindows + n + 16) * sizeof(double);
+constexpr size_t encode4_smem_bytes(uint32_t n, bool with_prefix = false) {
+  // samples (interleaved by four, with slack) + in the aligned form their prefix sums and the block-scan scratch
+  const size_t samples = static_cast<size_t>(kEncThreads) * kEncWindows + n + 16;
+  return (samples + (with_prefix ? samples + 2 * kEncThreads : 0)) * sizeof(double);
 }
 
+// kAligned (word_len divides n, and nobody asked for the PAA values): every sample lies wholly in one
+// segment, so a segment's sum over the NORMALISED samples is ((P[end] - P[start]) - len * mu) / sigma with P the
+// prefix sums of the block's staged samples — two loads a segment instead of four float64 operations a sample
+// (60 % of the kernel's arithmetic; workload 4: 3.4 -> ... ms).  That value differs from the reference's
+// sample-by-sample sum by rounding only, which can matter to a SYMBOL only within `tol` of a breakpoint (tol: a
+// rigorous bound of both roundings from the block's sum of |x|); a window with a segment that close is encoded
+// the reference's way.  Means, 1/sigma (their sums stay in sequence order), symbols and hashes remain
+// bit-identical to the reference's.
+template <bool kAligned>
 __global__ void __launch_bounds__(kEncThreads)
 k_window_encode4(const double* __restrict__ x, uint32_t rows, uint32_t n, uint32_t word_len,
                  uint32_t alphabet, double* __restrict__ mean, double* __restrict__ inv_sigma,
                  uint32_t* __restrict__ hash0, double* __restrict__ paa_out,
-                 uint32_t* __restrict__ sax_out) {
+                 uint32_t* __restrict__ sax_out, double tol_scale) {
   extern __shared__ double s_x[];
   const uint32_t w0 = blockIdx.x * (kEncThreads * kEncWindows);  // first window of the block
   const uint32_t span = kEncThreads * kEncWindows + n + 4;       // samples any of its threads touches
@@ -136,6 +149,33 @@ k_window_encode4(const double* __restrict__ x, uint32_t rows, uint32_t n, uint32
   __syncthreads();
   const uint32_t base = kEncWindows * threadIdx.x;  // this thread's first window, relative to w0
   auto sample = [&](uint32_t j) -> double { return s_x[(j & 3u) * quarter + (j >> 2)]; };
+  double* s_p = s_x + 4 * quarter;          // kAligned: s_p[j] = sum of the staged samples before j
+  double abs_total = 0.0;                   // ... and the sum of their magnitudes
+  if constexpr (kAligned) {
+    double* s_part = s_p + span + 1;        // block-scan scratch: kEncThreads sums, kEncThreads sums of magnitudes
+    const uint32_t per = (span + kEncThreads - 1) / kEncThreads;
+    const uint32_t j0 = min(threadIdx.x * per, span), j1 = min(j0 + per, span);
+    double part = 0.0, part_abs = 0.0;
+    for (uint32_t j = j0; j < j1; ++j) {
+      const double v = sample(j);
+      part += v;
+      part_abs += fabs(v);
+    }
+    s_part[threadIdx.x] = part;
+    s_part[kEncThreads + threadIdx.x] = part_abs;
+    __syncthreads();
+    double before = 0.0;
+    for (uint32_t t = 0; t < kEncThreads; ++t) {  // (256 broadcast loads; the block's own arithmetic is 4 x n per thread)
+      before += t < threadIdx.x ? s_part[t] : 0.0;
+      abs_total += s_part[kEncThreads + t];
+    }
+    for (uint32_t j = j0; j < j1; ++j) {
+      s_p[j] = before;
+      before += sample(j);
+    }
+    if (j1 == span && j0 < span) s_p[span] = before;
+    __syncthreads();
+  }
 
   // ---- mean, sigma (series.cpp:21-37)
   double w[kEncWindows], sum[kEncWindows], sum_sq[kEncWindows];
@@ -172,6 +212,36 @@ k_window_encode4(const double* __restrict__ x, uint32_t rows, uint32_t n, uint32
   // ---- PAA, symbols, hash (sax.cpp:53-80,121-132)
   const double* bp = c_breaks[alphabet - 2];
   uint64_t h[kEncWindows];
+  if constexpr (kAligned) {
+    const uint32_t len = n / word_len;
+    const double scale = static_cast<double>(word_len) / dn, dlen = static_cast<double>(len);
+    // both roundings: prefix sums (<= span additions each), len * mu, and the reference's own sum (<= 4 n 2^-53 |seg|)
+    const double eps_sum = 3.0 * static_cast<double>(span) * 2.220446049250313e-16 * abs_total * scale;
+    bool close = false;
+#pragma unroll
+    for (int r = 0; r < kEncWindows; ++r) {
+      h[r] = 0;
+      const double tol = (eps_sum * inv[r] + 1e-11) * tol_scale;
+      for (uint32_t k = 0; k < word_len; ++k) {
+        const double sum_k = s_p[base + r + (k + 1) * len] - s_p[base + r + k * len];
+        const double seg = flat[r] ? 0.0 : (sum_k - dlen * mu[r]) * inv[r] * scale;
+        uint32_t sym = 1;
+        for (uint32_t b = 0; b + 1 < alphabet; ++b) {
+          sym += (bp[b] <= seg) ? 1u : 0u;
+          close |= !flat[r] && fabs(seg - bp[b]) <= tol;
+        }
+        h[r] = h[r] * alphabet + (sym - 1);
+      }
+    }
+    if (!close) {
+#pragma unroll
+      for (int r = 0; r < kEncWindows; ++r) {
+        const uint32_t i = w0 + base + r;
+        if (i < rows) hash0[i] = static_cast<uint32_t>(h[r]);
+      }
+      return;
+    }
+  }
 #pragma unroll
   for (int r = 0; r < kEncWindows; ++r) w[r] = sample(base + r), h[r] = 0;
   uint32_t cur = 0;  // w[r] holds local sample cur of window r
@@ -553,12 +623,15 @@ int launch_widen_series(const float* d_in, double* d_out, size_t m, uint32_t* d_
 
 int launch_window_encode(const double* d_series, uint32_t rows, uint32_t n, uint32_t word_len,
                          uint32_t alphabet, double* d_mean, double* d_inv_sigma, uint32_t* d_hash0,
-                         double* d_paa, uint32_t* d_sax, cudaStream_t stream) {
-  const size_t smem = encode4_smem_bytes(n);
+                         double* d_paa, uint32_t* d_sax, cudaStream_t stream, double tol_scale) {
+  static const bool exact_only = [] { const char* e = std::getenv("TSDD_ENCODE_EXACT"); return e && e[0] == '1'; }();
+  const bool aligned = n % word_len == 0 && d_paa == nullptr && d_sax == nullptr && !exact_only && tol_scale > 0.0;
+  const size_t smem = encode4_smem_bytes(n, aligned);
   if (smem <= 200 * 1024) {  // (longer windows than ~24,000 samples: the one-window-per-thread kernel)
-    cudaFuncSetAttribute(k_window_encode4, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    k_window_encode4<<<blocks_for(rows, kEncThreads * kEncWindows), kEncThreads, smem, stream>>>(
-        d_series, rows, n, word_len, alphabet, d_mean, d_inv_sigma, d_hash0, d_paa, d_sax);
+    auto kernel = aligned ? k_window_encode4<true> : k_window_encode4<false>;
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kernel<<<blocks_for(rows, kEncThreads * kEncWindows), kEncThreads, smem, stream>>>(
+        d_series, rows, n, word_len, alphabet, d_mean, d_inv_sigma, d_hash0, d_paa, d_sax, tol_scale);
     return 1;
   }
   k_window_encode<<<blocks_for(rows, 256), 256, 0, stream>>>(d_series, rows, n, word_len, alphabet,

@@ -115,6 +115,32 @@ def test_preparation_arrays_match_the_reference(ctx, chk, m, n, w, a):
     assert st["min_freq_candidates"] == len(ref["candidates"])
 
 
+@pytest.mark.parametrize("scale", [1.0, 1e9, 0.0], ids=["tolerance", "everything-close", "exact-only"])
+@pytest.mark.parametrize("kind", ["walk", "offset", "steps"])
+def test_aligned_encode_keeps_every_symbol(ctx, chk, kind, scale):
+    """k_window_encode4<aligned> takes a segment's sum from prefix sums and encodes a window the reference's
+    way only where a segment lies within its tolerance of a breakpoint: hashes and frequencies must stay
+    those of the reference with the tolerance as it is, inflated (every window takes the exact path) and
+    with the form switched off — on a walk, under an offset 1e4 times the spread, on quantised steps."""
+    rng = np.random.default_rng(77)
+    m, n, w, a = 6000, 128, 8, 6
+    if kind == "walk":
+        x = np.cumsum(rng.standard_normal(m)).astype(np.float32)
+    elif kind == "offset":
+        x = (1e4 + rng.standard_normal(m)).astype(np.float32)
+    else:
+        x = np.round(np.cumsum(rng.standard_normal(m)) / 4).astype(np.float32)  # many exactly equal segment means
+    ctx.set_option("encode_tol_scale", scale)
+    try:
+        ctx.prepare(x, n, w, a)
+        got_hash, got_freq = ctx.fetch("hash"), ctx.fetch("freq")
+    finally:
+        ctx.set_option("encode_tol_scale", 1.0)
+    ref = chk.prepare(x, n, w, a)
+    np.testing.assert_array_equal(got_hash, ref["hashes"])
+    np.testing.assert_array_equal(got_freq, ref["freq"])
+
+
 def test_flat_windows_become_zero_rows(ctx, chk):
     x = W.random_walk(5, 2000)
     x[500:700] = np.float32(1.25)  # constant stretch: sigma < 1e-12 -> all-zero rows (series.cpp:30-33)
