@@ -105,7 +105,10 @@ struct DeviceCounters {
   // at most (2n - 1) / N of all pairs, are not taken out.)
   unsigned long long useful_terms;
   unsigned long long propagated;  // pair distances measured by the time-topology step (k_propagate)
-  unsigned long long tc_terms;    // of dot_terms, those computed on the tensor cores (tc_kernels.cu: 3 tf32 MACs a term)
+  unsigned long long tc_terms;    // of dot_terms, those computed on the tensor cores (tc_kernels.cu: 3 MMA multiply-adds a term)
+  // of calls, those of covering scans that ran on the tensor cores in a search that is NOT in the dot form
+  // (engine.cu: tail_now) — they never abandon and say nothing about whether abandoning pays
+  unsigned long long tail_calls;
 };
 
 }  // namespace tsdd_b200

@@ -255,6 +255,14 @@ struct tsdd_cuda_ctx {
   // anyway; used (and the discard band widened by margin_abs, for the rest of the search) from the
   // first batch on whose best-so-far dwarfs the error bound; dot_now: this batch launches it.
   bool dot_wanted = false, dot_used = false, dot_now = false;
+  // tail_now: this batch's covering scans of FEW candidates run on the tensor cores although the search is not in
+  // the dot form (the candidates that reach a covering scan of a search whose tiles are abandoned and ruled out are
+  // those that must meet every row — the rows around a discord: dense work); the band is widened like for dot_used
+  bool tail_now = false;
+  int sm_count = 148;
+  uint64_t lb_launches = 0;  // launches of the kernel with the lower-bound filter in this search (evidence for lb_decided)
+  bool opt_tc_tail = true;
+  uint32_t opt_tc_tail_most = 1024;  // ... while at most so many candidates are left
   uint32_t* h_sel = nullptr;      // pinned, 4 words + a ring of 4 x 4 words for lagged counts
   cudaEvent_t ev_ring[4] = {nullptr, nullptr, nullptr, nullptr};
   uint64_t* h_keys = nullptr;     // pinned, 4 keys
@@ -766,6 +774,40 @@ std::vector<uint32_t> range_bounds(uint32_t rows, int rounds, uint32_t first, do
   return bounds;
 }
 
+// The tensor-core form's operands: fp16 (or tf32) hi / lo parts of the matrix and, where it exists, of its
+// hash-sorted copy; skipped when memory is short.
+void build_split_copies(tsdd_cuda_ctx* ctx, uint32_t batch_now) {
+  cudaStream_t st = ctx->stream;
+  const size_t floats = static_cast<size_t>(ctx->rows_padded) * ctx->stride;
+  const size_t words = ctx->opt_tc_half ? (floats + 1) / 2 : floats;  // (the arrays are float-typed; fp16 parts take half)
+  size_t free_b = 0, total_b = 0;
+  const bool have = ctx->matrix_hi.count >= words && (!ctx->sorted_ready || ctx->sorted_hi.count >= words);
+  if (!have) CUDA_OK(cudaMemGetInfo(&free_b, &total_b));  // (slow: only when the copies have to grow)
+  const size_t need = words * sizeof(float) * (ctx->sorted_ready ? 4 : 2);
+  if (!have && free_b <= need + (size_t{2} << 30)) return;
+  ctx->matrix_hi.alloc(words);
+  ctx->matrix_lo.alloc(words);
+  if (!ctx->norms_ready) {  // one pass over the matrix for both
+    ctx->row_norms.alloc(static_cast<size_t>(ctx->rows) + 1);
+    ctx->stats.kernel_launches += launch_split_rows_norms(ctx->matrix.ptr, ctx->rows_padded, ctx->stride, ctx->opt_tc_half,
+                                                          ctx->matrix_hi.ptr, ctx->matrix_lo.ptr, ctx->row_norms.ptr, ctx->rows + 1, st);
+    ctx->norms_ready = true;
+  } else {
+    ctx->stats.kernel_launches += launch_split_rows(ctx->matrix.ptr, floats, ctx->opt_tc_half, ctx->matrix_hi.ptr, ctx->matrix_lo.ptr, st);
+  }
+  if (ctx->sorted_ready) {
+    ctx->sorted_hi.alloc(words);
+    ctx->sorted_lo.alloc(words);
+    ctx->stats.kernel_launches +=
+        launch_split_rows(ctx->matrix_sorted.ptr, floats, ctx->opt_tc_half, ctx->sorted_hi.ptr, ctx->sorted_lo.ptr, st);
+    ctx->sorted_split_ready = true;
+  }
+  ctx->split_ready = true;
+  const uint32_t capacity = ctx->batch_capacity;
+  ctx->batch_capacity = 0;  // (the batch buffers grow their split twins)
+  ensure_batch_capacity(ctx, std::max(capacity, batch_now));
+}
+
 struct Segment {
   bool window;              // same-word neighbourhood (bounds only) or covering scan
   uint32_t k_begin, k_end;  // neighbour tile numbers
@@ -827,10 +869,9 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
   // ring of tiles), so that the rows whose bounds drop as a by-product (d(i,j) = d(j,i))
   // are spread over the whole series instead of always being the first ones.
   const uint32_t slot_tiles = (ctx->rows + kTileRows - 1) / kTileRows;
-  // (not with the tensor-core kernel: it walks 256-row tiles in place, and a batch whose segments
-  // mix it with the rotated kernels would leave rows unvisited)
+  // (the tensor-core kernel walks 256-row tiles in place: its launches are given the rotated ranges, below)
   const uint32_t rotation =
-      (pruning && ctx->opt_rotate && !(ctx->opt_tensor_cores && ctx->split_ready))
+      (pruning && ctx->opt_rotate)
           ? static_cast<uint32_t>((ctx->stats.batches * 0.6180339887498949 - std::floor(ctx->stats.batches * 0.6180339887498949)) * slot_tiles) % slot_tiles
           : 0u;
   // The live count after each compaction is read back ONE segment late: segment r's grid is
@@ -838,6 +879,14 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
   // CTAs exit at once), so the host never waits for the segment the GPU is working on and
   // the GPU never waits for the host.
   const std::vector<Segment> plan = plan_segments(ctx, pruning);
+  struct SegEvent {
+    size_t r;
+    bool window, tc;
+    uint32_t tiles;
+    cudaEvent_t e0, e1;
+  };
+  std::vector<SegEvent> seg_events;  // this batch's tile launches (for the tensor-core tail's decision)
+  bool tail_on = false;
   // time topology: before anything else, and again once the window rounds are over
   if (pruning) launches += launch_propagate(s, list, ctx->sel.ptr, count, ctx->opt_propagate, st);
   for (size_t r = 0; r < plan.size(); ++r) {
@@ -868,6 +917,56 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
     ScanChoice choice_now = choice;
     if (choice_now.tc && plan[r].window && !ctx->sorted_split_ready) choice_now.tc = false;  // (no split copy of the sorted matrix)
     if (choice.tc && !choice_now.tc) choice_now.tile16 = ctx->opt_tile16 && count > 192;
+    // Tensor-core tail (tail_now): the covering scan of a search that is NOT in the dot form goes on on the tensor
+    // cores once that is the cheaper way for what is left of it.  Evidence: the time the latest FINISHED covering
+    // segment of this batch took per neighbour tile on the CUDA cores (filter, abandoning and all) against what the
+    // tensor cores need for the same tiles — every pair of the tile, about 40 % of their MMA rate — plus, the first
+    // time, the price of the split copies of the matrix.  (The early segments are small and cost next to nothing
+    // either way; the decision is taken again at every segment until it falls.)
+    if (ctx->tail_now && !plan[r].window && !choice_now.tc && !tail_on && count <= ctx->opt_tc_tail_most && ctx->opt_time_kernels) {
+      double cuda_ms_per_tile = -1.0;
+      for (size_t q = seg_events.size(); q-- > 0;) {  // the latest covering segment whose events have completed
+        const SegEvent& ev = seg_events[q];
+        if (ev.window || ev.tc || ev.tiles < 256 || ev.r + 2 > r) continue;  // (a small segment is mostly launch overhead)
+        float ms = 0.f;
+        if (cudaEventQuery(ev.e1) == cudaSuccess && cudaEventElapsedTime(&ms, ev.e0, ev.e1) == cudaSuccess)
+          cuda_ms_per_tile = ms / ev.tiles;
+        else
+          (void)cudaGetLastError();  // (not finished yet: no evidence this time)
+        break;
+      }
+      if (cuda_ms_per_tile > 0.0) {
+        uint64_t tiles_left = 0;
+        for (size_t q = r; q < plan.size(); ++q) tiles_left += plan[q].window ? 0 : plan[q].k_end - plan[q].k_begin;
+        const double cuda_ms = cuda_ms_per_tile * static_cast<double>(tiles_left);
+        const double cand_tiles = std::ceil(count / 128.0);
+        // one 128 x 256 tile: 3 MMAs per 16 columns, 128 cycles each at 1.9 GHz, over the SMs, at 40 % of that rate
+        const double tile_ms = 3.0 * (ctx->stride / 16.0) * 128.0 / 1.9e6 / ctx->sm_count / 0.4;
+        const double tc_ms = cand_tiles * (tiles_left / 2.0) * tile_ms;
+        const double matrix_bytes = static_cast<double>(ctx->rows_padded) * ctx->stride * sizeof(float);
+        const double split_ms = ctx->split_ready ? 0.0 : 2.0 * matrix_bytes / 6.0e9;  // (read once, written once, ~6 TB/s)
+        if (const char* env = std::getenv("TSDD_TRACE"); env && env[0] == '1')
+          std::fprintf(stderr, "tail? batch %llu segment %zu live<=%u: cuda %.3f ms for %llu tiles, tensor cores %.3f ms + split %.3f ms\n",
+                       static_cast<unsigned long long>(ctx->stats.batches), r, count, cuda_ms,
+                       static_cast<unsigned long long>(tiles_left), tc_ms, split_ms);
+        static const bool force = [] { const char* e = std::getenv("TSDD_TAIL_FORCE"); return e && e[0] == '1'; }();
+        if (force || cuda_ms > (ctx->split_ready ? 1.5 : 2.5) * (tc_ms + split_ms)) {
+          if (!ctx->split_ready) build_split_copies(ctx, count);
+          if (ctx->split_ready && !ctx->norms_ready) {
+            ctx->row_norms.alloc(static_cast<size_t>(ctx->rows) + 1);
+            ctx->stats.kernel_launches += launch_row_norms(ctx->matrix.ptr, ctx->rows + 1, ctx->stride, ctx->row_norms.ptr, st);
+            ctx->norms_ready = true;
+          }
+          tail_on = ctx->split_ready;
+          s = ctx->state();
+        }
+      }
+    }
+    if (tail_on && !plan[r].window && !choice_now.tc && count <= ctx->opt_tc_tail_most) {
+      choice_now = ScanChoice{};  // the tensor-core kernel: dot form, tensor-map boxes, no filter, no abandoning
+      choice_now.packed = choice.packed;
+      choice_now.ws = choice_now.dot = choice_now.tma = choice_now.tc = true;
+    }
     const uint32_t padded = round_up_u32(count, choice_now.tile16 ? 2 * kTileRows : kTileRows);
     if (choice_now.tc)
       launches += launch_gather_rows_split(s, list, ctx->sel.ptr, padded, ctx->opt_tc_half, ctx->batch_hi.ptr, ctx->batch_lo.ptr, st);
@@ -885,9 +984,21 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
     if (choice_now.tc) {
       ctx->tc_work.alloc(1);
       const TcOperands op{ctx->batch_hi.ptr, ctx->batch_lo.ptr, ctx->matrix_hi.ptr, ctx->matrix_lo.ptr,
-                          ctx->sorted_hi.ptr, ctx->sorted_lo.ptr, ctx->rows_padded, ctx->opt_tc_half, ctx->tc_work.ptr};
-      launched = launch_scan_tiles_tc(s, op, list, slots, ctx->sel.ptr, count, plan[r].window ? ctx->sorted_row : nullptr,
-                                      plan[r].k_begin, plan[r].k_end, pruning, ctx->opt_symmetric, st, &launch_error);
+                          ctx->sorted_hi.ptr, ctx->sorted_lo.ptr, ctx->rows_padded, ctx->opt_tc_half, ctx->tc_work.ptr,
+                          ctx->tail_now && !ctx->dot_now};
+      if (plan[r].window || rotation == 0) {
+        launched = launch_scan_tiles_tc(s, op, list, slots, ctx->sel.ptr, count, plan[r].window ? ctx->sorted_row : nullptr,
+                                        plan[r].k_begin, plan[r].k_end, pruning, ctx->opt_symmetric, st, &launch_error);
+      } else {
+        // the rows the other kernels reach as units (k + rotation) mod T: one range of the ring, or two where it wraps
+        const uint32_t from = (plan[r].k_begin + rotation) % slot_tiles, len = plan[r].k_end - plan[r].k_begin;
+        const uint32_t upto = std::min(from + len, slot_tiles);
+        launched = launch_scan_tiles_tc(s, op, list, slots, ctx->sel.ptr, count, nullptr, from, upto, pruning,
+                                        ctx->opt_symmetric, st, &launch_error);
+        if (from + len > slot_tiles && !launch_error)
+          launched += launch_scan_tiles_tc(s, op, list, slots, ctx->sel.ptr, count, nullptr, 0, from + len - slot_tiles, pruning,
+                                           ctx->opt_symmetric, st, &launch_error);
+      }
       if (launched) ctx->stats.scan_kernel_tc_launches += launched;
     } else {
       launched = launch_scan_tiles(choice_now, s, ctx->batch_matrix.ptr, list, slots, ctx->sel.ptr, count,
@@ -895,10 +1006,12 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
                                    pruning, ctx->opt_symmetric, st, &launch_error);
     }
     if (ctx->opt_time_kernels) CUDA_OK(cudaEventRecord(e1, st));
+    if (ctx->opt_time_kernels && launched) seg_events.push_back({r, plan[r].window, choice_now.tc, plan[r].k_end - plan[r].k_begin, e0, e1});
     if (launch_error) fail(TSDD_ERR_RUNTIME, launch_error);
     if (ctx->opt_time_kernels) ctx->trace.push_back({ctx->cur_pass, ctx->stats.batches, plan[r].window, plan[r].k_begin, plan[r].k_end, count, choice_now});
     launches += launched;
     ctx->stats.scan_kernel_launches += launched;
+    if (launched && choice_now.lb) ctx->lb_launches += launched;
     if (launched && choice_now.ws) ctx->stats.scan_kernel_ws_launches += launched;
     if (launched && choice_now.dot) ctx->stats.scan_kernel_dot_launches += launched;
   }
@@ -918,8 +1031,9 @@ bool few_abandoned(tsdd_cuda_ctx* ctx) {
   DeviceCounters c{};
   CUDA_OK(cudaMemcpyAsync(&c, ctx->counters.ptr, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
   sync_stream(ctx);
-  if (ctx->stats.batches < 2) return c.calls > 0 && c.abandoned == 0;  // after one batch: only if nothing at all
-  return c.calls > 0 && c.abandoned * 20 < c.calls;
+  const unsigned long long calls = c.calls - c.tail_calls;  // (tensor-core tails never abandon: no evidence either way)
+  if (ctx->stats.batches < 2) return calls > 0 && c.abandoned == 0;  // after one batch: only if nothing at all
+  return calls > 0 && c.abandoned * 20 < calls;
 }
 
 // One exact arg-max pass over this rank's share of the rarity order.
@@ -947,7 +1061,7 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
         // where it finds nothing (noise), the rest of the search runs the kernel without it.
         // (After ONE batch only on the plainest evidence: not a single pair ruled out.  Anything
         // less than that waits for the second batch — cfg 4 looks harmless after its first.)
-        if (pruning && ctx->opt_lower_bound && !ctx->lb_decided && ctx->stats.batches >= 1) {
+        if (pruning && ctx->opt_lower_bound && !ctx->lb_decided && ctx->stats.batches >= 1 && ctx->lb_launches > 0) {
           DeviceCounters c{};
           CUDA_OK(cudaMemcpyAsync(&c, ctx->counters.ptr, sizeof(c), cudaMemcpyDeviceToHost, st));
           sync_stream(ctx);
@@ -967,7 +1081,11 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
           sync_stream(ctx);
           const uint64_t best_now = ctx->h_keys[3];
           if (alone && ctx->dot_wanted && ctx->dot_eligible(best_now)) ctx->dot_used = true;
-          ctx->dot_now = ctx->dot_used && ctx->dot_eligible(best_now);
+          ctx->dot_now = ctx->dot_wanted && ctx->dot_used && ctx->dot_eligible(best_now);
+          // (the same on every rank: the option, and the best-so-far after the exchange)
+          ctx->tail_now = pruning && ctx->opt_tc_tail && ctx->opt_tensor_cores && !ctx->dot_now && ctx->opt_tensor_map &&
+                          key_bits(best_now) != 0 && ctx->dot_eligible(best_now);
+          if (ctx->tail_now) ctx->dot_used = true;  // the band stays widened from here on
           if (ctx->dot_now && !ctx->norms_ready) {
             ctx->row_norms.alloc(static_cast<size_t>(ctx->rows) + 1);
             ctx->stats.kernel_launches += launch_row_norms(ctx->matrix.ptr, ctx->rows + 1, ctx->stride, ctx->row_norms.ptr, st);
@@ -987,30 +1105,7 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
               ctx->sorted_ready = true;
             }
           }
-          if (ctx->dot_now && ctx->opt_tensor_cores && !ctx->split_ready) {
-            // the tensor-core form: fp16 (or tf32) hi / lo parts of the matrix and of its hash-sorted copy
-            const size_t floats = static_cast<size_t>(ctx->rows_padded) * ctx->stride;
-            const size_t words = ctx->opt_tc_half ? (floats + 1) / 2 : floats;  // (the arrays are float-typed; fp16 parts take half)
-            size_t free_b = 0, total_b = 0;
-            const bool have = ctx->matrix_hi.count >= words && (!ctx->sorted_ready || ctx->sorted_hi.count >= words);
-            if (!have) CUDA_OK(cudaMemGetInfo(&free_b, &total_b));  // (slow: only when the copies have to grow)
-            const size_t need = words * sizeof(float) * (ctx->sorted_ready ? 4 : 2);
-            if (have || free_b > need + (size_t{2} << 30)) {
-              ctx->matrix_hi.alloc(words);
-              ctx->matrix_lo.alloc(words);
-              ctx->stats.kernel_launches += launch_split_rows(ctx->matrix.ptr, floats, ctx->opt_tc_half, ctx->matrix_hi.ptr, ctx->matrix_lo.ptr, st);
-              if (ctx->sorted_ready) {
-                ctx->sorted_hi.alloc(words);
-                ctx->sorted_lo.alloc(words);
-                ctx->stats.kernel_launches +=
-                    launch_split_rows(ctx->matrix_sorted.ptr, floats, ctx->opt_tc_half, ctx->sorted_hi.ptr, ctx->sorted_lo.ptr, st);
-                ctx->sorted_split_ready = true;
-              }
-              ctx->split_ready = true;
-              ctx->batch_capacity = 0;  // (the batch buffers grow their split twins at the next ensure_batch_capacity)
-              ensure_batch_capacity(ctx, batch_now);
-            }
-          }
+          if (ctx->dot_now && ctx->opt_tensor_cores && !ctx->split_ready) build_split_copies(ctx, batch_now);
           s = ctx->state();
         }
         ctx->stats.scanned_candidates += count;
@@ -1092,6 +1187,8 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   ctx->lb_decided = false;
   ctx->dot_wanted = ctx->dot_used = ctx->opt_dot == 2;
   ctx->dot_now = false;
+  ctx->tail_now = false;
+  ctx->lb_launches = 0;
   s = ctx->state();
   ctx->stats.scan_kernel_dot_launches = 0;
   ctx->stats.scan_kernel_tc_launches = 0;
@@ -1315,6 +1412,7 @@ int tsdd_cuda_create(tsdd_cuda_ctx** out, int device) {
     ctx = new tsdd_cuda_ctx();
     ctx->device = device;
     CUDA_OK(cudaSetDevice(device));
+    CUDA_OK(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device));
     CUDA_OK(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
     ctx->stream = ctx->own_stream;
     for (auto& e : ctx->ev_prep) CUDA_OK(cudaEventCreate(&e));
@@ -1431,6 +1529,10 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
       ctx->opt_wide_tile = value != 0;
     } else if (key == "lower_bound") {
       ctx->opt_lower_bound = value != 0;
+    } else if (key == "tc_tail") {
+      if (value < 0 || value > 1048576) fail(TSDD_ERR_PARAMETER, "tc_tail must be in 0..1048576");
+      ctx->opt_tc_tail = value != 0;
+      if (value > 1) ctx->opt_tc_tail_most = static_cast<uint32_t>(value);
     } else if (key == "encode_tol_scale") {
       if (value < 0) fail(TSDD_ERR_PARAMETER, "encode_tol_scale must be >= 0");
       ctx->opt_encode_tol_scale = value;

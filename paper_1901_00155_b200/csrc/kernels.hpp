@@ -198,8 +198,12 @@ struct TcOperands {
   uint64_t rows_padded;                // rows of each of the four neighbour arrays
   bool half;                           // the parts are fp16 (kind::f16, 22 bits between them) instead of tf32 (kind::tf32, 21 bits)
   uint32_t* work;                      // one word of device memory: the launch's work-item counter
+  bool tail;                           // a covering scan of a search that is not in the dot form (counters only)
 };
 int launch_split_rows(const float* d_in, size_t floats, bool half, float* d_hi, float* d_lo, cudaStream_t stream);
+// ... row by row, with the rows' squared norms (the first n_norms of them) as a by-product
+int launch_split_rows_norms(const float* d_in, uint32_t n_rows, uint32_t stride, bool half, float* d_hi, float* d_lo,
+                            float* d_norms, uint32_t n_norms, cudaStream_t stream);
 int launch_gather_rows_split(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel, uint32_t capacity_padded,
                              bool half, float* d_hi, float* d_lo, cudaStream_t stream);
 int launch_scan_tiles_tc(SearchState s, const TcOperands& op, const uint32_t* d_batch_rows, const uint32_t* d_batch_slots,

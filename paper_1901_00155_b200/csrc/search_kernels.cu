@@ -49,7 +49,7 @@ __global__ void k_reset_search(SearchState s) {
   }
   if (i == 0) {
     *s.best = 0;
-    *s.counters = DeviceCounters{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    *s.counters = DeviceCounters{0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   }
 }
 

@@ -209,6 +209,7 @@ struct TcArgs {
   int pruning;
   uint32_t* work;             // the launch's work-item counter (zero at launch)
   float lim_factor;
+  int tail;                   // a covering scan of a search that is not in the dot form (counters: tail_calls, no tile_live)
 };
 
 template <bool kSymmetric, bool kHalf>
@@ -267,7 +268,7 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
     const uint32_t span = a.u_end - a.u_begin;
     const uint32_t items_per_cand = (span + a.tiles_per_item - 1) / a.tiles_per_item;
     const uint32_t total_items = cand_tiles * items_per_cand;
-    unsigned long long calls_total = 0, tiles_total = 0, live_total = 0;
+    unsigned long long calls_total = 0, tiles_total = 0, live_total = 0, skipped_total = 0;
     [[maybe_unused]] long long w_a = 0;
     [[maybe_unused]] const long long t_start = clock64();
     auto slot0_of = [&](uint32_t u, uint32_t centre) -> uint32_t {
@@ -311,6 +312,21 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
         if (crow[q] != 0xFFFFFFFFu) TSDD_BOUND(crow[q], s.n_rows);
         cnorm[q] = crow[q] != 0xFFFFFFFFu ? __ldg(s.row_norms + crow[q]) : 0.f;
       }
+      // the lower-bound filter of the covering scans (search_kernels.cu: k_scan_tiles<.., kLb>) for a tail: the
+      // candidates' 16 segment means, kept for the whole item
+      const bool filter = a.tail && a.pruning && !window && s.lb_means != nullptr;
+      float means[kM / 32][kLbSegments];
+      if (filter) {
+#pragma unroll
+        for (int q = 0; q < kM / 32; ++q) {
+          const float4* pm = reinterpret_cast<const float4*>(s.lb_means + static_cast<size_t>(crow[q] != 0xFFFFFFFFu ? crow[q] : 0u) * kLbSegments);
+#pragma unroll
+          for (int v = 0; v < kLbSegments / 4; ++v) {
+            const float4 m4 = __ldg(pm + v);
+            means[q][4 * v] = m4.x, means[q][4 * v + 1] = m4.y, means[q][4 * v + 2] = m4.z, means[q][4 * v + 3] = m4.w;
+          }
+        }
+      }
       uint32_t j_next[kN / 32];
       rows_of(slot0_of(u0, centre), j_next);
       for (uint32_t t = 0; t < n_tiles; ++t) {
@@ -333,9 +349,27 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
         if (t + 1 < n_tiles) rows_of(slot0_of(u0 + t + 1, centre), j_next);
         if (use >= 1 && !slot_held) { TC_T0(); bar_wait(&sh.meta_empty[m], (use - 1) & 1, 1); TC_ACC(w_a); }
         slot_held = true;
-        bool any_live = false;
+        bool any_live = false, any_needed = false;
         unsigned long long calls = 0;
-        uint32_t live = 0;
+        uint32_t live = 0, skipped = 0;
+        float4 tile_lo[kLbSegments / 4], tile_hi[kLbSegments / 4];
+        if (filter && valid > 0) {  // the box of the tile's boxes: lane l reduces component l (16 minima, 16 maxima)
+          const uint32_t first_unit = slot0 / kLbBoxRows, last_unit = (slot0 + valid - 1) / kLbBoxRows;
+          float comp = lane < kLbSegments ? 3.0e38f : -3.0e38f;
+          for (uint32_t unit = first_unit; unit <= last_unit; ++unit) {
+            const float v = __ldg(s.lb_boxes + static_cast<size_t>(unit) * 2 * kLbSegments + lane);
+            comp = lane < kLbSegments ? fminf(comp, v) : fmaxf(comp, v);
+          }
+          float box[2 * kLbSegments];
+#pragma unroll
+          for (int c = 0; c < 2 * kLbSegments; ++c) box[c] = __shfl_sync(0xFFFFFFFFu, comp, c);
+#pragma unroll
+          for (int v = 0; v < kLbSegments / 4; ++v) {
+            tile_lo[v] = make_float4(box[4 * v], box[4 * v + 1], box[4 * v + 2], box[4 * v + 3]);
+            tile_hi[v] = make_float4(box[kLbSegments + 4 * v], box[kLbSegments + 4 * v + 1], box[kLbSegments + 4 * v + 2],
+                                     box[kLbSegments + 4 * v + 3]);
+          }
+        }
 #pragma unroll
         for (int q = 0; q < kM / 32; ++q) {
           const uint32_t r = lane + 32 * q, row = crow[q];
@@ -348,11 +382,48 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
               if (!dead_bound(bound, best, s.margin, s.margin_abs, s.margin_q)) thr = bound;
             }
           }
+          if (thr >= 0.f) any_live = true;
+          if (filter && thr >= 0.f && valid > 0) {
+            // a candidate whose segment means lie further from every 16-row box of the tile than its threshold
+            // cannot find a neighbour below it here: it sits the tile out.  First against the box of the whole
+            // tile (a weaker bound, one test instead of sixteen), which settles most of them.
+            float lb_tile = 0.f;
+#pragma unroll
+            for (int v = 0; v < kLbSegments / 4; ++v) {
+              const float4 lo = tile_lo[v], hi = tile_hi[v];
+              float g;
+              g = fmaxf(fmaxf(lo.x - means[q][4 * v], means[q][4 * v] - hi.x), 0.f), lb_tile = fmaf(g, g, lb_tile);
+              g = fmaxf(fmaxf(lo.y - means[q][4 * v + 1], means[q][4 * v + 1] - hi.y), 0.f), lb_tile = fmaf(g, g, lb_tile);
+              g = fmaxf(fmaxf(lo.z - means[q][4 * v + 2], means[q][4 * v + 2] - hi.z), 0.f), lb_tile = fmaf(g, g, lb_tile);
+              g = fmaxf(fmaxf(lo.w - means[q][4 * v + 3], means[q][4 * v + 3] - hi.w), 0.f), lb_tile = fmaf(g, g, lb_tile);
+            }
+            bool needed = false;
+            const bool settled = lb_rules_out(lb_tile * s.lb_scale, thr, s.lb_q);
+            const uint32_t first_unit = slot0 / kLbBoxRows, last_unit = (slot0 + valid - 1) / kLbBoxRows;
+            for (uint32_t unit = first_unit; unit <= last_unit && !needed && !settled; ++unit) {
+              const float4* pb = reinterpret_cast<const float4*>(s.lb_boxes + static_cast<size_t>(unit) * 2 * kLbSegments);
+              float lb = 0.f;
+#pragma unroll
+              for (int v = 0; v < kLbSegments / 4; ++v) {
+                const float4 lo = __ldg(pb + v), hi = __ldg(pb + kLbSegments / 4 + v);
+                float g;
+                g = fmaxf(fmaxf(lo.x - means[q][4 * v], means[q][4 * v] - hi.x), 0.f), lb = fmaf(g, g, lb);
+                g = fmaxf(fmaxf(lo.y - means[q][4 * v + 1], means[q][4 * v + 1] - hi.y), 0.f), lb = fmaf(g, g, lb);
+                g = fmaxf(fmaxf(lo.z - means[q][4 * v + 2], means[q][4 * v + 2] - hi.z), 0.f), lb = fmaf(g, g, lb);
+                g = fmaxf(fmaxf(lo.w - means[q][4 * v + 3], means[q][4 * v + 3] - hi.w), 0.f), lb = fmaf(g, g, lb);
+              }
+              needed = !lb_rules_out(lb * s.lb_scale, thr, s.lb_q);
+            }
+            if (!needed) {
+              thr = -1.f;
+              skipped += 1;
+            }
+          }
           meta.thr[r] = thr;
           meta.cand[r] = row;
           meta.cnorm[r] = cnorm[q];
           if (thr >= 0.f) {
-            any_live = true;
+            any_needed = true;
             live += 1;
             uint32_t overlap = 0;
             if (!window) {  // (window tiles: the epilogue counts the self-match pairs)
@@ -365,6 +436,8 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
         }
         any_live = __any_sync(0xFFFFFFFFu, any_live);
         if (!any_live) break;  // every candidate of the tile is dead: the rest of the item is not needed (the slot stays held)
+        skipped_total += skipped;
+        if (!__any_sync(0xFFFFFFFFu, any_needed)) continue;  // the filter: nobody needs this tile (the slot stays held)
         if (window) {
 #pragma unroll
           for (int q = 0; q < kBinWords / 32; ++q) meta.bins[lane + 32 * q] = 0u;
@@ -419,11 +492,15 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
 #endif
     if (lane == 0) {
       if (calls_total) atomicAdd(&s.counters->calls, calls_total);
+      if (calls_total && a.tail) atomicAdd(&s.counters->tail_calls, calls_total);
       if (tiles_total) atomicAdd(&s.counters->tiles, tiles_total);
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) live_total += __shfl_xor_sync(0xFFFFFFFFu, live_total, d);
-    if (lane == 0 && live_total) atomicAdd(&s.counters->tile_live, live_total);
+    if (lane == 0 && live_total && !a.tail) atomicAdd(&s.counters->tile_live, live_total);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) skipped_total += __shfl_xor_sync(0xFFFFFFFFu, skipped_total, d);
+    if (lane == 0 && skipped_total) atomicAdd(&s.counters->lb_skipped, skipped_total);
   } else if (warp == 0) {
     // ================================================================ producer: the TMA streams
     uint32_t seq = 0;
@@ -716,6 +793,37 @@ k_split_f16(const float4* __restrict__ in, size_t quads, uint2* __restrict__ hi,
   lo[i] = l;
 }
 
+// The same split, one warp per row, with the row's squared norm as a by-product (the same sum k_row_norms
+// forms): a search that moves its covering scans to the tensor cores mid-way reads the matrix once, not twice.
+template <bool kHalf>
+__global__ void __launch_bounds__(256)
+k_split_rows_norms(const float* __restrict__ in, uint32_t n_rows, uint32_t stride, float* __restrict__ hi, float* __restrict__ lo,
+                   float* __restrict__ norms, uint32_t n_norms) {
+  const uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= n_rows) return;
+  const float4* p = reinterpret_cast<const float4*>(in + static_cast<size_t>(row) * stride);
+  auto top = [](float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); };
+  float acc = 0.f;
+  for (uint32_t c = lane; c < stride / 4; c += 32) {
+    const float4 x = p[c];
+    acc += (x.x * x.x + x.y * x.y) + (x.z * x.z + x.w * x.w);
+    if constexpr (kHalf) {
+      uint2 h, l;
+      split_half(x, h, l);
+      reinterpret_cast<uint2*>(hi)[static_cast<size_t>(row) * (stride / 4) + c] = h;
+      reinterpret_cast<uint2*>(lo)[static_cast<size_t>(row) * (stride / 4) + c] = l;
+    } else {
+      const float4 h = make_float4(top(x.x), top(x.y), top(x.z), top(x.w));
+      reinterpret_cast<float4*>(hi)[static_cast<size_t>(row) * (stride / 4) + c] = h;
+      reinterpret_cast<float4*>(lo)[static_cast<size_t>(row) * (stride / 4) + c] =
+          make_float4(top(x.x - h.x), top(x.y - h.y), top(x.z - h.z), top(x.w - h.w));
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, d);
+  if (lane == 0 && row < n_norms) norms[row] = acc;
+}
+
 // The batch's rows, split the same way, dense in batch order; rows past the batch size are zero.
 template <bool kHalf>
 __global__ void __launch_bounds__(256)
@@ -770,6 +878,14 @@ int launch_split_rows(const float* d_in, size_t floats, bool half, float* d_hi, 
   return 1;
 }
 
+int launch_split_rows_norms(const float* d_in, uint32_t n_rows, uint32_t stride, bool half, float* d_hi, float* d_lo,
+                            float* d_norms, uint32_t n_norms, cudaStream_t stream) {
+  const unsigned blocks = blocks_of(static_cast<size_t>(n_rows) * 32, 256);
+  if (half) k_split_rows_norms<true><<<blocks, 256, 0, stream>>>(d_in, n_rows, stride, d_hi, d_lo, d_norms, n_norms);
+  else k_split_rows_norms<false><<<blocks, 256, 0, stream>>>(d_in, n_rows, stride, d_hi, d_lo, d_norms, n_norms);
+  return 1;
+}
+
 int launch_gather_rows_split(SearchState s, const uint32_t* d_batch_rows, const uint32_t* d_sel, uint32_t capacity_padded,
                              bool half, float* d_hi, float* d_lo, cudaStream_t stream) {
   const unsigned blocks = blocks_of(static_cast<size_t>(capacity_padded) * 32, 256);
@@ -814,7 +930,9 @@ int launch_scan_tiles_tc(SearchState s, const TcOperands& op, const uint32_t* d_
     return 0;
   }
   cudaMemsetAsync(op.work, 0, sizeof(uint32_t), stream);
-  TcArgs a{d_batch_rows, d_batch_slots, d_sel, d_nbr_index, u_begin, u_end, tiles_per_item, pruning ? 1 : 0, op.work, lim_factor};
+  TcArgs a{d_batch_rows, d_batch_slots, d_sel, d_nbr_index, u_begin, u_end, tiles_per_item, pruning ? 1 : 0, op.work,
+           op.tail ? 1e30f : lim_factor,  // (a tail's neighbours take every symmetric update: the rows it meets are still to be scanned)
+           op.tail ? 1 : 0};
   dim3 grid(static_cast<unsigned>(items < static_cast<uint64_t>(sms) ? items : sms));
   const int smem = static_cast<int>(sizeof(SharedTc)) + 1024;
   auto launch = [&](auto kernel) {
