@@ -323,7 +323,7 @@ def run_cuda_arm(args) -> None:
         rp = line["roofline_prep"]
         rp["frac"] = rp["achieved"] / rp["peak"] if rp["achieved"] else None
         fp32 = fp32_roofline(totals, elapsed_ms, props.multi_processor_count, sm_max_mhz, ffma_ops, mix_ops)
-        if totals["tc_terms"] > 0.5 * totals["scan_terms"]:
+        if totals["tc_ms"] > 0.5 * totals["scan_ms"]:  # (by TIME inside the tile kernels)
             # the dominant kernel is the tensor-core tile kernel: the tensor roofline is the line's roofline,
             # the CUDA-core tile kernels' FP32 line (the same workload with dot_form = 1) follows below
             line["roofline"] = tensor_roofline(totals, elapsed_ms, traffic, prof)

@@ -114,10 +114,14 @@ int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream);
  * further away than its threshold), "dot_form" (the warp-specialised kernel
  * computes d^2 as |a|^2 + |b|^2 - 2 a.b, one FFMA per term, with the discard band widened by
  * its absolute error bound: 0 never; 1 once a search has found that tiles are not abandoned
- * early anyway and the best-so-far dwarfs the bound; 2 from the first launch; 3 / 4: as 1 / 2, with
- * the dot-form tiles of batches that fill 128 candidates on the TENSOR CORES — tcgen05.mma
- * kind::tf32 on rows split into two tf32 parts, three MMAs per 8 columns, accumulators in tensor
- * memory; an experiment, the CUDA-core kernels stay the default),
+ * early anyway and the best-so-far dwarfs the bound; 2 from the first launch; 3 / 4 and 5 / 6: as 1 / 2,
+ * with the dot-form tiles of batches that fill 128 candidates on the TENSOR CORES — tcgen05.mma on
+ * rows split into two tf32 parts (3 / 4, kind::tf32) or two fp16 parts (5 / 6, kind::f16), three MMAs
+ * per k-step, accumulators in tensor memory; 5 is the default),
+ * "tc_tail" (0/1, or the greatest number of candidates: the later ranges of a covering scan of a search that
+ * is NOT in the dot form move to the tensor cores — with the lower-bound filter — once the measured
+ * CUDA-core time per tile says that is cheaper; default 1, at most 1,024 candidates),
+ * "encode_tol_scale" (x the window encoder's distance-to-breakpoint tolerance; 0: its exact path only),
  * "tensor_map" (0/1: the warp-specialised kernel loads the tiles of covering scans — and, in
  * the dot-product form, of window rounds, from a copy of the matrix kept in the hash-sorted
  * order — as cp.async.bulk.tensor boxes instead of one bulk copy per row),

@@ -181,24 +181,24 @@ k_install_seed(SearchState s, const uint32_t* __restrict__ seed_lb, uint32_t see
   }
 }
 
-// The `keep` seed rows with the greatest values (ties: the earlier entry) — one block; every thread ranks its entries
-// against all the others in shared memory.
+// The `keep` seed rows with the greatest values (ties: the earlier entry): every block stages all the values in
+// shared memory and each of its threads ranks ONE entry against them (one block for all of it took 0.47 ms).
 constexpr int kSeedSelectMax = 8192;
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(256)
 k_seed_select(const uint32_t* __restrict__ order, const uint32_t* __restrict__ upper, uint32_t seed_rows, uint32_t keep,
               uint32_t* __restrict__ kept_rows) {
   __shared__ uint32_t s_val[kSeedSelectMax];
   for (uint32_t e = threadIdx.x; e < seed_rows; e += blockDim.x) s_val[e] = upper[e];
   __syncthreads();
-  for (uint32_t e = threadIdx.x; e < seed_rows; e += blockDim.x) {
-    const uint32_t mine = s_val[e];
-    uint32_t rank = 0;
-    for (uint32_t o = 0; o < seed_rows; ++o) {
-      const uint32_t other = s_val[o];
-      rank += (other > mine || (other == mine && o < e)) ? 1u : 0u;
-    }
-    if (rank < keep) kept_rows[rank] = order[e];
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= seed_rows) return;
+  const uint32_t mine = s_val[e];
+  uint32_t rank = 0;
+  for (uint32_t o = 0; o < seed_rows; ++o) {
+    const uint32_t other = s_val[o];
+    rank += (other > mine || (other == mine && o < e)) ? 1u : 0u;
   }
+  if (rank < keep) kept_rows[rank] = order[e];
 }
 
 // ------------------------------------------------------------------ same-word neighbours
@@ -2982,7 +2982,7 @@ int launch_seed_lower_bound(SearchState s, const uint32_t* d_order, uint32_t see
     const uint32_t coarse_units = (units + kCoarse - 1) / kCoarse;
     k_seed_lower_bound<<<dim3((coarse_units + kSeedUnits - 1) / kSeedUnits, (seed_rows + 255) / 256), 256, 0, stream>>>(
         s, d_order, seed_rows, d_seed_lb, kCoarse);
-    k_seed_select<<<1, 1024, 0, stream>>>(d_order, d_seed_lb, seed_rows, keep, d_rows);
+    k_seed_select<<<(seed_rows + 255) / 256, 256, 0, stream>>>(d_order, d_seed_lb, seed_rows, keep, d_rows);
     k_seed_lower_bound<<<dim3((units + kSeedUnits - 1) / kSeedUnits, (keep + 255) / 256), 256, 0, stream>>>(s, d_rows, keep, d_exact, 1);
     k_install_seed<<<1, 256, 0, stream>>>(s, d_exact, keep);
     return 4;

@@ -114,7 +114,7 @@ def metrics(src, dst, workload):
         a["dram_read"] += rec.get("dram__bytes_read.sum", 0.0)
         a["dram_write"] += rec.get("dram__bytes_write.sum", 0.0)
         for k, v in rec.items():
-            if k.endswith("pct_of_peak_sustained_active") or k.endswith("pct_of_peak_sustained_elapsed") or k.endswith(".ratio"):
+            if k.endswith("pct_of_peak_sustained_active") or k.endswith("pct_of_peak_sustained_elapsed") or k.endswith(".ratio") or k.endswith("hit_rate.pct"):
                 a["weighted"][k] += v * ms
         if a["longest"] is None or ms > a["longest"]["ms"]:
             a["longest"] = {"ms": ms, "grid": rec["grid"], "dram_bytes": rec.get("dram__bytes_read.sum", 0.0) + rec.get("dram__bytes_write.sum", 0.0),
@@ -124,7 +124,7 @@ def metrics(src, dst, workload):
     out = {"source": src, "workload": workload, "note": "ncu --metrics pass, cold-cache and serialised: compare shares, not absolutes",
            "total_ms": total, "kernels": {}}
     lines = [f"# {src}: per-kernel ncu metrics of one {workload} search (time-weighted averages; cold-cache, serialised)",
-             f"{'kernel':44} {'n':>4} {'ms':>8} {'share':>6} {'DRAM GB':>8} {'GB/s':>7} {'dram%':>6} {'fma%':>6} {'fp64%':>6} {'issue%':>6} {'occ%':>5}  top stall (per issue)"]
+             f"{'kernel':44} {'n':>4} {'ms':>8} {'share':>6} {'DRAM GB':>8} {'GB/s':>7} {'dram%':>6} {'fma%':>6} {'fp64%':>6} {'tensor%':>7} {'issue%':>6} {'occ%':>5}  top stall (per issue)"]
     for name, a in sorted(agg.items(), key=lambda kv: -kv[1]["ms"]):
         w = {k: v / a["ms"] for k, v in a["weighted"].items()} if a["ms"] else {}
         stalls = {k.split("issue_stalled_")[1].replace("_per_issue_active.ratio", ""): v for k, v in w.items() if "issue_stalled" in k}
@@ -135,6 +135,8 @@ def metrics(src, dst, workload):
              "dram_pct_of_peak": w.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
              "fma_pipe_pct": w.get("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
              "fp64_pipe_pct": w.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+             "tensor_pipe_pct": w.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
+             "l2_hit_rate_pct": w.get("lts__t_sector_hit_rate.pct"),
              "issue_active_pct": w.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
              "warps_active_pct": w.get("sm__warps_active.avg.pct_of_peak_sustained_active"),
              "l1_throughput_pct": w.get("l1tex__throughput.avg.pct_of_peak_sustained_active"),
@@ -143,7 +145,7 @@ def metrics(src, dst, workload):
         out["kernels"][name] = k
         f = lambda v: f"{v:6.1f}" if v is not None else "     -"
         lines.append(f"{name[:44]:44} {a['launches']:4d} {a['ms']:8.3f} {100 * k['share']:5.1f}% {gb:8.3f} {k['dram_gb_per_s']:7.0f} "
-                     f"{f(k['dram_pct_of_peak'])} {f(k['fma_pipe_pct'])} {f(k['fp64_pipe_pct'])} {f(k['issue_active_pct'])} "
+                     f"{f(k['dram_pct_of_peak'])} {f(k['fma_pipe_pct'])} {f(k['fp64_pipe_pct'])} {f(k['tensor_pipe_pct'])}  {f(k['issue_active_pct'])} "
                      f"{(k['warps_active_pct'] or 0):5.1f}  {top[0]} {top[1]:.2f}")
     json.dump(out, open(dst + ".json", "w"), indent=1)
     open(dst + ".txt", "w").write("\n".join(lines) + "\n")
