@@ -73,6 +73,7 @@ typedef struct tsdd_cuda_stats {
   uint64_t scan_kernel_tc_launches; /* of scan_kernel_dot_launches, those of the tensor-core tile kernel (dot_form 3 .. 6) */
   uint64_t scan_kernel_tc_terms;    /* of scan_kernel_dot_terms, those computed there (three MMA multiply-adds per term) */
   double scan_kernel_tc_ms;         /* of scan_kernel_ms, the device time inside the tensor-core tile kernel */
+  uint64_t tail_restarts;           /* searches started over because the first batch's tensor-core tails were not warranted */
 } tsdd_cuda_stats;
 
 /* ---- lifetime ------------------------------------------------------------ */
@@ -121,6 +122,8 @@ int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream);
  * "tc_tail" (0/1, or the greatest number of candidates: the later ranges of a covering scan of a search that
  * is NOT in the dot form move to the tensor cores — with the lower-bound filter — once the measured
  * CUDA-core time per tile says that is cheaper; default 1, at most 1,024 candidates),
+ * "tc_tail_first" (0/1: the first batch of a search may do so on trust, before there is a best-so-far to size the
+ * band against; should its result not dwarf the band, the search starts over without the tails),
  * "encode_tol_scale" (x the window encoder's distance-to-breakpoint tolerance; 0: its exact path only),
  * "tensor_map" (0/1: the warp-specialised kernel loads the tiles of covering scans — and, in
  * the dot-product form, of window rounds, from a copy of the matrix kept in the hash-sorted

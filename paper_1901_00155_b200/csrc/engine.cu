@@ -260,6 +260,13 @@ struct tsdd_cuda_ctx {
   // those that must meet every row — the rows around a discord: dense work); the band is widened like for dot_used
   bool tail_now = false;
   int sm_count = 148;
+  // The FIRST batch of a search has no best-so-far to size the band against, yet its candidates are the ones that scan
+  // every row: it may use the tails on trust (tail_unproven).  The best-so-far it ends with settles it: if that does
+  // not dwarf the band after all and tensor-core bounds are out (tail_used), the search starts over without
+  // (restart_wanted -> tail_blocked); if none are, the band is simply taken back.
+  bool tail_unproven = false, tail_used = false, tail_blocked = false, restart_wanted = false;
+  bool opt_tc_tail_first = true;
+  bool opt_tc_tail_force = false;
   uint64_t lb_launches = 0;  // launches of the kernel with the lower-bound filter in this search (evidence for lb_decided)
   bool opt_tc_tail = true;
   uint32_t opt_tc_tail_most = 1024;  // ... while at most so many candidates are left
@@ -780,22 +787,26 @@ void build_split_copies(tsdd_cuda_ctx* ctx, uint32_t batch_now) {
   cudaStream_t st = ctx->stream;
   const size_t floats = static_cast<size_t>(ctx->rows_padded) * ctx->stride;
   const size_t words = ctx->opt_tc_half ? (floats + 1) / 2 : floats;  // (the arrays are float-typed; fp16 parts take half)
+  const bool want_main = !ctx->split_ready, want_sorted = ctx->sorted_ready && !ctx->sorted_split_ready;
+  if (!want_main && !want_sorted) return;
   size_t free_b = 0, total_b = 0;
-  const bool have = ctx->matrix_hi.count >= words && (!ctx->sorted_ready || ctx->sorted_hi.count >= words);
+  const bool have = (!want_main || ctx->matrix_hi.count >= words) && (!want_sorted || ctx->sorted_hi.count >= words);
   if (!have) CUDA_OK(cudaMemGetInfo(&free_b, &total_b));  // (slow: only when the copies have to grow)
-  const size_t need = words * sizeof(float) * (ctx->sorted_ready ? 4 : 2);
+  const size_t need = words * sizeof(float) * ((want_main ? 2 : 0) + (want_sorted ? 2 : 0));
   if (!have && free_b <= need + (size_t{2} << 30)) return;
-  ctx->matrix_hi.alloc(words);
-  ctx->matrix_lo.alloc(words);
-  if (!ctx->norms_ready) {  // one pass over the matrix for both
-    ctx->row_norms.alloc(static_cast<size_t>(ctx->rows) + 1);
-    ctx->stats.kernel_launches += launch_split_rows_norms(ctx->matrix.ptr, ctx->rows_padded, ctx->stride, ctx->opt_tc_half,
-                                                          ctx->matrix_hi.ptr, ctx->matrix_lo.ptr, ctx->row_norms.ptr, ctx->rows + 1, st);
-    ctx->norms_ready = true;
-  } else {
-    ctx->stats.kernel_launches += launch_split_rows(ctx->matrix.ptr, floats, ctx->opt_tc_half, ctx->matrix_hi.ptr, ctx->matrix_lo.ptr, st);
+  if (want_main) {
+    ctx->matrix_hi.alloc(words);
+    ctx->matrix_lo.alloc(words);
+    if (!ctx->norms_ready) {  // one pass over the matrix for both
+      ctx->row_norms.alloc(static_cast<size_t>(ctx->rows) + 1);
+      ctx->stats.kernel_launches += launch_split_rows_norms(ctx->matrix.ptr, ctx->rows_padded, ctx->stride, ctx->opt_tc_half,
+                                                            ctx->matrix_hi.ptr, ctx->matrix_lo.ptr, ctx->row_norms.ptr, ctx->rows + 1, st);
+      ctx->norms_ready = true;
+    } else {
+      ctx->stats.kernel_launches += launch_split_rows(ctx->matrix.ptr, floats, ctx->opt_tc_half, ctx->matrix_hi.ptr, ctx->matrix_lo.ptr, st);
+    }
   }
-  if (ctx->sorted_ready) {
+  if (want_sorted) {  // (the hash-sorted copy may come later than the matrix's own split: a tail came first)
     ctx->sorted_hi.alloc(words);
     ctx->sorted_lo.alloc(words);
     ctx->stats.kernel_launches +=
@@ -927,7 +938,7 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
       double cuda_ms_per_tile = -1.0;
       for (size_t q = seg_events.size(); q-- > 0;) {  // the latest covering segment whose events have completed
         const SegEvent& ev = seg_events[q];
-        if (ev.window || ev.tc || ev.tiles < 256 || ev.r + 2 > r) continue;  // (a small segment is mostly launch overhead)
+        if (ev.window || ev.tc || (ev.tiles < 256 && !ctx->opt_tc_tail_force) || ev.r + 2 > r) continue;  // (a small segment is mostly launch overhead)
         float ms = 0.f;
         if (cudaEventQuery(ev.e1) == cudaSuccess && cudaEventElapsedTime(&ms, ev.e0, ev.e1) == cudaSuccess)
           cuda_ms_per_tile = ms / ev.tiles;
@@ -949,7 +960,7 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
           std::fprintf(stderr, "tail? batch %llu segment %zu live<=%u: cuda %.3f ms for %llu tiles, tensor cores %.3f ms + split %.3f ms\n",
                        static_cast<unsigned long long>(ctx->stats.batches), r, count, cuda_ms,
                        static_cast<unsigned long long>(tiles_left), tc_ms, split_ms);
-        static const bool force = [] { const char* e = std::getenv("TSDD_TAIL_FORCE"); return e && e[0] == '1'; }();
+        const bool force = ctx->opt_tc_tail_force;  // (tests: switch at the first chance, whatever the estimate says)
         if (force || cuda_ms > (ctx->split_ready ? 1.5 : 2.5) * (tc_ms + split_ms)) {
           if (!ctx->split_ready) build_split_copies(ctx, count);
           if (ctx->split_ready && !ctx->norms_ready) {
@@ -958,6 +969,7 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
             ctx->norms_ready = true;
           }
           tail_on = ctx->split_ready;
+          if (tail_on) ctx->tail_used = true;
           s = ctx->state();
         }
       }
@@ -1036,6 +1048,20 @@ bool few_abandoned(tsdd_cuda_ctx* ctx) {
   return calls > 0 && c.abandoned * 20 < calls;
 }
 
+// The first batch used the tensor-core tails before there was a best-so-far to size the band against.  `proven`:
+// the best-so-far does dwarf the band now.  Returns false when the search has to start over without tails.
+bool settle_tail_trust(tsdd_cuda_ctx* ctx, bool proven) {
+  ctx->tail_unproven = false;
+  if (proven) return true;
+  if (!ctx->tail_used) {  // no tensor-core bound is out: take the band back and go on
+    ctx->dot_used = false;
+    ctx->tail_blocked = true;
+    return true;
+  }
+  ctx->restart_wanted = true;
+  return false;
+}
+
 // One exact arg-max pass over this rank's share of the rarity order.
 uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
   cudaStream_t st = ctx->stream;
@@ -1083,8 +1109,15 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
           if (alone && ctx->dot_wanted && ctx->dot_eligible(best_now)) ctx->dot_used = true;
           ctx->dot_now = ctx->dot_wanted && ctx->dot_used && ctx->dot_eligible(best_now);
           // (the same on every rank: the option, and the best-so-far after the exchange)
-          ctx->tail_now = pruning && ctx->opt_tc_tail && ctx->opt_tensor_cores && !ctx->dot_now && ctx->opt_tensor_map &&
-                          key_bits(best_now) != 0 && ctx->dot_eligible(best_now);
+          const bool proven = key_bits(best_now) != 0 && ctx->dot_eligible(best_now);  // (a seeded bound counts: the final best is no smaller)
+          if (ctx->tail_unproven && ctx->stats.batches >= 1) {  // the first batch ran its tails on trust: was it right to?
+            if (!settle_tail_trust(ctx, proven)) return 0;
+          }
+          const bool tails = pruning && ctx->opt_tc_tail && ctx->opt_tensor_cores && !ctx->dot_now && ctx->opt_tensor_map &&
+                             !ctx->tail_blocked;
+          const bool on_trust = tails && ctx->opt_tc_tail_first && pass == 0 && ctx->stats.batches == 0 && !ctx->dot_used;
+          ctx->tail_now = tails && ((key_bits(best_now) != 0 && ctx->dot_eligible(best_now)) || on_trust);
+          if (on_trust && !proven) ctx->tail_unproven = true;
           if (ctx->tail_now) ctx->dot_used = true;  // the band stays widened from here on
           if (ctx->dot_now && !ctx->norms_ready) {
             ctx->row_norms.alloc(static_cast<size_t>(ctx->rows) + 1);
@@ -1105,7 +1138,7 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
               ctx->sorted_ready = true;
             }
           }
-          if (ctx->dot_now && ctx->opt_tensor_cores && !ctx->split_ready) build_split_copies(ctx, batch_now);
+          if (ctx->dot_now && ctx->opt_tensor_cores) build_split_copies(ctx, batch_now);  // (whatever of them is missing)
           s = ctx->state();
         }
         ctx->stats.scanned_candidates += count;
@@ -1132,6 +1165,11 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
   }
   CUDA_OK(cudaMemcpyAsync(ctx->h_keys, ctx->best.ptr, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
   sync_stream(ctx);
+  if (ctx->tail_unproven) {  // (a pass of one batch)
+    const uint64_t best_now = ctx->h_keys[0];
+    const bool proven = key_bits(best_now) != 0 && ctx->dot_eligible(best_now);
+    if (!settle_tail_trust(ctx, proven)) return 0;
+  }
   return ctx->h_keys[0];
 }
 
@@ -1188,7 +1226,9 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   ctx->dot_wanted = ctx->dot_used = ctx->opt_dot == 2;
   ctx->dot_now = false;
   ctx->tail_now = false;
+  ctx->tail_unproven = ctx->tail_used = ctx->tail_blocked = ctx->restart_wanted = false;
   ctx->lb_launches = 0;
+  ctx->stats.tail_restarts = 0;
   s = ctx->state();
   ctx->stats.scan_kernel_dot_launches = 0;
   ctx->stats.scan_kernel_tc_launches = 0;
@@ -1201,24 +1241,29 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
   ctx->trace.clear();
 
   CUDA_OK(cudaEventRecord(ctx->ev_a, st));
-  ctx->stats.kernel_launches += launch_reset_search(s, st);
   bool seeded = false;
-  if (pruning && ctx->opt_lower_bound && ctx->opt_seed_rows > 0 && s.lb_means != nullptr) {
-    // (the seed costs seed_rows x N / 16 box tests: keep it at 1/64 of the rows on small inputs)
-    const uint32_t seed_rows = std::min(ctx->opt_seed_rows, std::max(256u, ctx->rows / 64));
-    ctx->seed_lb.alloc(2 * static_cast<size_t>(seed_rows));  // (the two-pass seed keeps its selection there)
-    ctx->stats.kernel_launches += launch_seed_lower_bound(s, ctx->order, seed_rows, ctx->seed_lb.ptr, st);
-    seeded = true;
-  }
-  if (pruning) {  // (after the seed: a row whose first mates already put it below the seed stops there)
-    // Ranks that share their bounds split this stage too (slot p, or 32-slot chunk p, belongs to rank p mod world)
-    // and merge the results with the same min-exchange that follows every batch.
-    const bool split = ctx->several() && ctx->opt_share_bounds && ctx->opt_mates > 0;
-    ctx->stats.kernel_launches += launch_bucket_mates(
-        s, ctx->series.ptr, ctx->series_is_f32 ? ctx->series_f32.ptr : nullptr, ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->sorted_row, ctx->slot_bucket.ptr, ctx->offsets.ptr,
-        ctx->opt_mates, ctx->run_pairs, split ? static_cast<uint32_t>(ctx->world) : 1u, split ? static_cast<uint32_t>(ctx->rank) : 0u, st);
-    if (split) exchange_bounds(ctx);
-  }
+  auto begin_search = [&] {  // (again when the first batch's trust in the tensor-core tails was misplaced)
+    s = ctx->state();
+    ctx->stats.kernel_launches += launch_reset_search(s, st);
+    if (pruning && ctx->opt_lower_bound && ctx->opt_seed_rows > 0 && s.lb_means != nullptr) {
+      // (the seed costs seed_rows x N / 16 box tests: keep it at 1/64 of the rows on small inputs)
+      const uint32_t seed_rows = std::min(ctx->opt_seed_rows, std::max(256u, ctx->rows / 64));
+      ctx->seed_lb.alloc(2 * static_cast<size_t>(seed_rows));  // (the two-pass seed keeps its selection there)
+      ctx->stats.kernel_launches += launch_seed_lower_bound(s, ctx->order, seed_rows, ctx->seed_lb.ptr, st);
+      seeded = true;
+    }
+    if (pruning) {  // (after the seed: a row whose first mates already put it below the seed stops there)
+      // Ranks that share their bounds split this stage too (slot p, or 32-slot chunk p, belongs to rank p mod world)
+      // and merge the results with the same min-exchange that follows every batch.
+      const bool split = ctx->several() && ctx->opt_share_bounds && ctx->opt_mates > 0;
+      ctx->stats.kernel_launches += launch_bucket_mates(
+          s, ctx->series.ptr, ctx->series_is_f32 ? ctx->series_f32.ptr : nullptr, ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->sorted_row, ctx->slot_bucket.ptr, ctx->offsets.ptr,
+          ctx->opt_mates, ctx->run_pairs, split ? static_cast<uint32_t>(ctx->world) : 1u, split ? static_cast<uint32_t>(ctx->rank) : 0u, st);
+      if (split) exchange_bounds(ctx);
+    }
+
+};
+  begin_search();
 
   for (int pass = 0; pass < k; ++pass) {
     ctx->cur_pass = pass;
@@ -1227,6 +1272,21 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
       ctx->stats.kernel_launches += launch_seed_best(ctx->state(), st);
     }
     uint64_t key = run_pass(ctx, pruning, pass);
+    if (ctx->restart_wanted) {  // the first batch's best-so-far does not dwarf the band of its tensor-core tails: start over without
+      ctx->restart_wanted = false;
+      ctx->tail_blocked = true;
+      ctx->tail_now = ctx->tail_used = ctx->tail_unproven = false;
+      ctx->dot_wanted = ctx->dot_used = ctx->opt_dot == 2;
+      ctx->dot_now = false;
+      ctx->lb_active = true;
+      ctx->lb_decided = false;
+      ctx->lb_launches = 0;
+      ctx->stats.batches = 0;
+      ctx->stats.tail_restarts += 1;
+      begin_search();
+      pass = -1;
+      continue;
+    }
     if (pass == 0 && seeded && key != 0 && best_key_row(key) == 0xFFFFFFFFu) {
       // no candidate rose above the seeded bound (it can only happen through float32 rounding at
       // an exact tie): drop the seed and let the pass finish on its own best-so-far
@@ -1529,6 +1589,10 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
       ctx->opt_wide_tile = value != 0;
     } else if (key == "lower_bound") {
       ctx->opt_lower_bound = value != 0;
+    } else if (key == "tc_tail_force") {
+      ctx->opt_tc_tail_force = value != 0;
+    } else if (key == "tc_tail_first") {
+      ctx->opt_tc_tail_first = value != 0;
     } else if (key == "tc_tail") {
       if (value < 0 || value > 1048576) fail(TSDD_ERR_PARAMETER, "tc_tail must be in 0..1048576");
       ctx->opt_tc_tail = value != 0;

@@ -68,7 +68,8 @@ class Stats(ctypes.Structure):
                 ("scan_kernel_dot_terms", ctypes.c_uint64), ("finalists", ctypes.c_uint64),
                 ("exact_reruns", ctypes.c_uint64), ("useful_terms", ctypes.c_uint64),
                 ("propagated", ctypes.c_uint64), ("scan_kernel_tc_launches", ctypes.c_uint64),
-                ("scan_kernel_tc_terms", ctypes.c_uint64), ("scan_kernel_tc_ms", ctypes.c_double)]
+                ("scan_kernel_tc_terms", ctypes.c_uint64), ("scan_kernel_tc_ms", ctypes.c_double),
+                ("tail_restarts", ctypes.c_uint64)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}

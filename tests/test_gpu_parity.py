@@ -797,6 +797,37 @@ def test_dot_product_form_on_256_candidate_tiles(ctx, chk, seed, kind, n):
     np.testing.assert_allclose(again[1], dist, rtol=1e-9)
 
 
+@pytest.mark.parametrize("kind", ["walk", "periodic", "low-noise"])
+def test_tails_of_covering_scans_on_the_tensor_cores(ctx, chk, kind):
+    """The later ranges of a covering scan move to the tensor cores (engine.cu: tail_now; forced here at the
+    first chance, with the lower-bound filter in the kernel's metadata warp), the first batch on trust.  On the
+    low-noise series the first batch's best-so-far does NOT dwarf the error band: the search has to notice,
+    start over without the tails, and still return the reference's answer."""
+    rng = np.random.default_rng(4242)
+    m, n, w, a, k = 40000, 64, 4, 4, 2
+    if kind == "walk":
+        x = planted_walk(31, m, n)
+    elif kind == "periodic":
+        x = (np.sin(2 * np.pi * np.arange(m) / 50.0) + 0.3 * rng.standard_normal(m)).astype(np.float32)
+        x[17000:17064] += np.float32(1.5)
+    else:
+        x = (np.sin(2 * np.pi * np.arange(m) / 50.0) + 1e-4 * rng.standard_normal(m)).astype(np.float32)
+    for name, value in [("tc_tail_force", 1), ("first_batch", 128)]:
+        ctx.set_option(name, value)
+    try:
+        ctx.prepare(x, n, w, a)
+        pos, dist = ctx.search(k)
+        st = ctx.stats()
+    finally:
+        ctx.set_option("tc_tail_force", 0)
+    want = chk.topk(x, n, w, a, k)
+    assert_discords_match(chk, x, n, pos, dist, want)
+    if kind == "low-noise":
+        assert st["tail_restarts"] == 1 or st["scan_kernel_tc_launches"] == 0
+    else:
+        assert st["scan_kernel_tc_launches"] > 0 and st["tail_restarts"] == 0
+
+
 @pytest.mark.parametrize("form", [4, 6], ids=["tf32", "fp16"])
 @pytest.mark.parametrize("seed,kind,n", FUZZ[::3], ids=[f"{k}-n{n}" for _, k, n in FUZZ[::3]])
 def test_dot_product_form_on_the_tensor_cores(ctx, chk, seed, kind, n, form):
