@@ -122,6 +122,8 @@ int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream);
  * "tc_tail" (0/1, or the greatest number of candidates: the later ranges of a covering scan of a search that
  * is NOT in the dot form move to the tensor cores — with the lower-bound filter — once the measured
  * CUDA-core time per tile says that is cheaper; default 1, at most 1,024 candidates),
+ * "tc_growth" / "tc_window_rounds" / "tc_window_growth" (the ranges and window rounds of a dot-form batch on the
+ * tensor cores: 2.0 / 5 / 2.5 — fewer, wider launches than on the CUDA cores),
  * "tc_tail_first" (0/1: the first batch of a search may do so on trust, before there is a best-so-far to size the
  * band against; should its result not dwarf the band, the search starts over without the tails),
  * "encode_tol_scale" (x the window encoder's distance-to-breakpoint tolerance; 0: its exact path only),

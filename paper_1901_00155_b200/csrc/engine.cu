@@ -178,9 +178,9 @@ struct tsdd_cuda_ctx {
   std::string error;
 
   // tunables (tsdd_cuda_set_option)
-  uint32_t opt_batch = 262144;
+  uint32_t opt_batch = 1048576;     // (capped by batch_limit(): the batch's dense copy of its rows stays under 2 GB)
   uint32_t opt_first_batch = 128;
-  uint32_t opt_batch_growth = 8;
+  uint32_t opt_batch_growth = 12;
   int opt_rounds = 64;            // upper limit on neighbour ranges per batch
   uint32_t opt_first_range = 8192;  // rows in the first range
   double opt_growth = 2.0;          // each range is this much larger than the one before (dot form: opt_dot_growth)
@@ -214,6 +214,9 @@ struct tsdd_cuda_ctx {
   double opt_dot_growth = 1.3;      // ... range growth of a dot-form batch: no abandoning inside tiles, so dead
                                     // candidates cost full price until the next compaction — compact more often
   double opt_dot_window_growth = 1.6;
+  // ... and of a dot-form batch on the tensor cores: ranges, window rounds and their growth
+  double opt_tc_growth = 2.0, opt_tc_window_growth = 2.5;
+  int opt_tc_window_rounds = 5;
   int opt_dot_window_rounds = 8;    // ... of a batch in the dot-product form whose window tiles load as tensor-map boxes                  // dot-product form of the ws kernel: 0 never, 1 when it pays, 2 always
 
   // prepared series
@@ -325,6 +328,11 @@ struct tsdd_cuda_ctx {
     // (x 3 on the tensor cores: the tf32 split drops products below 3 x 2^-20 |a||b| <= 2.9e-6 n, and
     // the float32 accumulation in tensor memory may truncate where the CUDA cores round)
     return (opt_tensor_cores ? 3.0 : 1.0) * (static_cast<double>(n) + 32.0) * static_cast<double>(n) * 5.9604644775390625e-08;
+  }
+  // candidates per batch: the option, with the dense copy of the batch's rows (and its two split twins) kept under 2 GB each
+  uint32_t batch_limit() const {
+    const uint64_t by_memory = std::max<uint64_t>(4096, (uint64_t{1} << 29) / std::max<uint32_t>(stride, 1u));
+    return static_cast<uint32_t>(std::min<uint64_t>(opt_batch, by_memory));
   }
   bool dot_eligible(uint64_t best_key_now) const {
     if (opt_dot == 2) return true;
@@ -844,8 +852,13 @@ std::vector<Segment> plan_segments(const tsdd_cuda_ctx* ctx, bool pruning) {
     // dies costs full price until the round ends (the widest round of a 3x schedule ran with a
     // quarter of its candidate slots dead).
     const bool dot_windows = ctx->dot_now && ctx->sorted_ready;
-    const int window_rounds = dot_windows ? std::max(ctx->opt_window_rounds, ctx->opt_dot_window_rounds) : ctx->opt_window_rounds;
-    const double window_growth = dot_windows ? std::min(ctx->opt_window_growth, ctx->opt_dot_window_growth) : ctx->opt_window_growth;
+    // (on the tensor cores a dead candidate's slot costs a fifth of what it does on the CUDA cores, and a launch with
+    // its compaction, gather and time-topology step as much as ever: fewer, wider rounds — cfg 5: 27.0 -> 24.7 ms)
+    const bool tc_windows = dot_windows && ctx->opt_tensor_cores && ctx->sorted_split_ready;
+    const int window_rounds = tc_windows ? ctx->opt_tc_window_rounds
+                              : dot_windows ? std::max(ctx->opt_window_rounds, ctx->opt_dot_window_rounds) : ctx->opt_window_rounds;
+    const double window_growth = tc_windows ? ctx->opt_tc_window_growth
+                                 : dot_windows ? std::min(ctx->opt_window_growth, ctx->opt_dot_window_growth) : ctx->opt_window_growth;
     for (int r = 0; r < window_rounds && at < window_limit; ++r) {
       const uint32_t upto = std::min<uint64_t>(window_limit, at + static_cast<uint64_t>(size) / tile);
       plan.push_back({true, at, upto});
@@ -855,7 +868,8 @@ std::vector<Segment> plan_segments(const tsdd_cuda_ctx* ctx, bool pruning) {
   }
   const std::vector<uint32_t> bounds =
       range_bounds(ctx->rows, ctx->opt_rounds, ctx->opt_first_range,
-                   ctx->dot_now ? std::min(ctx->opt_growth, ctx->opt_dot_growth) : ctx->opt_growth, pruning);
+                   (ctx->dot_now && ctx->opt_tensor_cores && ctx->split_ready) ? ctx->opt_tc_growth
+                   : ctx->dot_now ? std::min(ctx->opt_growth, ctx->opt_dot_growth) : ctx->opt_growth, pruning);
   for (size_t r = 0; r + 1 < bounds.size(); ++r)
     plan.push_back({false, bounds[r] / tile, (bounds[r + 1] + tile - 1) / tile});
   return plan;
@@ -1072,7 +1086,8 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
   // already seeded with exact rows, so they use full batches at once — every batch leaves a
   // few long-lived survivors that scan the whole series in a part-filled tile, and fewer
   // batches mean fewer such tiles.
-  uint32_t batch_now = pass == 0 ? std::min(ctx->opt_first_batch, ctx->opt_batch) : ctx->opt_batch;
+  const uint32_t batch_most = ctx->batch_limit();
+  uint32_t batch_now = pass == 0 ? std::min(ctx->opt_first_batch, batch_most) : batch_most;
   for (;;) {
     if (cursor < ctx->rows) {
       ensure_batch_capacity(ctx, batch_now);
@@ -1144,7 +1159,7 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
         ctx->stats.scanned_candidates += count;
         scan_batch(ctx, count, pruning);
       }
-      batch_now = static_cast<uint32_t>(std::min<uint64_t>(static_cast<uint64_t>(batch_now) * ctx->opt_batch_growth, ctx->opt_batch));
+      batch_now = static_cast<uint32_t>(std::min<uint64_t>(static_cast<uint64_t>(batch_now) * ctx->opt_batch_growth, batch_most));
     }
     if (ctx->several()) {  // a 1-rank communicator still runs the exchange
       CUDA_OK(cudaMemcpyAsync(ctx->h_keys, ctx->best.ptr, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
@@ -1603,6 +1618,15 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
     } else if (key == "seed_rows") {
       if (value < 0 || value > 1048576) fail(TSDD_ERR_PARAMETER, "seed_rows must be in 0..1048576");
       ctx->opt_seed_rows = static_cast<uint32_t>(value);
+    } else if (key == "tc_growth") {
+      if (value < 1.0 || value > 16.0) fail(TSDD_ERR_PARAMETER, "tc_growth must be in 1..16");
+      ctx->opt_tc_growth = value;
+    } else if (key == "tc_window_growth") {
+      if (value < 1.0 || value > 16.0) fail(TSDD_ERR_PARAMETER, "tc_window_growth must be in 1..16");
+      ctx->opt_tc_window_growth = value;
+    } else if (key == "tc_window_rounds") {
+      if (value < 0 || value > 64) fail(TSDD_ERR_PARAMETER, "tc_window_rounds must be in 0..64");
+      ctx->opt_tc_window_rounds = static_cast<int>(value);
     } else if (key == "dot_growth") {
       if (value < 1.0 || value > 16.0) fail(TSDD_ERR_PARAMETER, "dot_growth must be in 1..16");
       ctx->opt_dot_growth = value;

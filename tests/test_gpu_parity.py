@@ -243,7 +243,7 @@ def test_search_is_repeatable_and_independent_of_tunables(ctx):
     for name, value in [("batch", 65536), ("rounds", 64), ("bucket_mates", 8), ("symmetric", 1),
                         ("packed", 1), ("first_batch", 128), ("wide_tile", 0), ("kernel", 0),
                         ("window_rounds", 2), ("rotate", 1), ("growth", 2.0), ("first_range", 8192),
-                        ("lower_bound", 1), ("margin_delta", -1), ("batch_growth", 8), ("dot_form", 5),
+                        ("lower_bound", 1), ("margin_delta", -1), ("batch_growth", 12), ("dot_form", 5),
                         ("seed_rows", 4096), ("tensor_map", 1), ("dot_window_rounds", 8), ("dot_growth", 1.3),
                         ("dot_tile16", 1)]:
         ctx.set_option(name, value)
