@@ -1130,7 +1130,10 @@ uint64_t run_pass(tsdd_cuda_ctx* ctx, bool pruning, int pass) {
           }
           const bool tails = pruning && ctx->opt_tc_tail && ctx->opt_tensor_cores && !ctx->dot_now && ctx->opt_tensor_map &&
                              !ctx->tail_blocked;
-          const bool on_trust = tails && ctx->opt_tc_tail_first && pass == 0 && ctx->stats.batches == 0 && !ctx->dot_used;
+          // (one rank only: whether a tail really ran is each rank's own, timing-dependent decision, and ranks that
+          // disagreed on starting over would part ways)
+          const bool on_trust = tails && ctx->opt_tc_tail_first && pass == 0 && ctx->stats.batches == 0 && !ctx->dot_used &&
+                                !ctx->several();
           ctx->tail_now = tails && ((key_bits(best_now) != 0 && ctx->dot_eligible(best_now)) || on_trust);
           if (on_trust && !proven) ctx->tail_unproven = true;
           if (ctx->tail_now) ctx->dot_used = true;  // the band stays widened from here on
