@@ -588,8 +588,8 @@ void prepare_on_device(tsdd_cuda_ctx* ctx, size_t m, size_t n, size_t word_len, 
   ctx->counters.alloc(1);
   ctx->flags.alloc(2 * static_cast<size_t>(rows));
   ctx->sel.alloc(4);
-  ctx->zrow.alloc(n);
-  ctx->nn_bits.alloc(1);
+  ctx->zrow.alloc(4 * n);   // (up to four finalists are settled per launch)
+  ctx->nn_bits.alloc(4);
   ctx->batch_capacity = 0;
   ctx->stats.kernel_launches = launches;
 }
@@ -1372,26 +1372,60 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
       };
       double best64 = -1.0;
       uint32_t best_row = 0xFFFFFFFFu;
-      for (const uint32_t f : by_value) {
-        const uint32_t cand = mine[f];
-        // an upper bound of the float64 nn just above the float32 value (relative rounding, the
-        // dot form's absolute error, the rows' quantisation), so that most rows abandon early
+      // an upper bound of the float64 nn just above the float32 value (relative rounding, the
+      // dot form's absolute error, the rows' quantisation), so that most rows abandon early
+      auto start_of = [&](uint32_t f) {
         const double nn32 = static_cast<double>(float_from_bits(key_bits(mine_keys[f])));
-        const double start = nn32 * static_cast<double>(s.margin) * static_cast<double>(s.margin) +
-                             2.0 * static_cast<double>(s.margin_abs) +
-                             2.0 * static_cast<double>(s.margin_q) * std::sqrt(nn32);
-        if (start < best64) continue;  // cannot reach the float64 leader
-        double exact = exact_nn_from(cand, start);
+        return nn32 * static_cast<double>(s.margin) * static_cast<double>(s.margin) + 2.0 * static_cast<double>(s.margin_abs) +
+               2.0 * static_cast<double>(s.margin_q) * std::sqrt(nn32);
+      };
+      auto settle = [&](uint32_t cand, double exact) {
         // the start bound was not one after all (float32 rows further off than the band allows
         // for): measure from +inf rather than report the bound itself
         if (exact == inf64) {
           ctx->stats.exact_reruns += 1;
           exact = exact_nn_from(cand, inf64);
         }
-        if (exact == inf64) continue;
+        if (exact == inf64) return;
         if (exact > best64 || (exact == best64 && cand < best_row)) {
           best64 = exact;
           best_row = cand;
+        }
+      };
+      // in descending order of the float32 values, up to four per launch (a group's members cannot rule one
+      // another out, the leader of an earlier group can)
+      for (size_t at = 0; at < by_value.size();) {
+        uint32_t rows_now[4];
+        uint32_t idx_now[4];
+        double start_now[4];
+        uint32_t count_now = 0;
+        while (at < by_value.size() && count_now < 4) {
+          const uint32_t f = by_value[at++];
+          const double start = start_of(f);
+          if (start < best64) continue;  // cannot reach the float64 leader
+          rows_now[count_now] = mine[f];
+          idx_now[count_now] = f;
+          start_now[count_now] = start;
+          ++count_now;
+        }
+        if (count_now == 0) break;
+        if (count_now == 1) {
+          settle(rows_now[0], exact_nn_from(rows_now[0], start_now[0]));
+          continue;
+        }
+        unsigned long long bits[4], start_bits[4];
+        std::memcpy(start_bits, start_now, sizeof(double) * count_now);
+        CUDA_OK(cudaMemcpyAsync(ctx->nn_bits.ptr, start_bits, sizeof(unsigned long long) * count_now, cudaMemcpyHostToDevice, st));
+        ctx->stats.kernel_launches += launch_exact_nn_group(
+            ctx->series.ptr, ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->rows, static_cast<uint32_t>(ctx->n), rows_now, count_now,
+            ctx->zrow.ptr, ctx->opt_lower_bound ? ctx->lb_means.ptr : nullptr, s.lb_scale, s.lb_q, ctx->nn_bits.ptr, st);
+        CUDA_OK(cudaMemcpyAsync(bits, ctx->nn_bits.ptr, sizeof(unsigned long long) * count_now, cudaMemcpyDeviceToHost, st));
+        sync_stream(ctx);
+        for (uint32_t g = 0; g < count_now; ++g) {
+          (void)idx_now[g];
+          double exact = inf64;
+          if (bits[g] != start_bits[g]) std::memcpy(&exact, &bits[g], sizeof(exact));
+          settle(rows_now[g], exact);
         }
       }
       if (ctx->several()) {

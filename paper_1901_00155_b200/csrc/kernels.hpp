@@ -248,6 +248,10 @@ int launch_gather_keys(SearchState s, const uint32_t* d_list, uint32_t count, ui
 int launch_exact_nn(const double* d_series, const double* d_mean, const double* d_inv_sigma,
                     uint32_t n_rows, uint32_t n, uint32_t row, double* d_zrow, const float* d_lb_means, float lb_scale,
                     float lb_q, unsigned long long* d_out_bits, cudaStream_t stream);
+// ... for up to 4 finalists in one launch (d_zrow: count x n doubles; d_out_bits: count start bounds in, results out)
+int launch_exact_nn_group(const double* d_series, const double* d_mean, const double* d_inv_sigma, uint32_t n_rows,
+                          uint32_t n, const uint32_t* rows, uint32_t count, double* d_zrow, const float* d_lb_means,
+                          float lb_scale, float lb_q, unsigned long long* d_out_bits, cudaStream_t stream);
 
 // ------------------------------------------------------------------ probes
 int launch_fp32_probe(int which, float* d_sink, int blocks, int iters, cudaStream_t stream);

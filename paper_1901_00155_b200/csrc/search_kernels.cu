@@ -2668,6 +2668,59 @@ k_exact_nn(const double* __restrict__ x, const double* __restrict__ mean, const 
     atomicMin(out_bits, static_cast<unsigned long long>(__double_as_longlong(mine)));  // doubles >= 0 order like their bits
 }
 
+// Several finalists at once (blockIdx.y): the same arithmetic per pair as k_exact_nn — the float64 results are
+// bit-identical — with one launch and one read-back for the group instead of one per finalist.
+constexpr int kExactGroup = 4;
+struct ExactGroup {
+  uint32_t row[kExactGroup];
+};
+__global__ void k_zrow_group(const double* __restrict__ x, const double* __restrict__ mean,
+                             const double* __restrict__ inv_sigma, uint32_t n, ExactGroup g, double* __restrict__ z) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x, row = g.row[blockIdx.y];
+  if (t < n) z[static_cast<size_t>(blockIdx.y) * n + t] = __dmul_rn(x[row + t] - mean[row], inv_sigma[row]);
+}
+__global__ void __launch_bounds__(256)
+k_exact_nn_group(const double* __restrict__ x, const double* __restrict__ mean, const double* __restrict__ inv_sigma,
+                 uint32_t n_rows, uint32_t n, ExactGroup g, const double* __restrict__ z_all,
+                 const float* __restrict__ lb_means, float lb_scale, float lb_q, unsigned long long* out_bits_all) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x, row = g.row[blockIdx.y];
+  const double* z = z_all + static_cast<size_t>(blockIdx.y) * n;
+  unsigned long long* out_bits = out_bits_all + blockIdx.y;
+  double mine = __longlong_as_double(0x7FF0000000000000ll);  // +inf
+  bool wanted = j < n_rows && gap_u32(row, j) >= n;
+  const double bound = __longlong_as_double(static_cast<long long>(
+      __ldcg(reinterpret_cast<const unsigned long long*>(out_bits))));
+  if (wanted && lb_means != nullptr) {
+    const float4* pi = reinterpret_cast<const float4*>(lb_means + static_cast<size_t>(row) * kLbSegments);
+    const float4* pj = reinterpret_cast<const float4*>(lb_means + static_cast<size_t>(j) * kLbSegments);
+    float lb = 0.f;
+#pragma unroll
+    for (int q = 0; q < kLbSegments / 4; ++q) {
+      const float4 a = __ldg(pi + q), b = __ldg(pj + q);
+      const float dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z, dw = a.w - b.w;
+      lb = fmaf(dx, dx, lb), lb = fmaf(dy, dy, lb), lb = fmaf(dz, dz, lb), lb = fmaf(dw, dw, lb);
+    }
+    wanted = !(static_cast<double>(lb * lb_scale) >
+               bound * 1.001 + static_cast<double>(lb_q) * sqrt(bound) + static_cast<double>(lb_q * lb_q));
+  }
+  if (wanted) {
+    const double mu = mean[j], inv = inv_sigma[j];
+    const double* p = x + j;
+    double sum = 0.0;
+    uint32_t t = 0;
+    for (; t < n; ++t) {
+      const double d = z[t] - __dmul_rn(p[t] - mu, inv);  // (both rows rounded the same way: see k_exact_nn)
+      sum = fma(d, d, sum);
+      if ((t & 31) == 31 && sum > bound) break;
+    }
+    if (t >= n) mine = sum;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) mine = fmin(mine, __shfl_xor_sync(0xFFFFFFFFu, mine, d));
+  if ((threadIdx.x & 31) == 0 && mine < __longlong_as_double(0x7FF0000000000000ll))
+    atomicMin(out_bits, static_cast<unsigned long long>(__double_as_longlong(mine)));
+}
+
 inline uint32_t slot_tiles_of(uint32_t rows) { return (rows + kTileRows - 1) / kTileRows; }
 
 }  // namespace
@@ -3023,6 +3076,18 @@ int launch_exact_nn(const double* d_series, const double* d_mean, const double* 
   k_zrow<<<blocks_for(n, 256), 256, 0, stream>>>(d_series, d_mean, d_inv_sigma, n, row, d_zrow);
   k_exact_nn<<<blocks_for(n_rows, 256), 256, 0, stream>>>(d_series, d_mean, d_inv_sigma, n_rows, n, row,
                                                          d_zrow, d_lb_means, lb_scale, lb_q, d_out_bits);
+  return 2;
+}
+
+// `count` <= 4 finalists in one launch: d_zrow holds count x n doubles, d_out_bits count start bounds (in) / results (out)
+int launch_exact_nn_group(const double* d_series, const double* d_mean, const double* d_inv_sigma, uint32_t n_rows,
+                          uint32_t n, const uint32_t* rows, uint32_t count, double* d_zrow, const float* d_lb_means,
+                          float lb_scale, float lb_q, unsigned long long* d_out_bits, cudaStream_t stream) {
+  ExactGroup g{};
+  for (uint32_t f = 0; f < count && f < static_cast<uint32_t>(kExactGroup); ++f) g.row[f] = rows[f];
+  k_zrow_group<<<dim3(blocks_for(n, 256), count), 256, 0, stream>>>(d_series, d_mean, d_inv_sigma, n, g, d_zrow);
+  k_exact_nn_group<<<dim3(blocks_for(n_rows, 256), count), 256, 0, stream>>>(d_series, d_mean, d_inv_sigma, n_rows, n, g, d_zrow,
+                                                                             d_lb_means, lb_scale, lb_q, d_out_bits);
   return 2;
 }
 
