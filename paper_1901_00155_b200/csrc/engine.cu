@@ -269,6 +269,7 @@ struct tsdd_cuda_ctx {
   // (restart_wanted -> tail_blocked); if none are, the band is simply taken back.
   bool tail_unproven = false, tail_used = false, tail_blocked = false, restart_wanted = false;
   bool opt_tc_tail_first = true;
+  bool opt_tc_convert = true;   // tails without split copies: the kernel converts the float32 neighbour rows itself
   bool opt_tc_tail_force = false;
   uint64_t lb_launches = 0;  // launches of the kernel with the lower-bound filter in this search (evidence for lb_decided)
   bool opt_tc_tail = true;
@@ -571,8 +572,11 @@ void prepare_on_device(tsdd_cuda_ctx* ctx, size_t m, size_t n, size_t word_len, 
                             static_cast<size_t>(ctx->rows_padded - rows) * ctx->stride * sizeof(float), st));
   ctx->lb_means.alloc(static_cast<size_t>(rows) * kLbSegments);
   ctx->lb_boxes.alloc(static_cast<size_t>((rows + kLbBoxRows - 1) / kLbBoxRows) * 2 * kLbSegments);
+  ctx->row_norms.alloc(static_cast<size_t>(rows) + 1);  // (a by-product of the matrix: the dot-product forms need them)
   launches += launch_build_rows(ctx->series.ptr, ctx->mean.ptr, ctx->inv_sigma.ptr, rows,
-                                static_cast<uint32_t>(n), ctx->stride, ctx->matrix.ptr, ctx->lb_means.ptr, st);
+                                static_cast<uint32_t>(n), ctx->stride, ctx->matrix.ptr, ctx->lb_means.ptr, st,
+                                ctx->row_norms.ptr);
+  ctx->norms_ready = true;
 
   CUDA_OK(cudaEventRecord(ctx->ev_prep[2], st));
   launches += launch_segment_boxes(ctx->lb_means.ptr, rows, ctx->lb_boxes.ptr, st);
@@ -759,6 +763,10 @@ void ensure_batch_capacity(tsdd_cuda_ctx* ctx, uint32_t batch) {
   if (ctx->opt_tensor_cores && ctx->split_ready) {
     ctx->batch_hi.alloc(static_cast<size_t>(padded) * ctx->stride);
     ctx->batch_lo.alloc(static_cast<size_t>(padded) * ctx->stride);
+  } else if (ctx->opt_tensor_cores && ctx->opt_tc_tail) {  // (a tail's candidates: at most opt_tc_tail_most of them)
+    const size_t tail_rows = round_up_u32(std::min(padded, ctx->opt_tc_tail_most + 2 * kTileRows), 2 * kTileRows);
+    ctx->batch_hi.alloc(tail_rows * ctx->stride);
+    ctx->batch_lo.alloc(tail_rows * ctx->stride);
   }
   ctx->batch_capacity = padded;
 }
@@ -788,6 +796,8 @@ std::vector<uint32_t> range_bounds(uint32_t rows, int rounds, uint32_t first, do
   bounds.push_back(rows);
   return bounds;
 }
+
+inline bool tail_on_possible(const tsdd_cuda_ctx* ctx) { return ctx->split_ready || ctx->opt_tc_convert; }
 
 // The tensor-core form's operands: fp16 (or tf32) hi / lo parts of the matrix and, where it exists, of its
 // hash-sorted copy; skipped when memory is short.
@@ -969,20 +979,20 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
         const double tile_ms = 3.0 * (ctx->stride / 16.0) * 128.0 / 1.9e6 / ctx->sm_count / 0.4;
         const double tc_ms = cand_tiles * (tiles_left / 2.0) * tile_ms;
         const double matrix_bytes = static_cast<double>(ctx->rows_padded) * ctx->stride * sizeof(float);
-        const double split_ms = ctx->split_ready ? 0.0 : 2.0 * matrix_bytes / 6.0e9;  // (read once, written once, ~6 TB/s)
+        const double split_ms = (ctx->split_ready || ctx->opt_tc_convert) ? 0.0 : 2.0 * matrix_bytes / 6.0e9;  // (read once, written once, ~6 TB/s)
         if (const char* env = std::getenv("TSDD_TRACE"); env && env[0] == '1')
           std::fprintf(stderr, "tail? batch %llu segment %zu live<=%u: cuda %.3f ms for %llu tiles, tensor cores %.3f ms + split %.3f ms\n",
                        static_cast<unsigned long long>(ctx->stats.batches), r, count, cuda_ms,
                        static_cast<unsigned long long>(tiles_left), tc_ms, split_ms);
         const bool force = ctx->opt_tc_tail_force;  // (tests: switch at the first chance, whatever the estimate says)
-        if (force || cuda_ms > (ctx->split_ready ? 1.5 : 2.5) * (tc_ms + split_ms)) {
-          if (!ctx->split_ready) build_split_copies(ctx, count);
-          if (ctx->split_ready && !ctx->norms_ready) {
+        if (force || cuda_ms > ((ctx->split_ready || ctx->opt_tc_convert) ? 1.5 : 2.5) * (tc_ms + split_ms)) {
+          if (!ctx->split_ready && !ctx->opt_tc_convert) build_split_copies(ctx, count);
+          if (tail_on_possible(ctx) && !ctx->norms_ready) {
             ctx->row_norms.alloc(static_cast<size_t>(ctx->rows) + 1);
             ctx->stats.kernel_launches += launch_row_norms(ctx->matrix.ptr, ctx->rows + 1, ctx->stride, ctx->row_norms.ptr, st);
             ctx->norms_ready = true;
           }
-          tail_on = ctx->split_ready;
+          tail_on = ctx->split_ready || ctx->opt_tc_convert;
           if (tail_on) ctx->tail_used = true;
           s = ctx->state();
         }
@@ -995,7 +1005,8 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
     }
     const uint32_t padded = round_up_u32(count, choice_now.tile16 ? 2 * kTileRows : kTileRows);
     if (choice_now.tc)
-      launches += launch_gather_rows_split(s, list, ctx->sel.ptr, padded, ctx->opt_tc_half, ctx->batch_hi.ptr, ctx->batch_lo.ptr, st);
+      launches += launch_gather_rows_split(s, list, ctx->sel.ptr, padded, (tail_on && !ctx->split_ready) ? true : ctx->opt_tc_half,
+                                           ctx->batch_hi.ptr, ctx->batch_lo.ptr, st);
     else
       launches += launch_gather_rows(s, list, ctx->sel.ptr, padded, choice_now.tile16 ? 2 : choice_now.tma ? 1 : 0,
                                      ctx->batch_matrix.ptr, st);
@@ -1009,9 +1020,11 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
     int launched = 0;
     if (choice_now.tc) {
       ctx->tc_work.alloc(1);
+      // (a tail of a search without split copies: the kernel makes the neighbours' fp16 parts itself)
+      const bool convert = tail_on && !ctx->split_ready && !plan[r].window;
       const TcOperands op{ctx->batch_hi.ptr, ctx->batch_lo.ptr, ctx->matrix_hi.ptr, ctx->matrix_lo.ptr,
-                          ctx->sorted_hi.ptr, ctx->sorted_lo.ptr, ctx->rows_padded, ctx->opt_tc_half, ctx->tc_work.ptr,
-                          ctx->tail_now && !ctx->dot_now};
+                          ctx->sorted_hi.ptr, ctx->sorted_lo.ptr, ctx->rows_padded, convert ? true : ctx->opt_tc_half,
+                          ctx->tc_work.ptr, ctx->tail_now && !ctx->dot_now, convert};
       if (plan[r].window || rotation == 0) {
         launched = launch_scan_tiles_tc(s, op, list, slots, ctx->sel.ptr, count, plan[r].window ? ctx->sorted_row : nullptr,
                                         plan[r].k_begin, plan[r].k_end, pruning, ctx->opt_symmetric, st, &launch_error);
@@ -1641,6 +1654,8 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
       ctx->opt_wide_tile = value != 0;
     } else if (key == "lower_bound") {
       ctx->opt_lower_bound = value != 0;
+    } else if (key == "tc_convert") {
+      ctx->opt_tc_convert = value != 0;
     } else if (key == "tc_tail_force") {
       ctx->opt_tc_tail_force = value != 0;
     } else if (key == "tc_tail_first") {

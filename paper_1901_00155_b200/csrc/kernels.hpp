@@ -40,7 +40,7 @@ int launch_window_encode(const double* d_series, uint32_t rows, uint32_t n, uint
 // given, the kLbSegments segment means of every row (from the same staged samples).
 int launch_build_rows(const double* d_series, const double* d_mean, const double* d_inv_sigma,
                       uint32_t rows, uint32_t n, uint32_t stride, float* d_rows, float* d_seg_means,
-                      cudaStream_t stream);
+                      cudaStream_t stream, float* d_norms = nullptr);  // d_norms: rows + 1 squared norms of the float32 rows
 
 // Bounding boxes of the rows' segment means per kLbBoxRows rows:
 // [ceil(rows / kLbBoxRows) x 2 x kLbSegments] (minimum then maximum per segment).
@@ -199,6 +199,7 @@ struct TcOperands {
   bool half;                           // the parts are fp16 (kind::f16, 22 bits between them) instead of tf32 (kind::tf32, 21 bits)
   uint32_t* work;                      // one word of device memory: the launch's work-item counter
   bool tail;                           // a covering scan of a search that is not in the dot form (counters only)
+  bool convert;                        // no split copy of the matrix: the kernel makes the neighbours' fp16 parts from SearchState::rows
 };
 int launch_split_rows(const float* d_in, size_t floats, bool half, float* d_hi, float* d_lo, cudaStream_t stream);
 // ... row by row, with the rows' squared norms (the first n_norms of them) as a by-product

@@ -316,8 +316,9 @@ constexpr int kBuildThreads = 256;
 __global__ void __launch_bounds__(kBuildThreads)
 k_build_rows(const double* __restrict__ x, const double* __restrict__ mean,
              const double* __restrict__ inv_sigma, uint32_t rows, uint32_t n, uint32_t stride,
-             float* __restrict__ out, float* __restrict__ seg_means) {
+             float* __restrict__ out, float* __restrict__ seg_means, float* __restrict__ norms) {
   __shared__ double s_x[kBuildRows + kBuildCols];
+  __shared__ float s_sq[kBuildThreads / 32][kBuildRows];  // per warp: the squares of what it wrote of every row
   __shared__ double s_p[kBuildRows + kBuildCols + 1];
   __shared__ double s_mu[kBuildRows], s_inv[kBuildRows];
   const uint32_t i0 = blockIdx.x * kBuildRows;
@@ -356,14 +357,32 @@ k_build_rows(const double* __restrict__ x, const double* __restrict__ mean,
   for (uint32_t r = 0; r < n_rows; ++r) {
     const double mu = s_mu[r], inv = s_inv[r];
     float* dst = out + static_cast<size_t>(i0 + r) * stride + t0;
+    float sq = 0.f;
 #pragma unroll
     for (int q = 0; q < kBuildCols / kBuildThreads; ++q) {
       const uint32_t c = threadIdx.x + q * kBuildThreads;
-      if (c < n_cols) dst[c] = (t0 + c < n) ? static_cast<float>((s_x[r + c] - mu) * inv) : 0.f;
+      if (c < n_cols) {
+        const float v = (t0 + c < n) ? static_cast<float>((s_x[r + c] - mu) * inv) : 0.f;
+        dst[c] = v;
+        sq = fmaf(v, v, sq);
+      }
+    }
+    if (norms != nullptr) {  // the squared norm of the float32 row (the dot-product forms of the search), in a fixed order
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, d);
+      if ((threadIdx.x & 31) == 0) s_sq[threadIdx.x >> 5][r] = sq;
     }
   }
+  if (seg_means == nullptr && norms == nullptr) return;
+  __syncthreads();  // s_p and s_sq complete
+  if (norms != nullptr && threadIdx.x < n_rows) {
+    float total = 0.f;
+#pragma unroll
+    for (int w = 0; w < kBuildThreads / 32; ++w) total += s_sq[w][threadIdx.x];
+    if (gridDim.y == 1) norms[i0 + threadIdx.x] = total;
+    else atomicAdd(norms + i0 + threadIdx.x, total);  // (rows wider than one column block: pre-zeroed)
+  }
   if (seg_means == nullptr) return;
-  __syncthreads();  // s_p complete
   const uint32_t seg_cols = stride / kLbSegments;
   for (uint32_t item = threadIdx.x; item < n_rows * kLbSegments; item += kBuildThreads) {
     const uint32_t r = item / kLbSegments, seg = item % kLbSegments;
@@ -642,12 +661,14 @@ int launch_window_encode(const double* d_series, uint32_t rows, uint32_t n, uint
 
 int launch_build_rows(const double* d_series, const double* d_mean, const double* d_inv_sigma,
                       uint32_t rows, uint32_t n, uint32_t stride, float* d_rows, float* d_seg_means,
-                      cudaStream_t stream) {
+                      cudaStream_t stream, float* d_norms) {
   dim3 grid(blocks_for(rows, kBuildRows), blocks_for(stride, kBuildCols));
+  if (d_norms != nullptr)  // (row `rows`, the zero row, has norm 0; wider rows are accumulated)
+    cudaMemsetAsync(d_norms, 0, (static_cast<size_t>(rows) + 1) * sizeof(float), stream);
   if (d_seg_means != nullptr && grid.y > 1)  // segments straddle column blocks: they are accumulated
     cudaMemsetAsync(d_seg_means, 0, static_cast<size_t>(rows) * kLbSegments * sizeof(float), stream);
   k_build_rows<<<grid, kBuildThreads, 0, stream>>>(d_series, d_mean, d_inv_sigma, rows, n, stride, d_rows,
-                                                   d_seg_means);
+                                                   d_seg_means, d_norms);
   return 1;
 }
 

@@ -72,7 +72,7 @@ struct alignas(16) TcMeta {
 struct SharedTc {
   alignas(1024) unsigned char stages[kTcStages][kTcStageBytes];
   TcMeta meta[kMetaSlots];
-  unsigned long long full[kTcStages], empty[kTcStages], tmem_full[2], tmem_empty[2], meta_full[kMetaSlots], meta_empty[kMetaSlots];
+  unsigned long long full[kTcStages], empty[kTcStages], ready[kTcStages], tmem_full[2], tmem_empty[2], meta_full[kMetaSlots], meta_empty[kMetaSlots];
   uint32_t tmem_base;
 };
 
@@ -184,6 +184,14 @@ __device__ __forceinline__ void tmem_wait(uint32_t (&v)[32]) {
                : "memory");
 }
 
+// x = hi + lo with both parts fp16 (round to nearest): 22 bits between them
+__device__ __forceinline__ void split_half(const float4& x, uint2& h, uint2& l) {
+  const __half2 h0 = __floats2half2_rn(x.x, x.y), h1 = __floats2half2_rn(x.z, x.w);
+  const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
+  const __half2 l0 = __floats2half2_rn(x.x - f0.x, x.y - f0.y), l1 = __floats2half2_rn(x.z - f1.x, x.w - f1.y);
+  h = make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
+  l = make_uint2(*reinterpret_cast<const uint32_t*>(&l0), *reinterpret_cast<const uint32_t*>(&l1));
+}
 // -DTSDD_TC_PROFILE: cycles every role spends in each of its waits, printed by a few CTAs (development aid)
 #ifdef TSDD_TC_PROFILE
 #define TC_T0() const long long t0_ = clock64()
@@ -212,8 +220,16 @@ struct TcArgs {
   int tail;                   // a covering scan of a search that is not in the dot form (counters: tail_calls, no tile_live)
 };
 
-template <bool kSymmetric, bool kHalf>
-__global__ void __launch_bounds__(kTcThreads, 1)
+// kFormat: 0 rows split into two tf32 parts, 1 into two fp16 parts (both read from split copies of the matrix), 3 fp16
+// parts of the NEIGHBOUR rows made inside the kernel: the producer streams the float32 matrix itself (128-byte pieces,
+// 128-byte swizzle) into a raw buffer beside each stage, and the otherwise idle warp 2 splits it into the stage's
+// B_hi / B_lo tiles in the layout a 64-byte-swizzled TMA box would have written (chunk c of row r at c ^ ((r >> 1) & 3)),
+// then fences the async proxy and signals the MMA warp.  No split copy of the matrix at all (16 GB and 4.8 ms at
+// workload 4): the tails of covering scans, which stream every neighbour row once per candidate tile anyway.
+constexpr int kConvertWarps = 4;   // warp 2 and three more (warps 8 .. 10)
+constexpr int kTcThreadsConvert = kTcThreads + 32 * (kConvertWarps - 1);
+template <bool kSymmetric, int kFormat>
+__global__ void __launch_bounds__(kFormat == 3 ? kTcThreadsConvert : kTcThreads, 1)
 k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map_a_hi,
                 const __grid_constant__ CUtensorMap map_a_lo, const __grid_constant__ CUtensorMap map_b_hi,
                 const __grid_constant__ CUtensorMap map_b_lo) {
@@ -226,14 +242,14 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
   const float inf = __uint_as_float(kInfBits);
 
   if (tid == 0) {
-    for (int i = 0; i < kTcStages; ++i) bar_init(&sh.full[i], 1), bar_init(&sh.empty[i], 1);
+    for (int i = 0; i < kTcStages; ++i) bar_init(&sh.full[i], 1), bar_init(&sh.empty[i], 1), bar_init(&sh.ready[i], kConvertWarps);
     for (int i = 0; i < 2; ++i) {
       bar_init(&sh.tmem_full[i], 1);
       bar_init(&sh.tmem_empty[i], 4);   // the four epilogue warps
     }
     for (int i = 0; i < kMetaSlots; ++i) {
       bar_init(&sh.meta_full[i], 1);
-      bar_init(&sh.meta_empty[i], 6);   // the four epilogue warps, the MMA warp and the producer
+      bar_init(&sh.meta_empty[i], kFormat == 3 ? 6 + kConvertWarps : 6);   // the four epilogue warps, the MMA warp, the producer (and the converter)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -249,7 +265,12 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
   const bool window = a.nbr_index != nullptr;
   const uint32_t bin_shift = 31 - __clz(s.n);  // position bins of 2^bin_shift <= n rows (TcMeta::bins)
   const uint32_t units = (s.n_rows + kN - 1) / kN;  // 256-row units of the (hash-sorted or positional) row order
+  constexpr bool kHalf = kFormat != 0, kConvert = kFormat == 3;
   constexpr uint32_t kStageCols = kHalf ? 32 : 16;  // columns of one 64-byte row piece
+  // (converting: the raw float32 neighbour rows land where B_hi | B_lo go — 256 rows x 128 bytes = 2 x 256 rows x 64 bytes —
+  // and are converted in place: the stage geometry is the same)
+  constexpr uint32_t kStages = kTcStages, kStageBytes = kTcStageBytes;
+  unsigned char* const stage_base = &sh.stages[0][0];
   const uint32_t chunks = s.stride / kStageCols;
 
   if (warp == 3) {
@@ -516,17 +537,19 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
       if (lane == 0) bar_arrive(&sh.meta_empty[m]);
       if (stop) break;
       for (uint32_t c = 0; c < chunks; ++c) {
-        const uint32_t st = seq % kTcStages, round = seq / kTcStages;
+        const uint32_t st = seq % kStages, round = seq / kStages;
         if (round >= 1) { TC_T0(); bar_wait(&sh.empty[st], (round - 1) & 1, 3); TC_ACC(w_a); }
         if (lane == 0) {
           bar_expect_tx(&sh.full[st], ((TSDD_TC_EXP & 8) ? 0 : 2 * kABytes) + ((TSDD_TC_EXP & 2) ? 0 : 2 * kBBytes));
-          unsigned char* dst = sh.stages[st];
+          unsigned char* dst = stage_base + st * kStageBytes;
           const uint32_t col = c * kStageCols;
           if (!(TSDD_TC_EXP & 8)) {
             tma_box(dst, &map_a_hi, col, cand0, &sh.full[st]);
             tma_box(dst + kABytes, &map_a_lo, col, cand0, &sh.full[st]);
           }
-          if (!(TSDD_TC_EXP & 2)) {
+          if (kConvert) {  // the float32 rows themselves: 256 rows x 128 bytes, where B_hi | B_lo will be
+            tma_box(dst + 2 * kABytes, &map_b_hi, col, slot0, &sh.full[st]);
+          } else if (!(TSDD_TC_EXP & 2)) {
             tma_box(dst + 2 * kABytes, &map_b_hi, col, slot0, &sh.full[st]);
             tma_box(dst + 2 * kABytes + kBBytes, &map_b_lo, col, slot0, &sh.full[st]);
           }
@@ -554,11 +577,11 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t tmem_d = tmem_base + buf * kN;
       for (uint32_t c = 0; c < chunks; ++c) {
-        const uint32_t st = seq % kTcStages, round = seq / kTcStages;
-        { TC_T0(); bar_wait(&sh.full[st], round & 1, 6); TC_ACC(w_b); }
+        const uint32_t st = seq % kStages, round = seq / kStages;
+        { TC_T0(); bar_wait(kConvert ? &sh.ready[st] : &sh.full[st], round & 1, 6); TC_ACC(w_b); }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (lane == 0) {
-          const uint32_t base = smem_u32(sh.stages[st]);
+          const uint32_t base = smem_u32(stage_base + st * kStageBytes);
           const uint64_t a_hi = umma_desc(base), a_lo = umma_desc(base + kABytes);
           const uint64_t b_hi = umma_desc(base + 2 * kABytes), b_lo = umma_desc(base + 2 * kABytes + kBBytes);
 #pragma unroll
@@ -581,7 +604,56 @@ k_scan_tiles_tc(SearchState s, TcArgs a, const __grid_constant__ CUtensorMap map
     if (lane == 0 && blockIdx.x % 37 == 0)
       printf("tc mma cta %u: total %lld wait meta %lld wait tmem_empty %lld wait full %lld stages %u\n", blockIdx.x, clock64() - t_start, w_meta, w_a, w_b, seq);
 #endif
-  } else if (warp >= 4) {
+  } else if (kConvert && (warp == 2 || warp >= 8)) {
+    // ================================================================ converters: float32 neighbour rows -> fp16 hi / lo tiles
+    const uint32_t part = warp == 2 ? 0u : warp - 7u;  // this warp's quarter of the tile's rows
+    uint32_t seq = 0;
+    for (uint32_t ti = 0;; ++ti) {
+      const uint32_t m = ti % kMetaSlots;
+      bar_wait(&sh.meta_full[m], (ti / kMetaSlots) & 1, 9);
+      const bool stop = *reinterpret_cast<volatile uint32_t*>(&sh.meta[m].stop) != 0;
+      __syncwarp();
+      if (lane == 0) bar_arrive(&sh.meta_empty[m]);
+      if (stop) break;
+      for (uint32_t c = 0; c < chunks; ++c) {
+        const uint32_t st = seq % kStages, round = seq / kStages;
+        bar_wait(&sh.full[st], round & 1, 10);
+        unsigned char* base = stage_base + st * kStageBytes;
+        const float4* raw = reinterpret_cast<const float4*>(base + 2 * kABytes);
+        constexpr uint32_t kRowsPerLane = kN / 32 / kConvertWarps;
+        uint32_t hi[kRowsPerLane][16], lo[kRowsPerLane][16];  // 32 halves a row each: the row's two 64-byte pieces
+#pragma unroll
+        for (uint32_t rr = 0; rr < kRowsPerLane; ++rr) {
+          const uint32_t r = part * (kN / kConvertWarps) + lane + 32 * rr;
+#pragma unroll
+          for (uint32_t q = 0; q < 8; ++q) {
+            const float4 x = raw[r * 8 + (q ^ (r & 7u))];  // (128-byte swizzle of the raw box)
+            uint2 h, l;
+            split_half(x, h, l);
+            hi[rr][2 * q] = h.x, hi[rr][2 * q + 1] = h.y;
+            lo[rr][2 * q] = l.x, lo[rr][2 * q + 1] = l.y;
+          }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kConvertWarps) : "memory");  // every converter has read its rows: now in place
+#pragma unroll
+        for (uint32_t rr = 0; rr < kRowsPerLane; ++rr) {
+          const uint32_t r = part * (kN / kConvertWarps) + lane + 32 * rr;
+#pragma unroll
+          for (uint32_t q = 0; q < 4; ++q) {
+            const uint32_t at = r * kRowPiece + ((q ^ ((r >> 1) & 3u)) << 4);  // (64-byte swizzle of the operand tile)
+            *reinterpret_cast<uint4*>(base + 2 * kABytes + at) =
+                make_uint4(hi[rr][4 * q], hi[rr][4 * q + 1], hi[rr][4 * q + 2], hi[rr][4 * q + 3]);
+            *reinterpret_cast<uint4*>(base + 2 * kABytes + kBBytes + at) =
+                make_uint4(lo[rr][4 * q], lo[rr][4 * q + 1], lo[rr][4 * q + 2], lo[rr][4 * q + 3]);
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy stores -> the tensor cores' reads
+        __syncwarp();
+        if (lane == 0) bar_arrive(&sh.ready[st]);
+        ++seq;
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
     // ================================================================ epilogue: thread = candidate = TMEM lane
     const uint32_t mrow = tid - 128;                 // candidate (TMEM lane) of this thread
     const uint32_t lane_base = (warp & 3u) * 32u;    // the TMEM lanes this warp may read
@@ -775,14 +847,6 @@ k_split_tf32(const float4* __restrict__ in, size_t quads, float4* __restrict__ h
   lo[i] = make_float4(top(x.x - h.x), top(x.y - h.y), top(x.z - h.z), top(x.w - h.w));
 }
 
-// x = hi + lo with both parts fp16 (round to nearest): 22 bits between them
-__device__ __forceinline__ void split_half(const float4& x, uint2& h, uint2& l) {
-  const __half2 h0 = __floats2half2_rn(x.x, x.y), h1 = __floats2half2_rn(x.z, x.w);
-  const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
-  const __half2 l0 = __floats2half2_rn(x.x - f0.x, x.y - f0.y), l1 = __floats2half2_rn(x.z - f1.x, x.w - f1.y);
-  h = make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
-  l = make_uint2(*reinterpret_cast<const uint32_t*>(&l0), *reinterpret_cast<const uint32_t*>(&l1));
-}
 __global__ void __launch_bounds__(256)
 k_split_f16(const float4* __restrict__ in, size_t quads, uint2* __restrict__ hi, uint2* __restrict__ lo) {
   const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -922,10 +986,17 @@ int launch_scan_tiles_tc(SearchState s, const TcOperands& op, const uint32_t* d_
   const float* b_lo = window ? op.sorted_lo : op.rows_lo;
   const uint64_t b_rows = op.rows_padded;  // (a box that reaches past the last row is zero-filled by the TMA unit)
   const uint32_t cols = op.half ? 32 : 16, elem = op.half ? 2 : 4;
+  if (op.convert && (window || !op.half)) {
+    if (error) *error = "the converting tensor-core kernel takes fp16 parts and covering scans only";
+    return 0;
+  }
   if (!make_row_map_boxed(&map_a_hi, op.batch_hi, static_cast<uint64_t>(cand_tiles) * kM, s.stride, cols, kM, elem) ||
       !make_row_map_boxed(&map_a_lo, op.batch_lo, static_cast<uint64_t>(cand_tiles) * kM, s.stride, cols, kM, elem) ||
-      !make_row_map_boxed(&map_b_hi, b_hi, b_rows, s.stride, cols, kN, elem) ||
-      !make_row_map_boxed(&map_b_lo, b_lo, b_rows, s.stride, cols, kN, elem)) {
+      // (converting: the float32 matrix itself, 32 columns = 128 bytes a piece, 128-byte swizzle; b_lo unused)
+      !(op.convert ? make_row_map_boxed(&map_b_hi, s.rows, b_rows, s.stride, 32, kN, 4)
+                   : make_row_map_boxed(&map_b_hi, b_hi, b_rows, s.stride, cols, kN, elem)) ||
+      !(op.convert ? make_row_map_boxed(&map_b_lo, s.rows, b_rows, s.stride, 32, kN, 4)
+                   : make_row_map_boxed(&map_b_lo, b_lo, b_rows, s.stride, cols, kN, elem))) {
     if (error) *error = "cuTensorMapEncodeTiled failed (tensor-core tile kernel)";
     return 0;
   }
@@ -937,14 +1008,16 @@ int launch_scan_tiles_tc(SearchState s, const TcOperands& op, const uint32_t* d_
   const int smem = static_cast<int>(sizeof(SharedTc)) + 1024;
   auto launch = [&](auto kernel) {
     cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    kernel<<<grid, kTcThreads, smem, stream>>>(s, a, map_a_hi, map_a_lo, map_b_hi, map_b_lo);
+    kernel<<<grid, op.convert ? kTcThreadsConvert : kTcThreads, smem, stream>>>(s, a, map_a_hi, map_a_lo, map_b_hi, map_b_lo);
   };
   if (symmetric) {
-    if (op.half) launch(k_scan_tiles_tc<true, true>);
-    else launch(k_scan_tiles_tc<true, false>);
+    if (op.convert) launch(k_scan_tiles_tc<true, 3>);
+    else if (op.half) launch(k_scan_tiles_tc<true, 1>);
+    else launch(k_scan_tiles_tc<true, 0>);
   } else {
-    if (op.half) launch(k_scan_tiles_tc<false, true>);
-    else launch(k_scan_tiles_tc<false, false>);
+    if (op.convert) launch(k_scan_tiles_tc<false, 3>);
+    else if (op.half) launch(k_scan_tiles_tc<false, 1>);
+    else launch(k_scan_tiles_tc<false, 0>);
   }
   return 1;
 }

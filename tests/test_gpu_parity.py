@@ -797,12 +797,14 @@ def test_dot_product_form_on_256_candidate_tiles(ctx, chk, seed, kind, n):
     np.testing.assert_allclose(again[1], dist, rtol=1e-9)
 
 
+@pytest.mark.parametrize("convert", [1, 0], ids=["converting", "split-copies"])
 @pytest.mark.parametrize("kind", ["walk", "periodic", "low-noise"])
-def test_tails_of_covering_scans_on_the_tensor_cores(ctx, chk, kind):
+def test_tails_of_covering_scans_on_the_tensor_cores(ctx, chk, kind, convert):
     """The later ranges of a covering scan move to the tensor cores (engine.cu: tail_now; forced here at the
     first chance, with the lower-bound filter in the kernel's metadata warp), the first batch on trust.  On the
     low-noise series the first batch's best-so-far does NOT dwarf the error band: the search has to notice,
-    start over without the tails, and still return the reference's answer."""
+    start over without the tails, and still return the reference's answer.  Both feeds of the kernel: the
+    neighbours' fp16 parts made inside it from the float32 matrix (the default), and split copies of the matrix."""
     rng = np.random.default_rng(4242)
     m, n, w, a, k = 40000, 64, 4, 4, 2
     if kind == "walk":
@@ -812,7 +814,7 @@ def test_tails_of_covering_scans_on_the_tensor_cores(ctx, chk, kind):
         x[17000:17064] += np.float32(1.5)
     else:
         x = (np.sin(2 * np.pi * np.arange(m) / 50.0) + 1e-4 * rng.standard_normal(m)).astype(np.float32)
-    for name, value in [("tc_tail_force", 1), ("first_batch", 128)]:
+    for name, value in [("tc_tail_force", 1), ("first_batch", 128), ("tc_convert", convert)]:
         ctx.set_option(name, value)
     try:
         ctx.prepare(x, n, w, a)
@@ -820,6 +822,7 @@ def test_tails_of_covering_scans_on_the_tensor_cores(ctx, chk, kind):
         st = ctx.stats()
     finally:
         ctx.set_option("tc_tail_force", 0)
+        ctx.set_option("tc_convert", 1)
     want = chk.topk(x, n, w, a, k)
     assert_discords_match(chk, x, n, pos, dist, want)
     if kind == "low-noise":
