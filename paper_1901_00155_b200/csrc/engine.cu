@@ -976,7 +976,7 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
         const double cuda_ms = cuda_ms_per_tile * static_cast<double>(tiles_left);
         const double cand_tiles = std::ceil(count / 128.0);
         // one 128 x 256 tile: 3 MMAs per 16 columns, 128 cycles each at 1.9 GHz, over the SMs, at 40 % of that rate
-        const double tile_ms = 3.0 * (ctx->stride / 16.0) * 128.0 / 1.9e6 / ctx->sm_count / 0.4;
+        const double tile_ms = 3.0 * (ctx->stride / 16.0) * 128.0 / 1.9e6 / ctx->sm_count / (ctx->split_ready ? 0.4 : 0.3);  // (converting: 0.3)
         const double tc_ms = cand_tiles * (tiles_left / 2.0) * tile_ms;
         const double matrix_bytes = static_cast<double>(ctx->rows_padded) * ctx->stride * sizeof(float);
         const double split_ms = (ctx->split_ready || ctx->opt_tc_convert) ? 0.0 : 2.0 * matrix_bytes / 6.0e9;  // (read once, written once, ~6 TB/s)
