@@ -328,7 +328,9 @@ struct tsdd_cuda_ctx {
   double dot_error() const {
     // (x 3 on the tensor cores: the tf32 split drops products below 3 x 2^-20 |a||b| <= 2.9e-6 n, and
     // the float32 accumulation in tensor memory may truncate where the CUDA cores round)
-    return (opt_tensor_cores ? 3.0 : 1.0) * (static_cast<double>(n) + 32.0) * static_cast<double>(n) * 5.9604644775390625e-08;
+    // (+ n 2^-22: the row norms are those of the float64 rows, k_build_rows; each float32 row's is within 2^-23 of it)
+    return (opt_tensor_cores ? 3.0 : 1.0) * (static_cast<double>(n) + 32.0) * static_cast<double>(n) * 5.9604644775390625e-08 +
+           static_cast<double>(n) * 2.384185791015625e-07;
   }
   // candidates per batch: the option, with the dense copy of the batch's rows (and its two split twins) kept under 2 GB each
   uint32_t batch_limit() const {

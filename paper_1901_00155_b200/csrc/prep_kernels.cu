@@ -318,7 +318,7 @@ k_build_rows(const double* __restrict__ x, const double* __restrict__ mean,
              const double* __restrict__ inv_sigma, uint32_t rows, uint32_t n, uint32_t stride,
              float* __restrict__ out, float* __restrict__ seg_means, float* __restrict__ norms) {
   __shared__ double s_x[kBuildRows + kBuildCols];
-  __shared__ float s_sq[kBuildThreads / 32][kBuildRows];  // per warp: the squares of what it wrote of every row
+  __shared__ double s_p2[kBuildRows + kBuildCols + 1];  // prefix sums of (sample - mean of the block's first row)^2: the row norms
   __shared__ double s_p[kBuildRows + kBuildCols + 1];
   __shared__ double s_mu[kBuildRows], s_inv[kBuildRows];
   const uint32_t i0 = blockIdx.x * kBuildRows;
@@ -336,7 +336,7 @@ k_build_rows(const double* __restrict__ x, const double* __restrict__ mean,
     s_inv[threadIdx.x] = inv_sigma[i0 + threadIdx.x];
   }
   __syncthreads();
-  if (seg_means != nullptr && threadIdx.x < 32) {  // one warp: prefix sums of the staged samples
+  if ((seg_means != nullptr || norms != nullptr) && threadIdx.x < 32) {  // one warp: prefix sums of the staged samples
     const uint32_t total = n_rows + n_cols, per_lane = (total + 31) / 32;
     const uint32_t lo = min(threadIdx.x * per_lane, total), hi = min(lo + per_lane, total);
     double mine = 0.0;
@@ -353,34 +353,57 @@ k_build_rows(const double* __restrict__ x, const double* __restrict__ mean,
       run += s_x[e];
     }
     if (threadIdx.x == 31) s_p[total] = run;  // lane 31's range ends at `total` (or is empty: run = grand total)
+  } else if (norms != nullptr && threadIdx.x >= 32 && threadIdx.x < 64) {  // a second warp: prefix sums of the shifted squares
+    const uint32_t lane = threadIdx.x - 32;
+    const uint32_t total = n_rows + n_cols, per_lane = (total + 31) / 32;
+    const uint32_t lo = min(lane * per_lane, total), hi = min(lo + per_lane, total);
+    const double shift = s_mu[0];
+    double mine = 0.0;
+    for (uint32_t e = lo; e < hi; ++e) {
+      const double v = s_x[e] - shift;
+      mine = fma(v, v, mine);
+    }
+    double incl = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const double up = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+      if (lane >= static_cast<uint32_t>(d)) incl += up;
+    }
+    double run = incl - mine;
+    for (uint32_t e = lo; e < hi; ++e) {
+      s_p2[e] = run;
+      const double v = s_x[e] - shift;
+      run = fma(v, v, run);
+    }
+    if (lane == 31) s_p2[total] = run;
   }
   for (uint32_t r = 0; r < n_rows; ++r) {
     const double mu = s_mu[r], inv = s_inv[r];
     float* dst = out + static_cast<size_t>(i0 + r) * stride + t0;
-    float sq = 0.f;
 #pragma unroll
     for (int q = 0; q < kBuildCols / kBuildThreads; ++q) {
       const uint32_t c = threadIdx.x + q * kBuildThreads;
-      if (c < n_cols) {
-        const float v = (t0 + c < n) ? static_cast<float>((s_x[r + c] - mu) * inv) : 0.f;
-        dst[c] = v;
-        sq = fmaf(v, v, sq);
-      }
-    }
-    if (norms != nullptr) {  // the squared norm of the float32 row (the dot-product forms of the search), in a fixed order
-#pragma unroll
-      for (int d = 16; d > 0; d >>= 1) sq += __shfl_xor_sync(0xFFFFFFFFu, sq, d);
-      if ((threadIdx.x & 31) == 0) s_sq[threadIdx.x >> 5][r] = sq;
+      if (c < n_cols) dst[c] = (t0 + c < n) ? static_cast<float>((s_x[r + c] - mu) * inv) : 0.f;
     }
   }
   if (seg_means == nullptr && norms == nullptr) return;
-  __syncthreads();  // s_p and s_sq complete
+  __syncthreads();  // s_p and s_p2 complete
+  // Squared norms of the rows (the dot-product forms of the search), from the same staged samples: with
+  // c the block's first row mean, sum (x - mu_r)^2 = S2 - 2 (mu_r - c) S1 + cnt (mu_r - c)^2 over the shifted
+  // samples x - c (S1, S2 from the prefix sums; c keeps every term of the size of the windows' variance).
+  // This is the norm of the float64 row; the float32 row's differs by at most 2^-23 of it (every element is
+  // rounded once), which the dot forms' error bound carries (engine.cu: dot_error).
   if (norms != nullptr && threadIdx.x < n_rows) {
-    float total = 0.f;
-#pragma unroll
-    for (int w = 0; w < kBuildThreads / 32; ++w) total += s_sq[w][threadIdx.x];
-    if (gridDim.y == 1) norms[i0 + threadIdx.x] = total;
-    else atomicAdd(norms + i0 + threadIdx.x, total);  // (rows wider than one column block: pre-zeroed)
+    const uint32_t r = threadIdx.x;
+    const uint32_t c0 = t0, c1 = min(t0 + n_cols, n);
+    if (c1 > c0) {
+      const double cnt = static_cast<double>(c1 - c0), shift = s_mu[0], d = s_mu[r] - shift;
+      const double s1 = (s_p[r + c1 - t0] - s_p[r + c0 - t0]) - cnt * shift;
+      const double s2 = s_p2[r + c1 - t0] - s_p2[r + c0 - t0];
+      const double part = fmax((s2 - 2.0 * d * s1 + cnt * d * d) * s_inv[r] * s_inv[r], 0.0);
+      if (gridDim.y == 1) norms[i0 + r] = static_cast<float>(part);
+      else atomicAdd(norms + i0 + r, static_cast<float>(part));  // (rows wider than one column block: pre-zeroed)
+    }
   }
   if (seg_means == nullptr) return;
   const uint32_t seg_cols = stride / kLbSegments;
