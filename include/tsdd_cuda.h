@@ -124,6 +124,7 @@ int tsdd_cuda_set_stream(tsdd_cuda_ctx* ctx, void* cuda_stream);
  * CUDA-core time per tile says that is cheaper; default 1, at most 1,024 candidates),
  * "tc_growth" / "tc_window_rounds" / "tc_window_growth" (the ranges and window rounds of a dot-form batch on the
  * tensor cores: 2.0 / 5 / 2.5 — fewer, wider launches than on the CUDA cores),
+ * "mates_form" (-1: the same-word step picks its kernel by the input; 0 float64, 1 float32, 2 along runs of consecutive rows),
  * "tc_convert" (0/1: such a tail reads the float32 matrix and makes the neighbours' fp16 parts inside the kernel,
  * instead of building split copies of the matrix first; default 1),
  * "tc_tail_first" (0/1: the first batch of a search may do so on trust, before there is a best-so-far to size the

@@ -189,6 +189,7 @@ struct tsdd_cuda_ctx {
   double opt_window_growth = 3.0;
   bool opt_rotate = true;           // each batch starts its covering scan at a different row
   int opt_mates = 8;
+  int opt_mates_form = -1;          // -1: by the input (k_bucket_mates_runs / _f32 / float64); 0 float64, 1 float32, 2 along runs
   int opt_propagate = 8;            // time-topology tries per candidate and call (0 = off)
   int opt_propagate_every = 2;      // ... called again after every this-many-th compaction of a batch (0: only at its start)
   bool opt_rescore = true;
@@ -1291,7 +1292,8 @@ void search(tsdd_cuda_ctx* ctx, int k, unsigned flags, uint64_t* positions, doub
       const bool split = ctx->several() && ctx->opt_share_bounds && ctx->opt_mates > 0;
       ctx->stats.kernel_launches += launch_bucket_mates(
           s, ctx->series.ptr, ctx->series_is_f32 ? ctx->series_f32.ptr : nullptr, ctx->mean.ptr, ctx->inv_sigma.ptr, ctx->sorted_row, ctx->slot_bucket.ptr, ctx->offsets.ptr,
-          ctx->opt_mates, ctx->run_pairs, split ? static_cast<uint32_t>(ctx->world) : 1u, split ? static_cast<uint32_t>(ctx->rank) : 0u, st);
+          ctx->opt_mates, ctx->run_pairs, split ? static_cast<uint32_t>(ctx->world) : 1u, split ? static_cast<uint32_t>(ctx->rank) : 0u, st,
+        ctx->opt_mates_form);
       if (split) exchange_bounds(ctx);
     }
 
@@ -1628,6 +1630,9 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
     } else if (key == "bucket_mates") {
       if (value < 0 || value > 1024) fail(TSDD_ERR_PARAMETER, "bucket_mates must be in 0..1024");
       ctx->opt_mates = static_cast<int>(value);
+    } else if (key == "mates_form") {
+      if (value != -1 && value != 0 && value != 1 && value != 2) fail(TSDD_ERR_PARAMETER, "mates_form must be -1, 0, 1 or 2");
+      ctx->opt_mates_form = static_cast<int>(value);
     } else if (key == "propagate") {
       if (value < 0 || value > 32) fail(TSDD_ERR_PARAMETER, "propagate must be in 0..32");
       ctx->opt_propagate = static_cast<int>(value);

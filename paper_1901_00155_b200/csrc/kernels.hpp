@@ -115,7 +115,7 @@ int launch_min_from_peers(uint64_t* d_nn, PeerPointers peers, uint32_t rows, cud
 int launch_bucket_mates(SearchState s, const double* d_series, const float* d_series_f32, const double* d_mean,
                         const double* d_inv_sigma, const uint32_t* d_sorted_row, const uint32_t* d_slot_bucket,
                         const uint32_t* d_offsets, int mates, uint32_t run_pairs, uint32_t world, uint32_t rank,
-                        cudaStream_t stream);  // run_pairs: launch_count_runs
+                        cudaStream_t stream, int form = -1);  // run_pairs: launch_count_runs; form: -1 by the input (runs / float32 / float64), 0 float64, 1 float32, 2 runs
 
 // Time topology: every live batch candidate c tries the matches of its neighbours in time,
 // shifted along (row c + delta knows neighbour j  ->  measure (c, j - delta)); up to `tries`

@@ -666,8 +666,7 @@ int launch_widen_series(const float* d_in, double* d_out, size_t m, uint32_t* d_
 int launch_window_encode(const double* d_series, uint32_t rows, uint32_t n, uint32_t word_len,
                          uint32_t alphabet, double* d_mean, double* d_inv_sigma, uint32_t* d_hash0,
                          double* d_paa, uint32_t* d_sax, cudaStream_t stream, double tol_scale) {
-  static const bool exact_only = [] { const char* e = std::getenv("TSDD_ENCODE_EXACT"); return e && e[0] == '1'; }();
-  const bool aligned = n % word_len == 0 && d_paa == nullptr && d_sax == nullptr && !exact_only && tol_scale > 0.0;
+  const bool aligned = n % word_len == 0 && d_paa == nullptr && d_sax == nullptr && tol_scale > 0.0;
   const size_t smem = encode4_smem_bytes(n, aligned);
   if (smem <= 200 * 1024) {  // (longer windows than ~24,000 samples: the one-window-per-thread kernel)
     auto kernel = aligned ? k_window_encode4<true> : k_window_encode4<false>;

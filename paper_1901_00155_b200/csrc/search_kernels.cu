@@ -2740,10 +2740,9 @@ int launch_min_from_peers(uint64_t* d_nn, PeerPointers peers, uint32_t rows, cud
 int launch_bucket_mates(SearchState s, const double* d_series, const float* d_series_f32, const double* d_mean,
                         const double* d_inv_sigma, const uint32_t* d_sorted_row, const uint32_t* d_slot_bucket,
                         const uint32_t* d_offsets, int mates, uint32_t run_pairs, uint32_t world, uint32_t rank,
-                        cudaStream_t stream) {
+                        cudaStream_t stream, int form) {
   if (mates <= 0) return 0;
   const size_t slots = (static_cast<size_t>(s.n_rows) + world - 1) / world;
-  static const int form = [] { const char* e = std::getenv("TSDD_MATES_FORM"); return e ? std::atoi(e) : -1; }();
   const bool old_form = form == 0;
   // buckets that are mostly runs of consecutive rows: chains along the diagonals (k_bucket_mates_runs)
   if (form == 2 || (form < 0 && static_cast<uint64_t>(run_pairs) * 2 >= s.n_rows)) {

@@ -797,6 +797,30 @@ def test_dot_product_form_on_256_candidate_tiles(ctx, chk, seed, kind, n):
     np.testing.assert_allclose(again[1], dist, rtol=1e-9)
 
 
+@pytest.mark.parametrize("form", [0, 1, 2], ids=["float64", "float32", "runs"])
+@pytest.mark.parametrize("kind", ["walk", "periodic", "repeats"])
+def test_every_form_of_the_bucket_mates(ctx, chk, kind, form):
+    """k_bucket_mates (float64), k_bucket_mates_f32 (float32, inflated) and k_bucket_mates_runs (chains along
+    runs of consecutive rows: full sums at the heads, one-product deltas and a segmented prefix sum for the
+    rest) publish upper bounds only: whichever runs, the search returns the reference's answer."""
+    rng = np.random.default_rng(991)
+    m, n, w, a, k = 9000, 96, 4, 3, 2
+    if kind == "walk":
+        x = planted_walk(17, m, n)
+    elif kind == "periodic":
+        x = (np.sin(2 * np.pi * np.arange(m) / 61.0) + 0.05 * rng.standard_normal(m)).astype(np.float32)
+        x[4000:4050] += np.float32(0.8)
+    else:
+        x = _fuzz_series(rng, "repeats", m)
+    ctx.set_option("mates_form", form)
+    try:
+        ctx.prepare(x, n, w, a)
+        pos, dist = ctx.search(k)
+    finally:
+        ctx.set_option("mates_form", -1)
+    assert_discords_match(chk, x, n, pos, dist, chk.topk(x, n, w, a, k))
+
+
 @pytest.mark.parametrize("convert", [1, 0], ids=["converting", "split-copies"])
 @pytest.mark.parametrize("kind", ["walk", "periodic", "low-noise"])
 def test_tails_of_covering_scans_on_the_tensor_cores(ctx, chk, kind, convert):
