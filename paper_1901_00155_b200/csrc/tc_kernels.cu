@@ -1,31 +1,36 @@
 // The dot-product form of the tile kernel on the 5th-generation tensor cores (tcgen05 + TMEM).
 //
-// EXPERIMENT, behind the option "tensor_cores" (dot_form = 3 / 4); the CUDA-core kernels of
-// search_kernels.cu stay the default and stay the FP32 roofline evidence.  The dot form of the
-// distance, d^2 = |a|^2 + |b|^2 - 2 a.b, is a dense contraction: a tile of 128 candidates x 256
-// neighbours is the matrix product A (128 x n) . B^T (n x 256).  Float32 inputs do not fit the
-// tensor cores' TF32 format (10 explicit mantissa bits), so every row is split once into
-//     x = hi + lo,   hi = x with the low 13 mantissa bits cleared,   lo = (x - hi) likewise cleared,
-// (x - hi is exact in float32) and a tile is THREE tf32 MMAs per 8 columns,
+// The default for the dot form (option dot_form = 5; 1 / 2 keep it on the CUDA-core kernels of
+// search_kernels.cu, which stay the FP32 roofline evidence) and for the tails of covering scans (tc_tail).
+// The dot form of the distance, d^2 = |a|^2 + |b|^2 - 2 a.b, is a dense contraction: a tile of 128
+// candidates x 256 neighbours is the matrix product A (128 x n) . B^T (n x 256).  Float32 inputs do
+// not fit a 16-bit or TF32 mantissa, so every row is split once into
+//     x = hi + lo,   hi = fp16(x), lo = fp16(x - hi)   (22 bits between them; or two tf32 parts, dot_form 3 / 4),
+// and a tile is THREE MMAs per k-step,
 //     A_hi.B_hi + A_hi.B_lo + A_lo.B_hi        (the missing lo.lo term is below 2^-20 |a||b|),
 // accumulated in float32 in tensor memory.  The split and the accumulation leave an absolute
-// error of the same kind as the CUDA-core dot form's, about three times its bound; the engine
+// error of the same kind as the CUDA-core dot form's, within three times its bound; the engine
 // widens the discard band accordingly (SearchState::margin_abs) and the float64 decision at the
 // end of a pass is unchanged — positions stay those of the reference.
 //
-// Kernel anatomy (one CTA per SM, 256 threads, no CTA-wide barrier after the set-up):
-//   warp 3      per tile, one tile ahead: the candidates' thresholds and the neighbours' rows / bounds / norms;
-//   warp 0      producer: per 16-column stage four TMA boxes (A_hi, A_lo: 128 rows; B_hi, B_lo:
-//               256 rows; 64-byte swizzle; 48 KB) onto a "full" mbarrier, four stages deep;
-//   warp 1      MMA issuer: one elected lane issues 6 tcgen05.mma.kind::tf32 per stage (M 128,
-//               N 256, K 8; operands straight from the swizzled shared-memory tiles through
-//               matrix descriptors) and tcgen05.commit's the stage back to the producer; the
-//               accumulators of tile t+1 go to the other half of tensor memory (2 x 256 columns);
-//   warp 2      allocates / frees the 512 TMEM columns;
-//   warps 4..7  epilogue: thread m of the warpgroup owns candidate m (TMEM lane m); it reads its
-//               256 accumulators with tcgen05.ld (32 columns at a time), forms the distances and
-//               keeps the smallest — no shuffle, no shared-memory reduction; one atomicMin per
-//               candidate per tile, plus the symmetric updates of the neighbours.
+// Kernel anatomy (PERSISTENT: one CTA per SM takes work items — a candidate tile x up to 16 neighbour tiles —
+// off a global counter; 256 threads, 352 when converting; no CTA-wide barrier after the set-up):
+//   warp 3      the head: work items, and per tile — everything requested in one batch, the next tile's rows a
+//               tile ahead — the candidates' rows / norms / thresholds, the neighbours' rows / norms / kill limits,
+//               the lower-bound filter of a tail, the position bins of a window tile; four metadata slots;
+//   warp 0      producer: per 64-byte row piece four TMA boxes (A_hi, A_lo: 128 rows; B_hi, B_lo: 256 rows;
+//               64-byte swizzle; 48 KB) onto a "full" mbarrier, four stages deep — or, converting (format 3),
+//               the float32 neighbour rows themselves as one 256 x 128-byte box where B_hi | B_lo go;
+//   warp 1      MMA issuer: one elected lane issues 6 tcgen05.mma per stage (M 128, N 256, K 16 fp16 / 8 tf32;
+//               operands straight from the swizzled shared-memory tiles through matrix descriptors) and
+//               tcgen05.commit's the stage back to the producer; the accumulators of tile t+1 go to the other
+//               half of tensor memory (2 x 256 columns);
+//   warp 2      allocates / frees the 512 TMEM columns; converting: one of the four converter warps (with warps
+//               8 .. 10) that split the float32 rows into the fp16 operand tiles in place;
+//   warps 4..7  epilogue: thread m of the warpgroup owns candidate m (TMEM lane m); it reads its 256 accumulators
+//               with tcgen05.ld (32 columns at a time, the next chunk in flight), keeps two running minima per
+//               chunk and looks at a chunk pair by pair only when one of them trips; one atomicMin per
+//               candidate per tile, plus the symmetric updates that kill a neighbour.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
