@@ -1,5 +1,6 @@
 """Randomised soak of the CUDA engine against the CPU oracle (not part of the test suite):
-   python tools/soak.py [cases] [seed]"""
+   python tools/soak.py [cases] [seed] [large]      (large: 100,000 - 250,000 samples, where tails and the
+   tensor-core forms come into play by themselves)"""
 import sys
 import time
 
@@ -13,12 +14,13 @@ from paper_1901_00155_b200 import Context  # noqa: E402
 def main():
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 20
     rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+    large = len(sys.argv) > 3 and sys.argv[3] == "large"
     chk = oracle.best()
     bad = 0
     with Context(0) as ctx:
         for c in range(cases):
             kind = rng.choice(["noise", "walk", "sine"])
-            m = int(rng.integers(15000, 45000))
+            m = int(rng.integers(100000, 250000)) if large else int(rng.integers(15000, 45000))
             n = int(rng.choice([24, 50, 64, 100, 128, 200, 256, 300]))
             w = int(rng.integers(2, 9))
             a = int(rng.integers(2, 7))
@@ -30,8 +32,10 @@ def main():
             else:
                 t = np.arange(m)
                 x = (np.sin(2 * np.pi * t / rng.integers(20, 200)) + 0.3 * rng.standard_normal(m)).astype(np.float32)
-            opts = {"dot_form": int(rng.choice([1, 2])), "first_batch": int(rng.choice([128, 4096])),
-                    "lower_bound": int(rng.choice([0, 1])), "filter_in_ws": int(rng.choice([0, 1]))}
+            opts = {"dot_form": int(rng.choice([1, 2, 5, 5, 6])), "first_batch": int(rng.choice([128, 4096])),
+                    "lower_bound": int(rng.choice([0, 1])), "filter_in_ws": int(rng.choice([0, 1])),
+                    "tc_tail_force": 0 if large else int(rng.choice([0, 1])), "tc_convert": int(rng.choice([0, 1])),
+                    "mates_form": int(rng.choice([-1, 0, 1, 2]))}
             for name, value in opts.items():
                 ctx.set_option(name, value)
             t0 = time.time()
@@ -40,6 +44,8 @@ def main():
             t1 = time.time()
             want = chk.topk(x, n, w, a, k)
             ok = pos == want["positions"] and np.allclose(dist, want["distances"], rtol=1e-4)
+            if not ok and np.allclose(dist, want["distances"], rtol=1e-9, atol=1e-9):
+                ok = True  # (an exact tie: the reference's own choice is order-dependent, SURVEY gap G5; the tests check those properly)
             st = ctx.stats()
             print(c, kind, m, n, w, a, k, opts, "ok" if ok else f"MISMATCH {pos} {want['positions']}",
                   f"gpu {t1 - t0:.3f}s cpu {time.time() - t1:.1f}s dot {st['scan_kernel_dot_launches']}", flush=True)
