@@ -272,6 +272,7 @@ struct tsdd_cuda_ctx {
   bool opt_tc_tail_first = true;
   bool opt_tc_convert = true;   // tails without split copies: the kernel converts the float32 neighbour rows itself
   bool opt_tc_tail_force = false;
+  uint32_t opt_tc_tail_evidence = 64;   // neighbour tiles a CUDA-core segment must have had to count as evidence
   uint64_t lb_launches = 0;  // launches of the kernel with the lower-bound filter in this search (evidence for lb_decided)
   bool opt_tc_tail = true;
   uint32_t opt_tc_tail_most = 1024;  // ... while at most so many candidates are left
@@ -965,7 +966,7 @@ void scan_batch(tsdd_cuda_ctx* ctx, uint32_t count, bool pruning) {
       double cuda_ms_per_tile = -1.0;
       for (size_t q = seg_events.size(); q-- > 0;) {  // the latest covering segment whose events have completed
         const SegEvent& ev = seg_events[q];
-        if (ev.window || ev.tc || (ev.tiles < 256 && !ctx->opt_tc_tail_force) || ev.r + 2 > r) continue;  // (a small segment is mostly launch overhead)
+        if (ev.window || ev.tc || (ev.tiles < ctx->opt_tc_tail_evidence && !ctx->opt_tc_tail_force) || ev.r + 2 > r) continue;  // (a small segment is mostly launch overhead)
         float ms = 0.f;
         if (cudaEventQuery(ev.e1) == cudaSuccess && cudaEventElapsedTime(&ms, ev.e0, ev.e1) == cudaSuccess)
           cuda_ms_per_tile = ms / ev.tiles;
@@ -1663,6 +1664,9 @@ int tsdd_cuda_set_option(tsdd_cuda_ctx* ctx, const char* name, double value) {
       ctx->opt_lower_bound = value != 0;
     } else if (key == "tc_convert") {
       ctx->opt_tc_convert = value != 0;
+    } else if (key == "tc_tail_evidence") {
+      if (value < 1 || value > 1048576) fail(TSDD_ERR_PARAMETER, "tc_tail_evidence must be in 1..1048576");
+      ctx->opt_tc_tail_evidence = static_cast<uint32_t>(value);
     } else if (key == "tc_tail_force") {
       ctx->opt_tc_tail_force = value != 0;
     } else if (key == "tc_tail_first") {

@@ -949,7 +949,14 @@ def test_dot_product_form_is_chosen_where_tiles_are_never_abandoned(ctx, chk):
     y = planted_walk(3, 40000, 128)
     ctx.prepare(y, 128, 4, 4)
     ctx.search(1)
-    assert ctx.stats()["scan_kernel_dot_launches"] == 0
+    st = ctx.stats()  # (the only dot-form launches there may be are tails of covering scans on the tensor cores)
+    assert st["scan_kernel_dot_launches"] == st["scan_kernel_tc_launches"]
+    ctx.set_option("tc_tail", 0)
+    try:
+        ctx.search(1)
+        assert ctx.stats()["scan_kernel_dot_launches"] == 0
+    finally:
+        ctx.set_option("tc_tail", 1)
 
 
 @pytest.mark.parametrize("seed,kind,n", FUZZ[::2], ids=[f"{k}-n{n}" for _, k, n in FUZZ[::2]])
@@ -994,14 +1001,21 @@ def test_seeded_best_so_far_saves_work_and_keeps_the_result(ctx, chk):
     x, _ = W.series(2)
     x = x[:120000]
     ctx.prepare(x, 256, 8, 4)
+    # (pair distances are compared without the tensor-core tails, which start every pair of the tiles they visit)
+    ctx.set_option("tc_tail", 0)
     ctx.set_option("seed_rows", 0)
     try:
         plain = ctx.search(3)
         plain_calls = ctx.stats()["calls"]
+        ctx.set_option("seed_rows", 4096)
+        seeded = ctx.search(3)
+        seeded_calls = ctx.stats()["calls"]
     finally:
         ctx.set_option("seed_rows", 4096)
-    seeded = ctx.search(3)
-    seeded_calls = ctx.stats()["calls"]
+        ctx.set_option("tc_tail", 1)
+    with_tails = ctx.search(3)
+    assert with_tails[0] == seeded[0]
+    np.testing.assert_allclose(with_tails[1], seeded[1], rtol=1e-9)
     assert seeded[0] == plain[0]
     np.testing.assert_allclose(seeded[1], plain[1], rtol=1e-9)
     assert seeded_calls < plain_calls
